@@ -1,0 +1,224 @@
+/* =========================================================================================
+ * bgs.h — C ABI of libbgs: the BlitzGS per-view distributed splatting step on B200 (sm_100a).
+ *
+ * Paper: "BlitzGS" (arXiv 2605.13794).  Citations: P:n = PAPER.md line n, S:n = SPEC.md line n
+ * (the paper text and the spec written from it).  Readings R1..R28 / decisions D1..D7 are
+ * listed in DESIGN.md §2.
+ *
+ * One view of the method, in call order per rank:
+ *   bgs_project        a1 gate (Eq.4-6) + a2 EWA projection / SH colour
+ *   bgs_route          a3 cost-aware tile ownership + a4 single all-to-all
+ *   bgs_sort_tiles     a5 (tile,depth) pair emission + a6 onesweep radix sort + a7 tile ranges
+ *   bgs_raster_fwd     a8 front-to-back compositing, Eq.2, + w_{i,v}, a_{i,v}
+ *   bgs_raster_bwd     a9 backward of Eq.2
+ *   bgs_route_reverse  a10 reverse exchange of per-splat gradients to the owning shard
+ *   bgs_project_bwd    a11 backward of the projection
+ *   bgs_importance     a12 Eq.3 score, c^rad, c^vis top-99% mass, Cull column
+ * bgs_view_step / bgs_view_step_host run a1..a11 (+a12 when requested) in one call.
+ *
+ * Conventions (all entry points):
+ *  - Status codes only; nothing throws across the ABI.  On a non-OK status the message is
+ *    available from bgs_last_error(ctx) until the next call on that ctx.
+ *  - Pointers documented "device" must be device-accessible memory on the ctx's device
+ *    (e.g. torch CUDA tensors); "host" pointers are ordinary (optionally pinned) memory.
+ *  - All inputs and fixed-size outputs are CALLER-owned.  Variable-size intermediates
+ *    (records, exchange buffers, pairs, per-splat gradients) live in the ctx arena and stay
+ *    valid until the next call of the same stage on that ctx.
+ *  - Every call enqueues on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *    stream is rejected, pass a real stream).  Calls marked HOST-SYNC block the host on that
+ *    stream once (to size variable buffers).
+ *  - One ctx per rank and per host thread.  world > 1 uses NCCL (ncclCommInitRank from a
+ *    unique id) or, for single-GPU testing, an in-process group sharing one device.
+ *  - Layouts: Gaussian parameters are structure-of-arrays of 16-byte rows so kernels issue
+ *    128-bit loads; the global id of local Gaussian j on rank m is j*world + m (index
+ *    parity sharding).
+ * ========================================================================================= */
+#ifndef BGS_H_
+#define BGS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BGS_OK = 0,
+  BGS_ERR_INVALID_ARGUMENT = 1, /* null pointer, n<0, W/H<=0, fx/fy<=0, world mismatch, world>8 */
+  BGS_ERR_CAPACITY = 2,         /* arena could not grow; bytes requested in bgs_last_error */
+  BGS_ERR_CUDA = 3,             /* a CUDA runtime error (message has cudaGetErrorString) */
+  BGS_ERR_NCCL = 4,             /* an NCCL error */
+  BGS_ERR_CONTRACT = 5,         /* stage called out of order / shapes inconsistent */
+  BGS_ERR_INTERNAL = 6
+} bgs_status;
+
+typedef struct bgs_ctx bgs_ctx;
+
+/* flags */
+#define BGS_NO_COLOR 1u   /* a2 skips SH colour (instrumented scoring pass "bypasses color shading") */
+#define BGS_IMPORTANCE 2u /* a8 accumulates w_fixed (sum of alpha*T in 2^-24 units) and a per splat */
+
+/* Pinhole camera.  R row-major world->camera, x right, y down, camera looks +z;
+ * campos = -R^T t is the camera centre c_v of Eq.5 (caller-computed); pixels are centred at
+ * integer coordinates (R6); near_clip in world units (R7). */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float R[9];
+  float t[3];
+  float campos[3];
+  float near_clip;
+} bgs_camera;
+
+/* The local shard G^(m), ACTIVATED parameters (R13: exp/sigmoid/normalise live in the
+ * caller).  All device pointers, n_local rows each:
+ *   mean_opac float4 (mu_x, mu_y, mu_z, opacity in (0,1))
+ *   quat      float4 (w, x, y, z), unit norm
+ *   scale     float4 (s_x, s_y, s_z, unused) per-axis standard deviation > 0
+ *   sh        float  [n_local][16][3] degree-3 SH, coefficient-major, RGB inner (R1)
+ *   lod       uint8  [n_local] LOD label l_i */
+typedef struct {
+  int64_t n_local;
+  const float* mean_opac;
+  const float* quat;
+  const float* scale;
+  const float* sh;
+  const uint8_t* lod;
+} bgs_gaussians;
+
+/* Gradients w.r.t. the activated parameters, same layouts as bgs_gaussians (device,
+ * caller-owned, ACCUMULATED into with +=: the caller zeroes them once per optimizer step).
+ * mean_opac row = (dL/dmu_x, dL/dmu_y, dL/dmu_z, dL/do); quat row = dL/d(w,x,y,z);
+ * scale row = (dL/ds_x, dL/ds_y, dL/ds_z, 0); sh [n][16][3]. */
+typedef struct {
+  float* mean_opac;
+  float* quat;
+  float* scale;
+  float* sh;
+} bgs_gaussian_grads;
+
+/* Distance-based LOD gate, Eq.4-5 with fallback.
+ * keep_lod(i) = l_i <= clamp(round_half_up(log2(d0/|mu_i - c_v|)), 0, l_max)
+ * evaluated as l_i == 0 || (l_i <= l_max && d^2 <= D2[l_i]), D2[l] = (d0*2^(1/2-l))^2
+ * (reading R18).  When enabled == 0 or fallback_den*|L| > fallback_num*|G^(m)| (R20; 19/20)
+ * the whole shard passes.  d0 > 0 world units (R19). */
+typedef struct {
+  int32_t enabled;
+  int32_t l_max;
+  double d0;
+  int32_t fallback_num;
+  int32_t fallback_den;
+} bgs_lod_gate;
+
+/* ---------------------------------------------------------------------------------------
+ * Context
+ * --------------------------------------------------------------------------------------- */
+/* 128-byte NCCL unique id for world > 1 (rank 0 creates, caller broadcasts). */
+bgs_status bgs_get_unique_id(void* out_128_bytes);
+/* One rank of a world-size group.  world == 1: nccl_unique_id may be NULL (no NCCL).
+ * world > 1: ncclCommInitRank; must be called concurrently by all ranks.  world <= 8. */
+bgs_status bgs_ctx_create(int32_t rank, int32_t world, const void* nccl_unique_id, int32_t device,
+                          bgs_ctx** out);
+/* An in-process group of `world` contexts on ONE device whose collectives are device-to-device
+ * copies (test transport: the M>1 kernels and routing on a single GPU).  Each ctx must then
+ * be driven by its own host thread, concurrently.  out: array of `world` ctx pointers. */
+bgs_status bgs_ctx_create_local_group(int32_t world, int32_t device, bgs_ctx** out);
+bgs_status bgs_ctx_destroy(bgs_ctx* ctx);
+const char* bgs_last_error(const bgs_ctx* ctx);
+/* Kernels this ctx has launched since creation (the bench's gpu_launches evidence). */
+int64_t bgs_launch_count(const bgs_ctx* ctx);
+
+/* Per-view counters (valid after the producing stage; host-visible after a HOST-SYNC call):
+ *   0 N_local  1 n_lod (|L^(m)|)  2 n_active (|A^(m)|)  3 F (in-frustum records)  4 D (records
+ *   sent, sum of destination multiplicity)  5 R (records received)  6 P (pairs of owned tiles)
+ *   7 tile_begin  8 tile_end (owned run)  9 fallback (0/1)  10 sort passes run  11 P_all
+ *   (pairs over all tiles of this rank's splats)  12 width 13 height */
+#define BGS_Q_COUNT 14
+bgs_status bgs_query(bgs_ctx* ctx, int64_t* out /*[BGS_Q_COUNT] host*/);
+
+/* Borrowed device views of arena intermediates for parity tests (valid until the next call of
+ * the producing stage):
+ *   0 records [F]x48 B {mx,my,A,B, C,o,r,g, b,depth,gid,rect(x0|y0<<8|x1<<16|y1<<24)}
+ *   1 record local index [F] u32       2 received records [R]x48 B (== 0 when world == 1)
+ *   3 sorted keys [P] u64 ((tile-tile_begin)<<31 | f32 bits(depth))   4 sorted values [P] u32
+ *     (index into received records)    5 tile ranges [tile_end-tile_begin] uint2 [start,end)
+ *   6 per-received-splat accumulators [R]x48 B {dL/d(mx,my,A,B,C,o,r,g,b) f32, a u32, w_fixed u64}
+ *   7 per-local-record owner-summed accumulators [F]x48 B (same layout; == 6 when world == 1)
+ *   8 tile owner map [T] i32    9 dest mask [F] u8    10 per-tile pair counts (all ranks) [T] i32 */
+bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** dev_ptr, int64_t* bytes);
+
+/* ---------------------------------------------------------------------------------------
+ * Steps
+ * --------------------------------------------------------------------------------------- */
+/* a1+a2.  cull_column: nullable device u32[ceil(n_local/32)], bit j = Cull_{j,v} (Eq.6).
+ * radius_out: device int32[n_local]; 0 when gated, culled, behind near_clip or off-screen
+ * (c^rad_{i,v} = radius > 0).  flags: BGS_NO_COLOR.  HOST-SYNC (reads F and P). */
+bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                       const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, void* stream);
+
+/* a3+a4.  Per-tile pair counts are all-reduced, tiles split into contiguous cost-balanced
+ * runs (owner(t) = min(M-1, floor((2 P_t + c_t) M / (2 C))), c_t = pairs_t + 1, D6), and
+ * every record is sent to each rank owning a tile of its rect in ONE all-to-all.
+ * tile_owner_out: nullable device int32[T].  HOST-SYNC (exchange sizes). */
+bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream);
+
+/* a5+a6+a7.  Pairs (owned tile, received record) keyed (tile, depth); onesweep LSD radix sort;
+ * runs of equal keys ordered by global id (R12); per-tile [start,end) ranges. */
+bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream);
+
+/* a8.  Writes the OWNED tiles of rgb (device f32 [3][H][W], black background), t_final
+ * (device f32 [H][W]) and n_contrib (device i32 [H][W] = 1 + position in the tile list of the
+ * last contributor).  flags: BGS_IMPORTANCE (accumulate w_fixed, a per received splat). */
+bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
+                          void* stream);
+
+/* a9.  dL_drgb: device f32 [3][H][W] (read on owned tiles only).  t_final / n_contrib: the
+ * buffers written by bgs_raster_fwd. */
+bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL_drgb, const float* t_final, const int32_t* n_contrib,
+                          void* stream);
+
+/* a10.  Returns per-received-splat partials (9 grads + w_fixed + a) to the source ranks along
+ * the transposed counts of a4 and sums them per local record in destination-rank order. */
+bgs_status bgs_route_reverse(bgs_ctx* ctx, void* stream);
+
+/* a11.  grads += d(loss)/d(activated params) for every projected local Gaussian. */
+bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                           const bgs_gaussian_grads* grads, void* stream);
+
+/* a12.  Eq.3 score and visibility bits for this view, selection GLOBAL over ranks.
+ * radius: device i32[n_local] from bgs_project.  w_fixed / a: nullable device u64 / u32
+ * [n_local]; when NULL the ctx's reverse-routed per-record values of this view are used.
+ * s (f64), c_rad, c_vis (u32): device [n_local], accumulated.  cull_out: device
+ * u32[ceil(n_local/32)], overwritten: bit j = 1 - c^vis_{j,v}.  Top set: smallest
+ * prefix of (w desc, global id asc) with mass_den*prefix >= mass_num*total (99/100, R16). */
+bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, const uint64_t* w_fixed,
+                          const uint32_t* a, int32_t mass_num, int32_t mass_den, double* s, uint32_t* c_rad,
+                          uint32_t* c_vis, uint32_t* cull_out, void* stream);
+
+/* a1..a11 in one call (a12 too when importance != NULL).  The per-view image gradient comes
+ * from the caller (the loss of Eq.7 is outside the hot path). */
+typedef struct {
+  double* s;
+  uint32_t* c_rad;
+  uint32_t* c_vis;
+  uint32_t* cull_out;
+  int32_t mass_num, mass_den;
+} bgs_importance_out;
+
+bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                         const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, float* rgb,
+                         float* t_final, int32_t* n_contrib, const float* dL_drgb, const bgs_gaussian_grads* grads,
+                         const bgs_importance_out* importance, void* stream);
+
+/* Same with the per-view I/O in HOST memory (end-to-end path): dL_drgb_host (f32 [3][H][W])
+ * is copied to the device and rgb_host (f32 [3][H][W], owned tiles) back, inside the call.
+ * Scratch device images live in the arena.  Host buffers should be pinned. */
+bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                              const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                              int32_t* radius_out, const float* dL_drgb_host, float* rgb_host,
+                              const bgs_gaussian_grads* grads, const bgs_importance_out* importance, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BGS_H_ */

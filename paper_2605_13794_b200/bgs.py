@@ -1,0 +1,321 @@
+"""Thin ctypes binding of libbgs (include/bgs.h): argument marshalling only.
+
+Every step of the per-view path runs in the sm_100a kernels of libbgs.so.  PyTorch supplies
+device memory (tensors), streams and, for world > 1, the process group used to broadcast the
+NCCL unique id.  There is no CPU fallback: if libbgs.so is missing, importing this module
+raises; if no CUDA device is present, every call returns BGS_ERR_CUDA and raises BgsError.
+Function names follow the C ABI (bgs_project, bgs_route, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbgs.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libbgs.so not built ({LIB_PATH}); run `python -m paper_2605_13794_b200.build` "
+                      "(or __graft_entry__.build()) — there is no CPU fallback")
+_lib = C.CDLL(LIB_PATH)
+
+BGS_NO_COLOR = 1
+BGS_IMPORTANCE = 2
+BGS_Q_COUNT = 14
+Q_NAMES = ("n_local", "n_lod", "n_active", "F", "D", "R", "P", "tile_begin", "tile_end", "fallback",
+           "sort_passes", "P_all", "width", "height")
+STATUS = {0: "BGS_OK", 1: "BGS_ERR_INVALID_ARGUMENT", 2: "BGS_ERR_CAPACITY", 3: "BGS_ERR_CUDA",
+          4: "BGS_ERR_NCCL", 5: "BGS_ERR_CONTRACT", 6: "BGS_ERR_INTERNAL"}
+DEBUG = {"records": 0, "rec_lidx": 1, "recv": 2, "keys": 3, "vals": 4, "ranges": 5, "acc": 6, "acc_local": 7,
+         "owner": 8, "dest_mask": 9, "tile_pairs": 10}
+
+
+class BgsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class bgs_camera(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("width", C.c_int32), ("height", C.c_int32), ("R", C.c_float * 9), ("t", C.c_float * 3),
+                ("campos", C.c_float * 3), ("near_clip", C.c_float)]
+
+
+class bgs_gaussians(C.Structure):
+    _fields_ = [("n_local", C.c_int64), ("mean_opac", C.c_void_p), ("quat", C.c_void_p), ("scale", C.c_void_p),
+                ("sh", C.c_void_p), ("lod", C.c_void_p)]
+
+
+class bgs_gaussian_grads(C.Structure):
+    _fields_ = [("mean_opac", C.c_void_p), ("quat", C.c_void_p), ("scale", C.c_void_p), ("sh", C.c_void_p)]
+
+
+class bgs_lod_gate(C.Structure):
+    _fields_ = [("enabled", C.c_int32), ("l_max", C.c_int32), ("d0", C.c_double), ("fallback_num", C.c_int32),
+                ("fallback_den", C.c_int32)]
+
+
+class bgs_importance_out(C.Structure):
+    _fields_ = [("s", C.c_void_p), ("c_rad", C.c_void_p), ("c_vis", C.c_void_p), ("cull_out", C.c_void_p),
+                ("mass_num", C.c_int32), ("mass_den", C.c_int32)]
+
+
+_vp = C.c_void_p
+_SIGS = {
+    "bgs_get_unique_id": [_vp],
+    "bgs_ctx_create": [C.c_int32, C.c_int32, _vp, C.c_int32, _vp],
+    "bgs_ctx_create_local_group": [C.c_int32, C.c_int32, _vp],
+    "bgs_ctx_destroy": [_vp],
+    "bgs_query": [_vp, _vp],
+    "bgs_debug_buffer": [_vp, C.c_int32, _vp, _vp],
+    "bgs_project": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp],
+    "bgs_route": [_vp, _vp, _vp],
+    "bgs_sort_tiles": [_vp, _vp],
+    "bgs_raster_fwd": [_vp, C.c_uint32, _vp, _vp, _vp, _vp],
+    "bgs_raster_bwd": [_vp, _vp, _vp, _vp, _vp],
+    "bgs_route_reverse": [_vp, _vp],
+    "bgs_project_bwd": [_vp, _vp, _vp, _vp, _vp],
+    "bgs_importance": [_vp, C.c_int64, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp],
+    "bgs_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_view_step_host": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = C.c_int
+_lib.bgs_last_error.argtypes = [_vp]
+_lib.bgs_last_error.restype = C.c_char_p
+_lib.bgs_launch_count.argtypes = [_vp]
+_lib.bgs_launch_count.restype = C.c_int64
+
+EXPORTS = tuple(_SIGS) + ("bgs_last_error", "bgs_launch_count")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return C.c_void_p(t.data_ptr())
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(C.c_void_p)
+    return t
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, torch.cuda.Stream):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+# ------------------------------------------------------------------------------------------
+# context
+# ------------------------------------------------------------------------------------------
+class Context:
+    """One rank's bgs_ctx.  world > 1: pass the 128-byte NCCL unique id (see unique_id())."""
+
+    def __init__(self, rank: int = 0, world: int = 1, device: int = 0, nccl_uid: bytes | None = None, _handle=None):
+        self.rank, self.world, self.device = rank, world, device
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = C.c_void_p()
+        uid = None if nccl_uid is None else C.create_string_buffer(bytes(nccl_uid), 128)
+        st = _lib.bgs_ctx_create(rank, world, uid, device, C.byref(h))
+        if st != 0:
+            raise BgsError(st, "bgs_ctx_create")
+        self._h = h
+
+    @staticmethod
+    def local_group(world: int, device: int = 0) -> list["Context"]:
+        arr = (C.c_void_p * world)()
+        st = _lib.bgs_ctx_create_local_group(world, device, arr)
+        if st != 0:
+            raise BgsError(st, "bgs_ctx_create_local_group")
+        return [Context(r, world, device, _handle=C.c_void_p(arr[r])) for r in range(world)]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def check(self, st: int, what: str):
+        if st != 0:
+            raise BgsError(st, f"{what}: {_lib.bgs_last_error(self._h).decode(errors='replace')}")
+
+    def launches(self) -> int:
+        return int(_lib.bgs_launch_count(self._h))
+
+    def query(self) -> dict:
+        out = (C.c_int64 * BGS_Q_COUNT)()
+        self.check(_lib.bgs_query(self._h, out), "bgs_query")
+        return dict(zip(Q_NAMES, list(out)))
+
+    def debug_buffer(self, name: str, dtype=torch.uint8) -> torch.Tensor:
+        """Copy of an arena intermediate (parity tests only)."""
+        p = C.c_void_p()
+        nbytes = C.c_int64()
+        self.check(_lib.bgs_debug_buffer(self._h, DEBUG[name], C.byref(p), C.byref(nbytes)), "bgs_debug_buffer")
+        n = int(nbytes.value)
+        out = torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}")
+        if n and p.value:
+            cudart = torch.cuda.cudart()
+            torch.cuda.synchronize(self.device)
+            st = cudart.cudaMemcpy(out.data_ptr(), p.value, n, 3)  # device to device
+            if int(st) != 0:
+                raise RuntimeError(f"cudaMemcpy failed: {st}")
+        return out.view(dtype) if n else out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.bgs_ctx_destroy(self._h)
+            self._h = None
+
+
+def unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = _lib.bgs_get_unique_id(buf)
+    if st != 0:
+        raise BgsError(st, "bgs_get_unique_id")
+    return buf.raw
+
+
+# ------------------------------------------------------------------------------------------
+# structs
+# ------------------------------------------------------------------------------------------
+def camera(cam: dict) -> bgs_camera:
+    c = bgs_camera()
+    c.fx, c.fy, c.cx, c.cy = cam["fx"], cam["fy"], cam["cx"], cam["cy"]
+    c.width, c.height = int(cam["W"]), int(cam["H"])
+    c.R[:] = [float(v) for v in np.asarray(cam["R"], np.float32).ravel()]
+    c.t[:] = [float(v) for v in np.asarray(cam["t"], np.float32).ravel()]
+    c.campos[:] = [float(v) for v in np.asarray(cam["campos"], np.float32).ravel()]
+    c.near_clip = float(cam["near"])
+    return c
+
+
+def lod_gate(enabled: bool = False, l_max: int = 31, d0: float = 1.0, num: int = 19, den: int = 20) -> bgs_lod_gate:
+    return bgs_lod_gate(int(enabled), int(l_max), float(d0), int(num), int(den))
+
+
+class GaussianPlanes:
+    """Activated parameters of one shard in the ABI layout (float4 rows, SH [n][48])."""
+
+    def __init__(self, mean_opac, quat, scale, sh, lod):
+        self.mean_opac, self.quat, self.scale, self.sh, self.lod = mean_opac, quat, scale, sh, lod
+        self.n = int(mean_opac.shape[0])
+
+    @staticmethod
+    def from_arrays(means, opac, quats, scales, sh, lod, device="cuda") -> "GaussianPlanes":
+        n = int(np.asarray(means).shape[0])
+        mo = np.empty((n, 4), np.float32)
+        mo[:, :3] = means
+        mo[:, 3] = opac
+        sc = np.zeros((n, 4), np.float32)
+        sc[:, :3] = scales
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)
+        return GaussianPlanes(t(mo), t(np.asarray(quats, np.float32)), t(sc),
+                              t(np.asarray(sh, np.float32).reshape(n, 48)), t(np.asarray(lod, np.uint8)))
+
+    @staticmethod
+    def from_scene(scene, device="cuda") -> "GaussianPlanes":
+        return GaussianPlanes.from_arrays(scene.means, scene.opac, scene.quats, scene.scales, scene.sh, scene.lod,
+                                          device)
+
+    def struct(self) -> bgs_gaussians:
+        return bgs_gaussians(self.n, self.mean_opac.data_ptr(), self.quat.data_ptr(), self.scale.data_ptr(),
+                             self.sh.data_ptr(), self.lod.data_ptr())
+
+    def zeros_grads(self) -> "GradPlanes":
+        z = lambda t: torch.zeros_like(t, dtype=torch.float32)
+        return GradPlanes(z(self.mean_opac), z(self.quat), z(self.scale), z(self.sh))
+
+
+class GradPlanes:
+    def __init__(self, mean_opac, quat, scale, sh):
+        self.mean_opac, self.quat, self.scale, self.sh = mean_opac, quat, scale, sh
+
+    def struct(self) -> bgs_gaussian_grads:
+        return bgs_gaussian_grads(self.mean_opac.data_ptr(), self.quat.data_ptr(), self.scale.data_ptr(),
+                                  self.sh.data_ptr())
+
+    def zero_(self):
+        for t in (self.mean_opac, self.quat, self.scale, self.sh):
+            t.zero_()
+
+
+# ------------------------------------------------------------------------------------------
+# the ABI calls (same names as include/bgs.h)
+# ------------------------------------------------------------------------------------------
+def bgs_project(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate: bgs_lod_gate | None, cull_column,
+                flags: int, radius_out: torch.Tensor, stream=None):
+    gs = g.struct()
+    ctx.check(_lib.bgs_project(ctx.handle, C.byref(gs), C.byref(cam), C.byref(gate) if gate is not None else None,
+                               _ptr(cull_column), flags, _ptr(radius_out), _stream(stream)), "bgs_project")
+
+
+def bgs_route(ctx: Context, tile_owner_out=None, stream=None):
+    ctx.check(_lib.bgs_route(ctx.handle, _ptr(tile_owner_out), _stream(stream)), "bgs_route")
+
+
+def bgs_sort_tiles(ctx: Context, stream=None):
+    ctx.check(_lib.bgs_sort_tiles(ctx.handle, _stream(stream)), "bgs_sort_tiles")
+
+
+def bgs_raster_fwd(ctx: Context, flags: int, rgb, t_final, n_contrib, stream=None):
+    ctx.check(_lib.bgs_raster_fwd(ctx.handle, flags, _ptr(rgb), _ptr(t_final), _ptr(n_contrib), _stream(stream)),
+              "bgs_raster_fwd")
+
+
+def bgs_raster_bwd(ctx: Context, dL_drgb, t_final, n_contrib, stream=None):
+    ctx.check(_lib.bgs_raster_bwd(ctx.handle, _ptr(dL_drgb), _ptr(t_final), _ptr(n_contrib), _stream(stream)),
+              "bgs_raster_bwd")
+
+
+def bgs_route_reverse(ctx: Context, stream=None):
+    ctx.check(_lib.bgs_route_reverse(ctx.handle, _stream(stream)), "bgs_route_reverse")
+
+
+def bgs_project_bwd(ctx: Context, g: GaussianPlanes, cam: bgs_camera, grads: GradPlanes, stream=None):
+    gs, gr = g.struct(), grads.struct()
+    ctx.check(_lib.bgs_project_bwd(ctx.handle, C.byref(gs), C.byref(cam), C.byref(gr), _stream(stream)),
+              "bgs_project_bwd")
+
+
+def bgs_importance(ctx: Context, n_local: int, radius, w_fixed, a, s, c_rad, c_vis, cull_out, mass_num=99,
+                   mass_den=100, stream=None):
+    ctx.check(_lib.bgs_importance(ctx.handle, int(n_local), _ptr(radius), _ptr(w_fixed), _ptr(a), mass_num, mass_den,
+                                  _ptr(s), _ptr(c_rad), _ptr(c_vis), _ptr(cull_out), _stream(stream)),
+              "bgs_importance")
+
+
+def bgs_view_step(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags, radius_out, rgb, t_final,
+                  n_contrib, dL_drgb, grads: GradPlanes | None, importance: bgs_importance_out | None, stream=None):
+    gs = g.struct()
+    gr = grads.struct() if grads is not None else None
+    ctx.check(_lib.bgs_view_step(ctx.handle, C.byref(gs), C.byref(cam), C.byref(gate) if gate is not None else None,
+                                 _ptr(cull_column), flags, _ptr(radius_out), _ptr(rgb), _ptr(t_final),
+                                 _ptr(n_contrib), _ptr(dL_drgb), C.byref(gr) if gr is not None else None,
+                                 C.byref(importance) if importance is not None else None, _stream(stream)),
+              "bgs_view_step")
+
+
+def bgs_view_step_host(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags, radius_out,
+                       dL_host: torch.Tensor, rgb_host: torch.Tensor, grads: GradPlanes | None,
+                       importance: bgs_importance_out | None, stream=None):
+    gs = g.struct()
+    gr = grads.struct() if grads is not None else None
+    ctx.check(_lib.bgs_view_step_host(ctx.handle, C.byref(gs), C.byref(cam),
+                                      C.byref(gate) if gate is not None else None, _ptr(cull_column), flags,
+                                      _ptr(radius_out), _ptr(dL_host), _ptr(rgb_host),
+                                      C.byref(gr) if gr is not None else None,
+                                      C.byref(importance) if importance is not None else None, _stream(stream)),
+              "bgs_view_step_host")
+
+
+def importance_out(s, c_rad, c_vis, cull_out, num=99, den=100) -> bgs_importance_out:
+    return bgs_importance_out(s.data_ptr(), c_rad.data_ptr(), c_vis.data_ptr(), cull_out.data_ptr(), num, den)

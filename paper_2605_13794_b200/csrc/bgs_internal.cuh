@@ -1,0 +1,182 @@
+// Internal declarations shared by the libbgs translation units (NOT part of the ABI).
+// Layouts here are documented in DESIGN.md §6 ("Data layout in HBM").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bgs.h"
+
+namespace bgs {
+
+constexpr int kTile = 16;           // 16x16 pixel tiles (vanilla 3DGS)
+constexpr int kMaxWorld = 8;        // dest mask is one byte
+constexpr int kSortBlock = 256;     // onesweep CTA
+constexpr int kSortItems = 16;      // keys per thread per onesweep partition
+constexpr int kSortPart = kSortBlock * kSortItems;  // 4096 keys per partition
+constexpr int kMaxSortPasses = 6;   // 8-bit digits over <= 48 key bits
+
+// ProjectedSplat record, 48 B, three 16-B rows.
+struct __align__(16) Rec {
+  float mx, my, A, B;        // mean2d (px), conic A, B
+  float C, opac, r, g;       // conic C, opacity, colour
+  float b, depth;            // colour, camera z
+  uint32_t gid;              // global id = local*world + rank
+  uint32_t rect;             // x0 | y0<<8 | x1<<16 | y1<<24  (tiles, exclusive max)
+};
+static_assert(sizeof(Rec) == 48, "record is 48 B");
+
+// Per-splat accumulators: 9 gradients + a + w_fixed (48 B), the unit of the reverse exchange.
+struct __align__(16) Acc {
+  float g[9];                // dL/d(mx, my, A, B, C, o, r, g, b)
+  uint32_t a;                // qualifying pixel count a_{i,v}
+  unsigned long long w;      // sum of rint(alpha*T*2^24)
+};
+static_assert(sizeof(Acc) == 48, "accumulator is 48 B");
+
+// Device counters (u64 each) in the ctx arena.
+enum Counter : int {
+  C_F = 0,        // records produced by project
+  C_PALL = 1,     // sum of rect areas (pairs over all tiles) of this rank's records
+  C_NLOD = 2,     // |L^(m)|
+  C_NACT = 3,     // |A^(m)|
+  C_P = 4,        // pairs emitted for owned tiles
+  C_NCOUNTERS = 8
+};
+
+struct CameraK {
+  float fx, fy, cx, cy;
+  int W, H, TX, TY;
+  float R[9], t[3], campos[3], near_clip;
+};
+
+struct ProjectArgs {
+  const float4* mean_opac;
+  const float4* quat;
+  const float4* scale;
+  const float* sh;
+  const uint8_t* lod;
+  const uint32_t* cull;      // nullable
+  int64_t n;
+  CameraK cam;
+  int gate_enabled, l_max, fb_num, fb_den;
+  float D2[32];
+  int no_color;
+  int rank, world;
+  // outputs
+  int32_t* radius;
+  Rec* recs;
+  uint32_t* rec_lidx;
+  unsigned long long* counters;
+  int32_t* tile_diff;        // nullable: (TY+1)*(TX+1) 2D difference array of rect coverage
+  int64_t rec_cap;
+};
+
+void launch_gate_count(const ProjectArgs& a, cudaStream_t s);
+void launch_project(const ProjectArgs& a, cudaStream_t s);
+
+// sort (a5-a7)
+struct SortArgs {
+  const Rec* recv;
+  int64_t n_recv;
+  int TX, t_begin, t_end;
+  unsigned long long* keys[2];
+  uint32_t* vals[2];
+  int64_t cap;               // capacity of key/val buffers
+  unsigned long long* counters;
+  uint32_t* digit_hist;      // [kMaxSortPasses][256]
+  uint32_t* pass_ctrl;       // [16]: active flags, src selectors, partition counters
+  uint32_t* status;          // look-back status [n_parts][256] per pass
+  int n_passes;
+  uint2* ranges;             // [t_end - t_begin]
+};
+// emits pairs and digit histograms; returns nothing (P stays on device, counters[C_P])
+void launch_emit(const SortArgs& a, cudaStream_t s);
+void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches);
+void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s);
+// which buffer (0/1) holds the sorted data after the passes: read from pass_ctrl on device
+// by the consumers below.
+
+// raster (a8, a9)
+struct RasterArgs {
+  const Rec* recv;
+  const uint2* ranges;
+  const unsigned long long* keys[2];
+  const uint32_t* vals[2];
+  const uint32_t* pass_ctrl;  // final buffer selector at pass_ctrl[kFinalSel]
+  int t_begin, n_tiles, TX, W, H;
+  Acc* acc;
+};
+constexpr int kFinalSel = 15;
+void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
+                       cudaStream_t s);
+void launch_raster_bwd(const RasterArgs& a, const float* dL, const float* t_final, const int32_t* n_contrib,
+                       cudaStream_t s);
+
+// projection backward (a11)
+struct ProjectBwdArgs {
+  const float4* mean_opac;
+  const float4* quat;
+  const float4* scale;
+  const float* sh;
+  const uint32_t* rec_lidx;
+  const Acc* acc;            // per local record, owner-summed
+  int64_t F;
+  CameraK cam;
+  float4* g_mean_opac;
+  float4* g_quat;
+  float4* g_scale;
+  float* g_sh;
+};
+void launch_project_bwd(const ProjectBwdArgs& a, cudaStream_t s);
+
+// routing (a3, a4, a10) for world > 1
+void launch_tile_costs(const int32_t* diff, int TX, int TY, int32_t* pairs_t, cudaStream_t s);
+void launch_owner_map(const int32_t* pairs_t, int T, int world, int32_t* owner, int32_t* run /*[2*world]*/,
+                      long long* pown /*[world]*/, cudaStream_t s);
+void launch_dest_count(const Rec* recs, int64_t F, const int32_t* owner, int TX, int world, uint8_t* dest_mask,
+                       uint32_t* block_counts, cudaStream_t s);
+void launch_block_scan(uint32_t* block_counts, int64_t n_blocks, int world, unsigned long long* totals,
+                       cudaStream_t s);
+void launch_pack(const Rec* recs, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs, int world,
+                 const int64_t* send_base, Rec* send, cudaStream_t s);
+void launch_gather_sum(const Acc* rev, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs,
+                       int world, const int64_t* send_base, Acc* out, cudaStream_t s);
+struct PtrList {
+  const void* p[kMaxWorld];
+  int n;
+};
+void launch_reduce_sum_i32(PtrList src, int32_t* dst, int64_t n, cudaStream_t s);
+void launch_reduce_sum_u64(PtrList src, unsigned long long* dst, int64_t n, cudaStream_t s);
+constexpr int kRouteBlock = 256;
+
+// importance (a12)
+struct ImportanceArgs {
+  int64_t n_items;           // n_local (dense) or F (per record)
+  const uint32_t* item_lidx; // nullable: dense when null
+  const int32_t* radius;     // dense only
+  const unsigned long long* w_dense;
+  const uint32_t* a_dense;
+  const Acc* acc;            // per record when dense arrays are null
+  int64_t n_local;
+  int rank, world;
+  double* s;
+  uint32_t* c_rad;
+  uint32_t* c_vis;
+  uint32_t* cull;
+};
+struct ImpState;
+constexpr size_t kImpStateBytes = 128;
+int imp_w_rounds();
+int imp_g_rounds();
+void launch_imp_stats(const ImportanceArgs& a, unsigned long long* total, cudaStream_t s);
+void launch_imp_hist(const ImportanceArgs& a, const ImpState* st, int round, unsigned long long* hist,
+                     cudaStream_t s);
+void launch_imp_decide(ImpState* st, const unsigned long long* total, int round, const unsigned long long* hist,
+                       int num, int den, cudaStream_t s);
+void launch_imp_gid_hist(const ImportanceArgs& a, const ImpState* st, int round, unsigned long long* hist,
+                         cudaStream_t s);
+void launch_imp_gid_decide(ImpState* st, int round, const unsigned long long* hist, cudaStream_t s);
+void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s);
+void launch_fill_bits(uint32_t* words, int64_t n_bits, cudaStream_t s);
+
+}  // namespace bgs

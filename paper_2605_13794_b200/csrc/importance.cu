@@ -1,0 +1,291 @@
+// a12 importance bookkeeping for one view (bgs_importance).
+//
+// Eq.3: s_i = sum_{v: a_{i,v} > 0} w_{i,v} / (a_{i,v} + eps), eps = 1e-8 (R17);
+// c^rad_{i,v} = [radius > 0], c^vis_{i,v} = [w_{i,v} in the per-view top-99% mass] and
+// Cull_{i,v} = 1 - c^vis_{i,v}.  The top set is the smallest prefix of the
+// view's Gaussians ordered by (w desc, global id asc) whose mass reaches 99% of the total
+// (R16), over ALL ranks (the view is global).
+//
+// Selection = exact distributed radix select on the u64 fixed-point w (D5): 7 rounds of
+// 8-bit digits from bit 55 down; per round every rank builds a 256-bin (count, mass)
+// histogram of the candidates that still match the selected high digits, the histograms are
+// summed over ranks (all-reduce), and a one-CTA kernel picks the digit where the cumulative
+// mass from the top crosses the target.  After the last round the threshold value tau is
+// exact; the number k of ties (w == tau) that must be included is closed form, and when
+// 0 < k < #ties a count-only radix select over global ids (4 rounds) finds the k smallest
+// ids.  Every decision is integer, so the result is bit-exact and independent of M.
+// All state stays on the device: no host round trip.
+#include "bgs_internal.cuh"
+
+namespace bgs {
+
+struct alignas(16) ImpState {
+  unsigned long long total;      // sum of w over all ranks
+  unsigned long long above;      // mass strictly above the selected prefix
+  unsigned long long prefix;     // selected high digits of tau
+  unsigned long long tau;        // threshold value (valid after the w rounds)
+  unsigned long long k;          // ties to include
+  unsigned long long below;      // ties with gid below the selected gid prefix
+  unsigned long long ntie;       // number of ties (w == tau)
+  uint32_t gprefix;              // selected high digits of the gid threshold
+  uint32_t gid_thr;              // include ties with gid <= gid_thr
+  uint32_t need_gid;             // 0 < k < ntie
+  uint32_t empty;                // total == 0
+  uint32_t pad[2];
+};
+
+namespace {
+
+constexpr int kWRounds = 7;   // bits [0, 56)
+constexpr int kGRounds = 4;   // gid bits [0, 32)
+
+struct Item {
+  unsigned long long w;
+  uint32_t a;
+  uint32_t lidx;
+  bool rad;
+};
+
+__device__ __forceinline__ Item load_item(const ImportanceArgs& a, int64_t t) {
+  Item it;
+  if (a.item_lidx) {
+    const Acc& ac = a.acc[t];
+    it.w = ac.w;
+    it.a = ac.a;
+    it.lidx = a.item_lidx[t];
+    it.rad = true;  // every record had radius > 0
+  } else {
+    it.w = a.w_dense[t];
+    it.a = a.a_dense[t];
+    it.lidx = uint32_t(t);
+    it.rad = a.radius[t] > 0;
+  }
+  return it;
+}
+
+__device__ __forceinline__ uint32_t gid_of(const ImportanceArgs& a, uint32_t lidx) {
+  return lidx * uint32_t(a.world) + uint32_t(a.rank);
+}
+
+__global__ void __launch_bounds__(256) k_imp_stats(ImportanceArgs a, unsigned long long* total) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long w = 0;
+  if (t < a.n_items) {
+    const Item it = load_item(a, t);
+    w = it.w;
+    if (it.a > 0) a.s[it.lidx] += (double(it.w) * (1.0 / 16777216.0)) / (double(it.a) + 1e-8);
+    if (it.rad) a.c_rad[it.lidx] += 1u;
+  }
+  // block sum of w, one atomic
+  __shared__ unsigned long long s_w[8];
+  unsigned long long v = w;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long sum = 0;
+    for (int i = 0; i < 8; ++i) sum += s_w[i];
+    if (sum) atomicAdd(total, sum);
+  }
+}
+
+// candidates of round r: w > 0 and w >> (shift + 8) == prefix
+__global__ void __launch_bounds__(256) k_imp_hist(ImportanceArgs a, const ImpState* st, int round,
+                                                  unsigned long long* hist /*[256] count, [256] mass*/) {
+  __shared__ unsigned long long s_cnt[256], s_mass[256];
+  s_cnt[threadIdx.x] = 0;
+  s_mass[threadIdx.x] = 0;
+  __syncthreads();
+  const int shift = 8 * (kWRounds - 1 - round);
+  const unsigned long long prefix = st->prefix;
+  const bool empty = st->empty;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; !empty && t < a.n_items;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long w = a.item_lidx ? a.acc[t].w : a.w_dense[t];
+    if (w == 0) continue;
+    if (shift + 8 < 64 && (w >> (shift + 8)) != prefix) continue;
+    const uint32_t d = uint32_t((w >> shift) & 255u);
+    atomicAdd(&s_cnt[d], 1ull);
+    atomicAdd(&s_mass[d], w);
+  }
+  __syncthreads();
+  if (s_cnt[threadIdx.x]) {
+    atomicAdd(hist + threadIdx.x, s_cnt[threadIdx.x]);
+    atomicAdd(hist + 256 + threadIdx.x, s_mass[threadIdx.x]);
+  }
+}
+
+// one CTA: pick the digit where the cumulative mass (from the top) crosses num/den of total
+__global__ void __launch_bounds__(256) k_imp_decide(ImpState* st, const unsigned long long* total_in, int round,
+                                                    const unsigned long long* hist, int num, int den) {
+  __shared__ unsigned long long s_suf[256];
+  __shared__ int s_pick;
+  const int d = threadIdx.x;
+  if (round == 0) {
+    if (d == 0) {
+      st->total = *total_in;
+      st->empty = st->total == 0;
+      st->above = 0;
+      st->prefix = 0;
+    }
+    __syncthreads();
+  }
+  if (st->empty) return;
+  const unsigned long long target = (unsigned long long)num * st->total;  // need den*prefix >= target
+  // inclusive suffix sums of mass (digits d..255)
+  s_suf[255 - d] = hist[256 + d];
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const unsigned long long v = d >= o ? s_suf[d - o] : 0ull;
+    __syncthreads();
+    s_suf[d] += v;
+    __syncthreads();
+  }
+  // s_suf[j] = mass of digits >= 255 - j.  The crossing digit is the largest d with
+  // den*(above + mass(>= d)) >= target.
+  if (d == 0) s_pick = -1;
+  __syncthreads();
+  const unsigned long long above = st->above;
+  const unsigned long long incl = s_suf[255 - d];                      // mass of digits >= d
+  const unsigned long long excl = d < 255 ? s_suf[254 - d] : 0ull;     // mass of digits > d
+  const bool cross = (unsigned long long)den * (above + incl) >= target &&
+                     (unsigned long long)den * (above + excl) < target;
+  if (cross && hist[d] > 0) s_pick = d;
+  __syncthreads();
+  if (d == 0) {
+    const int pick = s_pick;
+    if (pick >= 0) {
+      st->above = above + (pick < 255 ? s_suf[254 - pick] : 0ull);
+      st->prefix = (st->prefix << 8) | unsigned(pick);
+      if (round == kWRounds - 1) {
+        const unsigned long long tau = st->prefix;
+        st->tau = tau;
+        const unsigned long long ntie = hist[pick];
+        const unsigned long long need = target - (unsigned long long)den * st->above;  // > 0
+        const unsigned long long k = (need + (unsigned long long)den * tau - 1) / ((unsigned long long)den * tau);
+        st->k = k < ntie ? k : ntie;
+        st->ntie = ntie;
+        st->need_gid = (st->k < ntie) ? 1u : 0u;
+        st->gprefix = 0;
+        st->below = 0;
+        st->gid_thr = 0xffffffffu;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_imp_gid_hist(ImportanceArgs a, const ImpState* st, int round,
+                                                      unsigned long long* hist /*[256] counts*/) {
+  __shared__ unsigned long long s_cnt[256];
+  s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const bool run = !st->empty && st->need_gid;
+  const int shift = 8 * (kGRounds - 1 - round);
+  const unsigned long long tau = st->tau;
+  const uint32_t gp = st->gprefix;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; run && t < a.n_items;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const Item it = load_item(a, t);
+    if (it.w != tau) continue;
+    const uint32_t g = gid_of(a, it.lidx);
+    if (shift + 8 < 32 && (g >> (shift + 8)) != gp) continue;
+    atomicAdd(&s_cnt[(g >> shift) & 255u], 1ull);
+  }
+  __syncthreads();
+  if (s_cnt[threadIdx.x]) atomicAdd(hist + threadIdx.x, s_cnt[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_imp_gid_decide(ImpState* st, int round, const unsigned long long* hist) {
+  __shared__ unsigned long long s_pre[256];
+  __shared__ int s_pick;
+  if (st->empty || !st->need_gid) return;
+  const int d = threadIdx.x;
+  s_pre[d] = hist[d];
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const unsigned long long v = d >= o ? s_pre[d - o] : 0ull;
+    __syncthreads();
+    s_pre[d] += v;
+    __syncthreads();
+  }
+  if (d == 0) s_pick = -1;
+  __syncthreads();
+  const unsigned long long below = st->below, k = st->k;
+  const unsigned long long incl = s_pre[d], excl = d > 0 ? s_pre[d - 1] : 0ull;
+  if (below + incl >= k && below + excl < k) s_pick = d;
+  __syncthreads();
+  if (d == 0 && s_pick >= 0) {
+    st->below = below + (s_pick > 0 ? s_pre[s_pick - 1] : 0ull);
+    st->gprefix = (st->gprefix << 8) | uint32_t(s_pick);
+    if (round == kGRounds - 1) st->gid_thr = st->gprefix;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_imp_mark(ImportanceArgs a, const ImpState* st) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= a.n_items || st->empty) return;
+  const Item it = load_item(a, t);
+  if (it.w == 0) return;
+  const unsigned long long tau = st->tau;
+  bool in = it.w > tau;
+  if (it.w == tau) in = !st->need_gid || gid_of(a, it.lidx) <= st->gid_thr;
+  if (!in) return;
+  a.c_vis[it.lidx] += 1u;
+  atomicAnd(a.cull + (it.lidx >> 5), ~(1u << (it.lidx & 31)));
+}
+
+// all bits [0, n_bits) set, bits past n_bits in the last word clear
+__global__ void k_fill_bits(uint32_t* words, int64_t n_bits) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nw = (n_bits + 31) / 32;
+  if (t >= nw) return;
+  const int64_t rem = n_bits - 32 * t;
+  words[t] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+}
+
+}  // namespace
+
+static_assert(sizeof(ImpState) <= kImpStateBytes, "state fits its arena slot");
+int imp_w_rounds() { return kWRounds; }
+int imp_g_rounds() { return kGRounds; }
+
+void launch_fill_bits(uint32_t* words, int64_t n_bits, cudaStream_t s) {
+  const int64_t nw = (n_bits + 31) / 32;
+  if (nw > 0) k_fill_bits<<<unsigned((nw + 255) / 256), 256, 0, s>>>(words, n_bits);
+}
+
+void launch_imp_stats(const ImportanceArgs& a, unsigned long long* total, cudaStream_t s) {
+  if (a.n_items > 0) k_imp_stats<<<unsigned((a.n_items + 255) / 256), 256, 0, s>>>(a, total);
+}
+
+static unsigned grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
+  return unsigned(b < 1 ? 1 : b);
+}
+
+void launch_imp_hist(const ImportanceArgs& a, const ImpState* st, int round, unsigned long long* hist,
+                     cudaStream_t s) {
+  k_imp_hist<<<grid_for(a.n_items), 256, 0, s>>>(a, st, round, hist);
+}
+
+void launch_imp_decide(ImpState* st, const unsigned long long* total, int round, const unsigned long long* hist,
+                       int num, int den, cudaStream_t s) {
+  k_imp_decide<<<1, 256, 0, s>>>(st, total, round, hist, num, den);
+}
+
+void launch_imp_gid_hist(const ImportanceArgs& a, const ImpState* st, int round, unsigned long long* hist,
+                         cudaStream_t s) {
+  k_imp_gid_hist<<<grid_for(a.n_items), 256, 0, s>>>(a, st, round, hist);
+}
+
+void launch_imp_gid_decide(ImpState* st, int round, const unsigned long long* hist, cudaStream_t s) {
+  k_imp_gid_decide<<<1, 256, 0, s>>>(st, round, hist);
+}
+
+void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s) {
+  if (a.n_items > 0) k_imp_mark<<<unsigned((a.n_items + 255) / 256), 256, 0, s>>>(a, st);
+}
+
+}  // namespace bgs

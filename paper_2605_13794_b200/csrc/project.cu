@@ -1,0 +1,245 @@
+// a1 gate + a2 projection (bgs_project).
+//
+// PAPER.md §3.1 P:143-152 (Eq.1 Gaussian, EWA "projected to screen-space ellipses"), §3.2
+// ("every GPU projects only its own local Gaussians"), §3.4 Eq.4-6 P:195-210 (LOD gate, cull).
+//
+// PINNED ARITHMETIC (D2): this translation unit is compiled with -fmad=false and
+// IEEE div/sqrt so that every float expression below rounds exactly as written; radius,
+// rect, tile ids and pair counts are integers derived from these floats and must be
+// bit-identical to the oracle's.  Expression trees are the ones listed in DESIGN.md §4.
+//
+// Memory plan (HBM-bound): one thread per local Gaussian; 16-B loads of (mu, o) and the lod
+// byte for everyone; quat/scale (32 B) only for Gaussians that pass the gate; the 192-B SH
+// row only for Gaussians that are in the frustum; 48-B record + 4-B index written through a
+// warp-aggregated append; radius (4 B) written for all.
+#include "bgs_internal.cuh"
+
+namespace bgs {
+namespace {
+
+__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+
+__device__ __forceinline__ bool lod_keep(const ProjectArgs& a, float4 mo, int l) {
+  float dx = mo.x - a.cam.campos[0];
+  float dy = mo.y - a.cam.campos[1];
+  float dz = mo.z - a.cam.campos[2];
+  float d2 = (dx * dx + dy * dy) + dz * dz;
+  return (l <= a.l_max) && (l == 0 || d2 <= a.D2[l < 31 ? l : 31]);
+}
+
+__global__ void __launch_bounds__(256) k_gate_count(ProjectArgs a) {
+  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  int ok = 0;
+  if (i < a.n) ok = lod_keep(a, ldg4(a.mean_opac + i), a.lod[i]) ? 1 : 0;
+  int c = __syncthreads_count(ok);
+  if (threadIdx.x == 0 && c) atomicAdd(a.counters + C_NLOD, (unsigned long long)c);
+}
+
+__global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool valid = false;
+  bool active = false;
+  Rec rec;
+  int radius = 0;
+  uint32_t area = 0;
+  int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
+  if (i < a.n) {
+    const float4 mo = ldg4(a.mean_opac + i);
+    // ---- a1: Eq.5 gate with per-rank fallback, then Eq.6 cull column
+    bool keep = true;
+    if (a.gate_enabled) {
+      const unsigned long long nl = *((volatile unsigned long long*)(a.counters + C_NLOD));
+      const bool fallback = (unsigned long long)a.fb_den * nl > (unsigned long long)a.fb_num * (unsigned long long)a.n;
+      if (!fallback) keep = lod_keep(a, mo, a.lod[i]);
+    }
+    if (keep && a.cull) keep = !((__ldg(a.cull + (i >> 5)) >> (i & 31)) & 1u);
+    active = keep;
+    if (keep) {
+      const CameraK& cm = a.cam;
+      // ---- a2: t_c = R mu + t
+      const float tx = ((cm.R[0] * mo.x + cm.R[1] * mo.y) + cm.R[2] * mo.z) + cm.t[0];
+      const float ty = ((cm.R[3] * mo.x + cm.R[4] * mo.y) + cm.R[5] * mo.z) + cm.t[1];
+      const float tz = ((cm.R[6] * mo.x + cm.R[7] * mo.y) + cm.R[8] * mo.z) + cm.t[2];
+      if (tz > cm.near_clip) {
+        // Sigma = R(q) S S^T R(q)^T
+        const float4 q = ldg4(a.quat + i);
+        const float4 sc = ldg4(a.scale + i);
+        const float xx = q.y * q.y, yy = q.z * q.z, zz = q.w * q.w;
+        const float xy = q.y * q.z, xz = q.y * q.w, yz = q.z * q.w;
+        const float wx = q.x * q.y, wy = q.x * q.z, wz = q.x * q.w;
+        const float Rq[3][3] = {{1.0f - 2.0f * (yy + zz), 2.0f * (xy - wz), 2.0f * (xz + wy)},
+                                {2.0f * (xy + wz), 1.0f - 2.0f * (xx + zz), 2.0f * (yz - wx)},
+                                {2.0f * (xz - wy), 2.0f * (yz + wx), 1.0f - 2.0f * (xx + yy)}};
+        const float s3[3] = {sc.x, sc.y, sc.z};
+        float M[3][3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) M[r][c] = Rq[r][c] * s3[c];
+        float S[3][3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) S[r][c] = (M[r][0] * M[c][0] + M[r][1] * M[c][1]) + M[r][2] * M[c][2];
+        // EWA Jacobian with the 1.3 tan(fov/2) clamp (off-centre principal point)
+        const float Wf = float(cm.W), Hf = float(cm.H);
+        const float tan_fovx = (0.5f * Wf) / cm.fx;
+        const float tan_fovy = (0.5f * Hf) / cm.fy;
+        const float lim_xp = (Wf - cm.cx) / cm.fx + 0.3f * tan_fovx;
+        const float lim_xn = cm.cx / cm.fx + 0.3f * tan_fovx;
+        const float lim_yp = (Hf - cm.cy) / cm.fy + 0.3f * tan_fovy;
+        const float lim_yn = cm.cy / cm.fy + 0.3f * tan_fovy;
+        const float txtz = tx / tz, tytz = ty / tz;
+        const float ctx = fminf(lim_xp, fmaxf(-lim_xn, txtz)) * tz;
+        const float cty = fminf(lim_yp, fmaxf(-lim_yn, tytz)) * tz;
+        const float J00 = cm.fx / tz, J02 = -(cm.fx * ctx) / (tz * tz);
+        const float J11 = cm.fy / tz, J12 = -(cm.fy * cty) / (tz * tz);
+        float Tm[2][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          Tm[0][c] = J00 * cm.R[c] + J02 * cm.R[6 + c];
+          Tm[1][c] = J11 * cm.R[3 + c] + J12 * cm.R[6 + c];
+        }
+        float U[2][3];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) U[r][c] = (Tm[r][0] * S[0][c] + Tm[r][1] * S[1][c]) + Tm[r][2] * S[2][c];
+        float ca = (U[0][0] * Tm[0][0] + U[0][1] * Tm[0][1]) + U[0][2] * Tm[0][2];
+        const float cb = (U[0][0] * Tm[1][0] + U[0][1] * Tm[1][1]) + U[0][2] * Tm[1][2];
+        float cc = (U[1][0] * Tm[1][0] + U[1][1] * Tm[1][1]) + U[1][2] * Tm[1][2];
+        ca = ca + 0.3f;
+        cc = cc + 0.3f;
+        const float det = ca * cc - cb * cb;
+        if (det > 0.0f) {
+          rec.A = cc / det;
+          rec.B = (-cb) / det;
+          rec.C = ca / det;
+          rec.mx = cm.fx * txtz + cm.cx;
+          rec.my = cm.fy * tytz + cm.cy;
+          const float mid = 0.5f * (ca + cc);
+          const float disc = fmaxf(0.1f, mid * mid - det);
+          const float lambda1 = mid + sqrtf(disc);
+          const float rf = fminf(ceilf(3.0f * sqrtf(lambda1)), 1048576.0f);
+          const int rad = int(rf);
+          const float r_ = float(rad);
+          const float fx0 = (rec.mx - r_) / 16.0f;
+          const float fy0 = (rec.my - r_) / 16.0f;
+          const float fx1 = ((rec.mx + r_) + 15.0f) / 16.0f;
+          const float fy1 = ((rec.my + r_) + 15.0f) / 16.0f;
+          x0 = int(fminf(float(cm.TX), fmaxf(0.0f, fx0)));
+          y0 = int(fminf(float(cm.TY), fmaxf(0.0f, fy0)));
+          x1 = int(fminf(float(cm.TX), fmaxf(0.0f, fx1)));
+          y1 = int(fminf(float(cm.TY), fmaxf(0.0f, fy1)));
+          area = uint32_t((x1 - x0) * (y1 - y0));
+          if (area != 0) {
+            valid = true;
+            radius = rad;
+            rec.depth = tz;
+            rec.opac = mo.w;
+            rec.gid = uint32_t(i) * uint32_t(a.world) + uint32_t(a.rank);
+            rec.rect = uint32_t(x0) | (uint32_t(y0) << 8) | (uint32_t(x1) << 16) | (uint32_t(y1) << 24);
+            rec.r = rec.g = rec.b = 0.0f;
+            if (!a.no_color) {
+              // SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2
+              const float dx = mo.x - cm.campos[0], dy = mo.y - cm.campos[1], dz = mo.z - cm.campos[2];
+              const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
+              const float x = dx / len, y = dy / len, z = dz / len;
+              const float xx2 = x * x, yy2 = y * y, zz2 = z * z, xy2 = x * y, yz2 = y * z, xz2 = x * z;
+              float Y[16];
+              Y[0] = 0.28209479177387814f;
+              Y[1] = -(0.4886025119029199f * y);
+              Y[2] = 0.4886025119029199f * z;
+              Y[3] = -(0.4886025119029199f * x);
+              Y[4] = 1.0925484305920792f * xy2;
+              Y[5] = -1.0925484305920792f * yz2;
+              Y[6] = 0.31539156525252005f * ((2.0f * zz2 - xx2) - yy2);
+              Y[7] = -1.0925484305920792f * xz2;
+              Y[8] = 0.5462742152960396f * (xx2 - yy2);
+              Y[9] = (-0.5900435899266435f * y) * (3.0f * xx2 - yy2);
+              Y[10] = (2.890611442640554f * xy2) * z;
+              Y[11] = (-0.4570457994644658f * y) * ((4.0f * zz2 - xx2) - yy2);
+              Y[12] = (0.3731763325901154f * z) * ((2.0f * zz2 - 3.0f * xx2) - 3.0f * yy2);
+              Y[13] = (-0.4570457994644658f * x) * ((4.0f * zz2 - xx2) - yy2);
+              Y[14] = (1.445305721320277f * z) * (xx2 - yy2);
+              Y[15] = (-0.5900435899266435f * x) * (xx2 - 3.0f * yy2);
+              const float4* shp = reinterpret_cast<const float4*>(a.sh + 48 * i);
+              float col[3] = {0.f, 0.f, 0.f};
+              float v[48];
+#pragma unroll
+              for (int q4 = 0; q4 < 12; ++q4) {
+                const float4 f = ldg4(shp + q4);
+                v[4 * q4 + 0] = f.x;
+                v[4 * q4 + 1] = f.y;
+                v[4 * q4 + 2] = f.z;
+                v[4 * q4 + 3] = f.w;
+              }
+#pragma unroll
+              for (int ch = 0; ch < 3; ++ch) {
+                float c = Y[0] * v[ch];
+#pragma unroll
+                for (int k = 1; k < 16; ++k) c = c + Y[k] * v[3 * k + ch];
+                c = c + 0.5f;
+                col[ch] = c < 0.0f ? 0.0f : c;
+              }
+              rec.r = col[0];
+              rec.g = col[1];
+              rec.b = col[2];
+            }
+          }
+        }
+      }
+    }
+    a.radius[i] = valid ? radius : 0;
+  }
+  // ---- warp-aggregated append of the record (one atomic per warp)
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  const unsigned amask = __ballot_sync(0xffffffffu, active);
+  // pairs over all tiles (P_all) and active count: warp sums, one atomic per warp
+  unsigned long long wsum = __reduce_add_sync(0xffffffffu, area);
+  if (vmask) {
+    const int leader = __ffs(vmask) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) {
+      base = atomicAdd(a.counters + C_F, (unsigned long long)__popc(vmask));
+      atomicAdd(a.counters + C_PALL, wsum);
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) {
+      const unsigned long long slot = base + __popc(vmask & ((1u << lane) - 1u));
+      if ((int64_t)slot < a.rec_cap) {
+        float4* dst = reinterpret_cast<float4*>(a.recs + slot);
+        dst[0] = make_float4(rec.mx, rec.my, rec.A, rec.B);
+        dst[1] = make_float4(rec.C, rec.opac, rec.r, rec.g);
+        dst[2] = make_float4(rec.b, rec.depth, __uint_as_float(rec.gid), __uint_as_float(rec.rect));
+        a.rec_lidx[slot] = uint32_t(i);
+      }
+      if (a.tile_diff) {
+        // 2D difference array of rect coverage -> per-tile pair counts (a3 input)
+        const int W1 = a.cam.TX + 1;
+        atomicAdd(a.tile_diff + y0 * W1 + x0, 1);
+        atomicAdd(a.tile_diff + y0 * W1 + x1, -1);
+        atomicAdd(a.tile_diff + y1 * W1 + x0, -1);
+        atomicAdd(a.tile_diff + y1 * W1 + x1, 1);
+      }
+    }
+  }
+  if (amask && lane == __ffs(amask) - 1) atomicAdd(a.counters + C_NACT, (unsigned long long)__popc(amask));
+}
+
+}  // namespace
+
+void launch_gate_count(const ProjectArgs& a, cudaStream_t s) {
+  if (a.n <= 0) return;
+  const int64_t blocks = (a.n + 255) / 256;
+  k_gate_count<<<unsigned(blocks), 256, 0, s>>>(a);
+}
+
+void launch_project(const ProjectArgs& a, cudaStream_t s) {
+  if (a.n <= 0) return;
+  const int64_t blocks = (a.n + 255) / 256;
+  k_project<<<unsigned(blocks), 256, 0, s>>>(a);
+}
+
+}  // namespace bgs

@@ -1,0 +1,882 @@
+// libbgs host runtime: context, workspace arena, transports (NCCL / in-process device group),
+// and the C ABI entry points of include/bgs.h.  Orchestration only; every step of the path
+// runs in the kernels of project.cu, sort.cu, raster.cu, project_bwd.cu, route.cu and
+// importance.cu.  There is no CPU fallback: without a CUDA device every call fails.
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bgs_internal.cuh"
+
+using namespace bgs;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct Transport;
+
+}  // namespace
+
+struct bgs_ctx {
+  int rank = 0, world = 1, device = 0;
+  std::shared_ptr<Transport> tr;
+  std::string err;
+  int64_t launches = 0;
+  // view state
+  CameraK cam{};
+  int T = 0;
+  int stage = 0;  // 1 projected, 2 routed, 3 sorted, 4 fwd, 5 bwd, 6 reversed
+  int64_t n_local = 0, F = 0, P_all = 0, R = 0, D = 0, P = 0, n_lod = 0, n_act = 0;
+  int t_begin = 0, t_end = 0, n_passes = 0, fallback = 0;
+  const Rec* recv = nullptr;  // == recs at world 1
+  Acc* acc_local = nullptr;   // == acc at world 1
+  // arena
+  DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
+      send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
+      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts;
+  unsigned long long* h_counters = nullptr;  // pinned
+  int64_t* h_misc = nullptr;                 // pinned scratch for routing sizes
+  std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
+};
+
+namespace {
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKS(call)                                   \
+  do {                                              \
+    bgs_status s_ = (call);                         \
+    if (s_ != BGS_OK) return s_;                    \
+  } while (0)
+
+bgs_status fail(bgs_ctx* ctx, bgs_status st, const char* what, const char* detail = "") {
+  if (ctx) ctx->err = std::string(what) + (detail && *detail ? std::string(": ") + detail : std::string());
+  return st;
+}
+
+bgs_status launched(bgs_ctx* ctx, int n = 1) {
+  ctx->launches += n;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "kernel launch", cudaGetErrorString(e));
+  return BGS_OK;
+}
+
+bgs_status ensure(bgs_ctx* ctx, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (bytes <= b.cap) return BGS_OK;
+  if (b.p) {
+    cudaError_t e = cudaFree(b.p);
+    if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "cudaFree", cudaGetErrorString(e));
+  }
+  size_t want = bytes + bytes / 4 + 256;
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) {
+    b.p = nullptr;
+    b.cap = 0;
+    char msg[128];
+    snprintf(msg, sizeof msg, "arena grow to %zu bytes", want);
+    return fail(ctx, BGS_ERR_CAPACITY, msg, cudaGetErrorString(e));
+  }
+  b.cap = want;
+  return BGS_OK;
+}
+
+template <class T>
+T* P_(DevBuf& b) {
+  return static_cast<T*>(b.p);
+}
+
+// ---------------------------------------------------------------------------------------
+// Transports
+// ---------------------------------------------------------------------------------------
+struct Transport {
+  virtual ~Transport() = default;
+  virtual bgs_status allreduce_i32(bgs_ctx* ctx, int32_t* buf, int64_t n, cudaStream_t s) = 0;
+  virtual bgs_status allreduce_u64(bgs_ctx* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) = 0;
+  // device int64 [world] -> device int64 [world]: element d of send goes to rank d
+  virtual bgs_status alltoall1(bgs_ctx* ctx, const int64_t* send, int64_t* recv, cudaStream_t s) = 0;
+  virtual bgs_status alltoallv(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
+                               const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) = 0;
+};
+
+bgs_status nccl_fail(bgs_ctx* ctx, ncclResult_t r, const char* what) {
+  return fail(ctx, BGS_ERR_NCCL, what, ncclGetErrorString(r));
+}
+
+struct NcclTransport : Transport {
+  ncclComm_t comm = nullptr;
+  ~NcclTransport() override {
+    if (comm) ncclCommDestroy(comm);
+  }
+  bgs_status allreduce_i32(bgs_ctx* ctx, int32_t* buf, int64_t n, cudaStream_t s) override {
+    ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclInt32, ncclSum, comm, s);
+    return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
+  }
+  bgs_status allreduce_u64(bgs_ctx* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) override {
+    ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclUint64, ncclSum, comm, s);
+    return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
+  }
+  bgs_status alltoall1(bgs_ctx* ctx, const int64_t* send, int64_t* recv, cudaStream_t s) override {
+    ncclResult_t r = ncclGroupStart();
+    for (int p = 0; p < ctx->world && r == ncclSuccess; ++p) {
+      r = ncclSend(send + p, 1, ncclInt64, p, comm, s);
+      if (r == ncclSuccess) r = ncclRecv(recv + p, 1, ncclInt64, p, comm, s);
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclSend/Recv counts");
+    return r2 == ncclSuccess ? BGS_OK : nccl_fail(ctx, r2, "ncclGroupEnd");
+  }
+  bgs_status alltoallv(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
+                       const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) override {
+    ncclResult_t r = ncclGroupStart();
+    for (int p = 0; p < ctx->world && r == ncclSuccess; ++p) {
+      if (scnt[p] > 0)
+        r = ncclSend(static_cast<const char*>(send) + soff[p] * elem, size_t(scnt[p]) * elem, ncclChar, p, comm, s);
+      if (r == ncclSuccess && rcnt[p] > 0)
+        r = ncclRecv(static_cast<char*>(recv) + roff[p] * elem, size_t(rcnt[p]) * elem, ncclChar, p, comm, s);
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclSend/Recv records");
+    return r2 == ncclSuccess ? BGS_OK : nccl_fail(ctx, r2, "ncclGroupEnd");
+  }
+};
+
+// In-process group of `world` contexts on one device (test transport).  Collectives are
+// device-to-device copies / reduction kernels ordered by CUDA events; a host barrier orders
+// the publication of pointers.  Each ctx is driven by its own host thread.
+struct LocalGroup {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> ptr;
+  std::vector<const int64_t*> cnt, off;
+  std::vector<cudaEvent_t> ready, done;
+  explicit LocalGroup(int w) : world(w), ptr(w), cnt(w), off(w), ready(w), done(w) {
+    for (int i = 0; i < w; ++i) {
+      cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+    }
+  }
+  ~LocalGroup() {
+    for (int i = 0; i < world; ++i) {
+      cudaEventDestroy(ready[i]);
+      cudaEventDestroy(done[i]);
+    }
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LocalTransport : Transport {
+  std::shared_ptr<LocalGroup> g;
+  DevBuf tmp;  // reduction scratch
+  explicit LocalTransport(std::shared_ptr<LocalGroup> grp) : g(std::move(grp)) {}
+  ~LocalTransport() override {
+    if (tmp.p) cudaFree(tmp.p);
+  }
+  template <class T, class L>
+  bgs_status allreduce(bgs_ctx* ctx, T* buf, int64_t n, cudaStream_t s, L launch) {
+    const int r = ctx->rank;
+    CKS(ensure(ctx, tmp, size_t(n) * sizeof(T)));
+    g->ptr[r] = buf;
+    CK(cudaEventRecord(g->ready[r], s));
+    g->barrier();
+    PtrList pl{};
+    pl.n = g->world;
+    for (int k = 0; k < g->world; ++k) {
+      pl.p[k] = g->ptr[k];
+      CK(cudaStreamWaitEvent(s, g->ready[k], 0));
+    }
+    launch(pl, static_cast<T*>(tmp.p), n, s);
+    CKS(launched(ctx));
+    CK(cudaEventRecord(g->done[r], s));
+    g->barrier();
+    for (int k = 0; k < g->world; ++k) CK(cudaStreamWaitEvent(s, g->done[k], 0));
+    CK(cudaMemcpyAsync(buf, tmp.p, size_t(n) * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    g->barrier();  // nobody republishes before everyone has queued its waits
+    return BGS_OK;
+  }
+  bgs_status allreduce_i32(bgs_ctx* ctx, int32_t* buf, int64_t n, cudaStream_t s) override {
+    return allreduce(ctx, buf, n, s, [](PtrList p, int32_t* d, int64_t nn, cudaStream_t ss) {
+      launch_reduce_sum_i32(p, d, nn, ss);
+    });
+  }
+  bgs_status allreduce_u64(bgs_ctx* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) override {
+    return allreduce(ctx, buf, n, s, [](PtrList p, unsigned long long* d, int64_t nn, cudaStream_t ss) {
+      launch_reduce_sum_u64(p, d, nn, ss);
+    });
+  }
+  bgs_status exchange(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
+                      const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) {
+    const int r = ctx->rank;
+    g->ptr[r] = send;
+    g->cnt[r] = scnt;
+    g->off[r] = soff;
+    CK(cudaEventRecord(g->ready[r], s));
+    g->barrier();
+    for (int k = 0; k < g->world; ++k) {
+      CK(cudaStreamWaitEvent(s, g->ready[k], 0));
+      const int64_t c = g->cnt[k][r];
+      if (c != rcnt[k]) return fail(ctx, BGS_ERR_INTERNAL, "local exchange: count mismatch");
+      if (c > 0)
+        CK(cudaMemcpyAsync(static_cast<char*>(recv) + roff[k] * elem,
+                           static_cast<const char*>(g->ptr[k]) + g->off[k][r] * elem, size_t(c) * elem,
+                           cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaEventRecord(g->done[r], s));
+    g->barrier();
+    for (int k = 0; k < g->world; ++k) CK(cudaStreamWaitEvent(s, g->done[k], 0));
+    g->barrier();
+    return BGS_OK;
+  }
+  bgs_status alltoall1(bgs_ctx* ctx, const int64_t* send, int64_t* recv, cudaStream_t s) override {
+    std::vector<int64_t> one(ctx->world, 1), idx(ctx->world);
+    for (int k = 0; k < ctx->world; ++k) idx[k] = k;
+    return exchange(ctx, send, one.data(), idx.data(), recv, one.data(), idx.data(), sizeof(int64_t), s);
+  }
+  bgs_status alltoallv(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
+                       const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) override {
+    return exchange(ctx, send, scnt, soff, recv, rcnt, roff, elem, s);
+  }
+};
+
+// ---------------------------------------------------------------------------------------
+bgs_status check_ctx(bgs_ctx* ctx) {
+  if (!ctx) return BGS_ERR_INVALID_ARGUMENT;
+  ctx->err.clear();
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "cudaSetDevice", cudaGetErrorString(e));
+  return BGS_OK;
+}
+
+bgs_status check_stream(bgs_ctx* ctx, void* stream) {
+  if (!stream) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "stream must be a real cudaStream_t (not NULL)");
+  return BGS_OK;
+}
+
+bgs_status set_camera(bgs_ctx* ctx, const bgs_camera* c) {
+  if (!c) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "camera is NULL");
+  if (c->width <= 0 || c->height <= 0 || !(c->fx > 0) || !(c->fy > 0) || !(c->near_clip > 0))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "camera: width/height/fx/fy/near_clip must be > 0");
+  CameraK& k = ctx->cam;
+  k.fx = c->fx;
+  k.fy = c->fy;
+  k.cx = c->cx;
+  k.cy = c->cy;
+  k.W = c->width;
+  k.H = c->height;
+  k.TX = (c->width + kTile - 1) / kTile;
+  k.TY = (c->height + kTile - 1) / kTile;
+  if (k.TX > 255 || k.TY > 255) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "image too large (tiles per axis <= 255)");
+  std::memcpy(k.R, c->R, sizeof k.R);
+  std::memcpy(k.t, c->t, sizeof k.t);
+  std::memcpy(k.campos, c->campos, sizeof k.campos);
+  k.near_clip = c->near_clip;
+  ctx->T = k.TX * k.TY;
+  return BGS_OK;
+}
+
+bgs_status check_gaussians(bgs_ctx* ctx, const bgs_gaussians* g) {
+  if (!g) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "gaussians is NULL");
+  if (g->n_local < 0) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "n_local < 0");
+  if (g->n_local > 0 && (!g->mean_opac || !g->quat || !g->scale || !g->sh || !g->lod))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "gaussian plane pointer is NULL");
+  if (g->n_local >= (int64_t(1) << 31)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "n_local >= 2^31");
+  return BGS_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+bgs_status bgs_get_unique_id(void* out) {
+  if (!out) return BGS_ERR_INVALID_ARGUMENT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return BGS_ERR_NCCL;
+  std::memcpy(out, &id, sizeof id);
+  return BGS_OK;
+}
+
+static bgs_status ctx_alloc_common(bgs_ctx* c) {
+  bgs_ctx* ctx = c;
+  CK(cudaSetDevice(c->device));
+  CK(cudaMallocHost(&c->h_counters, sizeof(unsigned long long) * C_NCOUNTERS));
+  CK(cudaMallocHost(&c->h_misc, sizeof(int64_t) * 64));
+  CKS(ensure(c, c->counters, sizeof(unsigned long long) * C_NCOUNTERS));
+  return BGS_OK;
+}
+
+bgs_status bgs_ctx_create(int32_t rank, int32_t world, const void* uid, int32_t device, bgs_ctx** out) {
+  if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world) return BGS_ERR_INVALID_ARGUMENT;
+  if (world > 1 && !uid) return BGS_ERR_INVALID_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return BGS_ERR_CUDA;  // no CPU fallback
+  auto* c = new bgs_ctx();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  bgs_status st = ctx_alloc_common(c);
+  if (st != BGS_OK) {
+    delete c;
+    return st;
+  }
+  if (world > 1) {
+    auto t = std::make_shared<NcclTransport>();
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    if (ncclCommInitRank(&t->comm, world, id, rank) != ncclSuccess) {
+      delete c;
+      return BGS_ERR_NCCL;
+    }
+    c->tr = t;
+  }
+  *out = c;
+  return BGS_OK;
+}
+
+bgs_status bgs_ctx_create_local_group(int32_t world, int32_t device, bgs_ctx** out) {
+  if (!out || world < 1 || world > kMaxWorld) return BGS_ERR_INVALID_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return BGS_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return BGS_ERR_CUDA;
+  auto grp = std::make_shared<LocalGroup>(world);
+  for (int r = 0; r < world; ++r) {
+    auto* c = new bgs_ctx();
+    c->rank = r;
+    c->world = world;
+    c->device = device;
+    if (ctx_alloc_common(c) != BGS_OK) return BGS_ERR_CUDA;
+    if (world > 1) c->tr = std::make_shared<LocalTransport>(grp);
+    out[r] = c;
+  }
+  return BGS_OK;
+}
+
+bgs_status bgs_ctx_destroy(bgs_ctx* c) {
+  if (!c) return BGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  DevBuf* bufs[] = {&c->counters, &c->recs, &c->rec_lidx, &c->tile_diff, &c->tile_pairs, &c->owner, &c->runinfo,
+                    &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
+                    &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
+                    &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts};
+  for (DevBuf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (c->h_counters) cudaFreeHost(c->h_counters);
+  if (c->h_misc) cudaFreeHost(c->h_misc);
+  c->tr.reset();
+  delete c;
+  return BGS_OK;
+}
+
+const char* bgs_last_error(const bgs_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+int64_t bgs_launch_count(const bgs_ctx* c) { return c ? c->launches : -1; }
+
+bgs_status bgs_query(bgs_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return BGS_ERR_INVALID_ARGUMENT;
+  const int64_t v[BGS_Q_COUNT] = {ctx->n_local, ctx->n_lod, ctx->n_act, ctx->F, ctx->D, ctx->R, ctx->P,
+                                  ctx->t_begin, ctx->t_end, ctx->fallback, ctx->n_passes, ctx->P_all,
+                                  ctx->cam.W, ctx->cam.H};
+  std::memcpy(out, v, sizeof v);
+  return BGS_OK;
+}
+
+bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** ptr, int64_t* bytes) {
+  if (!ctx || !ptr || !bytes) return BGS_ERR_INVALID_ARGUMENT;
+  void* p = nullptr;
+  int64_t b = 0;
+  uint32_t sel = 0;
+  if (which == 3 || which == 4) {
+    if (ctx->stage < 3) return fail(ctx, BGS_ERR_CONTRACT, "sorted pairs requested before bgs_sort_tiles");
+    // final ping-pong buffer selector lives on the device
+    cudaError_t e = cudaMemcpy(&sel, P_<uint32_t>(ctx->pass_ctrl) + kFinalSel, 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "debug_buffer", cudaGetErrorString(e));
+  }
+  switch (which) {
+    case 0: p = ctx->recs.p; b = ctx->F * 48; break;
+    case 1: p = ctx->rec_lidx.p; b = ctx->F * 4; break;
+    case 2: p = ctx->world > 1 ? ctx->recvbuf.p : nullptr; b = ctx->world > 1 ? ctx->R * 48 : 0; break;
+    case 3: p = ctx->keys[sel].p; b = ctx->P * 8; break;
+    case 4: p = ctx->vals[sel].p; b = ctx->P * 4; break;
+    case 5: p = ctx->ranges.p; b = int64_t(ctx->t_end - ctx->t_begin) * 8; break;
+    case 6: p = ctx->acc.p; b = ctx->R * 48; break;
+    case 7: p = ctx->acc_local; b = ctx->F * 48; break;
+    case 8: p = ctx->owner.p; b = ctx->world > 1 ? int64_t(ctx->T) * 4 : 0; break;
+    case 9: p = ctx->dest_mask.p; b = ctx->world > 1 ? ctx->F : 0; break;
+    case 10: p = ctx->tile_pairs.p; b = ctx->world > 1 ? int64_t(ctx->T) * 4 : 0; break;
+    default: return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "unknown debug buffer");
+  }
+  *ptr = p;
+  *bytes = b;
+  return BGS_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// a1 + a2
+// ---------------------------------------------------------------------------------------
+bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                       const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  CKS(check_gaussians(ctx, g));
+  CKS(set_camera(ctx, cam));
+  if (g->n_local > 0 && !radius_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "radius_out is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ctx->stage = 0;
+  ctx->n_local = g->n_local;
+  ProjectArgs a{};
+  a.mean_opac = reinterpret_cast<const float4*>(g->mean_opac);
+  a.quat = reinterpret_cast<const float4*>(g->quat);
+  a.scale = reinterpret_cast<const float4*>(g->scale);
+  a.sh = g->sh;
+  a.lod = g->lod;
+  a.cull = cull_column;
+  a.n = g->n_local;
+  a.cam = ctx->cam;
+  a.gate_enabled = 0;
+  if (gate && gate->enabled) {
+    if (!(gate->d0 > 0)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "gate d0 must be > 0");
+    if (gate->fallback_den <= 0 || gate->fallback_num < 0)
+      return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "gate fallback ratio must be num >= 0, den > 0");
+    a.gate_enabled = 1;
+    a.l_max = gate->l_max;
+    a.fb_num = gate->fallback_num;
+    a.fb_den = gate->fallback_den;
+    // D2[l] = (d0 * 2^(1/2 - l))^2 in double, rounded to float (Eq.4 threshold form, R18)
+    for (int l = 0; l < 32; ++l) {
+      const double v = gate->d0 * std::ldexp(std::sqrt(2.0), -l);
+      a.D2[l] = static_cast<float>(v * v);
+    }
+  }
+  a.no_color = (flags & BGS_NO_COLOR) ? 1 : 0;
+  a.rank = ctx->rank;
+  a.world = ctx->world;
+  a.radius = radius_out;
+  CKS(ensure(ctx, ctx->recs, size_t(std::max<int64_t>(g->n_local, 1)) * sizeof(Rec)));
+  CKS(ensure(ctx, ctx->rec_lidx, size_t(std::max<int64_t>(g->n_local, 1)) * 4));
+  a.recs = P_<Rec>(ctx->recs);
+  a.rec_lidx = P_<uint32_t>(ctx->rec_lidx);
+  a.rec_cap = g->n_local;
+  a.counters = P_<unsigned long long>(ctx->counters);
+  CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_NCOUNTERS, s));
+  a.tile_diff = nullptr;
+  if (ctx->world > 1) {
+    const size_t nd = size_t(ctx->cam.TX + 1) * (ctx->cam.TY + 1);
+    CKS(ensure(ctx, ctx->tile_diff, nd * 4));
+    CK(cudaMemsetAsync(ctx->tile_diff.p, 0, nd * 4, s));
+    a.tile_diff = P_<int32_t>(ctx->tile_diff);
+  }
+  if (a.gate_enabled && a.n > 0) {
+    launch_gate_count(a, s);
+    CKS(launched(ctx));
+  }
+  if (a.n > 0) {
+    launch_project(a, s);
+    CKS(launched(ctx));
+  }
+  CK(cudaMemcpyAsync(ctx->h_counters, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->F = int64_t(ctx->h_counters[C_F]);
+  ctx->P_all = int64_t(ctx->h_counters[C_PALL]);
+  ctx->n_lod = a.gate_enabled ? int64_t(ctx->h_counters[C_NLOD]) : g->n_local;
+  ctx->n_act = int64_t(ctx->h_counters[C_NACT]);
+  ctx->fallback = a.gate_enabled ? int((unsigned long long)a.fb_den * ctx->h_counters[C_NLOD] >
+                                       (unsigned long long)a.fb_num * (unsigned long long)g->n_local)
+                                 : 1;
+  ctx->stage = 1;
+  return BGS_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// a3 + a4
+// ---------------------------------------------------------------------------------------
+bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (ctx->stage < 1) return fail(ctx, BGS_ERR_CONTRACT, "bgs_route before bgs_project");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int M = ctx->world;
+  if (M == 1) {
+    ctx->recv = P_<Rec>(ctx->recs);
+    ctx->R = ctx->F;
+    ctx->D = ctx->F;
+    ctx->t_begin = 0;
+    ctx->t_end = ctx->T;
+    ctx->P = ctx->P_all;
+    if (tile_owner_out) CK(cudaMemsetAsync(tile_owner_out, 0, size_t(ctx->T) * 4, s));
+    ctx->stage = 2;
+    return BGS_OK;
+  }
+  if (ctx->T > 16384) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "world > 1 supports at most 16384 tiles");
+  const int T = ctx->T;
+  // a3: per-tile pair counts -> all ranks -> owner map
+  CKS(ensure(ctx, ctx->tile_pairs, size_t(T) * 4));
+  CKS(ensure(ctx, ctx->owner, size_t(T) * 4));
+  CKS(ensure(ctx, ctx->runinfo, size_t(2 * M) * 4 + size_t(M) * 8 + 64));
+  launch_tile_costs(P_<int32_t>(ctx->tile_diff), ctx->cam.TX, ctx->cam.TY, P_<int32_t>(ctx->tile_pairs), s);
+  CKS(launched(ctx));
+  CKS(ctx->tr->allreduce_i32(ctx, P_<int32_t>(ctx->tile_pairs), T, s));
+  int32_t* run = P_<int32_t>(ctx->runinfo);
+  long long* pown = reinterpret_cast<long long*>(P_<char>(ctx->runinfo) + 64);
+  launch_owner_map(P_<int32_t>(ctx->tile_pairs), T, M, P_<int32_t>(ctx->owner), run, pown, s);
+  CKS(launched(ctx));
+  if (tile_owner_out) CK(cudaMemcpyAsync(tile_owner_out, ctx->owner.p, size_t(T) * 4, cudaMemcpyDeviceToDevice, s));
+  // a4: destination masks, per-destination counts, count exchange
+  const int64_t F = ctx->F;
+  const int64_t nb = std::max<int64_t>(1, (F + kRouteBlock - 1) / kRouteBlock);
+  CKS(ensure(ctx, ctx->dest_mask, size_t(std::max<int64_t>(F, 1))));
+  CKS(ensure(ctx, ctx->block_counts, size_t(nb) * M * 4));
+  CKS(ensure(ctx, ctx->totals, size_t(M) * 8));
+  CKS(ensure(ctx, ctx->xchg_counts, size_t(M) * 8));
+  CKS(ensure(ctx, ctx->send_base, size_t(M) * 8));
+  CK(cudaMemsetAsync(ctx->totals.p, 0, size_t(M) * 8, s));
+  if (F > 0) {
+    launch_dest_count(ctx->recs.p ? P_<Rec>(ctx->recs) : nullptr, F, P_<int32_t>(ctx->owner), ctx->cam.TX, M,
+                      P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), s);
+    CKS(launched(ctx));
+    launch_block_scan(P_<uint32_t>(ctx->block_counts), nb, M, P_<unsigned long long>(ctx->totals), s);
+    CKS(launched(ctx));
+  }
+  CKS(ctx->tr->alltoall1(ctx, P_<int64_t>(ctx->totals), P_<int64_t>(ctx->xchg_counts), s));
+  int64_t* h = ctx->h_misc;  // [0,M) send, [M,2M) recv, [2M,4M) run, [4M,5M) pown
+  CK(cudaMemcpyAsync(h, ctx->totals.p, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + M, ctx->xchg_counts.p, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + 2 * M, run, size_t(2 * M) * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + 4 * M, pown, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->send_cnt.assign(h, h + M);
+  ctx->recv_cnt.assign(h + M, h + 2 * M);
+  const int32_t* hrun = reinterpret_cast<const int32_t*>(h + 2 * M);
+  ctx->t_begin = hrun[2 * ctx->rank];
+  ctx->t_end = hrun[2 * ctx->rank + 1];
+  ctx->P = h[4 * M + ctx->rank];
+  ctx->send_off.assign(M, 0);
+  ctx->recv_off.assign(M, 0);
+  int64_t D = 0, R = 0;
+  for (int d = 0; d < M; ++d) {
+    ctx->send_off[d] = D;
+    ctx->recv_off[d] = R;
+    D += ctx->send_cnt[d];
+    R += ctx->recv_cnt[d];
+  }
+  ctx->D = D;
+  ctx->R = R;
+  CKS(ensure(ctx, ctx->send, size_t(std::max<int64_t>(D, 1)) * sizeof(Rec)));
+  CKS(ensure(ctx, ctx->recvbuf, size_t(std::max<int64_t>(R, 1)) * sizeof(Rec)));
+  CK(cudaMemcpyAsync(ctx->send_base.p, ctx->send_off.data(), size_t(M) * 8, cudaMemcpyHostToDevice, s));
+  if (F > 0) {
+    launch_pack(P_<Rec>(ctx->recs), F, P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), M,
+                P_<int64_t>(ctx->send_base), P_<Rec>(ctx->send), s);
+    CKS(launched(ctx));
+  }
+  CKS(ctx->tr->alltoallv(ctx, ctx->send.p, ctx->send_cnt.data(), ctx->send_off.data(), ctx->recvbuf.p,
+                         ctx->recv_cnt.data(), ctx->recv_off.data(), sizeof(Rec), s));
+  ctx->recv = P_<Rec>(ctx->recvbuf);
+  ctx->stage = 2;
+  return BGS_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// a5 + a6 + a7
+// ---------------------------------------------------------------------------------------
+bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (ctx->stage < 2) return fail(ctx, BGS_ERR_CONTRACT, "bgs_sort_tiles before bgs_route");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t P = ctx->P;
+  if (P >= (int64_t(1) << 30)) return fail(ctx, BGS_ERR_CAPACITY, "more than 2^30 pairs in one view");
+  const int nt = ctx->t_end - ctx->t_begin;
+  int tbits = 0;
+  while ((1 << tbits) < std::max(nt, 1)) ++tbits;
+  ctx->n_passes = (31 + tbits + 7) / 8;
+  SortArgs a{};
+  a.recv = ctx->recv;
+  a.n_recv = ctx->R;
+  a.TX = ctx->cam.TX;
+  a.t_begin = ctx->t_begin;
+  a.t_end = ctx->t_end;
+  for (int b = 0; b < 2; ++b) {
+    CKS(ensure(ctx, ctx->keys[b], size_t(std::max<int64_t>(P, 1)) * 8));
+    CKS(ensure(ctx, ctx->vals[b], size_t(std::max<int64_t>(P, 1)) * 4));
+    a.keys[b] = P_<unsigned long long>(ctx->keys[b]);
+    a.vals[b] = P_<uint32_t>(ctx->vals[b]);
+  }
+  a.cap = P;
+  a.counters = P_<unsigned long long>(ctx->counters);
+  CKS(ensure(ctx, ctx->digit_hist, kMaxSortPasses * 256 * 4));
+  CKS(ensure(ctx, ctx->pass_ctrl, 64 * 4));
+  const int64_t n_parts = std::max<int64_t>(1, (P + kSortPart - 1) / kSortPart);
+  CKS(ensure(ctx, ctx->status, size_t(n_parts) * 256 * 4 * ctx->n_passes));
+  CKS(ensure(ctx, ctx->ranges, size_t(std::max(nt, 1)) * 8));
+  a.digit_hist = P_<uint32_t>(ctx->digit_hist);
+  a.pass_ctrl = P_<uint32_t>(ctx->pass_ctrl);
+  a.status = P_<uint32_t>(ctx->status);
+  a.n_passes = ctx->n_passes;
+  a.ranges = P_<uint2>(ctx->ranges);
+  CK(cudaMemsetAsync(ctx->digit_hist.p, 0, kMaxSortPasses * 256 * 4, s));
+  CK(cudaMemsetAsync(ctx->pass_ctrl.p, 0, 64 * 4, s));
+  CK(cudaMemsetAsync(P_<unsigned long long>(ctx->counters) + C_P, 0, 8, s));
+  CK(cudaMemsetAsync(ctx->status.p, 0, size_t(n_parts) * 256 * 4 * ctx->n_passes, s));
+  CK(cudaMemsetAsync(ctx->ranges.p, 0, size_t(std::max(nt, 1)) * 8, s));
+  if (ctx->R > 0) {
+    launch_emit(a, s);
+    CKS(launched(ctx));
+  }
+  int64_t nl = 0;
+  launch_sort_passes(a, P, s, &nl);
+  CKS(launched(ctx, int(nl)));
+  if (P > 0) {
+    launch_ranges_fixup(a, P, s);
+    CKS(launched(ctx));
+  }
+  ctx->stage = 3;
+  return BGS_OK;
+}
+
+static RasterArgs raster_args(bgs_ctx* ctx) {
+  RasterArgs a{};
+  a.recv = ctx->recv;
+  a.ranges = P_<uint2>(ctx->ranges);
+  for (int b = 0; b < 2; ++b) {
+    a.keys[b] = P_<unsigned long long>(ctx->keys[b]);
+    a.vals[b] = P_<uint32_t>(ctx->vals[b]);
+  }
+  a.pass_ctrl = P_<uint32_t>(ctx->pass_ctrl);
+  a.t_begin = ctx->t_begin;
+  a.n_tiles = ctx->t_end - ctx->t_begin;
+  a.TX = ctx->cam.TX;
+  a.W = ctx->cam.W;
+  a.H = ctx->cam.H;
+  a.acc = P_<Acc>(ctx->acc);
+  return a;
+}
+
+bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
+                          void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (ctx->stage < 3) return fail(ctx, BGS_ERR_CONTRACT, "bgs_raster_fwd before bgs_sort_tiles");
+  if (!rgb || !t_final || !n_contrib) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "output image pointer is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CKS(ensure(ctx, ctx->acc, size_t(std::max<int64_t>(ctx->R, 1)) * sizeof(Acc)));
+  CK(cudaMemsetAsync(ctx->acc.p, 0, size_t(std::max<int64_t>(ctx->R, 1)) * sizeof(Acc), s));
+  const RasterArgs a = raster_args(ctx);
+  if (a.n_tiles > 0) {
+    launch_raster_fwd(a, flags, rgb, t_final, n_contrib, s);
+    CKS(launched(ctx));
+  }
+  ctx->stage = 4;
+  return BGS_OK;
+}
+
+bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL, const float* t_final, const int32_t* n_contrib,
+                          void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_raster_bwd before bgs_raster_fwd");
+  if (!dL || !t_final || !n_contrib) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "image pointer is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const RasterArgs a = raster_args(ctx);
+  if (a.n_tiles > 0) {
+    launch_raster_bwd(a, dL, t_final, n_contrib, s);
+    CKS(launched(ctx));
+  }
+  ctx->stage = 5;
+  return BGS_OK;
+}
+
+bgs_status bgs_route_reverse(bgs_ctx* ctx, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_route_reverse before bgs_raster_fwd");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int M = ctx->world;
+  if (M == 1) {
+    ctx->acc_local = P_<Acc>(ctx->acc);
+    ctx->stage = 6;
+    return BGS_OK;
+  }
+  CKS(ensure(ctx, ctx->rev, size_t(std::max<int64_t>(ctx->D, 1)) * sizeof(Acc)));
+  CKS(ensure(ctx, ctx->accl, size_t(std::max<int64_t>(ctx->F, 1)) * sizeof(Acc)));
+  // transposed counts: what I received from k goes back to k; what I sent to d comes back from d
+  CKS(ctx->tr->alltoallv(ctx, ctx->acc.p, ctx->recv_cnt.data(), ctx->recv_off.data(), ctx->rev.p,
+                         ctx->send_cnt.data(), ctx->send_off.data(), sizeof(Acc), s));
+  if (ctx->F > 0) {
+    launch_gather_sum(P_<Acc>(ctx->rev), ctx->F, P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), M,
+                      P_<int64_t>(ctx->send_base), P_<Acc>(ctx->accl), s);
+    CKS(launched(ctx));
+  }
+  ctx->acc_local = P_<Acc>(ctx->accl);
+  ctx->stage = 6;
+  return BGS_OK;
+}
+
+bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                           const bgs_gaussian_grads* grads, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  CKS(check_gaussians(ctx, g));
+  if (ctx->stage < 6) return fail(ctx, BGS_ERR_CONTRACT, "bgs_project_bwd before bgs_route_reverse");
+  if (g->n_local != ctx->n_local) return fail(ctx, BGS_ERR_CONTRACT, "n_local differs from bgs_project's");
+  if (!grads || !grads->mean_opac || !grads->quat || !grads->scale || !grads->sh)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "gradient pointer is NULL");
+  if (!cam) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "camera is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ProjectBwdArgs a{};
+  a.mean_opac = reinterpret_cast<const float4*>(g->mean_opac);
+  a.quat = reinterpret_cast<const float4*>(g->quat);
+  a.scale = reinterpret_cast<const float4*>(g->scale);
+  a.sh = g->sh;
+  a.rec_lidx = P_<uint32_t>(ctx->rec_lidx);
+  a.acc = ctx->acc_local;
+  a.F = ctx->F;
+  a.cam = ctx->cam;
+  a.g_mean_opac = reinterpret_cast<float4*>(grads->mean_opac);
+  a.g_quat = reinterpret_cast<float4*>(grads->quat);
+  a.g_scale = reinterpret_cast<float4*>(grads->scale);
+  a.g_sh = grads->sh;
+  if (a.F > 0) {
+    launch_project_bwd(a, s);
+    CKS(launched(ctx));
+  }
+  return BGS_OK;
+}
+
+bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, const uint64_t* w_fixed,
+                          const uint32_t* a_in, int32_t mass_num, int32_t mass_den, double* s_out, uint32_t* c_rad,
+                          uint32_t* c_vis, uint32_t* cull_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (n_local < 0 || !s_out || !c_rad || !c_vis || !cull_out)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "importance outputs must be non-NULL");
+  if (mass_den <= 0 || mass_num < 0 || mass_num > mass_den)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "mass fraction must satisfy 0 <= num <= den, den > 0");
+  const bool dense = w_fixed != nullptr;
+  if (dense && (!a_in || !radius)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "dense w_fixed needs a and radius");
+  if (!dense && ctx->stage < 6) return fail(ctx, BGS_ERR_CONTRACT, "bgs_importance before bgs_route_reverse");
+  if (!dense && n_local != ctx->n_local) return fail(ctx, BGS_ERR_CONTRACT, "stale n_local (S:384)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ImportanceArgs a{};
+  a.n_items = dense ? n_local : ctx->F;
+  a.item_lidx = dense ? nullptr : P_<uint32_t>(ctx->rec_lidx);
+  a.radius = radius;
+  a.w_dense = reinterpret_cast<const unsigned long long*>(w_fixed);
+  a.a_dense = a_in;
+  a.acc = ctx->acc_local;
+  a.n_local = n_local;
+  a.rank = ctx->rank;
+  a.world = ctx->world;
+  a.s = s_out;
+  a.c_rad = c_rad;
+  a.c_vis = c_vis;
+  a.cull = cull_out;
+  const int WR = imp_w_rounds(), GR = imp_g_rounds();
+  CKS(ensure(ctx, ctx->imp_state, kImpStateBytes));
+  CKS(ensure(ctx, ctx->imp_total, 16));
+  CKS(ensure(ctx, ctx->imp_hist, size_t(WR * 512 + GR * 256) * 8));
+  CK(cudaMemsetAsync(ctx->imp_state.p, 0, kImpStateBytes, s));
+  CK(cudaMemsetAsync(ctx->imp_total.p, 0, 16, s));
+  CK(cudaMemsetAsync(ctx->imp_hist.p, 0, size_t(WR * 512 + GR * 256) * 8, s));
+  ImpState* st = static_cast<ImpState*>(ctx->imp_state.p);
+  unsigned long long* total = P_<unsigned long long>(ctx->imp_total);
+  unsigned long long* hist = P_<unsigned long long>(ctx->imp_hist);
+  int nl = 0;
+  launch_fill_bits(cull_out, n_local, s);
+  ++nl;
+  launch_imp_stats(a, total, s);
+  ++nl;
+  if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, total, 1, s));
+  for (int r = 0; r < WR; ++r) {
+    launch_imp_hist(a, st, r, hist + r * 512, s);
+    if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, hist + r * 512, 512, s));
+    launch_imp_decide(st, total, r, hist + r * 512, mass_num, mass_den, s);
+    nl += 2;
+  }
+  for (int r = 0; r < GR; ++r) {
+    launch_imp_gid_hist(a, st, r, hist + WR * 512 + r * 256, s);
+    if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, hist + WR * 512 + r * 256, 256, s));
+    launch_imp_gid_decide(st, r, hist + WR * 512 + r * 256, s);
+    nl += 2;
+  }
+  launch_imp_mark(a, st, s);
+  ++nl;
+  CKS(launched(ctx, nl));
+  return BGS_OK;
+}
+
+bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                         const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, float* rgb,
+                         float* t_final, int32_t* n_contrib, const float* dL, const bgs_gaussian_grads* grads,
+                         const bgs_importance_out* imp, void* stream) {
+  if (imp) flags |= BGS_IMPORTANCE;
+  CKS(bgs_project(ctx, g, cam, gate, cull_column, flags, radius_out, stream));
+  CKS(bgs_route(ctx, nullptr, stream));
+  CKS(bgs_sort_tiles(ctx, stream));
+  CKS(bgs_raster_fwd(ctx, flags, rgb, t_final, n_contrib, stream));
+  if (dL) CKS(bgs_raster_bwd(ctx, dL, t_final, n_contrib, stream));
+  CKS(bgs_route_reverse(ctx, stream));
+  if (dL && grads) CKS(bgs_project_bwd(ctx, g, cam, grads, stream));
+  if (imp)
+    CKS(bgs_importance(ctx, g->n_local, radius_out, nullptr, nullptr, imp->mass_num, imp->mass_den, imp->s,
+                       imp->c_rad, imp->c_vis, imp->cull_out, stream));
+  return BGS_OK;
+}
+
+bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                              const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                              int32_t* radius_out, const float* dL_host, float* rgb_host,
+                              const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  CKS(set_camera(ctx, cam));
+  if (!dL_host || !rgb_host) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "host image pointer is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t npix = size_t(ctx->cam.W) * ctx->cam.H;
+  CKS(ensure(ctx, ctx->scr_rgb, npix * 12));
+  CKS(ensure(ctx, ctx->scr_dl, npix * 12));
+  CKS(ensure(ctx, ctx->scr_t, npix * 4));
+  CKS(ensure(ctx, ctx->scr_n, npix * 4));
+  CK(cudaMemcpyAsync(ctx->scr_dl.p, dL_host, npix * 12, cudaMemcpyHostToDevice, s));
+  CKS(bgs_view_step(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
+                    P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), P_<float>(ctx->scr_dl), grads, imp, stream));
+  CK(cudaMemcpyAsync(rgb_host, ctx->scr_rgb.p, npix * 12, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return BGS_OK;
+}
+
+}  // extern "C"

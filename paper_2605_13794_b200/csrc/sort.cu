@@ -1,0 +1,336 @@
+// a5 pair emission, a6 onesweep LSD radix sort, a7 tile ranges (bgs_sort_tiles).
+//
+// PAPER.md P:152 ("rasterized by tile-based front-to-back alpha compositing"), Eq.2
+// (N(p) depth-ordered), SPEC S:116 / S:172 (ties by global id, reading R12).
+//
+// Key = (local tile << 31) | f32 bits(depth).  depth > near_clip > 0, so bit 31 of the float
+// is 0 and the unsigned order of the bits is the numeric order of the depths.
+//
+// a5: one warp expands the rects of 32 received records cooperatively (slot = position in a
+//     rect, warp-scan + 5-step shuffle search for the owning lane), keeps the slots whose tile
+//     is owned, compacts them with a ballot and writes them coalesced after ONE atomicAdd per
+//     warp (warp-aggregated atomics, north_star).  The same kernel builds the 8-bit digit
+//     histograms of every pass (the "upfront" histogram of onesweep) in shared memory.
+// a6: per pass, a CTA takes the next partition of 4096 keys (dynamic partition id so the
+//     look-back always waits on CTAs that already run), ranks keys inside each warp with
+//     __match_any_sync, publishes its per-digit counts with decoupled look-back (flag in
+//     bits 31:30 of one 32-bit word: 1 = aggregate, 2 = inclusive prefix), reorders the
+//     partition in shared memory and writes each digit run contiguously.  Passes whose digit
+//     is the same for every key are skipped on the device (no host round trip): a tiny scan
+//     kernel writes per-pass active flags and ping-pong selectors.
+// a7: one pass over the sorted keys writes [start, end) per tile and re-orders runs of
+//     identical (tile, depth) keys by global id (insertion sort; runs are tiny).
+#include "bgs_internal.cuh"
+
+namespace bgs {
+namespace {
+
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagInc = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1u;
+// pass_ctrl layout
+constexpr int kCtrlActive = 0;   // [8]
+constexpr int kCtrlSel = 8;      // [7] input buffer of pass p
+constexpr int kCtrlPart = 16;    // [8] partition counters
+
+__device__ __forceinline__ unsigned long long make_key(uint32_t lt, float depth) {
+  return (static_cast<unsigned long long>(lt) << 31) | static_cast<unsigned long long>(__float_as_uint(depth));
+}
+
+__global__ void __launch_bounds__(256) k_emit(SortArgs a) {
+  __shared__ uint32_t s_hist[kMaxSortPasses][256];
+  for (int j = threadIdx.x; j < kMaxSortPasses * 256; j += blockDim.x) (&s_hist[0][0])[j] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t rect = 0, area = 0, own = 0, dbits = 0;
+  if (r < a.n_recv) {
+    const uint4 q2 = __ldg(reinterpret_cast<const uint4*>(a.recv + r) + 2);  // (b, depth, gid, rect)
+    rect = q2.w;
+    dbits = q2.y;
+    const int x0 = rect & 255, y0 = (rect >> 8) & 255, x1 = (rect >> 16) & 255, y1 = rect >> 24;
+    area = uint32_t((x1 - x0) * (y1 - y0));
+    // owned count: rows of the rect intersected with the contiguous run [t_begin, t_end)
+    for (int y = y0; y < y1; ++y) {
+      const int lo = max(y * a.TX + x0, a.t_begin), hi = min(y * a.TX + x1, a.t_end);
+      own += hi > lo ? uint32_t(hi - lo) : 0u;
+    }
+  }
+  // warp inclusive scans of area and own
+  uint32_t incl = area, oincl = own;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    const uint32_t w = __shfl_up_sync(0xffffffffu, oincl, o);
+    if (lane >= o) {
+      incl += v;
+      oincl += w;
+    }
+  }
+  const uint32_t total_area = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t total_own = __shfl_sync(0xffffffffu, oincl, 31);
+  unsigned long long base = 0;
+  if (lane == 0 && total_own) base = atomicAdd(a.counters + C_P, (unsigned long long)total_own);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const int npass = a.n_passes;
+  uint32_t run = 0;
+  for (uint32_t chunk = 0; chunk < total_area; chunk += 32) {
+    const uint32_t slot = chunk + lane;
+    bool ok = false;
+    unsigned long long key = 0;
+    uint32_t val = 0;
+    // smallest lane j with incl[j] > slot
+    int j = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const uint32_t v = __shfl_sync(0xffffffffu, incl, j + step - 1);
+      if (v <= slot) j += step;
+    }
+    j = min(j, 31);
+    const uint32_t rj = __shfl_sync(0xffffffffu, rect, j);
+    const uint32_t dj = __shfl_sync(0xffffffffu, dbits, j);
+    const uint32_t ij = __shfl_sync(0xffffffffu, incl, j);
+    const uint32_t aj = __shfl_sync(0xffffffffu, area, j);
+    if (slot < total_area) {
+      const uint32_t k = slot - (ij - aj);
+      const int x0 = rj & 255, y0 = (rj >> 8) & 255, x1 = (rj >> 16) & 255;
+      const int w = x1 - x0;
+      const int t = (y0 + int(k) / w) * a.TX + x0 + int(k) % w;
+      if (t >= a.t_begin && t < a.t_end) {
+        ok = true;
+        key = make_key(uint32_t(t - a.t_begin), __uint_as_float(dj));
+        val = uint32_t(int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31) + j);
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      const unsigned long long pos = base + run + __popc(m & ((1u << lane) - 1u));
+      if ((int64_t)pos < a.cap) {
+        a.keys[0][pos] = key;
+        a.vals[0][pos] = val;
+      }
+      for (int p = 0; p < npass; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
+    }
+    run += __popc(m);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < npass * 256; j += blockDim.x) {
+    const uint32_t c = (&s_hist[0][0])[j];
+    if (c) atomicAdd(a.digit_hist + j, c);
+  }
+}
+
+// One CTA: per pass, detect constant digits (inactive pass), exclusive-scan the digit
+// histogram in place, and assign ping-pong input selectors.
+__global__ void __launch_bounds__(256) k_digit_scan(SortArgs a) {
+  __shared__ uint32_t s_scan[256];
+  __shared__ int s_trivial;
+  const unsigned long long P = a.counters[C_P];
+  uint32_t sel = 0;
+  for (int p = 0; p < a.n_passes; ++p) {
+    const uint32_t c = a.digit_hist[p * 256 + threadIdx.x];
+    if (threadIdx.x == 0) s_trivial = 0;
+    __syncthreads();
+    if ((unsigned long long)c == P) s_trivial = 1;  // all keys share this digit (also P == 0)
+    s_scan[threadIdx.x] = c;
+    __syncthreads();
+    // Hillis-Steele inclusive scan over 256
+    for (int o = 1; o < 256; o <<= 1) {
+      const uint32_t v = threadIdx.x >= o ? s_scan[threadIdx.x - o] : 0u;
+      __syncthreads();
+      s_scan[threadIdx.x] += v;
+      __syncthreads();
+    }
+    a.digit_hist[p * 256 + threadIdx.x] = s_scan[threadIdx.x] - c;  // exclusive
+    const int active = !s_trivial;
+    if (threadIdx.x == 0) {
+      a.pass_ctrl[kCtrlActive + p] = uint32_t(active);
+      a.pass_ctrl[kCtrlSel + p] = sel;
+    }
+    if (active) sel ^= 1u;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.pass_ctrl[kFinalSel] = sel;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int pass, int n_parts) {
+  constexpr int NT = NW * 32;
+  constexpr int PART = NT * kSortItems;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem_raw);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + PART);
+  __shared__ uint32_t s_whist[NW][256];
+  __shared__ uint32_t s_bstart[256];
+  __shared__ uint32_t s_gstart[256];
+  __shared__ int s_part;
+
+  if (a.pass_ctrl[kCtrlActive + pass] == 0) return;
+  const uint32_t sel = a.pass_ctrl[kCtrlSel + pass];
+  const unsigned long long* __restrict__ kin = a.keys[sel];
+  const uint32_t* __restrict__ vin = a.vals[sel];
+  unsigned long long* __restrict__ kout = a.keys[sel ^ 1u];
+  uint32_t* __restrict__ vout = a.vals[sel ^ 1u];
+  const int shift = 8 * pass;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+  if (tid == 0) s_part = int(atomicAdd(a.pass_ctrl + kCtrlPart + pass, 1u));
+  for (int j = tid; j < NW * 256; j += NT) (&s_whist[0][0])[j] = 0;
+  __syncthreads();
+  const int part = s_part;
+  const int64_t base = int64_t(part) * PART;
+  const int64_t wbase = base + int64_t(w) * (32 * kSortItems);
+
+  unsigned long long key[kSortItems];
+  uint32_t val[kSortItems];
+  uint32_t rank[kSortItems];
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    if (idx < P) {
+      key[i] = kin[idx];
+      val[i] = vin[idx];
+    } else {
+      key[i] = ~0ull;
+      val[i] = 0;
+    }
+  }
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    const bool valid = idx < P;
+    const uint32_t d = valid ? uint32_t((key[i] >> shift) & 255u) : 256u + lane;  // invalid: unique
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    uint32_t prev = 0;
+    if (valid) prev = s_whist[w][d];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) s_whist[w][d] = prev + __popc(peers);
+    __syncwarp();
+    rank[i] = prev + __popc(peers & lt);
+  }
+  __syncthreads();
+  // per digit: exclusive offsets across warps, block count
+  const int d = tid;  // NT == 256
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int ww = 0; ww < NW; ++ww) {
+    const uint32_t c = s_whist[ww][d];
+    s_whist[ww][d] = cnt;
+    cnt += c;
+  }
+  // decoupled look-back over partitions for digit d
+  uint32_t* st = a.status + (size_t(pass) * n_parts) * 256;
+  volatile uint32_t* my = st + size_t(part) * 256 + d;
+  uint32_t excl = 0;
+  if (part == 0) {
+    *my = kFlagInc | cnt;
+  } else {
+    *my = kFlagAgg | cnt;
+    int j = part - 1;
+    while (true) {
+      const uint32_t s = *(volatile uint32_t*)(st + size_t(j) * 256 + d);
+      const uint32_t f = s & ~kValMask;
+      if (f == 0) continue;
+      excl += s & kValMask;
+      if (f == kFlagInc) break;
+      --j;
+    }
+    *my = kFlagInc | (excl + cnt);
+  }
+  // block-local exclusive scan of cnt over digits (256 threads)
+  s_bstart[d] = cnt;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const uint32_t v = d >= o ? s_bstart[d - o] : 0u;
+    __syncthreads();
+    s_bstart[d] += v;
+    __syncthreads();
+  }
+  const uint32_t bstart = s_bstart[d] - cnt;
+  __syncthreads();
+  s_bstart[d] = bstart;
+  s_gstart[d] = a.digit_hist[pass * 256 + d] + excl;
+  __syncthreads();
+  // local reorder in shared memory (stable: warp-major, then item, then lane == input order)
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    const int64_t idx = wbase + i * 32 + lane;
+    if (idx < P) {
+      const uint32_t dd = uint32_t((key[i] >> shift) & 255u);
+      const uint32_t pos = s_bstart[dd] + s_whist[w][dd] + rank[i];
+      s_keys[pos] = key[i];
+      s_vals[pos] = val[i];
+    }
+  }
+  __syncthreads();
+  const int nvalid = int(P - base < int64_t(PART) ? P - base : int64_t(PART));
+  for (int j = tid; j < nvalid; j += NT) {
+    const unsigned long long k = s_keys[j];
+    const uint32_t dd = uint32_t((k >> shift) & 255u);
+    const uint32_t o = s_gstart[dd] + (uint32_t(j) - s_bstart[dd]);
+    kout[o] = k;
+    vout[o] = s_vals[j];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const uint32_t sel = a.pass_ctrl[kFinalSel];
+  const unsigned long long* keys = a.keys[sel];
+  uint32_t* vals = a.vals[sel];
+  const unsigned long long k = keys[i];
+  const uint32_t t = uint32_t(k >> 31);
+  const unsigned long long kp = i > 0 ? keys[i - 1] : ~0ull;
+  const unsigned long long kn = i + 1 < P ? keys[i + 1] : ~0ull;
+  if (i == 0 || uint32_t(kp >> 31) != t) a.ranges[t].x = uint32_t(i);
+  if (i + 1 == P || uint32_t(kn >> 31) != t) a.ranges[t].y = uint32_t(i + 1);
+  if (kn == k && kp != k) {
+    // run of identical (tile, depth) keys starting at i: order by global id (R12)
+    int64_t e = i + 1;
+    while (e + 1 < P && keys[e + 1] == k) ++e;
+    for (int64_t x = i + 1; x <= e; ++x) {
+      const uint32_t v = vals[x];
+      const uint32_t g = a.recv[v].gid;
+      int64_t y = x - 1;
+      while (y >= i && a.recv[vals[y]].gid > g) {
+        vals[y + 1] = vals[y];
+        --y;
+      }
+      vals[y + 1] = v;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_emit(const SortArgs& a, cudaStream_t s) {
+  if (a.n_recv <= 0) return;
+  const int64_t blocks = (a.n_recv + 255) / 256;
+  k_emit<<<unsigned(blocks), 256, 0, s>>>(a);
+}
+
+void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches) {
+  k_digit_scan<<<1, 256, 0, s>>>(a);
+  ++*launches;
+  if (P <= 0) return;
+  const int n_parts = int((P + kSortPart - 1) / kSortPart);
+  const size_t smem = size_t(kSortPart) * (sizeof(unsigned long long) + sizeof(uint32_t));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_onesweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr_set = true;
+  }
+  for (int p = 0; p < a.n_passes; ++p) {
+    k_onesweep<8><<<n_parts, 256, smem, s>>>(a, P, p, n_parts);
+    ++*launches;
+  }
+}
+
+void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s) {
+  if (P <= 0) return;
+  k_ranges_fixup<<<unsigned((P + 255) / 256), 256, 0, s>>>(a, P);
+}
+
+}  // namespace bgs

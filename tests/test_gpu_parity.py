@@ -1,0 +1,263 @@
+"""CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bit-exact: radius, rect, tile ids, per-tile pair counts, sort order, ranges, routing, gate and
+cull decisions, record floats (pinned arithmetic), a and n_contrib (except attributed early-stop
+flips), c_rad, and c_vis / Cull given identical w_fixed.  Pixels |d| <= 1e-4.  Gradients
+|d| <= 1e-3 |g| + 1e-5 max|g| per parameter group.  w_fixed within one fixed-point unit per
+contributing pixel + 1e-5 relative.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle as O  # noqa: E402
+import synthetic as S  # noqa: E402
+from gpu_helpers import GpuStep  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+ET_MARGIN = 1e-4  # relative distance of T(1-alpha) to 1e-4 below which an early-stop flip is excused
+
+
+def _f32(x):
+    return np.asarray(x, np.float64).astype(np.float32)
+
+
+def _flip_info(st, gs, cam):
+    """Pixels whose early-stop decision may legitimately differ (exp rounding), and the gids
+    whose a / w / gradients they can affect (every splat of that pixel's list up to max nc)."""
+    H, W = cam["H"], cam["W"]
+    margin = st.get("et_margin").reshape(H, W)
+    nc_o = st.get("n_contrib").reshape(H, W)
+    cand = margin < ET_MARGIN
+    diff = (nc_o != gs.nc)
+    flips = diff & cand
+    affected = set()
+    TX = (W + 15) // 16
+    ys, xs = np.nonzero(cand)
+    tiles = st.get("pair_tile", 0)
+    gids = st.get("pair_gid", 0)
+    lo, hi = st.get("range_lo", 0), st.get("range_hi", 0)
+    for y, x in zip(ys, xs):
+        t = (y // 16) * TX + x // 16
+        upto = max(nc_o[y, x], gs.nc[y, x]) + 1
+        affected.update(gids[lo[t]:min(hi[t], lo[t] + upto)].tolist())
+    return cand, flips, affected
+
+
+@pytest.fixture(scope="module")
+def tiny_run(tiny_scene):
+    cam = tiny_scene.cameras[0]
+    dl = S.grad_image(cam["H"], cam["W"])
+    st = O.OracleStep(tiny_scene, cam, M=1, dLdC=dl)
+    gs = GpuStep(tiny_scene, cam, M=1, dLdC=dl)
+    yield tiny_scene, cam, dl, st, gs
+    gs.close()
+
+
+def test_project_bit_exact(tiny_run):
+    sc, cam, dl, st, gs = tiny_run
+    assert np.array_equal(gs.radius, st.get("radius"))
+    rec = gs.rank[0]["records"]
+    order = np.argsort(rec["gid"])
+    gid = rec["gid"][order]
+    valid = np.nonzero(st.get("radius") > 0)[0]
+    assert np.array_equal(gid, valid)
+    m2 = st.get("mean2d").reshape(-1, 2)[valid]
+    con = st.get("conic").reshape(-1, 3)[valid]
+    for name, ref in (("mx", m2[:, 0]), ("my", m2[:, 1]), ("A", con[:, 0]), ("B", con[:, 1]), ("C", con[:, 2]),
+                      ("depth", st.get("depth")[valid])):
+        assert np.array_equal(rec[name][order].view(np.uint32), _f32(ref).view(np.uint32)), name
+    assert np.array_equal(rec["rgb"][order].view(np.uint32), _f32(st.get("rgb").reshape(-1, 3)[valid]).view(np.uint32))
+    assert np.array_equal(rec["rect"][order], st.get("rect").reshape(-1, 4)[valid])
+    q = gs.rank[0]["q_project"]
+    assert q["F"] == len(valid) and q["P_all"] == st.get("n_pairs_total")[0]
+
+
+def test_sort_and_ranges_bit_exact(tiny_run):
+    sc, cam, dl, st, gs = tiny_run
+    o = gs.rank[0]
+    keys, vals = o["keys"], o["vals"]
+    tiles = (keys >> np.uint64(31)).astype(np.int32)
+    dbits = (keys & np.uint64(0x7FFFFFFF)).astype(np.uint32)
+    gid = o["recv"]["gid"][vals]
+    assert np.array_equal(tiles, st.get("pair_tile", 0))
+    assert np.array_equal(gid, st.get("pair_gid", 0))
+    assert np.array_equal(dbits, _f32(st.get("depth")[gid]).view(np.uint32))
+    assert np.array_equal(o["ranges"][:, 0], st.get("range_lo", 0))
+    assert np.array_equal(o["ranges"][:, 1], st.get("range_hi", 0))
+
+
+def test_raster_fwd_parity(tiny_run):
+    sc, cam, dl, st, gs = tiny_run
+    H, W = cam["H"], cam["W"]
+    cand, flips, affected = _flip_info(st, gs, cam)
+    img = st.get("img").reshape(3, H, W)
+    T = st.get("t_final").reshape(H, W)
+    ok = ~flips
+    assert np.abs(gs.img - img)[:, ok].max() <= 1e-4
+    assert np.abs(gs.T - T)[ok].max() <= 1e-5
+    assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
+    a_o, w_o = st.get("a"), st.get("w_fixed")
+    mism = np.nonzero(gs.a != a_o)[0]
+    assert set(mism.tolist()) <= affected, (len(mism), flips.sum())
+    keep = np.ones(sc.n, bool)
+    keep[list(affected)] = False
+    dw = np.abs(gs.w.astype(np.float64) - w_o.astype(np.float64))
+    assert np.all(dw[keep] <= a_o[keep] + 1e-5 * w_o[keep].astype(np.float64))
+    print(f"flip candidates {cand.sum()}, flips {flips.sum()}, affected splats {len(affected)}")
+
+
+def test_backward_parity(tiny_run):
+    sc, cam, dl, st, gs = tiny_run
+    _, _, affected = _flip_info(st, gs, cam)
+    keep = np.ones(sc.n, bool)
+    keep[list(affected)] = False
+    g_ref = st.get("g2d").reshape(-1, 9)
+    for k in range(9):
+        ref, got = g_ref[keep, k], gs.g2d[keep, k]
+        tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
+        assert np.all(np.abs(got - ref) <= tol), k
+    for name, width in (("d_mean", 3), ("d_quat", 4), ("d_scale", 3), ("d_opac", 1), ("d_sh", 48)):
+        ref = st.get(name).reshape(sc.n, width)[keep]
+        got = gs.grads[name].reshape(sc.n, width)[keep]
+        tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
+        bad = np.abs(got - ref) > tol
+        assert not bad.any(), (name, int(bad.sum()), float(np.max(np.abs(got - ref) / (np.abs(ref) + 1e-30))))
+
+
+def test_importance_parity(tiny_run):
+    sc, cam, dl, st, gs = tiny_run
+    # same w_fixed -> bit-exact selection; s is the same fp64 expression
+    ref = O.importance(gs.radius, gs.w, gs.a)
+    assert np.array_equal(gs.c_rad, ref["c_rad"])
+    assert np.array_equal(gs.c_vis, ref["c_vis"])
+    assert np.array_equal(gs.cull_bits, S.unpack_bits(ref["cull"], sc.n))
+    np.testing.assert_allclose(gs.s, ref["s"], rtol=1e-12, atol=0)
+    # against the oracle's own w: s within the fixed-point bound
+    ref2 = O.importance(st.get("radius"), st.get("w_fixed"), st.get("a"))
+    _, _, affected = _flip_info(st, gs, cam)
+    keep = np.ones(sc.n, bool)
+    keep[list(affected)] = False
+    np.testing.assert_allclose(gs.s[keep], ref2["s"][keep], rtol=2e-5, atol=1e-9)
+
+
+def test_importance_dense_path_bit_exact():
+    """bgs_importance with caller-supplied dense w_fixed equals the oracle selection on the same
+    values, including heavy ties (count-only gid select) and an empty view."""
+    import paper_2605_13794_b200.bgs as B
+    ctx = B.Context()
+    rng = np.random.default_rng(5)
+    for trial in range(6):
+        n = int(rng.integers(1, 200_000))
+        if trial == 0:
+            w = np.zeros(n, np.uint64)
+        elif trial < 3:
+            w = (rng.integers(0, 4, n) * (1 << 20)).astype(np.uint64)  # massive ties
+        else:
+            w = rng.integers(0, 1 << 40, n).astype(np.uint64) * rng.integers(0, 2, n).astype(np.uint64)
+        a = np.where(w > 0, rng.integers(1, 300, n), 0).astype(np.uint32)
+        rad = np.where(a > 0, 4, rng.integers(0, 2, n) * 4).astype(np.int32)
+        ref = O.importance(rad, w, a)
+        dev = "cuda"
+        s = torch.zeros(n, dtype=torch.float64, device=dev)
+        crad = torch.zeros(n, dtype=torch.int32, device=dev)
+        cvis = torch.zeros(n, dtype=torch.int32, device=dev)
+        cull = torch.zeros((n + 31) // 32, dtype=torch.int32, device=dev)
+        B.bgs_importance(ctx, n, torch.from_numpy(rad).to(dev), torch.from_numpy(w.view(np.int64)).to(dev),
+                         torch.from_numpy(a.view(np.int32)).to(dev), s, crad, cvis, cull)
+        torch.cuda.synchronize()
+        assert np.array_equal(cvis.cpu().numpy().view(np.uint32), ref["c_vis"]), trial
+        assert np.array_equal(cull.cpu().numpy().view(np.uint32), ref["cull"]), trial
+        assert np.array_equal(crad.cpu().numpy().view(np.uint32), ref["c_rad"]), trial
+        np.testing.assert_allclose(s.cpu().numpy(), ref["s"], rtol=1e-12)
+    ctx.close()
+
+
+@pytest.mark.parametrize("M", [2, 3, 4])
+def test_multirank_local_group_parity(tiny_scene, tiny_run, M):
+    """The M > 1 kernels (tile costs, owner map, dest masks, pack, exchange, reverse gather-sum,
+    distributed radix select) on one GPU through the in-process transport: owner map and routing
+    bit-exact vs the oracle at the same M; pixels / n_contrib / w / a bitwise equal to the GPU
+    M = 1 run ("identical to what a single-GPU renderer would produce")."""
+    sc, cam, dl, st1, gs1 = tiny_run
+    st = O.OracleStep(sc, cam, M=M, dLdC=dl)
+    gs = GpuStep(sc, cam, M=M, dLdC=dl)
+    try:
+        owner = st.get("owner")
+        for r in range(M):
+            assert np.array_equal(gs.rank[r]["owner"], owner)
+            q = gs.rank[r]["q"]
+            b, e = st.get("tile_range", r)
+            assert (q["tile_begin"], q["tile_end"]) == (b, e)
+            assert q["P"] == len(st.get("pair_tile", r))
+            assert q["R"] == len(st.get("recv", r))
+            # received set and sorted pair sequence per owner
+            tiles = (gs.rank[r]["keys"] >> np.uint64(31)).astype(np.int32) + b
+            gids = gs.rank[r]["recv"]["gid"][gs.rank[r]["vals"]]
+            assert np.array_equal(tiles, st.get("pair_tile", r))
+            assert np.array_equal(gids, st.get("pair_gid", r))
+        counts = st.get("counts").reshape(M, M)
+        for r in range(M):
+            assert gs.rank[r]["q"]["D"] == counts[r].sum()
+        assert np.array_equal(gs.img, gs1.img) and np.array_equal(gs.T, gs1.T) and np.array_equal(gs.nc, gs1.nc)
+        assert np.array_equal(gs.a, gs1.a) and np.array_equal(gs.w, gs1.w)
+        assert np.array_equal(gs.c_vis, gs1.c_vis) and np.array_equal(gs.cull_bits, gs1.cull_bits)
+        for name in ("d_mean", "d_quat", "d_scale", "d_opac", "d_sh"):
+            ref = gs1.grads[name]
+            tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
+            assert np.all(np.abs(gs.grads[name] - ref) <= tol), name
+    finally:
+        gs.close()
+
+
+def test_gate_and_cull_bit_exact():
+    sc = S.gen_city("rubble", n=200_000, W=576, H=432, V=4)
+    cam = sc.cameras[2]
+    gate = dict(enabled=1, l_max=3, d0=sc.d0 * 4)
+    cull = S.random_cull_column(sc.n, 0.8, seed=2)
+    for M in (1, 2):
+        st = O.OracleStep(sc, cam, gate=gate, cull_global=cull, M=M)
+        gs = GpuStep(sc, cam, M=M, gate=gate, cull_global=cull)
+        try:
+            assert np.array_equal(gs.radius, st.get("radius"))
+            for r in range(M):
+                assert gs.rank[r]["q"]["n_lod"] == st.get("n_lod")[r]
+                assert gs.rank[r]["q"]["n_active"] == st.get("n_keep")[r]
+                assert gs.rank[r]["q"]["fallback"] == st.get("fallback")[r]
+            img = st.get("img").reshape(3, cam["H"], cam["W"])
+            cand = st.get("et_margin").reshape(cam["H"], cam["W"]) < ET_MARGIN
+            assert np.abs(gs.img - img)[:, ~cand].max() <= 1e-4
+        finally:
+            gs.close()
+
+
+@pytest.mark.parametrize("case", ["empty", "single", "ragged", "behind_and_offscreen"])
+def test_edge_cases(case):
+    if case == "empty":
+        sc = S.gen_small(1, 5, 40, 24)
+        sc.means[:, 2] = -3.0  # everything behind the camera
+    elif case == "single":
+        sc = S.gen_small(2, 1, 33, 33, spread=0.01)
+    elif case == "ragged":
+        sc = S.gen_tiny(n=3000, W=250, H=181, seed=4)
+        sc.cameras = [S.make_camera(250, 181, np.eye(3), np.zeros(3))]
+    else:
+        sc = S.gen_small(3, 400, 64, 48, spread=4.0)
+    cam = sc.cameras[0]
+    dl = S.grad_image(cam["H"], cam["W"], seed=3)
+    st = O.OracleStep(sc, cam, dLdC=dl)
+    gs = GpuStep(sc, cam, dLdC=dl)
+    try:
+        assert np.array_equal(gs.radius, st.get("radius"))
+        H, W = cam["H"], cam["W"]
+        cand = st.get("et_margin").reshape(H, W) < ET_MARGIN
+        assert np.abs(gs.img - st.get("img").reshape(3, H, W))[:, ~cand].max(initial=0) <= 1e-4
+        assert np.array_equal(gs.nc[~cand], st.get("n_contrib").reshape(H, W)[~cand])
+        if case == "empty":
+            assert np.all(gs.img == 0) and np.all(gs.T == 1) and np.all(gs.nc == 0)
+            assert gs.rank[0]["q"]["F"] == 0 and gs.rank[0]["q"]["P"] == 0
+    finally:
+        gs.close()
