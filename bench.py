@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the BlitzGS per-view distributed splatting step (fwd+bwd views/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config rubble] [--impl reference]
+
+N > 1: launched by torch.distributed.run (one rank per GPU, NCCL).  One step = one view through
+every SURVEY §8(a) row: a1 gate + a2 projection -> a3/a4 ownership + all-to-all -> a5-a7 pair
+emission / onesweep sort / ranges -> a8 compositing (+ w, a) -> a9 backward -> a10 reverse
+exchange -> a11 projection backward -> a12 importance (Eq.3, top-99% mass, Cull column).
+The per-view image gradient dL/dC is a fixed seeded tensor (the Eq.7 loss is outside the path).
+Rank 0 prints ONE JSON line.  See DESIGN.md §7 for every number's definition.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd views/s"
+CONFIG_SHAPES = {
+    # name: (label, gate on?) -- shapes in synthetic.CITY_CONFIGS
+    "rubble": ("Mill-19 Rubble-shaped synthetic aerial scene (6M Gaussians, 1152x864)", False),
+    "building": ("Mill-19 Building-shaped synthetic scene (8M Gaussians, 1152x864), LOD gate + importance mask",
+                 True),
+    "residence": ("UrbanScene3D Residence-shaped synthetic scene (8M Gaussians, 1368x912)", False),
+    "matrixcity": ("MatrixCity aerial-shaped synthetic city (20M Gaussians, 1920x1080)", False),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="rubble", choices=sorted(CONFIG_SHAPES))
+    p.add_argument("--impl", default="native", choices=["native", "reference"])
+    p.add_argument("--n", type=int, default=None, help="override Gaussian count (debug only)")
+    p.add_argument("--views", type=int, default=64)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--stages", action="store_true", help="also print per-stage timings to stderr")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# the native arm
+# ------------------------------------------------------------------------------------------
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_13794_b200.bgs as B
+    import synthetic as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(B.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        ctx = B.Context(rank, world, local, bytes(uid.cpu().numpy().tobytes()))
+    else:
+        ctx = B.Context(0, 1, local)
+
+    label, gate_on = CONFIG_SHAPES[args.config]
+    t0 = time.perf_counter()
+    scene = S.gen_city(args.config, n=args.n, V=args.views)
+    gen_s = time.perf_counter() - t0
+    shard = scene.shard(rank, world)
+    g = B.GaussianPlanes.from_scene(shard, dev)
+    n_local = shard.n
+    W, H = scene.cameras[0]["W"], scene.cameras[0]["H"]
+    cams = [B.camera(c) for c in scene.cameras]
+    gate = B.lod_gate(True, scene.k_levels - 1, scene.d0) if gate_on else None
+    stream = torch.cuda.Stream(dev)
+    grads = g.zeros_grads()
+    radius = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
+    rgb = torch.zeros(3, H, W, device=dev)
+    Tf = torch.zeros(H, W, device=dev)
+    nc = torch.zeros(H, W, dtype=torch.int32, device=dev)
+    s_imp = torch.zeros(max(n_local, 1), dtype=torch.float64, device=dev)
+    c_rad = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
+    c_vis = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
+    cull_cols = None
+    imp = B.importance_out(s_imp, c_rad, c_vis, torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32,
+                                                             device=dev))
+    dl = torch.from_numpy(S.grad_image(H, W)).to(dev)
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    if gate_on:
+        # Building config: per-view Cull columns from one untimed importance sweep
+        cull_cols = []
+        with torch.cuda.stream(stream):
+            for v, cam in enumerate(cams):
+                cc = torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32, device=dev)
+                B.bgs_view_step(ctx, g, cam, None, None, B.BGS_NO_COLOR, radius, rgb, Tf, nc, None, None,
+                                B.importance_out(s_imp, c_rad, c_vis, cc), stream)
+                cull_cols.append(cc)
+        stream.synchronize()
+
+    stage_names = ("project", "route", "sort", "raster_fwd", "raster_bwd", "route_reverse", "project_bwd",
+                   "importance")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stage_names) + 1)]
+
+    def one_view(v, record):
+        cam = cams[v % len(cams)]
+        cull = cull_cols[v % len(cams)] if cull_cols is not None else None
+        if record:
+            ev[0].record(stream)
+        B.bgs_project(ctx, g, cam, gate, cull, 0, radius, stream)
+        if record:
+            ev[1].record(stream)
+        B.bgs_route(ctx, None, stream)
+        if record:
+            ev[2].record(stream)
+        B.bgs_sort_tiles(ctx, stream)
+        if record:
+            ev[3].record(stream)
+        B.bgs_raster_fwd(ctx, B.BGS_IMPORTANCE, rgb, Tf, nc, stream)
+        if record:
+            ev[4].record(stream)
+        B.bgs_raster_bwd(ctx, dl, Tf, nc, stream)
+        if record:
+            ev[5].record(stream)
+        B.bgs_route_reverse(ctx, stream)
+        if record:
+            ev[6].record(stream)
+        B.bgs_project_bwd(ctx, g, cam, grads, stream)
+        if record:
+            ev[7].record(stream)
+        B.bgs_importance(ctx, n_local, radius, None, None, s_imp, c_rad, c_vis, imp_cull(v), 99, 100, stream)
+        if record:
+            ev[8].record(stream)
+
+    cull_out = torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32, device=dev)
+
+    def imp_cull(v):
+        return cull_out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for w in range(args.warmup):
+            one_view(w, False)
+        stream.synchronize()
+        barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        stage_ms = np.zeros(len(stage_names))
+        qs = []
+        total_ms = 0.0
+        E_sum = 0.0
+        launches0 = ctx.launches()
+        for k in range(args.steps):
+            l2_flush.zero_()  # between timed views: evict the L2 (inputs also exceed it)
+            stream.synchronize()
+            one_view(args.warmup + k, True)
+            stream.synchronize()
+            st = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(stage_names))]
+            stage_ms += st
+            total_ms += ev[0].elapsed_time(ev[-1])
+            qs.append(ctx.query())
+            E_sum += float(nc.sum(dtype=torch.int64).item())  # outside the timed events
+        launches = ctx.launches() - launches0
+        clk = clocks.stop()
+    torch.cuda.synchronize()
+    barrier()
+    tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_ms_max = float(tmax.item())
+    ms_per_view = total_ms_max / args.steps
+    views_per_s = 1000.0 / ms_per_view
+
+    # ---- per-view workload statistics (summed over ranks)
+    P_rank = float(np.mean([q["P"] for q in qs]))
+    stats = torch.tensor([P_rank, np.mean([q["F"] for q in qs]), np.mean([q["R"] for q in qs]),
+                          np.mean([q["D"] for q in qs]), np.mean([q["n_active"] for q in qs]), float(n_local)],
+                         dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats)
+    P_all, F_all, R_all, D_all, A_all, N_all = [float(x) for x in stats.cpu().numpy()]
+    pairs_per_s = P_all * views_per_s
+
+    # ---- e2e: same metric through the host-buffer ABI call (H2D of dL/dC, D2H of the image)
+    dl_host = torch.from_numpy(S.grad_image(H, W)).pin_memory()
+    rgb_host = torch.empty(3, H, W).pin_memory()
+    with torch.cuda.stream(stream):
+        for w in range(2):
+            B.bgs_view_step_host(ctx, g, cams[w], gate, None, 0, radius, dl_host, rgb_host, grads, imp, stream)
+        stream.synchronize()
+        barrier()
+        e2e_s = 0.0
+        for k in range(args.steps):
+            l2_flush.zero_()
+            stream.synchronize()
+            t1 = time.perf_counter()
+            B.bgs_view_step_host(ctx, g, cams[(args.warmup + k) % len(cams)], gate,
+                                 cull_cols[(args.warmup + k) % len(cams)] if cull_cols is not None else None, 0,
+                                 radius, dl_host, rgb_host, grads, imp, stream)
+            e2e_s += time.perf_counter() - t1
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_views = args.steps / float(te.item())
+
+    # ---- roofline of every stage, dominant one reported at top level
+    from paper_2605_13794_b200.roofline import stage_rooflines
+    peaks = load_peaks()
+    stage_avg = stage_ms / args.steps
+    roof = stage_rooflines(stage_avg, qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
+                           sm_mhz=clk.get("sm_mhz"), E=E_sum / args.steps, cull=cull_cols is not None)
+    dominant = max(roof, key=lambda r: r["ms"])
+
+    result = {
+        "metric": METRIC, "value": round(views_per_s, 3), "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_view, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": label, "config": args.config, "gaussians": int(N_all), "width": W, "height": H,
+                   "views": len(cams), "lod_gate": gate_on, "importance_mask": gate_on,
+                   "parallelism": f"index-parity shards x {world}, tile-owner all-to-all",
+                   "l2": "flushed between timed views (256 MB write); inputs also exceed L2"},
+        "splat_pairs_per_s": round(pairs_per_s, 1),
+        "per_view": {"pairs": P_all, "records_F": F_all, "received_R": R_all, "sent_D": D_all,
+                     "active": A_all, "duplication_D_over_F": (D_all / F_all if F_all else None)},
+        "stages_ms": {n: round(float(v), 4) for n, v in zip(stage_names, stage_avg)},
+        "roofline": {k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+        "roofline_kernel": dominant["stage"],
+        "roofline_stages": roof,
+        "e2e": {"value": round(e2e_views, 3), "unit": "views/s", "h2d_bytes_per_step": int(3 * H * W * 4),
+                "d2h_bytes_per_step": int(3 * H * W * 4)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "scene_gen_s": round(gen_s, 2),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(scene, args)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured", "sm_max_mhz": d.get("sm_max_mhz", 1965.0)}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
+
+
+# ------------------------------------------------------------------------------------------
+# oracle baselines (the one other place bench.py executes oracle/)
+# ------------------------------------------------------------------------------------------
+def oracle_sample(scene, views, frac_tiles: float):
+    """The oracle's time per view on this workload: full projection + routing + sort of every
+    view, compositing fwd+bwd on a `frac_tiles` sample of the tiles, scaled to a whole view."""
+    import oracle as O
+    import synthetic as S
+    cam = scene.cameras[views % len(scene.cameras)]
+    dl = S.grad_image(cam["H"], cam["W"])
+    st = O.OracleStep(scene, cam, M=1, dLdC=dl, tile_frac=frac_tiles)
+    return st.seconds, st.seconds_by_phase()
+
+
+def cpu_baseline(scene, args):
+    import oracle as O
+    frac = 1.0 / 8
+    secs, phases = oracle_sample(scene, args.warmup, frac)
+    comp = phases["composite"] / frac
+    per_view = phases["project"] + phases["route_sort"] + comp + phases["project_bwd"]
+    return {"value": round(1.0 / per_view, 5), "unit": "views/s", "cores": 1, "kind": "oracle",
+            "sample": f"one view of the same workload: oracle projection, ownership, routing and sort of all "
+                      f"{scene.n} Gaussians, compositing fwd+bwd of a {frac:.3f} sample of the tiles scaled "
+                      f"x{1 / frac:.0f} ({secs:.1f} s of CPU work, 1 thread)",
+            "phases_s": {k: round(v, 3) for k, v in phases.items()}, "oracle_lib": os.path.basename(O.build())}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synthetic as S
+    label, gate_on = CONFIG_SHAPES[args.config]
+    scene = S.gen_city(args.config, n=args.n, V=args.views)
+    frac = 1.0 / 16
+    for w in range(args.warmup):
+        oracle_sample(scene, w, frac)
+    tot = 0.0
+    phase_tot = {}
+    for k in range(args.steps):
+        secs, ph = oracle_sample(scene, args.warmup + k, frac)
+        per_view = ph["project"] + ph["route_sort"] + ph["composite"] / frac + ph["project_bwd"]
+        tot += per_view
+        for kk, v in ph.items():
+            phase_tot[kk] = phase_tot.get(kk, 0.0) + v
+    v = args.steps / tot
+    W, H = scene.cameras[0]["W"], scene.cameras[0]["H"]
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "views/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * tot / args.steps, 2),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": label, "config": args.config, "gaussians": scene.n, "width": W, "height": H},
+           "cpu_baseline": {"value": round(v, 6), "unit": "views/s", "cores": 1, "kind": "oracle",
+                            "sample": f"per step: oracle projection/ownership/sort of all {scene.n} Gaussians of "
+                                      f"one view + fwd+bwd compositing of a {frac:.4f} tile sample scaled "
+                                      f"x{1 / frac:.0f}"},
+           "e2e": {"value": round(v, 6), "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_native(a)

@@ -24,9 +24,9 @@
  *  - All inputs and fixed-size outputs are CALLER-owned.  Variable-size intermediates
  *    (records, exchange buffers, pairs, per-splat gradients) live in the ctx arena and stay
  *    valid until the next call of the same stage on that ctx.
- *  - Every call enqueues on `stream` (a cudaStream_t passed as void*; NULL = legacy default
- *    stream is rejected, pass a real stream).  Calls marked HOST-SYNC block the host on that
- *    stream once (to size variable buffers).
+ *  - Every call enqueues on `stream` (a cudaStream_t passed as void*; NULL selects the legacy
+ *    default stream).  Calls marked HOST-SYNC block the host on that stream once (to size
+ *    variable buffers).
  *  - One ctx per rank and per host thread.  world > 1 uses NCCL (ncclCommInitRank from a
  *    unique id) or, for single-GPU testing, an in-process group sharing one device.
  *  - Layouts: Gaussian parameters are structure-of-arrays of 16-byte rows so kernels issue

@@ -52,7 +52,8 @@ def lib():
     if _lib is None:
         _lib = C.CDLL(build())
         _lib.or_step.restype = C.c_void_p
-        _lib.or_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        _lib.or_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                C.c_int32]
         _lib.or_free.argtypes = [C.c_void_p]
         _lib.or_get.restype = C.c_int64
         _lib.or_get.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_void_p]
@@ -87,7 +88,7 @@ _FIELD_DTYPES = {
     "w_fixed": np.uint64, "a": np.uint32, "g2d": np.float64, "d_mean": np.float64, "d_quat": np.float64,
     "d_scale": np.float64, "d_opac": np.float64, "d_sh": np.float64, "n_pairs_total": np.int64,
     "mean2d": np.float64, "conic": np.float64, "depth": np.float64, "rgb": np.float64, "thr": np.float64,
-    "rect": np.int32, "img64": np.float64, "margins": np.float64, "tile_range": np.int32, "recv": np.int64, "pair_tile": np.int32, "pair_gid": np.int64,
+    "rect": np.int32, "phase_seconds": np.float64, "img64": np.float64, "margins": np.float64, "tile_range": np.int32, "recv": np.int64, "pair_tile": np.int32, "pair_gid": np.int64,
     "range_lo": np.int64, "range_hi": np.int64,
 }
 
@@ -99,7 +100,7 @@ class OracleStep:
     """One simulated view step at M ranks (O1..O11 of DESIGN.md §5)."""
 
     def __init__(self, scene, cam: dict, gate: dict | None = None, cull_global: np.ndarray | None = None,
-                 M: int = 1, flags: int = 0, dLdC: np.ndarray | None = None):
+                 M: int = 1, flags: int = 0, dLdC: np.ndarray | None = None, tile_frac: float = 1.0):
         L = lib()
         self._keep = []
         n = scene.n
@@ -119,7 +120,8 @@ class OracleStep:
         self.n = n
         self.cam = cam
         t0 = time.perf_counter()
-        self._h = L.or_step(C.byref(sc), C.byref(cm), C.byref(gt), _ptr(cull), M, flags, _ptr(dl))
+        stride = max(1, int(round(1.0 / tile_frac)))
+        self._h = L.or_step(C.byref(sc), C.byref(cm), C.byref(gt), _ptr(cull), M, flags, _ptr(dl), stride)
         self.seconds = time.perf_counter() - t0
 
     def get(self, name: str, rank: int = 0) -> np.ndarray:
@@ -130,6 +132,10 @@ class OracleStep:
         out = np.empty(cnt, dtype=_FIELD_DTYPES[name])
         L.or_get(self._h, name.encode(), rank, _ptr(out))
         return out
+
+    def seconds_by_phase(self) -> dict:
+        v = self.get("phase_seconds")
+        return dict(project=float(v[0]), route_sort=float(v[1]), composite=float(v[2]), project_bwd=float(v[3]))
 
     def bruteforce(self):
         H, W = self.cam["H"], self.cam["W"]

@@ -21,6 +21,7 @@
 // finite-difference pins (tests/test_oracle_fd.py).
 // ==========================================================================================
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -279,6 +280,7 @@ struct Step {
   std::vector<double> g2d;                 // [n][9] d/d(mx,my,A,B,C,o,r,g,b), owner-summed
   std::vector<double> d_mean, d_quat, d_scale, d_opac, d_sh;
   int64_t n_pairs_total = 0;
+  double t_project = 0, t_route_sort = 0, t_composite = 0, t_project_bwd = 0;  // seconds
 };
 
 struct Contrib {
@@ -527,7 +529,10 @@ void project_bwd_one(const Scene& s, int64_t i, const Camera& cam, const double*
 
 template <class T>
 Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uint32_t* cull_global, int M,
-                  int flags, const float* dLdC) {
+                  int flags, const float* dLdC, int tile_stride) {
+  using clk = std::chrono::steady_clock;
+  auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+  auto t0 = clk::now();
   const bool no_color = flags & 1;
   auto* st = new Step<T>();
   st->M = M;
@@ -576,6 +581,8 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
     st->proj[i] = project_one<T>(s, i, cam, no_color);
     st->radius[i] = st->proj[i].valid ? st->proj[i].radius : 0;
   }
+  auto t1 = clk::now();
+  st->t_project = secs(t0, t1);
   // O4 cost-aware tile ownership (reading R24 / D6): c_t = pairs_t + 1
   st->tile_pairs.assign(st->T_, 0);
   for (int64_t i = 0; i < n; ++i) {
@@ -650,6 +657,8 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
       if (q + 1 == os.pairs.size() || os.pairs[q + 1].first != os.pairs[q].first) os.range_hi[lt] = int64_t(q) + 1;
     }
   }
+  auto t2 = clk::now();
+  st->t_route_sort = secs(t1, t2);
   // O8/O9 composite (+ backward) per owner, tiles ascending
   const size_t npix = size_t(cam.W) * cam.H;
   st->img.assign(3 * npix, 0.f);
@@ -666,6 +675,7 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
     OwnerState& os = st->owners[m];
     if (dLdC) g_owner.assign(size_t(9) * n, 0.0);
     for (int t = os.t_begin; t < os.t_end; ++t) {
+      if (tile_stride > 1 && t % tile_stride != 0) continue;  // timing samples only (bench.py)
       int lt = t - os.t_begin;
       std::vector<int64_t> list;
       for (int64_t q = os.range_lo[lt]; q < os.range_hi[lt]; ++q) list.push_back(os.pairs[q].second);
@@ -675,6 +685,8 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
     if (dLdC)
       for (size_t e = 0; e < g_owner.size(); ++e) st->g2d[e] += g_owner[e];
   }
+  auto t3 = clk::now();
+  st->t_composite = secs(t2, t3);
   // O11 projection backward
   if (dLdC) {
     st->d_mean.assign(3 * n, 0.0);
@@ -688,6 +700,7 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
                       &st->d_scale[3 * i], &st->d_opac[i], &st->d_sh[48 * i]);
     }
   }
+  st->t_project_bwd = secs(t3, clk::now());
   return st;
 }
 
@@ -736,6 +749,10 @@ int64_t get_field(Step<T>& st, const std::string& name, int rank, void* out) {
   if (name == "d_scale") return copy_out(st.d_scale, out);
   if (name == "d_opac") return copy_out(st.d_opac, out);
   if (name == "d_sh") return copy_out(st.d_sh, out);
+  if (name == "phase_seconds") {
+    std::vector<double> v = {st.t_project, st.t_route_sort, st.t_composite, st.t_project_bwd};
+    return copy_out(v, out);
+  }
   if (name == "n_pairs_total") {
     if (out) *static_cast<int64_t*>(out) = st.n_pairs_total;
     return 1;
@@ -796,7 +813,7 @@ struct or_gate { int32_t enabled, l_max; double d0; int32_t fb_num, fb_den; };
 
 // flags: bit0 = NO_COLOR (skip SH), bit1 = fp64 forward (FD pins)
 void* or_step(const or_scene* sc, const or_camera* cm, const or_gate* gt, const uint32_t* cull_global, int32_t M,
-              int32_t flags, const float* dLdC) {
+              int32_t flags, const float* dLdC, int32_t tile_stride) {
   Scene s{sc->n, sc->mean, sc->quat, sc->scale, sc->opac, sc->sh, sc->lod};
   Camera c;
   std::memcpy(&c, cm, sizeof(Camera));
@@ -804,9 +821,9 @@ void* or_step(const or_scene* sc, const or_camera* cm, const or_gate* gt, const 
   auto* h = new Handle();
   if (flags & 2) {
     h->is_f64 = 1;
-    h->d.reset(run_step<double>(s, c, g, cull_global, M, flags, dLdC));
+    h->d.reset(run_step<double>(s, c, g, cull_global, M, flags, dLdC, tile_stride));
   } else {
-    h->f.reset(run_step<float>(s, c, g, cull_global, M, flags, dLdC));
+    h->f.reset(run_step<float>(s, c, g, cull_global, M, flags, dLdC, tile_stride));
   }
   return h;
 }

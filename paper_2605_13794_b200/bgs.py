@@ -163,9 +163,8 @@ class Context:
         n = int(nbytes.value)
         out = torch.empty(n, dtype=torch.uint8, device=f"cuda:{self.device}")
         if n and p.value:
-            cudart = torch.cuda.cudart()
             torch.cuda.synchronize(self.device)
-            st = cudart.cudaMemcpy(out.data_ptr(), p.value, n, 3)  # device to device
+            st = _cudart().cudaMemcpy(C.c_void_p(out.data_ptr()), p, C.c_size_t(n), 3)  # device to device
             if int(st) != 0:
                 raise RuntimeError(f"cudaMemcpy failed: {st}")
         return out.view(dtype) if n else out
@@ -174,6 +173,29 @@ class Context:
         if getattr(self, "_h", None):
             _lib.bgs_ctx_destroy(self._h)
             self._h = None
+
+
+_CUDART = None
+
+
+def _cudart():
+    """The CUDA runtime torch already loaded (for raw device-to-device copies of debug views)."""
+    global _CUDART
+    if _CUDART is None:
+        import glob
+        cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib",
+                                       "libcudart.so*")) + ["libcudart.so.12", "libcudart.so"]
+        for c in cands:
+            try:
+                _CUDART = C.CDLL(c)
+                break
+            except OSError:
+                continue
+        if _CUDART is None:
+            raise RuntimeError("libcudart not found")
+        _CUDART.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+        _CUDART.cudaMemcpy.restype = C.c_int
+    return _CUDART
 
 
 def unique_id() -> bytes:

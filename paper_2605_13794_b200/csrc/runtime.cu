@@ -277,9 +277,8 @@ bgs_status check_ctx(bgs_ctx* ctx) {
   return BGS_OK;
 }
 
-bgs_status check_stream(bgs_ctx* ctx, void* stream) {
-  if (!stream) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "stream must be a real cudaStream_t (not NULL)");
-  return BGS_OK;
+bgs_status check_stream(bgs_ctx*, void*) {
+  return BGS_OK;  // NULL is the legacy default stream (allowed; callers should prefer their own)
 }
 
 bgs_status set_camera(bgs_ctx* ctx, const bgs_camera* c) {

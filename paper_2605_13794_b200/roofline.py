@@ -1,0 +1,57 @@
+"""Algorithmic bytes / operations per stage of one view.
+
+These are what the METHOD must move or compute, not what a kernel happens to do:
+  a1+a2 project      16 N (mu,o) + 1 N (lod) + N/8 (cull column, if any) + 32 A (q, s of active)
+                     + 192 F (SH of in-frustum) + 52 F (record + index) + 4 N (radius)      [bytes]
+  a5-a7 sort         16 R (rect, depth of received) + 12 P (pairs) + 24 P per executed 8-bit
+                     radix pass + 8 P (ranges pass)                                        [bytes]
+  a8 raster fwd      22 FP32 ops per (pixel, list entry) up to the pixel's last contributor
+                     (E = sum of n_contrib)                                               [ALU]
+  a9 raster bwd      45 FP32 ops per (pixel, list entry) up to the last contributor       [ALU]
+  a10 reverse (M>1)  48 D (send back) + 48 D (gather)                                     [bytes]
+  a11 project bwd    240 F (params) + 52 F (partials + index) + 2 x 236 F (grads RMW)     [bytes]
+  a12 importance     52 F (w, a, index) + 2 x 16 F (s, c_rad, c_vis RMW) + N/8 (Cull)    [bytes]
+Peaks: HBM = MEASURED_PEAKS.json hbm_gbs (copy bandwidth); ALU = 148 SMs x 128 FP32 lanes x
+sm_max clock (one FP32 instruction per lane per clock; FFMA counted as one op).
+"""
+from __future__ import annotations
+
+FWD_OPS = 22.0
+BWD_OPS = 45.0
+
+
+def _avg(qs, k):
+    return sum(q[k] for q in qs) / max(1, len(qs))
+
+
+def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=None, cull=False):
+    N = float(n_local)
+    A, F, R, D, P = (_avg(qs, k) for k in ("n_active", "F", "R", "D", "P"))
+    passes = _avg(qs, "sort_passes")
+    hbm = float(peaks["hbm_gbs"])
+    alu = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12  # T ops/s
+    names = ("project", "route", "sort", "raster_fwd", "raster_bwd", "route_reverse", "project_bwd", "importance")
+    bytes_ = {
+        "project": 16 * N + N + (N / 8 if cull else 0) + 32 * A + 192 * F + 52 * F + 4 * N,
+        "route": (48 * D + 48 * R) if world > 1 else 0.0,
+        "sort": 16 * R + 12 * P + 24 * P * passes + 8 * P,
+        "route_reverse": (96 * D) if world > 1 else 0.0,
+        "project_bwd": 240 * F + 52 * F + 2 * 236 * F,
+        "importance": 52 * F + 32 * F + N / 8,
+    }
+    E = float(E) if E is not None else 0.0
+    ops = {"raster_fwd": FWD_OPS * E, "raster_bwd": BWD_OPS * E}
+    out = []
+    for name, ms in zip(names, stage_ms):
+        ms = float(ms)
+        if name in ops:
+            ach = ops[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+            out.append(dict(stage=name, ms=round(ms, 4), bound="alu", achieved=round(ach, 3), peak=round(alu, 2),
+                            unit="TFLOP/s", frac=round(ach / alu, 4), traffic=None,
+                            work=f"{ops[name]:.3e} ops ({FWD_OPS if name == 'raster_fwd' else BWD_OPS:.0f} x E)"))
+        else:
+            b = bytes_.get(name, 0.0)
+            ach = b / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+            out.append(dict(stage=name, ms=round(ms, 4), bound="hbm", achieved=round(ach, 1), peak=hbm,
+                            unit="GB/s", frac=round(ach / hbm, 4), traffic=None, work=f"{b:.3e} bytes"))
+    return out
