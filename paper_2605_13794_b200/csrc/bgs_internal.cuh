@@ -73,6 +73,7 @@ struct ProjectArgs {
 
 void launch_gate_count(const ProjectArgs& a, cudaStream_t s);
 void launch_project(const ProjectArgs& a, cudaStream_t s);
+void launch_color(const ProjectArgs& a, cudaStream_t s);  // after launch_project; F read on device
 
 // sort (a5-a7)
 struct SortArgs {

@@ -100,14 +100,28 @@ __global__ void __launch_bounds__(256) k_imp_hist(ImportanceArgs a, const ImpSta
   const int shift = 8 * (kWRounds - 1 - round);
   const unsigned long long prefix = st->prefix;
   const bool empty = st->empty;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; !empty && t < a.n_items;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const unsigned long long w = a.item_lidx ? a.acc[t].w : a.w_dense[t];
-    if (w == 0) continue;
-    if (shift + 8 < 64 && (w >> (shift + 8)) != prefix) continue;
-    const uint32_t d = uint32_t((w >> shift) & 255u);
-    atomicAdd(&s_cnt[d], 1ull);
-    atomicAdd(&s_mass[d], w);
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count so every lane reaches the warp collectives
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); !empty && base < a.n_items;
+       base += stride) {
+    const int64_t t = base + lane;
+    unsigned long long w = 0;
+    if (t < a.n_items) w = a.item_lidx ? a.acc[t].w : a.w_dense[t];
+    const bool cand = w != 0 && !(shift + 8 < 64 && (w >> (shift + 8)) != prefix);
+    const uint32_t d = cand ? uint32_t((w >> shift) & 255u) : 256u + lane;
+    // one shared-memory atomic per distinct digit of the warp: the early rounds put almost
+    // every candidate in one bin, which serialised per-lane 64-bit atomics
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t lo = uint32_t(w & 0xffffffu), mid = uint32_t((w >> 24) & 0xffffffu), hi = uint32_t(w >> 48);
+    const uint32_t slo = __reduce_add_sync(peers, lo);
+    const uint32_t smid = __reduce_add_sync(peers, mid);
+    const uint32_t shi = __reduce_add_sync(peers, hi);
+    if (cand && lane == __ffs(peers) - 1) {
+      atomicAdd(&s_cnt[d], (unsigned long long)__popc(peers));
+      atomicAdd(&s_mass[d], (unsigned long long)slo + ((unsigned long long)smid << 24) +
+                                ((unsigned long long)shi << 48));
+    }
   }
   __syncthreads();
   if (s_cnt[threadIdx.x]) {

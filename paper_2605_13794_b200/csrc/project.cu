@@ -8,10 +8,15 @@
 // rect, tile ids and pair counts are integers derived from these floats and must be
 // bit-identical to the oracle's.  Expression trees are the ones listed in DESIGN.md §4.
 //
-// Memory plan (HBM-bound): one thread per local Gaussian; 16-B loads of (mu, o) and the lod
-// byte for everyone; quat/scale (32 B) only for Gaussians that pass the gate; the 192-B SH
-// row only for Gaussians that are in the frustum; 48-B record + 4-B index written through a
-// warp-aggregated append; radius (4 B) written for all.
+// Two kernels, both HBM-bound:
+//  k_project (one thread per local Gaussian): 16-B (mu, o) + lod byte (+ cull bit) for
+//    everyone; quat/scale (32 B) issued up front when no gate/cull can drop the Gaussian,
+//    otherwise only for kept ones; EWA geometry, radius, rect; a warp-aggregated append of
+//    the 48-B record (colour left for k_color) + 4-B index; radius written for all.
+//  k_color (one thread per record): the 192-B SH row of in-frustum Gaussians only, as 12
+//    independent 128-bit loads in flight per thread, evaluated along the view direction.
+// Splitting keeps k_project at low register pressure (full occupancy for latency hiding) and
+// reads SH only for the F records.
 #include "bgs_internal.cuh"
 
 namespace bgs {
@@ -35,16 +40,22 @@ __global__ void __launch_bounds__(256) k_gate_count(ProjectArgs a) {
   if (threadIdx.x == 0 && c) atomicAdd(a.counters + C_NLOD, (unsigned long long)c);
 }
 
-__global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
+__global__ void __launch_bounds__(256, 6) k_project(ProjectArgs a) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool valid = false;
   bool active = false;
-  Rec rec;
+  float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, depth = 0.f, opac = 0.f;
   int radius = 0;
   uint32_t area = 0;
   int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
   if (i < a.n) {
+    const bool filtered = a.gate_enabled || a.cull;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), sc = q;
+    if (!filtered) {  // nothing can drop this Gaussian before projection: issue all loads now
+      q = ldg4(a.quat + i);
+      sc = ldg4(a.scale + i);
+    }
     const float4 mo = ldg4(a.mean_opac + i);
     // ---- a1: Eq.5 gate with per-rank fallback, then Eq.6 cull column
     bool keep = true;
@@ -56,6 +67,10 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
     if (keep && a.cull) keep = !((__ldg(a.cull + (i >> 5)) >> (i & 31)) & 1u);
     active = keep;
     if (keep) {
+      if (filtered) {
+        q = ldg4(a.quat + i);
+        sc = ldg4(a.scale + i);
+      }
       const CameraK& cm = a.cam;
       // ---- a2: t_c = R mu + t
       const float tx = ((cm.R[0] * mo.x + cm.R[1] * mo.y) + cm.R[2] * mo.z) + cm.t[0];
@@ -63,8 +78,6 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
       const float tz = ((cm.R[6] * mo.x + cm.R[7] * mo.y) + cm.R[8] * mo.z) + cm.t[2];
       if (tz > cm.near_clip) {
         // Sigma = R(q) S S^T R(q)^T
-        const float4 q = ldg4(a.quat + i);
-        const float4 sc = ldg4(a.scale + i);
         const float xx = q.y * q.y, yy = q.z * q.z, zz = q.w * q.w;
         const float xy = q.y * q.z, xz = q.y * q.w, yz = q.z * q.w;
         const float wx = q.x * q.y, wy = q.x * q.z, wz = q.x * q.w;
@@ -113,21 +126,21 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
         cc = cc + 0.3f;
         const float det = ca * cc - cb * cb;
         if (det > 0.0f) {
-          rec.A = cc / det;
-          rec.B = (-cb) / det;
-          rec.C = ca / det;
-          rec.mx = cm.fx * txtz + cm.cx;
-          rec.my = cm.fy * tytz + cm.cy;
+          cA = cc / det;
+          cB = (-cb) / det;
+          cC = ca / det;
+          mx = cm.fx * txtz + cm.cx;
+          my = cm.fy * tytz + cm.cy;
           const float mid = 0.5f * (ca + cc);
           const float disc = fmaxf(0.1f, mid * mid - det);
           const float lambda1 = mid + sqrtf(disc);
           const float rf = fminf(ceilf(3.0f * sqrtf(lambda1)), 1048576.0f);
           const int rad = int(rf);
           const float r_ = float(rad);
-          const float fx0 = (rec.mx - r_) / 16.0f;
-          const float fy0 = (rec.my - r_) / 16.0f;
-          const float fx1 = ((rec.mx + r_) + 15.0f) / 16.0f;
-          const float fy1 = ((rec.my + r_) + 15.0f) / 16.0f;
+          const float fx0 = (mx - r_) / 16.0f;
+          const float fy0 = (my - r_) / 16.0f;
+          const float fx1 = ((mx + r_) + 15.0f) / 16.0f;
+          const float fy1 = ((my + r_) + 15.0f) / 16.0f;
           x0 = int(fminf(float(cm.TX), fmaxf(0.0f, fx0)));
           y0 = int(fminf(float(cm.TY), fmaxf(0.0f, fy0)));
           x1 = int(fminf(float(cm.TX), fmaxf(0.0f, fx1)));
@@ -136,57 +149,8 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
           if (area != 0) {
             valid = true;
             radius = rad;
-            rec.depth = tz;
-            rec.opac = mo.w;
-            rec.gid = uint32_t(i) * uint32_t(a.world) + uint32_t(a.rank);
-            rec.rect = uint32_t(x0) | (uint32_t(y0) << 8) | (uint32_t(x1) << 16) | (uint32_t(y1) << 24);
-            rec.r = rec.g = rec.b = 0.0f;
-            if (!a.no_color) {
-              // SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2
-              const float dx = mo.x - cm.campos[0], dy = mo.y - cm.campos[1], dz = mo.z - cm.campos[2];
-              const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
-              const float x = dx / len, y = dy / len, z = dz / len;
-              const float xx2 = x * x, yy2 = y * y, zz2 = z * z, xy2 = x * y, yz2 = y * z, xz2 = x * z;
-              float Y[16];
-              Y[0] = 0.28209479177387814f;
-              Y[1] = -(0.4886025119029199f * y);
-              Y[2] = 0.4886025119029199f * z;
-              Y[3] = -(0.4886025119029199f * x);
-              Y[4] = 1.0925484305920792f * xy2;
-              Y[5] = -1.0925484305920792f * yz2;
-              Y[6] = 0.31539156525252005f * ((2.0f * zz2 - xx2) - yy2);
-              Y[7] = -1.0925484305920792f * xz2;
-              Y[8] = 0.5462742152960396f * (xx2 - yy2);
-              Y[9] = (-0.5900435899266435f * y) * (3.0f * xx2 - yy2);
-              Y[10] = (2.890611442640554f * xy2) * z;
-              Y[11] = (-0.4570457994644658f * y) * ((4.0f * zz2 - xx2) - yy2);
-              Y[12] = (0.3731763325901154f * z) * ((2.0f * zz2 - 3.0f * xx2) - 3.0f * yy2);
-              Y[13] = (-0.4570457994644658f * x) * ((4.0f * zz2 - xx2) - yy2);
-              Y[14] = (1.445305721320277f * z) * (xx2 - yy2);
-              Y[15] = (-0.5900435899266435f * x) * (xx2 - 3.0f * yy2);
-              const float4* shp = reinterpret_cast<const float4*>(a.sh + 48 * i);
-              float col[3] = {0.f, 0.f, 0.f};
-              float v[48];
-#pragma unroll
-              for (int q4 = 0; q4 < 12; ++q4) {
-                const float4 f = ldg4(shp + q4);
-                v[4 * q4 + 0] = f.x;
-                v[4 * q4 + 1] = f.y;
-                v[4 * q4 + 2] = f.z;
-                v[4 * q4 + 3] = f.w;
-              }
-#pragma unroll
-              for (int ch = 0; ch < 3; ++ch) {
-                float c = Y[0] * v[ch];
-#pragma unroll
-                for (int k = 1; k < 16; ++k) c = c + Y[k] * v[3 * k + ch];
-                c = c + 0.5f;
-                col[ch] = c < 0.0f ? 0.0f : c;
-              }
-              rec.r = col[0];
-              rec.g = col[1];
-              rec.b = col[2];
-            }
+            depth = tz;
+            opac = mo.w;
           }
         }
       }
@@ -196,8 +160,7 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
   // ---- warp-aggregated append of the record (one atomic per warp)
   const unsigned vmask = __ballot_sync(0xffffffffu, valid);
   const unsigned amask = __ballot_sync(0xffffffffu, active);
-  // pairs over all tiles (P_all) and active count: warp sums, one atomic per warp
-  unsigned long long wsum = __reduce_add_sync(0xffffffffu, area);
+  const unsigned long long wsum = __reduce_add_sync(0xffffffffu, area);  // P_all contribution
   if (vmask) {
     const int leader = __ffs(vmask) - 1;
     unsigned long long base = 0;
@@ -209,10 +172,12 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
     if (valid) {
       const unsigned long long slot = base + __popc(vmask & ((1u << lane) - 1u));
       if ((int64_t)slot < a.rec_cap) {
+        const uint32_t gid = uint32_t(i) * uint32_t(a.world) + uint32_t(a.rank);
+        const uint32_t rect = uint32_t(x0) | (uint32_t(y0) << 8) | (uint32_t(x1) << 16) | (uint32_t(y1) << 24);
         float4* dst = reinterpret_cast<float4*>(a.recs + slot);
-        dst[0] = make_float4(rec.mx, rec.my, rec.A, rec.B);
-        dst[1] = make_float4(rec.C, rec.opac, rec.r, rec.g);
-        dst[2] = make_float4(rec.b, rec.depth, __uint_as_float(rec.gid), __uint_as_float(rec.rect));
+        dst[0] = make_float4(mx, my, cA, cB);
+        dst[1] = make_float4(cC, opac, 0.f, 0.f);
+        dst[2] = make_float4(0.f, depth, __uint_as_float(gid), __uint_as_float(rect));
         a.rec_lidx[slot] = uint32_t(i);
       }
       if (a.tile_diff) {
@@ -228,6 +193,67 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
   if (amask && lane == __ffs(amask) - 1) atomicAdd(a.counters + C_NACT, (unsigned long long)__popc(amask));
 }
 
+__device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f);
+__device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f) { color_one_impl(a, f); }
+
+// SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2.
+// Persistent grid-stride over the F records (F read on the device: no host round trip).
+__global__ void __launch_bounds__(256) k_color(ProjectArgs a) {
+  const int64_t F = int64_t(*((volatile unsigned long long*)(a.counters + C_F)));
+  for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < F; f += int64_t(gridDim.x) * blockDim.x)
+    color_one(a, f);
+}
+
+__device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f) {
+  const uint32_t i = a.rec_lidx[f];
+  const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i);
+  float v[48];
+#pragma unroll
+  for (int q4 = 0; q4 < 12; ++q4) {
+    const float4 t = ldg4(shp + q4);
+    v[4 * q4 + 0] = t.x;
+    v[4 * q4 + 1] = t.y;
+    v[4 * q4 + 2] = t.z;
+    v[4 * q4 + 3] = t.w;
+  }
+  const float4 mo = ldg4(a.mean_opac + i);
+  const CameraK& cm = a.cam;
+  const float dx = mo.x - cm.campos[0], dy = mo.y - cm.campos[1], dz = mo.z - cm.campos[2];
+  const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
+  const float x = dx / len, y = dy / len, z = dz / len;
+  const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+  float Y[16];
+  Y[0] = 0.28209479177387814f;
+  Y[1] = -(0.4886025119029199f * y);
+  Y[2] = 0.4886025119029199f * z;
+  Y[3] = -(0.4886025119029199f * x);
+  Y[4] = 1.0925484305920792f * xy;
+  Y[5] = -1.0925484305920792f * yz;
+  Y[6] = 0.31539156525252005f * ((2.0f * zz - xx) - yy);
+  Y[7] = -1.0925484305920792f * xz;
+  Y[8] = 0.5462742152960396f * (xx - yy);
+  Y[9] = (-0.5900435899266435f * y) * (3.0f * xx - yy);
+  Y[10] = (2.890611442640554f * xy) * z;
+  Y[11] = (-0.4570457994644658f * y) * ((4.0f * zz - xx) - yy);
+  Y[12] = (0.3731763325901154f * z) * ((2.0f * zz - 3.0f * xx) - 3.0f * yy);
+  Y[13] = (-0.4570457994644658f * x) * ((4.0f * zz - xx) - yy);
+  Y[14] = (1.445305721320277f * z) * (xx - yy);
+  Y[15] = (-0.5900435899266435f * x) * (xx - 3.0f * yy);
+  float col[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float c = Y[0] * v[ch];
+#pragma unroll
+    for (int k = 1; k < 16; ++k) c = c + Y[k] * v[3 * k + ch];
+    c = c + 0.5f;
+    col[ch] = c < 0.0f ? 0.0f : c;
+  }
+  float* rp = reinterpret_cast<float*>(a.recs + f);
+  rp[6] = col[0];
+  rp[7] = col[1];
+  rp[8] = col[2];
+}
+
 }  // namespace
 
 void launch_gate_count(const ProjectArgs& a, cudaStream_t s) {
@@ -240,6 +266,13 @@ void launch_project(const ProjectArgs& a, cudaStream_t s) {
   if (a.n <= 0) return;
   const int64_t blocks = (a.n + 255) / 256;
   k_project<<<unsigned(blocks), 256, 0, s>>>(a);
+}
+
+void launch_color(const ProjectArgs& a, cudaStream_t s) {
+  if (a.n <= 0 || a.no_color) return;
+  int64_t blocks = (a.n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_color<<<unsigned(blocks), 256, 0, s>>>(a);
 }
 
 }  // namespace bgs

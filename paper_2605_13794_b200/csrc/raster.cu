@@ -8,10 +8,20 @@
 // the splat contributed (R15), accumulated as u64 fixed point 2^-24 (D5) with one warp
 // reduction (__reduce_add_sync) and one atomic per (warp, splat).
 //
-// Launch: one 256-thread CTA per owned 16x16 tile (one thread per pixel).  Records of the
-// tile's sorted list are staged 256 at a time into shared memory (one record per thread,
-// 128-bit loads), the block exits when all 256 pixels are done (__syncthreads_count) and a
+// Launch: one 256-thread CTA per owned 16x16 tile; warp w owns pixel rows 2w, 2w+1 of the tile
+// (a 16x2 strip).  Records of the tile's sorted list are staged 256 at a time into shared
+// memory (one record per thread, 128-bit loads).  At staging each record also gets the exact
+// bounding box of its alpha >= 1/255 ellipse {d : d^T Q d <= -2 thr} (half extents
+// sqrt(-2 thr (Q^-1)_xx), sqrt(-2 thr (Q^-1)_yy), widened by 1e-3 relative + 0.01 px so it is
+// conservative under fp32 rounding); a warp whose strip misses the box skips the record with
+// a warp-uniform branch.  This changes no decision: every skipped pixel would fail the
+// power >= thr test.  The block exits when all 256 pixels are done (__syncthreads_count) and a
 // warp whose 32 pixels are done skips the batch (warp-ballot early termination).
+//
+// Backward: per (warp, record) the 9 partial gradients are reduced with a transposed butterfly
+// (8 values in 4+2+1+2 shuffles, each lane ending with one value; the 9th with 5 shuffles) and
+// issued as 9 parallel red.global.add.f32 from 9 lanes instead of 45 shuffles + 9 serial
+// atomics.
 //
 // The power expression is pinned with __fmul_rn/__fadd_rn (no FMA) so that the alpha-cut
 // decision, n_contrib and a are bit-identical to the oracle's.
@@ -24,16 +34,18 @@ constexpr int kBlock = kTile * kTile;
 
 struct __align__(16) Staged {
   float mx, my, A, B;
-  float C, o, thr, pad;
-  float r, g, b;
+  float C, o, thr, r;
+  float g, b;
   uint32_t ridx;
+  float pad;
+  float4 box;  // xmin, xmax, ymin, ymax of the alpha >= 1/255 ellipse
 };
 
-__device__ __forceinline__ float pinned_power(const Staged& s, float dx, float dy) {
+__device__ __forceinline__ float pinned_power(float A, float B, float C, float dx, float dy) {
   // (-0.5 * ((A*dx)*dx + (C*dy)*dy)) - (B*dx)*dy, every op rounded (no contraction)
-  const float t1 = __fmul_rn(__fmul_rn(s.A, dx), dx);
-  const float t2 = __fmul_rn(__fmul_rn(s.C, dy), dy);
-  const float t3 = __fmul_rn(__fmul_rn(s.B, dx), dy);
+  const float t1 = __fmul_rn(__fmul_rn(A, dx), dx);
+  const float t2 = __fmul_rn(__fmul_rn(C, dy), dy);
+  const float t3 = __fmul_rn(__fmul_rn(B, dx), dy);
   return __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
 }
 
@@ -51,24 +63,39 @@ __device__ __forceinline__ void stage(Staged* sm, const Rec* recv, uint32_t r) {
   s.g = q1.w;
   s.b = q2.x;
   s.thr = float(-log(255.0 * double(q1.y)));  // alpha >= 1/255  <=>  power >= thr
-  s.pad = 0.f;
   s.ridx = r;
+  s.pad = 0.f;
+  const float k = -2.0f * s.thr;
+  const float det = s.A * s.C - s.B * s.B;
+  if (k > 0.f && det > 0.f) {
+    const float hx = sqrtf(k * s.C / det) * 1.001f + 0.01f;
+    const float hy = sqrtf(k * s.A / det) * 1.001f + 0.01f;
+    s.box = make_float4(s.mx - hx, s.mx + hx, s.my - hy, s.my + hy);
+  } else {
+    s.box = make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never contributes
+  }
   *sm = s;
+}
+
+__device__ __forceinline__ bool box_hits(const float4& b, float x0, float x1, float y0, float y1) {
+  return b.x <= x1 && b.y >= x0 && b.z <= y1 && b.w >= y0;
 }
 
 template <bool kImportance>
 __global__ void __launch_bounds__(kBlock) k_raster_fwd(RasterArgs a, float* __restrict__ rgb,
                                                        float* __restrict__ t_final, int32_t* __restrict__ n_contrib) {
   __shared__ Staged s_rec[kBlock];
-  const uint32_t* __restrict__ vals = a.vals[a.pass_ctrl[kFinalSel]];
+  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
   const int lt = blockIdx.x;
   const int tile = a.t_begin + lt;
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid >> 4);
   const bool inside = px < a.W && py < a.H;
   const uint2 range = a.ranges[lt];
   const float pxf = float(px), pyf = float(py);
+  const float wx0 = float(tx * kTile), wx1 = wx0 + float(kTile - 1);
+  const float wy0 = float(ty * kTile + 2 * warp), wy1 = wy0 + 1.f;
   float T = 1.0f, cr = 0.f, cg = 0.f, cb = 0.f;
   uint32_t last = 0;
   bool done = !inside;
@@ -80,12 +107,13 @@ __global__ void __launch_bounds__(kBlock) k_raster_fwd(RasterArgs a, float* __re
     const int n = int(range.y - start < uint32_t(kBlock) ? range.y - start : uint32_t(kBlock));
     if (__all_sync(0xffffffffu, done)) continue;
     for (int j = 0; j < n; ++j) {
+      const Staged& s = s_rec[j];
+      if (!box_hits(s.box, wx0, wx1, wy0, wy1)) continue;  // warp-uniform
       bool contrib = false;
       uint32_t fixed = 0;
       if (!done) {
-        const Staged& s = s_rec[j];
         const float dx = s.mx - pxf, dy = s.my - pyf;
-        const float power = pinned_power(s, dx, dy);
+        const float power = pinned_power(s.A, s.B, s.C, dx, dy);
         if (power <= 0.0f && power >= s.thr) {
           const float G = __expf(power);
           const float alpha = fminf(0.99f, s.o * G);
@@ -109,7 +137,7 @@ __global__ void __launch_bounds__(kBlock) k_raster_fwd(RasterArgs a, float* __re
         if (m) {
           const uint32_t sum = __reduce_add_sync(0xffffffffu, fixed);
           if (lane == 0) {
-            Acc* acc = a.acc + s_rec[j].ridx;
+            Acc* acc = a.acc + s.ridx;
             atomicAdd(&acc->a, uint32_t(__popc(m)));
             atomicAdd(&acc->w, (unsigned long long)sum);
           }
@@ -127,25 +155,24 @@ __global__ void __launch_bounds__(kBlock) k_raster_fwd(RasterArgs a, float* __re
   }
 }
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
+__device__ __forceinline__ float xsel(bool hi, float a, float b) { return hi ? a : b; }
 
 __global__ void __launch_bounds__(kBlock) k_raster_bwd(RasterArgs a, const float* __restrict__ dL,
                                                        const float* __restrict__ t_final,
                                                        const int32_t* __restrict__ n_contrib) {
   __shared__ Staged s_rec[kBlock];
-  const uint32_t* __restrict__ vals = a.vals[a.pass_ctrl[kFinalSel]];
+  __shared__ uint32_t s_maxlast;
+  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
   const int lt = blockIdx.x;
   const int tile = a.t_begin + lt;
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid >> 4);
   const bool inside = px < a.W && py < a.H;
   const uint2 range = a.ranges[lt];
   const float pxf = float(px), pyf = float(py);
+  const float wx0 = float(tx * kTile), wx1 = wx0 + float(kTile - 1);
+  const float wy0 = float(ty * kTile + 2 * warp), wy1 = wy0 + 1.f;
   const size_t pix = size_t(py) * a.W + px, plane = size_t(a.W) * a.H;
   float T = 1.f, dr = 0.f, dg = 0.f, db = 0.f;
   uint32_t last = 0;
@@ -156,13 +183,16 @@ __global__ void __launch_bounds__(kBlock) k_raster_bwd(RasterArgs a, const float
     dg = dL[plane + pix];
     db = dL[2 * plane + pix];
   }
-  // the block's deepest contributor bounds the work
-  __shared__ uint32_t s_maxlast;
   if (tid == 0) s_maxlast = 0;
   __syncthreads();
-  atomicMax(&s_maxlast, last);
+  // the warp's / block's deepest contributor bounds the work
+  const uint32_t wlast = __reduce_max_sync(0xffffffffu, last);
+  if (lane == 0) atomicMax(&s_maxlast, wlast);
   __syncthreads();
   const uint32_t end = range.x + s_maxlast;
+  const uint32_t wend = range.x + wlast;
+  const bool hi16 = lane & 16, hi8 = lane & 8, hi4 = lane & 4;
+  const int my_idx = (hi16 ? 4 : 0) + (hi8 ? 2 : 0) + (hi4 ? 1 : 0);
   float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, last_alpha = 0.f, last_r = 0.f, last_g = 0.f, last_b = 0.f;
   for (int64_t bstart = int64_t(end) - kBlock; bstart > int64_t(range.x) - kBlock; bstart -= kBlock) {
     __syncthreads();
@@ -170,21 +200,24 @@ __global__ void __launch_bounds__(kBlock) k_raster_bwd(RasterArgs a, const float
     if (idx >= int64_t(range.x) && idx < int64_t(end)) stage(&s_rec[tid], a.recv, __ldg(vals + idx));
     __syncthreads();
     const int jlo = int(int64_t(range.x) - bstart > 0 ? int64_t(range.x) - bstart : 0);
-    for (int j = kBlock - 1; j >= jlo; --j) {
-      const int64_t pos = bstart + j;  // absolute position in the sorted list
-      if (pos >= int64_t(end)) continue;
+    const int jhi = int(int64_t(wend) - bstart < int64_t(kBlock) ? int64_t(wend) - bstart : int64_t(kBlock)) - 1;
+    for (int j = jhi; j >= jlo; --j) {
+      const Staged& s = s_rec[j];
+      if (!box_hits(s.box, wx0, wx1, wy0, wy1)) continue;  // warp-uniform
+      const uint32_t pos = uint32_t(bstart + j) - range.x;
       bool contrib = false;
       float g[9];
-      if (inside && uint32_t(pos - range.x) < last) {
-        const Staged& s = s_rec[j];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) g[k] = 0.f;
+      if (pos < last) {
         const float dx = s.mx - pxf, dy = s.my - pyf;
-        const float power = pinned_power(s, dx, dy);
+        const float power = pinned_power(s.A, s.B, s.C, dx, dy);
         if (power <= 0.0f && power >= s.thr) {
           contrib = true;
           const float G = __expf(power);
           const float og = s.o * G;
           const float alpha = fminf(0.99f, og);
-          T = T / (1.0f - alpha);
+          T = __fdividef(T, 1.0f - alpha);
           const float wgt = alpha * T;
           g[6] = wgt * dr;
           g[7] = wgt * dg;
@@ -197,10 +230,7 @@ __global__ void __launch_bounds__(kBlock) k_raster_bwd(RasterArgs a, const float
           last_g = s.g;
           last_b = s.b;
           const float dLda = T * ((s.r - acc_r) * dr + (s.g - acc_g) * dg + (s.b - acc_b) * db);
-          if (og > 0.99f) {
-#pragma unroll
-            for (int k = 0; k < 6; ++k) g[k] = 0.f;
-          } else {
+          if (og <= 0.99f) {  // clamped alpha is constant: true derivative 0 (R14)
             g[5] = G * dLda;
             const float dpow = G * s.o * dLda;
             g[0] = -dpow * (s.A * dx + s.B * dy);
@@ -211,19 +241,34 @@ __global__ void __launch_bounds__(kBlock) k_raster_bwd(RasterArgs a, const float
           }
         }
       }
-      const unsigned m = __ballot_sync(0xffffffffu, contrib);
-      if (m == 0) continue;
-      if (!contrib) {
+      if (!__any_sync(0xffffffffu, contrib)) continue;
+      // transposed butterfly over g[0..7]: lane ends with the warp sum of g[my_idx]
+      float v4[4], v2[2], v1;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) g[k] = 0.f;
+      for (int i = 0; i < 4; ++i) {
+        const float send = xsel(hi16, g[i], g[i + 4]);
+        const float keep = xsel(hi16, g[i + 4], g[i]);
+        v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
       }
 #pragma unroll
-      for (int k = 0; k < 9; ++k) g[k] = warp_sum(g[k]);
-      if (lane == 0) {
-        float* dst = a.acc[s_rec[j].ridx].g;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) atomicAdd(dst + k, g[k]);
+      for (int i = 0; i < 2; ++i) {
+        const float send = xsel(hi8, v4[i], v4[i + 2]);
+        const float keep = xsel(hi8, v4[i + 2], v4[i]);
+        v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
       }
+      {
+        const float send = xsel(hi4, v2[0], v2[1]);
+        const float keep = xsel(hi4, v2[1], v2[0]);
+        v1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+      float v8 = g[8];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, o);
+      float* dst = a.acc[s.ridx].g;
+      if ((lane & 3) == 0) atomicAdd(dst + my_idx, v1);
+      if (lane == 1) atomicAdd(dst + 8, v8);
     }
   }
 }

@@ -505,6 +505,10 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
   if (a.n > 0) {
     launch_project(a, s);
     CKS(launched(ctx));
+    if (!a.no_color) {
+      launch_color(a, s);
+      CKS(launched(ctx));
+    }
   }
   CK(cudaMemcpyAsync(ctx->h_counters, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
                      cudaMemcpyDeviceToHost, s));

@@ -167,10 +167,10 @@ __global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int
 
   if (a.pass_ctrl[kCtrlActive + pass] == 0) return;
   const uint32_t sel = a.pass_ctrl[kCtrlSel + pass];
-  const unsigned long long* __restrict__ kin = a.keys[sel];
-  const uint32_t* __restrict__ vin = a.vals[sel];
-  unsigned long long* __restrict__ kout = a.keys[sel ^ 1u];
-  uint32_t* __restrict__ vout = a.vals[sel ^ 1u];
+  const unsigned long long* __restrict__ kin = sel ? a.keys[1] : a.keys[0];
+  const uint32_t* __restrict__ vin = sel ? a.vals[1] : a.vals[0];
+  unsigned long long* __restrict__ kout = sel ? a.keys[0] : a.keys[1];
+  uint32_t* __restrict__ vout = sel ? a.vals[0] : a.vals[1];
   const int shift = 8 * pass;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
@@ -278,8 +278,8 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const uint32_t sel = a.pass_ctrl[kFinalSel];
-  const unsigned long long* keys = a.keys[sel];
-  uint32_t* vals = a.vals[sel];
+  const unsigned long long* keys = sel ? a.keys[1] : a.keys[0];
+  uint32_t* vals = sel ? a.vals[1] : a.vals[0];
   const unsigned long long k = keys[i];
   const uint32_t t = uint32_t(k >> 31);
   const unsigned long long kp = i > 0 ? keys[i - 1] : ~0ull;
