@@ -35,10 +35,10 @@ static_assert(sizeof(Acc) == 48, "accumulator is 48 B");
 
 // Device counters (u64 each) in the ctx arena.
 enum Counter : int {
-  C_F = 0,        // records produced by project
+  C_F = 0,        // packed: (records produced by project << 32) | |A^(m)|
   C_PALL = 1,     // sum of rect areas (pairs over all tiles) of this rank's records
   C_NLOD = 2,     // |L^(m)|
-  C_NACT = 3,     // |A^(m)|
+  C_NACT = 3,     // unused (|A^(m)| lives in the low half of C_F)
   C_P = 4,        // pairs emitted for owned tiles
   C_NCOUNTERS = 8
 };

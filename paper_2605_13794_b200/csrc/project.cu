@@ -40,9 +40,14 @@ __global__ void __launch_bounds__(256) k_gate_count(ProjectArgs a) {
   if (threadIdx.x == 0 && c) atomicAdd(a.counters + C_NLOD, (unsigned long long)c);
 }
 
-__global__ void __launch_bounds__(256, 6) k_project(ProjectArgs a) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
+struct ProjOut {
+  float mx, my, A, B, C, depth, opac;
+  uint32_t rect, area;
+  bool valid, active;
+  int x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ ProjOut project_one(const ProjectArgs& a, int64_t i) {
   bool valid = false;
   bool active = false;
   float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, depth = 0.f, opac = 0.f;
@@ -157,40 +162,121 @@ __global__ void __launch_bounds__(256, 6) k_project(ProjectArgs a) {
     }
     a.radius[i] = valid ? radius : 0;
   }
-  // ---- warp-aggregated append of the record (one atomic per warp)
-  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-  const unsigned amask = __ballot_sync(0xffffffffu, active);
-  const unsigned long long wsum = __reduce_add_sync(0xffffffffu, area);  // P_all contribution
-  if (vmask) {
-    const int leader = __ffs(vmask) - 1;
-    unsigned long long base = 0;
-    if (lane == leader) {
-      base = atomicAdd(a.counters + C_F, (unsigned long long)__popc(vmask));
-      atomicAdd(a.counters + C_PALL, wsum);
+  ProjOut o;
+  o.mx = mx;
+  o.my = my;
+  o.A = cA;
+  o.B = cB;
+  o.C = cC;
+  o.depth = depth;
+  o.opac = opac;
+  o.rect = uint32_t(x0) | (uint32_t(y0) << 8) | (uint32_t(x1) << 16) | (uint32_t(y1) << 24);
+  o.area = area;
+  o.valid = valid;
+  o.active = active;
+  o.x0 = x0;
+  o.y0 = y0;
+  o.x1 = x1;
+  o.y1 = y1;
+  return o;
+}
+
+// Block-level compaction: a CTA projects kProjChunk consecutive Gaussians, assigns its records
+// block-local slots with a deterministic scan (item round, warp, lane), stages them in shared
+// memory, takes ONE global slot range (a single 64-bit atomic packing F and |A|, plus one for
+// P_all) and writes the records out coalesced.  Per-warp global atomics on one counter were
+// the bottleneck (hundreds of thousands of same-address atomics serialise at the L2).
+constexpr int kProjPer = 2;
+constexpr int kProjChunk = 256 * kProjPer;
+
+__global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
+  __shared__ float4 s_rec[kProjChunk * 3];
+  __shared__ uint32_t s_lidx[kProjChunk];
+  __shared__ uint32_t s_cnt[kProjPer * 8];
+  __shared__ uint32_t s_act[8];
+  __shared__ unsigned long long s_area[8];
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t chunk0 = int64_t(blockIdx.x) * kProjChunk;
+  ProjOut o[kProjPer];
+  uint32_t nact = 0;
+  unsigned long long area = 0;
+#pragma unroll
+  for (int k = 0; k < kProjPer; ++k) {
+    const int64_t i = chunk0 + k * 256 + tid;
+    if (i < a.n) {
+      o[k] = project_one(a, i);
+    } else {
+      o[k].valid = false;
+      o[k].active = false;
+      o[k].area = 0;
     }
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (valid) {
-      const unsigned long long slot = base + __popc(vmask & ((1u << lane) - 1u));
-      if ((int64_t)slot < a.rec_cap) {
-        const uint32_t gid = uint32_t(i) * uint32_t(a.world) + uint32_t(a.rank);
-        const uint32_t rect = uint32_t(x0) | (uint32_t(y0) << 8) | (uint32_t(x1) << 16) | (uint32_t(y1) << 24);
-        float4* dst = reinterpret_cast<float4*>(a.recs + slot);
-        dst[0] = make_float4(mx, my, cA, cB);
-        dst[1] = make_float4(cC, opac, 0.f, 0.f);
-        dst[2] = make_float4(0.f, depth, __uint_as_float(gid), __uint_as_float(rect));
-        a.rec_lidx[slot] = uint32_t(i);
-      }
-      if (a.tile_diff) {
-        // 2D difference array of rect coverage -> per-tile pair counts (a3 input)
-        const int W1 = a.cam.TX + 1;
-        atomicAdd(a.tile_diff + y0 * W1 + x0, 1);
-        atomicAdd(a.tile_diff + y0 * W1 + x1, -1);
-        atomicAdd(a.tile_diff + y1 * W1 + x0, -1);
-        atomicAdd(a.tile_diff + y1 * W1 + x1, 1);
-      }
+    nact += o[k].active ? 1u : 0u;
+    area += o[k].area;
+  }
+  uint32_t rank_in_warp[kProjPer];
+#pragma unroll
+  for (int k = 0; k < kProjPer; ++k) {
+    const unsigned m = __ballot_sync(0xffffffffu, o[k].valid);
+    rank_in_warp[k] = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) s_cnt[k * 8 + warp] = __popc(m);
+  }
+  const uint32_t wact = __reduce_add_sync(0xffffffffu, nact);
+  unsigned long long warea = area;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) warea += __shfl_xor_sync(0xffffffffu, warea, off);
+  if (lane == 0) {
+    s_act[warp] = wact;
+    s_area[warp] = warea;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t run = 0, act = 0;
+    unsigned long long ar = 0;
+    for (int j = 0; j < kProjPer * 8; ++j) {
+      const uint32_t c = s_cnt[j];
+      s_cnt[j] = run;
+      run += c;
+    }
+    for (int w = 0; w < 8; ++w) {
+      act += s_act[w];
+      ar += s_area[w];
+    }
+    s_total = run;
+    unsigned long long base = 0;
+    if (run || act) base = atomicAdd(a.counters + C_F, ((unsigned long long)run << 32) | act) >> 32;
+    if (ar) atomicAdd(a.counters + C_PALL, ar);
+    s_base = base;
+  }
+  __syncthreads();
+  const unsigned long long base = s_base;
+#pragma unroll
+  for (int k = 0; k < kProjPer; ++k) {
+    if (!o[k].valid) continue;
+    const uint32_t ls = s_cnt[k * 8 + warp] + rank_in_warp[k];
+    const int64_t i = chunk0 + k * 256 + tid;
+    const uint32_t gid = uint32_t(i) * uint32_t(a.world) + uint32_t(a.rank);
+    s_rec[3 * ls + 0] = make_float4(o[k].mx, o[k].my, o[k].A, o[k].B);
+    s_rec[3 * ls + 1] = make_float4(o[k].C, o[k].opac, 0.f, 0.f);
+    s_rec[3 * ls + 2] = make_float4(0.f, o[k].depth, __uint_as_float(gid), __uint_as_float(o[k].rect));
+    s_lidx[ls] = uint32_t(i);
+    if (a.tile_diff) {
+      // 2D difference array of rect coverage -> per-tile pair counts (a3 input)
+      const int W1 = a.cam.TX + 1;
+      atomicAdd(a.tile_diff + o[k].y0 * W1 + o[k].x0, 1);
+      atomicAdd(a.tile_diff + o[k].y0 * W1 + o[k].x1, -1);
+      atomicAdd(a.tile_diff + o[k].y1 * W1 + o[k].x0, -1);
+      atomicAdd(a.tile_diff + o[k].y1 * W1 + o[k].x1, 1);
     }
   }
-  if (amask && lane == __ffs(amask) - 1) atomicAdd(a.counters + C_NACT, (unsigned long long)__popc(amask));
+  __syncthreads();
+  const uint32_t total = s_total;
+  float4* dst = reinterpret_cast<float4*>(a.recs + base);
+  for (uint32_t j = tid; j < 3 * total; j += 256)
+    if (base + j / 3 < (unsigned long long)a.rec_cap) dst[j] = s_rec[j];
+  for (uint32_t j = tid; j < total; j += 256)
+    if (base + j < (unsigned long long)a.rec_cap) a.rec_lidx[base + j] = s_lidx[j];
 }
 
 __device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f);
@@ -199,7 +285,7 @@ __device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f) { col
 // SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2.
 // Persistent grid-stride over the F records (F read on the device: no host round trip).
 __global__ void __launch_bounds__(256) k_color(ProjectArgs a) {
-  const int64_t F = int64_t(*((volatile unsigned long long*)(a.counters + C_F)));
+  const int64_t F = int64_t(*((volatile unsigned long long*)(a.counters + C_F)) >> 32);
   for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < F; f += int64_t(gridDim.x) * blockDim.x)
     color_one(a, f);
 }
@@ -264,7 +350,7 @@ void launch_gate_count(const ProjectArgs& a, cudaStream_t s) {
 
 void launch_project(const ProjectArgs& a, cudaStream_t s) {
   if (a.n <= 0) return;
-  const int64_t blocks = (a.n + 255) / 256;
+  const int64_t blocks = (a.n + kProjChunk - 1) / kProjChunk;
   k_project<<<unsigned(blocks), 256, 0, s>>>(a);
 }
 

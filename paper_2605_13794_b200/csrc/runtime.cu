@@ -513,10 +513,10 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
   CK(cudaMemcpyAsync(ctx->h_counters, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
                      cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  ctx->F = int64_t(ctx->h_counters[C_F]);
+  ctx->F = int64_t(ctx->h_counters[C_F] >> 32);  // packed (F << 32) | |A|
+  ctx->n_act = int64_t(ctx->h_counters[C_F] & 0xffffffffull);
   ctx->P_all = int64_t(ctx->h_counters[C_PALL]);
   ctx->n_lod = a.gate_enabled ? int64_t(ctx->h_counters[C_NLOD]) : g->n_local;
-  ctx->n_act = int64_t(ctx->h_counters[C_NACT]);
   ctx->fallback = a.gate_enabled ? int((unsigned long long)a.fb_den * ctx->h_counters[C_NLOD] >
                                        (unsigned long long)a.fb_num * (unsigned long long)g->n_local)
                                  : 1;

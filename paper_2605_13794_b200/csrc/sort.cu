@@ -69,9 +69,23 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
   }
   const uint32_t total_area = __shfl_sync(0xffffffffu, incl, 31);
   const uint32_t total_own = __shfl_sync(0xffffffffu, oincl, 31);
-  unsigned long long base = 0;
-  if (lane == 0 && total_own) base = atomicAdd(a.counters + C_P, (unsigned long long)total_own);
-  base = __shfl_sync(0xffffffffu, base, 0);
+  // one global atomic per CTA (warp totals scanned in shared memory)
+  __shared__ uint32_t s_wown[8];
+  __shared__ unsigned long long s_bbase;
+  const int warp = threadIdx.x >> 5;
+  if (lane == 0) s_wown[warp] = total_own;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t c = s_wown[w];
+      s_wown[w] = run;
+      run += c;
+    }
+    s_bbase = run ? atomicAdd(a.counters + C_P, (unsigned long long)run) : 0ull;
+  }
+  __syncthreads();
+  const unsigned long long base = s_bbase + s_wown[warp];
   const int npass = a.n_passes;
   uint32_t run = 0;
   for (uint32_t chunk = 0; chunk < total_area; chunk += 32) {
