@@ -9,14 +9,15 @@
 // reduction (__reduce_add_sync) and one atomic per (warp, splat).
 //
 // Launch: one 256-thread CTA per owned 16x16 tile; warp w owns pixel rows 2w, 2w+1 of the tile
-// (a 16x2 strip).  Records of the tile's sorted list are staged 256 at a time into shared
-// memory (one record per thread, 128-bit loads).  At staging each record also gets the exact
-// bounding box of its alpha >= 1/255 ellipse {d : d^T Q d <= -2 thr} (half extents
+// (a 16x2 strip).  The tile's sorted list is staged kBatch = 512 records at a time into shared
+// memory (structure of arrays, two records per thread, 128-bit loads).  Each staged record also
+// gets the exact bounding box of its alpha >= 1/255 ellipse {d : d^T Q d <= -2 thr} (half extents
 // sqrt(-2 thr (Q^-1)_xx), sqrt(-2 thr (Q^-1)_yy), widened by 1e-3 relative + 0.01 px so it is
-// conservative under fp32 rounding); a warp whose strip misses the box skips the record with
-// a warp-uniform branch.  This changes no decision: every skipped pixel would fail the
-// power >= thr test.  The block exits when all 256 pixels are done (__syncthreads_count) and a
-// warp whose 32 pixels are done skips the batch (warp-ballot early termination).
+// conservative under fp32 rounding).  Each warp tests 32 staged boxes at once against its strip
+// (one per lane), ballots a hit mask and walks only the set bits, so records that cannot touch
+// the strip cost nothing.  This changes no decision: every skipped pixel would fail the
+// power >= thr test.  The CTA stops when all 256 pixels are done (__syncthreads_count once per
+// 512 records) and a warp whose 32 pixels are done skips the batch (warp-ballot termination).
 //
 // Backward: per (warp, record) the 9 partial gradients are reduced with a transposed butterfly
 // (8 values in 4+2+1+2 shuffles, each lane ending with one value; the 9th with 5 shuffles) and
@@ -31,14 +32,13 @@ namespace bgs {
 namespace {
 
 constexpr int kBlock = kTile * kTile;
+constexpr int kBatch = 512;
 
-struct __align__(16) Staged {
-  float mx, my, A, B;
-  float C, o, thr, r;
-  float g, b;
-  uint32_t ridx;
-  float pad;
-  float4 box;  // xmin, xmax, ymin, ymax of the alpha >= 1/255 ellipse
+struct Stage {
+  float4 geo[kBatch];  // mx, my, A, B
+  float4 co[kBatch];   // C, o, thr, ridx (bits)
+  float4 rgb[kBatch];  // r, g, b, -
+  float4 box[kBatch];  // xmin, xmax, ymin, ymax of the alpha >= 1/255 ellipse
 };
 
 __device__ __forceinline__ float pinned_power(float A, float B, float C, float dx, float dy) {
@@ -49,42 +49,32 @@ __device__ __forceinline__ float pinned_power(float A, float B, float C, float d
   return __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
 }
 
-__device__ __forceinline__ void stage(Staged* sm, const Rec* recv, uint32_t r) {
+__device__ __forceinline__ void stage(Stage& sm, int slot, const Rec* recv, uint32_t r) {
   const float4* p = reinterpret_cast<const float4*>(recv + r);
   const float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
-  Staged s;
-  s.mx = q0.x;
-  s.my = q0.y;
-  s.A = q0.z;
-  s.B = q0.w;
-  s.C = q1.x;
-  s.o = q1.y;
-  s.r = q1.z;
-  s.g = q1.w;
-  s.b = q2.x;
-  s.thr = float(-log(255.0 * double(q1.y)));  // alpha >= 1/255  <=>  power >= thr
-  s.ridx = r;
-  s.pad = 0.f;
-  const float k = -2.0f * s.thr;
-  const float det = s.A * s.C - s.B * s.B;
+  const float thr = float(-log(255.0 * double(q1.y)));  // alpha >= 1/255  <=>  power >= thr
+  sm.geo[slot] = q0;
+  sm.co[slot] = make_float4(q1.x, q1.y, thr, __uint_as_float(r));
+  sm.rgb[slot] = make_float4(q1.z, q1.w, q2.x, 0.f);
+  const float k = -2.0f * thr;
+  const float det = q0.z * q1.x - q0.w * q0.w;
   if (k > 0.f && det > 0.f) {
-    const float hx = sqrtf(k * s.C / det) * 1.001f + 0.01f;
-    const float hy = sqrtf(k * s.A / det) * 1.001f + 0.01f;
-    s.box = make_float4(s.mx - hx, s.mx + hx, s.my - hy, s.my + hy);
+    const float hx = sqrtf(k * q1.x / det) * 1.001f + 0.01f;
+    const float hy = sqrtf(k * q0.z / det) * 1.001f + 0.01f;
+    sm.box[slot] = make_float4(q0.x - hx, q0.x + hx, q0.y - hy, q0.y + hy);
   } else {
-    s.box = make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never contributes
+    sm.box[slot] = make_float4(1e30f, -1e30f, 1e30f, -1e30f);  // never contributes
   }
-  *sm = s;
 }
 
 __device__ __forceinline__ bool box_hits(const float4& b, float x0, float x1, float y0, float y1) {
-  return b.x <= x1 && b.y >= x0 && b.z <= y1 && b.w >= y0;
+  return (b.x <= x1) & (b.y >= x0) & (b.z <= y1) & (b.w >= y0);
 }
 
 template <bool kImportance>
 __global__ void __launch_bounds__(kBlock) k_raster_fwd(RasterArgs a, float* __restrict__ rgb,
                                                        float* __restrict__ t_final, int32_t* __restrict__ n_contrib) {
-  __shared__ Staged s_rec[kBlock];
+  __shared__ Stage sm;
   const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
   const int lt = blockIdx.x;
   const int tile = a.t_begin + lt;
@@ -99,50 +89,57 @@ __global__ void __launch_bounds__(kBlock) k_raster_fwd(RasterArgs a, float* __re
   float T = 1.0f, cr = 0.f, cg = 0.f, cb = 0.f;
   uint32_t last = 0;
   bool done = !inside;
-  for (uint32_t start = range.x; start < range.y; start += kBlock) {
+  for (uint32_t start = range.x; start < range.y; start += kBatch) {
     if (__syncthreads_count(done) == kBlock) break;
-    const uint32_t idx = start + tid;
-    if (idx < range.y) stage(&s_rec[tid], a.recv, __ldg(vals + idx));
+    const int n = int(range.y - start < uint32_t(kBatch) ? range.y - start : uint32_t(kBatch));
+    for (int s = tid; s < n; s += kBlock) stage(sm, s, a.recv, __ldg(vals + start + s));
     __syncthreads();
-    const int n = int(range.y - start < uint32_t(kBlock) ? range.y - start : uint32_t(kBlock));
     if (__all_sync(0xffffffffu, done)) continue;
-    for (int j = 0; j < n; ++j) {
-      const Staged& s = s_rec[j];
-      if (!box_hits(s.box, wx0, wx1, wy0, wy1)) continue;  // warp-uniform
-      bool contrib = false;
-      uint32_t fixed = 0;
-      if (!done) {
-        const float dx = s.mx - pxf, dy = s.my - pyf;
-        const float power = pinned_power(s.A, s.B, s.C, dx, dy);
-        if (power <= 0.0f && power >= s.thr) {
-          const float G = __expf(power);
-          const float alpha = fminf(0.99f, s.o * G);
-          const float test_T = T * (1.0f - alpha);
-          if (test_T < 0.0001f) {
-            done = true;
-          } else {
-            const float wgt = alpha * T;
-            cr += s.r * wgt;
-            cg += s.g * wgt;
-            cb += s.b * wgt;
-            T = test_T;
-            last = start + j + 1 - range.x;
-            contrib = true;
-            if (kImportance) fixed = __float2uint_rn(wgt * 16777216.0f);
+    for (int w0 = 0; w0 < n; w0 += 32) {
+      const int jl = w0 + lane;
+      unsigned m = __ballot_sync(0xffffffffu, jl < n && box_hits(sm.box[jl], wx0, wx1, wy0, wy1));
+      while (m) {
+        const int j = w0 + __ffs(m) - 1;
+        m &= m - 1;
+        const float4 geo = sm.geo[j];
+        const float4 co = sm.co[j];
+        bool contrib = false;
+        uint32_t fixed = 0;
+        if (!done) {
+          const float dx = geo.x - pxf, dy = geo.y - pyf;
+          const float power = pinned_power(geo.z, geo.w, co.x, dx, dy);
+          if (power <= 0.0f && power >= co.z) {
+            const float G = __expf(power);
+            const float alpha = fminf(0.99f, co.y * G);
+            const float test_T = T * (1.0f - alpha);
+            if (test_T < 0.0001f) {
+              done = true;
+            } else {
+              const float4 c = sm.rgb[j];
+              const float wgt = alpha * T;
+              cr += c.x * wgt;
+              cg += c.y * wgt;
+              cb += c.z * wgt;
+              T = test_T;
+              last = start + j + 1 - range.x;
+              contrib = true;
+              if (kImportance) fixed = __float2uint_rn(wgt * 16777216.0f);
+            }
+          }
+        }
+        if (kImportance) {
+          const unsigned cm = __ballot_sync(0xffffffffu, contrib);
+          if (cm) {
+            const uint32_t sum = __reduce_add_sync(0xffffffffu, fixed);
+            if (lane == 0) {
+              Acc* acc = a.acc + __float_as_uint(co.w);
+              atomicAdd(&acc->a, uint32_t(__popc(cm)));
+              atomicAdd(&acc->w, (unsigned long long)sum);
+            }
           }
         }
       }
-      if (kImportance) {
-        const unsigned m = __ballot_sync(0xffffffffu, contrib);
-        if (m) {
-          const uint32_t sum = __reduce_add_sync(0xffffffffu, fixed);
-          if (lane == 0) {
-            Acc* acc = a.acc + s.ridx;
-            atomicAdd(&acc->a, uint32_t(__popc(m)));
-            atomicAdd(&acc->w, (unsigned long long)sum);
-          }
-        }
-      }
+      if (__all_sync(0xffffffffu, done)) break;
     }
   }
   if (inside) {
@@ -160,7 +157,7 @@ __device__ __forceinline__ float xsel(bool hi, float a, float b) { return hi ? a
 __global__ void __launch_bounds__(kBlock) k_raster_bwd(RasterArgs a, const float* __restrict__ dL,
                                                        const float* __restrict__ t_final,
                                                        const int32_t* __restrict__ n_contrib) {
-  __shared__ Staged s_rec[kBlock];
+  __shared__ Stage sm;
   __shared__ uint32_t s_maxlast;
   const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
   const int lt = blockIdx.x;
@@ -194,81 +191,89 @@ __global__ void __launch_bounds__(kBlock) k_raster_bwd(RasterArgs a, const float
   const bool hi16 = lane & 16, hi8 = lane & 8, hi4 = lane & 4;
   const int my_idx = (hi16 ? 4 : 0) + (hi8 ? 2 : 0) + (hi4 ? 1 : 0);
   float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, last_alpha = 0.f, last_r = 0.f, last_g = 0.f, last_b = 0.f;
-  for (int64_t bstart = int64_t(end) - kBlock; bstart > int64_t(range.x) - kBlock; bstart -= kBlock) {
-    __syncthreads();
-    const int64_t idx = bstart + tid;
-    if (idx >= int64_t(range.x) && idx < int64_t(end)) stage(&s_rec[tid], a.recv, __ldg(vals + idx));
+  for (int64_t bstart = int64_t(end) - kBatch; bstart > int64_t(range.x) - kBatch; bstart -= kBatch) {
     __syncthreads();
     const int jlo = int(int64_t(range.x) - bstart > 0 ? int64_t(range.x) - bstart : 0);
-    const int jhi = int(int64_t(wend) - bstart < int64_t(kBlock) ? int64_t(wend) - bstart : int64_t(kBlock)) - 1;
-    for (int j = jhi; j >= jlo; --j) {
-      const Staged& s = s_rec[j];
-      if (!box_hits(s.box, wx0, wx1, wy0, wy1)) continue;  // warp-uniform
-      const uint32_t pos = uint32_t(bstart + j) - range.x;
-      bool contrib = false;
-      float g[9];
+    for (int s = jlo + tid; s < kBatch; s += kBlock) stage(sm, s, a.recv, __ldg(vals + bstart + s));
+    __syncthreads();
+    // this warp only needs positions < wend
+    const int jhi = int(int64_t(wend) - bstart < int64_t(kBatch) ? int64_t(wend) - bstart : int64_t(kBatch));
+    for (int w0 = ((jhi - 1) & ~31); w0 >= (jlo & ~31) && jhi > jlo; w0 -= 32) {
+      const int jl = w0 + lane;
+      unsigned m = __ballot_sync(0xffffffffu, jl >= jlo && jl < jhi && box_hits(sm.box[jl], wx0, wx1, wy0, wy1));
+      while (m) {
+        const int b = 31 - __clz(m);
+        m &= ~(1u << b);
+        const int j = w0 + b;
+        const uint32_t pos = uint32_t(bstart + j) - range.x;
+        const float4 geo = sm.geo[j];
+        const float4 co = sm.co[j];
+        bool contrib = false;
+        float g[9];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) g[k] = 0.f;
-      if (pos < last) {
-        const float dx = s.mx - pxf, dy = s.my - pyf;
-        const float power = pinned_power(s.A, s.B, s.C, dx, dy);
-        if (power <= 0.0f && power >= s.thr) {
-          contrib = true;
-          const float G = __expf(power);
-          const float og = s.o * G;
-          const float alpha = fminf(0.99f, og);
-          T = __fdividef(T, 1.0f - alpha);
-          const float wgt = alpha * T;
-          g[6] = wgt * dr;
-          g[7] = wgt * dg;
-          g[8] = wgt * db;
-          acc_r = last_alpha * last_r + (1.f - last_alpha) * acc_r;
-          acc_g = last_alpha * last_g + (1.f - last_alpha) * acc_g;
-          acc_b = last_alpha * last_b + (1.f - last_alpha) * acc_b;
-          last_alpha = alpha;
-          last_r = s.r;
-          last_g = s.g;
-          last_b = s.b;
-          const float dLda = T * ((s.r - acc_r) * dr + (s.g - acc_g) * dg + (s.b - acc_b) * db);
-          if (og <= 0.99f) {  // clamped alpha is constant: true derivative 0 (R14)
-            g[5] = G * dLda;
-            const float dpow = G * s.o * dLda;
-            g[0] = -dpow * (s.A * dx + s.B * dy);
-            g[1] = -dpow * (s.C * dy + s.B * dx);
-            g[2] = -0.5f * dpow * dx * dx;
-            g[3] = -dpow * dx * dy;
-            g[4] = -0.5f * dpow * dy * dy;
+        for (int k = 0; k < 9; ++k) g[k] = 0.f;
+        if (pos < last) {
+          const float dx = geo.x - pxf, dy = geo.y - pyf;
+          const float power = pinned_power(geo.z, geo.w, co.x, dx, dy);
+          if (power <= 0.0f && power >= co.z) {
+            contrib = true;
+            const float4 c = sm.rgb[j];
+            const float G = __expf(power);
+            const float og = co.y * G;
+            const float alpha = fminf(0.99f, og);
+            T = __fdividef(T, 1.0f - alpha);
+            const float wgt = alpha * T;
+            g[6] = wgt * dr;
+            g[7] = wgt * dg;
+            g[8] = wgt * db;
+            acc_r = last_alpha * last_r + (1.f - last_alpha) * acc_r;
+            acc_g = last_alpha * last_g + (1.f - last_alpha) * acc_g;
+            acc_b = last_alpha * last_b + (1.f - last_alpha) * acc_b;
+            last_alpha = alpha;
+            last_r = c.x;
+            last_g = c.y;
+            last_b = c.z;
+            const float dLda = T * ((c.x - acc_r) * dr + (c.y - acc_g) * dg + (c.z - acc_b) * db);
+            if (og <= 0.99f) {  // clamped alpha is constant: true derivative 0 (R14)
+              g[5] = G * dLda;
+              const float dpow = G * co.y * dLda;
+              g[0] = -dpow * (geo.z * dx + geo.w * dy);
+              g[1] = -dpow * (co.x * dy + geo.w * dx);
+              g[2] = -0.5f * dpow * dx * dx;
+              g[3] = -dpow * dx * dy;
+              g[4] = -0.5f * dpow * dy * dy;
+            }
           }
         }
-      }
-      if (!__any_sync(0xffffffffu, contrib)) continue;
-      // transposed butterfly over g[0..7]: lane ends with the warp sum of g[my_idx]
-      float v4[4], v2[2], v1;
+        if (!__any_sync(0xffffffffu, contrib)) continue;
+        // transposed butterfly over g[0..7]: lane ends with the warp sum of g[my_idx]
+        float v4[4], v2[2], v1;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float send = xsel(hi16, g[i], g[i + 4]);
-        const float keep = xsel(hi16, g[i + 4], g[i]);
-        v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
+        for (int i = 0; i < 4; ++i) {
+          const float send = xsel(hi16, g[i], g[i + 4]);
+          const float keep = xsel(hi16, g[i + 4], g[i]);
+          v4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const float send = xsel(hi8, v4[i], v4[i + 2]);
-        const float keep = xsel(hi8, v4[i + 2], v4[i]);
-        v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      {
-        const float send = xsel(hi4, v2[0], v2[1]);
-        const float keep = xsel(hi4, v2[1], v2[0]);
-        v1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
-      v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
-      float v8 = g[8];
+        for (int i = 0; i < 2; ++i) {
+          const float send = xsel(hi8, v4[i], v4[i + 2]);
+          const float keep = xsel(hi8, v4[i + 2], v4[i]);
+          v2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        {
+          const float send = xsel(hi4, v2[0], v2[1]);
+          const float keep = xsel(hi4, v2[1], v2[0]);
+          v1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+        float v8 = g[8];
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, o);
-      float* dst = a.acc[s.ridx].g;
-      if ((lane & 3) == 0) atomicAdd(dst + my_idx, v1);
-      if (lane == 1) atomicAdd(dst + 8, v8);
+        for (int o = 16; o >= 1; o >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, o);
+        float* dst = a.acc[__float_as_uint(co.w)].g;
+        if ((lane & 3) == 0) atomicAdd(dst + my_idx, v1);
+        if (lane == 1) atomicAdd(dst + 8, v8);
+      }
     }
   }
 }
