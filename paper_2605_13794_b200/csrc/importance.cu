@@ -9,13 +9,22 @@
 // Selection = exact distributed radix select on the u64 fixed-point w (D5): 7 rounds of
 // 8-bit digits from bit 55 down; per round every rank builds a 256-bin (count, mass)
 // histogram of the candidates that still match the selected high digits, the histograms are
-// summed over ranks (all-reduce), and a one-CTA kernel picks the digit where the cumulative
-// mass from the top crosses the target.  After the last round the threshold value tau is
-// exact; the number k of ties (w == tau) that must be included is closed form, and when
-// 0 < k < #ties a count-only radix select over global ids (4 rounds) finds the k smallest
-// ids.  Every decision is integer, so the result is bit-exact and independent of M.
-// All state stays on the device: no host round trip.
+// summed over ranks (all-reduce), and the digit where the cumulative mass from the top
+// crosses the target is picked.  After the last round the threshold value tau is exact; the
+// number k of ties (w == tau) to include is closed form, and when 0 < k < #ties a count-only
+// radix select over global ids (4 rounds) finds the k smallest ids.  Every decision is
+// integer, so the result is bit-exact and independent of M.
+//
+// world > 1: one kernel per histogram / decision (the all-reduce sits between them, stream
+// ordered, no host round trip).  world == 1: ONE cooperative kernel runs every round with
+// grid-wide barriers; each CTA recomputes the (identical) decision from the global histogram
+// so a round costs one grid barrier.  Histograms are warp-aggregated (__match_any_sync +
+// __reduce_add_sync on three 24-bit limbs of w) before the shared-memory atomics.
+#include <cooperative_groups.h>
+
 #include "bgs_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace bgs {
 
@@ -63,51 +72,53 @@ __device__ __forceinline__ Item load_item(const ImportanceArgs& a, int64_t t) {
   return it;
 }
 
+__device__ __forceinline__ unsigned long long load_w(const ImportanceArgs& a, int64_t t) {
+  return a.item_lidx ? a.acc[t].w : a.w_dense[t];
+}
+
 __device__ __forceinline__ uint32_t gid_of(const ImportanceArgs& a, uint32_t lidx) {
   return lidx * uint32_t(a.world) + uint32_t(a.rank);
 }
 
-__global__ void __launch_bounds__(256) k_imp_stats(ImportanceArgs a, unsigned long long* total) {
-  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  unsigned long long w = 0;
-  if (t < a.n_items) {
+// ---- bodies shared by the per-round kernels and the cooperative kernel -----------------
+
+// s, c_rad and the (rank-local) total mass; one atomic per CTA
+__device__ void stats_body(const ImportanceArgs& a, unsigned long long* total) {
+  __shared__ unsigned long long s_w[8];
+  unsigned long long wsum = 0;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items;
+       t += int64_t(gridDim.x) * blockDim.x) {
     const Item it = load_item(a, t);
-    w = it.w;
+    wsum += it.w;
     if (it.a > 0) a.s[it.lidx] += (double(it.w) * (1.0 / 16777216.0)) / (double(it.a) + 1e-8);
     if (it.rad) a.c_rad[it.lidx] += 1u;
   }
-  // block sum of w, one atomic
-  __shared__ unsigned long long s_w[8];
-  unsigned long long v = w;
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  for (int o = 16; o >= 1; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = wsum;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long sum = 0;
     for (int i = 0; i < 8; ++i) sum += s_w[i];
     if (sum) atomicAdd(total, sum);
   }
+  __syncthreads();
 }
 
 // candidates of round r: w > 0 and w >> (shift + 8) == prefix
-__global__ void __launch_bounds__(256) k_imp_hist(ImportanceArgs a, const ImpState* st, int round,
-                                                  unsigned long long* hist /*[256] count, [256] mass*/) {
+__device__ void hist_body(const ImportanceArgs& a, unsigned long long prefix, int round,
+                          unsigned long long* hist /*[256] count, [256] mass*/) {
   __shared__ unsigned long long s_cnt[256], s_mass[256];
   s_cnt[threadIdx.x] = 0;
   s_mass[threadIdx.x] = 0;
   __syncthreads();
   const int shift = 8 * (kWRounds - 1 - round);
-  const unsigned long long prefix = st->prefix;
-  const bool empty = st->empty;
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count so every lane reaches the warp collectives
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); !empty && base < a.n_items;
-       base += stride) {
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < a.n_items; base += stride) {
     const int64_t t = base + lane;
-    unsigned long long w = 0;
-    if (t < a.n_items) w = a.item_lidx ? a.acc[t].w : a.w_dense[t];
+    const unsigned long long w = t < a.n_items ? load_w(a, t) : 0ull;
     const bool cand = w != 0 && !(shift + 8 < 64 && (w >> (shift + 8)) != prefix);
     const uint32_t d = cand ? uint32_t((w >> shift) & 255u) : 256u + lane;
     // one shared-memory atomic per distinct digit of the warp: the early rounds put almost
@@ -128,26 +139,29 @@ __global__ void __launch_bounds__(256) k_imp_hist(ImportanceArgs a, const ImpSta
     atomicAdd(hist + threadIdx.x, s_cnt[threadIdx.x]);
     atomicAdd(hist + 256 + threadIdx.x, s_mass[threadIdx.x]);
   }
+  __syncthreads();
 }
 
-// one CTA: pick the digit where the cumulative mass (from the top) crosses num/den of total
-__global__ void __launch_bounds__(256) k_imp_decide(ImpState* st, const unsigned long long* total_in, int round,
-                                                    const unsigned long long* hist, int num, int den) {
+// whole CTA: pick the digit where the cumulative mass (from the top) crosses num/den of total.
+// `st` may be global (one-CTA kernel) or shared (cooperative kernel); thread 0 writes it.
+__device__ void decide_body(ImpState* st, unsigned long long total_in, int round, const unsigned long long* hist,
+                            int num, int den) {
   __shared__ unsigned long long s_suf[256];
   __shared__ int s_pick;
   const int d = threadIdx.x;
   if (round == 0) {
     if (d == 0) {
-      st->total = *total_in;
-      st->empty = st->total == 0;
+      st->total = total_in;
+      st->empty = total_in == 0;
       st->above = 0;
       st->prefix = 0;
+      st->need_gid = 0;
+      st->tau = 0;
     }
     __syncthreads();
   }
   if (st->empty) return;
   const unsigned long long target = (unsigned long long)num * st->total;  // need den*prefix >= target
-  // inclusive suffix sums of mass (digits d..255)
   s_suf[255 - d] = hist[256 + d];
   __syncthreads();
   for (int o = 1; o < 256; o <<= 1) {
@@ -156,13 +170,13 @@ __global__ void __launch_bounds__(256) k_imp_decide(ImpState* st, const unsigned
     s_suf[d] += v;
     __syncthreads();
   }
-  // s_suf[j] = mass of digits >= 255 - j.  The crossing digit is the largest d with
-  // den*(above + mass(>= d)) >= target.
+  // s_suf[j] = mass of digits >= 255 - j; the crossing digit is the largest d with
+  // den*(above + mass(>= d)) >= target
   if (d == 0) s_pick = -1;
   __syncthreads();
   const unsigned long long above = st->above;
-  const unsigned long long incl = s_suf[255 - d];                      // mass of digits >= d
-  const unsigned long long excl = d < 255 ? s_suf[254 - d] : 0ull;     // mass of digits > d
+  const unsigned long long incl = s_suf[255 - d];
+  const unsigned long long excl = d < 255 ? s_suf[254 - d] : 0ull;
   const bool cross = (unsigned long long)den * (above + incl) >= target &&
                      (unsigned long long)den * (above + excl) < target;
   if (cross && hist[d] > 0) s_pick = d;
@@ -187,30 +201,28 @@ __global__ void __launch_bounds__(256) k_imp_decide(ImpState* st, const unsigned
       }
     }
   }
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_imp_gid_hist(ImportanceArgs a, const ImpState* st, int round,
-                                                      unsigned long long* hist /*[256] counts*/) {
+__device__ void gid_hist_body(const ImportanceArgs& a, unsigned long long tau, uint32_t gp, int round,
+                              unsigned long long* hist /*[256] counts*/) {
   __shared__ unsigned long long s_cnt[256];
   s_cnt[threadIdx.x] = 0;
   __syncthreads();
-  const bool run = !st->empty && st->need_gid;
   const int shift = 8 * (kGRounds - 1 - round);
-  const unsigned long long tau = st->tau;
-  const uint32_t gp = st->gprefix;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; run && t < a.n_items;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items;
        t += int64_t(gridDim.x) * blockDim.x) {
-    const Item it = load_item(a, t);
-    if (it.w != tau) continue;
-    const uint32_t g = gid_of(a, it.lidx);
+    if (load_w(a, t) != tau) continue;
+    const uint32_t g = gid_of(a, a.item_lidx ? a.item_lidx[t] : uint32_t(t));
     if (shift + 8 < 32 && (g >> (shift + 8)) != gp) continue;
     atomicAdd(&s_cnt[(g >> shift) & 255u], 1ull);
   }
   __syncthreads();
   if (s_cnt[threadIdx.x]) atomicAdd(hist + threadIdx.x, s_cnt[threadIdx.x]);
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_imp_gid_decide(ImpState* st, int round, const unsigned long long* hist) {
+__device__ void gid_decide_body(ImpState* st, int round, const unsigned long long* hist) {
   __shared__ unsigned long long s_pre[256];
   __shared__ int s_pick;
   if (st->empty || !st->need_gid) return;
@@ -234,19 +246,79 @@ __global__ void __launch_bounds__(256) k_imp_gid_decide(ImpState* st, int round,
     st->gprefix = (st->gprefix << 8) | uint32_t(s_pick);
     if (round == kGRounds - 1) st->gid_thr = st->gprefix;
   }
+  __syncthreads();
+}
+
+__device__ void mark_body(const ImportanceArgs& a, const ImpState& st) {
+  if (st.empty) return;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long w = load_w(a, t);
+    if (w == 0 || w < st.tau) continue;
+    const uint32_t lidx = a.item_lidx ? a.item_lidx[t] : uint32_t(t);
+    if (w == st.tau && st.need_gid && gid_of(a, lidx) > st.gid_thr) continue;
+    a.c_vis[lidx] += 1u;
+    atomicAnd(a.cull + (lidx >> 5), ~(1u << (lidx & 31)));
+  }
+}
+
+// ---- per-round kernels (world > 1) -----------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_imp_stats(ImportanceArgs a, unsigned long long* total) {
+  stats_body(a, total);
+}
+
+__global__ void __launch_bounds__(256) k_imp_hist(ImportanceArgs a, const ImpState* st, int round,
+                                                  unsigned long long* hist) {
+  if (st->empty) return;
+  hist_body(a, st->prefix, round, hist);
+}
+
+__global__ void __launch_bounds__(256) k_imp_decide(ImpState* st, const unsigned long long* total_in, int round,
+                                                    const unsigned long long* hist, int num, int den) {
+  decide_body(st, *total_in, round, hist, num, den);
+}
+
+__global__ void __launch_bounds__(256) k_imp_gid_hist(ImportanceArgs a, const ImpState* st, int round,
+                                                      unsigned long long* hist) {
+  if (st->empty || !st->need_gid) return;
+  gid_hist_body(a, st->tau, st->gprefix, round, hist);
+}
+
+__global__ void __launch_bounds__(256) k_imp_gid_decide(ImpState* st, int round, const unsigned long long* hist) {
+  gid_decide_body(st, round, hist);
 }
 
 __global__ void __launch_bounds__(256) k_imp_mark(ImportanceArgs a, const ImpState* st) {
-  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= a.n_items || st->empty) return;
-  const Item it = load_item(a, t);
-  if (it.w == 0) return;
-  const unsigned long long tau = st->tau;
-  bool in = it.w > tau;
-  if (it.w == tau) in = !st->need_gid || gid_of(a, it.lidx) <= st->gid_thr;
-  if (!in) return;
-  a.c_vis[it.lidx] += 1u;
-  atomicAnd(a.cull + (it.lidx >> 5), ~(1u << (it.lidx & 31)));
+  const ImpState s = *st;
+  mark_body(a, s);
+}
+
+// ---- world == 1: everything in one cooperative launch ------------------------------------
+
+__global__ void __launch_bounds__(256) k_imp_coop(ImportanceArgs a, ImpState* st_out, unsigned long long* total,
+                                                  unsigned long long* hist /*[7*512 + 4*256], zeroed*/, int num,
+                                                  int den) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ ImpState st;
+  stats_body(a, total);
+  grid.sync();
+  const unsigned long long tot = *((volatile unsigned long long*)total);
+  for (int r = 0; r < kWRounds; ++r) {
+    if (r > 0 && st.empty) break;
+    if (r > 0 || tot != 0) hist_body(a, r == 0 ? 0ull : st.prefix, r, hist + r * 512);
+    grid.sync();
+    decide_body(&st, tot, r, hist + r * 512, num, den);
+  }
+  if (!st.empty && st.need_gid) {
+    for (int r = 0; r < kGRounds; ++r) {
+      gid_hist_body(a, st.tau, st.gprefix, r, hist + kWRounds * 512 + r * 256);
+      grid.sync();
+      gid_decide_body(&st, r, hist + kWRounds * 512 + r * 256);
+    }
+  }
+  mark_body(a, st);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *st_out = st;
 }
 
 // all bits [0, n_bits) set, bits past n_bits in the last word clear
@@ -256,6 +328,12 @@ __global__ void k_fill_bits(uint32_t* words, int64_t n_bits) {
   if (t >= nw) return;
   const int64_t rem = n_bits - 32 * t;
   words[t] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+}
+
+unsigned grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
+  return unsigned(b < 1 ? 1 : b);
 }
 
 }  // namespace
@@ -270,13 +348,7 @@ void launch_fill_bits(uint32_t* words, int64_t n_bits, cudaStream_t s) {
 }
 
 void launch_imp_stats(const ImportanceArgs& a, unsigned long long* total, cudaStream_t s) {
-  if (a.n_items > 0) k_imp_stats<<<unsigned((a.n_items + 255) / 256), 256, 0, s>>>(a, total);
-}
-
-static unsigned grid_for(int64_t n) {
-  int64_t b = (n + 255) / 256;
-  if (b > 148 * 8) b = 148 * 8;
-  return unsigned(b < 1 ? 1 : b);
+  if (a.n_items > 0) k_imp_stats<<<grid_for(a.n_items), 256, 0, s>>>(a, total);
 }
 
 void launch_imp_hist(const ImportanceArgs& a, const ImpState* st, int round, unsigned long long* hist,
@@ -299,7 +371,24 @@ void launch_imp_gid_decide(ImpState* st, int round, const unsigned long long* hi
 }
 
 void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s) {
-  if (a.n_items > 0) k_imp_mark<<<unsigned((a.n_items + 255) / 256), 256, 0, s>>>(a, st);
+  if (a.n_items > 0) k_imp_mark<<<grid_for(a.n_items), 256, 0, s>>>(a, st);
+}
+
+cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* total,
+                            unsigned long long* hist, int num, int den, cudaStream_t s) {
+  static int blocks = 0;
+  if (blocks == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_imp_coop, 256, 0);
+    blocks = sms * (per_sm < 4 ? per_sm : 4);
+    if (blocks < 1) blocks = 1;
+  }
+  ImportanceArgs aa = a;
+  int nn = num, dd = den;
+  void* args[] = {&aa, &st, &total, &hist, &nn, &dd};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_imp_coop), dim3(blocks), dim3(256), args, 0, s);
 }
 
 }  // namespace bgs

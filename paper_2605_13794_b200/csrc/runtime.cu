@@ -821,6 +821,10 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   int nl = 0;
   launch_fill_bits(cull_out, n_local, s);
   ++nl;
+  if (ctx->world == 1) {
+    CK(launch_imp_coop(a, st, total, hist, mass_num, mass_den, s));
+    return launched(ctx, nl + 1);
+  }
   launch_imp_stats(a, total, s);
   ++nl;
   if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, total, 1, s));
