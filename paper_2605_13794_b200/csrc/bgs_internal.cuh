@@ -62,6 +62,8 @@ struct ProjectArgs {
   float D2[32];
   int no_color;
   int rank, world;
+  float lim[4];              // Jacobian clamp limits x+, x-, y+, y- (same float expressions as the oracle)
+  float cull_K;              // fx^2 (1 + Lx^2) + fy^2 (1 + Ly^2) for the conservative radius bound
   // outputs
   int32_t* radius;
   Rec* recs;

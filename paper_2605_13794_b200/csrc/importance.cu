@@ -40,7 +40,8 @@ struct alignas(16) ImpState {
   uint32_t gid_thr;              // include ties with gid <= gid_thr
   uint32_t need_gid;             // 0 < k < ntie
   uint32_t empty;                // total == 0
-  uint32_t pad[2];
+  uint32_t r0;                   // first w round with a non-zero digit (from the MSB histogram)
+  uint32_t pad1;
 };
 
 namespace {
@@ -82,17 +83,25 @@ __device__ __forceinline__ uint32_t gid_of(const ImportanceArgs& a, uint32_t lid
 
 // ---- bodies shared by the per-round kernels and the cooperative kernel -----------------
 
-// s, c_rad and the (rank-local) total mass; one atomic per CTA
+// s, c_rad, the (rank-local) total mass total[0] and the histogram of the most significant
+// bit of w in total[1..64] (so the rounds above the global maximum can be skipped); one
+// atomic per CTA for the total
 __device__ void stats_body(const ImportanceArgs& a, unsigned long long* total) {
   __shared__ unsigned long long s_w[8];
+  __shared__ uint32_t s_msb[64];
+  if (threadIdx.x < 64) s_msb[threadIdx.x] = 0;
+  __syncthreads();
   unsigned long long wsum = 0;
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items;
        t += int64_t(gridDim.x) * blockDim.x) {
     const Item it = load_item(a, t);
     wsum += it.w;
+    if (it.w) atomicAdd(&s_msb[63 - __clzll((long long)it.w)], 1u);
     if (it.a > 0) a.s[it.lidx] += (double(it.w) * (1.0 / 16777216.0)) / (double(it.a) + 1e-8);
     if (it.rad) a.c_rad[it.lidx] += 1u;
   }
+  __syncthreads();
+  if (threadIdx.x < 64 && s_msb[threadIdx.x]) atomicAdd(total + 1 + threadIdx.x, (unsigned long long)s_msb[threadIdx.x]);
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
   if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = wsum;
@@ -124,14 +133,23 @@ __device__ void hist_body(const ImportanceArgs& a, unsigned long long prefix, in
     // one shared-memory atomic per distinct digit of the warp: the early rounds put almost
     // every candidate in one bin, which serialised per-lane 64-bit atomics
     const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t lo = uint32_t(w & 0xffffffu), mid = uint32_t((w >> 24) & 0xffffffu), hi = uint32_t(w >> 48);
-    const uint32_t slo = __reduce_add_sync(peers, lo);
-    const uint32_t smid = __reduce_add_sync(peers, mid);
-    const uint32_t shi = __reduce_add_sync(peers, hi);
-    if (cand && lane == __ffs(peers) - 1) {
-      atomicAdd(&s_cnt[d], (unsigned long long)__popc(peers));
-      atomicAdd(&s_mass[d], (unsigned long long)slo + ((unsigned long long)smid << 24) +
-                                ((unsigned long long)shi << 48));
+    const bool single = peers == (1u << lane);
+    if (cand && single) {
+      atomicAdd(&s_cnt[d], 1ull);
+      atomicAdd(&s_mass[d], w);
+    }
+    // groups of lanes sharing a digit: reduce in-warp first (redux.sync runs once per group)
+    const bool multi = cand && !single;
+    if (__any_sync(0xffffffffu, multi) && multi) {
+      const uint32_t lo = uint32_t(w & 0xffffffu), mid = uint32_t((w >> 24) & 0xffffffu), hi = uint32_t(w >> 48);
+      const uint32_t slo = __reduce_add_sync(peers, lo);
+      const uint32_t smid = __reduce_add_sync(peers, mid);
+      const uint32_t shi = __reduce_add_sync(peers, hi);
+      if (lane == __ffs(peers) - 1) {
+        atomicAdd(&s_cnt[d], (unsigned long long)__popc(peers));
+        atomicAdd(&s_mass[d], (unsigned long long)slo + ((unsigned long long)smid << 24) +
+                                  ((unsigned long long)shi << 48));
+      }
     }
   }
   __syncthreads();
@@ -142,25 +160,32 @@ __device__ void hist_body(const ImportanceArgs& a, unsigned long long prefix, in
   __syncthreads();
 }
 
+// thread 0: state before the first round (total and MSB histogram already summed over ranks)
+__device__ void init_state(ImpState* st, const unsigned long long* total) {
+  st->total = total[0];
+  st->empty = total[0] == 0;
+  st->above = 0;
+  st->prefix = 0;
+  st->need_gid = 0;
+  st->tau = 0;
+  int maxbit = 0;
+  for (int b = 63; b >= 0; --b)
+    if (total[1 + b]) {
+      maxbit = b;
+      break;
+    }
+  // rounds whose 8-bit digit lies above the maximum are all-zero digits: skipped
+  const int r0 = (kWRounds - 1) - maxbit / 8;
+  st->r0 = uint32_t(r0 < 0 ? 0 : r0);
+}
+
 // whole CTA: pick the digit where the cumulative mass (from the top) crosses num/den of total.
 // `st` may be global (one-CTA kernel) or shared (cooperative kernel); thread 0 writes it.
-__device__ void decide_body(ImpState* st, unsigned long long total_in, int round, const unsigned long long* hist,
-                            int num, int den) {
+__device__ void decide_body(ImpState* st, int round, const unsigned long long* hist, int num, int den) {
   __shared__ unsigned long long s_suf[256];
   __shared__ int s_pick;
   const int d = threadIdx.x;
-  if (round == 0) {
-    if (d == 0) {
-      st->total = total_in;
-      st->empty = total_in == 0;
-      st->above = 0;
-      st->prefix = 0;
-      st->need_gid = 0;
-      st->tau = 0;
-    }
-    __syncthreads();
-  }
-  if (st->empty) return;
+  if (st->empty || round < int(st->r0)) return;
   const unsigned long long target = (unsigned long long)num * st->total;  // need den*prefix >= target
   s_suf[255 - d] = hist[256 + d];
   __syncthreads();
@@ -270,13 +295,17 @@ __global__ void __launch_bounds__(256) k_imp_stats(ImportanceArgs a, unsigned lo
 
 __global__ void __launch_bounds__(256) k_imp_hist(ImportanceArgs a, const ImpState* st, int round,
                                                   unsigned long long* hist) {
-  if (st->empty) return;
+  if (st->empty || round < int(st->r0)) return;
   hist_body(a, st->prefix, round, hist);
 }
 
 __global__ void __launch_bounds__(256) k_imp_decide(ImpState* st, const unsigned long long* total_in, int round,
                                                     const unsigned long long* hist, int num, int den) {
-  decide_body(st, *total_in, round, hist, num, den);
+  if (round == 0) {
+    if (threadIdx.x == 0) init_state(st, total_in);
+    __syncthreads();
+  }
+  decide_body(st, round, hist, num, den);
 }
 
 __global__ void __launch_bounds__(256) k_imp_gid_hist(ImportanceArgs a, const ImpState* st, int round,
@@ -303,12 +332,12 @@ __global__ void __launch_bounds__(256) k_imp_coop(ImportanceArgs a, ImpState* st
   __shared__ ImpState st;
   stats_body(a, total);
   grid.sync();
-  const unsigned long long tot = *((volatile unsigned long long*)total);
-  for (int r = 0; r < kWRounds; ++r) {
-    if (r > 0 && st.empty) break;
-    if (r > 0 || tot != 0) hist_body(a, r == 0 ? 0ull : st.prefix, r, hist + r * 512);
+  if (threadIdx.x == 0) init_state(&st, total);
+  __syncthreads();
+  for (int r = int(st.r0); r < kWRounds && !st.empty; ++r) {
+    hist_body(a, st.prefix, r, hist + r * 512);
     grid.sync();
-    decide_body(&st, tot, r, hist + r * 512, num, den);
+    decide_body(&st, r, hist + r * 512, num, den);
   }
   if (!st.empty && st.need_gid) {
     for (int r = 0; r < kGRounds; ++r) {

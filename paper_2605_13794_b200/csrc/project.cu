@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(256) k_gate_count(ProjectArgs a) {
 
 struct ProjOut {
   float mx, my, A, B, C, depth, opac;
+  float mux, muy, muz;  // parked in the record's colour slots for k_color
   uint32_t rect, area;
   bool valid, active;
   int x0, y0, x1, y1;
@@ -50,17 +51,15 @@ struct ProjOut {
 __device__ __forceinline__ ProjOut project_one(const ProjectArgs& a, int64_t i) {
   bool valid = false;
   bool active = false;
-  float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, depth = 0.f, opac = 0.f;
+  float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, depth = 0.f, opac = 0.f, mux = 0.f, muy = 0.f,
+        muz = 0.f;
   int radius = 0;
   uint32_t area = 0;
   int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
   if (i < a.n) {
     const bool filtered = a.gate_enabled || a.cull;
     float4 q = make_float4(0.f, 0.f, 0.f, 0.f), sc = q;
-    if (!filtered) {  // nothing can drop this Gaussian before projection: issue all loads now
-      q = ldg4(a.quat + i);
-      sc = ldg4(a.scale + i);
-    }
+    if (!filtered) sc = ldg4(a.scale + i);  // nothing can drop it before the frustum test: load now
     const float4 mo = ldg4(a.mean_opac + i);
     // ---- a1: Eq.5 gate with per-rank fallback, then Eq.6 cull column
     bool keep = true;
@@ -72,16 +71,29 @@ __device__ __forceinline__ ProjOut project_one(const ProjectArgs& a, int64_t i) 
     if (keep && a.cull) keep = !((__ldg(a.cull + (i >> 5)) >> (i & 31)) & 1u);
     active = keep;
     if (keep) {
-      if (filtered) {
-        q = ldg4(a.quat + i);
-        sc = ldg4(a.scale + i);
-      }
+      if (filtered) sc = ldg4(a.scale + i);
       const CameraK& cm = a.cam;
       // ---- a2: t_c = R mu + t
       const float tx = ((cm.R[0] * mo.x + cm.R[1] * mo.y) + cm.R[2] * mo.z) + cm.t[0];
       const float ty = ((cm.R[3] * mo.x + cm.R[4] * mo.y) + cm.R[5] * mo.z) + cm.t[1];
       const float tz = ((cm.R[6] * mo.x + cm.R[7] * mo.y) + cm.R[8] * mo.z) + cm.t[2];
-      if (tz > cm.near_clip) {
+      const float txtz = tx / tz, tytz = ty / tz;
+      // Conservative off-screen rejection before any covariance work:
+      // radius <= 3 sqrt(|J|_F^2 s_max^2 + 0.3 + sqrt(0.1)) + 1 with |J|_F^2 <= K / tz^2
+      // (K = fx^2 (1 + Lx^2) + fy^2 (1 + Ly^2), L = clamp limits), widened by 1% + 2 px; a
+      // Gaussian whose centre is further than that outside the image has an empty rect in the
+      // exact computation too, so the decision is unchanged.
+      bool maybe = tz > cm.near_clip;
+      if (maybe) {
+        const float mxb = cm.fx * txtz + cm.cx, myb = cm.fy * tytz + cm.cy;
+        const float smax = fmaxf(sc.x, fmaxf(sc.y, sc.z));
+        const float iz = __fdividef(1.0f, tz);
+        const float rb = 3.0f * sqrtf(a.cull_K * (smax * smax) * (iz * iz) + 0.62f) * 1.01f + 2.0f;
+        maybe = !(mxb + rb < 0.0f || mxb - rb > float(16 * cm.TX + 1) || myb + rb < 0.0f ||
+                  myb - rb > float(16 * cm.TY + 1));
+      }
+      if (maybe) q = ldg4(a.quat + i);
+      if (maybe) {
         // Sigma = R(q) S S^T R(q)^T
         const float xx = q.y * q.y, yy = q.z * q.z, zz = q.w * q.w;
         const float xy = q.y * q.z, xz = q.y * q.w, yz = q.z * q.w;
@@ -100,15 +112,9 @@ __device__ __forceinline__ ProjOut project_one(const ProjectArgs& a, int64_t i) 
         for (int r = 0; r < 3; ++r)
 #pragma unroll
           for (int c = 0; c < 3; ++c) S[r][c] = (M[r][0] * M[c][0] + M[r][1] * M[c][1]) + M[r][2] * M[c][2];
-        // EWA Jacobian with the 1.3 tan(fov/2) clamp (off-centre principal point)
-        const float Wf = float(cm.W), Hf = float(cm.H);
-        const float tan_fovx = (0.5f * Wf) / cm.fx;
-        const float tan_fovy = (0.5f * Hf) / cm.fy;
-        const float lim_xp = (Wf - cm.cx) / cm.fx + 0.3f * tan_fovx;
-        const float lim_xn = cm.cx / cm.fx + 0.3f * tan_fovx;
-        const float lim_yp = (Hf - cm.cy) / cm.fy + 0.3f * tan_fovy;
-        const float lim_yn = cm.cy / cm.fy + 0.3f * tan_fovy;
-        const float txtz = tx / tz, tytz = ty / tz;
+        // EWA Jacobian with the 1.3 tan(fov/2) clamp (off-centre principal point); the four
+        // per-camera limits are computed once on the host with the same float expressions
+        const float lim_xp = a.lim[0], lim_xn = a.lim[1], lim_yp = a.lim[2], lim_yn = a.lim[3];
         const float ctx = fminf(lim_xp, fmaxf(-lim_xn, txtz)) * tz;
         const float cty = fminf(lim_yp, fmaxf(-lim_yn, tytz)) * tz;
         const float J00 = cm.fx / tz, J02 = -(cm.fx * ctx) / (tz * tz);
@@ -156,6 +162,11 @@ __device__ __forceinline__ ProjOut project_one(const ProjectArgs& a, int64_t i) 
             radius = rad;
             depth = tz;
             opac = mo.w;
+            if (!a.no_color) {
+              mux = mo.x;
+              muy = mo.y;
+              muz = mo.z;
+            }
           }
         }
       }
@@ -170,6 +181,9 @@ __device__ __forceinline__ ProjOut project_one(const ProjectArgs& a, int64_t i) 
   o.C = cC;
   o.depth = depth;
   o.opac = opac;
+  o.mux = mux;
+  o.muy = muy;
+  o.muz = muz;
   o.rect = uint32_t(x0) | (uint32_t(y0) << 8) | (uint32_t(x1) << 16) | (uint32_t(y1) << 24);
   o.area = area;
   o.valid = valid;
@@ -258,8 +272,8 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
     const int64_t i = chunk0 + k * 256 + tid;
     const uint32_t gid = uint32_t(i) * uint32_t(a.world) + uint32_t(a.rank);
     s_rec[3 * ls + 0] = make_float4(o[k].mx, o[k].my, o[k].A, o[k].B);
-    s_rec[3 * ls + 1] = make_float4(o[k].C, o[k].opac, 0.f, 0.f);
-    s_rec[3 * ls + 2] = make_float4(0.f, o[k].depth, __uint_as_float(gid), __uint_as_float(o[k].rect));
+    s_rec[3 * ls + 1] = make_float4(o[k].C, o[k].opac, o[k].mux, o[k].muy);
+    s_rec[3 * ls + 2] = make_float4(o[k].muz, o[k].depth, __uint_as_float(gid), __uint_as_float(o[k].rect));
     s_lidx[ls] = uint32_t(i);
     if (a.tile_diff) {
       // 2D difference array of rect coverage -> per-tile pair counts (a3 input)
@@ -302,7 +316,9 @@ __device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f) 
     v[4 * q4 + 2] = t.z;
     v[4 * q4 + 3] = t.w;
   }
-  const float4 mo = ldg4(a.mean_opac + i);
+  // mu was parked in the colour slots by k_project (no scattered 16-B read of mean_opac)
+  float* rp = reinterpret_cast<float*>(a.recs + f);
+  const float4 mo = make_float4(rp[6], rp[7], rp[8], 0.f);
   const CameraK& cm = a.cam;
   const float dx = mo.x - cm.campos[0], dy = mo.y - cm.campos[1], dz = mo.z - cm.campos[2];
   const float len = sqrtf((dx * dx + dy * dy) + dz * dz);
@@ -334,7 +350,6 @@ __device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f) 
     c = c + 0.5f;
     col[ch] = c < 0.0f ? 0.0f : c;
   }
-  float* rp = reinterpret_cast<float*>(a.recs + f);
   rp[6] = col[0];
   rp[7] = col[1];
   rp[8] = col[2];

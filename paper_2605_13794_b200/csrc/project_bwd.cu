@@ -148,7 +148,35 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
   gy += 2.f * qz * dRq[2][1]; gz += 2.f * qy * dRq[2][1]; gw += 2.f * qx * dRq[2][1]; gx += 2.f * w * dRq[2][1];
   gx -= 4.f * qx * dRq[2][2]; gy -= 4.f * qy * dRq[2][2];
 
-  // SH colour backward
+  float4 gm = a.g_mean_opac[i];
+  gm.x += dmu[0];
+  gm.y += dmu[1];
+  gm.z += dmu[2];
+  gm.w += g[5];
+  a.g_mean_opac[i] = gm;
+  float4 gq = a.g_quat[i];
+  gq.x += gw;
+  gq.y += gx;
+  gq.z += gy;
+  gq.w += gz;
+  a.g_quat[i] = gq;
+  float4 gs = a.g_scale[i];
+  gs.x += ds[0];
+  gs.y += ds[1];
+  gs.z += ds[2];
+  a.g_scale[i] = gs;
+}
+
+// SH colour backward (second kernel: keeps each kernel's register footprint small so enough
+// warps are resident to hide the scattered 192-B row loads)
+__global__ void __launch_bounds__(256) k_project_bwd_sh(ProjectBwdArgs a) {
+  const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (f >= a.F) return;
+  const uint32_t i = a.rec_lidx[f];
+  const CameraK& cm = a.cam;
+  const float4 mo = __ldg(a.mean_opac + i);
+  const float* g = a.acc[f].g;
+  const float g6 = g[6], g7 = g[7], g8 = g[8];
   const float ddx = mo.x - cm.campos[0], ddy = mo.y - cm.campos[1], ddz = mo.z - cm.campos[2];
   const float len = sqrtf(ddx * ddx + ddy * ddy + ddz * ddz), il = 1.f / len;
   const float X = ddx * il, Y = ddy * il, Z = ddz * il;
@@ -170,24 +198,6 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
   Yb[13] = SHC3[4] * X * (4.f * zz - xx - yy);
   Yb[14] = SHC3[5] * Z * (xx - yy);
   Yb[15] = SHC3[6] * X * (xx - 3.f * yy);
-  float dY[16][3];
-  dY[0][0] = dY[0][1] = dY[0][2] = 0.f;
-  dY[1][0] = 0.f; dY[1][1] = -SHC1; dY[1][2] = 0.f;
-  dY[2][0] = 0.f; dY[2][1] = 0.f; dY[2][2] = SHC1;
-  dY[3][0] = -SHC1; dY[3][1] = 0.f; dY[3][2] = 0.f;
-  dY[4][0] = SHC2[0] * Y; dY[4][1] = SHC2[0] * X; dY[4][2] = 0.f;
-  dY[5][0] = 0.f; dY[5][1] = SHC2[1] * Z; dY[5][2] = SHC2[1] * Y;
-  dY[6][0] = -2.f * SHC2[2] * X; dY[6][1] = -2.f * SHC2[2] * Y; dY[6][2] = 4.f * SHC2[2] * Z;
-  dY[7][0] = SHC2[3] * Z; dY[7][1] = 0.f; dY[7][2] = SHC2[3] * X;
-  dY[8][0] = 2.f * SHC2[4] * X; dY[8][1] = -2.f * SHC2[4] * Y; dY[8][2] = 0.f;
-  dY[9][0] = SHC3[0] * 6.f * xy; dY[9][1] = SHC3[0] * 3.f * (xx - yy); dY[9][2] = 0.f;
-  dY[10][0] = SHC3[1] * yz; dY[10][1] = SHC3[1] * xz; dY[10][2] = SHC3[1] * xy;
-  dY[11][0] = -2.f * SHC3[2] * xy; dY[11][1] = SHC3[2] * (4.f * zz - xx - 3.f * yy); dY[11][2] = 8.f * SHC3[2] * yz;
-  dY[12][0] = -6.f * SHC3[3] * xz; dY[12][1] = -6.f * SHC3[3] * yz; dY[12][2] = SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy);
-  dY[13][0] = SHC3[4] * (4.f * zz - 3.f * xx - yy); dY[13][1] = -2.f * SHC3[4] * xy; dY[13][2] = 8.f * SHC3[4] * xz;
-  dY[14][0] = 2.f * SHC3[5] * xz; dY[14][1] = -2.f * SHC3[5] * yz; dY[14][2] = SHC3[5] * (xx - yy);
-  dY[15][0] = SHC3[6] * 3.f * (xx - yy); dY[15][1] = -6.f * SHC3[6] * xy; dY[15][2] = 0.f;
-
   const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i);
   float v[48];
 #pragma unroll
@@ -204,38 +214,30 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
     float c = 0.5f;
 #pragma unroll
     for (int k = 0; k < 16; ++k) c += Yb[k] * v[3 * k + ch];
-    dcol[ch] = c < 0.f ? 0.f : g[6 + ch];
+    dcol[ch] = c < 0.f ? 0.f : (ch == 0 ? g6 : (ch == 1 ? g7 : g8));
   }
-  float ddir[3] = {0.f, 0.f, 0.f};
+  float sk[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const float s = dcol[0] * v[3 * k] + dcol[1] * v[3 * k + 1] + dcol[2] * v[3 * k + 2];
-    ddir[0] += s * dY[k][0];
-    ddir[1] += s * dY[k][1];
-    ddir[2] += s * dY[k][2];
-  }
+  for (int k = 0; k < 16; ++k) sk[k] = dcol[0] * v[3 * k] + dcol[1] * v[3 * k + 1] + dcol[2] * v[3 * k + 2];
+  // d(sum_k sk Y_k)/d(x,y,z): the partial derivatives of the 16 basis functions, written out
+  float ddir[3];
+  ddir[0] = -SHC1 * sk[3] + SHC2[0] * Y * sk[4] - 2.f * SHC2[2] * X * sk[6] + SHC2[3] * Z * sk[7] +
+            2.f * SHC2[4] * X * sk[8] + 6.f * SHC3[0] * xy * sk[9] + SHC3[1] * yz * sk[10] -
+            2.f * SHC3[2] * xy * sk[11] - 6.f * SHC3[3] * xz * sk[12] + SHC3[4] * (4.f * zz - 3.f * xx - yy) * sk[13] +
+            2.f * SHC3[5] * xz * sk[14] + 3.f * SHC3[6] * (xx - yy) * sk[15];
+  ddir[1] = -SHC1 * sk[1] + SHC2[0] * X * sk[4] + SHC2[1] * Z * sk[5] - 2.f * SHC2[2] * Y * sk[6] -
+            2.f * SHC2[4] * Y * sk[8] + 3.f * SHC3[0] * (xx - yy) * sk[9] + SHC3[1] * xz * sk[10] +
+            SHC3[2] * (4.f * zz - xx - 3.f * yy) * sk[11] - 6.f * SHC3[3] * yz * sk[12] - 2.f * SHC3[4] * xy * sk[13] -
+            2.f * SHC3[5] * yz * sk[14] - 6.f * SHC3[6] * xy * sk[15];
+  ddir[2] = SHC1 * sk[2] + SHC2[1] * Y * sk[5] + 4.f * SHC2[2] * Z * sk[6] + SHC2[3] * X * sk[7] +
+            SHC3[1] * xy * sk[10] + 8.f * SHC3[2] * yz * sk[11] + SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * sk[12] +
+            8.f * SHC3[4] * xz * sk[13] + SHC3[5] * (xx - yy) * sk[14];
   const float dot = ddir[0] * X + ddir[1] * Y + ddir[2] * Z;
-  dmu[0] += (ddir[0] - X * dot) * il;
-  dmu[1] += (ddir[1] - Y * dot) * il;
-  dmu[2] += (ddir[2] - Z * dot) * il;
-
   float4 gm = a.g_mean_opac[i];
-  gm.x += dmu[0];
-  gm.y += dmu[1];
-  gm.z += dmu[2];
-  gm.w += g[5];
+  gm.x += (ddir[0] - X * dot) * il;
+  gm.y += (ddir[1] - Y * dot) * il;
+  gm.z += (ddir[2] - Z * dot) * il;
   a.g_mean_opac[i] = gm;
-  float4 gq = a.g_quat[i];
-  gq.x += gw;
-  gq.y += gx;
-  gq.z += gy;
-  gq.w += gz;
-  a.g_quat[i] = gq;
-  float4 gs = a.g_scale[i];
-  gs.x += ds[0];
-  gs.y += ds[1];
-  gs.z += ds[2];
-  a.g_scale[i] = gs;
   float4* gsh = reinterpret_cast<float4*>(a.g_sh + size_t(48) * i);
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
@@ -254,6 +256,7 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
 void launch_project_bwd(const ProjectBwdArgs& a, cudaStream_t s) {
   if (a.F <= 0) return;
   k_project_bwd<<<unsigned((a.F + 127) / 128), 128, 0, s>>>(a);
+  k_project_bwd_sh<<<unsigned((a.F + 255) / 256), 256, 0, s>>>(a);
 }
 
 }  // namespace bgs

@@ -481,6 +481,20 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
     }
   }
   a.no_color = (flags & BGS_NO_COLOR) ? 1 : 0;
+  {
+    // per-camera constants, float expressions identical to the per-Gaussian ones of the
+    // oracle (IEEE binary32 on the host: same bits)
+    const volatile float Wf = float(cam->width), Hf = float(cam->height);
+    const float tan_fovx = (0.5f * Wf) / cam->fx;
+    const float tan_fovy = (0.5f * Hf) / cam->fy;
+    a.lim[0] = (Wf - cam->cx) / cam->fx + 0.3f * tan_fovx;
+    a.lim[1] = cam->cx / cam->fx + 0.3f * tan_fovx;
+    a.lim[2] = (Hf - cam->cy) / cam->fy + 0.3f * tan_fovy;
+    a.lim[3] = cam->cy / cam->fy + 0.3f * tan_fovy;
+    const double Lx = std::max(a.lim[0], a.lim[1]), Ly = std::max(a.lim[2], a.lim[3]);
+    const double K = double(cam->fx) * cam->fx * (1.0 + Lx * Lx) + double(cam->fy) * cam->fy * (1.0 + Ly * Ly);
+    a.cull_K = float(K * 1.0001);
+  }
   a.rank = ctx->rank;
   a.world = ctx->world;
   a.radius = radius_out;
@@ -810,10 +824,10 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   a.cull = cull_out;
   const int WR = imp_w_rounds(), GR = imp_g_rounds();
   CKS(ensure(ctx, ctx->imp_state, kImpStateBytes));
-  CKS(ensure(ctx, ctx->imp_total, 16));
+  CKS(ensure(ctx, ctx->imp_total, 65 * 8));  // total + 64-bin MSB histogram
   CKS(ensure(ctx, ctx->imp_hist, size_t(WR * 512 + GR * 256) * 8));
   CK(cudaMemsetAsync(ctx->imp_state.p, 0, kImpStateBytes, s));
-  CK(cudaMemsetAsync(ctx->imp_total.p, 0, 16, s));
+  CK(cudaMemsetAsync(ctx->imp_total.p, 0, 65 * 8, s));
   CK(cudaMemsetAsync(ctx->imp_hist.p, 0, size_t(WR * 512 + GR * 256) * 8, s));
   ImpState* st = static_cast<ImpState*>(ctx->imp_state.p);
   unsigned long long* total = P_<unsigned long long>(ctx->imp_total);
@@ -827,7 +841,7 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   }
   launch_imp_stats(a, total, s);
   ++nl;
-  if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, total, 1, s));
+  if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, total, 65, s));
   for (int r = 0; r < WR; ++r) {
     launch_imp_hist(a, st, r, hist + r * 512, s);
     if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, hist + r * 512, 512, s));
