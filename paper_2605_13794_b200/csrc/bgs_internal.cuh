@@ -91,6 +91,7 @@ struct SortArgs {
   uint32_t* status;          // look-back status [n_parts][256] per pass
   int n_passes;
   uint2* ranges;             // [t_end - t_begin]
+  float4* aux;               // [n_recv] per-record raster constants (thr, half extent x, half extent y, -)
 };
 // emits pairs and digit histograms; returns nothing (P stays on device, counters[C_P])
 void launch_emit(const SortArgs& a, cudaStream_t s);
@@ -108,6 +109,7 @@ struct RasterArgs {
   const uint32_t* pass_ctrl;  // final buffer selector at pass_ctrl[kFinalSel]
   int t_begin, n_tiles, TX, W, H;
   Acc* acc;
+  const float4* aux;          // per received record: thr, box half extents (from k_emit)
 };
 constexpr int kFinalSel = 15;
 void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,

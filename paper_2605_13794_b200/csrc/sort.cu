@@ -48,6 +48,23 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
     const uint4 q2 = __ldg(reinterpret_cast<const uint4*>(a.recv + r) + 2);  // (b, depth, gid, rect)
     rect = q2.w;
     dbits = q2.y;
+    if (a.aux) {
+      // per-record raster constants, computed once here instead of once per (tile, warp):
+      // thr = -log(255 o) (alpha >= 1/255 <=> power >= thr, D3) and the half extents of the
+      // ellipse {d : d^T Q d <= -2 thr} (sqrt(-2 thr (Q^-1)_xx), sqrt(-2 thr (Q^-1)_yy)) widened
+      // by 1e-3 relative + 0.01 px so that box culling is conservative under fp32 rounding
+      const float4 q0 = __ldg(reinterpret_cast<const float4*>(a.recv + r));
+      const float4 q1 = __ldg(reinterpret_cast<const float4*>(a.recv + r) + 1);
+      const float thr = float(-log(255.0 * double(q1.y)));
+      const float k = -2.0f * thr;
+      const float det = q0.z * q1.x - q0.w * q0.w;
+      float hx = -1e30f, hy = -1e30f;  // empty box: never contributes
+      if (k > 0.f && det > 0.f) {
+        hx = sqrtf(k * q1.x / det) * 1.001f + 0.01f;
+        hy = sqrtf(k * q0.z / det) * 1.001f + 0.01f;
+      }
+      a.aux[r] = make_float4(thr, hx, hy, 0.f);
+    }
     const int x0 = rect & 255, y0 = (rect >> 8) & 255, x1 = (rect >> 16) & 255, y1 = rect >> 24;
     area = uint32_t((x1 - x0) * (y1 - y0));
     // owned count: rows of the rect intersected with the contiguous run [t_begin, t_end)
