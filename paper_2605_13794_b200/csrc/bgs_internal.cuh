@@ -97,6 +97,7 @@ struct SortArgs {
 void launch_emit(const SortArgs& a, cudaStream_t s);
 void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches);
 void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s);
+void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* perm, cudaStream_t s);
 // which buffer (0/1) holds the sorted data after the passes: read from pass_ctrl on device
 // by the consumers below.
 
@@ -110,6 +111,7 @@ struct RasterArgs {
   int t_begin, n_tiles, TX, W, H;
   Acc* acc;
   const float4* aux;          // per received record: thr, box half extents (from k_emit)
+  const uint32_t* tile_perm;  // launch order of the owned tiles (longest list first)
 };
 constexpr int kFinalSel = 15;
 void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,

@@ -76,28 +76,38 @@ struct PixF {
   bool done;
 };
 
-// one forward evaluation; returns alpha*T in fixed point (0 when not contributing)
-__device__ __forceinline__ bool eval_fwd(PixF& px, const WRec& s, float pxf, float pyf, uint32_t pos,
-                                         uint32_t& fixed) {
-  if (px.done) return false;
-  const float dx = s.geo.x - pxf, dy = s.geo.y - pyf;
-  const float power = pinned_power(s.geo.z, s.geo.w, s.co.x, dx, dy);
-  if (!(power <= 0.0f && power >= s.co.z)) return false;
-  const float G = fast_exp(power);
-  const float alpha = fminf(0.99f, s.co.y * G);
-  const float test_T = px.T * (1.0f - alpha);
-  if (test_T < 0.0001f) {
-    px.done = true;
-    return false;
-  }
-  const float wgt = alpha * px.T;
-  px.r += s.rgb.x * wgt;
-  px.g += s.rgb.y * wgt;
-  px.b += s.rgb.z * wgt;
-  px.T = test_T;
-  px.last = pos;
-  fixed = __float2uint_rn(wgt * 16777216.0f);
-  return true;
+// Forward evaluation of the two pixels of a lane against one record, branch-free so that the
+// two dependency chains interleave (no divergent control flow per pixel).  c0/c1: contributed;
+// f0/f1: alpha*T in 2^-24 fixed point.
+__device__ __forceinline__ void eval_fwd2(PixF& p0, PixF& p1, const WRec& s, float pxf, float pyf0, float pyf1,
+                                          uint32_t pos, bool& c0, bool& c1, uint32_t& f0, uint32_t& f1) {
+  const float dx = s.geo.x - pxf;
+  const float dy0 = s.geo.y - pyf0, dy1 = s.geo.y - pyf1;
+  const float pw0 = pinned_power(s.geo.z, s.geo.w, s.co.x, dx, dy0);
+  const float pw1 = pinned_power(s.geo.z, s.geo.w, s.co.x, dx, dy1);
+  const bool ok0 = !p0.done && pw0 <= 0.0f && pw0 >= s.co.z;
+  const bool ok1 = !p1.done && pw1 <= 0.0f && pw1 >= s.co.z;
+  const float a0 = fminf(0.99f, s.co.y * fast_exp(pw0));
+  const float a1 = fminf(0.99f, s.co.y * fast_exp(pw1));
+  const float t0 = p0.T * (1.0f - a0), t1 = p1.T * (1.0f - a1);
+  const bool stop0 = ok0 && t0 < 0.0001f, stop1 = ok1 && t1 < 0.0001f;
+  c0 = ok0 && !stop0;
+  c1 = ok1 && !stop1;
+  p0.done = p0.done || stop0;
+  p1.done = p1.done || stop1;
+  const float w0 = c0 ? a0 * p0.T : 0.f, w1 = c1 ? a1 * p1.T : 0.f;
+  p0.r += s.rgb.x * w0;
+  p0.g += s.rgb.y * w0;
+  p0.b += s.rgb.z * w0;
+  p1.r += s.rgb.x * w1;
+  p1.g += s.rgb.y * w1;
+  p1.b += s.rgb.z * w1;
+  p0.T = c0 ? t0 : p0.T;
+  p1.T = c1 ? t1 : p1.T;
+  p0.last = c0 ? pos : p0.last;
+  p1.last = c1 ? pos : p1.last;
+  f0 = __float2uint_rn(w0 * 16777216.0f);
+  f1 = __float2uint_rn(w1 * 16777216.0f);
 }
 
 template <bool kImportance>
@@ -106,13 +116,14 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
                                                          int32_t* __restrict__ n_contrib) {
   __shared__ WRec s_rec[kWarps][32];
   const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
-  const int tile = a.t_begin + blockIdx.x;
+  const int lt = int(__ldg(a.tile_perm + blockIdx.x));
+  const int tile = a.t_begin + lt;
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + 4 * warp + (lane >> 4), py1 = py0 + 2;
   const bool in0 = px < a.W && py0 < a.H, in1 = px < a.W && py1 < a.H;
-  const uint2 range = a.ranges[blockIdx.x];
+  const uint2 range = a.ranges[lt];
   const float pxf = float(px), pyf0 = float(py0), pyf1 = float(py1);
   const float x0 = float(tx * kTile), y0 = float(ty * kTile + 4 * warp);
   PixF p0{1.f, 0.f, 0.f, 0.f, 0u, !in0}, p1{1.f, 0.f, 0.f, 0.f, 0u, !in1};
@@ -130,9 +141,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
       m &= m - 1;
       const WRec s = mine[j];
       const uint32_t pos = base + j + 1 - range.x;
-      uint32_t f0 = 0, f1 = 0;
-      const bool c0 = eval_fwd(p0, s, pxf, pyf0, pos, f0);
-      const bool c1 = eval_fwd(p1, s, pxf, pyf1, pos, f1);
+      uint32_t f0, f1;
+      bool c0, c1;
+      eval_fwd2(p0, p1, s, pxf, pyf0, pyf1, pos, c0, c1, f0, f1);
       if (kImportance) {
         const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
         if (b0 | b1) {
@@ -187,38 +198,41 @@ __device__ __forceinline__ void init_pixb(PixB& p, bool inside, size_t pix, size
   }
 }
 
-// one backward evaluation, accumulating this pixel's partials into g[9]
-__device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float pxf, float pyf, uint32_t pos, float* g) {
-  if (pos >= p.last) return false;
-  const float dx = s.geo.x - pxf, dy = s.geo.y - pyf;
+// Backward evaluation of one pixel against one record (branch-free: `ok` predicates every
+// update so the two pixels of a lane interleave); accumulates the pixel's partials into g[9].
+__device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float dy, uint32_t pos, float* g) {
   const float power = pinned_power(s.geo.z, s.geo.w, s.co.x, dx, dy);
-  if (!(power <= 0.0f && power >= s.co.z)) return false;
+  const bool ok = pos < p.last && power <= 0.0f && power >= s.co.z;
   const float G = fast_exp(power);
   const float og = s.co.y * G;
   const float alpha = fminf(0.99f, og);
-  p.T = __fdividef(p.T, 1.0f - alpha);
-  const float wgt = alpha * p.T;
+  const float Tn = __fdividef(p.T, 1.0f - alpha);
+  p.T = ok ? Tn : p.T;
+  const float wgt = ok ? alpha * Tn : 0.f;
   g[6] += wgt * p.dr;
   g[7] += wgt * p.dg;
   g[8] += wgt * p.db;
-  p.acc_r = p.last_alpha * p.last_r + (1.f - p.last_alpha) * p.acc_r;
-  p.acc_g = p.last_alpha * p.last_g + (1.f - p.last_alpha) * p.acc_g;
-  p.acc_b = p.last_alpha * p.last_b + (1.f - p.last_alpha) * p.acc_b;
-  p.last_alpha = alpha;
-  p.last_r = s.rgb.x;
-  p.last_g = s.rgb.y;
-  p.last_b = s.rgb.z;
-  const float dLda = p.T * ((s.rgb.x - p.acc_r) * p.dr + (s.rgb.y - p.acc_g) * p.dg + (s.rgb.z - p.acc_b) * p.db);
-  if (og <= 0.99f) {  // clamped alpha is constant: true derivative 0 (R14)
-    g[5] += G * dLda;
-    const float dpow = G * s.co.y * dLda;
-    g[0] -= dpow * (s.geo.z * dx + s.geo.w * dy);
-    g[1] -= dpow * (s.co.x * dy + s.geo.w * dx);
-    g[2] -= 0.5f * dpow * dx * dx;
-    g[3] -= dpow * dx * dy;
-    g[4] -= 0.5f * dpow * dy * dy;
-  }
-  return true;
+  const float ar = p.last_alpha * p.last_r + (1.f - p.last_alpha) * p.acc_r;
+  const float ag = p.last_alpha * p.last_g + (1.f - p.last_alpha) * p.acc_g;
+  const float ab = p.last_alpha * p.last_b + (1.f - p.last_alpha) * p.acc_b;
+  p.acc_r = ok ? ar : p.acc_r;
+  p.acc_g = ok ? ag : p.acc_g;
+  p.acc_b = ok ? ab : p.acc_b;
+  p.last_alpha = ok ? alpha : p.last_alpha;
+  p.last_r = ok ? s.rgb.x : p.last_r;
+  p.last_g = ok ? s.rgb.y : p.last_g;
+  p.last_b = ok ? s.rgb.z : p.last_b;
+  const float dLda = Tn * ((s.rgb.x - ar) * p.dr + (s.rgb.y - ag) * p.dg + (s.rgb.z - ab) * p.db);
+  // clamped alpha is constant: true derivative 0 (R14)
+  const float gd = (ok && og <= 0.99f) ? G * dLda : 0.f;
+  g[5] += gd;
+  const float dpow = gd * s.co.y;
+  g[0] -= dpow * (s.geo.z * dx + s.geo.w * dy);
+  g[1] -= dpow * (s.co.x * dy + s.geo.w * dx);
+  g[2] -= 0.5f * dpow * dx * dx;
+  g[3] -= dpow * dx * dy;
+  g[4] -= 0.5f * dpow * dy * dy;
+  return ok;
 }
 
 __device__ __forceinline__ float xsel(bool hi, float a, float b) { return hi ? a : b; }
@@ -228,13 +242,14 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterArgs a, const flo
                                                          const int32_t* __restrict__ n_contrib) {
   __shared__ WRec s_rec[kWarps][32];
   const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
-  const int tile = a.t_begin + blockIdx.x;
+  const int lt = int(__ldg(a.tile_perm + blockIdx.x));
+  const int tile = a.t_begin + lt;
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int px = tx * kTile + (lane & 15);
   const int py0 = ty * kTile + 4 * warp + (lane >> 4), py1 = py0 + 2;
   const bool in0 = px < a.W && py0 < a.H, in1 = px < a.W && py1 < a.H;
-  const uint2 range = a.ranges[blockIdx.x];
+  const uint2 range = a.ranges[lt];
   const float pxf = float(px), pyf0 = float(py0), pyf1 = float(py1);
   const float x0 = float(tx * kTile), y0 = float(ty * kTile + 4 * warp);
   const size_t plane = size_t(a.W) * a.H;
@@ -262,8 +277,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterArgs a, const flo
       float g[9];
 #pragma unroll
       for (int k = 0; k < 9; ++k) g[k] = 0.f;
-      const bool c0 = eval_bwd(p0, s, pxf, pyf0, pos, g);
-      const bool c1 = eval_bwd(p1, s, pxf, pyf1, pos, g);
+      const float dx = s.geo.x - pxf;
+      const bool c0 = eval_bwd(p0, s, dx, s.geo.y - pyf0, pos, g);
+      const bool c1 = eval_bwd(p1, s, dx, s.geo.y - pyf1, pos, g);
       if (!__any_sync(0xffffffffu, c0 || c1)) continue;
       // transposed butterfly over g[0..7]: lane ends with the warp sum of g[my_idx]
       float v4[4], v2[2], v1;

@@ -46,7 +46,7 @@ struct bgs_ctx {
   // arena
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
-      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux;
+      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm;
   unsigned long long* h_counters = nullptr;  // pinned
   int64_t* h_misc = nullptr;                 // pinned scratch for routing sizes
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
@@ -390,7 +390,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux};
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -683,6 +683,9 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
     launch_ranges_fixup(a, P, s);
     CKS(launched(ctx));
   }
+  CKS(ensure(ctx, ctx->tile_perm, size_t(std::max(nt, 1)) * 4));
+  launch_tile_order(P_<uint2>(ctx->ranges), nt, P_<uint32_t>(ctx->tile_perm), s);
+  CKS(launched(ctx));
   ctx->stage = 3;
   return BGS_OK;
 }
@@ -703,6 +706,7 @@ static RasterArgs raster_args(bgs_ctx* ctx) {
   a.H = ctx->cam.H;
   a.acc = P_<Acc>(ctx->acc);
   a.aux = P_<float4>(ctx->aux);
+  a.tile_perm = P_<uint32_t>(ctx->tile_perm);
   return a;
 }
 

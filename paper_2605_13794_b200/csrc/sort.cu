@@ -364,4 +364,42 @@ void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s) {
   k_ranges_fixup<<<unsigned((P + 255) / 256), 256, 0, s>>>(a, P);
 }
 
+namespace {
+// Longest-list-first launch order for the raster kernels (LPT scheduling): a one-CTA counting
+// sort of the owned tiles by list length into 256 descending buckets.  The heaviest tiles
+// start in the first wave instead of extending the tail.
+__global__ void __launch_bounds__(1024) k_tile_order(const uint2* ranges, int n, uint32_t* perm) {
+  __shared__ uint32_t s_cnt[256];
+  __shared__ uint32_t s_max;
+  if (threadIdx.x < 256) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_max = 1;
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += blockDim.x) atomicMax(&s_max, ranges[t].y - ranges[t].x);
+  __syncthreads();
+  const uint32_t width = (s_max + 255) / 256;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const uint32_t b = min(255u, (ranges[t].y - ranges[t].x) / width);
+    atomicAdd(&s_cnt[255 - b], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int b = 0; b < 256; ++b) {
+      const uint32_t c = s_cnt[b];
+      s_cnt[b] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const uint32_t b = min(255u, (ranges[t].y - ranges[t].x) / width);
+    perm[atomicAdd(&s_cnt[255 - b], 1u)] = uint32_t(t);
+  }
+}
+}  // namespace
+
+void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* perm, cudaStream_t s) {
+  if (n_tiles > 0) k_tile_order<<<1, 1024, 0, s>>>(ranges, n_tiles, perm);
+}
+
 }  // namespace bgs
