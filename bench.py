@@ -141,7 +141,8 @@ def run_native(args):
     n_local = shard.n
     W, H = scene.cameras[0]["W"], scene.cameras[0]["H"]
     cams = [B.camera(c) for c in scene.cameras]
-    gate = B.lod_gate(True, scene.k_levels - 1, scene.d0) if gate_on else None
+    # d0: 4x the median camera distance (R19) so the gate is selective, not degenerate
+    gate = B.lod_gate(True, scene.k_levels - 1, scene.d0 * 4) if gate_on else None
     stream = torch.cuda.Stream(dev)
     grads = g.zeros_grads()
     radius = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
