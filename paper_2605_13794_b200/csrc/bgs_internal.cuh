@@ -35,11 +35,12 @@ static_assert(sizeof(Acc) == 48, "accumulator is 48 B");
 
 // Device counters (u64 each) in the ctx arena.
 enum Counter : int {
-  C_F = 0,        // packed: (records produced by project << 32) | |A^(m)|
+  C_F = 0,        // records produced by project
   C_PALL = 1,     // sum of rect areas (pairs over all tiles) of this rank's records
   C_NLOD = 2,     // |L^(m)|
-  C_NACT = 3,     // unused (|A^(m)| lives in the low half of C_F)
+  C_NACT = 3,     // |A^(m)|
   C_P = 4,        // pairs emitted for owned tiles
+  C_CAND = 5,     // candidates passing the conservative off-screen bound
   C_NCOUNTERS = 8
 };
 
@@ -70,6 +71,7 @@ struct ProjectArgs {
   uint32_t* rec_lidx;
   unsigned long long* counters;
   int32_t* tile_diff;        // nullable: (TY+1)*(TX+1) 2D difference array of rect coverage
+  uint32_t* cand;            // [n] candidate list written by k_cull
   int64_t rec_cap;
 };
 
@@ -170,6 +172,7 @@ struct ImportanceArgs {
   uint32_t* c_rad;
   uint32_t* c_vis;
   uint32_t* cull;
+  unsigned long long* wbuf;  // [n_items] scratch: w copied densely by the stats pass
 };
 struct ImpState;
 constexpr size_t kImpStateBytes = 128;

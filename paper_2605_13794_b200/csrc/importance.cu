@@ -74,7 +74,7 @@ __device__ __forceinline__ Item load_item(const ImportanceArgs& a, int64_t t) {
 }
 
 __device__ __forceinline__ unsigned long long load_w(const ImportanceArgs& a, int64_t t) {
-  return a.item_lidx ? a.acc[t].w : a.w_dense[t];
+  return a.wbuf ? a.wbuf[t] : (a.item_lidx ? a.acc[t].w : a.w_dense[t]);
 }
 
 __device__ __forceinline__ uint32_t gid_of(const ImportanceArgs& a, uint32_t lidx) {
@@ -96,6 +96,7 @@ __device__ void stats_body(const ImportanceArgs& a, unsigned long long* total) {
        t += int64_t(gridDim.x) * blockDim.x) {
     const Item it = load_item(a, t);
     wsum += it.w;
+    if (a.wbuf) a.wbuf[t] = it.w;  // dense copy for the radix rounds (8 B instead of a 48-B row)
     if (it.w) atomicAdd(&s_msb[63 - __clzll((long long)it.w)], 1u);
     if (it.a > 0) a.s[it.lidx] += (double(it.w) * (1.0 / 16777216.0)) / (double(it.a) + 1e-8);
     if (it.rad) a.c_rad[it.lidx] += 1u;

@@ -4,19 +4,20 @@
 // ("every GPU projects only its own local Gaussians"), §3.4 Eq.4-6 P:195-210 (LOD gate, cull).
 //
 // PINNED ARITHMETIC (D2): this translation unit is compiled with -fmad=false and
-// IEEE div/sqrt so that every float expression below rounds exactly as written; radius,
-// rect, tile ids and pair counts are integers derived from these floats and must be
-// bit-identical to the oracle's.  Expression trees are the ones listed in DESIGN.md §4.
+// IEEE div/sqrt so that every float expression of the exact projection rounds exactly as
+// written; radius, rect, tile ids and pair counts are integers derived from these floats and
+// must be bit-identical to the oracle's.  Expression trees are the ones listed in DESIGN.md §4.
 //
-// Two kernels, both HBM-bound:
-//  k_project (one thread per local Gaussian): 16-B (mu, o) + lod byte (+ cull bit) for
-//    everyone; quat/scale (32 B) issued up front when no gate/cull can drop the Gaussian,
-//    otherwise only for kept ones; EWA geometry, radius, rect; a warp-aggregated append of
-//    the 48-B record (colour left for k_color) + 4-B index; radius written for all.
-//  k_color (one thread per record): the 192-B SH row of in-frustum Gaussians only, as 12
-//    independent 128-bit loads in flight per thread, evaluated along the view direction.
-// Splitting keeps k_project at low register pressure (full occupancy for latency hiding) and
-// reads SH only for the F records.
+// Three kernels:
+//  k_cull (streaming, 4 Gaussians per thread, ~36 B read per Gaussian): the Eq.5 gate with its
+//    per-rank fallback, the Eq.6 cull column, the near plane and a CONSERVATIVE analytic bound
+//    on the splat radius; Gaussians that cannot produce a record get radius 0,
+//    the rest are compacted into a candidate list (one global atomic per CTA).
+//  k_project (candidates only): the exact pinned EWA projection, radius, rect; records are
+//    compacted per CTA and written coalesced through shared memory (one atomic per CTA chunk).
+//  k_color (records only): the 192-B SH row, 12 independent 128-bit loads per thread.
+// Per-warp global atomics on one counter were a bottleneck earlier (hundreds of thousands of
+// same-address atomics serialise at the L2): every counter here is touched once per CTA.
 #include "bgs_internal.cuh"
 
 namespace bgs {
@@ -40,271 +41,275 @@ __global__ void __launch_bounds__(256) k_gate_count(ProjectArgs a) {
   if (threadIdx.x == 0 && c) atomicAdd(a.counters + C_NLOD, (unsigned long long)c);
 }
 
+// a1 + the off-screen bound.  `active`: passed the gate and the cull column (|A^(m)|).
+// Returns whether the exact projection can produce a record.  The bound:
+// radius <= 3 sqrt(|J|_F^2 s_max^2 + 0.3 + sqrt(0.1)) + 1 with |J|_F^2 <= K / tz^2
+// (K = fx^2 (1 + Lx^2) + fy^2 (1 + Ly^2), L = clamp limits), widened by 1% + 2 px; a Gaussian
+// whose centre is further than that outside the image has an empty rect in the exact
+// computation too.  Approximate arithmetic is fine here: the margins dwarf its error.
+__device__ __forceinline__ bool cull_test(const ProjectArgs& a, int64_t i, bool& active) {
+  const bool filtered = a.gate_enabled || a.cull;
+  float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!filtered) sc = ldg4(a.scale + i);  // nothing can drop it before the bound: load now
+  const float4 mo = ldg4(a.mean_opac + i);
+  bool keep = true;
+  if (a.gate_enabled) {
+    const unsigned long long nl = *((volatile unsigned long long*)(a.counters + C_NLOD));
+    const bool fallback = (unsigned long long)a.fb_den * nl > (unsigned long long)a.fb_num * (unsigned long long)a.n;
+    if (!fallback) keep = lod_keep(a, mo, a.lod[i]);
+  }
+  if (keep && a.cull) keep = !((__ldg(a.cull + (i >> 5)) >> (i & 31)) & 1u);
+  active = keep;
+  if (!keep) return false;
+  if (filtered) sc = ldg4(a.scale + i);
+  const CameraK& cm = a.cam;
+  // same pinned expression as the exact path, so the near-plane decision is identical
+  const float tz = ((cm.R[6] * mo.x + cm.R[7] * mo.y) + cm.R[8] * mo.z) + cm.t[2];
+  if (!(tz > cm.near_clip)) return false;
+  const float tx = ((cm.R[0] * mo.x + cm.R[1] * mo.y) + cm.R[2] * mo.z) + cm.t[0];
+  const float ty = ((cm.R[3] * mo.x + cm.R[4] * mo.y) + cm.R[5] * mo.z) + cm.t[1];
+  const float iz = __fdividef(1.0f, tz);
+  const float mxb = cm.fx * (tx * iz) + cm.cx, myb = cm.fy * (ty * iz) + cm.cy;
+  const float smax = fmaxf(sc.x, fmaxf(sc.y, sc.z));
+  const float rb = 3.0f * sqrtf(a.cull_K * (smax * smax) * (iz * iz) + 0.62f) * 1.01f + 2.0f;
+  return !(mxb + rb < 0.0f || mxb - rb > float(16 * cm.TX + 1) || myb + rb < 0.0f ||
+           myb - rb > float(16 * cm.TY + 1));
+}
+
 struct ProjOut {
   float mx, my, A, B, C, depth, opac;
   float mux, muy, muz;  // parked in the record's colour slots for k_color
   uint32_t rect, area;
-  bool valid, active;
+  bool valid;
   int x0, y0, x1, y1;
 };
 
-__device__ __forceinline__ ProjOut project_one(const ProjectArgs& a, int64_t i) {
-  bool valid = false;
-  bool active = false;
-  float mx = 0.f, my = 0.f, cA = 0.f, cB = 0.f, cC = 0.f, depth = 0.f, opac = 0.f, mux = 0.f, muy = 0.f,
-        muz = 0.f;
-  int radius = 0;
-  uint32_t area = 0;
-  int x0 = 0, y0 = 0, x1 = 0, y1 = 0;
-  if (i < a.n) {
-    const bool filtered = a.gate_enabled || a.cull;
-    float4 q = make_float4(0.f, 0.f, 0.f, 0.f), sc = q;
-    if (!filtered) sc = ldg4(a.scale + i);  // nothing can drop it before the frustum test: load now
-    const float4 mo = ldg4(a.mean_opac + i);
-    // ---- a1: Eq.5 gate with per-rank fallback, then Eq.6 cull column
-    bool keep = true;
-    if (a.gate_enabled) {
-      const unsigned long long nl = *((volatile unsigned long long*)(a.counters + C_NLOD));
-      const bool fallback = (unsigned long long)a.fb_den * nl > (unsigned long long)a.fb_num * (unsigned long long)a.n;
-      if (!fallback) keep = lod_keep(a, mo, a.lod[i]);
-    }
-    if (keep && a.cull) keep = !((__ldg(a.cull + (i >> 5)) >> (i & 31)) & 1u);
-    active = keep;
-    if (keep) {
-      if (filtered) sc = ldg4(a.scale + i);
-      const CameraK& cm = a.cam;
-      // ---- a2: t_c = R mu + t
-      const float tx = ((cm.R[0] * mo.x + cm.R[1] * mo.y) + cm.R[2] * mo.z) + cm.t[0];
-      const float ty = ((cm.R[3] * mo.x + cm.R[4] * mo.y) + cm.R[5] * mo.z) + cm.t[1];
-      const float tz = ((cm.R[6] * mo.x + cm.R[7] * mo.y) + cm.R[8] * mo.z) + cm.t[2];
-      const float txtz = tx / tz, tytz = ty / tz;
-      // Conservative off-screen rejection before any covariance work:
-      // radius <= 3 sqrt(|J|_F^2 s_max^2 + 0.3 + sqrt(0.1)) + 1 with |J|_F^2 <= K / tz^2
-      // (K = fx^2 (1 + Lx^2) + fy^2 (1 + Ly^2), L = clamp limits), widened by 1% + 2 px; a
-      // Gaussian whose centre is further than that outside the image has an empty rect in the
-      // exact computation too, so the decision is unchanged.
-      bool maybe = tz > cm.near_clip;
-      if (maybe) {
-        const float mxb = cm.fx * txtz + cm.cx, myb = cm.fy * tytz + cm.cy;
-        const float smax = fmaxf(sc.x, fmaxf(sc.y, sc.z));
-        const float iz = __fdividef(1.0f, tz);
-        const float rb = 3.0f * sqrtf(a.cull_K * (smax * smax) * (iz * iz) + 0.62f) * 1.01f + 2.0f;
-        maybe = !(mxb + rb < 0.0f || mxb - rb > float(16 * cm.TX + 1) || myb + rb < 0.0f ||
-                  myb - rb > float(16 * cm.TY + 1));
-      }
-      if (maybe) q = ldg4(a.quat + i);
-      if (maybe) {
-        // Sigma = R(q) S S^T R(q)^T
-        const float xx = q.y * q.y, yy = q.z * q.z, zz = q.w * q.w;
-        const float xy = q.y * q.z, xz = q.y * q.w, yz = q.z * q.w;
-        const float wx = q.x * q.y, wy = q.x * q.z, wz = q.x * q.w;
-        const float Rq[3][3] = {{1.0f - 2.0f * (yy + zz), 2.0f * (xy - wz), 2.0f * (xz + wy)},
-                                {2.0f * (xy + wz), 1.0f - 2.0f * (xx + zz), 2.0f * (yz - wx)},
-                                {2.0f * (xz - wy), 2.0f * (yz + wx), 1.0f - 2.0f * (xx + yy)}};
-        const float s3[3] = {sc.x, sc.y, sc.z};
-        float M[3][3];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) M[r][c] = Rq[r][c] * s3[c];
-        float S[3][3];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) S[r][c] = (M[r][0] * M[c][0] + M[r][1] * M[c][1]) + M[r][2] * M[c][2];
-        // EWA Jacobian with the 1.3 tan(fov/2) clamp (off-centre principal point); the four
-        // per-camera limits are computed once on the host with the same float expressions
-        const float lim_xp = a.lim[0], lim_xn = a.lim[1], lim_yp = a.lim[2], lim_yn = a.lim[3];
-        const float ctx = fminf(lim_xp, fmaxf(-lim_xn, txtz)) * tz;
-        const float cty = fminf(lim_yp, fmaxf(-lim_yn, tytz)) * tz;
-        const float J00 = cm.fx / tz, J02 = -(cm.fx * ctx) / (tz * tz);
-        const float J11 = cm.fy / tz, J12 = -(cm.fy * cty) / (tz * tz);
-        float Tm[2][3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          Tm[0][c] = J00 * cm.R[c] + J02 * cm.R[6 + c];
-          Tm[1][c] = J11 * cm.R[3 + c] + J12 * cm.R[6 + c];
-        }
-        float U[2][3];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) U[r][c] = (Tm[r][0] * S[0][c] + Tm[r][1] * S[1][c]) + Tm[r][2] * S[2][c];
-        float ca = (U[0][0] * Tm[0][0] + U[0][1] * Tm[0][1]) + U[0][2] * Tm[0][2];
-        const float cb = (U[0][0] * Tm[1][0] + U[0][1] * Tm[1][1]) + U[0][2] * Tm[1][2];
-        float cc = (U[1][0] * Tm[1][0] + U[1][1] * Tm[1][1]) + U[1][2] * Tm[1][2];
-        ca = ca + 0.3f;
-        cc = cc + 0.3f;
-        const float det = ca * cc - cb * cb;
-        if (det > 0.0f) {
-          cA = cc / det;
-          cB = (-cb) / det;
-          cC = ca / det;
-          mx = cm.fx * txtz + cm.cx;
-          my = cm.fy * tytz + cm.cy;
-          const float mid = 0.5f * (ca + cc);
-          const float disc = fmaxf(0.1f, mid * mid - det);
-          const float lambda1 = mid + sqrtf(disc);
-          const float rf = fminf(ceilf(3.0f * sqrtf(lambda1)), 1048576.0f);
-          const int rad = int(rf);
-          const float r_ = float(rad);
-          const float fx0 = (mx - r_) / 16.0f;
-          const float fy0 = (my - r_) / 16.0f;
-          const float fx1 = ((mx + r_) + 15.0f) / 16.0f;
-          const float fy1 = ((my + r_) + 15.0f) / 16.0f;
-          x0 = int(fminf(float(cm.TX), fmaxf(0.0f, fx0)));
-          y0 = int(fminf(float(cm.TY), fmaxf(0.0f, fy0)));
-          x1 = int(fminf(float(cm.TX), fmaxf(0.0f, fx1)));
-          y1 = int(fminf(float(cm.TY), fmaxf(0.0f, fy1)));
-          area = uint32_t((x1 - x0) * (y1 - y0));
-          if (area != 0) {
-            valid = true;
-            radius = rad;
-            depth = tz;
-            opac = mo.w;
-            if (!a.no_color) {
-              mux = mo.x;
-              muy = mo.y;
-              muz = mo.z;
-            }
-          }
-        }
-      }
-    }
-    a.radius[i] = valid ? radius : 0;
-  }
+// The exact a2 projection of a candidate (passed the gate, the cull column and the bound).
+__device__ __forceinline__ ProjOut project_exact(const ProjectArgs& a, int64_t i) {
   ProjOut o;
-  o.mx = mx;
-  o.my = my;
-  o.A = cA;
-  o.B = cB;
-  o.C = cC;
-  o.depth = depth;
-  o.opac = opac;
-  o.mux = mux;
-  o.muy = muy;
-  o.muz = muz;
-  o.rect = uint32_t(x0) | (uint32_t(y0) << 8) | (uint32_t(x1) << 16) | (uint32_t(y1) << 24);
-  o.area = area;
-  o.valid = valid;
-  o.active = active;
-  o.x0 = x0;
-  o.y0 = y0;
-  o.x1 = x1;
-  o.y1 = y1;
+  o.valid = false;
+  o.area = 0;
+  o.x0 = o.y0 = o.x1 = o.y1 = 0;
+  o.mx = o.my = o.A = o.B = o.C = o.depth = o.opac = o.mux = o.muy = o.muz = 0.f;
+  int radius = 0;
+  const float4 mo = ldg4(a.mean_opac + i);
+  const float4 sc = ldg4(a.scale + i);
+  const float4 q = ldg4(a.quat + i);
+  const CameraK& cm = a.cam;
+  // ---- t_c = R mu + t
+  const float tx = ((cm.R[0] * mo.x + cm.R[1] * mo.y) + cm.R[2] * mo.z) + cm.t[0];
+  const float ty = ((cm.R[3] * mo.x + cm.R[4] * mo.y) + cm.R[5] * mo.z) + cm.t[1];
+  const float tz = ((cm.R[6] * mo.x + cm.R[7] * mo.y) + cm.R[8] * mo.z) + cm.t[2];
+  const float txtz = tx / tz, tytz = ty / tz;
+  if (tz > cm.near_clip) {
+    // Sigma = R(q) S S^T R(q)^T
+    const float xx = q.y * q.y, yy = q.z * q.z, zz = q.w * q.w;
+    const float xy = q.y * q.z, xz = q.y * q.w, yz = q.z * q.w;
+    const float wx = q.x * q.y, wy = q.x * q.z, wz = q.x * q.w;
+    const float Rq[3][3] = {{1.0f - 2.0f * (yy + zz), 2.0f * (xy - wz), 2.0f * (xz + wy)},
+                            {2.0f * (xy + wz), 1.0f - 2.0f * (xx + zz), 2.0f * (yz - wx)},
+                            {2.0f * (xz - wy), 2.0f * (yz + wx), 1.0f - 2.0f * (xx + yy)}};
+    const float s3[3] = {sc.x, sc.y, sc.z};
+    float M[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) M[r][c] = Rq[r][c] * s3[c];
+    float S[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) S[r][c] = (M[r][0] * M[c][0] + M[r][1] * M[c][1]) + M[r][2] * M[c][2];
+    // EWA Jacobian with the 1.3 tan(fov/2) clamp (off-centre principal point); the four
+    // per-camera limits are computed once on the host with the same float expressions
+    const float lim_xp = a.lim[0], lim_xn = a.lim[1], lim_yp = a.lim[2], lim_yn = a.lim[3];
+    const float ctx = fminf(lim_xp, fmaxf(-lim_xn, txtz)) * tz;
+    const float cty = fminf(lim_yp, fmaxf(-lim_yn, tytz)) * tz;
+    const float J00 = cm.fx / tz, J02 = -(cm.fx * ctx) / (tz * tz);
+    const float J11 = cm.fy / tz, J12 = -(cm.fy * cty) / (tz * tz);
+    float Tm[2][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      Tm[0][c] = J00 * cm.R[c] + J02 * cm.R[6 + c];
+      Tm[1][c] = J11 * cm.R[3 + c] + J12 * cm.R[6 + c];
+    }
+    float U[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) U[r][c] = (Tm[r][0] * S[0][c] + Tm[r][1] * S[1][c]) + Tm[r][2] * S[2][c];
+    float ca = (U[0][0] * Tm[0][0] + U[0][1] * Tm[0][1]) + U[0][2] * Tm[0][2];
+    const float cb = (U[0][0] * Tm[1][0] + U[0][1] * Tm[1][1]) + U[0][2] * Tm[1][2];
+    float cc = (U[1][0] * Tm[1][0] + U[1][1] * Tm[1][1]) + U[1][2] * Tm[1][2];
+    ca = ca + 0.3f;
+    cc = cc + 0.3f;
+    const float det = ca * cc - cb * cb;
+    if (det > 0.0f) {
+      o.A = cc / det;
+      o.B = (-cb) / det;
+      o.C = ca / det;
+      o.mx = cm.fx * txtz + cm.cx;
+      o.my = cm.fy * tytz + cm.cy;
+      const float mid = 0.5f * (ca + cc);
+      const float disc = fmaxf(0.1f, mid * mid - det);
+      const float lambda1 = mid + sqrtf(disc);
+      const float rf = fminf(ceilf(3.0f * sqrtf(lambda1)), 1048576.0f);
+      const int rad = int(rf);
+      const float r_ = float(rad);
+      const float fx0 = (o.mx - r_) / 16.0f;
+      const float fy0 = (o.my - r_) / 16.0f;
+      const float fx1 = ((o.mx + r_) + 15.0f) / 16.0f;
+      const float fy1 = ((o.my + r_) + 15.0f) / 16.0f;
+      o.x0 = int(fminf(float(cm.TX), fmaxf(0.0f, fx0)));
+      o.y0 = int(fminf(float(cm.TY), fmaxf(0.0f, fy0)));
+      o.x1 = int(fminf(float(cm.TX), fmaxf(0.0f, fx1)));
+      o.y1 = int(fminf(float(cm.TY), fmaxf(0.0f, fy1)));
+      o.area = uint32_t((o.x1 - o.x0) * (o.y1 - o.y0));
+      if (o.area != 0) {
+        o.valid = true;
+        radius = rad;
+        o.depth = tz;
+        o.opac = mo.w;
+        if (!a.no_color) {
+          o.mux = mo.x;
+          o.muy = mo.y;
+          o.muz = mo.z;
+        }
+      }
+    }
+  }
+  a.radius[i] = o.valid ? radius : 0;
+  o.rect = uint32_t(o.x0) | (uint32_t(o.y0) << 8) | (uint32_t(o.x1) << 16) | (uint32_t(o.y1) << 24);
+  if (!o.valid) o.area = 0;
   return o;
 }
 
-// Block-level compaction: a CTA projects kProjChunk consecutive Gaussians, assigns its records
-// block-local slots with a deterministic scan (item round, warp, lane), stages them in shared
-// memory, takes ONE global slot range (a single 64-bit atomic packing F and |A|, plus one for
-// P_all) and writes the records out coalesced.  Per-warp global atomics on one counter were
-// the bottleneck (hundreds of thousands of same-address atomics serialise at the L2).
-constexpr int kProjPer = 2;
-constexpr int kProjChunk = 256 * kProjPer;
-
-__global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
-  __shared__ float4 s_rec[kProjChunk * 3];
-  __shared__ uint32_t s_lidx[kProjChunk];
-  __shared__ uint32_t s_cnt[kProjPer * 8];
-  __shared__ uint32_t s_act[8];
-  __shared__ unsigned long long s_area[8];
-  __shared__ unsigned long long s_base;
-  __shared__ uint32_t s_total;
+// Deterministic block-local slots for flagged items (order: item round, warp, lane) and one
+// global range per CTA.  Returns the CTA's base; `ls` receives the block-local slot.
+template <int PER>
+__device__ __forceinline__ unsigned long long block_compact(const bool (&flag)[PER], uint32_t (&ls)[PER],
+                                                            unsigned long long* counter, uint32_t* s_cnt,
+                                                            uint32_t& total, unsigned long long* s_base,
+                                                            uint32_t* s_total) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t chunk0 = int64_t(blockIdx.x) * kProjChunk;
-  ProjOut o[kProjPer];
-  uint32_t nact = 0;
-  unsigned long long area = 0;
+  uint32_t rk[PER];
 #pragma unroll
-  for (int k = 0; k < kProjPer; ++k) {
-    const int64_t i = chunk0 + k * 256 + tid;
-    if (i < a.n) {
-      o[k] = project_one(a, i);
-    } else {
-      o[k].valid = false;
-      o[k].active = false;
-      o[k].area = 0;
-    }
-    nact += o[k].active ? 1u : 0u;
-    area += o[k].area;
-  }
-  uint32_t rank_in_warp[kProjPer];
-#pragma unroll
-  for (int k = 0; k < kProjPer; ++k) {
-    const unsigned m = __ballot_sync(0xffffffffu, o[k].valid);
-    rank_in_warp[k] = __popc(m & ((1u << lane) - 1u));
+  for (int k = 0; k < PER; ++k) {
+    const unsigned m = __ballot_sync(0xffffffffu, flag[k]);
+    rk[k] = __popc(m & ((1u << lane) - 1u));
     if (lane == 0) s_cnt[k * 8 + warp] = __popc(m);
-  }
-  const uint32_t wact = __reduce_add_sync(0xffffffffu, nact);
-  unsigned long long warea = area;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) warea += __shfl_xor_sync(0xffffffffu, warea, off);
-  if (lane == 0) {
-    s_act[warp] = wact;
-    s_area[warp] = warea;
   }
   __syncthreads();
   if (tid == 0) {
-    uint32_t run = 0, act = 0;
-    unsigned long long ar = 0;
-    for (int j = 0; j < kProjPer * 8; ++j) {
+    uint32_t run = 0;
+    for (int j = 0; j < PER * 8; ++j) {
       const uint32_t c = s_cnt[j];
       s_cnt[j] = run;
       run += c;
     }
-    for (int w = 0; w < 8; ++w) {
-      act += s_act[w];
-      ar += s_area[w];
-    }
-    s_total = run;
-    unsigned long long base = 0;
-    if (run || act) base = atomicAdd(a.counters + C_F, ((unsigned long long)run << 32) | act) >> 32;
-    if (ar) atomicAdd(a.counters + C_PALL, ar);
-    s_base = base;
+    *s_total = run;
+    *s_base = run ? atomicAdd(counter, (unsigned long long)run) : 0ull;
   }
   __syncthreads();
-  const unsigned long long base = s_base;
 #pragma unroll
-  for (int k = 0; k < kProjPer; ++k) {
-    if (!o[k].valid) continue;
-    const uint32_t ls = s_cnt[k * 8 + warp] + rank_in_warp[k];
+  for (int k = 0; k < PER; ++k) ls[k] = s_cnt[k * 8 + warp] + rk[k];
+  total = *s_total;
+  return *s_base;
+}
+
+constexpr int kCullPer = 4;
+constexpr int kCullChunk = 256 * kCullPer;
+
+__global__ void __launch_bounds__(256) k_cull(ProjectArgs a) {
+  __shared__ uint32_t s_idx[kCullChunk];
+  __shared__ uint32_t s_cnt[kCullPer * 8];
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_total;
+  __shared__ uint32_t s_act;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_act = 0;
+  const int64_t chunk0 = int64_t(blockIdx.x) * kCullChunk;
+  bool maybe[kCullPer];
+  uint32_t nact = 0;
+#pragma unroll
+  for (int k = 0; k < kCullPer; ++k) {
     const int64_t i = chunk0 + k * 256 + tid;
-    const uint32_t gid = uint32_t(i) * uint32_t(a.world) + uint32_t(a.rank);
-    s_rec[3 * ls + 0] = make_float4(o[k].mx, o[k].my, o[k].A, o[k].B);
-    s_rec[3 * ls + 1] = make_float4(o[k].C, o[k].opac, o[k].mux, o[k].muy);
-    s_rec[3 * ls + 2] = make_float4(o[k].muz, o[k].depth, __uint_as_float(gid), __uint_as_float(o[k].rect));
-    s_lidx[ls] = uint32_t(i);
-    if (a.tile_diff) {
-      // 2D difference array of rect coverage -> per-tile pair counts (a3 input)
-      const int W1 = a.cam.TX + 1;
-      atomicAdd(a.tile_diff + o[k].y0 * W1 + o[k].x0, 1);
-      atomicAdd(a.tile_diff + o[k].y0 * W1 + o[k].x1, -1);
-      atomicAdd(a.tile_diff + o[k].y1 * W1 + o[k].x0, -1);
-      atomicAdd(a.tile_diff + o[k].y1 * W1 + o[k].x1, 1);
-    }
+    bool act = false;
+    maybe[k] = i < a.n && cull_test(a, i, act);
+    nact += act ? 1u : 0u;
+    if (i < a.n && !maybe[k]) a.radius[i] = 0;
   }
+  const uint32_t wact = __reduce_add_sync(0xffffffffu, nact);
+  uint32_t ls[kCullPer], total;
+  const unsigned long long base = block_compact<kCullPer>(maybe, ls, a.counters + C_CAND, s_cnt, total, &s_base,
+                                                          &s_total);
+  if ((tid & 31) == 0 && wact) atomicAdd(&s_act, wact);
+#pragma unroll
+  for (int k = 0; k < kCullPer; ++k)
+    if (maybe[k]) s_idx[ls[k]] = uint32_t(chunk0 + k * 256 + tid);
   __syncthreads();
-  const uint32_t total = s_total;
-  float4* dst = reinterpret_cast<float4*>(a.recs + base);
-  for (uint32_t j = tid; j < 3 * total; j += 256)
-    if (base + j / 3 < (unsigned long long)a.rec_cap) dst[j] = s_rec[j];
-  for (uint32_t j = tid; j < total; j += 256)
-    if (base + j < (unsigned long long)a.rec_cap) a.rec_lidx[base + j] = s_lidx[j];
+  if (tid == 0 && s_act) atomicAdd(a.counters + C_NACT, (unsigned long long)s_act);
+  for (uint32_t j = tid; j < total; j += 256) a.cand[base + j] = s_idx[j];
 }
 
-__device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f);
-__device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f) { color_one_impl(a, f); }
-
-// SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2.
-// Persistent grid-stride over the F records (F read on the device: no host round trip).
-__global__ void __launch_bounds__(256) k_color(ProjectArgs a) {
-  const int64_t F = int64_t(*((volatile unsigned long long*)(a.counters + C_F)) >> 32);
-  for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < F; f += int64_t(gridDim.x) * blockDim.x)
-    color_one(a, f);
+// Persistent grid over the candidate list (count read on the device).
+__global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
+  __shared__ float4 s_rec[256 * 3];
+  __shared__ uint32_t s_lidx[256];
+  __shared__ uint32_t s_cnt[8];
+  __shared__ unsigned long long s_area[8];
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n_cand = int64_t(*((volatile unsigned long long*)(a.counters + C_CAND)));
+  for (int64_t c0 = int64_t(blockIdx.x) * 256; c0 < n_cand; c0 += int64_t(gridDim.x) * 256) {
+    const int64_t c = c0 + tid;
+    ProjOut o;
+    o.valid = false;
+    o.area = 0;
+    uint32_t i = 0;
+    if (c < n_cand) {
+      i = a.cand[c];
+      o = project_exact(a, i);
+    }
+    unsigned long long area = o.area;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) area += __shfl_xor_sync(0xffffffffu, area, off);
+    if (lane == 0) s_area[warp] = area;
+    const bool flag[1] = {o.valid};
+    uint32_t ls[1], total;
+    const unsigned long long base = block_compact<1>(flag, ls, a.counters + C_F, s_cnt, total, &s_base, &s_total);
+    if (tid == 0) {
+      unsigned long long ar = 0;
+      for (int w = 0; w < 8; ++w) ar += s_area[w];
+      if (ar) atomicAdd(a.counters + C_PALL, ar);
+    }
+    if (o.valid) {
+      const uint32_t gid = i * uint32_t(a.world) + uint32_t(a.rank);
+      s_rec[3 * ls[0] + 0] = make_float4(o.mx, o.my, o.A, o.B);
+      s_rec[3 * ls[0] + 1] = make_float4(o.C, o.opac, o.mux, o.muy);
+      s_rec[3 * ls[0] + 2] = make_float4(o.muz, o.depth, __uint_as_float(gid), __uint_as_float(o.rect));
+      s_lidx[ls[0]] = i;
+      if (a.tile_diff) {
+        // 2D difference array of rect coverage -> per-tile pair counts (a3 input)
+        const int W1 = a.cam.TX + 1;
+        atomicAdd(a.tile_diff + o.y0 * W1 + o.x0, 1);
+        atomicAdd(a.tile_diff + o.y0 * W1 + o.x1, -1);
+        atomicAdd(a.tile_diff + o.y1 * W1 + o.x0, -1);
+        atomicAdd(a.tile_diff + o.y1 * W1 + o.x1, 1);
+      }
+    }
+    __syncthreads();
+    float4* dst = reinterpret_cast<float4*>(a.recs + base);
+    for (uint32_t j = tid; j < 3 * total; j += 256)
+      if (base + j / 3 < (unsigned long long)a.rec_cap) dst[j] = s_rec[j];
+    for (uint32_t j = tid; j < total; j += 256)
+      if (base + j < (unsigned long long)a.rec_cap) a.rec_lidx[base + j] = s_lidx[j];
+    __syncthreads();
+  }
 }
 
-__device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f) {
+__device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f) {
   const uint32_t i = a.rec_lidx[f];
   const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i);
   float v[48];
@@ -355,6 +360,25 @@ __device__ __forceinline__ void color_one_impl(const ProjectArgs& a, int64_t f) 
   rp[8] = col[2];
 }
 
+// SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2.
+// Persistent grid-stride over the F records (F read on the device: no host round trip).
+__global__ void __launch_bounds__(256) k_color(ProjectArgs a) {
+  const int64_t F = int64_t(*((volatile unsigned long long*)(a.counters + C_F)));
+  for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < F; f += int64_t(gridDim.x) * blockDim.x)
+    color_one(a, f);
+}
+
+int persistent_blocks(int per_sm) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms * per_sm;
+}
+
 }  // namespace
 
 void launch_gate_count(const ProjectArgs& a, cudaStream_t s) {
@@ -365,15 +389,14 @@ void launch_gate_count(const ProjectArgs& a, cudaStream_t s) {
 
 void launch_project(const ProjectArgs& a, cudaStream_t s) {
   if (a.n <= 0) return;
-  const int64_t blocks = (a.n + kProjChunk - 1) / kProjChunk;
-  k_project<<<unsigned(blocks), 256, 0, s>>>(a);
+  const int64_t blocks = (a.n + kCullChunk - 1) / kCullChunk;
+  k_cull<<<unsigned(blocks), 256, 0, s>>>(a);
+  k_project<<<persistent_blocks(6), 256, 0, s>>>(a);
 }
 
 void launch_color(const ProjectArgs& a, cudaStream_t s) {
   if (a.n <= 0 || a.no_color) return;
-  int64_t blocks = (a.n + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  k_color<<<unsigned(blocks), 256, 0, s>>>(a);
+  k_color<<<persistent_blocks(8), 256, 0, s>>>(a);
 }
 
 }  // namespace bgs

@@ -46,7 +46,7 @@ struct bgs_ctx {
   // arena
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
-      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm;
+      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf;
   unsigned long long* h_counters = nullptr;  // pinned
   int64_t* h_misc = nullptr;                 // pinned scratch for routing sizes
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
@@ -390,7 +390,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm};
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -500,8 +500,10 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
   a.radius = radius_out;
   CKS(ensure(ctx, ctx->recs, size_t(std::max<int64_t>(g->n_local, 1)) * sizeof(Rec)));
   CKS(ensure(ctx, ctx->rec_lidx, size_t(std::max<int64_t>(g->n_local, 1)) * 4));
+  CKS(ensure(ctx, ctx->cand, size_t(std::max<int64_t>(g->n_local, 1)) * 4));
   a.recs = P_<Rec>(ctx->recs);
   a.rec_lidx = P_<uint32_t>(ctx->rec_lidx);
+  a.cand = P_<uint32_t>(ctx->cand);
   a.rec_cap = g->n_local;
   a.counters = P_<unsigned long long>(ctx->counters);
   CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_NCOUNTERS, s));
@@ -518,7 +520,7 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
   }
   if (a.n > 0) {
     launch_project(a, s);
-    CKS(launched(ctx));
+    CKS(launched(ctx, 2));
     if (!a.no_color) {
       launch_color(a, s);
       CKS(launched(ctx));
@@ -527,8 +529,8 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
   CK(cudaMemcpyAsync(ctx->h_counters, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
                      cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  ctx->F = int64_t(ctx->h_counters[C_F] >> 32);  // packed (F << 32) | |A|
-  ctx->n_act = int64_t(ctx->h_counters[C_F] & 0xffffffffull);
+  ctx->F = int64_t(ctx->h_counters[C_F]);
+  ctx->n_act = int64_t(ctx->h_counters[C_NACT]);
   ctx->P_all = int64_t(ctx->h_counters[C_PALL]);
   ctx->n_lod = a.gate_enabled ? int64_t(ctx->h_counters[C_NLOD]) : g->n_local;
   ctx->fallback = a.gate_enabled ? int((unsigned long long)a.fb_den * ctx->h_counters[C_NLOD] >
@@ -829,6 +831,8 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   a.c_rad = c_rad;
   a.c_vis = c_vis;
   a.cull = cull_out;
+  CKS(ensure(ctx, ctx->wbuf, size_t(std::max<int64_t>(a.n_items, 1)) * 8));
+  a.wbuf = P_<unsigned long long>(ctx->wbuf);
   const int WR = imp_w_rounds(), GR = imp_g_rounds();
   CKS(ensure(ctx, ctx->imp_state, kImpStateBytes));
   CKS(ensure(ctx, ctx->imp_total, 65 * 8));  // total + 64-bin MSB histogram
