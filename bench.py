@@ -115,20 +115,17 @@ def run_native(args):
     import paper_2605_13794_b200.bgs as B
     import synthetic as S
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2605_13794_b200 import dist as D
+
+    rank, world, local = D.env_rank_world()
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(dev))
-        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(B.unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        ctx = B.Context(rank, world, local, bytes(uid.cpu().numpy().tobytes()))
+        D.init("nccl", torch.device(dev))
+        uid = D.broadcast_bytes(B.unique_id() if rank == 0 else None, 128, torch.device(dev))
+        ctx = B.Context(rank, world, local, uid)
     else:
         ctx = B.Context(0, 1, local)
 
@@ -238,21 +235,16 @@ def run_native(args):
         clk = clocks.stop()
     torch.cuda.synchronize()
     barrier()
-    tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    total_ms_max = float(tmax.item())
+    total_ms_max = D.max_over_ranks(total_ms, torch.device(dev))
     ms_per_view = total_ms_max / args.steps
     views_per_s = 1000.0 / ms_per_view
 
     # ---- per-view workload statistics (summed over ranks)
     P_rank = float(np.mean([q["P"] for q in qs]))
-    stats = torch.tensor([P_rank, np.mean([q["F"] for q in qs]), np.mean([q["R"] for q in qs]),
-                          np.mean([q["D"] for q in qs]), np.mean([q["n_active"] for q in qs]), float(n_local)],
-                         dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats)
-    P_all, F_all, R_all, D_all, A_all, N_all = [float(x) for x in stats.cpu().numpy()]
+    stats = D.sum_over_ranks([P_rank, np.mean([q["F"] for q in qs]), np.mean([q["R"] for q in qs]),
+                              np.mean([q["D"] for q in qs]), np.mean([q["n_active"] for q in qs]), float(n_local)],
+                             torch.device(dev))
+    P_all, F_all, R_all, D_all, A_all, N_all = [float(x) for x in stats]
     pairs_per_s = P_all * views_per_s
 
     # ---- e2e: same metric through the host-buffer ABI call (H2D of dL/dC, D2H of the image)
@@ -272,10 +264,7 @@ def run_native(args):
                                  cull_cols[(args.warmup + k) % len(cams)] if cull_cols is not None else None, 0,
                                  radius, dl_host, rgb_host, grads, imp, stream)
             e2e_s += time.perf_counter() - t1
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_views = args.steps / float(te.item())
+    e2e_views = args.steps / D.max_over_ranks(e2e_s, torch.device(dev))
 
     # ---- roofline of every stage, dominant one reported at top level
     from paper_2605_13794_b200.roofline import stage_rooflines

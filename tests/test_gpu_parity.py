@@ -234,6 +234,46 @@ def test_gate_and_cull_bit_exact():
             gs.close()
 
 
+@pytest.mark.parametrize("config,view", [("rubble", 7)])
+def test_full_size_sampled(config, view):
+    """BASELINE configs[1] at full size (6M Gaussians, 1152x864) in the bench's launch
+    configuration: projection, records, the complete sorted pair sequence and ranges bit-exact;
+    pixels compared on a 1/16 sample of the tiles (the ones the oracle composites)."""
+    sc = S.gen_city(config)
+    cam = sc.cameras[view]
+    st = O.OracleStep(sc, cam, M=1, tile_frac=1.0 / 16)
+    gs = GpuStep(sc, cam, M=1, importance=False)
+    try:
+        assert np.array_equal(gs.radius, st.get("radius"))
+        rec = gs.rank[0]["records"]
+        order = np.argsort(rec["gid"])
+        valid = np.nonzero(st.get("radius") > 0)[0]
+        assert np.array_equal(rec["gid"][order], valid)
+        m2 = st.get("mean2d").reshape(-1, 2)[valid]
+        assert np.array_equal(rec["mx"][order].view(np.uint32), _f32(m2[:, 0]).view(np.uint32))
+        assert np.array_equal(rec["rgb"][order].view(np.uint32),
+                              _f32(st.get("rgb").reshape(-1, 3)[valid]).view(np.uint32))
+        o = gs.rank[0]
+        tiles = (o["keys"] >> np.uint64(31)).astype(np.int32)
+        assert np.array_equal(tiles, st.get("pair_tile", 0))
+        assert np.array_equal(o["recv"]["gid"][o["vals"]], st.get("pair_gid", 0))
+        assert np.array_equal(o["ranges"][:, 0], st.get("range_lo", 0))
+        H, W = cam["H"], cam["W"]
+        TX = (W + 15) // 16
+        sample = np.zeros((H, W), bool)
+        for t in range(0, TX * ((H + 15) // 16), 16):
+            ty, tx = divmod(t, TX)
+            sample[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
+        cand = st.get("et_margin").reshape(H, W) < ET_MARGIN
+        ok = sample & ~cand
+        assert ok.sum() > 0.05 * H * W
+        img = st.get("img").reshape(3, H, W)
+        assert np.abs(gs.img - img)[:, ok].max() <= 1e-4
+        assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
+    finally:
+        gs.close()
+
+
 @pytest.mark.parametrize("case", ["empty", "single", "ragged", "behind_and_offscreen"])
 def test_edge_cases(case):
     if case == "empty":
