@@ -284,7 +284,6 @@ def test_edge_cases(case):
     elif case == "ragged":
         sc = S.gen_tiny(n=3000, W=250, H=181, seed=4)
         sc.cameras = [S.make_camera(250, 181, np.eye(3), np.zeros(3))]
-    else:
     elif case == "behind_and_offscreen":
         sc = S.gen_small(3, 400, 64, 48, spread=4.0)
     else:
