@@ -140,7 +140,7 @@ bgs_status bgs_query(bgs_ctx* ctx, int64_t* out /*[BGS_Q_COUNT] host*/);
  * the producing stage):
  *   0 records [F]x48 B {mx,my,A,B, C,o,r,g, b,depth,gid,rect(x0|y0<<8|x1<<16|y1<<24)}
  *   1 record local index [F] u32       2 received records [R]x48 B (== 0 when world == 1)
- *   3 sorted keys [P] u64 ((tile-tile_begin)<<32 | f32 bits(depth))   4 sorted values [P] u32
+ *   3 sorted keys [P] u64 ((tile-tile_begin)<<31 | f32 bits(depth))   4 sorted values [P] u32
  *     (index into received records)    5 tile ranges [tile_end-tile_begin] uint2 [start,end)
  *   6 per-received-splat accumulators [R]x48 B {dL/d(mx,my,A,B,C,o,r,g,b) f32, a u32, w_fixed u64}
  *   7 per-local-record owner-summed accumulators [F]x48 B (same layout; == 6 when world == 1)

@@ -94,10 +94,7 @@ struct SortArgs {
   int n_passes;
   uint2* ranges;             // [t_end - t_begin]
   float4* aux;               // [n_recv] per-record raster constants (thr, half extent x, half extent y, -)
-  uint32_t* tile_count;      // [t_end - t_begin] pairs per owned tile (zeroed before k_emit)
 };
-constexpr int kTileSortMax = 4096;  // largest tile list sorted in shared memory (32 KB of keys)
-void launch_tile_sort(const SortArgs& a, cudaStream_t s);
 // emits pairs and digit histograms; returns nothing (P stays on device, counters[C_P])
 void launch_emit(const SortArgs& a, cudaStream_t s);
 void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches);

@@ -46,7 +46,7 @@ struct bgs_ctx {
   // arena
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
-      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, tile_count;
+      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf;
   unsigned long long* h_counters = nullptr;  // pinned
   int64_t* h_misc = nullptr;                 // pinned scratch for routing sizes
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
@@ -390,7 +390,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->tile_count};
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -642,7 +642,7 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   const int nt = ctx->t_end - ctx->t_begin;
   int tbits = 0;
   while ((1 << tbits) < std::max(nt, 1)) ++tbits;
-  ctx->n_passes = (32 + tbits + 7) / 8;  // key = (local tile << 32) | depth bits
+  ctx->n_passes = (31 + tbits + 7) / 8;
   SortArgs a{};
   a.recv = ctx->recv;
   a.n_recv = ctx->R;
@@ -669,9 +669,6 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   a.ranges = P_<uint2>(ctx->ranges);
   CKS(ensure(ctx, ctx->aux, size_t(std::max<int64_t>(ctx->R, 1)) * 16));
   a.aux = P_<float4>(ctx->aux);
-  CKS(ensure(ctx, ctx->tile_count, size_t(std::max(nt, 1)) * 4));
-  a.tile_count = P_<uint32_t>(ctx->tile_count);
-  CK(cudaMemsetAsync(ctx->tile_count.p, 0, size_t(std::max(nt, 1)) * 4, s));
   CK(cudaMemsetAsync(ctx->digit_hist.p, 0, kMaxSortPasses * 256 * 4, s));
   CK(cudaMemsetAsync(ctx->pass_ctrl.p, 0, 64 * 4, s));
   CK(cudaMemsetAsync(P_<unsigned long long>(ctx->counters) + C_P, 0, 8, s));
@@ -686,8 +683,7 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   CKS(launched(ctx, int(nl)));
   if (P > 0) {
     launch_ranges_fixup(a, P, s);
-    launch_tile_sort(a, s);
-    CKS(launched(ctx, 2));
+    CKS(launched(ctx));
   }
   CKS(ensure(ctx, ctx->tile_perm, size_t(std::max(nt, 1)) * 4));
   launch_tile_order(P_<uint2>(ctx->ranges), nt, P_<uint32_t>(ctx->tile_perm), s);

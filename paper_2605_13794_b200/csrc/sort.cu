@@ -3,8 +3,8 @@
 // PAPER.md P:152 ("rasterized by tile-based front-to-back alpha compositing"), Eq.2
 // (N(p) depth-ordered), SPEC S:116 / S:172 (ties by global id, reading R12).
 //
-// Key = (local tile << 32) | f32 bits(depth).  depth > near_clip > 0, so the unsigned order of
-// the float bits is the numeric order of the depths; tile digits are whole 8-bit passes.
+// Key = (local tile << 31) | f32 bits(depth).  depth > near_clip > 0, so bit 31 of the float
+// is 0 and the unsigned order of the bits is the numeric order of the depths.
 //
 // a5: one warp expands the rects of 32 received records cooperatively (slot = position in a
 //     rect, warp-scan + 5-step shuffle search for the owning lane), keeps the slots whose tile
@@ -32,10 +32,9 @@ constexpr uint32_t kValMask = (1u << 30) - 1u;
 constexpr int kCtrlActive = 0;   // [8]
 constexpr int kCtrlSel = 8;      // [7] input buffer of pass p
 constexpr int kCtrlPart = 16;    // [8] partition counters
-constexpr int kCtrlFallback = 24;  // 1: some tile exceeds kTileSortMax -> all-digit onesweep
 
 __device__ __forceinline__ unsigned long long make_key(uint32_t lt, float depth) {
-  return (static_cast<unsigned long long>(lt) << 32) | static_cast<unsigned long long>(__float_as_uint(depth));
+  return (static_cast<unsigned long long>(lt) << 31) | static_cast<unsigned long long>(__float_as_uint(depth));
 }
 
 __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
@@ -143,11 +142,6 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
       }
       for (int p = 0; p < npass; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
     }
-    // per-tile pair counts (one atomic per distinct tile of the warp chunk): the largest tile
-    // decides between the shared-memory tile sort and the all-digit onesweep fallback
-    const uint32_t tl = ok ? uint32_t(key >> 32) : 0xffffffffu;
-    const unsigned tpeers = __match_any_sync(0xffffffffu, tl);
-    if (ok && lane == __ffs(tpeers) - 1) atomicAdd(a.tile_count + tl, uint32_t(__popc(tpeers)));
     run += __popc(m);
   }
   __syncthreads();
@@ -158,27 +152,15 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
 }
 
 // One CTA: per pass, detect constant digits (inactive pass), exclusive-scan the digit
-// histogram in place, and assign ping-pong input selectors.  Fast path (every owned tile has at
-// most kTileSortMax pairs): only the tile-digit passes (key bits >= 32) run, i.e. onesweep
-// partitions the pairs by tile (MSD) and k_tile_sort orders each tile by depth in shared
-// memory.  Otherwise every digit pass runs (plain LSD onesweep over the whole key).
+// histogram in place, and assign ping-pong input selectors.
 __global__ void __launch_bounds__(256) k_digit_scan(SortArgs a) {
   __shared__ uint32_t s_scan[256];
   __shared__ int s_trivial;
-  __shared__ uint32_t s_maxtile;
   const unsigned long long P = a.counters[C_P];
-  if (threadIdx.x == 0) s_maxtile = 0;
-  __syncthreads();
-  uint32_t mx = 0;
-  for (int t = threadIdx.x; t < a.t_end - a.t_begin; t += blockDim.x) mx = max(mx, a.tile_count[t]);
-  atomicMax(&s_maxtile, mx);
-  __syncthreads();
-  const bool fallback = s_maxtile > uint32_t(kTileSortMax);
-  if (threadIdx.x == 0) a.pass_ctrl[kCtrlFallback] = fallback ? 1u : 0u;
   uint32_t sel = 0;
   for (int p = 0; p < a.n_passes; ++p) {
     const uint32_t c = a.digit_hist[p * 256 + threadIdx.x];
-    if (threadIdx.x == 0) s_trivial = (!fallback && 8 * p < 32) ? 1 : 0;  // depth digits: tile sort
+    if (threadIdx.x == 0) s_trivial = 0;
     __syncthreads();
     if ((unsigned long long)c == P) s_trivial = 1;  // all keys share this digit (also P == 0)
     s_scan[threadIdx.x] = c;
@@ -330,13 +312,12 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
   const unsigned long long* keys = sel ? a.keys[1] : a.keys[0];
   uint32_t* vals = sel ? a.vals[1] : a.vals[0];
   const unsigned long long k = keys[i];
-  const uint32_t t = uint32_t(k >> 32);
+  const uint32_t t = uint32_t(k >> 31);
   const unsigned long long kp = i > 0 ? keys[i - 1] : ~0ull;
   const unsigned long long kn = i + 1 < P ? keys[i + 1] : ~0ull;
-  if (i == 0 || uint32_t(kp >> 32) != t) a.ranges[t].x = uint32_t(i);
-  if (i + 1 == P || uint32_t(kn >> 32) != t) a.ranges[t].y = uint32_t(i + 1);
-  // fast path: depth is still unsorted inside each tile here; k_tile_sort breaks the ties
-  if (kn == k && kp != k && a.pass_ctrl[kCtrlFallback]) {
+  if (i == 0 || uint32_t(kp >> 31) != t) a.ranges[t].x = uint32_t(i);
+  if (i + 1 == P || uint32_t(kn >> 31) != t) a.ranges[t].y = uint32_t(i + 1);
+  if (kn == k && kp != k) {
     // run of identical (tile, depth) keys starting at i: order by global id (R12)
     int64_t e = i + 1;
     while (e + 1 < P && keys[e + 1] == k) ++e;
@@ -350,68 +331,6 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
       }
       vals[y + 1] = v;
     }
-  }
-}
-
-// Fast path, one CTA per owned tile: the tile's pairs (already grouped by the onesweep tile
-// passes) are sorted in shared memory by (depth bits, received index) with a bitonic network,
-// then runs of equal depth are re-ordered by global id (R12).  Writes keys and values back in
-// place.  No-op when the fallback (all-digit onesweep) ran.
-__global__ void __launch_bounds__(256) k_tile_sort(SortArgs a) {
-  extern __shared__ unsigned long long s_k[];
-  if (a.pass_ctrl[kCtrlFallback]) return;
-  const int lt = blockIdx.x;
-  const uint2 range = a.ranges[lt];
-  const int n = int(range.y - range.x);
-  if (n <= 1) return;
-  const uint32_t sel = a.pass_ctrl[kFinalSel];
-  unsigned long long* keys = (sel ? a.keys[1] : a.keys[0]) + range.x;
-  uint32_t* vals = (sel ? a.vals[1] : a.vals[0]) + range.x;
-  int np = 1;
-  while (np < n) np <<= 1;
-  for (int i = threadIdx.x; i < np; i += blockDim.x)
-    s_k[i] = i < n ? ((keys[i] & 0xffffffffull) << 32) | vals[i] : ~0ull;
-  __syncthreads();
-  for (int k = 2; k <= np; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < np; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long x = s_k[i], y = s_k[ixj];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) {
-            s_k[i] = y;
-            s_k[ixj] = x;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  // equal depth: order by global id instead of received index (tiny runs)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t d = uint32_t(s_k[i] >> 32);
-    const bool start = (i == 0 || uint32_t(s_k[i - 1] >> 32) != d) && i + 1 < n && uint32_t(s_k[i + 1] >> 32) == d;
-    if (!start) continue;
-    int e = i + 1;
-    while (e + 1 < n && uint32_t(s_k[e + 1] >> 32) == d) ++e;
-    for (int x = i + 1; x <= e; ++x) {
-      const unsigned long long v = s_k[x];
-      const uint32_t g = a.recv[uint32_t(v)].gid;
-      int y = x - 1;
-      while (y >= i && a.recv[uint32_t(s_k[y])].gid > g) {
-        s_k[y + 1] = s_k[y];
-        --y;
-      }
-      s_k[y + 1] = v;
-    }
-  }
-  __syncthreads();
-  const unsigned long long tile_hi = (unsigned long long)(uint32_t)lt << 32;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const unsigned long long v = s_k[i];
-    keys[i] = tile_hi | (v >> 32);
-    vals[i] = uint32_t(v);
   }
 }
 
@@ -478,12 +397,6 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* ranges, int n,
   }
 }
 }  // namespace
-
-void launch_tile_sort(const SortArgs& a, cudaStream_t s) {
-  const int nt = a.t_end - a.t_begin;
-  if (nt <= 0) return;
-  k_tile_sort<<<nt, 256, size_t(kTileSortMax) * 8, s>>>(a);
-}
 
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* perm, cudaStream_t s) {
   if (n_tiles > 0) k_tile_order<<<1, 1024, 0, s>>>(ranges, n_tiles, perm);
