@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--views", type=int, default=64)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--stages", action="store_true", help="also print per-stage timings to stderr")
+    p.add_argument("--layout", default="morton", choices=["morton", "input"],
+                   help="shard storage order: Z-order (bgs_spatial_order) or the generator's random ids")
     return p.parse_args()
 
 
@@ -136,6 +138,14 @@ def run_native(args):
     shard = scene.shard(rank, world)
     g = B.GaussianPlanes.from_scene(shard, dev)
     n_local = shard.n
+    if args.layout == "morton":
+        # framework layout: each shard stored in Z-order (bgs_spatial_order), ids relabelled
+        perm = B.spatial_order(ctx, g)
+        g = B.GaussianPlanes(g.mean_opac[perm].contiguous(), g.quat[perm].contiguous(), g.scale[perm].contiguous(),
+                             g.sh[perm].contiguous(), g.lod[perm].contiguous())
+        if world == 1:
+            scene = scene.subset(perm.cpu().numpy())  # the oracle baseline sees the same labelling
+        torch.cuda.synchronize()
     W, H = scene.cameras[0]["W"], scene.cameras[0]["H"]
     cams = [B.camera(c) for c in scene.cameras]
     # d0: 4x the median camera distance (R19) so the gate is selective, not degenerate
@@ -281,6 +291,7 @@ def run_native(args):
         "config": {"workload": label, "config": args.config, "gaussians": int(N_all), "width": W, "height": H,
                    "views": len(cams), "lod_gate": gate_on, "importance_mask": gate_on,
                    "parallelism": f"index-parity shards x {world}, tile-owner all-to-all",
+                   "shard_layout": args.layout,
                    "l2": "flushed between timed views (256 MB write); inputs also exceed L2"},
         "splat_pairs_per_s": round(pairs_per_s, 1),
         "per_view": {"pairs": P_all, "records_F": F_all, "received_R": R_all, "sent_D": D_all,

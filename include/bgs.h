@@ -218,6 +218,18 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
                               int32_t* radius_out, const float* dL_drgb_host, float* rgb_host,
                               const bgs_gaussian_grads* grads, const bgs_importance_out* importance, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Shard layout (not a step of the method; a one-time data-layout utility)
+ * --------------------------------------------------------------------------------------- */
+/* Z-order (Morton) permutation of a shard: perm_out[new] = old local index, from 16-bit-per-axis
+ * codes of mu over the shard's bounding box, sorted with the library's onesweep (ties keep index
+ * order).  The caller applies it to every per-Gaussian array (parameters, optimizer state) and
+ * relabels: after reordering, local j of rank m is global id j*world + m again (ids are labels;
+ * the paper renumbers on redistribution).  Spatially coherent shards make the
+ * per-view gathers of 16-B rows touch whole DRAM granules.  mean_opac: device float4[n];
+ * perm_out: device u32[n].  Invalidates the ctx's current view.  HOST-SYNC. */
+bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, uint32_t* perm_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,7 @@ _SIGS = {
     "bgs_importance": [_vp, C.c_int64, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp],
     "bgs_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_view_step_host": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_spatial_order": [_vp, _vp, C.c_int64, _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -337,6 +338,18 @@ def bgs_view_step_host(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, c
                                       C.byref(gr) if gr is not None else None,
                                       C.byref(importance) if importance is not None else None, _stream(stream)),
               "bgs_view_step_host")
+
+
+def bgs_spatial_order(ctx: Context, mean_opac: torch.Tensor, perm_out: torch.Tensor, stream=None):
+    ctx.check(_lib.bgs_spatial_order(ctx.handle, _ptr(mean_opac), int(mean_opac.shape[0]), _ptr(perm_out),
+                                     _stream(stream)), "bgs_spatial_order")
+
+
+def spatial_order(ctx: Context, g: GaussianPlanes) -> torch.Tensor:
+    """Z-order permutation of a shard (perm[new] = old local index), computed by libbgs."""
+    perm = torch.empty(max(g.n, 1), dtype=torch.int32, device=g.mean_opac.device)
+    bgs_spatial_order(ctx, g.mean_opac, perm)
+    return perm[:g.n].long()
 
 
 def importance_out(s, c_rad, c_vis, cull_out, num=99, den=100) -> bgs_importance_out:

@@ -16,7 +16,8 @@ BUILD = os.path.join(os.path.dirname(HERE), "build", "libbgs")
 LIB = os.path.join(HERE, "libbgs.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
-SOURCES = ["runtime.cu", "project.cu", "sort.cu", "raster.cu", "project_bwd.cu", "route.cu", "importance.cu"]
+SOURCES = ["runtime.cu", "project.cu", "sort.cu", "raster.cu", "project_bwd.cu", "route.cu", "importance.cu",
+           "layout.cu"]
 # per-TU extra flags: the projection TU is pinned (no FMA contraction; IEEE div/sqrt are the
 # nvcc defaults) so that integer decisions match the oracle bit for bit (D2)
 EXTRA = {"project.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"]}

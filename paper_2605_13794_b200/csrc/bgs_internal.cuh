@@ -100,6 +100,9 @@ void launch_emit(const SortArgs& a, cudaStream_t s);
 void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches);
 void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s);
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* perm, cudaStream_t s);
+// layout.cu: Morton permutation of a shard (keys/vals/digit_hist/pass_ctrl/status of `a` used as scratch)
+void launch_spatial_order(const float4* mean_opac, int64_t n, unsigned int* box, const SortArgs& a, uint32_t* perm,
+                          cudaStream_t s, int64_t* launches);
 // which buffer (0/1) holds the sorted data after the passes: read from pass_ctrl on device
 // by the consumers below.
 

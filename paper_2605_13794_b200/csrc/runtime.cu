@@ -871,6 +871,46 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   return BGS_OK;
 }
 
+bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, uint32_t* perm_out, void* stream) {
+  CKS(check_ctx(ctx));
+  if (n < 0 || (n > 0 && (!mean_opac || !perm_out))) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "spatial_order args");
+  if (n >= (int64_t(1) << 30)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "spatial_order: n >= 2^30");
+  if (n == 0) return BGS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ctx->stage = 0;  // reuses the sort scratch: the current view's intermediates are gone
+  SortArgs a{};
+  for (int b = 0; b < 2; ++b) {
+    CKS(ensure(ctx, ctx->keys[b], size_t(n) * 8));
+    CKS(ensure(ctx, ctx->vals[b], size_t(n) * 4));
+    a.keys[b] = P_<unsigned long long>(ctx->keys[b]);
+    a.vals[b] = P_<uint32_t>(ctx->vals[b]);
+  }
+  a.cap = n;
+  a.n_passes = 6;  // 48-bit codes
+  const int64_t n_parts = (n + kSortPart - 1) / kSortPart;
+  CKS(ensure(ctx, ctx->digit_hist, kMaxSortPasses * 256 * 4));
+  CKS(ensure(ctx, ctx->pass_ctrl, 64 * 4));
+  CKS(ensure(ctx, ctx->status, size_t(n_parts) * 256 * 4 * a.n_passes));
+  CKS(ensure(ctx, ctx->tile_diff, 64));  // bounding-box scratch
+  a.counters = P_<unsigned long long>(ctx->counters);
+  a.digit_hist = P_<uint32_t>(ctx->digit_hist);
+  a.pass_ctrl = P_<uint32_t>(ctx->pass_ctrl);
+  a.status = P_<uint32_t>(ctx->status);
+  CK(cudaMemsetAsync(ctx->digit_hist.p, 0, kMaxSortPasses * 256 * 4, s));
+  CK(cudaMemsetAsync(ctx->pass_ctrl.p, 0, 64 * 4, s));
+  CK(cudaMemsetAsync(ctx->status.p, 0, size_t(n_parts) * 256 * 4 * a.n_passes, s));
+  CK(cudaMemsetAsync(ctx->tile_diff.p, 0xff, 12, s));                       // min (ordered ints)
+  CK(cudaMemsetAsync(P_<char>(ctx->tile_diff) + 12, 0, 12, s));             // max
+  ctx->h_misc[63] = n;
+  CK(cudaMemcpyAsync(P_<unsigned long long>(ctx->counters) + C_P, ctx->h_misc + 63, 8, cudaMemcpyHostToDevice, s));
+  int64_t nl = 0;
+  launch_spatial_order(reinterpret_cast<const float4*>(mean_opac), n, P_<unsigned int>(ctx->tile_diff), a, perm_out,
+                       s, &nl);
+  CKS(launched(ctx, int(nl)));
+  CK(cudaStreamSynchronize(s));  // h_misc is reused
+  return BGS_OK;
+}
+
 bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
                          const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, float* rgb,
                          float* t_final, int32_t* n_contrib, const float* dL, const bgs_gaussian_grads* grads,
