@@ -67,31 +67,7 @@ __device__ __forceinline__ bool stage_test(const RasterArgs& a, const uint32_t* 
   out.geo = q0;
   out.co = make_float4(q1.x, q1.y, ax.x, __uint_as_float(r));
   out.rgb = make_float4(q1.z, q1.w, q2.x, 0.f);
-  const float x1 = x0 + 15.f, y1 = y0 + 3.f;
-  if (!((q0.x - ax.y <= x1) & (q0.x + ax.y >= x0) & (q0.y - ax.z <= y1) & (q0.y + ax.z >= y0))) return false;
-  // Exact test: min over the strip rectangle of the quadratic form q(d) = A dx^2 + 2B dx dy + C dy^2
-  // (d = mean - p) against k = -2 thr; the minimum of a convex quadratic over a rectangle is 0 if
-  // the mean is inside, else it lies on an edge, where it is a clamped 1D minimum.  Widened by
-  // 1e-3 relative + 1e-3 so no pixel that passes the pinned power test is ever culled.
-  const float mx = q0.x, my = q0.y, A = q0.z, B = q0.w, C = q1.x;
-  if (mx >= x0 && mx <= x1 && my >= y0 && my <= y1) return true;
-  const float k = -2.0f * ax.x;
-  float qmin = 3.4e38f;
-  // horizontal edges (dy fixed), minimise over dx in [mx - x1, mx - x0]
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const float dy = my - (e ? y1 : y0);
-    const float dx = fminf(mx - x0, fmaxf(mx - x1, -B * dy / A));
-    qmin = fminf(qmin, A * dx * dx + 2.f * B * dx * dy + C * dy * dy);
-  }
-  // vertical edges (dx fixed), minimise over dy in [my - y1, my - y0]
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const float dx = mx - (e ? x1 : x0);
-    const float dy = fminf(my - y0, fmaxf(my - y1, -B * dx / C));
-    qmin = fminf(qmin, A * dx * dx + 2.f * B * dx * dy + C * dy * dy);
-  }
-  return qmin <= k * 1.001f + 1e-3f;
+  return (q0.x - ax.y <= x0 + 15.f) & (q0.x + ax.y >= x0) & (q0.y - ax.z <= y0 + 3.f) & (q0.y + ax.z >= y0);
 }
 
 struct PixF {
