@@ -277,11 +277,13 @@ def run_native(args):
     e2e_views = args.steps / D.max_over_ranks(e2e_s, torch.device(dev))
 
     # ---- roofline of every stage, dominant one reported at top level
-    from paper_2605_13794_b200.roofline import stage_rooflines
+    from paper_2605_13794_b200.roofline import load_traffic, stage_rooflines
     peaks = load_peaks()
     stage_avg = stage_ms / args.steps
     roof = stage_rooflines(stage_avg, qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
-                           sm_mhz=clk.get("sm_mhz"), E=E_sum / args.steps, cull=cull_cols is not None)
+                           sm_mhz=clk.get("sm_mhz"), E=E_sum / args.steps, cull=cull_cols is not None,
+                           traffic=load_traffic(os.path.join(ROOT, "profiles", "ncu_traffic.json"))
+                           if args.config == "rubble" and world == 1 else None)
     dominant = max(roof, key=lambda r: r["ms"])
 
     result = {

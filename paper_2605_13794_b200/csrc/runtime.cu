@@ -49,6 +49,7 @@ struct bgs_ctx {
       imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf;
   unsigned long long* h_counters = nullptr;  // pinned
   int64_t* h_misc = nullptr;                 // pinned scratch for routing sizes
+  cudaEvent_t ev_counters = nullptr;         // counters copied to the host (bgs_project)
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
 };
 
@@ -395,6 +396,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
     if (b->p) cudaFree(b->p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
   if (c->h_misc) cudaFreeHost(c->h_misc);
+  if (c->ev_counters) cudaEventDestroy(c->ev_counters);
   c->tr.reset();
   delete c;
   return BGS_OK;
@@ -521,14 +523,19 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
   if (a.n > 0) {
     launch_project(a, s);
     CKS(launched(ctx, 2));
-    if (!a.no_color) {
-      launch_color(a, s);
-      CKS(launched(ctx));
-    }
   }
+  // The counters (F, P_all, ...) are final once the geometry kernels are done: copy them out
+  // and wait on that copy only, while the colour kernel keeps the device busy during the host
+  // round trip (the one host synchronisation of a world-1 step).
   CK(cudaMemcpyAsync(ctx->h_counters, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
                      cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  if (!ctx->ev_counters) CK(cudaEventCreateWithFlags(&ctx->ev_counters, cudaEventDisableTiming));
+  CK(cudaEventRecord(ctx->ev_counters, s));
+  if (a.n > 0 && !a.no_color) {
+    launch_color(a, s);
+    CKS(launched(ctx));
+  }
+  CK(cudaEventSynchronize(ctx->ev_counters));
   ctx->F = int64_t(ctx->h_counters[C_F]);
   ctx->n_act = int64_t(ctx->h_counters[C_NACT]);
   ctx->P_all = int64_t(ctx->h_counters[C_PALL]);

@@ -24,7 +24,9 @@ def _avg(qs, k):
     return sum(q[k] for q in qs) / max(1, len(qs))
 
 
-def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=None, cull=False):
+def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=None, cull=False, traffic=None):
+    """traffic: optional {stage: DRAM bytes per view} from a committed ncu capture (profiles/)."""
+    traffic = traffic or {}
     N = float(n_local)
     A, F, R, D, P = (_avg(qs, k) for k in ("n_active", "F", "R", "D", "P"))
     passes = _avg(qs, "sort_passes")
@@ -47,11 +49,21 @@ def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=No
         if name in ops:
             ach = ops[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
             out.append(dict(stage=name, ms=round(ms, 4), bound="alu", achieved=round(ach, 3), peak=round(alu, 2),
-                            unit="TFLOP/s", frac=round(ach / alu, 4), traffic=None,
+                            unit="TFLOP/s", frac=round(ach / alu, 4), traffic=traffic.get(name),
                             work=f"{ops[name]:.3e} ops ({FWD_OPS if name == 'raster_fwd' else BWD_OPS:.0f} x E)"))
         else:
             b = bytes_.get(name, 0.0)
             ach = b / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
             out.append(dict(stage=name, ms=round(ms, 4), bound="hbm", achieved=round(ach, 1), peak=hbm,
-                            unit="GB/s", frac=round(ach / hbm, 4), traffic=None, work=f"{b:.3e} bytes"))
+                            unit="GB/s", frac=round(ach / hbm, 4), traffic=traffic.get(name), work=f"{b:.3e} bytes"))
     return out
+
+
+def load_traffic(path):
+    """{stage: dram bytes per view} from profiles/ncu_traffic.json (profiles/make_traffic.py)."""
+    import json
+    import os
+    if not os.path.exists(path):
+        return {}
+    d = json.load(open(path))
+    return {k: v["dram_bytes_per_view"] for k, v in d.get("stages", {}).items()}
