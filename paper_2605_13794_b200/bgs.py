@@ -15,7 +15,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbgs.so")
+# BGS_LIB selects an in-tree A/B variant (libbgs_<name>.so, build.py --name); default libbgs.so
+LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ.get("BGS_LIB", "libbgs.so")))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libbgs.so not built ({LIB_PATH}); run `python -m paper_2605_13794_b200.build` "

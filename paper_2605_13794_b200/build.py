@@ -44,15 +44,15 @@ def nccl_root() -> str:
     raise RuntimeError("NCCL headers not found (expected nvidia/nccl in site-packages)")
 
 
-def _compile(src: str, force: bool) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-    deps = [os.path.join(CSRC, src), os.path.join(CSRC, "bgs_internal.cuh"), os.path.join(INCLUDE, "bgs.h")]
+def _compile(src: str, force: bool, csrc: str = CSRC, bdir: str = BUILD) -> str:
+    os.makedirs(bdir, exist_ok=True)
+    obj = os.path.join(bdir, src.replace(".cu", ".o"))
+    deps = [os.path.join(csrc, src), os.path.join(csrc, "bgs_internal.cuh"), os.path.join(INCLUDE, "bgs.h")]
     if not force and os.path.exists(obj) and all(os.path.getmtime(obj) >= os.path.getmtime(d) for d in deps):
         return obj
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "-I" + os.path.join(nccl_root(), "include"), "-I" + INCLUDE, *EXTRA.get(src, []),
-           "-c", os.path.join(CSRC, src), "-o", obj]
+           "-c", os.path.join(csrc, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(obj + ".log", "w") as f:
         f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
@@ -61,20 +61,31 @@ def _compile(src: str, force: bool) -> str:
     return obj
 
 
-def build(force: bool = False) -> str:
+def build(force: bool = False, csrc: str = CSRC, name: str = "") -> str:
+    """name != "": an A/B variant built from another source tree (e.g. a `git archive` of a
+    previous commit) into build/libbgs_<name>/ and libbgs_<name>.so; bgs.py loads it when
+    BGS_LIB=libbgs_<name>.so is set.  The product library is always libbgs.so."""
+    bdir = BUILD + (f"_{name}" if name else "")
+    lib = LIB if not name else os.path.join(HERE, f"libbgs_{name}.so")
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
-    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(o) for o in objs):
-        return LIB
+        objs = list(ex.map(lambda s: _compile(s, force, csrc, bdir), SOURCES))
+    if not force and os.path.exists(lib) and all(os.path.getmtime(lib) >= os.path.getmtime(o) for o in objs):
+        return lib
     nl = os.path.join(nccl_root(), "lib")
-    tmp = LIB + f".{os.getpid()}.tmp"
+    tmp = lib + f".{os.getpid()}.tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-L" + nl, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nl]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv))
+    a = sys.argv[1:]
+    kw = {}
+    if "--csrc" in a:
+        kw["csrc"] = os.path.abspath(a[a.index("--csrc") + 1])
+    if "--name" in a:
+        kw["name"] = a[a.index("--name") + 1]
+    print(build(force="--force" in a, **kw))

@@ -177,9 +177,13 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
   }
 }
 
+// Backward state of one pixel.  s = sum over the contributors BEHIND the current one of
+// (c_j . dL/dC) alpha_j T_j, so that (Eq.2 product rule, black background)
+//   dL/dalpha_k = T_k (c_k . dL/dC) - s_k / (1 - alpha_k)
+// with one scalar recursion (equivalent to 3DGS's per-channel accum_rec, fewer operations);
+// T_k = T_{k+1} / (1 - alpha_k) reuses the same reciprocal.
 struct PixB {
-  float T, dr, dg, db;
-  float acc_r, acc_g, acc_b, last_alpha, last_r, last_g, last_b;
+  float T, dr, dg, db, s;
   uint32_t last;
 };
 
@@ -187,7 +191,7 @@ __device__ __forceinline__ void init_pixb(PixB& p, bool inside, size_t pix, size
                                           const float* t_final, const int32_t* n_contrib) {
   p.T = 1.f;
   p.dr = p.dg = p.db = 0.f;
-  p.acc_r = p.acc_g = p.acc_b = p.last_alpha = p.last_r = p.last_g = p.last_b = 0.f;
+  p.s = 0.f;
   p.last = 0;
   if (inside) {
     p.T = t_final[pix];
@@ -206,23 +210,15 @@ __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float
   const float G = fast_exp(power);
   const float og = s.co.y * G;
   const float alpha = fminf(0.99f, og);
-  const float Tn = __fdividef(p.T, 1.0f - alpha);
-  p.T = ok ? Tn : p.T;
-  const float wgt = ok ? alpha * Tn : 0.f;
+  const float inv = ok ? __frcp_rn(1.0f - alpha) : 1.0f;  // 1 - alpha >= 0.01
+  p.T *= inv;                                              // T before this splat
+  const float wgt = ok ? alpha * p.T : 0.f;
   g[6] += wgt * p.dr;
   g[7] += wgt * p.dg;
   g[8] += wgt * p.db;
-  const float ar = p.last_alpha * p.last_r + (1.f - p.last_alpha) * p.acc_r;
-  const float ag = p.last_alpha * p.last_g + (1.f - p.last_alpha) * p.acc_g;
-  const float ab = p.last_alpha * p.last_b + (1.f - p.last_alpha) * p.acc_b;
-  p.acc_r = ok ? ar : p.acc_r;
-  p.acc_g = ok ? ag : p.acc_g;
-  p.acc_b = ok ? ab : p.acc_b;
-  p.last_alpha = ok ? alpha : p.last_alpha;
-  p.last_r = ok ? s.rgb.x : p.last_r;
-  p.last_g = ok ? s.rgb.y : p.last_g;
-  p.last_b = ok ? s.rgb.z : p.last_b;
-  const float dLda = Tn * ((s.rgb.x - ar) * p.dr + (s.rgb.y - ag) * p.dg + (s.rgb.z - ab) * p.db);
+  const float cdl = s.rgb.x * p.dr + s.rgb.y * p.dg + s.rgb.z * p.db;
+  const float dLda = p.T * cdl - p.s * inv;
+  p.s += cdl * wgt;  // now includes this splat for the ones in front of it
   // clamped alpha is constant: true derivative 0 (R14)
   const float gd = (ok && og <= 0.99f) ? G * dLda : 0.f;
   g[5] += gd;
