@@ -75,8 +75,13 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
   const float cc = U[1][0] * Tm[1][0] + U[1][1] * Tm[1][1] + U[1][2] * Tm[1][2] + 0.3f;
   const float idet = 1.f / (ca * cc - cb * cb);
   const float Q00 = cc * idet, Q01 = -cb * idet, Q11 = ca * idet;
-  // dL/dS2 = -Q G_Q Q, G_Q = [[gA, gB/2], [gB/2, gC]]
-  const float G00 = g[2], G01 = 0.5f * g[3], G11 = g[4];
+  // raster moments -> dL/d(mean2d, conic): power = -(A dx^2 + C dy^2)/2 - B dx dy, dL/dpower =
+  // o gd; the conic is this thread's Q (the record's A, B, C up to rounding)
+  const float o = mo.w;
+  const float g_mx = -o * (Q00 * g[0] + Q01 * g[1]);
+  const float g_my = -o * (Q01 * g[0] + Q11 * g[1]);
+  // dL/dS2 = -Q G_Q Q, G_Q = [[gA, gB/2], [gB/2, gC]], gA = -o m_xx/2, gB = -o m_xy, gC = -o m_yy/2
+  const float G00 = -0.5f * o * g[2], G01 = -0.5f * o * g[3], G11 = -0.5f * o * g[4];
   const float t00 = Q00 * G00 + Q01 * G01, t01 = Q00 * G01 + Q01 * G11;
   const float t10 = Q01 * G00 + Q11 * G01, t11 = Q01 * G01 + Q11 * G11;
   const float H00 = -(t00 * Q00 + t01 * Q01);
@@ -116,10 +121,10 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
   else dz_ += dctx * (txtz > lim_xp ? lim_xp : -lim_xn);
   if (!cly) dy_ += dcty;
   else dz_ += dcty * (tytz > lim_yp ? lim_yp : -lim_yn);
-  dx_ += g[0] * cm.fx * iz;
-  dz_ -= g[0] * cm.fx * x * iz2;
-  dy_ += g[1] * cm.fy * iz;
-  dz_ -= g[1] * cm.fy * y * iz2;
+  dx_ += g_mx * cm.fx * iz;
+  dz_ -= g_mx * cm.fx * x * iz2;
+  dy_ += g_my * cm.fy * iz;
+  dz_ -= g_my * cm.fy * y * iz2;
   float dmu[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) dmu[c] = R[c] * dx_ + R[3 + c] * dy_ + R[6 + c] * dz_;

@@ -5,9 +5,15 @@ These are what the METHOD must move or compute, not what a kernel happens to do:
                      + 192 F (SH of in-frustum) + 52 F (record + index) + 4 N (radius)      [bytes]
   a5-a7 sort         16 R (rect, depth of received) + 12 P (pairs) + 24 P per executed 8-bit
                      radix pass + 8 P (ranges pass)                                        [bytes]
-  a8 raster fwd      22 FP32 ops per (pixel, list entry) up to the pixel's last contributor
-                     (E = sum of n_contrib)                                               [ALU]
-  a9 raster bwd      45 FP32 ops per (pixel, list entry) up to the last contributor       [ALU]
+  a8 raster fwd      19 FP32 ops per (pixel, list entry) up to the pixel's last contributor
+                     (E = sum of n_contrib): dx,dy 2, power 5, alpha cut 1, exp 1, alpha = min(.99,
+                     oG) 2, w = alpha T and T -= w 2, early stop 1, colour 3, w and a sums 2 [ALU]
+  a9 raster bwd      33 FP32 ops per (pixel, list entry) up to the last contributor: recompute
+                     dx,dy,power,cut,exp,alpha 11, T_k = T_{k+1}/(1-alpha) 3, w 1, colour
+                     grads 3, dL/dalpha (c.dL, T c.dL - s/(1-alpha), s update) 6, G dL/dalpha 1,
+                     dL/do 1, mean2d/conic moments 7                                      [ALU]
+                     (the minimal formulation: any kernel does at least this much per entry it
+                     does not cull; MUFU and FFMA count as one op)
   a10 reverse (M>1)  48 D (send back) + 48 D (gather)                                     [bytes]
   a11 project bwd    240 F (params) + 52 F (partials + index) + 2 x 236 F (grads RMW)     [bytes]
   a12 importance     52 F (w, a, index) + 2 x 16 F (s, c_rad, c_vis RMW) + N/8 (Cull)    [bytes]
@@ -16,8 +22,8 @@ sm_max clock (one FP32 instruction per lane per clock; FFMA counted as one op).
 """
 from __future__ import annotations
 
-FWD_OPS = 22.0
-BWD_OPS = 45.0
+FWD_OPS = 19.0
+BWD_OPS = 33.0
 
 
 def _avg(qs, k):

@@ -27,6 +27,19 @@ def acc_view(raw: torch.Tensor) -> dict:
                 w=b.view(np.uint64).reshape(-1, 6)[:, 5].copy())
 
 
+def moments_to_g2d(g: np.ndarray, rec: dict) -> np.ndarray:
+    """Accumulator moments (include/bgs.h debug buffer 6) -> dL/d(mx,my,A,B,C,o,r,g,b), with the
+    record's own o, A, B, C (bit-identical to the oracle's, test_project_bit_exact)."""
+    o, A, B, C = (rec[k].astype(np.float64) for k in ("opac", "A", "B", "C"))
+    out = g.copy()
+    out[:, 0] = -o * (A * g[:, 0] + B * g[:, 1])
+    out[:, 1] = -o * (B * g[:, 0] + C * g[:, 1])
+    out[:, 2] = -0.5 * o * g[:, 2]
+    out[:, 3] = -o * g[:, 3]
+    out[:, 4] = -0.5 * o * g[:, 4]
+    return out
+
+
 class GpuStep:
     """One view through a1..a12 on one ctx (world 1) or an in-process group (world > 1)."""
 
@@ -155,7 +168,7 @@ class GpuStep:
             acc = o["acc_local"]
             self.a[g] = acc["a"]
             self.w[g] = acc["w"]
-            self.g2d[g] = acc["g"]
+            self.g2d[g] = moments_to_g2d(acc["g"], o["records"])
             if "s" in o:
                 self.s[gids] = o["s"]
                 self.c_rad[gids] = o["c_rad"]
