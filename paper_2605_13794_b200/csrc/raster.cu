@@ -38,24 +38,37 @@ constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 
 struct WRec {
-  float4 geo;  // mx, my, A, B
-  float4 co;   // C, o, thr, ridx (bits)
+  float4 geo;  // mx, my, A/2, B
+  float4 co;   // C/2, o, -thr, ridx (bits)
   float4 rgb;  // r, g, b, -
 };
 
-__device__ __forceinline__ float pinned_power(float A, float B, float C, float dx, float dy) {
-  // (-0.5 * ((A*dx)*dx + (C*dy)*dy)) - (B*dx)*dy, every op rounded (no contraction)
-  const float t1 = __fmul_rn(__fmul_rn(A, dx), dx);
-  const float t2 = __fmul_rn(__fmul_rn(C, dy), dy);
+// nq = -power.  The oracle's pinned fp32 expression is power = (-0.5*((A dx)dx + (C dy)dy)) -
+// (B dx)dy with every op rounded.  Halving A and C is exact and commutes with round-to-nearest
+// (normal range), so with hA = A/2, hC = C/2: RN(RN(hA dx)dx + RN(hC dy)dy) = RN(t1 + t2)/2 and
+// RN(that + (B dx)dy) = -power bit for bit (up to the sign of an exact zero, which no test
+// below distinguishes): one multiply fewer per pixel, same decisions.
+__device__ __forceinline__ float pinned_negpower(float hA, float B, float hC, float dx, float dy) {
+  const float t1 = __fmul_rn(__fmul_rn(hA, dx), dx);
+  const float t2 = __fmul_rn(__fmul_rn(hC, dy), dy);
   const float t3 = __fmul_rn(__fmul_rn(B, dx), dy);
-  return __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(t1, t2)), t3);
+  return __fadd_rn(__fadd_rn(t1, t2), t3);
 }
 
-__device__ __forceinline__ float fast_exp(float p) {
-  // exp(p) for p in [thr, 0] (|p| < 6): ex2.approx.ftz of p*log2(e); the same instruction in
+// power <= 0 && power >= thr  <=>  nq >= 0 && nq <= -thr (also for +-0)
+__device__ __forceinline__ bool in_cut(float nq, float nthr) { return nq >= 0.0f && nq <= nthr; }
+
+__device__ __forceinline__ float fast_exp_neg(float nq) {
+  // exp(-nq) for nq in [0, -thr] (< 6): ex2.approx.ftz of -nq*log2(e); the same instruction in
   // the forward and the backward, so both see identical alpha
   float r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p * 1.4426950408889634f));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(nq * -1.4426950408889634f));
+  return r;
+}
+
+__device__ __forceinline__ float fast_rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -67,8 +80,8 @@ __device__ __forceinline__ bool stage_test(const RasterArgs& a, const uint32_t* 
   const float4* p = reinterpret_cast<const float4*>(a.recv + r);
   const float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
   const float4 ax = __ldg(a.aux + r);
-  out.geo = q0;
-  out.co = make_float4(q1.x, q1.y, ax.x, __uint_as_float(r));
+  out.geo = make_float4(q0.x, q0.y, 0.5f * q0.z, q0.w);
+  out.co = make_float4(0.5f * q1.x, q1.y, -ax.x, __uint_as_float(r));
   out.rgb = make_float4(q1.z, q1.w, q2.x, 0.f);
   return (q0.x - ax.y <= x0 + 15.f) & (q0.x + ax.y >= x0) & (q0.y - ax.z <= y0 + float(h - 1)) &
          (q0.y + ax.z >= y0);
@@ -87,12 +100,12 @@ __device__ __forceinline__ void eval_fwd2(PixF& p0, PixF& p1, const WRec& s, flo
                                           uint32_t pos, bool& c0, bool& c1, uint32_t& f0, uint32_t& f1) {
   const float dx = s.geo.x - pxf;
   const float dy0 = s.geo.y - pyf0, dy1 = s.geo.y - pyf1;
-  const float pw0 = pinned_power(s.geo.z, s.geo.w, s.co.x, dx, dy0);
-  const float pw1 = pinned_power(s.geo.z, s.geo.w, s.co.x, dx, dy1);
-  const bool ok0 = !p0.done && pw0 <= 0.0f && pw0 >= s.co.z;
-  const bool ok1 = !p1.done && pw1 <= 0.0f && pw1 >= s.co.z;
-  const float a0 = fminf(0.99f, s.co.y * fast_exp(pw0));
-  const float a1 = fminf(0.99f, s.co.y * fast_exp(pw1));
+  const float nq0 = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy0);
+  const float nq1 = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy1);
+  const bool ok0 = !p0.done && in_cut(nq0, s.co.z);
+  const bool ok1 = !p1.done && in_cut(nq1, s.co.z);
+  const float a0 = fminf(0.99f, s.co.y * fast_exp_neg(nq0));
+  const float a1 = fminf(0.99f, s.co.y * fast_exp_neg(nq1));
   const float t0 = p0.T * (1.0f - a0), t1 = p1.T * (1.0f - a1);
   const bool stop0 = ok0 && t0 < 0.0001f, stop1 = ok1 && t1 < 0.0001f;
   c0 = ok0 && !stop0;
@@ -209,12 +222,12 @@ __device__ __forceinline__ void init_pixb(PixB& p, bool inside, size_t pix, size
 // Backward evaluation of one pixel against one record (branch-free: `ok` predicates every
 // update so the two pixels of a lane interleave); accumulates the pixel's partials into g[9].
 __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float dy, uint32_t pos, float* g) {
-  const float power = pinned_power(s.geo.z, s.geo.w, s.co.x, dx, dy);
-  const bool ok = pos < p.last && power <= 0.0f && power >= s.co.z;
-  const float G = fast_exp(power);
+  const float nq = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy);
+  const bool ok = pos < p.last && in_cut(nq, s.co.z);
+  const float G = fast_exp_neg(nq);
   const float og = s.co.y * G;
   const float alpha = fminf(0.99f, og);
-  const float inv = ok ? __frcp_rn(1.0f - alpha) : 1.0f;  // 1 - alpha >= 0.01
+  const float inv = ok ? fast_rcp(1.0f - alpha) : 1.0f;  // 1 - alpha >= 0.01: rel. error 2^-23
   p.T *= inv;                                              // T before this splat
   const float wgt = ok ? alpha * p.T : 0.f;
   g[6] += wgt * p.dr;
