@@ -87,44 +87,37 @@ __device__ __forceinline__ bool stage_test(const RasterArgs& a, const uint32_t* 
          (q0.y + ax.z >= y0);
 }
 
+// Forward state of one pixel.  While the pixel composites, T >= 1e-4 > 0; when the early stop
+// fires T is stored negated, which makes every later T (1 - alpha) negative, so the contribution
+// test (T (1 - alpha) >= 1e-4) fails without a separate flag.  |T| is the transmittance.
 struct PixF {
   float T, r, g, b;
   uint32_t last;
-  bool done;
 };
 
+__device__ __forceinline__ void eval_fwd1(PixF& p, const WRec& s, float dx, float dy, uint32_t pos, bool& c,
+                                          uint32_t& f) {
+  const float nq = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy);
+  const bool ok = in_cut(nq, s.co.z);
+  const float alpha = fminf(0.99f, s.co.y * fast_exp_neg(nq));
+  const float t = p.T * (1.0f - alpha);
+  c = ok && t >= 0.0001f;  // false once stopped (T < 0)
+  const float w = c ? alpha * p.T : 0.f;
+  p.r += s.rgb.x * w;
+  p.g += s.rgb.y * w;
+  p.b += s.rgb.z * w;
+  p.T = c ? t : (ok ? -fabsf(p.T) : p.T);
+  p.last = c ? pos : p.last;
+  f = __float2uint_rn(w * 16777216.0f);
+}
+
 // Forward evaluation of the two pixels of a lane against one record, branch-free so that the
-// two dependency chains interleave (no divergent control flow per pixel).  c0/c1: contributed;
-// f0/f1: alpha*T in 2^-24 fixed point.
+// two dependency chains interleave.  c0/c1: contributed; f0/f1: alpha*T in 2^-24 fixed point.
 __device__ __forceinline__ void eval_fwd2(PixF& p0, PixF& p1, const WRec& s, float pxf, float pyf0, float pyf1,
                                           uint32_t pos, bool& c0, bool& c1, uint32_t& f0, uint32_t& f1) {
   const float dx = s.geo.x - pxf;
-  const float dy0 = s.geo.y - pyf0, dy1 = s.geo.y - pyf1;
-  const float nq0 = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy0);
-  const float nq1 = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy1);
-  const bool ok0 = !p0.done && in_cut(nq0, s.co.z);
-  const bool ok1 = !p1.done && in_cut(nq1, s.co.z);
-  const float a0 = fminf(0.99f, s.co.y * fast_exp_neg(nq0));
-  const float a1 = fminf(0.99f, s.co.y * fast_exp_neg(nq1));
-  const float t0 = p0.T * (1.0f - a0), t1 = p1.T * (1.0f - a1);
-  const bool stop0 = ok0 && t0 < 0.0001f, stop1 = ok1 && t1 < 0.0001f;
-  c0 = ok0 && !stop0;
-  c1 = ok1 && !stop1;
-  p0.done = p0.done || stop0;
-  p1.done = p1.done || stop1;
-  const float w0 = c0 ? a0 * p0.T : 0.f, w1 = c1 ? a1 * p1.T : 0.f;
-  p0.r += s.rgb.x * w0;
-  p0.g += s.rgb.y * w0;
-  p0.b += s.rgb.z * w0;
-  p1.r += s.rgb.x * w1;
-  p1.g += s.rgb.y * w1;
-  p1.b += s.rgb.z * w1;
-  p0.T = c0 ? t0 : p0.T;
-  p1.T = c1 ? t1 : p1.T;
-  p0.last = c0 ? pos : p0.last;
-  p1.last = c1 ? pos : p1.last;
-  f0 = __float2uint_rn(w0 * 16777216.0f);
-  f1 = __float2uint_rn(w1 * 16777216.0f);
+  eval_fwd1(p0, s, dx, s.geo.y - pyf0, pos, c0, f0);
+  eval_fwd1(p1, s, dx, s.geo.y - pyf1, pos, c1, f1);
 }
 
 template <bool kImportance>
@@ -143,16 +136,19 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
   const uint2 range = a.ranges[lt];
   const float pxf = float(px), pyf0 = float(py0), pyf1 = float(py1);
   const float x0 = float(tx * kTile), y0 = float(ty * kTile + 4 * warp);
-  PixF p0{1.f, 0.f, 0.f, 0.f, 0u, !in0}, p1{1.f, 0.f, 0.f, 0.f, 0u, !in1};
+  PixF p0{in0 ? 1.f : -1.f, 0.f, 0.f, 0.f, 0u}, p1{in1 ? 1.f : -1.f, 0.f, 0.f, 0.f, 0u};
   WRec* mine = s_rec[warp];
   for (uint32_t base = range.x; base < range.y; base += 32) {
-    if (__all_sync(0xffffffffu, p0.done && p1.done)) break;
+    if (__all_sync(0xffffffffu, p0.T < 0.f && p1.T < 0.f)) break;
     const uint32_t idx = base + lane;
     WRec st;
     const bool hit = idx < range.y && stage_test(a, vals, idx, x0, y0, 4, st);
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (hit) mine[lane] = st;
     __syncwarp();
+    // importance of the record this lane staged: the warp sums land in the staging lane's
+    // registers and it issues the two atomics after the batch
+    uint32_t my_w = 0, my_a = 0;
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
@@ -162,16 +158,18 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
       bool c0, c1;
       eval_fwd2(p0, p1, s, pxf, pyf0, pyf1, pos, c0, c1, f0, f1);
       if (kImportance) {
-        const unsigned b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
-        if (b0 | b1) {
-          const uint32_t sum = __reduce_add_sync(0xffffffffu, f0 + f1);
-          if (lane == 0) {
-            Acc* acc = a.acc + __float_as_uint(s.co.w);
-            atomicAdd(&acc->a, uint32_t(__popc(b0) + __popc(b1)));
-            atomicAdd(&acc->w, (unsigned long long)sum);
-          }
+        const uint32_t sum = __reduce_add_sync(0xffffffffu, f0 + f1);
+        const uint32_t cnt = __reduce_add_sync(0xffffffffu, uint32_t(c0) + uint32_t(c1));
+        if (lane == j) {
+          my_w = sum;
+          my_a = cnt;
         }
       }
+    }
+    if (kImportance && my_a) {
+      Acc* acc = a.acc + __float_as_uint(st.co.w);
+      atomicAdd(&acc->a, my_a);
+      atomicAdd(&acc->w, (unsigned long long)my_w);
     }
     __syncwarp();
   }
@@ -181,7 +179,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
     rgb[pix] = p0.r;
     rgb[plane + pix] = p0.g;
     rgb[2 * plane + pix] = p0.b;
-    t_final[pix] = p0.T;
+    t_final[pix] = fabsf(p0.T);
     n_contrib[pix] = int32_t(p0.last);
   }
   if (in1) {
@@ -189,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
     rgb[pix] = p1.r;
     rgb[plane + pix] = p1.g;
     rgb[2 * plane + pix] = p1.b;
-    t_final[pix] = p1.T;
+    t_final[pix] = fabsf(p1.T);
     n_contrib[pix] = int32_t(p1.last);
   }
 }
