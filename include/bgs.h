@@ -140,14 +140,18 @@ bgs_status bgs_query(bgs_ctx* ctx, int64_t* out /*[BGS_Q_COUNT] host*/);
  * the producing stage):
  *   0 records [F]x48 B {mx,my,A,B, C,o,r,g, b,depth,gid,rect(x0|y0<<8|x1<<16|y1<<24)}
  *   1 record local index [F] u32       2 received records [R]x48 B (== 0 when world == 1)
- *   3 sorted keys [P] u64 ((tile-tile_begin)<<31 | f32 bits(depth))   4 sorted values [P] u32
+ *   3 sorted keys [P] u64 ((tile-tile_begin) << nb | (f32 bits(depth) - lo)), lo = 0xffffffff -
+ *     counters[6], hi = counters[7] (min / max depth bits of the received records), nb = bit width
+ *     of hi - lo: an exact order-preserving packing of (tile, depth)     4 sorted values [P] u32
  *     (index into received records)    5 tile ranges [tile_end-tile_begin] uint2 [start,end)
  *   6 per-received-splat accumulators [R]x48 B {m_x, m_y, m_xx, m_xy, m_yy, dL/do, dL/d(r,g,b) f32,
  *     a u32, w_fixed u64}; m_* = sums over pixels of gd*dx, gd*dy, gd*dx^2, gd*dx*dy, gd*dy^2 with
  *     gd = G dL/dalpha, (dx,dy) = mean2d - pixel, so dL/dmx = -o(A m_x + B m_y), dL/dmy =
  *     -o(B m_x + C m_y), dL/dA = -o m_xx/2, dL/dB = -o m_xy, dL/dC = -o m_yy/2 (Eq.2 chain rule)
  *   7 per-local-record owner-summed accumulators [F]x48 B (same layout; == 6 when world == 1)
- *   8 tile owner map [T] i32    9 dest mask [F] u8    10 per-tile pair counts (all ranks) [T] i32 */
+ *   8 tile owner map [T] i32    9 dest mask [F] u8    10 per-tile pair counts (all ranks) [T] i32
+ *   11 device counters [8] u64 (0 F, 1 P_all, 2 n_lod, 3 n_active, 4 P, 5 candidates, 6 and 7 the
+ *      depth range of buffer 3) */
 bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** dev_ptr, int64_t* bytes);
 
 /* ---------------------------------------------------------------------------------------

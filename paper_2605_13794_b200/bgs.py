@@ -31,7 +31,7 @@ Q_NAMES = ("n_local", "n_lod", "n_active", "F", "D", "R", "P", "tile_begin", "ti
 STATUS = {0: "BGS_OK", 1: "BGS_ERR_INVALID_ARGUMENT", 2: "BGS_ERR_CAPACITY", 3: "BGS_ERR_CUDA",
           4: "BGS_ERR_NCCL", 5: "BGS_ERR_CONTRACT", 6: "BGS_ERR_INTERNAL"}
 DEBUG = {"records": 0, "rec_lidx": 1, "recv": 2, "keys": 3, "vals": 4, "ranges": 5, "acc": 6, "acc_local": 7,
-         "owner": 8, "dest_mask": 9, "tile_pairs": 10}
+         "owner": 8, "dest_mask": 9, "tile_pairs": 10, "counters": 11}
 
 
 class BgsError(RuntimeError):

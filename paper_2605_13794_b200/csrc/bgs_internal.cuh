@@ -41,8 +41,29 @@ enum Counter : int {
   C_NACT = 3,     // |A^(m)|
   C_P = 4,        // pairs emitted for owned tiles
   C_CAND = 5,     // candidates passing the conservative off-screen bound
+  C_DLO = 6,      // 0xffffffff - min f32 bits(depth) over the records the pairs come from (atomicMax)
+  C_DHI = 7,      // max f32 bits(depth) over the same records
   C_NCOUNTERS = 8
 };
+
+// Sort key of a pair (a5/a6): (local tile << nb) | (bits(depth) - lo), lo = min depth bits,
+// nb = bit width of (max - min) depth bits.  Depths are positive floats, so their bit patterns
+// order like the values and the subtraction is an exact order-preserving map onto [0, 2^nb):
+// the key orders (tile, depth) exactly as (tile << 31 | bits) would, in nb + tile bits.
+struct KeyLayout {
+  uint32_t lo;
+  int nb;
+};
+__host__ __device__ inline KeyLayout key_layout(unsigned long long c_dlo, unsigned long long c_dhi) {
+  KeyLayout k;
+  k.lo = 0xffffffffu - uint32_t(c_dlo);
+  const uint32_t hi = uint32_t(c_dhi);
+  const uint32_t span = hi > k.lo ? hi - k.lo : 0u;
+  int nb = 0;
+  while (nb < 32 && (span >> nb) != 0u) ++nb;
+  k.nb = nb;
+  return k;
+}
 
 struct CameraK {
   float fx, fy, cx, cy;
@@ -97,6 +118,8 @@ struct SortArgs {
 };
 // emits pairs and digit histograms; returns nothing (P stays on device, counters[C_P])
 void launch_emit(const SortArgs& a, cudaStream_t s);
+// world > 1: depth range of the received records into counters C_DLO / C_DHI (zeroed by the caller)
+void launch_depth_range(const Rec* recv, int64_t n, unsigned long long* counters, cudaStream_t s);
 void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches);
 void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s);
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* perm, cudaStream_t s);

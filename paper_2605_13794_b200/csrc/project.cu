@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
   __shared__ uint32_t s_total;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n_cand = int64_t(*((volatile unsigned long long*)(a.counters + C_CAND)));
+  uint32_t dhi = 0, dlo = 0;  // max bits(depth), max (0xffffffff - bits(depth)) of this thread's records
   for (int64_t c0 = int64_t(blockIdx.x) * 256; c0 < n_cand; c0 += int64_t(gridDim.x) * 256) {
     const int64_t c = c0 + tid;
     ProjOut o;
@@ -271,6 +272,11 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
     if (c < n_cand) {
       i = a.cand[c];
       o = project_exact(a, i);
+    }
+    if (o.valid) {
+      const uint32_t db = __float_as_uint(o.depth);
+      dhi = db > dhi ? db : dhi;
+      dlo = (0xffffffffu - db) > dlo ? (0xffffffffu - db) : dlo;
     }
     unsigned long long area = o.area;
 #pragma unroll
@@ -306,6 +312,21 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
     for (uint32_t j = tid; j < total; j += 256)
       if (base + j < (unsigned long long)a.rec_cap) a.rec_lidx[base + j] = s_lidx[j];
     __syncthreads();
+  }
+  // depth range of the records (sort key layout, KeyLayout): one atomic pair per CTA
+  dhi = __reduce_max_sync(0xffffffffu, dhi);
+  dlo = __reduce_max_sync(0xffffffffu, dlo);
+  __shared__ uint32_t s_dr[2];
+  if (tid == 0) s_dr[0] = s_dr[1] = 0;
+  __syncthreads();
+  if (lane == 0) {
+    atomicMax(&s_dr[0], dhi);
+    atomicMax(&s_dr[1], dlo);
+  }
+  __syncthreads();
+  if (tid == 0 && s_dr[0]) {
+    atomicMax(a.counters + C_DHI, (unsigned long long)s_dr[0]);
+    atomicMax(a.counters + C_DLO, (unsigned long long)s_dr[1]);
   }
 }
 

@@ -438,6 +438,7 @@ bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** ptr, int64_t* by
     case 8: p = ctx->owner.p; b = ctx->world > 1 ? int64_t(ctx->T) * 4 : 0; break;
     case 9: p = ctx->dest_mask.p; b = ctx->world > 1 ? ctx->F : 0; break;
     case 10: p = ctx->tile_pairs.p; b = ctx->world > 1 ? int64_t(ctx->T) * 4 : 0; break;
+    case 11: p = ctx->counters.p; b = int64_t(C_NCOUNTERS) * 8; break;
     default: return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "unknown debug buffer");
   }
   *ptr = p;
@@ -649,7 +650,12 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   const int nt = ctx->t_end - ctx->t_begin;
   int tbits = 0;
   while ((1 << tbits) < std::max(nt, 1)) ++tbits;
-  ctx->n_passes = (31 + tbits + 7) / 8;
+  // key = (local tile << nb) | (bits(depth) - lo) (KeyLayout).  World 1: the records are the
+  // received set and their depth range came back with the projection counters, so the pass
+  // count is exact.  World > 1: the range of the received records is computed on the device and
+  // the passes are launched for nb = 32; passes whose digit is constant skip on the device.
+  const int nbits = ctx->world == 1 ? key_layout(ctx->h_counters[C_DLO], ctx->h_counters[C_DHI]).nb : 32;
+  ctx->n_passes = std::max(1, (nbits + tbits + 7) / 8);
   SortArgs a{};
   a.recv = ctx->recv;
   a.n_recv = ctx->R;
@@ -681,6 +687,13 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   CK(cudaMemsetAsync(P_<unsigned long long>(ctx->counters) + C_P, 0, 8, s));
   CK(cudaMemsetAsync(ctx->status.p, 0, size_t(n_parts) * 256 * 4 * ctx->n_passes, s));
   CK(cudaMemsetAsync(ctx->ranges.p, 0, size_t(std::max(nt, 1)) * 8, s));
+  if (ctx->world > 1) {
+    CK(cudaMemsetAsync(P_<unsigned long long>(ctx->counters) + C_DLO, 0, 16, s));
+    if (ctx->R > 0) {
+      launch_depth_range(ctx->recv, ctx->R, P_<unsigned long long>(ctx->counters), s);
+      CKS(launched(ctx));
+    }
+  }
   if (ctx->R > 0) {
     launch_emit(a, s);
     CKS(launched(ctx));

@@ -3,8 +3,12 @@
 // PAPER.md P:152 ("rasterized by tile-based front-to-back alpha compositing"), Eq.2
 // (N(p) depth-ordered), SPEC S:116 / S:172 (ties by global id, reading R12).
 //
-// Key = (local tile << 31) | f32 bits(depth).  depth > near_clip > 0, so bit 31 of the float
-// is 0 and the unsigned order of the bits is the numeric order of the depths.
+// Key = (local tile << nb) | (f32 bits(depth) - lo) (KeyLayout, bgs_internal.cuh).  depth >
+// near_clip > 0, so the unsigned order of the bits is the numeric order of the depths and
+// subtracting the minimum maps them exactly onto [0, 2^nb); a view's depths span 22-24 bits on
+// the Rubble workload, so the key has 34-36 bits (5 onesweep passes instead of 6 for tile << 31).
+// The digit histograms of the passes that see depth bits only are added once per record
+// (weighted by its owned pair count); only the tile-bearing digits are counted per pair.
 //
 // a5: one warp expands the rects of 32 received records cooperatively (slot = position in a
 //     rect, warp-scan + 5-step shuffle search for the owning lane), keeps the slots whose tile
@@ -33,8 +37,42 @@ constexpr int kCtrlActive = 0;   // [8]
 constexpr int kCtrlSel = 8;      // [7] input buffer of pass p
 constexpr int kCtrlPart = 16;    // [8] partition counters
 
-__device__ __forceinline__ unsigned long long make_key(uint32_t lt, float depth) {
-  return (static_cast<unsigned long long>(lt) << 31) | static_cast<unsigned long long>(__float_as_uint(depth));
+__device__ __forceinline__ unsigned long long make_key(uint32_t lt, uint32_t dbits, KeyLayout kl) {
+  return (static_cast<unsigned long long>(lt) << kl.nb) | static_cast<unsigned long long>(dbits - kl.lo);
+}
+
+// Exclusive scan of one value per thread over a 256-thread CTA (warp shuffles + 8 warp totals).
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* s_w /*[8]*/) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  uint32_t wb = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) wb += k < w ? s_w[k] : 0u;
+  __syncthreads();  // s_w reusable by the caller
+  return wb + inc - v;
+}
+
+__global__ void __launch_bounds__(256) k_depth_range(const Rec* __restrict__ recv, int64_t n,
+                                                     unsigned long long* counters) {
+  uint32_t dhi = 0, dlo = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t db = __float_as_uint(__ldg(&recv[r].depth));
+    dhi = db > dhi ? db : dhi;
+    dlo = (0xffffffffu - db) > dlo ? (0xffffffffu - db) : dlo;
+  }
+  dhi = __reduce_max_sync(0xffffffffu, dhi);
+  dlo = __reduce_max_sync(0xffffffffu, dlo);
+  if ((threadIdx.x & 31) == 0 && dhi) {
+    atomicMax(counters + C_DHI, (unsigned long long)dhi);
+    atomicMax(counters + C_DLO, (unsigned long long)dlo);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
@@ -43,6 +81,8 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const KeyLayout kl = key_layout(a.counters[C_DLO], a.counters[C_DHI]);
+  const int p_pair = kl.nb / 8;  // passes below this one see depth bits only
   uint32_t rect = 0, area = 0, own = 0, dbits = 0;
   if (r < a.n_recv) {
     const uint4 q2 = __ldg(reinterpret_cast<const uint4*>(a.recv + r) + 2);  // (b, depth, gid, rect)
@@ -71,6 +111,12 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
     for (int y = y0; y < y1; ++y) {
       const int lo = max(y * a.TX + x0, a.t_begin), hi = min(y * a.TX + x1, a.t_end);
       own += hi > lo ? uint32_t(hi - lo) : 0u;
+    }
+    // digits made of depth bits only are the same for every pair of this record: one weighted
+    // add per record instead of one per pair
+    if (own) {
+      const uint32_t dk = dbits - kl.lo;
+      for (int p = 0; p < p_pair && p < a.n_passes; ++p) atomicAdd(&s_hist[p][(dk >> (8 * p)) & 255u], own);
     }
   }
   // warp inclusive scans of area and own
@@ -129,7 +175,7 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
       const int t = (y0 + int(k) / w) * a.TX + x0 + int(k) % w;
       if (t >= a.t_begin && t < a.t_end) {
         ok = true;
-        key = make_key(uint32_t(t - a.t_begin), __uint_as_float(dj));
+        key = make_key(uint32_t(t - a.t_begin), dj, kl);
         val = uint32_t(int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31) + j);
       }
     }
@@ -140,7 +186,7 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
         a.keys[0][pos] = key;
         a.vals[0][pos] = val;
       }
-      for (int p = 0; p < npass; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
+      for (int p = p_pair; p < npass; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
     }
     run += __popc(m);
   }
@@ -154,32 +200,19 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
 // One CTA: per pass, detect constant digits (inactive pass), exclusive-scan the digit
 // histogram in place, and assign ping-pong input selectors.
 __global__ void __launch_bounds__(256) k_digit_scan(SortArgs a) {
-  __shared__ uint32_t s_scan[256];
-  __shared__ int s_trivial;
+  __shared__ uint32_t s_w[8];
   const unsigned long long P = a.counters[C_P];
   uint32_t sel = 0;
   for (int p = 0; p < a.n_passes; ++p) {
     const uint32_t c = a.digit_hist[p * 256 + threadIdx.x];
-    if (threadIdx.x == 0) s_trivial = 0;
-    __syncthreads();
-    if ((unsigned long long)c == P) s_trivial = 1;  // all keys share this digit (also P == 0)
-    s_scan[threadIdx.x] = c;
-    __syncthreads();
-    // Hillis-Steele inclusive scan over 256
-    for (int o = 1; o < 256; o <<= 1) {
-      const uint32_t v = threadIdx.x >= o ? s_scan[threadIdx.x - o] : 0u;
-      __syncthreads();
-      s_scan[threadIdx.x] += v;
-      __syncthreads();
-    }
-    a.digit_hist[p * 256 + threadIdx.x] = s_scan[threadIdx.x] - c;  // exclusive
-    const int active = !s_trivial;
+    // all keys share this digit (also P == 0): the pass is skipped
+    const int active = !__syncthreads_or((unsigned long long)c == P);
+    a.digit_hist[p * 256 + threadIdx.x] = block_excl_scan256(c, s_w);
     if (threadIdx.x == 0) {
       a.pass_ctrl[kCtrlActive + p] = uint32_t(active);
       a.pass_ctrl[kCtrlSel + p] = sel;
     }
     if (active) sel ^= 1u;
-    __syncthreads();
   }
   if (threadIdx.x == 0) a.pass_ctrl[kFinalSel] = sel;
 }
@@ -270,17 +303,8 @@ __global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int
     *my = kFlagInc | (excl + cnt);
   }
   // block-local exclusive scan of cnt over digits (256 threads)
-  s_bstart[d] = cnt;
-  __syncthreads();
-  for (int o = 1; o < 256; o <<= 1) {
-    const uint32_t v = d >= o ? s_bstart[d - o] : 0u;
-    __syncthreads();
-    s_bstart[d] += v;
-    __syncthreads();
-  }
-  const uint32_t bstart = s_bstart[d] - cnt;
-  __syncthreads();
-  s_bstart[d] = bstart;
+  __shared__ uint32_t s_w8[8];
+  s_bstart[d] = block_excl_scan256(cnt, s_w8);
   s_gstart[d] = a.digit_hist[pass * 256 + d] + excl;
   __syncthreads();
   // local reorder in shared memory (stable: warp-major, then item, then lane == input order)
@@ -311,12 +335,13 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
   const uint32_t sel = a.pass_ctrl[kFinalSel];
   const unsigned long long* keys = sel ? a.keys[1] : a.keys[0];
   uint32_t* vals = sel ? a.vals[1] : a.vals[0];
+  const int nb = key_layout(a.counters[C_DLO], a.counters[C_DHI]).nb;
   const unsigned long long k = keys[i];
-  const uint32_t t = uint32_t(k >> 31);
+  const uint32_t t = uint32_t(k >> nb);
   const unsigned long long kp = i > 0 ? keys[i - 1] : ~0ull;
   const unsigned long long kn = i + 1 < P ? keys[i + 1] : ~0ull;
-  if (i == 0 || uint32_t(kp >> 31) != t) a.ranges[t].x = uint32_t(i);
-  if (i + 1 == P || uint32_t(kn >> 31) != t) a.ranges[t].y = uint32_t(i + 1);
+  if (i == 0 || uint32_t(kp >> nb) != t) a.ranges[t].x = uint32_t(i);
+  if (i + 1 == P || uint32_t(kn >> nb) != t) a.ranges[t].y = uint32_t(i + 1);
   if (kn == k && kp != k) {
     // run of identical (tile, depth) keys starting at i: order by global id (R12)
     int64_t e = i + 1;
@@ -340,6 +365,13 @@ void launch_emit(const SortArgs& a, cudaStream_t s) {
   if (a.n_recv <= 0) return;
   const int64_t blocks = (a.n_recv + 255) / 256;
   k_emit<<<unsigned(blocks), 256, 0, s>>>(a);
+}
+
+void launch_depth_range(const Rec* recv, int64_t n, unsigned long long* counters, cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t nb = (n + 255) / 256;
+  const int64_t blocks = nb < 148 * 8 ? nb : 148 * 8;
+  k_depth_range<<<unsigned(blocks), 256, 0, s>>>(recv, n, counters);
 }
 
 void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches) {

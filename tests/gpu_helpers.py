@@ -27,6 +27,16 @@ def acc_view(raw: torch.Tensor) -> dict:
                 w=b.view(np.uint64).reshape(-1, 6)[:, 5].copy())
 
 
+def decode_keys(keys: np.ndarray, counters: np.ndarray):
+    """Sorted keys (include/bgs.h debug buffer 3) -> (local tile, f32 bits of depth)."""
+    lo = 0xFFFFFFFF - int(counters[6] & np.uint64(0xFFFFFFFF))
+    hi = int(counters[7] & np.uint64(0xFFFFFFFF))
+    nb = max(0, hi - lo).bit_length()
+    tiles = (keys >> np.uint64(nb)).astype(np.int32)
+    dbits = ((keys & np.uint64((1 << nb) - 1)) + np.uint64(lo)).astype(np.uint32)
+    return tiles, dbits
+
+
 def moments_to_g2d(g: np.ndarray, rec: dict) -> np.ndarray:
     """Accumulator moments (include/bgs.h debug buffer 6) -> dL/d(mx,my,A,B,C,o,r,g,b), with the
     record's own o, A, B, C (bit-identical to the oracle's, test_project_bit_exact)."""
@@ -87,6 +97,8 @@ class GpuStep:
                     B.bgs_sort_tiles(ctx, stream)
                     out["q"] = ctx.query()
                     out["keys"] = ctx.debug_buffer("keys").view(torch.int64).cpu().numpy().view(np.uint64)
+                    out["counters"] = ctx.debug_buffer("counters").view(torch.int64).cpu().numpy().view(np.uint64)
+                    out["key_tile"], out["key_dbits"] = decode_keys(out["keys"], out["counters"])
                     out["vals"] = ctx.debug_buffer("vals").view(torch.int32).cpu().numpy()
                     out["ranges"] = ctx.debug_buffer("ranges").view(torch.int32).cpu().numpy().reshape(-1, 2)
                     recv = ctx.debug_buffer("recv") if M > 1 else ctx.debug_buffer("records")

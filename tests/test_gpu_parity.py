@@ -79,9 +79,8 @@ def test_project_bit_exact(tiny_run):
 def test_sort_and_ranges_bit_exact(tiny_run):
     sc, cam, dl, st, gs = tiny_run
     o = gs.rank[0]
-    keys, vals = o["keys"], o["vals"]
-    tiles = (keys >> np.uint64(31)).astype(np.int32)
-    dbits = (keys & np.uint64(0x7FFFFFFF)).astype(np.uint32)
+    vals = o["vals"]
+    tiles, dbits = o["key_tile"], o["key_dbits"]
     gid = o["recv"]["gid"][vals]
     assert np.array_equal(tiles, st.get("pair_tile", 0))
     assert np.array_equal(gid, st.get("pair_gid", 0))
@@ -195,7 +194,7 @@ def test_multirank_local_group_parity(tiny_scene, tiny_run, M):
             assert q["P"] == len(st.get("pair_tile", r))
             assert q["R"] == len(st.get("recv", r))
             # received set and sorted pair sequence per owner
-            tiles = (gs.rank[r]["keys"] >> np.uint64(31)).astype(np.int32) + b
+            tiles = gs.rank[r]["key_tile"] + b
             gids = gs.rank[r]["recv"]["gid"][gs.rank[r]["vals"]]
             assert np.array_equal(tiles, st.get("pair_tile", r))
             assert np.array_equal(gids, st.get("pair_gid", r))
@@ -290,7 +289,7 @@ def test_full_size_sampled(config, view):
         assert np.array_equal(rec["rgb"][order].view(np.uint32),
                               _f32(st.get("rgb").reshape(-1, 3)[valid]).view(np.uint32))
         o = gs.rank[0]
-        tiles = (o["keys"] >> np.uint64(31)).astype(np.int32)
+        tiles = o["key_tile"]
         assert np.array_equal(tiles, st.get("pair_tile", 0))
         assert np.array_equal(o["recv"]["gid"][o["vals"]], st.get("pair_gid", 0))
         assert np.array_equal(o["ranges"][:, 0], st.get("range_lo", 0))
@@ -336,7 +335,7 @@ def test_edge_cases(case):
         assert np.abs(gs.img - st.get("img").reshape(3, H, W))[:, ~cand].max(initial=0) <= 1e-4
         assert np.array_equal(gs.nc[~cand], st.get("n_contrib").reshape(H, W)[~cand])
         o = gs.rank[0]
-        tiles = (o["keys"] >> np.uint64(31)).astype(np.int32)
+        tiles = o["key_tile"]
         assert np.array_equal(tiles, st.get("pair_tile", 0))
         assert np.array_equal(o["recv"]["gid"][o["vals"]], st.get("pair_gid", 0))
         if case == "empty":
