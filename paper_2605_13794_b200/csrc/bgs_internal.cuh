@@ -59,9 +59,13 @@ __host__ __device__ inline KeyLayout key_layout(unsigned long long c_dlo, unsign
   k.lo = 0xffffffffu - uint32_t(c_dlo);
   const uint32_t hi = uint32_t(c_dhi);
   const uint32_t span = hi > k.lo ? hi - k.lo : 0u;
+#ifdef __CUDA_ARCH__
+  k.nb = 32 - __clz(span);
+#else
   int nb = 0;
   while (nb < 32 && (span >> nb) != 0u) ++nb;
   k.nb = nb;
+#endif
   return k;
 }
 

@@ -75,14 +75,20 @@ __global__ void __launch_bounds__(256) k_depth_range(const Rec* __restrict__ rec
   }
 }
 
+// Persistent: each CTA walks chunks of 256 received records and keeps its digit histograms in
+// shared memory across them, so the global histogram atomics scale with the grid, not with R.
 __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
   __shared__ uint32_t s_hist[kMaxSortPasses][256];
+  __shared__ uint32_t s_wown[8];
+  __shared__ unsigned long long s_bbase;
   for (int j = threadIdx.x; j < kMaxSortPasses * 256; j += blockDim.x) (&s_hist[0][0])[j] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const KeyLayout kl = key_layout(a.counters[C_DLO], a.counters[C_DHI]);
   const int p_pair = kl.nb / 8;  // passes below this one see depth bits only
+  const int64_t n_chunks = (a.n_recv + 255) / 256;
+  for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+  const int64_t r = ch * 256 + threadIdx.x;
   uint32_t rect = 0, area = 0, own = 0, dbits = 0;
   if (r < a.n_recv) {
     const uint4 q2 = __ldg(reinterpret_cast<const uint4*>(a.recv + r) + 2);  // (b, depth, gid, rect)
@@ -132,9 +138,7 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
   }
   const uint32_t total_area = __shfl_sync(0xffffffffu, incl, 31);
   const uint32_t total_own = __shfl_sync(0xffffffffu, oincl, 31);
-  // one global atomic per CTA (warp totals scanned in shared memory)
-  __shared__ uint32_t s_wown[8];
-  __shared__ unsigned long long s_bbase;
+  // one global atomic per chunk (warp totals scanned in shared memory)
   const int warp = threadIdx.x >> 5;
   if (lane == 0) s_wown[warp] = total_own;
   __syncthreads();
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
       if (t >= a.t_begin && t < a.t_end) {
         ok = true;
         key = make_key(uint32_t(t - a.t_begin), dj, kl);
-        val = uint32_t(int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31) + j);
+        val = uint32_t(ch * 256 + (threadIdx.x & ~31) + j);
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, ok);
@@ -190,8 +194,9 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
     }
     run += __popc(m);
   }
-  __syncthreads();
-  for (int j = threadIdx.x; j < npass * 256; j += blockDim.x) {
+  __syncthreads();  // s_wown / s_bbase reused by the next chunk
+  }
+  for (int j = threadIdx.x; j < a.n_passes * 256; j += blockDim.x) {
     const uint32_t c = (&s_hist[0][0])[j];
     if (c) atomicAdd(a.digit_hist + j, c);
   }
@@ -363,7 +368,16 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
 
 void launch_emit(const SortArgs& a, cudaStream_t s) {
   if (a.n_recv <= 0) return;
-  const int64_t blocks = (a.n_recv + 255) / 256;
+  const int64_t chunks = (a.n_recv + 255) / 256;
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, 256, 0);
+    max_blocks = sms * (occ < 4 ? (occ > 0 ? occ : 1) : 4);
+  }
+  const int64_t blocks = chunks < max_blocks ? chunks : max_blocks;
   k_emit<<<unsigned(blocks), 256, 0, s>>>(a);
 }
 
@@ -402,11 +416,16 @@ namespace {
 // start in the first wave instead of extending the tail.
 __global__ void __launch_bounds__(1024) k_tile_order(const uint2* ranges, int n, uint32_t* perm) {
   __shared__ uint32_t s_cnt[256];
+  __shared__ uint32_t s_w[8];
   __shared__ uint32_t s_max;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < 256) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_max = 1;
   __syncthreads();
-  for (int t = threadIdx.x; t < n; t += blockDim.x) atomicMax(&s_max, ranges[t].y - ranges[t].x);
+  uint32_t mx = 0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) mx = max(mx, ranges[t].y - ranges[t].x);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) atomicMax(&s_max, mx);
   __syncthreads();
   const uint32_t width = (s_max + 255) / 256;
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
@@ -414,13 +433,23 @@ __global__ void __launch_bounds__(1024) k_tile_order(const uint2* ranges, int n,
     atomicAdd(&s_cnt[255 - b], 1u);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int b = 0; b < 256; ++b) {
-      const uint32_t c = s_cnt[b];
-      s_cnt[b] = run;
-      run += c;
+  // exclusive scan of the 256 bucket counts by warps 0..7 (shuffles + 8 warp totals)
+  uint32_t c = 0, inc = 0;
+  if (warp < 8) {
+    c = s_cnt[threadIdx.x];
+    inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
     }
+    if (lane == 31) s_w[warp] = inc;
+  }
+  __syncthreads();
+  if (warp < 8) {
+    uint32_t wb = 0;
+    for (int k = 0; k < warp; ++k) wb += s_w[k];
+    s_cnt[threadIdx.x] = wb + inc - c;
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
