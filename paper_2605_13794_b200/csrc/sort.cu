@@ -296,14 +296,29 @@ __global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int
     *my = kFlagInc | cnt;
   } else {
     *my = kFlagAgg | cnt;
+    // look back 4 predecessors per round trip: consume them nearest first until an inclusive
+    // prefix; stop at a not-yet-published one and re-read from there (partition 0 is always
+    // inclusive, so the walk never passes it)
     int j = part - 1;
-    while (true) {
-      const uint32_t s = *(volatile uint32_t*)(st + size_t(j) * 256 + d);
-      const uint32_t f = s & ~kValMask;
-      if (f == 0) continue;
-      excl += s & kValMask;
-      if (f == kFlagInc) break;
-      --j;
+    bool found = false;
+    while (!found) {
+      uint32_t sv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        sv[k] = j - k >= 0 ? uint32_t(*(volatile uint32_t*)(st + size_t(j - k) * 256 + d)) : uint32_t(2u << 30);
+      int used = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t f = sv[k] & ~kValMask;
+        if (f == 0) break;
+        excl += sv[k] & kValMask;
+        if (f == kFlagInc) {
+          found = true;
+          break;
+        }
+        used = k + 1;
+      }
+      j -= used;
     }
     *my = kFlagInc | (excl + cnt);
   }
