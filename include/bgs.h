@@ -140,9 +140,11 @@ bgs_status bgs_query(bgs_ctx* ctx, int64_t* out /*[BGS_Q_COUNT] host*/);
  * the producing stage):
  *   0 records [F]x48 B {mx,my,A,B, C,o,r,g, b,depth,gid,rect(x0|y0<<8|x1<<16|y1<<24)}
  *   1 record local index [F] u32       2 received records [R]x48 B (== 0 when world == 1)
- *   3 sorted keys [P] u64 ((tile-tile_begin) << nb | (f32 bits(depth) - lo)), lo = 0xffffffff -
- *     counters[6], hi = counters[7] (min / max depth bits of the received records), nb = bit width
- *     of hi - lo: an exact order-preserving packing of (tile, depth)     4 sorted values [P] u32
+ *   3 sorted keys [P] u32 ((tile-tile_begin) << kd | (f32 bits(depth) - lo) >> (nb - kd)), lo =
+ *     0xffffffff - counters[6], hi = counters[7] (min / max depth bits of the received records),
+ *     nb = bit width of hi - lo, kd = min(nb, 32 - tile bits), tile bits = bit width of
+ *     (tile_end - tile_begin - 1); equal keys are ordered by (depth, global id)
+ *                                                                     4 sorted values [P] u32
  *     (index into received records)    5 tile ranges [tile_end-tile_begin] uint2 [start,end)
  *   6 per-received-splat accumulators [R]x48 B {m_x, m_y, m_xx, m_xy, m_yy, dL/do, dL/d(r,g,b) f32,
  *     a u32, w_fixed u64}; m_* = sums over pixels of gd*dx, gd*dy, gd*dx^2, gd*dx*dy, gd*dy^2 with

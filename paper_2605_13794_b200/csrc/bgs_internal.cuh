@@ -46,15 +46,18 @@ enum Counter : int {
   C_NCOUNTERS = 8
 };
 
-// Sort key of a pair (a5/a6): (local tile << nb) | (bits(depth) - lo), lo = min depth bits,
-// nb = bit width of (max - min) depth bits.  Depths are positive floats, so their bit patterns
-// order like the values and the subtraction is an exact order-preserving map onto [0, 2^nb):
-// the key orders (tile, depth) exactly as (tile << 31 | bits) would, in nb + tile bits.
+// Sort key of a pair (a5/a6), 32 bits: (local tile << kd) | ((bits(depth) - lo) >> sd).
+// lo = min depth bits, nb = bit width of (max - min) depth bits.  Depths are positive floats, so
+// their bit patterns order like the values and bits - lo is an exact order-preserving map onto
+// [0, 2^nb).  kd = min(nb, 32 - tbits) of those bits are kept (sd = nb - kd dropped from the
+// bottom, 0 unless nb + tbits > 32); the key then orders pairs by (tile, depth) up to runs of
+// equal keys, which k_ranges_fixup orders by (full depth bits, global id) -- so the final order
+// is exactly (tile, depth, gid) (R12).  Rubble views: nb = 22..24, tbits = 12, sd = 2..4.
 struct KeyLayout {
   uint32_t lo;
-  int nb;
+  int nb, kd, sd;
 };
-__host__ __device__ inline KeyLayout key_layout(unsigned long long c_dlo, unsigned long long c_dhi) {
+__host__ __device__ inline KeyLayout key_layout(unsigned long long c_dlo, unsigned long long c_dhi, int tbits) {
   KeyLayout k;
   k.lo = 0xffffffffu - uint32_t(c_dlo);
   const uint32_t hi = uint32_t(c_dhi);
@@ -66,6 +69,8 @@ __host__ __device__ inline KeyLayout key_layout(unsigned long long c_dlo, unsign
   while (nb < 32 && (span >> nb) != 0u) ++nb;
   k.nb = nb;
 #endif
+  k.kd = k.nb < 32 - tbits ? k.nb : 32 - tbits;
+  k.sd = k.nb - k.kd;
   return k;
 }
 
@@ -117,6 +122,7 @@ struct SortArgs {
   uint32_t* pass_ctrl;       // [16]: active flags, src selectors, partition counters
   uint32_t* status;          // look-back status [n_parts][256] per pass
   int n_passes;
+  int tbits;                 // bits of the local tile index (per-view sort: 32-bit keys, KeyLayout)
   uint2* ranges;             // [t_end - t_begin]
   float4* aux;               // [n_recv] per-record raster constants (thr, half extent x, half extent y, -)
 };
@@ -124,7 +130,8 @@ struct SortArgs {
 void launch_emit(const SortArgs& a, cudaStream_t s);
 // world > 1: depth range of the received records into counters C_DLO / C_DHI (zeroed by the caller)
 void launch_depth_range(const Rec* recv, int64_t n, unsigned long long* counters, cudaStream_t s);
-void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches);
+// key_bytes: 4 (per-view pairs, keys[] hold uint32_t) or 8 (Morton layout, unsigned long long)
+void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches, int key_bytes);
 void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s);
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* perm, cudaStream_t s);
 // layout.cu: Morton permutation of a shard (keys/vals/digit_hist/pass_ctrl/status of `a` used as scratch)

@@ -104,7 +104,7 @@ void launch_spatial_order(const float4* mean_opac, int64_t n, unsigned int* box,
   k_bbox<<<grid_of(n), 256, 0, s>>>(mean_opac, n, box);
   k_morton<<<grid_of(n), 256, 0, s>>>(mean_opac, n, box, a);
   *launches += 2;
-  launch_sort_passes(a, n, s, launches);
+  launch_sort_passes(a, n, s, launches, 8);
   k_copy_perm<<<grid_of(n), 256, 0, s>>>(a, n, perm);
   *launches += 1;
 }

@@ -430,7 +430,7 @@ bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** ptr, int64_t* by
     case 0: p = ctx->recs.p; b = ctx->F * 48; break;
     case 1: p = ctx->rec_lidx.p; b = ctx->F * 4; break;
     case 2: p = ctx->world > 1 ? ctx->recvbuf.p : nullptr; b = ctx->world > 1 ? ctx->R * 48 : 0; break;
-    case 3: p = ctx->keys[sel].p; b = ctx->P * 8; break;
+    case 3: p = ctx->keys[sel].p; b = ctx->P * 4; break;
     case 4: p = ctx->vals[sel].p; b = ctx->P * 4; break;
     case 5: p = ctx->ranges.p; b = int64_t(ctx->t_end - ctx->t_begin) * 8; break;
     case 6: p = ctx->acc.p; b = ctx->R * 48; break;
@@ -650,12 +650,14 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   const int nt = ctx->t_end - ctx->t_begin;
   int tbits = 0;
   while ((1 << tbits) < std::max(nt, 1)) ++tbits;
-  // key = (local tile << nb) | (bits(depth) - lo) (KeyLayout).  World 1: the records are the
-  // received set and their depth range came back with the projection counters, so the pass
-  // count is exact.  World > 1: the range of the received records is computed on the device and
-  // the passes are launched for nb = 32; passes whose digit is constant skip on the device.
-  const int nbits = ctx->world == 1 ? key_layout(ctx->h_counters[C_DLO], ctx->h_counters[C_DHI]).nb : 32;
-  ctx->n_passes = std::max(1, (nbits + tbits + 7) / 8);
+  // 32-bit key = (local tile << kd) | ((bits(depth) - lo) >> sd) (KeyLayout).  World 1: the
+  // records are the received set and their depth range came back with the projection counters,
+  // so the pass count is exact.  World > 1: the range of the received records is computed on
+  // the device and 4 passes are launched; passes whose digit is constant skip on the device.
+  const int kbits = ctx->world == 1 ? std::min(32, tbits + key_layout(ctx->h_counters[C_DLO],
+                                                                      ctx->h_counters[C_DHI], tbits).nb)
+                                    : 32;
+  ctx->n_passes = std::max(1, (kbits + 7) / 8);
   SortArgs a{};
   a.recv = ctx->recv;
   a.n_recv = ctx->R;
@@ -679,6 +681,7 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   a.pass_ctrl = P_<uint32_t>(ctx->pass_ctrl);
   a.status = P_<uint32_t>(ctx->status);
   a.n_passes = ctx->n_passes;
+  a.tbits = tbits;
   a.ranges = P_<uint2>(ctx->ranges);
   CKS(ensure(ctx, ctx->aux, size_t(std::max<int64_t>(ctx->R, 1)) * 16));
   a.aux = P_<float4>(ctx->aux);
@@ -699,7 +702,7 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
     CKS(launched(ctx));
   }
   int64_t nl = 0;
-  launch_sort_passes(a, P, s, &nl);
+  launch_sort_passes(a, P, s, &nl, 4);
   CKS(launched(ctx, int(nl)));
   if (P > 0) {
     launch_ranges_fixup(a, P, s);

@@ -3,12 +3,14 @@
 // PAPER.md P:152 ("rasterized by tile-based front-to-back alpha compositing"), Eq.2
 // (N(p) depth-ordered), SPEC S:116 / S:172 (ties by global id, reading R12).
 //
-// Key = (local tile << nb) | (f32 bits(depth) - lo) (KeyLayout, bgs_internal.cuh).  depth >
-// near_clip > 0, so the unsigned order of the bits is the numeric order of the depths and
-// subtracting the minimum maps them exactly onto [0, 2^nb); a view's depths span 22-24 bits on
-// the Rubble workload, so the key has 34-36 bits (5 onesweep passes instead of 6 for tile << 31).
-// The digit histograms of the passes that see depth bits only are added once per record
-// (weighted by its owned pair count); only the tile-bearing digits are counted per pair.
+// Key (32 bits) = (local tile << kd) | ((f32 bits(depth) - lo) >> sd) (KeyLayout,
+// bgs_internal.cuh).  depth > near_clip > 0, so the unsigned order of the bits is the numeric
+// order of the depths and subtracting the minimum maps them exactly onto [0, 2^nb); the lowest
+// sd = nb - kd of those bits are dropped when nb + tile bits > 32 and k_ranges_fixup orders the
+// resulting runs of equal keys by (full depth bits, gid), so the final order is exact.  Rubble
+// views: nb = 22..24 and 12 tile bits -> 4 passes over 4-byte keys (vs 6 over 8-byte keys for
+// tile << 31 | bits).  The digit histograms of the passes that see depth bits only are added
+// once per record (weighted by its owned pair count); only tile-bearing digits count per pair.
 //
 // a5: one warp expands the rects of 32 received records cooperatively (slot = position in a
 //     rect, warp-scan + 5-step shuffle search for the owning lane), keeps the slots whose tile
@@ -37,8 +39,8 @@ constexpr int kCtrlActive = 0;   // [8]
 constexpr int kCtrlSel = 8;      // [7] input buffer of pass p
 constexpr int kCtrlPart = 16;    // [8] partition counters
 
-__device__ __forceinline__ unsigned long long make_key(uint32_t lt, uint32_t dbits, KeyLayout kl) {
-  return (static_cast<unsigned long long>(lt) << kl.nb) | static_cast<unsigned long long>(dbits - kl.lo);
+__device__ __forceinline__ uint32_t make_key(uint32_t lt, uint32_t dbits, KeyLayout kl) {
+  return uint32_t((static_cast<unsigned long long>(lt) << kl.kd) | ((dbits - kl.lo) >> kl.sd));
 }
 
 // Exclusive scan of one value per thread over a 256-thread CTA (warp shuffles + 8 warp totals).
@@ -84,8 +86,9 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
   for (int j = threadIdx.x; j < kMaxSortPasses * 256; j += blockDim.x) (&s_hist[0][0])[j] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const KeyLayout kl = key_layout(a.counters[C_DLO], a.counters[C_DHI]);
-  const int p_pair = kl.nb / 8;  // passes below this one see depth bits only
+  const KeyLayout kl = key_layout(a.counters[C_DLO], a.counters[C_DHI], a.tbits);
+  const int p_pair = kl.kd / 8;  // passes below this one see depth bits only
+  uint32_t* __restrict__ keys_out = reinterpret_cast<uint32_t*>(a.keys[0]);
   const int64_t n_chunks = (a.n_recv + 255) / 256;
   for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
   const int64_t r = ch * 256 + threadIdx.x;
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
     // digits made of depth bits only are the same for every pair of this record: one weighted
     // add per record instead of one per pair
     if (own) {
-      const uint32_t dk = dbits - kl.lo;
+      const uint32_t dk = (dbits - kl.lo) >> kl.sd;
       for (int p = 0; p < p_pair && p < a.n_passes; ++p) atomicAdd(&s_hist[p][(dk >> (8 * p)) & 255u], own);
     }
   }
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
   for (uint32_t chunk = 0; chunk < total_area; chunk += 32) {
     const uint32_t slot = chunk + lane;
     bool ok = false;
-    unsigned long long key = 0;
+    uint32_t key = 0;
     uint32_t val = 0;
     // smallest lane j with incl[j] > slot
     int j = 0;
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
     if (ok) {
       const unsigned long long pos = base + run + __popc(m & ((1u << lane) - 1u));
       if ((int64_t)pos < a.cap) {
-        a.keys[0][pos] = key;
+        keys_out[pos] = key;
         a.vals[0][pos] = val;
       }
       for (int p = p_pair; p < npass; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 255u], 1u);
@@ -222,12 +225,13 @@ __global__ void __launch_bounds__(256) k_digit_scan(SortArgs a) {
   if (threadIdx.x == 0) a.pass_ctrl[kFinalSel] = sel;
 }
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int pass, int n_parts) {
+template <int NW, typename K>
+__global__ void __launch_bounds__(NW * 32, sizeof(K) == 4 ? 3 : 2) k_onesweep(SortArgs a, int64_t P, int pass,
+                                                                            int n_parts) {
   constexpr int NT = NW * 32;
   constexpr int PART = NT * kSortItems;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(smem_raw);
+  K* s_keys = reinterpret_cast<K*>(smem_raw);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + PART);
   __shared__ uint32_t s_whist[NW][256];
   __shared__ uint32_t s_bstart[256];
@@ -236,9 +240,9 @@ __global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int
 
   if (a.pass_ctrl[kCtrlActive + pass] == 0) return;
   const uint32_t sel = a.pass_ctrl[kCtrlSel + pass];
-  const unsigned long long* __restrict__ kin = sel ? a.keys[1] : a.keys[0];
+  const K* __restrict__ kin = reinterpret_cast<const K*>(sel ? a.keys[1] : a.keys[0]);
   const uint32_t* __restrict__ vin = sel ? a.vals[1] : a.vals[0];
-  unsigned long long* __restrict__ kout = sel ? a.keys[0] : a.keys[1];
+  K* __restrict__ kout = reinterpret_cast<K*>(sel ? a.keys[0] : a.keys[1]);
   uint32_t* __restrict__ vout = sel ? a.vals[0] : a.vals[1];
   const int shift = 8 * pass;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -250,7 +254,7 @@ __global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int
   const int64_t base = int64_t(part) * PART;
   const int64_t wbase = base + int64_t(w) * (32 * kSortItems);
 
-  unsigned long long key[kSortItems];
+  K key[kSortItems];
   uint32_t val[kSortItems];
   uint32_t rank[kSortItems];
 #pragma unroll
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int
       key[i] = kin[idx];
       val[i] = vin[idx];
     } else {
-      key[i] = ~0ull;
+      key[i] = K(~K(0));
       val[i] = 0;
     }
   }
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(NW * 32) k_onesweep(SortArgs a, int64_t P, int
   __syncthreads();
   const int nvalid = int(P - base < int64_t(PART) ? P - base : int64_t(PART));
   for (int j = tid; j < nvalid; j += NT) {
-    const unsigned long long k = s_keys[j];
+    const K k = s_keys[j];
     const uint32_t dd = uint32_t((k >> shift) & 255u);
     const uint32_t o = s_gstart[dd] + (uint32_t(j) - s_bstart[dd]);
     kout[o] = k;
@@ -353,24 +357,28 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const uint32_t sel = a.pass_ctrl[kFinalSel];
-  const unsigned long long* keys = sel ? a.keys[1] : a.keys[0];
+  const uint32_t* keys = reinterpret_cast<const uint32_t*>(sel ? a.keys[1] : a.keys[0]);
   uint32_t* vals = sel ? a.vals[1] : a.vals[0];
-  const int nb = key_layout(a.counters[C_DLO], a.counters[C_DHI]).nb;
-  const unsigned long long k = keys[i];
-  const uint32_t t = uint32_t(k >> nb);
-  const unsigned long long kp = i > 0 ? keys[i - 1] : ~0ull;
-  const unsigned long long kn = i + 1 < P ? keys[i + 1] : ~0ull;
-  if (i == 0 || uint32_t(kp >> nb) != t) a.ranges[t].x = uint32_t(i);
-  if (i + 1 == P || uint32_t(kn >> nb) != t) a.ranges[t].y = uint32_t(i + 1);
-  if (kn == k && kp != k) {
-    // run of identical (tile, depth) keys starting at i: order by global id (R12)
+  const int kd = key_layout(a.counters[C_DLO], a.counters[C_DHI], a.tbits).kd;
+  const uint32_t k = keys[i];
+  const uint32_t t = uint32_t((unsigned long long)k >> kd);
+  const bool first = i == 0 || keys[i - 1] != k;
+  const bool last = i + 1 == P || keys[i + 1] != k;
+  if ((i == 0 || uint32_t((unsigned long long)keys[i - 1] >> kd) != t)) a.ranges[t].x = uint32_t(i);
+  if ((i + 1 == P || uint32_t((unsigned long long)keys[i + 1] >> kd) != t)) a.ranges[t].y = uint32_t(i + 1);
+  if (first && !last) {
+    // run of identical keys starting at i (same tile, same kept depth bits): order it by
+    // (full f32 depth bits, global id) (R12; KeyLayout drops the lowest sd depth bits)
     int64_t e = i + 1;
     while (e + 1 < P && keys[e + 1] == k) ++e;
     for (int64_t x = i + 1; x <= e; ++x) {
       const uint32_t v = vals[x];
-      const uint32_t g = a.recv[v].gid;
+      const unsigned long long o = ((unsigned long long)__float_as_uint(a.recv[v].depth) << 32) | a.recv[v].gid;
       int64_t y = x - 1;
-      while (y >= i && a.recv[vals[y]].gid > g) {
+      while (y >= i) {
+        const Rec& ry = a.recv[vals[y]];
+        const unsigned long long oy = ((unsigned long long)__float_as_uint(ry.depth) << 32) | ry.gid;
+        if (oy <= o) break;
         vals[y + 1] = vals[y];
         --y;
       }
@@ -403,21 +411,29 @@ void launch_depth_range(const Rec* recv, int64_t n, unsigned long long* counters
   k_depth_range<<<unsigned(blocks), 256, 0, s>>>(recv, n, counters);
 }
 
-void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches) {
-  k_digit_scan<<<1, 256, 0, s>>>(a);
-  ++*launches;
-  if (P <= 0) return;
+template <typename K>
+static void sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches) {
   const int n_parts = int((P + kSortPart - 1) / kSortPart);
-  const size_t smem = size_t(kSortPart) * (sizeof(unsigned long long) + sizeof(uint32_t));
+  const size_t smem = size_t(kSortPart) * (sizeof(K) + sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_onesweep<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_onesweep<8, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr_set = true;
   }
   for (int p = 0; p < a.n_passes; ++p) {
-    k_onesweep<8><<<n_parts, 256, smem, s>>>(a, P, p, n_parts);
+    k_onesweep<8, K><<<n_parts, 256, smem, s>>>(a, P, p, n_parts);
     ++*launches;
   }
+}
+
+void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches, int key_bytes) {
+  k_digit_scan<<<1, 256, 0, s>>>(a);
+  ++*launches;
+  if (P <= 0) return;
+  if (key_bytes == 4)
+    sort_passes<uint32_t>(a, P, s, launches);
+  else
+    sort_passes<unsigned long long>(a, P, s, launches);
 }
 
 void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s) {

@@ -27,14 +27,14 @@ def acc_view(raw: torch.Tensor) -> dict:
                 w=b.view(np.uint64).reshape(-1, 6)[:, 5].copy())
 
 
-def decode_keys(keys: np.ndarray, counters: np.ndarray):
-    """Sorted keys (include/bgs.h debug buffer 3) -> (local tile, f32 bits of depth)."""
+def decode_key_tiles(keys: np.ndarray, counters: np.ndarray, n_tiles: int) -> np.ndarray:
+    """Sorted u32 keys (include/bgs.h debug buffer 3) -> local tile of every pair."""
     lo = 0xFFFFFFFF - int(counters[6] & np.uint64(0xFFFFFFFF))
     hi = int(counters[7] & np.uint64(0xFFFFFFFF))
     nb = max(0, hi - lo).bit_length()
-    tiles = (keys >> np.uint64(nb)).astype(np.int32)
-    dbits = ((keys & np.uint64((1 << nb) - 1)) + np.uint64(lo)).astype(np.uint32)
-    return tiles, dbits
+    tbits = max(0, int(n_tiles) - 1).bit_length()
+    kd = min(nb, 32 - tbits)
+    return (keys.astype(np.uint64) >> np.uint64(kd)).astype(np.int32)
 
 
 def moments_to_g2d(g: np.ndarray, rec: dict) -> np.ndarray:
@@ -96,9 +96,10 @@ class GpuStep:
                     out["owner"] = owner.cpu().numpy()
                     B.bgs_sort_tiles(ctx, stream)
                     out["q"] = ctx.query()
-                    out["keys"] = ctx.debug_buffer("keys").view(torch.int64).cpu().numpy().view(np.uint64)
+                    out["keys"] = ctx.debug_buffer("keys").view(torch.int32).cpu().numpy().view(np.uint32)
                     out["counters"] = ctx.debug_buffer("counters").view(torch.int64).cpu().numpy().view(np.uint64)
-                    out["key_tile"], out["key_dbits"] = decode_keys(out["keys"], out["counters"])
+                    out["key_tile"] = decode_key_tiles(out["keys"], out["counters"],
+                                                       out["q"]["tile_end"] - out["q"]["tile_begin"])
                     out["vals"] = ctx.debug_buffer("vals").view(torch.int32).cpu().numpy()
                     out["ranges"] = ctx.debug_buffer("ranges").view(torch.int32).cpu().numpy().reshape(-1, 2)
                     recv = ctx.debug_buffer("recv") if M > 1 else ctx.debug_buffer("records")

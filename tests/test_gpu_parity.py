@@ -80,7 +80,8 @@ def test_sort_and_ranges_bit_exact(tiny_run):
     sc, cam, dl, st, gs = tiny_run
     o = gs.rank[0]
     vals = o["vals"]
-    tiles, dbits = o["key_tile"], o["key_dbits"]
+    tiles = o["key_tile"]
+    dbits = o["recv"]["depth"][vals].view(np.uint32)
     gid = o["recv"]["gid"][vals]
     assert np.array_equal(tiles, st.get("pair_tile", 0))
     assert np.array_equal(gid, st.get("pair_gid", 0))
