@@ -3,8 +3,8 @@
 These are what the METHOD must move or compute, not what a kernel happens to do:
   a1+a2 project      16 N (mu,o) + 1 N (lod) + N/8 (cull column, if any) + 32 A (q, s of active)
                      + 192 F (SH of in-frustum) + 52 F (record + index) + 4 N (radius)      [bytes]
-  a5-a7 sort         16 R (rect, depth of received) + 12 P (pairs) + 24 P per executed 8-bit
-                     radix pass + 8 P (ranges pass)                                        [bytes]
+  a5-a7 sort         16 R (rect, depth of received) + 8 P (u32 key + u32 value written) + 16 P
+                     per executed 8-bit radix pass (read + write) + 4 P (ranges pass)     [bytes]
   a8 raster fwd      19 FP32 ops per (pixel, list entry) up to the pixel's last contributor
                      (E = sum of n_contrib): dx,dy 2, power 5, alpha cut 1, exp 1, alpha = min(.99,
                      oG) 2, w = alpha T and T -= w 2, early stop 1, colour 3, w and a sums 2 [ALU]
@@ -42,7 +42,7 @@ def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=No
     bytes_ = {
         "project": 16 * N + N + (N / 8 if cull else 0) + 32 * A + 192 * F + 52 * F + 4 * N,
         "route": (48 * D + 48 * R) if world > 1 else 0.0,
-        "sort": 16 * R + 12 * P + 24 * P * passes + 8 * P,
+        "sort": 16 * R + 8 * P + 16 * P * passes + 4 * P,
         "route_reverse": (96 * D) if world > 1 else 0.0,
         "project_bwd": 240 * F + 52 * F + 2 * 236 * F,
         "importance": 52 * F + 32 * F + N / 8,
