@@ -151,6 +151,7 @@ struct RasterArgs {
   Acc* acc;
   const float4* aux;          // per received record: thr, box half extents (from k_emit)
   const uint32_t* tile_perm;  // launch order of the owned tiles (longest list first)
+  int n_split;                // the first n_split tiles of tile_perm run as two half-tile CTAs
 };
 constexpr int kFinalSel = 15;
 void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,

@@ -111,38 +111,37 @@ __device__ __forceinline__ void eval_fwd1(PixF& p, const WRec& s, float dx, floa
   f = __float2uint_rn(w * 16777216.0f);
 }
 
-// Forward evaluation of the two pixels of a lane against one record, branch-free so that the
-// two dependency chains interleave.  c0/c1: contributed; f0/f1: alpha*T in 2^-24 fixed point.
-__device__ __forceinline__ void eval_fwd2(PixF& p0, PixF& p1, const WRec& s, float pxf, float pyf0, float pyf1,
-                                          uint32_t pos, bool& c0, bool& c1, uint32_t& f0, uint32_t& f1) {
-  const float dx = s.geo.x - pxf;
-  eval_fwd1(p0, s, dx, s.geo.y - pyf0, pos, c0, f0);
-  eval_fwd1(p1, s, dx, s.geo.y - pyf1, pos, c1, f1);
-}
-
-template <bool kImportance>
-__global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __restrict__ rgb,
-                                                         float* __restrict__ t_final,
-                                                         int32_t* __restrict__ n_contrib) {
-  __shared__ WRec s_rec[kWarps][32];
-  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
-  const int lt = int(__ldg(a.tile_perm + blockIdx.x));
+// One warp composites a 16 x 2kPix strip of tile lt starting at tile row `row0`: lane covers
+// column lane & 15 and rows row0 + (lane >> 4) + 2i, i < kPix (kPix independent dependency
+// chains per lane, branch-free).
+template <bool kImportance, int kPix>
+__device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* __restrict__ vals, int lt, int row0,
+                                          WRec* mine, float* __restrict__ rgb, float* __restrict__ t_final,
+                                          int32_t* __restrict__ n_contrib) {
   const int tile = a.t_begin + lt;
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int px = tx * kTile + (lane & 15);
-  const int py0 = ty * kTile + 4 * warp + (lane >> 4), py1 = py0 + 2;
-  const bool in0 = px < a.W && py0 < a.H, in1 = px < a.W && py1 < a.H;
+  const int pyb = ty * kTile + row0 + (lane >> 4);
   const uint2 range = a.ranges[lt];
-  const float pxf = float(px), pyf0 = float(py0), pyf1 = float(py1);
-  const float x0 = float(tx * kTile), y0 = float(ty * kTile + 4 * warp);
-  PixF p0{in0 ? 1.f : -1.f, 0.f, 0.f, 0.f, 0u}, p1{in1 ? 1.f : -1.f, 0.f, 0.f, 0.f, 0u};
-  WRec* mine = s_rec[warp];
+  const float pxf = float(px);
+  const float x0 = float(tx * kTile), y0 = float(ty * kTile + row0);
+  PixF p[kPix];
+  float pyf[kPix];
+#pragma unroll
+  for (int i = 0; i < kPix; ++i) {
+    const int py = pyb + 2 * i;
+    pyf[i] = float(py);
+    p[i] = PixF{px < a.W && py < a.H ? 1.f : -1.f, 0.f, 0.f, 0.f, 0u};
+  }
   for (uint32_t base = range.x; base < range.y; base += 32) {
-    if (__all_sync(0xffffffffu, p0.T < 0.f && p1.T < 0.f)) break;
+    bool done = true;
+#pragma unroll
+    for (int i = 0; i < kPix; ++i) done = done && p[i].T < 0.f;
+    if (__all_sync(0xffffffffu, done)) break;
     const uint32_t idx = base + lane;
     WRec st;
-    const bool hit = idx < range.y && stage_test(a, vals, idx, x0, y0, 4, st);
+    const bool hit = idx < range.y && stage_test(a, vals, idx, x0, y0, 2 * kPix, st);
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (hit) mine[lane] = st;
     __syncwarp();
@@ -154,12 +153,19 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
       m &= m - 1;
       const WRec s = mine[j];
       const uint32_t pos = base + j + 1 - range.x;
-      uint32_t f0, f1;
-      bool c0, c1;
-      eval_fwd2(p0, p1, s, pxf, pyf0, pyf1, pos, c0, c1, f0, f1);
+      const float dx = s.geo.x - pxf;
+      uint32_t fs = 0, cs = 0;
+#pragma unroll
+      for (int i = 0; i < kPix; ++i) {
+        uint32_t f;
+        bool c;
+        eval_fwd1(p[i], s, dx, s.geo.y - pyf[i], pos, c, f);
+        fs += f;
+        cs += uint32_t(c);
+      }
       if (kImportance) {
-        const uint32_t sum = __reduce_add_sync(0xffffffffu, f0 + f1);
-        const uint32_t cnt = __reduce_add_sync(0xffffffffu, uint32_t(c0) + uint32_t(c1));
+        const uint32_t sum = __reduce_add_sync(0xffffffffu, fs);
+        const uint32_t cnt = __reduce_add_sync(0xffffffffu, cs);
         if (lane == j) {
           my_w = sum;
           my_a = cnt;
@@ -174,21 +180,40 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
     __syncwarp();
   }
   const size_t plane = size_t(a.W) * a.H;
-  if (in0) {
-    const size_t pix = size_t(py0) * a.W + px;
-    rgb[pix] = p0.r;
-    rgb[plane + pix] = p0.g;
-    rgb[2 * plane + pix] = p0.b;
-    t_final[pix] = fabsf(p0.T);
-    n_contrib[pix] = int32_t(p0.last);
+#pragma unroll
+  for (int i = 0; i < kPix; ++i) {
+    const int py = pyb + 2 * i;
+    if (px < a.W && py < a.H) {
+      const size_t pix = size_t(py) * a.W + px;
+      rgb[pix] = p[i].r;
+      rgb[plane + pix] = p[i].g;
+      rgb[2 * plane + pix] = p[i].b;
+      t_final[pix] = fabsf(p[i].T);
+      n_contrib[pix] = int32_t(p[i].last);
+    }
   }
-  if (in1) {
-    const size_t pix = size_t(py1) * a.W + px;
-    rgb[pix] = p1.r;
-    rgb[plane + pix] = p1.g;
-    rgb[2 * plane + pix] = p1.b;
-    t_final[pix] = fabsf(p1.T);
-    n_contrib[pix] = int32_t(p1.last);
+}
+
+// Work split (longest-list-first order in tile_perm): the n_split heaviest tiles get TWO CTAs
+// each (blocks 2k, 2k+1 = rows 0-7 / 8-15 of tile perm[k]; 4 warps x 16x2 strips, one pixel per
+// lane), every other tile one CTA (4 warps x 16x4 strips, two pixels per lane).  A warp walks the
+// whole list of its tile, so the heaviest tiles (6-8x the mean list length on Rubble views) set
+// the kernel's makespan; halving their pixels per warp and their strip height shortens exactly
+// those walks.
+template <bool kImportance>
+__global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __restrict__ rgb,
+                                                         float* __restrict__ t_final,
+                                                         int32_t* __restrict__ n_contrib) {
+  __shared__ WRec s_rec[kWarps][32];
+  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
+  const int warp = threadIdx.x >> 5;
+  const int b = blockIdx.x;
+  if (b < 2 * a.n_split) {
+    const int lt = int(__ldg(a.tile_perm + (b >> 1)));
+    fwd_strip<kImportance, 1>(a, vals, lt, (b & 1) * 8 + 2 * warp, s_rec[warp], rgb, t_final, n_contrib);
+  } else {
+    const int lt = int(__ldg(a.tile_perm + (b - a.n_split)));
+    fwd_strip<kImportance, 2>(a, vals, lt, 4 * warp, s_rec[warp], rgb, t_final, n_contrib);
   }
 }
 
@@ -251,24 +276,22 @@ __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float
 
 __device__ __forceinline__ float xsel(bool hi, float a, float b) { return hi ? a : b; }
 
-// kPix pixels per lane (rows r, r+2, ..., r+2(kPix-1) of a 16 x 2kPix strip per warp; 8/kPix warps
-// per tile): more pixels per lane amortise the per-(warp, record) gradient reduction.
+// Backward of one warp's 16 x 2kPix strip starting at tile row `row0` (layout as fwd_strip).
+// More pixels per lane amortise the per-(warp, record) gradient reduction; fewer shorten the
+// walk of the heaviest tiles (k_raster_bwd's work split).
 template <int kPix>
-__global__ void __launch_bounds__(32 * (8 / kPix)) k_raster_bwd(RasterArgs a, const float* __restrict__ dL,
-                                                                const float* __restrict__ t_final,
-                                                                const int32_t* __restrict__ n_contrib) {
-  constexpr int kW = 8 / kPix, kStripH = 2 * kPix;
-  __shared__ WRec s_rec[kW][32];
-  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
-  const int lt = int(__ldg(a.tile_perm + blockIdx.x));
+__device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* __restrict__ vals, int lt, int row0,
+                                          WRec* mine, const float* __restrict__ dL,
+                                          const float* __restrict__ t_final, const int32_t* __restrict__ n_contrib) {
+  constexpr int kStripH = 2 * kPix;
   const int tile = a.t_begin + lt;
   const int tx = tile % a.TX, ty = tile / a.TX;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int px = tx * kTile + (lane & 15);
-  const int pyb = ty * kTile + kStripH * warp + (lane >> 4);
+  const int pyb = ty * kTile + row0 + (lane >> 4);
   const uint2 range = a.ranges[lt];
   const float pxf = float(px);
-  const float x0 = float(tx * kTile), y0 = float(ty * kTile + kStripH * warp);
+  const float x0 = float(tx * kTile), y0 = float(ty * kTile + row0);
   const size_t plane = size_t(a.W) * a.H;
   PixB p[kPix];
   float pyf[kPix];
@@ -283,7 +306,6 @@ __global__ void __launch_bounds__(32 * (8 / kPix)) k_raster_bwd(RasterArgs a, co
   const uint32_t wlast = __reduce_max_sync(0xffffffffu, plast);
   const bool hi16 = lane & 16, hi8 = lane & 8, hi4 = lane & 4;
   const int my_idx = (hi16 ? 4 : 0) + (hi8 ? 2 : 0) + (hi4 ? 1 : 0);
-  WRec* mine = s_rec[warp];
   // chunks of 32 list positions, from the warp's deepest contributor back to the front
   for (int c = int((wlast + 31) / 32) - 1; c >= 0; --c) {
     const uint32_t pos0 = uint32_t(c) * 32;  // relative to range.x
@@ -346,24 +368,66 @@ __global__ void __launch_bounds__(32 * (8 / kPix)) k_raster_bwd(RasterArgs a, co
   }
 }
 
+// Same work split as k_raster_fwd.
+__global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterArgs a, const float* __restrict__ dL,
+                                                         const float* __restrict__ t_final,
+                                                         const int32_t* __restrict__ n_contrib) {
+  __shared__ WRec s_rec[kWarps][32];
+  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
+  const int warp = threadIdx.x >> 5;
+  const int b = blockIdx.x;
+  if (b < 2 * a.n_split) {
+    const int lt = int(__ldg(a.tile_perm + (b >> 1)));
+    bwd_strip<1>(a, vals, lt, (b & 1) * 8 + 2 * warp, s_rec[warp], dL, t_final, n_contrib);
+  } else {
+    const int lt = int(__ldg(a.tile_perm + (b - a.n_split)));
+    bwd_strip<2>(a, vals, lt, 4 * warp, s_rec[warp], dL, t_final, n_contrib);
+  }
+}
+
 }  // namespace
+
+// Heavy tiles split over two CTAs (k_raster_fwd).  BGS_SPLIT_TILES overrides the count (tuning).
+static int split_count(int n_tiles) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("BGS_SPLIT_TILES");
+    env = e ? atoi(e) : -1;
+  }
+  int sms = 148;
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+  }
+  sms = cached > 0 ? cached : sms;
+  // 2 x SMs: measured on Rubble (fwd+bwd ms per view) 0.58 unsplit, 0.530 at 148, 0.526 at 296,
+  // 0.535 at 592
+  const int want = env >= 0 ? env : 2 * sms;
+  return want < n_tiles ? want : n_tiles;
+}
 
 void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
                        cudaStream_t s) {
   if (a.n_tiles <= 0) return;
+  RasterArgs b = a;
+  b.n_split = split_count(a.n_tiles);
+  const unsigned grid = unsigned(a.n_tiles + b.n_split);
   if (flags & BGS_IMPORTANCE)
-    k_raster_fwd<true><<<a.n_tiles, kThreads, 0, s>>>(a, rgb, t_final, n_contrib);
+    k_raster_fwd<true><<<grid, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
   else
-    k_raster_fwd<false><<<a.n_tiles, kThreads, 0, s>>>(a, rgb, t_final, n_contrib);
+    k_raster_fwd<false><<<grid, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
 }
 
 void launch_raster_bwd(const RasterArgs& a, const float* dL, const float* t_final, const int32_t* n_contrib,
                        cudaStream_t s) {
   if (a.n_tiles <= 0) return;
-  // 2 pixels per lane: measured 0.415 ms per Rubble view vs 0.73 ms with 4 (the coarser strip
+  // light tiles: 2 pixels per lane (0.415 ms per Rubble view vs 0.73 ms with 4: the coarser strip
   // culls worse and a warp walks to the deepest of 128 pixels)
-  constexpr int kBwdPix = 2;
-  k_raster_bwd<kBwdPix><<<a.n_tiles, 32 * (8 / kBwdPix), 0, s>>>(a, dL, t_final, n_contrib);
+  RasterArgs b = a;
+  b.n_split = split_count(a.n_tiles);
+  k_raster_bwd<<<unsigned(a.n_tiles + b.n_split), kThreads, 0, s>>>(b, dL, t_final, n_contrib);
 }
 
 }  // namespace bgs
