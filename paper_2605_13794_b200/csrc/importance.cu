@@ -41,8 +41,11 @@ struct alignas(16) ImpState {
   uint32_t need_gid;             // 0 < k < ntie
   uint32_t empty;                // total == 0
   uint32_t r0;                   // first w round with a non-zero digit (from the MSB histogram)
+  uint32_t tshift;               // selection: (w >> tshift) >= prefix (0 after all rounds)
+  uint32_t final_;               // threshold resolved (crossing bin holds one item): no more rounds
   uint32_t pad1;
 };
+static_assert(sizeof(ImpState) <= kImpStateBytes, "ImpState fits its arena slot");
 
 namespace {
 
@@ -79,6 +82,24 @@ __device__ __forceinline__ unsigned long long load_w(const ImportanceArgs& a, in
 
 __device__ __forceinline__ uint32_t gid_of(const ImportanceArgs& a, uint32_t lidx) {
   return lidx * uint32_t(a.world) + uint32_t(a.rank);
+}
+
+// Inclusive scan of one u64 per thread over a 256-thread CTA (shuffles + 8 warp totals).
+__device__ __forceinline__ unsigned long long block_incl_scan256(unsigned long long v) {
+  __shared__ unsigned long long s_w[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) s_w[w] = v;
+  __syncthreads();
+  unsigned long long wb = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) wb += k < w ? s_w[k] : 0ull;
+  __syncthreads();
+  return wb + v;
 }
 
 // ---- bodies shared by the per-round kernels and the cooperative kernel -----------------
@@ -169,6 +190,8 @@ __device__ void init_state(ImpState* st, const unsigned long long* total) {
   st->prefix = 0;
   st->need_gid = 0;
   st->tau = 0;
+  st->tshift = 0;
+  st->final_ = 0;
   int maxbit = 0;
   for (int b = 63; b >= 0; --b)
     if (total[1 + b]) {
@@ -186,18 +209,11 @@ __device__ void decide_body(ImpState* st, int round, const unsigned long long* h
   __shared__ unsigned long long s_suf[256];
   __shared__ int s_pick;
   const int d = threadIdx.x;
-  if (st->empty || round < int(st->r0)) return;
+  if (st->empty || st->final_ || round < int(st->r0)) return;
   const unsigned long long target = (unsigned long long)num * st->total;  // need den*prefix >= target
-  s_suf[255 - d] = hist[256 + d];
-  __syncthreads();
-  for (int o = 1; o < 256; o <<= 1) {
-    const unsigned long long v = d >= o ? s_suf[d - o] : 0ull;
-    __syncthreads();
-    s_suf[d] += v;
-    __syncthreads();
-  }
   // s_suf[j] = mass of digits >= 255 - j; the crossing digit is the largest d with
   // den*(above + mass(>= d)) >= target
+  s_suf[d] = block_incl_scan256(hist[256 + 255 - d]);
   if (d == 0) s_pick = -1;
   __syncthreads();
   const unsigned long long above = st->above;
@@ -212,6 +228,16 @@ __device__ void decide_body(ImpState* st, int round, const unsigned long long* h
     if (pick >= 0) {
       st->above = above + (pick < 255 ? s_suf[254 - pick] : 0ull);
       st->prefix = (st->prefix << 8) | unsigned(pick);
+      st->tshift = uint32_t(8 * (kWRounds - 1 - round));
+      if (round < kWRounds - 1 && hist[pick] == 1) {
+        // the crossing bin holds one item: it is the threshold item (k = ntie = 1) and the
+        // selection is exactly {w : (w >> tshift) >= prefix}; the remaining rounds are skipped
+        st->final_ = 1u;
+        st->k = 1;
+        st->ntie = 1;
+        st->need_gid = 0;
+        st->gid_thr = 0xffffffffu;
+      }
       if (round == kWRounds - 1) {
         const unsigned long long tau = st->prefix;
         st->tau = tau;
@@ -253,14 +279,7 @@ __device__ void gid_decide_body(ImpState* st, int round, const unsigned long lon
   __shared__ int s_pick;
   if (st->empty || !st->need_gid) return;
   const int d = threadIdx.x;
-  s_pre[d] = hist[d];
-  __syncthreads();
-  for (int o = 1; o < 256; o <<= 1) {
-    const unsigned long long v = d >= o ? s_pre[d - o] : 0ull;
-    __syncthreads();
-    s_pre[d] += v;
-    __syncthreads();
-  }
+  s_pre[d] = block_incl_scan256(hist[d]);
   if (d == 0) s_pick = -1;
   __syncthreads();
   const unsigned long long below = st->below, k = st->k;
@@ -280,7 +299,8 @@ __device__ void mark_body(const ImportanceArgs& a, const ImpState& st) {
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items;
        t += int64_t(gridDim.x) * blockDim.x) {
     const unsigned long long w = load_w(a, t);
-    if (w == 0 || w < st.tau) continue;
+    // (w >> tshift) >= prefix; after all rounds tshift = 0 and prefix = tau
+    if (w == 0 || (w >> st.tshift) < st.prefix) continue;
     const uint32_t lidx = a.item_lidx ? a.item_lidx[t] : uint32_t(t);
     if (w == st.tau && st.need_gid && gid_of(a, lidx) > st.gid_thr) continue;
     a.c_vis[lidx] += 1u;
@@ -296,7 +316,7 @@ __global__ void __launch_bounds__(256) k_imp_stats(ImportanceArgs a, unsigned lo
 
 __global__ void __launch_bounds__(256) k_imp_hist(ImportanceArgs a, const ImpState* st, int round,
                                                   unsigned long long* hist) {
-  if (st->empty || round < int(st->r0)) return;
+  if (st->empty || st->final_ || round < int(st->r0)) return;
   hist_body(a, st->prefix, round, hist);
 }
 
@@ -335,7 +355,7 @@ __global__ void __launch_bounds__(256) k_imp_coop(ImportanceArgs a, ImpState* st
   grid.sync();
   if (threadIdx.x == 0) init_state(&st, total);
   __syncthreads();
-  for (int r = int(st.r0); r < kWRounds && !st.empty; ++r) {
+  for (int r = int(st.r0); r < kWRounds && !st.empty && !st.final_; ++r) {
     hist_body(a, st.prefix, r, hist + r * 512);
     grid.sync();
     decide_body(&st, r, hist + r * 512, num, den);

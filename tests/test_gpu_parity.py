@@ -150,14 +150,29 @@ def test_importance_dense_path_bit_exact():
     import paper_2605_13794_b200.bgs as B
     ctx = B.Context()
     rng = np.random.default_rng(5)
-    for trial in range(6):
+    for trial in range(10):
         n = int(rng.integers(1, 200_000))
         if trial == 0:
             w = np.zeros(n, np.uint64)
         elif trial < 3:
             w = (rng.integers(0, 4, n) * (1 << 20)).astype(np.uint64)  # massive ties
-        else:
+        elif trial < 6:
             w = rng.integers(0, 1 << 40, n).astype(np.uint64) * rng.integers(0, 2, n).astype(np.uint64)
+        elif trial == 6:
+            # one dominant item: the crossing bin of the first round holds only it (early exit)
+            w = rng.integers(1, 1 << 20, n).astype(np.uint64)
+            w[rng.integers(0, n)] = np.uint64(1 << 45)
+        elif trial == 7:
+            # heavy-tailed (log-uniform) weights, as the rasterizer produces: crossing bins thin out
+            # after a few rounds
+            w = np.exp(rng.uniform(np.log(1e3), np.log(1e12), n)).astype(np.uint64)
+        elif trial == 8:
+            # a unique item straddling the 99% cut with equal high bits to many others
+            w = np.full(n, np.uint64(1 << 30)) + rng.integers(0, 1 << 8, n).astype(np.uint64)
+        else:
+            # two items only; either may be the threshold
+            n = 2
+            w = np.array([(1 << 33) + 5, (1 << 33) + 3], np.uint64)
         a = np.where(w > 0, rng.integers(1, 300, n), 0).astype(np.uint32)
         rad = np.where(a > 0, 4, rng.integers(0, 2, n) * 4).astype(np.int32)
         ref = O.importance(rad, w, a)
