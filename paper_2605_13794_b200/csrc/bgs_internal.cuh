@@ -226,8 +226,11 @@ void launch_imp_gid_hist(const ImportanceArgs& a, const ImpState* st, int round,
 void launch_imp_gid_decide(ImpState* st, int round, const unsigned long long* hist, cudaStream_t s);
 void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s);
 void launch_fill_bits(uint32_t* words, int64_t n_bits, cudaStream_t s);
-// world == 1: stats + every round + mark in one cooperative launch (hist zeroed by the caller)
-cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* total,
-                            unsigned long long* hist, int num, int den, cudaStream_t s);
+// world == 1: cull fill + stats + every round + mark in one cooperative launch.  `set` (total,
+// histograms, candidate count; imp_set_words() u64) must be zero on entry; the kernel zeroes
+// `next` (same size) for the following call.  cand: u32 scratch [n_items].
+int64_t imp_set_words();
+cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* set,
+                            unsigned long long* next, uint32_t* cand, int num, int den, cudaStream_t s);
 
 }  // namespace bgs

@@ -136,21 +136,33 @@ __device__ void stats_body(const ImportanceArgs& a, unsigned long long* total) {
   __syncthreads();
 }
 
-// candidates of round r: w > 0 and w >> (shift + 8) == prefix
+// candidates of round r: w > 0 and w >> (shift + 8) == prefix.  Items are t in [0, n) or
+// list[t] when list != null; when out != null the candidates are also appended to out
+// (one atomic per warp on *out_count): later rounds scan only them.
 __device__ void hist_body(const ImportanceArgs& a, unsigned long long prefix, int round,
-                          unsigned long long* hist /*[256] count, [256] mass*/) {
+                          unsigned long long* hist /*[256] count, [256] mass*/, const uint32_t* list = nullptr,
+                          int64_t n = -1, uint32_t* out = nullptr, unsigned long long* out_count = nullptr) {
   __shared__ unsigned long long s_cnt[256], s_mass[256];
   s_cnt[threadIdx.x] = 0;
   s_mass[threadIdx.x] = 0;
   __syncthreads();
+  if (n < 0) n = a.n_items;
   const int shift = 8 * (kWRounds - 1 - round);
   const int lane = threadIdx.x & 31;
   // warp-uniform trip count so every lane reaches the warp collectives
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < a.n_items; base += stride) {
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
     const int64_t t = base + lane;
-    const unsigned long long w = t < a.n_items ? load_w(a, t) : 0ull;
+    const int64_t item = t < n ? (list ? int64_t(list[t]) : t) : 0;
+    const unsigned long long w = t < n ? load_w(a, item) : 0ull;
     const bool cand = w != 0 && !(shift + 8 < 64 && (w >> (shift + 8)) != prefix);
+    if (out) {
+      const unsigned cm = __ballot_sync(0xffffffffu, cand);
+      unsigned long long ob = 0;
+      if (lane == 0 && cm) ob = atomicAdd(out_count, (unsigned long long)__popc(cm));
+      ob = __shfl_sync(0xffffffffu, ob, 0);
+      if (cand) out[ob + __popc(cm & ((1u << lane) - 1u))] = uint32_t(item);
+    }
     const uint32_t d = cand ? uint32_t((w >> shift) & 255u) : 256u + lane;
     // one shared-memory atomic per distinct digit of the warp: the early rounds put almost
     // every candidate in one bin, which serialised per-lane 64-bit atomics
@@ -257,13 +269,15 @@ __device__ void decide_body(ImpState* st, int round, const unsigned long long* h
 }
 
 __device__ void gid_hist_body(const ImportanceArgs& a, unsigned long long tau, uint32_t gp, int round,
-                              unsigned long long* hist /*[256] counts*/) {
+                              unsigned long long* hist /*[256] counts*/, const uint32_t* list = nullptr,
+                              int64_t n = -1) {
   __shared__ unsigned long long s_cnt[256];
   s_cnt[threadIdx.x] = 0;
   __syncthreads();
+  if (n < 0) n = a.n_items;
   const int shift = 8 * (kGRounds - 1 - round);
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items;
-       t += int64_t(gridDim.x) * blockDim.x) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = list ? int64_t(list[i]) : i;
     if (load_w(a, t) != tau) continue;
     const uint32_t g = gid_of(a, a.item_lidx ? a.item_lidx[t] : uint32_t(t));
     if (shift + 8 < 32 && (g >> (shift + 8)) != gp) continue;
@@ -296,15 +310,35 @@ __device__ void gid_decide_body(ImpState* st, int round, const unsigned long lon
 
 __device__ void mark_body(const ImportanceArgs& a, const ImpState& st) {
   if (st.empty) return;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const unsigned long long w = load_w(a, t);
-    // (w >> tshift) >= prefix; after all rounds tshift = 0 and prefix = tau
-    if (w == 0 || (w >> st.tshift) < st.prefix) continue;
-    const uint32_t lidx = a.item_lidx ? a.item_lidx[t] : uint32_t(t);
-    if (w == st.tau && st.need_gid && gid_of(a, lidx) > st.gid_thr) continue;
-    a.c_vis[lidx] += 1u;
-    atomicAnd(a.cull + (lidx >> 5), ~(1u << (lidx & 31)));
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < a.n_items; base += stride) {
+    const int64_t t = base + lane;
+    bool sel = false;
+    uint32_t lidx = 0;
+    if (t < a.n_items) {
+      const unsigned long long w = load_w(a, t);
+      // (w >> tshift) >= prefix; after all rounds tshift = 0 and prefix = tau
+      sel = w != 0 && (w >> st.tshift) >= st.prefix;
+      lidx = a.item_lidx ? a.item_lidx[t] : uint32_t(t);
+      if (sel && w == st.tau && st.need_gid && gid_of(a, lidx) > st.gid_thr) sel = false;
+    }
+    if (sel) a.c_vis[lidx] += 1u;
+    // one atomicAnd per (warp, cull word): records come in local-index order, so a warp's
+    // selected items share a few words
+    const uint32_t word = sel ? (lidx >> 5) : (0x80000000u | uint32_t(lane));
+    const unsigned peers = __match_any_sync(0xffffffffu, word);
+    const uint32_t bits = __reduce_or_sync(peers, sel ? (1u << (lidx & 31)) : 0u);
+    if (sel && lane == __ffs(peers) - 1) atomicAnd(a.cull + word, ~bits);
+  }
+}
+
+// all bits [0, n_bits) set, bits past n_bits in the last word clear (grid-stride)
+__device__ __forceinline__ void fill_bits_body(uint32_t* words, int64_t n_bits) {
+  const int64_t nw = (n_bits + 31) / 32;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nw; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t rem = n_bits - 32 * t;
+    words[t] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
   }
 }
 
@@ -346,23 +380,41 @@ __global__ void __launch_bounds__(256) k_imp_mark(ImportanceArgs a, const ImpSta
 
 // ---- world == 1: everything in one cooperative launch ------------------------------------
 
-__global__ void __launch_bounds__(256) k_imp_coop(ImportanceArgs a, ImpState* st_out, unsigned long long* total,
-                                                  unsigned long long* hist /*[7*512 + 4*256], zeroed*/, int num,
-                                                  int den) {
+// set = [total + MSB histogram (65)] [w rounds 7 x 512] [gid rounds 4 x 256] [candidate count 1]
+constexpr int64_t kImpSetWords = 65 + kWRounds * 512 + kGRounds * 256 + 1;
+
+// `set` was zeroed by the previous call (or at allocation); `next` is zeroed here for the next
+// call, so the launch needs no memsets.  The cull words are filled here too.
+__global__ void __launch_bounds__(256) k_imp_coop(ImportanceArgs a, ImpState* st_out, unsigned long long* set,
+                                                  unsigned long long* next, uint32_t* cand, int num, int den) {
   cg::grid_group grid = cg::this_grid();
   __shared__ ImpState st;
+  unsigned long long* total = set;
+  unsigned long long* hist = set + 65;
+  unsigned long long* cand_count = set + kImpSetWords - 1;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < kImpSetWords;
+       t += int64_t(gridDim.x) * blockDim.x)
+    next[t] = 0;
+  fill_bits_body(a.cull, a.n_local);
   stats_body(a, total);
   grid.sync();
   if (threadIdx.x == 0) init_state(&st, total);
   __syncthreads();
+  // (compacting the candidates of round r0 + 1 for the later rounds was measured slower: the
+  // crossing bins stay large and the list append serialises on one counter)
+  const bool listed = false;
+  (void)cand;
+  (void)cand_count;
   for (int r = int(st.r0); r < kWRounds && !st.empty && !st.final_; ++r) {
     hist_body(a, st.prefix, r, hist + r * 512);
     grid.sync();
     decide_body(&st, r, hist + r * 512, num, den);
   }
   if (!st.empty && st.need_gid) {
+    // every tie (w == tau) matched the prefix of every round, so it is in the candidate list
+    const int64_t nl = listed ? int64_t(*(volatile unsigned long long*)cand_count) : -1;
     for (int r = 0; r < kGRounds; ++r) {
-      gid_hist_body(a, st.tau, st.gprefix, r, hist + kWRounds * 512 + r * 256);
+      gid_hist_body(a, st.tau, st.gprefix, r, hist + kWRounds * 512 + r * 256, listed ? cand : nullptr, nl);
       grid.sync();
       gid_decide_body(&st, r, hist + kWRounds * 512 + r * 256);
     }
@@ -424,8 +476,10 @@ void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s
   if (a.n_items > 0) k_imp_mark<<<grid_for(a.n_items), 256, 0, s>>>(a, st);
 }
 
-cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* total,
-                            unsigned long long* hist, int num, int den, cudaStream_t s) {
+int64_t imp_set_words() { return kImpSetWords; }
+
+cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* set,
+                            unsigned long long* next, uint32_t* cand, int num, int den, cudaStream_t s) {
   static int blocks = 0;
   if (blocks == 0) {
     int per_sm = 0, dev = 0, sms = 0;
@@ -437,7 +491,7 @@ cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long
   }
   ImportanceArgs aa = a;
   int nn = num, dd = den;
-  void* args[] = {&aa, &st, &total, &hist, &nn, &dd};
+  void* args[] = {&aa, &st, &set, &next, &cand, &nn, &dd};
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_imp_coop), dim3(blocks), dim3(256), args, 0, s);
 }
 

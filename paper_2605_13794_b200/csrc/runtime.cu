@@ -41,6 +41,7 @@ struct bgs_ctx {
   int stage = 0;  // 1 projected, 2 routed, 3 sorted, 4 fwd, 5 bwd, 6 reversed
   int64_t n_local = 0, F = 0, P_all = 0, R = 0, D = 0, P = 0, n_lod = 0, n_act = 0;
   int t_begin = 0, t_end = 0, n_passes = 0, fallback = 0;
+  int imp_parity = 0;  // which half of imp_hist the next world-1 importance call uses
   const Rec* recv = nullptr;  // == recs at world 1
   Acc* acc_local = nullptr;   // == acc at world 1
   // arena
@@ -858,21 +859,32 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   a.wbuf = P_<unsigned long long>(ctx->wbuf);
   const int WR = imp_w_rounds(), GR = imp_g_rounds();
   CKS(ensure(ctx, ctx->imp_state, kImpStateBytes));
+  ImpState* st = static_cast<ImpState*>(ctx->imp_state.p);
+  if (ctx->world == 1) {
+    // one cooperative launch; its histogram sets alternate between calls and each call zeroes
+    // the other one, so only a freshly allocated pair is cleared here
+    const size_t set_bytes = size_t(imp_set_words()) * 8;
+    const bool fresh = ctx->imp_hist.cap < 2 * set_bytes;
+    CKS(ensure(ctx, ctx->imp_hist, 2 * set_bytes));
+    if (fresh) CK(cudaMemsetAsync(ctx->imp_hist.p, 0, 2 * set_bytes, s));
+    CKS(ensure(ctx, ctx->cand, size_t(std::max<int64_t>(a.n_items, 1)) * 4));
+    unsigned long long* sets = P_<unsigned long long>(ctx->imp_hist);
+    unsigned long long* cur = sets + (ctx->imp_parity ? imp_set_words() : 0);
+    unsigned long long* nxt = sets + (ctx->imp_parity ? 0 : imp_set_words());
+    ctx->imp_parity ^= 1;
+    CK(launch_imp_coop(a, st, cur, nxt, P_<uint32_t>(ctx->cand), mass_num, mass_den, s));
+    return launched(ctx, 1);
+  }
   CKS(ensure(ctx, ctx->imp_total, 65 * 8));  // total + 64-bin MSB histogram
   CKS(ensure(ctx, ctx->imp_hist, size_t(WR * 512 + GR * 256) * 8));
   CK(cudaMemsetAsync(ctx->imp_state.p, 0, kImpStateBytes, s));
   CK(cudaMemsetAsync(ctx->imp_total.p, 0, 65 * 8, s));
   CK(cudaMemsetAsync(ctx->imp_hist.p, 0, size_t(WR * 512 + GR * 256) * 8, s));
-  ImpState* st = static_cast<ImpState*>(ctx->imp_state.p);
   unsigned long long* total = P_<unsigned long long>(ctx->imp_total);
   unsigned long long* hist = P_<unsigned long long>(ctx->imp_hist);
   int nl = 0;
   launch_fill_bits(cull_out, n_local, s);
   ++nl;
-  if (ctx->world == 1) {
-    CK(launch_imp_coop(a, st, total, hist, mass_num, mass_den, s));
-    return launched(ctx, nl + 1);
-  }
   launch_imp_stats(a, total, s);
   ++nl;
   if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, total, 65, s));
