@@ -146,14 +146,15 @@ struct RasterArgs {
   const uint2* ranges;
   const unsigned long long* keys[2];
   const uint32_t* vals[2];
-  const uint32_t* pass_ctrl;  // final buffer selector at pass_ctrl[kFinalSel]
+  const uint32_t* pass_ctrl;  // value buffer selector at pass_ctrl[kValsSel]
   int t_begin, n_tiles, TX, W, H;
   Acc* acc;
   const float4* aux;          // per received record: thr, box half extents (from k_emit)
   const uint32_t* tile_perm;  // launch order of the owned tiles (longest list first)
   int n_split;                // the first n_split tiles of tile_perm run as two half-tile CTAs
 };
-constexpr int kFinalSel = 15;
+constexpr int kFinalSel = 15;  // buffer holding the sorted keys after the passes
+constexpr int kValsSel = 24;   // buffer holding the final (tie-fixed) values, written by k_ranges_fixup
 void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
                        cudaStream_t s);
 void launch_raster_bwd(const RasterArgs& a, const float* dL, const float* t_final, const int32_t* n_contrib,

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
                                                          float* __restrict__ t_final,
                                                          int32_t* __restrict__ n_contrib) {
   __shared__ WRec s_rec[kWarps][32];
-  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
+  const uint32_t* __restrict__ vals = a.pass_ctrl[kValsSel] ? a.vals[1] : a.vals[0];
   const int warp = threadIdx.x >> 5;
   const int b = blockIdx.x;
   if (b < 2 * a.n_split) {
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterArgs a, const flo
                                                          const float* __restrict__ t_final,
                                                          const int32_t* __restrict__ n_contrib) {
   __shared__ WRec s_rec[kWarps][32];
-  const uint32_t* __restrict__ vals = a.pass_ctrl[kFinalSel] ? a.vals[1] : a.vals[0];
+  const uint32_t* __restrict__ vals = a.pass_ctrl[kValsSel] ? a.vals[1] : a.vals[0];
   const int warp = threadIdx.x >> 5;
   const int b = blockIdx.x;
   if (b < 2 * a.n_split) {

@@ -423,8 +423,10 @@ bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** ptr, int64_t* by
   uint32_t sel = 0;
   if (which == 3 || which == 4) {
     if (ctx->stage < 3) return fail(ctx, BGS_ERR_CONTRACT, "sorted pairs requested before bgs_sort_tiles");
-    // final ping-pong buffer selector lives on the device
-    cudaError_t e = cudaMemcpy(&sel, P_<uint32_t>(ctx->pass_ctrl) + kFinalSel, 4, cudaMemcpyDeviceToHost);
+    // final ping-pong buffer selectors live on the device (keys: after the passes; values:
+    // after the tie fix-up)
+    cudaError_t e = cudaMemcpy(&sel, P_<uint32_t>(ctx->pass_ctrl) + (which == 3 ? kFinalSel : kValsSel), 4,
+                               cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "debug_buffer", cudaGetErrorString(e));
   }
   switch (which) {

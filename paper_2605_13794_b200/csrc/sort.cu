@@ -358,33 +358,36 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
   if (i >= P) return;
   const uint32_t sel = a.pass_ctrl[kFinalSel];
   const uint32_t* keys = reinterpret_cast<const uint32_t*>(sel ? a.keys[1] : a.keys[0]);
-  uint32_t* vals = sel ? a.vals[1] : a.vals[0];
+  const uint32_t* vin = sel ? a.vals[1] : a.vals[0];
+  uint32_t* vout = sel ? a.vals[0] : a.vals[1];
+  if (i == 0) a.pass_ctrl[kValsSel] = sel ^ 1u;
   const int kd = key_layout(a.counters[C_DLO], a.counters[C_DHI], a.tbits).kd;
   const uint32_t k = keys[i];
   const uint32_t t = uint32_t((unsigned long long)k >> kd);
-  const bool first = i == 0 || keys[i - 1] != k;
-  const bool last = i + 1 == P || keys[i + 1] != k;
+  const bool eq_prev = i > 0 && keys[i - 1] == k;
+  const bool eq_next = i + 1 < P && keys[i + 1] == k;
   if ((i == 0 || uint32_t((unsigned long long)keys[i - 1] >> kd) != t)) a.ranges[t].x = uint32_t(i);
   if ((i + 1 == P || uint32_t((unsigned long long)keys[i + 1] >> kd) != t)) a.ranges[t].y = uint32_t(i + 1);
-  if (first && !last) {
-    // run of identical keys starting at i (same tile, same kept depth bits): order it by
-    // (full f32 depth bits, global id) (R12; KeyLayout drops the lowest sd depth bits)
-    int64_t e = i + 1;
-    while (e + 1 < P && keys[e + 1] == k) ++e;
-    for (int64_t x = i + 1; x <= e; ++x) {
-      const uint32_t v = vals[x];
-      const unsigned long long o = ((unsigned long long)__float_as_uint(a.recv[v].depth) << 32) | a.recv[v].gid;
-      int64_t y = x - 1;
-      while (y >= i) {
-        const Rec& ry = a.recv[vals[y]];
-        const unsigned long long oy = ((unsigned long long)__float_as_uint(ry.depth) << 32) | ry.gid;
-        if (oy <= o) break;
-        vals[y + 1] = vals[y];
-        --y;
-      }
-      vals[y + 1] = v;
-    }
+  const uint32_t v = vin[i];
+  if (!eq_prev && !eq_next) {
+    vout[i] = v;
+    return;
   }
+  // member of a run of identical keys (same tile, same kept depth bits; short -- KeyLayout
+  // drops only the lowest sd depth bits): its final slot is the run start plus its rank by
+  // (full f32 depth bits, global id) (R12).  Every member ranks itself; no dependent chains.
+  int64_t s = i, e = i;
+  while (s > 0 && keys[s - 1] == k) --s;
+  while (e + 1 < P && keys[e + 1] == k) ++e;
+  const unsigned long long mine = ((unsigned long long)__float_as_uint(a.recv[v].depth) << 32) | a.recv[v].gid;
+  int64_t rank = 0;
+  for (int64_t j = s; j <= e; ++j) {
+    if (j == i) continue;
+    const Rec& rj = a.recv[vin[j]];
+    const unsigned long long o = ((unsigned long long)__float_as_uint(rj.depth) << 32) | rj.gid;
+    rank += (o < mine || (o == mine && j < i)) ? 1 : 0;
+  }
+  vout[s + rank] = v;
 }
 
 }  // namespace
