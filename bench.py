@@ -276,6 +276,32 @@ def run_native(args):
             e2e_s += time.perf_counter() - t1
     e2e_views = args.steps / D.max_over_ranks(e2e_s, torch.device(dev))
 
+    # ---- scoring views/s: the a12 sweep step = NO_COLOR projection, routing,
+    # sort, instrumented forward, reverse exchange of (w, a), importance; no backward
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with torch.cuda.stream(stream):
+        score_ms = 0.0
+        for k in range(args.warmup + args.steps):
+            v = args.warmup + k
+            cam = cams[v % len(cams)]
+            cull = cull_cols[v % len(cams)] if cull_cols is not None else None
+            if k >= args.warmup:
+                l2_flush.zero_()
+                stream.synchronize()
+                sev[0].record(stream)
+            B.bgs_project(ctx, g, cam, gate, cull, B.BGS_NO_COLOR, radius, stream)
+            B.bgs_route(ctx, None, stream)
+            B.bgs_sort_tiles(ctx, stream)
+            B.bgs_raster_fwd(ctx, B.BGS_IMPORTANCE, rgb, Tf, nc, stream)
+            B.bgs_route_reverse(ctx, stream)
+            B.bgs_importance(ctx, n_local, radius, None, None, s_imp, c_rad, c_vis, cull_out, 99, 100, stream)
+            if k >= args.warmup:
+                sev[1].record(stream)
+                stream.synchronize()
+                score_ms += sev[0].elapsed_time(sev[1])
+    score_ms_max = D.max_over_ranks(score_ms, torch.device(dev)) / args.steps
+    P_max = D.max_over_ranks(P_rank, torch.device(dev))
+
     # ---- roofline of every stage, dominant one reported at top level
     from paper_2605_13794_b200.roofline import load_traffic, stage_rooflines
     peaks = load_peaks()
@@ -297,7 +323,13 @@ def run_native(args):
                    "l2": "flushed between timed views (256 MB write); inputs also exceed L2"},
         "splat_pairs_per_s": round(pairs_per_s, 1),
         "per_view": {"pairs": P_all, "records_F": F_all, "received_R": R_all, "sent_D": D_all,
-                     "active": A_all, "duplication_D_over_F": (D_all / F_all if F_all else None)},
+                     "active": A_all, "duplication_D_over_F": (D_all / F_all if F_all else None),
+                     "E_pixel_entries": round(E_sum / args.steps, 1),
+                     "gate_keep": (float(np.mean([q["n_lod"] for q in qs])) / n_local) if gate_on and n_local else None,
+                     "owned_pairs_max_over_mean": (P_max * world / P_all) if P_all else None},
+        "scoring": {"metric": "scoring views/s (a1-a8 NO_COLOR + a10 + a12, no backward)",
+                    "value": round(1000.0 / score_ms_max, 3) if score_ms_max > 0 else None, "unit": "views/s",
+                    "ms_per_view": round(score_ms_max, 4)},
         "stages_ms": {n: round(float(v), 4) for n, v in zip(stage_names, stage_avg)},
         "roofline": {k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
         "roofline_kernel": dominant["stage"],
