@@ -239,6 +239,51 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
  * perm_out: device u32[n].  Invalidates the ctx's current view.  HOST-SYNC. */
 bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, uint32_t* perm_out, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-1: the scoring report's phi and the scheduled simplification
+ * (readings R30-R33).  s / c_rad / c_vis are the
+ * per-Gaussian outputs accumulated by bgs_importance over a V-view sweep.  Every selection is
+ * GLOBAL over the ranks of the ctx and bit-identical for any M.
+ * --------------------------------------------------------------------------------------- */
+
+/* Output shard of bgs_redistribute: device arrays with room for `capacity` rows each, layouts
+ * as bgs_gaussians (lod nullable). */
+typedef struct {
+  int64_t capacity;
+  float* mean_opac;
+  float* quat;
+  float* scale;
+  float* sh;
+  uint8_t* lod;
+} bgs_gaussians_out;
+
+/* phi_i = c_vis_i / (c_rad_i + 1e-8) (fp64).  c_rad, c_vis: device u32 [n_local];
+ * phi: device f64 [n_local]. */
+bgs_status bgs_score_phi(bgs_ctx* ctx, int64_t n_local, const uint32_t* c_rad, const uint32_t* c_vis, double* phi,
+                         void* stream);
+
+/* Pass 1, stochastic importance-weighted sampling without replacement:
+ * keep_out[i] = 1 for the keep_count Gaussians (counted over ALL ranks) with the largest
+ * exponential-race keys ln(u)/s (u from (seed, global id); s = 0 -> -inf; ties by global id;
+ * R30).  keep_count <= 0 keeps nothing, >= the global population keeps all.  s: device f64
+ * [n_local]; keep_out: device u8 [n_local].  HOST-SYNC. */
+bgs_status bgs_prune_stochastic(bgs_ctx* ctx, int64_t n_local, const double* s, int64_t keep_count, uint64_t seed,
+                                uint8_t* keep_out, void* stream);
+
+/* Pass 2, deterministic cumulative-mass cut: keep the smallest prefix of
+ * (floor(s 2^24) desc, global id asc) whose mass reaches num/den of the global total (R31);
+ * num == den keeps exactly the s > 0 set.  All-zero scores keep only global id 0 and set
+ * *all_zero_out (host, nullable) to 1.  0 < num <= den.  HOST-SYNC. */
+bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s, int32_t num, int32_t den,
+                              uint8_t* keep_out, int32_t* all_zero_out, void* stream);
+
+/* Index-parity redistribution of the survivors (R33): rows with keep[i] != 0 are
+ * renumbered densely in global-id order (new gid), sent to rank new_gid mod M and stored at
+ * local index new_gid div M of `out` (exact copies).  *n_out (host) = this rank's new shard
+ * size; BGS_ERR_CAPACITY when it exceeds out->capacity.  out must not alias in.  HOST-SYNC. */
+bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t* keep, const bgs_gaussians_out* out,
+                            int64_t* n_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

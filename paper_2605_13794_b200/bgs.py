@@ -65,6 +65,11 @@ class bgs_importance_out(C.Structure):
                 ("mass_num", C.c_int32), ("mass_den", C.c_int32)]
 
 
+class bgs_gaussians_out(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("mean_opac", C.c_void_p), ("quat", C.c_void_p), ("scale", C.c_void_p),
+                ("sh", C.c_void_p), ("lod", C.c_void_p)]
+
+
 _vp = C.c_void_p
 _SIGS = {
     "bgs_get_unique_id": [_vp],
@@ -84,6 +89,10 @@ _SIGS = {
     "bgs_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_view_step_host": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_spatial_order": [_vp, _vp, C.c_int64, _vp, _vp],
+    "bgs_score_phi": [_vp, C.c_int64, _vp, _vp, _vp, _vp],
+    "bgs_prune_stochastic": [_vp, C.c_int64, _vp, C.c_int64, C.c_uint64, _vp, _vp],
+    "bgs_prune_mass_cut": [_vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp],
+    "bgs_redistribute": [_vp, _vp, _vp, _vp, _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -355,3 +364,36 @@ def spatial_order(ctx: Context, g: GaussianPlanes) -> torch.Tensor:
 
 def importance_out(s, c_rad, c_vis, cull_out, num=99, den=100) -> bgs_importance_out:
     return bgs_importance_out(s.data_ptr(), c_rad.data_ptr(), c_vis.data_ptr(), cull_out.data_ptr(), num, den)
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT-1: scoring report phi, scheduled simplification, index-parity redistribution
+# ------------------------------------------------------------------------------------------
+def bgs_score_phi(ctx: Context, n_local: int, c_rad, c_vis, phi, stream=None):
+    ctx.check(_lib.bgs_score_phi(ctx.handle, int(n_local), _ptr(c_rad), _ptr(c_vis), _ptr(phi), _stream(stream)),
+              "bgs_score_phi")
+
+
+def bgs_prune_stochastic(ctx: Context, n_local: int, s, keep_count: int, seed: int, keep_out, stream=None):
+    ctx.check(_lib.bgs_prune_stochastic(ctx.handle, int(n_local), _ptr(s), int(keep_count), int(seed) & (2**64 - 1),
+                                        _ptr(keep_out), _stream(stream)), "bgs_prune_stochastic")
+
+
+def bgs_prune_mass_cut(ctx: Context, n_local: int, s, num: int, den: int, keep_out, stream=None) -> bool:
+    """Returns the all-zero warning flag."""
+    flag = C.c_int32(0)
+    ctx.check(_lib.bgs_prune_mass_cut(ctx.handle, int(n_local), _ptr(s), int(num), int(den), _ptr(keep_out),
+                                      C.byref(flag), _stream(stream)), "bgs_prune_mass_cut")
+    return bool(flag.value)
+
+
+def bgs_redistribute(ctx: Context, g: GaussianPlanes, keep, out: GaussianPlanes, stream=None) -> int:
+    """Survivors of `g` (keep != 0) renumbered and re-sharded into `out` (capacity = out.n rows);
+    returns this rank's new shard size."""
+    gs = g.struct()
+    o = bgs_gaussians_out(out.n, out.mean_opac.data_ptr(), out.quat.data_ptr(), out.scale.data_ptr(),
+                          out.sh.data_ptr(), out.lod.data_ptr() if out.lod is not None else None)
+    n_out = C.c_int64(0)
+    ctx.check(_lib.bgs_redistribute(ctx.handle, C.byref(gs), _ptr(keep), C.byref(o), C.byref(n_out),
+                                    _stream(stream)), "bgs_redistribute")
+    return int(n_out.value)

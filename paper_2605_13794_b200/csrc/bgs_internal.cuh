@@ -234,4 +234,35 @@ int64_t imp_set_words();
 cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* set,
                             unsigned long long* next, uint32_t* cand, int num, int den, cudaStream_t s);
 
+// NEXT-1 simplification (simplify.cu)
+void launch_phi(int64_t n, const uint32_t* c_rad, const uint32_t* c_vis, double* phi, cudaStream_t s);
+void launch_keys_race(int64_t n, const double* sc, unsigned long long seed, int rank, int world,
+                      unsigned long long* key, cudaStream_t s);
+void launch_keys_mass(int64_t n, const double* sc, unsigned long long* key, cudaStream_t s);
+size_t sel_state_bytes();
+int sel_rounds();
+int sel_gid_rounds();
+void launch_sel_total(int64_t n, const unsigned long long* key, int mass, unsigned long long* total, cudaStream_t s);
+void launch_sel_hist(int64_t n, const unsigned long long* key, const void* st, int round, unsigned long long* hist,
+                     cudaStream_t s);
+void launch_sel_decide(void* st, const unsigned long long* total, int round, const unsigned long long* hist, int mass,
+                       long long num, long long den, unsigned long long k, cudaStream_t s);
+void launch_sel_gid_hist(int64_t n, const unsigned long long* key, const void* st, int round, int rank, int world,
+                         unsigned long long* hist, cudaStream_t s);
+void launch_sel_gid_decide(void* st, int round, const unsigned long long* hist, cudaStream_t s);
+void launch_sel_mark(int64_t n, const unsigned long long* key, const void* st, int rank, int world, uint8_t* keep,
+                     cudaStream_t s);
+void launch_keep_positive(int64_t n, const double* sc, uint8_t* keep, unsigned long long* count, cudaStream_t s);
+void launch_fill_u8(int64_t n, uint8_t* p, uint8_t v, cudaStream_t s);
+size_t param_row_bytes();
+void launch_pack_bits(int64_t n, const uint8_t* keep, uint32_t* bits, cudaStream_t s);
+void launch_new_ids(int64_t N, const uint32_t* masks, int64_t wpr, int world, int rank, uint32_t* bc,
+                    unsigned long long* total, int64_t n_local, uint32_t* new_gid, cudaStream_t s);
+void launch_dest_hist(int64_t n, const uint32_t* new_gid, int world, unsigned long long* cnt, cudaStream_t s);
+void launch_pack_rows(int64_t n, const uint32_t* new_gid, int world, const int64_t* dest_base,
+                      unsigned long long* cursor, const bgs_gaussians& g, void* out, cudaStream_t s);
+void launch_scatter_direct(int64_t n, const uint32_t* new_gid, const bgs_gaussians& g, const bgs_gaussians_out& o,
+                           int64_t cap, cudaStream_t s);
+void launch_unpack_rows(int64_t n, const void* in, const bgs_gaussians_out& o, int64_t cap, cudaStream_t s);
+
 }  // namespace bgs

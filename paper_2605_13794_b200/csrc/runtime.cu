@@ -48,6 +48,8 @@ struct bgs_ctx {
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
       imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf;
+  // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
+  DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
   int64_t* h_misc = nullptr;                 // pinned scratch for routing sizes
   cudaEvent_t ev_counters = nullptr;         // counters copied to the host (bgs_project)
@@ -392,7 +394,9 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf};
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf,
+                    &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
+                    &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -984,6 +988,227 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
   CKS(bgs_view_step(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
                     P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), P_<float>(ctx->scr_dl), grads, imp, stream));
   CK(cudaMemcpyAsync(rgb_host, ctx->scr_rgb.p, npix * 12, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return BGS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// NEXT-1: phi, scheduled simplification passes, index-parity redistribution (simplify.cu)
+// ---------------------------------------------------------------------------------------
+namespace {
+
+// sum of n host values over the ranks (small scratch in dcnt[0, 8)); synchronises the stream
+bgs_status sum_over_ranks(bgs_ctx* ctx, unsigned long long* vals, int n, cudaStream_t s) {
+  if (ctx->world == 1) return BGS_OK;
+  CKS(ensure(ctx, ctx->dcnt, 64 * 8));
+  unsigned long long* d = P_<unsigned long long>(ctx->dcnt);
+  CK(cudaMemcpyAsync(d, vals, size_t(n) * 8, cudaMemcpyHostToDevice, s));
+  CKS(ctx->tr->allreduce_u64(ctx, d, n, s));
+  CK(cudaMemcpyAsync(vals, d, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return BGS_OK;
+}
+
+// keep = top of (key desc, global id asc) over all ranks: the first k items (count mode) or the
+// smallest prefix with den * mass >= num * total (mass mode)
+bgs_status run_select(bgs_ctx* ctx, int64_t n, const unsigned long long* key, int mass, long long num, long long den,
+                      unsigned long long k, uint8_t* keep, cudaStream_t s) {
+  const int R = sel_rounds(), GR = sel_gid_rounds();
+  const size_t hw = size_t(R) * 512 + size_t(GR) * 256 + 8;
+  CKS(ensure(ctx, ctx->sel_state, sel_state_bytes()));
+  CKS(ensure(ctx, ctx->sel_hist, hw * 8));
+  CK(cudaMemsetAsync(ctx->sel_state.p, 0, sel_state_bytes(), s));
+  CK(cudaMemsetAsync(ctx->sel_hist.p, 0, hw * 8, s));
+  unsigned long long* hist = P_<unsigned long long>(ctx->sel_hist);
+  unsigned long long* total = hist + size_t(R) * 512 + size_t(GR) * 256;
+  void* st = ctx->sel_state.p;
+  int nl = 0;
+  launch_sel_total(n, key, mass, total, s);
+  ++nl;
+  if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, total, 1, s));
+  for (int r = 0; r < R; ++r) {
+    launch_sel_hist(n, key, st, r, hist + r * 512, s);
+    if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, hist + r * 512, 512, s));
+    launch_sel_decide(st, total, r, hist + r * 512, mass, num, den, k, s);
+    nl += 2;
+  }
+  for (int r = 0; r < GR; ++r) {
+    unsigned long long* h = hist + size_t(R) * 512 + size_t(r) * 256;
+    launch_sel_gid_hist(n, key, st, r, ctx->rank, ctx->world, h, s);
+    if (ctx->world > 1) CKS(ctx->tr->allreduce_u64(ctx, h, 256, s));
+    launch_sel_gid_decide(st, r, h, s);
+    nl += 2;
+  }
+  launch_sel_mark(n, key, st, ctx->rank, ctx->world, keep, s);
+  return launched(ctx, nl + 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+bgs_status bgs_score_phi(bgs_ctx* ctx, int64_t n_local, const uint32_t* c_rad, const uint32_t* c_vis, double* phi,
+                         void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (n_local < 0 || (n_local > 0 && (!c_rad || !c_vis || !phi)))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_score_phi: arguments");
+  launch_phi(n_local, c_rad, c_vis, phi, static_cast<cudaStream_t>(stream));
+  return n_local > 0 ? launched(ctx) : BGS_OK;
+}
+
+bgs_status bgs_prune_stochastic(bgs_ctx* ctx, int64_t n_local, const double* s_score, int64_t keep_count,
+                                uint64_t seed, uint8_t* keep_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (n_local < 0 || (n_local > 0 && (!s_score || !keep_out)))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_prune_stochastic: arguments");
+  if (n_local >= (int64_t(1) << 32) / ctx->world) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "global ids exceed 32 bits");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long N = (unsigned long long)n_local;
+  CKS(sum_over_ranks(ctx, &N, 1, s));
+  if (keep_count <= 0 || (unsigned long long)keep_count >= N) {
+    launch_fill_u8(n_local, keep_out, keep_count <= 0 ? 0 : 1, s);
+    CKS(n_local > 0 ? launched(ctx) : BGS_OK);
+    CK(cudaStreamSynchronize(s));
+    return BGS_OK;
+  }
+  CKS(ensure(ctx, ctx->sel_keys, size_t(std::max<int64_t>(n_local, 1)) * 8));
+  unsigned long long* key = P_<unsigned long long>(ctx->sel_keys);
+  launch_keys_race(n_local, s_score, (unsigned long long)seed, ctx->rank, ctx->world, key, s);
+  CKS(n_local > 0 ? launched(ctx) : BGS_OK);
+  CKS(run_select(ctx, n_local, key, 0, 0, 1, (unsigned long long)keep_count, keep_out, s));
+  CK(cudaStreamSynchronize(s));
+  return BGS_OK;
+}
+
+bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s_score, int32_t num, int32_t den,
+                              uint8_t* keep_out, int32_t* all_zero_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (n_local < 0 || (n_local > 0 && (!s_score || !keep_out)))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_prune_mass_cut: arguments");
+  if (den <= 0 || num <= 0 || num > den) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "mass cut needs 0 < num <= den");
+  if (n_local >= (int64_t(1) << 32) / ctx->world) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "global ids exceed 32 bits");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (all_zero_out) *all_zero_out = 0;
+  CKS(ensure(ctx, ctx->sel_keys, size_t(std::max<int64_t>(n_local, 1)) * 8));
+  CKS(ensure(ctx, ctx->dcnt, 64 * 8));
+  unsigned long long* key = P_<unsigned long long>(ctx->sel_keys);
+  unsigned long long* cnt = P_<unsigned long long>(ctx->dcnt) + 8;  // [0] positive count, [1] total mass
+  CK(cudaMemsetAsync(cnt, 0, 16, s));
+  launch_keys_mass(n_local, s_score, key, s);
+  launch_keep_positive(n_local, s_score, keep_out, cnt, s);  // keep = (s > 0): the num == den answer
+  launch_sel_total(n_local, key, 1, cnt + 1, s);
+  CKS(n_local > 0 ? launched(ctx, 3) : BGS_OK);
+  unsigned long long h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CKS(sum_over_ranks(ctx, h, 2, s));
+  if (num == den && h[0] > 0) return BGS_OK;  // every s > 0 is kept
+  if (h[1] == 0) {
+    // all-zero scores: only the forced first element (global id 0 = local 0 of rank 0)
+    launch_fill_u8(n_local, keep_out, 0, s);
+    CKS(n_local > 0 ? launched(ctx) : BGS_OK);
+    if (ctx->rank == 0 && n_local > 0) CK(cudaMemsetAsync(keep_out, 1, 1, s));
+    if (all_zero_out) *all_zero_out = 1;
+    CK(cudaStreamSynchronize(s));
+    return BGS_OK;
+  }
+  CKS(run_select(ctx, n_local, key, 1, num, den, 0, keep_out, s));
+  CK(cudaStreamSynchronize(s));
+  return BGS_OK;
+}
+
+bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t* keep, const bgs_gaussians_out* out,
+                            int64_t* n_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (!in || !out || !n_out || in->n_local < 0 || (in->n_local > 0 && (!keep || !in->mean_opac || !in->quat ||
+                                                                     !in->scale || !in->sh)))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_redistribute: arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int M = ctx->world, rank = ctx->rank;
+  const int64_t n = in->n_local;
+  unsigned long long Nv = (unsigned long long)n;
+  CKS(sum_over_ranks(ctx, &Nv, 1, s));
+  const int64_t N = int64_t(Nv);
+  if (n != (N - rank + M - 1) / M)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_redistribute: shard is not the index-parity slice (S:166)");
+  const int64_t wpr = ((N + M - 1) / M + 31) / 32;  // mask words per rank
+  CKS(ensure(ctx, ctx->masks, size_t(std::max<int64_t>((M + 1) * wpr, 1)) * 4));
+  uint32_t* masks = P_<uint32_t>(ctx->masks);
+  CK(cudaMemsetAsync(masks, 0, size_t((M + 1) * wpr) * 4, s));
+  int nl = 0;
+  if (M == 1) {
+    launch_pack_bits(n, keep, masks, s);
+    nl += n > 0;
+  } else {
+    // allgather of the keep masks: own bits in slot M, gathered into slots [0, M)
+    launch_pack_bits(n, keep, masks + size_t(M) * wpr, s);
+    nl += n > 0;
+    std::vector<int64_t> scnt(M, wpr), soff(M, 0), rcnt(M, wpr), roff(M);
+    for (int d = 0; d < M; ++d) roff[d] = d * wpr;
+    CKS(ctx->tr->alltoallv(ctx, masks + size_t(M) * wpr, scnt.data(), soff.data(), masks, rcnt.data(), roff.data(), 4,
+                           s));
+  }
+  const int64_t nb = std::max<int64_t>(1, (N + 255) / 256);
+  CKS(ensure(ctx, ctx->sblocks, size_t(nb) * 4));
+  CKS(ensure(ctx, ctx->new_gid, size_t(std::max<int64_t>(n, 1)) * 4));
+  CKS(ensure(ctx, ctx->dcnt, 64 * 8));
+  unsigned long long* dc = P_<unsigned long long>(ctx->dcnt);
+  CK(cudaMemsetAsync(dc + 16, 0, 48 * 8, s));
+  uint32_t* new_gid = P_<uint32_t>(ctx->new_gid);
+  launch_new_ids(N, masks, wpr, M, rank, P_<uint32_t>(ctx->sblocks), dc + 16, n, new_gid, s);
+  nl += N > 0 ? 3 : 0;
+  unsigned long long kept = 0;
+  CK(cudaMemcpyAsync(&kept, dc + 16, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t nk = int64_t(kept);
+  const int64_t mine = nk > rank ? (nk - rank + M - 1) / M : 0;
+  *n_out = mine;
+  if (mine > out->capacity) return fail(ctx, BGS_ERR_CAPACITY, "bgs_redistribute: new shard exceeds out->capacity");
+  if (mine > 0 && (!out->mean_opac || !out->quat || !out->scale || !out->sh))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_redistribute: output arrays");
+  if (M == 1) {
+    launch_scatter_direct(n, new_gid, *in, *out, out->capacity, s);
+    CKS(launched(ctx, nl + (n > 0)));
+    CK(cudaStreamSynchronize(s));
+    return BGS_OK;
+  }
+  // per-destination counts -> exchange -> pack 256-B rows -> one all-to-all -> scatter
+  unsigned long long* scnt_d = dc + 24;
+  int64_t* rcnt_d = reinterpret_cast<int64_t*>(dc + 32);
+  int64_t* base_d = reinterpret_cast<int64_t*>(dc + 40);
+  unsigned long long* cursor = dc + 48;
+  launch_dest_hist(n, new_gid, M, scnt_d, s);
+  nl += n > 0;
+  CKS(ctx->tr->alltoall1(ctx, reinterpret_cast<const int64_t*>(scnt_d), rcnt_d, s));
+  std::vector<int64_t> scnt(M), rcnt(M), soff(M), roff(M);
+  CK(cudaMemcpyAsync(scnt.data(), scnt_d, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(rcnt.data(), rcnt_d, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int64_t D = 0, R = 0;
+  for (int d = 0; d < M; ++d) {
+    soff[d] = D;
+    roff[d] = R;
+    D += scnt[d];
+    R += rcnt[d];
+  }
+  if (R != mine) return fail(ctx, BGS_ERR_INTERNAL, "bgs_redistribute: received rows != new shard size");
+  const size_t row = param_row_bytes();
+  CKS(ensure(ctx, ctx->rows_send, size_t(std::max<int64_t>(D, 1)) * row));
+  CKS(ensure(ctx, ctx->rows_recv, size_t(std::max<int64_t>(R, 1)) * row));
+  CK(cudaMemcpyAsync(base_d, soff.data(), size_t(M) * 8, cudaMemcpyHostToDevice, s));
+  launch_pack_rows(n, new_gid, M, base_d, cursor, *in, ctx->rows_send.p, s);
+  nl += n > 0;
+  CKS(ctx->tr->alltoallv(ctx, ctx->rows_send.p, scnt.data(), soff.data(), ctx->rows_recv.p, rcnt.data(), roff.data(),
+                         row, s));
+  launch_unpack_rows(R, ctx->rows_recv.p, *out, out->capacity, s);
+  nl += R > 0;
+  CKS(launched(ctx, nl));
   CK(cudaStreamSynchronize(s));
   return BGS_OK;
 }
