@@ -302,6 +302,39 @@ def run_native(args):
     score_ms_max = D.max_over_ranks(score_ms, torch.device(dev)) / args.steps
     P_max = D.max_over_ranks(P_rank, torch.device(dev))
 
+    # ---- NEXT-1 scheduled simplification on the same shard, with the s / c_rad / c_vis the
+    # timed views accumulated (one pass each; HOST-SYNC calls, wall time between barriers)
+    simplify = {}
+    with torch.cuda.stream(stream):
+        phi = torch.empty(max(n_local, 1), dtype=torch.float64, device=dev)
+        keep = torch.empty(max(n_local, 1), dtype=torch.uint8, device=dev)
+        cap = (n_local + 1)
+        out_g = B.GaussianPlanes(torch.empty(cap, 4, device=dev), torch.empty(cap, 4, device=dev),
+                                 torch.empty(cap, 4, device=dev), torch.empty(cap, 48, device=dev),
+                                 torch.empty(cap, dtype=torch.uint8, device=dev))
+        N_glob = int(N_all)
+
+        def timed(fn):
+            fn()  # warm-up: first calls grow the ctx arena (cudaMalloc)
+            stream.synchronize()
+            barrier()
+            t1 = time.perf_counter()
+            r = fn()
+            stream.synchronize()
+            return r, D.max_over_ranks((time.perf_counter() - t1) * 1e3, torch.device(dev))
+
+        _, simplify["phi_ms"] = timed(lambda: B.bgs_score_phi(ctx, n_local, c_rad, c_vis, phi, stream))
+        _, simplify["pass1_stochastic_ms"] = timed(
+            lambda: B.bgs_prune_stochastic(ctx, n_local, s_imp, int(round(0.6 * N_glob)), 1234, keep, stream))
+        n_keep1 = D.sum_over_ranks([float(keep[:n_local].sum().item())], torch.device(dev))[0]
+        _, simplify["pass2_mass_cut_ms"] = timed(lambda: B.bgs_prune_mass_cut(ctx, n_local, s_imp, 99, 100, keep,
+                                                                              stream))
+        n_keep2 = D.sum_over_ranks([float(keep[:n_local].sum().item())], torch.device(dev))[0]
+        n_new, simplify["redistribute_ms"] = timed(lambda: B.bgs_redistribute(ctx, g, keep, out_g, stream))
+        simplify.update({"gaussians": N_glob, "kept_pass1": int(n_keep1), "kept_pass2": int(n_keep2),
+                         "note": "keep_fraction 0.6 (S:318 default), target 99/100; scores from the timed views"})
+        del out_g
+
     # ---- roofline of every stage, dominant one reported at top level
     from paper_2605_13794_b200.roofline import load_traffic, stage_rooflines
     peaks = load_peaks()
@@ -330,6 +363,7 @@ def run_native(args):
         "scoring": {"metric": "scoring views/s (a1-a8 NO_COLOR + a10 + a12, no backward)",
                     "value": round(1000.0 / score_ms_max, 3) if score_ms_max > 0 else None, "unit": "views/s",
                     "ms_per_view": round(score_ms_max, 4)},
+        "simplify": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in simplify.items()},
         "stages_ms": {n: round(float(v), 4) for n, v in zip(stage_names, stage_avg)},
         "roofline": {k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
         "roofline_kernel": dominant["stage"],

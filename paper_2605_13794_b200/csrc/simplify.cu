@@ -22,6 +22,10 @@ namespace {
 constexpr double kLn2 = 0.6931471805599453;
 constexpr double kSqrt2 = 1.4142135623730951;
 constexpr int kSeries = 12;
+// 1/(2k+1) as correctly rounded doubles: compile-time IEEE division gives the same bits as the
+// oracle's runtime np.float64(1.0) / np.float64(2k+1)
+__constant__ double kInvOdd[kSeries] = {1.0 / 1,  1.0 / 3,  1.0 / 5,  1.0 / 7,  1.0 / 9,  1.0 / 11,
+                                        1.0 / 13, 1.0 / 15, 1.0 / 17, 1.0 / 19, 1.0 / 21, 1.0 / 23};
 
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   unsigned long long z = x + 0x9E3779B97F4A7C15ull;
@@ -46,9 +50,9 @@ __device__ double ln_pinned(double u) {
   }
   const double f = __ddiv_rn(__dadd_rn(m, -1.0), __dadd_rn(m, 1.0));
   const double f2 = __dmul_rn(f, f);
-  double p = __ddiv_rn(1.0, double(2 * (kSeries - 1) + 1));
+  double p = kInvOdd[kSeries - 1];
 #pragma unroll
-  for (int k = kSeries - 2; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, f2), __ddiv_rn(1.0, double(2 * k + 1)));
+  for (int k = kSeries - 2; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, f2), kInvOdd[k]);
   const double lm = __dmul_rn(__dadd_rn(f, f), p);
   return __dadd_rn(__dmul_rn(double(e), kLn2), lm);
 }
@@ -116,12 +120,22 @@ __global__ void __launch_bounds__(256) k_sel_hist(int64_t n, const unsigned long
   __syncthreads();
   const int shift = 8 * (kSelRounds - 1 - round);
   const unsigned long long prefix = st->prefix;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const unsigned long long k = key[i];
-    if (shift + 8 < 64 && (k >> (shift + 8)) != prefix) continue;
-    const uint32_t d = uint32_t((k >> shift) & 255u);
-    atomicAdd(&s_cnt[d], 1ull);
-    atomicAdd(&s_mass[d], k);
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count; lanes sharing a digit are reduced in-warp first (early rounds put
+  // almost every item in one bin, which serialised per-lane shared atomics)
+  for (int64_t b = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); b < n; b += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = b + lane;
+    const unsigned long long k = i < n ? key[i] : 0ull;
+    const bool cand = i < n && !(shift + 8 < 64 && (k >> (shift + 8)) != prefix);
+    const uint32_t d = cand ? uint32_t((k >> shift) & 255u) : 256u + lane;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const uint32_t lo = uint32_t(k & 0xffffffu), mid = uint32_t((k >> 24) & 0xffffffu), hi = uint32_t(k >> 48);
+    const uint32_t slo = __reduce_add_sync(peers, lo), smid = __reduce_add_sync(peers, mid),
+                   shi = __reduce_add_sync(peers, hi);
+    if (cand && lane == __ffs(peers) - 1) {
+      atomicAdd(&s_cnt[d], (unsigned long long)__popc(peers));
+      atomicAdd(&s_mass[d], (unsigned long long)slo + ((unsigned long long)smid << 24) + ((unsigned long long)shi << 48));
+    }
   }
   __syncthreads();
   if (s_cnt[threadIdx.x]) {
