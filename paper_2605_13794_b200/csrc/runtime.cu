@@ -53,6 +53,8 @@ struct bgs_ctx {
   unsigned long long* h_counters = nullptr;  // pinned
   int64_t* h_misc = nullptr;                 // pinned scratch for routing sizes
   cudaEvent_t ev_counters = nullptr;         // counters copied to the host (bgs_project)
+  cudaEvent_t ev_geom = nullptr;             // geometry kernels done (bgs_project)
+  cudaStream_t side = nullptr;               // carries the counters copy off the working stream
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
 };
 
@@ -402,6 +404,8 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
   if (c->h_counters) cudaFreeHost(c->h_counters);
   if (c->h_misc) cudaFreeHost(c->h_misc);
   if (c->ev_counters) cudaEventDestroy(c->ev_counters);
+  if (c->ev_geom) cudaEventDestroy(c->ev_geom);
+  if (c->side) cudaStreamDestroy(c->side);
   c->tr.reset();
   delete c;
   return BGS_OK;
@@ -532,13 +536,18 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
     launch_project(a, s);
     CKS(launched(ctx, 2));
   }
-  // The counters (F, P_all, ...) are final once the geometry kernels are done: copy them out
-  // and wait on that copy only, while the colour kernel keeps the device busy during the host
-  // round trip (the one host synchronisation of a world-1 step).
-  CK(cudaMemcpyAsync(ctx->h_counters, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
-                     cudaMemcpyDeviceToHost, s));
+  // The counters (F, P_all, ...) are final once the geometry kernels are done: copy them out on a
+  // side stream and wait on that copy only, while the colour kernel (next on the working stream,
+  // not queued behind the copy) keeps the device busy during the host round trip (the one host
+  // synchronisation of a world-1 step).
   if (!ctx->ev_counters) CK(cudaEventCreateWithFlags(&ctx->ev_counters, cudaEventDisableTiming));
-  CK(cudaEventRecord(ctx->ev_counters, s));
+  if (!ctx->ev_geom) CK(cudaEventCreateWithFlags(&ctx->ev_geom, cudaEventDisableTiming));
+  if (!ctx->side) CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CK(cudaEventRecord(ctx->ev_geom, s));
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_geom, 0));
+  CK(cudaMemcpyAsync(ctx->h_counters, ctx->counters.p, sizeof(unsigned long long) * C_NCOUNTERS,
+                     cudaMemcpyDeviceToHost, ctx->side));
+  CK(cudaEventRecord(ctx->ev_counters, ctx->side));
   if (a.n > 0 && !a.no_color) {
     launch_color(a, s);
     CKS(launched(ctx));
