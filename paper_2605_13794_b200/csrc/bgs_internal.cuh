@@ -231,6 +231,7 @@ void launch_fill_bits(uint32_t* words, int64_t n_bits, cudaStream_t s);
 // histograms, candidate count; imp_set_words() u64) must be zero on entry; the kernel zeroes
 // `next` (same size) for the following call.  cand: u32 scratch [n_items].
 int64_t imp_set_words();
+int64_t imp_cand_words(int64_t n_items);  // u32 scratch the cooperative kernel's candidate segments need
 cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* set,
                             unsigned long long* next, uint32_t* cand, int num, int den, cudaStream_t s);
 

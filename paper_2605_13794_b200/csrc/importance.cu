@@ -41,6 +41,7 @@ struct alignas(16) ImpState {
   uint32_t need_gid;             // 0 < k < ntie
   uint32_t empty;                // total == 0
   uint32_t r0;                   // first w round with a non-zero digit (from the MSB histogram)
+  unsigned long long next_cnt;   // items in the crossing bin of the last round (next round's candidates)
   uint32_t tshift;               // selection: (w >> tshift) >= prefix (0 after all rounds)
   uint32_t final_;               // threshold resolved (crossing bin holds one item): no more rounds
   uint32_t pad1;
@@ -136,55 +137,79 @@ __device__ void stats_body(const ImportanceArgs& a, unsigned long long* total) {
   __syncthreads();
 }
 
-// candidates of round r: w > 0 and w >> (shift + 8) == prefix.  Items are t in [0, n) or
-// list[t] when list != null; when out != null the candidates are also appended to out
-// (one atomic per warp on *out_count): later rounds scan only them.
+// Per-warp candidate segments (world-1 cooperative kernel): warp gw (global warp id) owns
+// cand[gw * cap, gw * cap + cnt[gw]), filled by one full scan and rescanned by later rounds, so
+// no atomics and no cross-warp order are involved.
+struct Seg {
+  uint32_t* cand;
+  uint32_t* cnt;
+  int64_t cap;
+};
+
+// one warp's candidates into the CTA histogram (warp-aggregated shared-memory atomics: the early
+// rounds put almost every candidate in one bin, which serialised per-lane 64-bit atomics)
+__device__ __forceinline__ void hist_add(bool cand, uint32_t d, unsigned long long w, int lane,
+                                         unsigned long long* s_cnt, unsigned long long* s_mass) {
+  const unsigned peers = __match_any_sync(0xffffffffu, d);
+  const bool single = peers == (1u << lane);
+  if (cand && single) {
+    atomicAdd(&s_cnt[d], 1ull);
+    atomicAdd(&s_mass[d], w);
+  }
+  // groups of lanes sharing a digit: reduce in-warp first (redux.sync runs once per group)
+  const bool multi = cand && !single;
+  if (__any_sync(0xffffffffu, multi) && multi) {
+    const uint32_t lo = uint32_t(w & 0xffffffu), mid = uint32_t((w >> 24) & 0xffffffu), hi = uint32_t(w >> 48);
+    const uint32_t slo = __reduce_add_sync(peers, lo);
+    const uint32_t smid = __reduce_add_sync(peers, mid);
+    const uint32_t shi = __reduce_add_sync(peers, hi);
+    if (lane == __ffs(peers) - 1) {
+      atomicAdd(&s_cnt[d], (unsigned long long)__popc(peers));
+      atomicAdd(&s_mass[d], (unsigned long long)slo + ((unsigned long long)smid << 24) + ((unsigned long long)shi << 48));
+    }
+  }
+}
+
+// candidates of round r: w > 0 and w >> (shift + 8) == prefix.  seg_mode 0: scan every item;
+// 1: scan every item and append the candidates to this warp's segment; 2: scan the segment only
+// (a superset of this round's candidates: they matched every earlier prefix).
 __device__ void hist_body(const ImportanceArgs& a, unsigned long long prefix, int round,
-                          unsigned long long* hist /*[256] count, [256] mass*/, const uint32_t* list = nullptr,
-                          int64_t n = -1, uint32_t* out = nullptr, unsigned long long* out_count = nullptr) {
+                          unsigned long long* hist /*[256] count, [256] mass*/, int seg_mode = 0, Seg seg = {}) {
   __shared__ unsigned long long s_cnt[256], s_mass[256];
   s_cnt[threadIdx.x] = 0;
   s_mass[threadIdx.x] = 0;
   __syncthreads();
-  if (n < 0) n = a.n_items;
+  const int64_t n = a.n_items;
   const int shift = 8 * (kWRounds - 1 - round);
   const int lane = threadIdx.x & 31;
-  // warp-uniform trip count so every lane reaches the warp collectives
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
-    const int64_t t = base + lane;
-    const int64_t item = t < n ? (list ? int64_t(list[t]) : t) : 0;
-    const unsigned long long w = t < n ? load_w(a, item) : 0ull;
-    const bool cand = w != 0 && !(shift + 8 < 64 && (w >> (shift + 8)) != prefix);
-    if (out) {
-      const unsigned cm = __ballot_sync(0xffffffffu, cand);
-      unsigned long long ob = 0;
-      if (lane == 0 && cm) ob = atomicAdd(out_count, (unsigned long long)__popc(cm));
-      ob = __shfl_sync(0xffffffffu, ob, 0);
-      if (cand) out[ob + __popc(cm & ((1u << lane) - 1u))] = uint32_t(item);
+  const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  auto is_cand = [&](unsigned long long w) { return w != 0 && !(shift + 8 < 64 && (w >> (shift + 8)) != prefix); };
+  if (seg_mode == 2) {
+    const uint32_t cnt = seg.cnt[gw];
+    const uint32_t* L = seg.cand + gw * seg.cap;
+    for (uint32_t b = 0; b < cnt; b += 32) {
+      const uint32_t j = b + lane;
+      const unsigned long long w = j < cnt ? load_w(a, L[j]) : 0ull;
+      const bool cand = j < cnt && is_cand(w);
+      hist_add(cand, cand ? uint32_t((w >> shift) & 255u) : 256u + lane, w, lane, s_cnt, s_mass);
     }
-    const uint32_t d = cand ? uint32_t((w >> shift) & 255u) : 256u + lane;
-    // one shared-memory atomic per distinct digit of the warp: the early rounds put almost
-    // every candidate in one bin, which serialised per-lane 64-bit atomics
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const bool single = peers == (1u << lane);
-    if (cand && single) {
-      atomicAdd(&s_cnt[d], 1ull);
-      atomicAdd(&s_mass[d], w);
-    }
-    // groups of lanes sharing a digit: reduce in-warp first (redux.sync runs once per group)
-    const bool multi = cand && !single;
-    if (__any_sync(0xffffffffu, multi) && multi) {
-      const uint32_t lo = uint32_t(w & 0xffffffu), mid = uint32_t((w >> 24) & 0xffffffu), hi = uint32_t(w >> 48);
-      const uint32_t slo = __reduce_add_sync(peers, lo);
-      const uint32_t smid = __reduce_add_sync(peers, mid);
-      const uint32_t shi = __reduce_add_sync(peers, hi);
-      if (lane == __ffs(peers) - 1) {
-        atomicAdd(&s_cnt[d], (unsigned long long)__popc(peers));
-        atomicAdd(&s_mass[d], (unsigned long long)slo + ((unsigned long long)smid << 24) +
-                                  ((unsigned long long)shi << 48));
+  } else {
+    uint32_t appended = 0;
+    uint32_t* L = seg_mode == 1 ? seg.cand + gw * seg.cap : nullptr;
+    // warp-uniform trip count so every lane reaches the warp collectives
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+      const int64_t t = base + lane;
+      const unsigned long long w = t < n ? load_w(a, t) : 0ull;
+      const bool cand = t < n && is_cand(w);
+      if (seg_mode == 1) {
+        const unsigned cm = __ballot_sync(0xffffffffu, cand);
+        if (cand) L[appended + __popc(cm & ((1u << lane) - 1u))] = uint32_t(t);
+        appended += __popc(cm);
       }
+      hist_add(cand, cand ? uint32_t((w >> shift) & 255u) : 256u + lane, w, lane, s_cnt, s_mass);
     }
+    if (seg_mode == 1 && lane == 0) seg.cnt[gw] = appended;
   }
   __syncthreads();
   if (s_cnt[threadIdx.x]) {
@@ -241,6 +266,7 @@ __device__ void decide_body(ImpState* st, int round, const unsigned long long* h
       st->above = above + (pick < 255 ? s_suf[254 - pick] : 0ull);
       st->prefix = (st->prefix << 8) | unsigned(pick);
       st->tshift = uint32_t(8 * (kWRounds - 1 - round));
+      st->next_cnt = hist[pick];
       if (round < kWRounds - 1 && hist[pick] == 1) {
         // the crossing bin holds one item: it is the threshold item (k = ntie = 1) and the
         // selection is exactly {w : (w >> tshift) >= prefix}; the remaining rounds are skipped
@@ -268,20 +294,28 @@ __device__ void decide_body(ImpState* st, int round, const unsigned long long* h
   __syncthreads();
 }
 
+// seg != null: scan this warp's candidate segment only (every tie w == tau is in it)
 __device__ void gid_hist_body(const ImportanceArgs& a, unsigned long long tau, uint32_t gp, int round,
-                              unsigned long long* hist /*[256] counts*/, const uint32_t* list = nullptr,
-                              int64_t n = -1) {
+                              unsigned long long* hist /*[256] counts*/, const Seg* seg = nullptr) {
   __shared__ unsigned long long s_cnt[256];
   s_cnt[threadIdx.x] = 0;
   __syncthreads();
-  if (n < 0) n = a.n_items;
   const int shift = 8 * (kGRounds - 1 - round);
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t t = list ? int64_t(list[i]) : i;
-    if (load_w(a, t) != tau) continue;
+  auto visit = [&](int64_t t) {
+    if (load_w(a, t) != tau) return;
     const uint32_t g = gid_of(a, a.item_lidx ? a.item_lidx[t] : uint32_t(t));
-    if (shift + 8 < 32 && (g >> (shift + 8)) != gp) continue;
+    if (shift + 8 < 32 && (g >> (shift + 8)) != gp) return;
     atomicAdd(&s_cnt[(g >> shift) & 255u], 1ull);
+  };
+  if (seg) {
+    const int64_t gw = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t cnt = seg->cnt[gw];
+    const uint32_t* L = seg->cand + gw * seg->cap;
+    for (uint32_t j = threadIdx.x & 31; j < cnt; j += 32) visit(L[j]);
+  } else {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n_items;
+         i += int64_t(gridDim.x) * blockDim.x)
+      visit(i);
   }
   __syncthreads();
   if (s_cnt[threadIdx.x]) atomicAdd(hist + threadIdx.x, s_cnt[threadIdx.x]);
@@ -391,7 +425,6 @@ __global__ void __launch_bounds__(256) k_imp_coop(ImportanceArgs a, ImpState* st
   __shared__ ImpState st;
   unsigned long long* total = set;
   unsigned long long* hist = set + 65;
-  unsigned long long* cand_count = set + kImpSetWords - 1;
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < kImpSetWords;
        t += int64_t(gridDim.x) * blockDim.x)
     next[t] = 0;
@@ -400,21 +433,26 @@ __global__ void __launch_bounds__(256) k_imp_coop(ImportanceArgs a, ImpState* st
   grid.sync();
   if (threadIdx.x == 0) init_state(&st, total);
   __syncthreads();
-  // (compacting the candidates of round r0 + 1 for the later rounds was measured slower: the
-  // crossing bins stay large and the list append serialises on one counter)
-  const bool listed = false;
-  (void)cand;
-  (void)cand_count;
+  // The first round whose candidates (the previous crossing bin) are at most half of the items
+  // scans everything once more and leaves each warp its candidates in a private segment; the
+  // later rounds and the gid rounds rescan only the segments.  Every CTA holds the same state,
+  // so the choice is grid-uniform.
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  Seg seg{cand, cand + ((a.n_items + stride - 1) / stride) * stride, (a.n_items + stride - 1) / stride * 32};
+  bool listed = false;
   for (int r = int(st.r0); r < kWRounds && !st.empty && !st.final_; ++r) {
-    hist_body(a, st.prefix, r, hist + r * 512);
+    int mode = 0;
+    if (listed) mode = 2;
+    else if (r > int(st.r0) && 2 * st.next_cnt <= (unsigned long long)a.n_items) mode = 1;
+    hist_body(a, st.prefix, r, hist + r * 512, mode, seg);
+    listed = listed || mode == 1;
     grid.sync();
     decide_body(&st, r, hist + r * 512, num, den);
   }
   if (!st.empty && st.need_gid) {
-    // every tie (w == tau) matched the prefix of every round, so it is in the candidate list
-    const int64_t nl = listed ? int64_t(*(volatile unsigned long long*)cand_count) : -1;
+    // every tie (w == tau) matched the prefix of every round, so it is in the segments
     for (int r = 0; r < kGRounds; ++r) {
-      gid_hist_body(a, st.tau, st.gprefix, r, hist + kWRounds * 512 + r * 256, listed ? cand : nullptr, nl);
+      gid_hist_body(a, st.tau, st.gprefix, r, hist + kWRounds * 512 + r * 256, listed ? &seg : nullptr);
       grid.sync();
       gid_decide_body(&st, r, hist + kWRounds * 512 + r * 256);
     }
@@ -478,8 +516,7 @@ void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s
 
 int64_t imp_set_words() { return kImpSetWords; }
 
-cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* set,
-                            unsigned long long* next, uint32_t* cand, int num, int den, cudaStream_t s) {
+static int coop_blocks() {
   static int blocks = 0;
   if (blocks == 0) {
     int per_sm = 0, dev = 0, sms = 0;
@@ -489,6 +526,17 @@ cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long
     blocks = sms * (per_sm < 4 ? per_sm : 4);
     if (blocks < 1) blocks = 1;
   }
+  return blocks;
+}
+
+int64_t imp_cand_words(int64_t n_items) {
+  const int64_t stride = int64_t(coop_blocks()) * 256;
+  return (n_items + stride - 1) / stride * stride + stride / 32 + 1;
+}
+
+cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* set,
+                            unsigned long long* next, uint32_t* cand, int num, int den, cudaStream_t s) {
+  const int blocks = coop_blocks();
   ImportanceArgs aa = a;
   int nn = num, dd = den;
   void* args[] = {&aa, &st, &set, &next, &cand, &nn, &dd};

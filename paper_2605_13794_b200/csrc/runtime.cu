@@ -882,7 +882,7 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
     const bool fresh = ctx->imp_hist.cap < 2 * set_bytes;
     CKS(ensure(ctx, ctx->imp_hist, 2 * set_bytes));
     if (fresh) CK(cudaMemsetAsync(ctx->imp_hist.p, 0, 2 * set_bytes, s));
-    CKS(ensure(ctx, ctx->cand, size_t(std::max<int64_t>(a.n_items, 1)) * 4));
+    CKS(ensure(ctx, ctx->cand, size_t(imp_cand_words(a.n_items)) * 4));
     unsigned long long* sets = P_<unsigned long long>(ctx->imp_hist);
     unsigned long long* cur = sets + (ctx->imp_parity ? imp_set_words() : 0);
     unsigned long long* nxt = sets + (ctx->imp_parity ? 0 : imp_set_words());
