@@ -176,44 +176,20 @@ def run_native(args):
                 cull_cols.append(cc)
         stream.synchronize()
 
-    stage_names = ("project", "route", "sort", "raster_fwd", "raster_bwd", "route_reverse", "project_bwd",
-                   "importance")
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(stage_names) + 1)]
+    stage_names = B.STAGES
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    cull_out = torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32, device=dev)
+    imp_view = B.importance_out(s_imp, c_rad, c_vis, cull_out, 99, 100)
 
     def one_view(v, record):
+        # one step = one bgs_view_step call (a1..a12; the library records its stage events)
         cam = cams[v % len(cams)]
         cull = cull_cols[v % len(cams)] if cull_cols is not None else None
         if record:
             ev[0].record(stream)
-        B.bgs_project(ctx, g, cam, gate, cull, 0, radius, stream)
+        B.bgs_view_step(ctx, g, cam, gate, cull, 0, radius, rgb, Tf, nc, dl, grads, imp_view, stream)
         if record:
             ev[1].record(stream)
-        B.bgs_route(ctx, None, stream)
-        if record:
-            ev[2].record(stream)
-        B.bgs_sort_tiles(ctx, stream)
-        if record:
-            ev[3].record(stream)
-        B.bgs_raster_fwd(ctx, B.BGS_IMPORTANCE, rgb, Tf, nc, stream)
-        if record:
-            ev[4].record(stream)
-        B.bgs_raster_bwd(ctx, dl, Tf, nc, stream)
-        if record:
-            ev[5].record(stream)
-        B.bgs_route_reverse(ctx, stream)
-        if record:
-            ev[6].record(stream)
-        B.bgs_project_bwd(ctx, g, cam, grads, stream)
-        if record:
-            ev[7].record(stream)
-        B.bgs_importance(ctx, n_local, radius, None, None, s_imp, c_rad, c_vis, imp_cull(v), 99, 100, stream)
-        if record:
-            ev[8].record(stream)
-
-    cull_out = torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32, device=dev)
-
-    def imp_cull(v):
-        return cull_out
 
     def barrier():
         if world > 1:
@@ -231,17 +207,19 @@ def run_native(args):
         total_ms = 0.0
         E_sum = 0.0
         launches0 = ctx.launches()
+        B.bgs_set_stage_timing(ctx, True)
         for k in range(args.steps):
             l2_flush.zero_()  # between timed views: evict the L2 (inputs also exceed it)
             stream.synchronize()
             one_view(args.warmup + k, True)
             stream.synchronize()
-            st = [ev[i].elapsed_time(ev[i + 1]) for i in range(len(stage_names))]
-            stage_ms += st
-            total_ms += ev[0].elapsed_time(ev[-1])
+            st = B.bgs_stage_times(ctx)
+            stage_ms += np.array([st[n] for n in stage_names])
+            total_ms += ev[0].elapsed_time(ev[1])
             qs.append(ctx.query())
             E_sum += float(nc.sum(dtype=torch.int64).item())  # outside the timed events
         launches = ctx.launches() - launches0
+        B.bgs_set_stage_timing(ctx, False)
         clk = clocks.stop()
     torch.cuda.synchronize()
     barrier()

@@ -227,6 +227,13 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
                               int32_t* radius_out, const float* dL_drgb_host, float* rgb_host,
                               const bgs_gaussian_grads* grads, const bgs_importance_out* importance, void* stream);
 
+/* Per-stage device timing of bgs_view_step: when enabled, CUDA events are recorded on the
+ * working stream between its stages; bgs_stage_times waits for the last one and writes the
+ * elapsed ms of the most recent step: [project, route, sort, raster_fwd, raster_bwd,
+ * route_reverse, project_bwd, importance] (ms_out host f32 [8]). */
+bgs_status bgs_set_stage_timing(bgs_ctx* ctx, int32_t enable);
+bgs_status bgs_stage_times(bgs_ctx* ctx, float* ms_out);
+
 /* ---------------------------------------------------------------------------------------
  * Shard layout (not a step of the method; a one-time data-layout utility)
  * --------------------------------------------------------------------------------------- */

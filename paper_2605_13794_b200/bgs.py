@@ -89,6 +89,8 @@ _SIGS = {
     "bgs_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_view_step_host": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_spatial_order": [_vp, _vp, C.c_int64, _vp, _vp],
+    "bgs_set_stage_timing": [_vp, C.c_int32],
+    "bgs_stage_times": [_vp, _vp],
     "bgs_score_phi": [_vp, C.c_int64, _vp, _vp, _vp, _vp],
     "bgs_prune_stochastic": [_vp, C.c_int64, _vp, C.c_int64, C.c_uint64, _vp, _vp],
     "bgs_prune_mass_cut": [_vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp],
@@ -397,3 +399,17 @@ def bgs_redistribute(ctx: Context, g: GaussianPlanes, keep, out: GaussianPlanes,
     ctx.check(_lib.bgs_redistribute(ctx.handle, C.byref(gs), _ptr(keep), C.byref(o), C.byref(n_out),
                                     _stream(stream)), "bgs_redistribute")
     return int(n_out.value)
+
+
+def bgs_set_stage_timing(ctx: Context, enable: bool):
+    ctx.check(_lib.bgs_set_stage_timing(ctx.handle, int(bool(enable))), "bgs_set_stage_timing")
+
+
+STAGES = ("project", "route", "sort", "raster_fwd", "raster_bwd", "route_reverse", "project_bwd", "importance")
+
+
+def bgs_stage_times(ctx: Context) -> dict:
+    """Device ms per stage of the most recent bgs_view_step (stage timing enabled)."""
+    out = (C.c_float * 8)()
+    ctx.check(_lib.bgs_stage_times(ctx.handle, out), "bgs_stage_times")
+    return dict(zip(STAGES, [float(x) for x in out]))

@@ -55,6 +55,8 @@ struct bgs_ctx {
   cudaEvent_t ev_counters = nullptr;         // counters copied to the host (bgs_project)
   cudaEvent_t ev_geom = nullptr;             // geometry kernels done (bgs_project)
   cudaStream_t side = nullptr;               // carries the counters copy off the working stream
+  bool stage_timing = false, stage_recorded = false;  // bgs_set_stage_timing / bgs_stage_times
+  cudaEvent_t stage_ev[9] = {};
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
 };
 
@@ -406,6 +408,8 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
   if (c->ev_counters) cudaEventDestroy(c->ev_counters);
   if (c->ev_geom) cudaEventDestroy(c->ev_geom);
   if (c->side) cudaStreamDestroy(c->side);
+  for (cudaEvent_t e : c->stage_ev)
+    if (e) cudaEventDestroy(e);
   c->tr.reset();
   delete c;
   return BGS_OK;
@@ -966,16 +970,50 @@ bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera*
                          float* t_final, int32_t* n_contrib, const float* dL, const bgs_gaussian_grads* grads,
                          const bgs_importance_out* imp, void* stream) {
   if (imp) flags |= BGS_IMPORTANCE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // stage boundaries (bgs_stage_times): events on the working stream, recorded only when enabled
+  auto mark = [&](int k) -> bgs_status {
+    if (ctx->stage_timing) CK(cudaEventRecord(ctx->stage_ev[k], s));
+    return BGS_OK;
+  };
+  if (ctx->stage_timing && !ctx->stage_ev[0])
+    for (auto& e : ctx->stage_ev) CK(cudaEventCreate(&e));
+  CKS(mark(0));
   CKS(bgs_project(ctx, g, cam, gate, cull_column, flags, radius_out, stream));
+  CKS(mark(1));
   CKS(bgs_route(ctx, nullptr, stream));
+  CKS(mark(2));
   CKS(bgs_sort_tiles(ctx, stream));
+  CKS(mark(3));
   CKS(bgs_raster_fwd(ctx, flags, rgb, t_final, n_contrib, stream));
+  CKS(mark(4));
   if (dL) CKS(bgs_raster_bwd(ctx, dL, t_final, n_contrib, stream));
+  CKS(mark(5));
   CKS(bgs_route_reverse(ctx, stream));
+  CKS(mark(6));
   if (dL && grads) CKS(bgs_project_bwd(ctx, g, cam, grads, stream));
+  CKS(mark(7));
   if (imp)
     CKS(bgs_importance(ctx, g->n_local, radius_out, nullptr, nullptr, imp->mass_num, imp->mass_den, imp->s,
                        imp->c_rad, imp->c_vis, imp->cull_out, stream));
+  CKS(mark(8));
+  ctx->stage_recorded = ctx->stage_timing;
+  return BGS_OK;
+}
+
+bgs_status bgs_set_stage_timing(bgs_ctx* ctx, int32_t enable) {
+  CKS(check_ctx(ctx));
+  ctx->stage_timing = enable != 0;
+  ctx->stage_recorded = false;
+  return BGS_OK;
+}
+
+bgs_status bgs_stage_times(bgs_ctx* ctx, float* ms_out) {
+  CKS(check_ctx(ctx));
+  if (!ms_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_stage_times: ms_out is NULL");
+  if (!ctx->stage_recorded) return fail(ctx, BGS_ERR_CONTRACT, "no bgs_view_step with stage timing enabled");
+  CK(cudaEventSynchronize(ctx->stage_ev[8]));
+  for (int k = 0; k < 8; ++k) CK(cudaEventElapsedTime(ms_out + k, ctx->stage_ev[k], ctx->stage_ev[k + 1]));
   return BGS_OK;
 }
 
