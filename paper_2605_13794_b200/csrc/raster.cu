@@ -244,6 +244,15 @@ __device__ __forceinline__ void init_pixb(PixB& p, bool inside, size_t pix, size
 
 // Backward evaluation of one pixel against one record (branch-free: `ok` predicates every
 // update so the two pixels of a lane interleave); accumulates the pixel's partials into g[9].
+// kFirst: g is written (the lane's first pixel) instead of accumulated, so no 0 + x adds
+// (which the compiler keeps for signed-zero semantics)
+template <bool kFirst>
+__device__ __forceinline__ void acc(float& g, float v) {
+  if (kFirst) g = v;
+  else g += v;
+}
+
+template <bool kFirst>
 __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float dy, uint32_t pos, float* g) {
   const float nq = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy);
   const bool ok = pos < p.last && in_cut(nq, s.co.z);
@@ -253,9 +262,9 @@ __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float
   const float inv = ok ? fast_rcp(1.0f - alpha) : 1.0f;  // 1 - alpha >= 0.01: rel. error 2^-23
   p.T *= inv;                                              // T before this splat
   const float wgt = ok ? alpha * p.T : 0.f;
-  g[6] += wgt * p.dr;
-  g[7] += wgt * p.dg;
-  g[8] += wgt * p.db;
+  acc<kFirst>(g[6], wgt * p.dr);
+  acc<kFirst>(g[7], wgt * p.dg);
+  acc<kFirst>(g[8], wgt * p.db);
   const float cdl = s.rgb.x * p.dr + s.rgb.y * p.dg + s.rgb.z * p.db;
   const float dLda = p.T * cdl - p.s * inv;
   p.s += cdl * wgt;  // now includes this splat for the ones in front of it
@@ -264,13 +273,13 @@ __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float
   // dL/do = sum gd; the geometry partials are linear in the per-pixel moments of gd
   // (dL/dpower = o gd, dpower/dmx = -(A dx + B dy), ...), so the record's o, A, B, C are
   // applied once per record in k_project_bwd instead of once per pixel
-  g[5] += gd;
+  acc<kFirst>(g[5], gd);
   const float gx = gd * dx, gy = gd * dy;
-  g[0] += gx;
-  g[1] += gy;
-  g[2] += gx * dx;
-  g[3] += gx * dy;
-  g[4] += gy * dy;
+  acc<kFirst>(g[0], gx);
+  acc<kFirst>(g[1], gy);
+  acc<kFirst>(g[2], gx * dx);
+  acc<kFirst>(g[3], gx * dy);
+  acc<kFirst>(g[4], gy * dy);
   return ok;
 }
 
@@ -321,12 +330,10 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
       const WRec s = mine[b];
       const uint32_t pos = pos0 + b;
       float g[9];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) g[k] = 0.f;
       const float dx = s.geo.x - pxf;
-      bool any = false;
+      bool any = eval_bwd<true>(p[0], s, dx, s.geo.y - pyf[0], pos, g);
 #pragma unroll
-      for (int i = 0; i < kPix; ++i) any |= eval_bwd(p[i], s, dx, s.geo.y - pyf[i], pos, g);
+      for (int i = 1; i < kPix; ++i) any |= eval_bwd<false>(p[i], s, dx, s.geo.y - pyf[i], pos, g);
       const unsigned cm = __ballot_sync(0xffffffffu, any);
       if (cm == 0) continue;
       float* dst = a.acc[__float_as_uint(s.co.w)].g;
