@@ -93,7 +93,9 @@ bgs_status ensure(bgs_ctx* ctx, DevBuf& b, size_t bytes) {
     cudaError_t e = cudaFree(b.p);
     if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "cudaFree", cudaGetErrorString(e));
   }
-  size_t want = bytes + bytes / 4 + 256;
+  // 1.5x headroom: per-view sizes vary by 2-3x across a camera set, and every regrowth is a
+  // cudaFree + cudaMalloc in the middle of a step
+  size_t want = bytes + bytes / 2 + 4096;
   cudaError_t e = cudaMalloc(&b.p, want);
   if (e != cudaSuccess) {
     b.p = nullptr;
