@@ -12,7 +12,9 @@ constexpr int kTile = 16;           // 16x16 pixel tiles (vanilla 3DGS)
 constexpr int kMaxWorld = 8;        // dest mask is one byte
 constexpr int kSortBlock = 256;     // onesweep CTA
 constexpr int kSortItems = 16;      // keys per thread per onesweep partition
-constexpr int kSortPart = kSortBlock * kSortItems;  // 4096 keys per partition
+constexpr int kSortPart = kSortBlock * kSortItems;  // 4096 keys per partition (Morton layout sort)
+constexpr int kViewSortItems = 16;  // per-view pair sort (u32 keys); 8 measured slower (longer look-back chains)
+constexpr int kViewSortPart = kSortBlock * kViewSortItems;
 constexpr int kMaxSortPasses = 6;   // 8-bit digits over <= 48 key bits
 
 // ProjectedSplat record, 48 B, three 16-B rows.

@@ -696,7 +696,7 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   a.counters = P_<unsigned long long>(ctx->counters);
   CKS(ensure(ctx, ctx->digit_hist, kMaxSortPasses * 256 * 4));
   CKS(ensure(ctx, ctx->pass_ctrl, 64 * 4));
-  const int64_t n_parts = std::max<int64_t>(1, (P + kSortPart - 1) / kSortPart);
+  const int64_t n_parts = std::max<int64_t>(1, (P + kViewSortPart - 1) / kViewSortPart);
   CKS(ensure(ctx, ctx->status, size_t(n_parts) * 256 * 4 * ctx->n_passes));
   CKS(ensure(ctx, ctx->ranges, size_t(std::max(nt, 1)) * 8));
   a.digit_hist = P_<uint32_t>(ctx->digit_hist);

@@ -225,11 +225,11 @@ __global__ void __launch_bounds__(256) k_digit_scan(SortArgs a) {
   if (threadIdx.x == 0) a.pass_ctrl[kFinalSel] = sel;
 }
 
-template <int NW, typename K>
-__global__ void __launch_bounds__(NW * 32, sizeof(K) == 4 ? 3 : 2) k_onesweep(SortArgs a, int64_t P, int pass,
+template <int NW, typename K, int ITEMS>
+__global__ void __launch_bounds__(NW * 32, sizeof(K) == 4 ? (ITEMS <= 8 ? 5 : 3) : 2) k_onesweep(SortArgs a, int64_t P, int pass,
                                                                             int n_parts) {
   constexpr int NT = NW * 32;
-  constexpr int PART = NT * kSortItems;
+  constexpr int PART = NT * ITEMS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   K* s_keys = reinterpret_cast<K*>(smem_raw);
   uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + PART);
@@ -252,13 +252,13 @@ __global__ void __launch_bounds__(NW * 32, sizeof(K) == 4 ? 3 : 2) k_onesweep(So
   __syncthreads();
   const int part = s_part;
   const int64_t base = int64_t(part) * PART;
-  const int64_t wbase = base + int64_t(w) * (32 * kSortItems);
+  const int64_t wbase = base + int64_t(w) * (32 * ITEMS);
 
-  K key[kSortItems];
-  uint32_t val[kSortItems];
-  uint32_t rank[kSortItems];
+  K key[ITEMS];
+  uint32_t val[ITEMS];
+  uint32_t rank[ITEMS];
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = wbase + i * 32 + lane;
     if (idx < P) {
       key[i] = kin[idx];
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(NW * 32, sizeof(K) == 4 ? 3 : 2) k_onesweep(So
   }
   const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = wbase + i * 32 + lane;
     const bool valid = idx < P;
     const uint32_t d = valid ? uint32_t((key[i] >> shift) & 255u) : 256u + lane;  // invalid: unique
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(NW * 32, sizeof(K) == 4 ? 3 : 2) k_onesweep(So
   __syncthreads();
   // local reorder in shared memory (stable: warp-major, then item, then lane == input order)
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
+  for (int i = 0; i < ITEMS; ++i) {
     const int64_t idx = wbase + i * 32 + lane;
     if (idx < P) {
       const uint32_t dd = uint32_t((key[i] >> shift) & 255u);
@@ -414,17 +414,18 @@ void launch_depth_range(const Rec* recv, int64_t n, unsigned long long* counters
   k_depth_range<<<unsigned(blocks), 256, 0, s>>>(recv, n, counters);
 }
 
-template <typename K>
+template <typename K, int ITEMS>
 static void sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches) {
-  const int n_parts = int((P + kSortPart - 1) / kSortPart);
-  const size_t smem = size_t(kSortPart) * (sizeof(K) + sizeof(uint32_t));
+  constexpr int PART = kSortBlock * ITEMS;
+  const int n_parts = int((P + PART - 1) / PART);
+  const size_t smem = size_t(PART) * (sizeof(K) + sizeof(uint32_t));
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_onesweep<8, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_onesweep<8, K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     attr_set = true;
   }
   for (int p = 0; p < a.n_passes; ++p) {
-    k_onesweep<8, K><<<n_parts, 256, smem, s>>>(a, P, p, n_parts);
+    k_onesweep<8, K, ITEMS><<<n_parts, 256, smem, s>>>(a, P, p, n_parts);
     ++*launches;
   }
 }
@@ -434,9 +435,9 @@ void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* l
   ++*launches;
   if (P <= 0) return;
   if (key_bytes == 4)
-    sort_passes<uint32_t>(a, P, s, launches);
+    sort_passes<uint32_t, kViewSortItems>(a, P, s, launches);
   else
-    sort_passes<unsigned long long>(a, P, s, launches);
+    sort_passes<unsigned long long, kSortItems>(a, P, s, launches);
 }
 
 void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s) {
