@@ -120,8 +120,10 @@ __device__ void stats_body(const ImportanceArgs& a, unsigned long long* total) {
     wsum += it.w;
     if (a.wbuf) a.wbuf[t] = it.w;  // dense copy for the radix rounds (8 B instead of a 48-B row)
     if (it.w) atomicAdd(&s_msb[63 - __clzll((long long)it.w)], 1u);
-    if (it.a > 0) a.s[it.lidx] += (double(it.w) * (1.0 / 16777216.0)) / (double(it.a) + 1e-8);
-    if (it.rad) a.c_rad[it.lidx] += 1u;
+    // reductions, not read-modify-writes: several views may be in flight on one shard (their
+    // contexts share the caller's s / c_rad / c_vis)
+    if (it.a > 0) atomicAdd(a.s + it.lidx, (double(it.w) * (1.0 / 16777216.0)) / (double(it.a) + 1e-8));
+    if (it.rad) atomicAdd(a.c_rad + it.lidx, 1u);
   }
   __syncthreads();
   if (threadIdx.x < 64 && s_msb[threadIdx.x]) atomicAdd(total + 1 + threadIdx.x, (unsigned long long)s_msb[threadIdx.x]);
@@ -357,7 +359,7 @@ __device__ void mark_body(const ImportanceArgs& a, const ImpState& st) {
       lidx = a.item_lidx ? a.item_lidx[t] : uint32_t(t);
       if (sel && w == st.tau && st.need_gid && gid_of(a, lidx) > st.gid_thr) sel = false;
     }
-    if (sel) a.c_vis[lidx] += 1u;
+    if (sel) atomicAdd(a.c_vis + lidx, 1u);
     // one atomicAnd per (warp, cull word): records come in local-index order, so a warp's
     // selected items share a few words
     const uint32_t word = sel ? (lidx >> 5) : (0x80000000u | uint32_t(lane));

@@ -153,23 +153,10 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
   gy += 2.f * qz * dRq[2][1]; gz += 2.f * qy * dRq[2][1]; gw += 2.f * qx * dRq[2][1]; gx += 2.f * w * dRq[2][1];
   gx -= 4.f * qx * dRq[2][2]; gy -= 4.f * qy * dRq[2][2];
 
-  float4 gm = a.g_mean_opac[i];
-  gm.x += dmu[0];
-  gm.y += dmu[1];
-  gm.z += dmu[2];
-  gm.w += g[5];
-  a.g_mean_opac[i] = gm;
-  float4 gq = a.g_quat[i];
-  gq.x += gw;
-  gq.y += gx;
-  gq.z += gy;
-  gq.w += gz;
-  a.g_quat[i] = gq;
-  float4 gs = a.g_scale[i];
-  gs.x += ds[0];
-  gs.y += ds[1];
-  gs.z += ds[2];
-  a.g_scale[i] = gs;
+  // accumulate with 128-bit reductions (no read round trip on the SM; the L2 adds)
+  atomicAdd(a.g_mean_opac + i, make_float4(dmu[0], dmu[1], dmu[2], g[5]));
+  atomicAdd(a.g_quat + i, make_float4(gw, gx, gy, gz));
+  atomicAdd(a.g_scale + i, make_float4(ds[0], ds[1], ds[2], 0.f));
 }
 
 // SH colour backward (second kernel: keeps each kernel's register footprint small so enough
@@ -238,21 +225,14 @@ __global__ void __launch_bounds__(256) k_project_bwd_sh(ProjectBwdArgs a) {
             SHC3[1] * xy * sk[10] + 8.f * SHC3[2] * yz * sk[11] + SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * sk[12] +
             8.f * SHC3[4] * xz * sk[13] + SHC3[5] * (xx - yy) * sk[14];
   const float dot = ddir[0] * X + ddir[1] * Y + ddir[2] * Z;
-  float4 gm = a.g_mean_opac[i];
-  gm.x += (ddir[0] - X * dot) * il;
-  gm.y += (ddir[1] - Y * dot) * il;
-  gm.z += (ddir[2] - Z * dot) * il;
-  a.g_mean_opac[i] = gm;
+  atomicAdd(a.g_mean_opac + i, make_float4((ddir[0] - X * dot) * il, (ddir[1] - Y * dot) * il,
+                                           (ddir[2] - Z * dot) * il, 0.f));
   float4* gsh = reinterpret_cast<float4*>(a.g_sh + size_t(48) * i);
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
-    float4 t = gsh[k];
     const int e = 4 * k;
-    t.x += Yb[(e) / 3] * dcol[(e) % 3];
-    t.y += Yb[(e + 1) / 3] * dcol[(e + 1) % 3];
-    t.z += Yb[(e + 2) / 3] * dcol[(e + 2) % 3];
-    t.w += Yb[(e + 3) / 3] * dcol[(e + 3) % 3];
-    gsh[k] = t;
+    atomicAdd(gsh + k, make_float4(Yb[(e) / 3] * dcol[(e) % 3], Yb[(e + 1) / 3] * dcol[(e + 1) % 3],
+                                   Yb[(e + 2) / 3] * dcol[(e + 2) % 3], Yb[(e + 3) / 3] * dcol[(e + 3) % 3]));
   }
 }
 
