@@ -265,6 +265,7 @@ def run_native(args):
         qs = []
         total_ms = 0.0
         E_sum = 0.0
+        A_sum = 0.0
         B.bgs_set_stage_timing(ctx, True)
         for k in range(args.steps):
             l2_flush.zero_()  # between timed views: evict the L2 (inputs also exceed it)
@@ -276,6 +277,10 @@ def run_native(args):
             total_ms += ev[0].elapsed_time(ev[1])
             qs.append(ctx.query())
             E_sum += float(nc.sum(dtype=torch.int64).item())  # outside the timed events
+            # contributing (pixel, splat) pairs = sum of a over this rank's received splats
+            acc = ctx.debug_buffer("acc")
+            if acc.numel():
+                A_sum += float(acc.view(torch.int32).view(-1, 12)[:, 9].sum(dtype=torch.int64).item())
         B.bgs_set_stage_timing(ctx, False)
     torch.cuda.synchronize()
     barrier()
@@ -414,7 +419,8 @@ def run_native(args):
     peaks = load_peaks()
     stage_avg = stage_ms / args.steps
     roof = stage_rooflines(stage_avg, qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
-                           sm_mhz=clk.get("sm_mhz"), E=E_sum / args.steps, cull=cull_cols is not None,
+                           sm_mhz=clk.get("sm_mhz"), E=E_sum / args.steps, A=A_sum / args.steps,
+                           cull=cull_cols is not None,
                            traffic=load_traffic(os.path.join(ROOT, "profiles", "ncu_traffic.json"))
                            if args.config == "rubble" and world == 1 else None)
     dominant = max(roof, key=lambda r: r["ms"])
@@ -437,6 +443,7 @@ def run_native(args):
         "per_view": {"pairs": P_all, "records_F": F_all, "received_R": R_all, "sent_D": D_all,
                      "active": A_all, "duplication_D_over_F": (D_all / F_all if F_all else None),
                      "E_pixel_entries": round(E_sum / args.steps, 1),
+                     "contributing_pairs": round(A_sum / args.steps, 1),
                      "gate_keep": (float(np.mean([q["n_lod"] for q in qs])) / n_local) if gate_on and n_local else None,
                      "owned_pairs_max_over_mean": (P_max * world / P_all) if P_all else None},
         "scoring": {"metric": "scoring views/s (a1-a8 NO_COLOR + a10 + a12, no backward)",

@@ -6,14 +6,20 @@ These are what the METHOD must move or compute, not what a kernel happens to do:
   a5-a7 sort         16 R (rect, depth of received) + 8 P (u32 key + u32 value written) + 16 P
                      per executed 8-bit radix pass (read + write) + 4 P (ranges pass)     [bytes]
   a8 raster fwd      19 FP32 ops per (pixel, list entry) up to the pixel's last contributor
-                     (E = sum of n_contrib): dx,dy 2, power 5, alpha cut 1, exp 1, alpha = min(.99,
-                     oG) 2, w = alpha T and T -= w 2, early stop 1, colour 3, w and a sums 2 [ALU]
-  a9 raster bwd      33 FP32 ops per (pixel, list entry) up to the last contributor: recompute
-                     dx,dy,power,cut,exp,alpha 11, T_k = T_{k+1}/(1-alpha) 3, w 1, colour
-                     grads 3, dL/dalpha (c.dL, T c.dL - s/(1-alpha), s update) 6, G dL/dalpha 1,
-                     dL/do 1, mean2d/conic moments 7                                      [ALU]
-                     (the minimal formulation: any kernel does at least this much per entry it
-                     does not cull; MUFU and FFMA count as one op)
+                     (SURVEY §8(d)'s E_min = sum of n_contrib): dx,dy 2, power 5, alpha cut 1,
+                     exp 1, alpha = min(.99, oG) 2, w = alpha T and T -= w 2, early stop 1,
+                     colour 3, w and a sums 2                                              [ALU]
+  a9 raster bwd      33 FP32 ops per E_min entry: recompute dx,dy,power,cut,exp,alpha 11,
+                     T_k = T_{k+1}/(1-alpha) 3, w 1, colour grads 3, dL/dalpha (c.dL,
+                     T c.dL - s/(1-alpha), s update) 6, G dL/dalpha 1, dL/do 1, mean2d/conic
+                     moments 7                                                            [ALU]
+                     (MUFU and FFMA count as one op.)  Exact culling skips most E_min entries
+                     (a splat whose alpha >= 1/255 ellipse misses a warp's 8x8 block cannot
+                     contribute there), so this fraction can exceed 1 on scenes with large
+                     splats.  `frac_contributing` is the strict bound beside it: the same ops per
+                     CONTRIBUTING (pixel, splat) pair (A = sum over splats of a_{i,v}), which every
+                     exact kernel must evaluate in full; on Rubble A is ~6% of E_min, i.e. most
+                     evaluations a block-culled kernel issues do not contribute.
   a10 reverse (M>1)  48 D (send back) + 48 D (gather)                                     [bytes]
   a11 project bwd    240 F (params) + 52 F (partials + index) + 2 x 236 F (grads RMW)     [bytes]
   a12 importance     52 F (w, a, index) + 2 x 16 F (s, c_rad, c_vis RMW) + N/8 (Cull)    [bytes]
@@ -30,7 +36,8 @@ def _avg(qs, k):
     return sum(q[k] for q in qs) / max(1, len(qs))
 
 
-def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=None, cull=False, traffic=None):
+def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=None, cull=False, traffic=None,
+                    A=None):
     """traffic: optional {stage: DRAM bytes per view} from a committed ncu capture (profiles/)."""
     traffic = traffic or {}
     N = float(n_local)
@@ -48,15 +55,20 @@ def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=No
         "importance": 52 * F + 32 * F + N / 8,
     }
     E = float(E) if E is not None else 0.0
+    A = float(A) if A is not None else E
     ops = {"raster_fwd": FWD_OPS * E, "raster_bwd": BWD_OPS * E}
+    ops_a = {"raster_fwd": FWD_OPS * A, "raster_bwd": BWD_OPS * A}
     out = []
     for name, ms in zip(names, stage_ms):
         ms = float(ms)
         if name in ops:
             ach = ops[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+            ach_a = ops_a[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+            k = FWD_OPS if name == "raster_fwd" else BWD_OPS
             out.append(dict(stage=name, ms=round(ms, 4), bound="alu", achieved=round(ach, 3), peak=round(alu, 2),
                             unit="TFLOP/s", frac=round(ach / alu, 4), traffic=traffic.get(name),
-                            work=f"{ops[name]:.3e} ops ({FWD_OPS if name == 'raster_fwd' else BWD_OPS:.0f} x E)"))
+                            work=f"{ops[name]:.3e} ops ({k:.0f} x E_min)",
+                            frac_contributing=round(ach_a / alu, 4)))
         else:
             b = bytes_.get(name, 0.0)
             ach = b / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
