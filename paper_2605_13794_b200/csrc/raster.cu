@@ -87,7 +87,13 @@ __device__ __forceinline__ bool stage_test(const RasterArgs& a, const uint32_t* 
   const float4 ax = __ldg(a.aux + r);
   out.geo = make_float4(q0.x, q0.y, 0.5f * q0.z, q0.w);
   out.co = make_float4(0.5f * q1.x, q1.y, -ax.x, __uint_as_float(r));
-  out.rgb = make_float4(q1.z, q1.w, q2.x, 0.f);
+  // pixel slot i of every lane covers block rows [y0 + kLaneRows i, y0 + kLaneRows (i+1) - 1]: bit i
+  // = the box reaches those rows (a warp-uniform skip of the slot's evaluation when it does not)
+  uint32_t slots = 0;
+  for (int i = 0; i * kLaneRows < h; ++i)
+    slots |= uint32_t((q0.y - ax.z <= y0 + float(kLaneRows * (i + 1) - 1)) & (q0.y + ax.z >= y0 + float(kLaneRows * i)))
+             << i;
+  out.rgb = make_float4(q1.z, q1.w, q2.x, __uint_as_float(slots));
   return (q0.x - ax.y <= x0 + float(w - 1)) & (q0.x + ax.y >= x0) & (q0.y - ax.z <= y0 + float(h - 1)) &
          (q0.y + ax.z >= y0);
 }
@@ -162,6 +168,7 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
       uint32_t fs = 0, cs = 0;
 #pragma unroll
       for (int i = 0; i < kPix; ++i) {
+        if (kPix > 1 && !((__float_as_uint(s.rgb.w) >> i) & 1u)) continue;  // warp-uniform: box misses these rows
         uint32_t f;
         bool c;
         eval_fwd1(p[i], s, dx, s.geo.y - pyf[i], pos, c, f);
@@ -339,9 +346,24 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
       const uint32_t pos = pos0 + b;
       float g[9];
       const float dx = s.geo.x - pxf;
-      bool any = eval_bwd<true>(p[0], s, dx, s.geo.y - pyf[0], pos, g);
+      bool any;
+      if (kPix == 2) {
+        // warp-uniform: evaluate only the pixel slots whose rows the record's box reaches (a
+        // skipped slot would fail the alpha cut: T, s and the partials are unchanged)
+        const uint32_t slots = __float_as_uint(s.rgb.w);
+        if (slots == 3u) {
+          any = eval_bwd<true>(p[0], s, dx, s.geo.y - pyf[0], pos, g);
+          any |= eval_bwd<false>(p[kPix - 1], s, dx, s.geo.y - pyf[kPix - 1], pos, g);
+        } else if (slots == 1u) {
+          any = eval_bwd<true>(p[0], s, dx, s.geo.y - pyf[0], pos, g);
+        } else {
+          any = eval_bwd<true>(p[kPix - 1], s, dx, s.geo.y - pyf[kPix - 1], pos, g);
+        }
+      } else {
+        any = eval_bwd<true>(p[0], s, dx, s.geo.y - pyf[0], pos, g);
 #pragma unroll
-      for (int i = 1; i < kPix; ++i) any |= eval_bwd<false>(p[i], s, dx, s.geo.y - pyf[i], pos, g);
+        for (int i = 1; i < kPix; ++i) any |= eval_bwd<false>(p[i], s, dx, s.geo.y - pyf[i], pos, g);
+      }
       const unsigned cm = __ballot_sync(0xffffffffu, any);
       if (cm == 0) continue;
       float* dst = a.acc[__float_as_uint(s.co.w)].g;
