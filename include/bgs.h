@@ -226,6 +226,16 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
                               const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
                               int32_t* radius_out, const float* dL_drgb_host, float* rgb_host,
                               const bgs_gaussian_grads* grads, const bgs_importance_out* importance, void* stream);
+/* Non-blocking form: returns once everything is enqueued.  The upload runs on a ctx-owned copy
+ * stream and only the compositing backward waits for it; the image is downloaded on a second copy
+ * stream as soon as the forward is done (overlapping the backward).  rgb_host is valid, and
+ * dL_drgb_host may be reused, after `stream` is synchronised (the call makes `stream` wait for
+ * both copies).  Several ctxs on several streams keep several views (and their copies) in flight. */
+bgs_status bgs_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                                    const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                                    int32_t* radius_out, const float* dL_drgb_host, float* rgb_host,
+                                    const bgs_gaussian_grads* grads, const bgs_importance_out* importance,
+                                    void* stream);
 
 /* Per-stage device timing of bgs_view_step: when enabled, CUDA events are recorded on the
  * working stream between its stages; bgs_stage_times waits for the last one and writes the

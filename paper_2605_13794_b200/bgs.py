@@ -88,6 +88,7 @@ _SIGS = {
     "bgs_importance": [_vp, C.c_int64, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp],
     "bgs_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_view_step_host": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_view_step_host_async": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_spatial_order": [_vp, _vp, C.c_int64, _vp, _vp],
     "bgs_set_stage_timing": [_vp, C.c_int32],
     "bgs_stage_times": [_vp, _vp],
@@ -413,3 +414,17 @@ def bgs_stage_times(ctx: Context) -> dict:
     out = (C.c_float * 8)()
     ctx.check(_lib.bgs_stage_times(ctx.handle, out), "bgs_stage_times")
     return dict(zip(STAGES, [float(x) for x in out]))
+
+
+def bgs_view_step_host_async(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags, radius_out,
+                             dL_host: torch.Tensor, rgb_host: torch.Tensor, grads: GradPlanes | None,
+                             importance: bgs_importance_out | None, stream=None):
+    """Non-blocking host-buffer step: rgb_host is valid after `stream` is synchronised."""
+    gs = g.struct()
+    gr = grads.struct() if grads is not None else None
+    ctx.check(_lib.bgs_view_step_host_async(ctx.handle, C.byref(gs), C.byref(cam),
+                                            C.byref(gate) if gate is not None else None, _ptr(cull_column), flags,
+                                            _ptr(radius_out), _ptr(dL_host), _ptr(rgb_host),
+                                            C.byref(gr) if gr is not None else None,
+                                            C.byref(importance) if importance is not None else None,
+                                            _stream(stream)), "bgs_view_step_host_async")

@@ -56,6 +56,8 @@ struct bgs_ctx {
   cudaEvent_t ev_geom = nullptr;             // geometry kernels done (bgs_project)
   cudaStream_t side = nullptr;               // carries the counters copy off the working stream
   bool stage_timing = false, stage_recorded = false;  // bgs_set_stage_timing / bgs_stage_times
+  cudaStream_t h2d = nullptr, d2h = nullptr;          // host-buffer step: copy streams
+  cudaEvent_t ev_in = nullptr, ev_dl = nullptr, ev_fwd = nullptr, ev_out = nullptr;
   cudaEvent_t stage_ev[9] = {};
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
 };
@@ -412,6 +414,10 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   for (cudaEvent_t e : c->stage_ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_in, c->ev_dl, c->ev_fwd, c->ev_out})
+    if (e) cudaEventDestroy(e);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   c->tr.reset();
   delete c;
   return BGS_OK;
@@ -967,10 +973,13 @@ bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, ui
   return BGS_OK;
 }
 
-bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
-                         const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, float* rgb,
-                         float* t_final, int32_t* n_contrib, const float* dL, const bgs_gaussian_grads* grads,
-                         const bgs_importance_out* imp, void* stream) {
+// dl_ready: event the compositing backward waits for (dL/dC still arriving); fwd_done: event
+// recorded once the image is final (the host path copies it out while the backward runs)
+static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                                 const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                                 int32_t* radius_out, float* rgb, float* t_final, int32_t* n_contrib, const float* dL,
+                                 const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream,
+                                 cudaEvent_t dl_ready, cudaEvent_t fwd_done) {
   if (imp) flags |= BGS_IMPORTANCE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // stage boundaries (bgs_stage_times): events on the working stream, recorded only when enabled
@@ -988,7 +997,9 @@ bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera*
   CKS(bgs_sort_tiles(ctx, stream));
   CKS(mark(3));
   CKS(bgs_raster_fwd(ctx, flags, rgb, t_final, n_contrib, stream));
+  if (fwd_done) CK(cudaEventRecord(fwd_done, s));
   CKS(mark(4));
+  if (dl_ready) CK(cudaStreamWaitEvent(s, dl_ready, 0));
   if (dL) CKS(bgs_raster_bwd(ctx, dL, t_final, n_contrib, stream));
   CKS(mark(5));
   CKS(bgs_route_reverse(ctx, stream));
@@ -1001,6 +1012,14 @@ bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera*
   CKS(mark(8));
   ctx->stage_recorded = ctx->stage_timing;
   return BGS_OK;
+}
+
+bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                         const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, float* rgb,
+                         float* t_final, int32_t* n_contrib, const float* dL, const bgs_gaussian_grads* grads,
+                         const bgs_importance_out* imp, void* stream) {
+  return view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, rgb, t_final, n_contrib, dL, grads, imp,
+                        stream, nullptr, nullptr);
 }
 
 bgs_status bgs_set_stage_timing(bgs_ctx* ctx, int32_t enable) {
@@ -1019,10 +1038,10 @@ bgs_status bgs_stage_times(bgs_ctx* ctx, float* ms_out) {
   return BGS_OK;
 }
 
-bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
-                              const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
-                              int32_t* radius_out, const float* dL_host, float* rgb_host,
-                              const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream) {
+bgs_status bgs_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                                    const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                                    int32_t* radius_out, const float* dL_host, float* rgb_host,
+                                    const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream) {
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   CKS(set_camera(ctx, cam));
@@ -1033,11 +1052,37 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
   CKS(ensure(ctx, ctx->scr_dl, npix * 12));
   CKS(ensure(ctx, ctx->scr_t, npix * 4));
   CKS(ensure(ctx, ctx->scr_n, npix * 4));
-  CK(cudaMemcpyAsync(ctx->scr_dl.p, dL_host, npix * 12, cudaMemcpyHostToDevice, s));
-  CKS(bgs_view_step(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
-                    P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), P_<float>(ctx->scr_dl), grads, imp, stream));
-  CK(cudaMemcpyAsync(rgb_host, ctx->scr_rgb.p, npix * 12, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  if (!ctx->h2d) {
+    CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ctx->ev_in, &ctx->ev_dl, &ctx->ev_fwd, &ctx->ev_out})
+      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  // dL/dC upload on its own copy engine, needed only by the compositing backward; it starts once
+  // this ctx's previous step no longer reads the scratch (everything queued on s so far)
+  CK(cudaEventRecord(ctx->ev_in, s));
+  CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_in, 0));
+  CK(cudaMemcpyAsync(ctx->scr_dl.p, dL_host, npix * 12, cudaMemcpyHostToDevice, ctx->h2d));
+  CK(cudaEventRecord(ctx->ev_dl, ctx->h2d));
+  CKS(view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
+                     P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), P_<float>(ctx->scr_dl), grads, imp, stream,
+                     ctx->ev_dl, ctx->ev_fwd));
+  // the image is final after the forward: download it while the backward runs; the working
+  // stream then waits for the download, so a sync of `stream` covers rgb_host
+  CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_fwd, 0));
+  CK(cudaMemcpyAsync(rgb_host, ctx->scr_rgb.p, npix * 12, cudaMemcpyDeviceToHost, ctx->d2h));
+  CK(cudaEventRecord(ctx->ev_out, ctx->d2h));
+  CK(cudaStreamWaitEvent(s, ctx->ev_out, 0));
+  return BGS_OK;
+}
+
+bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                              const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                              int32_t* radius_out, const float* dL_host, float* rgb_host,
+                              const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream) {
+  CKS(bgs_view_step_host_async(ctx, g, cam, gate, cull_column, flags, radius_out, dL_host, rgb_host, grads, imp,
+                               stream));
+  CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return BGS_OK;
 }
 
