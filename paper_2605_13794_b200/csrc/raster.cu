@@ -430,11 +430,9 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterArgs a, const flo
 
 // Heavy tiles split over two CTAs (k_raster_fwd).  BGS_SPLIT_TILES overrides the count (tuning).
 static int split_count(int n_tiles) {
-  static int env = -2;
-  if (env == -2) {
-    const char* e = getenv("BGS_SPLIT_TILES");
-    env = e ? atoi(e) : -1;
-  }
+  // read at every launch (a getenv), so tests can force either work unit on small images
+  const char* e = getenv("BGS_SPLIT_TILES");
+  const int env = e ? atoi(e) : -1;
   int sms = 148;
   static int cached = 0;
   if (!cached) {

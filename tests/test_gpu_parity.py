@@ -325,8 +325,11 @@ def test_full_size_sampled(config, view):
         gs.close()
 
 
+@pytest.mark.parametrize("split", ["default", "0"])
 @pytest.mark.parametrize("case", ["empty", "single", "ragged", "behind_and_offscreen", "dense_tile"])
-def test_edge_cases(case):
+def test_edge_cases(case, split, monkeypatch):
+    if split == "0":  # every tile on the two-pixels-per-lane work unit
+        monkeypatch.setenv("BGS_SPLIT_TILES", "0")
     if case == "empty":
         sc = S.gen_small(1, 5, 40, 24)
         sc.means[:, 2] = -3.0  # everything behind the camera
@@ -408,3 +411,32 @@ def test_views_in_flight_match_sequential(tiny_scene):
         assert torch.all((x - y).abs() <= 1e-3 * x.abs() + 1e-5 * float(x.abs().max())), name
     assert torch.equal(seq[3], par[3]) and torch.equal(seq[4], par[4])
     assert torch.allclose(seq[2], par[2], rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("split", ["0", "all"])
+def test_raster_work_units_parity(tiny_scene, monkeypatch, split):
+    """Both compositing work units against the oracle: every tile as one CTA with two pixels per
+    lane and the row-half skip (split 0: the path most Rubble tiles take) and every tile as two
+    half-tile CTAs with one pixel per lane (the heavy-tile path)."""
+    monkeypatch.setenv("BGS_SPLIT_TILES", "0" if split == "0" else "100000")
+    sc = tiny_scene
+    cam = sc.cameras[0]
+    dl = S.grad_image(cam["H"], cam["W"])
+    st = O.OracleStep(sc, cam, M=1, dLdC=dl)
+    gs = GpuStep(sc, cam, M=1, dLdC=dl)
+    try:
+        H, W = cam["H"], cam["W"]
+        cand, flips, affected = _flip_info(st, gs, cam)
+        ok = ~flips
+        assert np.abs(gs.img - st.get("img").reshape(3, H, W))[:, ok].max() <= 1e-4
+        assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
+        keep = np.ones(sc.n, bool)
+        keep[list(affected)] = False
+        assert np.array_equal(gs.a[keep], st.get("a")[keep])
+        for name, width in (("d_mean", 3), ("d_quat", 4), ("d_scale", 3), ("d_opac", 1), ("d_sh", 48)):
+            ref = st.get(name).reshape(sc.n, width)[keep]
+            got = gs.grads[name].reshape(sc.n, width)[keep]
+            tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
+            assert not (np.abs(got - ref) > tol).any(), name
+    finally:
+        gs.close()
