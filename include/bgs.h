@@ -182,7 +182,9 @@ bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_fin
                           void* stream);
 
 /* a9.  dL_drgb: device f32 [3][H][W] (read on owned tiles only).  t_final / n_contrib: the
- * buffers written by bgs_raster_fwd. */
+ * buffers written by the preceding bgs_raster_fwd on this ctx (same view); the backward also
+ * reads the per-(8x8 block, 32-entry chunk) contributor masks that forward left in the arena
+ * and evaluates only the list entries some pixel of the block composited. */
 bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL_drgb, const float* t_final, const int32_t* n_contrib,
                           void* stream);
 

@@ -154,11 +154,14 @@ struct RasterArgs {
   const float4* aux;          // per received record: thr, box half extents (from k_emit)
   const uint32_t* tile_perm;  // launch order of the owned tiles (longest list first)
   int n_split;                // the first n_split tiles of tile_perm run as two half-tile CTAs
+  uint32_t* cmask;            // contributor masks: written by the forward, read by the backward
 };
+constexpr int kRasterSlots = 8;  // warp blocks per tile (8 in a split tile, 4 otherwise)
 constexpr int kFinalSel = 15;  // buffer holding the sorted keys after the passes
 constexpr int kValsSel = 24;   // buffer holding the final (tie-fixed) values, written by k_ranges_fixup
-void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
-                       cudaStream_t s);
+// returns the number of split tiles used (the backward must be launched with the same split)
+int launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
+                      cudaStream_t s);
 void launch_raster_bwd(const RasterArgs& a, const float* dL, const float* t_final, const int32_t* n_contrib,
                        cudaStream_t s);
 

@@ -127,8 +127,8 @@ __device__ __forceinline__ void eval_fwd1(PixF& p, const WRec& s, float dx, floa
 // independent dependency chains per lane, branch-free).
 template <bool kImportance, int kPix>
 __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* __restrict__ vals, int lt, int col0,
-                                          int row0, WRec* mine, float* __restrict__ rgb, float* __restrict__ t_final,
-                                          int32_t* __restrict__ n_contrib) {
+                                          int row0, int slot, WRec* mine, float* __restrict__ rgb,
+                                          float* __restrict__ t_final, int32_t* __restrict__ n_contrib) {
   const int tile = a.t_begin + lt;
   const int tx = tile % a.TX, ty = tile / a.TX;
   const int lane = threadIdx.x & 31;
@@ -145,7 +145,9 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
     pyf[i] = float(py);
     p[i] = PixF{px < a.W && py < a.H ? 1.f : -1.f, 0.f, 0.f, 0.f, 0u};
   }
-  for (uint32_t base = range.x; base < range.y; base += 32) {
+  // word of chunk k: ((range.x >> 5) + lt + k) kRasterSlots + slot (32-bit index: fewer live registers)
+  uint32_t widx = ((range.x >> 5) + uint32_t(lt)) * kRasterSlots + uint32_t(slot);
+  for (uint32_t base = range.x; base < range.y; base += 32, widx += kRasterSlots) {
     bool done = true;
 #pragma unroll
     for (int i = 0; i < kPix; ++i) done = done && p[i].T < 0.f;
@@ -158,7 +160,7 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
     __syncwarp();
     // importance of the record this lane staged: the warp sums land in the staging lane's
     // registers and it issues the two atomics after the batch
-    uint32_t my_w = 0, my_a = 0;
+    uint32_t my_w = 0, my_a = 0, contrib = 0;
     while (m) {
       const int j = __ffs(m) - 1;
       m &= m - 1;
@@ -182,8 +184,13 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
           my_w = sum;
           my_a = cnt;
         }
+      } else {
+        contrib |= uint32_t(__any_sync(0xffffffffu, cs != 0)) << j;
       }
     }
+    // contributor mask of this chunk for the backward: bit j = some pixel of the block took record j
+    if (kImportance) contrib = __ballot_sync(0xffffffffu, my_a != 0);
+    if (lane == 0) a.cmask[widx] = contrib;
     if (kImportance && my_a) {
       Acc* acc = a.acc + __float_as_uint(st.co.w);
       atomicAdd(&acc->a, my_a);
@@ -223,11 +230,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
   if (b < 2 * a.n_split) {
     const int lt = int(__ldg(a.tile_perm + (b >> 1)));
     fwd_strip<kImportance, 1>(a, vals, lt, kStripW * (warp % kStripsX), (b & 1) * 8 + kLaneRows * (warp / kStripsX),
-                              s_rec[warp], rgb, t_final, n_contrib);
+                              (b & 1) * kWarps + warp, s_rec[warp], rgb, t_final, n_contrib);
   } else {
     const int lt = int(__ldg(a.tile_perm + (b - a.n_split)));
-    fwd_strip<kImportance, 2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), s_rec[warp],
-                              rgb, t_final, n_contrib);
+    fwd_strip<kImportance, 2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), warp,
+                              s_rec[warp], rgb, t_final, n_contrib);
   }
 }
 
@@ -304,8 +311,7 @@ __device__ __forceinline__ float xsel(bool hi, float a, float b) { return hi ? a
 // walk of the heaviest tiles (k_raster_bwd's work split).
 template <int kPix>
 __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* __restrict__ vals, int lt, int col0,
-                                          int row0,
-                                          WRec* mine, const float* __restrict__ dL,
+                                          int row0, int slot, WRec* mine, const float* __restrict__ dL,
                                           const float* __restrict__ t_final, const int32_t* __restrict__ n_contrib) {
   constexpr int kStripH = kLaneRows * kPix;
   const int tile = a.t_begin + lt;
@@ -334,8 +340,12 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
   for (int c = int((wlast + 31) / 32) - 1; c >= 0; --c) {
     const uint32_t pos0 = uint32_t(c) * 32;  // relative to range.x
     const uint32_t rel = pos0 + lane;
+    // the forward's contributor mask of this chunk: entries none of the block's pixels took are
+    // exactly the ones every pixel's `ok` rejects here (same power, cut and last decisions)
+    const uint32_t cw = __ldg(a.cmask + size_t((range.x >> 5) + uint32_t(lt) + uint32_t(c)) * kRasterSlots + slot);
+    if (cw == 0u) continue;
     WRec st;
-    const bool hit = rel < wlast && stage_test(a, vals, range.x + rel, x0, y0, kStripW, kStripH, st);
+    const bool hit = ((cw >> lane) & 1u) && rel < wlast && stage_test(a, vals, range.x + rel, x0, y0, kStripW, kStripH, st);
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (hit) mine[lane] = st;
     __syncwarp();
@@ -417,11 +427,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterArgs a, const flo
   const int b = blockIdx.x;
   if (b < 2 * a.n_split) {
     const int lt = int(__ldg(a.tile_perm + (b >> 1)));
-    bwd_strip<1>(a, vals, lt, kStripW * (warp % kStripsX), (b & 1) * 8 + kLaneRows * (warp / kStripsX), s_rec[warp],
-                 dL, t_final, n_contrib);
+    bwd_strip<1>(a, vals, lt, kStripW * (warp % kStripsX), (b & 1) * 8 + kLaneRows * (warp / kStripsX),
+                 (b & 1) * kWarps + warp, s_rec[warp], dL, t_final, n_contrib);
   } else {
     const int lt = int(__ldg(a.tile_perm + (b - a.n_split)));
-    bwd_strip<2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), s_rec[warp], dL,
+    bwd_strip<2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), warp, s_rec[warp], dL,
                  t_final, n_contrib);
   }
 }
@@ -447,9 +457,9 @@ static int split_count(int n_tiles) {
   return want < n_tiles ? want : n_tiles;
 }
 
-void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
-                       cudaStream_t s) {
-  if (a.n_tiles <= 0) return;
+int launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
+                      cudaStream_t s) {
+  if (a.n_tiles <= 0) return 0;
   RasterArgs b = a;
   b.n_split = split_count(a.n_tiles);
   const unsigned grid = unsigned(a.n_tiles + b.n_split);
@@ -457,6 +467,7 @@ void launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t
     k_raster_fwd<true><<<grid, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
   else
     k_raster_fwd<false><<<grid, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+  return b.n_split;
 }
 
 void launch_raster_bwd(const RasterArgs& a, const float* dL, const float* t_final, const int32_t* n_contrib,
@@ -464,8 +475,8 @@ void launch_raster_bwd(const RasterArgs& a, const float* dL, const float* t_fina
   if (a.n_tiles <= 0) return;
   // light tiles: 2 pixels per lane (0.415 ms per Rubble view vs 0.73 ms with 4: the coarser strip
   // culls worse and a warp walks to the deepest of 128 pixels)
-  RasterArgs b = a;
-  b.n_split = split_count(a.n_tiles);
+  // a.n_split: the forward's split (the contributor masks are per warp block of that layout)
+  const RasterArgs& b = a;
   k_raster_bwd<<<unsigned(a.n_tiles + b.n_split), kThreads, 0, s>>>(b, dL, t_final, n_contrib);
 }
 

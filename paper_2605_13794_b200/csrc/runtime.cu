@@ -41,13 +41,14 @@ struct bgs_ctx {
   int stage = 0;  // 1 projected, 2 routed, 3 sorted, 4 fwd, 5 bwd, 6 reversed
   int64_t n_local = 0, F = 0, P_all = 0, R = 0, D = 0, P = 0, n_lod = 0, n_act = 0;
   int t_begin = 0, t_end = 0, n_passes = 0, fallback = 0;
+  int raster_split = 0;  // heavy tiles split over two CTAs in the last forward (the backward reuses it)
   int imp_parity = 0;  // which half of imp_hist the next world-1 importance call uses
   const Rec* recv = nullptr;  // == recs at world 1
   Acc* acc_local = nullptr;   // == acc at world 1
   // arena
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
-      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf;
+      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask;
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
@@ -402,7 +403,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -760,6 +761,7 @@ static RasterArgs raster_args(bgs_ctx* ctx) {
   a.acc = P_<Acc>(ctx->acc);
   a.aux = P_<float4>(ctx->aux);
   a.tile_perm = P_<uint32_t>(ctx->tile_perm);
+  a.cmask = P_<uint32_t>(ctx->cmask);
   return a;
 }
 
@@ -772,9 +774,12 @@ bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_fin
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CKS(ensure(ctx, ctx->acc, size_t(std::max<int64_t>(ctx->R, 1)) * sizeof(Acc)));
   CK(cudaMemsetAsync(ctx->acc.p, 0, size_t(std::max<int64_t>(ctx->R, 1)) * sizeof(Acc), s));
-  const RasterArgs a = raster_args(ctx);
+  // contributor masks: one word per (warp block, 32-entry chunk of its tile's list), chunk index
+  // floor(range.x / 32) + lt + c is injective over (lt, c) (raster.cu), 8 warp blocks per tile
+  CKS(ensure(ctx, ctx->cmask, size_t(kRasterSlots) * size_t(ctx->P / 32 + (ctx->t_end - ctx->t_begin) + 2) * 4));
+  RasterArgs a = raster_args(ctx);
   if (a.n_tiles > 0) {
-    launch_raster_fwd(a, flags, rgb, t_final, n_contrib, s);
+    ctx->raster_split = launch_raster_fwd(a, flags, rgb, t_final, n_contrib, s);
     CKS(launched(ctx));
   }
   ctx->stage = 4;
@@ -788,7 +793,8 @@ bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL, const float* t_final, c
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_raster_bwd before bgs_raster_fwd");
   if (!dL || !t_final || !n_contrib) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "image pointer is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const RasterArgs a = raster_args(ctx);
+  RasterArgs a = raster_args(ctx);
+  a.n_split = ctx->raster_split;
   if (a.n_tiles > 0) {
     launch_raster_bwd(a, dL, t_final, n_contrib, s);
     CKS(launched(ctx));

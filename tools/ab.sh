@@ -1,0 +1,5 @@
+# usage: ab.sh variantA variantB ... ; runs bench alternately twice
+for rep in 1 2; do for v in "$@"; do
+  if [ "$v" = "cur" ]; then L=libbgs.so; else L=libbgs_$v.so; fi
+  BGS_LIB=$L timeout 300 python bench.py --no-cpu-baseline $BENCH_ARGS 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['value'], d['single_view_ms'], {k:v for k,v in d['stages_ms'].items() if 'route' not in k})"
+done; done
