@@ -14,6 +14,8 @@
  *   bgs_route_reverse  a10 reverse exchange of per-splat gradients to the owning shard
  *   bgs_project_bwd    a11 backward of the projection
  *   bgs_importance     a12 Eq.3 score, c^rad, c^vis top-99% mass, Cull column
+ *   bgs_loss_photo     NEXT-4 Eq.7 L1 + SSIM on the owned tiles with its gradient
+ *   bgs_loss_scale     NEXT-4 Eq.8 scale regulariser over the visible set
  * bgs_view_step / bgs_view_step_host run a1..a11 (+a12 when requested) in one call.
  *
  * Conventions (all entry points):
@@ -302,6 +304,32 @@ bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s, in
  * size; BGS_ERR_CAPACITY when it exceeds out->capacity.  out must not alias in.  HOST-SYNC. */
 bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t* keep, const bgs_gaussians_out* out,
                             int64_t* n_out, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * NEXT-4 supervision: the loss of Eq.7-8 on the owned tiles
+ * --------------------------------------------------------------------------------------- */
+/* Eq.7 photometric term of one view, fused with its gradient.  Call after
+ * bgs_raster_fwd of the view on this ctx (ownership and camera of that view).
+ * l_v = (1 - lambda) mean|rgb - target| + lambda (1 - SSIM(rgb, target)), means over the 3 H W
+ * elements; SSIM per channel with the 11x11 Gaussian window (sigma 1.5, normalised), zero
+ * padding, C1 = 0.01^2, C2 = 0.03^2 (reading R34).  rgb: device f32 [3][H][W] as written by
+ * bgs_raster_fwd (owned tiles valid; at world > 1 the owned pixels of every rank are summed
+ * into one full image first so that windows straddling ownership boundaries see the same
+ * pixels as on one GPU).  target: device f32 [3][H][W] (read on the owned tiles + 10 px).
+ * dL_drgb: device f32 [3][H][W], OVERWRITTEN on the owned tiles with
+ * batch_inv * dl_v/drgb (batch_inv = 1/B of Eq.7; sign(0) = 0 for the L1 term).
+ * out: device f64 [3], overwritten with {l_v, L1_v, SSIM_v} (global over ranks; not scaled by
+ * batch_inv).  0 <= lambda <= 1. */
+bgs_status bgs_loss_photo(bgs_ctx* ctx, const float* rgb, const float* target, float lambda, float batch_inv,
+                          float* dL_drgb, double* out, void* stream);
+
+/* Eq.8 scale regulariser of one view: L_scale = (1/|V|) sum_{i in V} min_j s_ij,
+ * V = Gaussians with radius > 0 in this view over ALL ranks (radius from bgs_project);
+ * grads->scale[i][argmin_j s_ij] += beta / |V| for the visible local Gaussians (first axis
+ * among equal minima, R35; beta includes the caller's 1/B).  out: device f64 [2], overwritten
+ * with {L_scale, |V|}; |V| = 0 gives L_scale = 0 and no gradient. */
+bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, const int32_t* radius, float beta,
+                          const bgs_gaussian_grads* grads, double* out, void* stream);
 
 #ifdef __cplusplus
 }

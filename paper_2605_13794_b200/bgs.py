@@ -96,6 +96,8 @@ _SIGS = {
     "bgs_prune_stochastic": [_vp, C.c_int64, _vp, C.c_int64, C.c_uint64, _vp, _vp],
     "bgs_prune_mass_cut": [_vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp],
     "bgs_redistribute": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_loss_photo": [_vp, _vp, _vp, C.c_float, C.c_float, _vp, _vp, _vp],
+    "bgs_loss_scale": [_vp, _vp, _vp, C.c_float, _vp, _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -327,6 +329,20 @@ def bgs_importance(ctx: Context, n_local: int, radius, w_fixed, a, s, c_rad, c_v
     ctx.check(_lib.bgs_importance(ctx.handle, int(n_local), _ptr(radius), _ptr(w_fixed), _ptr(a), mass_num, mass_den,
                                   _ptr(s), _ptr(c_rad), _ptr(c_vis), _ptr(cull_out), _stream(stream)),
               "bgs_importance")
+
+
+def bgs_loss_photo(ctx: Context, rgb, target, lam: float, batch_inv: float, dL_drgb, out, stream=None):
+    """NEXT-4, Eq.7: out (device f64[3]) = {l_v, L1, SSIM}; dL_drgb overwritten on owned tiles."""
+    ctx.check(_lib.bgs_loss_photo(ctx.handle, _ptr(rgb), _ptr(target), float(lam), float(batch_inv), _ptr(dL_drgb),
+                                  _ptr(out), _stream(stream)), "bgs_loss_photo")
+
+
+def bgs_loss_scale(ctx: Context, g: GaussianPlanes, radius, beta: float, grads: GradPlanes, out, stream=None):
+    """NEXT-4, Eq.8: out (device f64[2]) = {L_scale, |V|}; grads.scale += beta/|V| on argmin axes."""
+    gs = g.struct()
+    gr = grads.struct()
+    ctx.check(_lib.bgs_loss_scale(ctx.handle, C.byref(gs), _ptr(radius), float(beta), C.byref(gr), _ptr(out),
+                                  _stream(stream)), "bgs_loss_scale")
 
 
 def bgs_view_step(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags, radius_out, rgb, t_final,

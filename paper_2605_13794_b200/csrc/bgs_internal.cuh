@@ -200,6 +200,8 @@ struct PtrList {
 };
 void launch_reduce_sum_i32(PtrList src, int32_t* dst, int64_t n, cudaStream_t s);
 void launch_reduce_sum_u64(PtrList src, unsigned long long* dst, int64_t n, cudaStream_t s);
+void launch_reduce_sum_f32(PtrList src, float* dst, int64_t n, cudaStream_t s);
+void launch_reduce_sum_f64(PtrList src, double* dst, int64_t n, cudaStream_t s);
 constexpr int kRouteBlock = 256;
 
 // importance (a12)
@@ -270,5 +272,28 @@ void launch_pack_rows(int64_t n, const uint32_t* new_gid, int world, const int64
 void launch_scatter_direct(int64_t n, const uint32_t* new_gid, const bgs_gaussians& g, const bgs_gaussians_out& o,
                            int64_t cap, cudaStream_t s);
 void launch_unpack_rows(int64_t n, const void* in, const bgs_gaussians_out& o, int64_t cap, cudaStream_t s);
+
+// NEXT-4 supervision: Eq.7 photometric loss on the owned tiles (fused with its gradient) and the
+// Eq.8 scale regulariser (loss.cu)
+struct LossArgs {
+  const float* x;      // rendered image [3][H][W] (full image at world > 1: all-reduced)
+  const float* y;      // target image [3][H][W]
+  float* dL;           // dl/dx on the owned pixels, [3][H][W]
+  double2* partials;   // per CTA: (sum |x - y|, sum SSIM) over its owned pixels
+  int W, H, TX, t_begin, t_end;
+  float k_l1, k_ssim;  // batch_inv (1 - lambda) / (3 H W), batch_inv lambda / (3 H W)
+  float g[11];         // normalised 1-D Gaussian window, sigma 1.5
+};
+size_t loss_smem_bytes();
+int64_t loss_n_blocks(int W, int H);
+void launch_loss_photo(const LossArgs& a, cudaStream_t s);
+void launch_loss_sums(const double2* partials, int n, double* sums, cudaStream_t s);
+void launch_loss_finish(const double* sums, double n_elem, double lambda, double* out, cudaStream_t s);
+void launch_owned_copy(const float* rgb, int W, int H, int TX, int t_begin, int t_end, float* full, cudaStream_t s);
+int scale_n_blocks(int64_t n);
+void launch_scale_sum(const float4* scale, const int32_t* radius, int64_t n, double2* partials, cudaStream_t s);
+void launch_scale_finish(const double* sums, double* out, cudaStream_t s);
+void launch_scale_grad(const float4* scale, const int32_t* radius, int64_t n, const double* sums, float beta,
+                       float* g_scale, cudaStream_t s);
 
 }  // namespace bgs

@@ -233,6 +233,15 @@ __global__ void k_reduce_u64(PtrList src, unsigned long long* dst, int64_t n) {
   dst[i] = v;
 }
 
+template <class T>
+__global__ void k_reduce_sum(PtrList src, T* dst, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T v = static_cast<const T*>(src.p[0])[i];
+  for (int k = 1; k < src.n; ++k) v += static_cast<const T*>(src.p[k])[i];  // rank order
+  dst[i] = v;
+}
+
 }  // namespace
 
 void launch_tile_costs(const int32_t* diff, int TX, int TY, int32_t* pairs_t, cudaStream_t s) {
@@ -282,6 +291,14 @@ void launch_gather_sum(const Acc* rev, int64_t F, const uint8_t* dest_mask, cons
 
 void launch_reduce_sum_i32(PtrList src, int32_t* dst, int64_t n, cudaStream_t s) {
   if (n > 0) k_reduce_i32<<<unsigned((n + 255) / 256), 256, 0, s>>>(src, dst, n);
+}
+
+void launch_reduce_sum_f32(PtrList src, float* dst, int64_t n, cudaStream_t s) {
+  if (n > 0) k_reduce_sum<float><<<unsigned((n + 255) / 256), 256, 0, s>>>(src, dst, n);
+}
+
+void launch_reduce_sum_f64(PtrList src, double* dst, int64_t n, cudaStream_t s) {
+  if (n > 0) k_reduce_sum<double><<<unsigned((n + 255) / 256), 256, 0, s>>>(src, dst, n);
 }
 
 void launch_reduce_sum_u64(PtrList src, unsigned long long* dst, int64_t n, cudaStream_t s) {

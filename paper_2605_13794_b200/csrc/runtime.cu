@@ -48,7 +48,8 @@ struct bgs_ctx {
   // arena
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
-      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask;
+      imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask,
+      loss_img, loss_part, loss_sums;
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
@@ -123,6 +124,8 @@ struct Transport {
   virtual ~Transport() = default;
   virtual bgs_status allreduce_i32(bgs_ctx* ctx, int32_t* buf, int64_t n, cudaStream_t s) = 0;
   virtual bgs_status allreduce_u64(bgs_ctx* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) = 0;
+  virtual bgs_status allreduce_f32(bgs_ctx* ctx, float* buf, int64_t n, cudaStream_t s) = 0;
+  virtual bgs_status allreduce_f64(bgs_ctx* ctx, double* buf, int64_t n, cudaStream_t s) = 0;
   // device int64 [world] -> device int64 [world]: element d of send goes to rank d
   virtual bgs_status alltoall1(bgs_ctx* ctx, const int64_t* send, int64_t* recv, cudaStream_t s) = 0;
   virtual bgs_status alltoallv(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
@@ -144,6 +147,14 @@ struct NcclTransport : Transport {
   }
   bgs_status allreduce_u64(bgs_ctx* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) override {
     ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclUint64, ncclSum, comm, s);
+    return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
+  }
+  bgs_status allreduce_f32(bgs_ctx* ctx, float* buf, int64_t n, cudaStream_t s) override {
+    ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclFloat32, ncclSum, comm, s);
+    return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
+  }
+  bgs_status allreduce_f64(bgs_ctx* ctx, double* buf, int64_t n, cudaStream_t s) override {
+    ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclFloat64, ncclSum, comm, s);
     return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
   }
   bgs_status alltoall1(bgs_ctx* ctx, const int64_t* send, int64_t* recv, cudaStream_t s) override {
@@ -245,6 +256,16 @@ struct LocalTransport : Transport {
   bgs_status allreduce_u64(bgs_ctx* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) override {
     return allreduce(ctx, buf, n, s, [](PtrList p, unsigned long long* d, int64_t nn, cudaStream_t ss) {
       launch_reduce_sum_u64(p, d, nn, ss);
+    });
+  }
+  bgs_status allreduce_f32(bgs_ctx* ctx, float* buf, int64_t n, cudaStream_t s) override {
+    return allreduce(ctx, buf, n, s, [](PtrList p, float* d, int64_t nn, cudaStream_t ss) {
+      launch_reduce_sum_f32(p, d, nn, ss);
+    });
+  }
+  bgs_status allreduce_f64(bgs_ctx* ctx, double* buf, int64_t n, cudaStream_t s) override {
+    return allreduce(ctx, buf, n, s, [](PtrList p, double* d, int64_t nn, cudaStream_t ss) {
+      launch_reduce_sum_f64(p, d, nn, ss);
     });
   }
   bgs_status exchange(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
@@ -403,7 +424,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -1089,6 +1110,88 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
   CKS(bgs_view_step_host_async(ctx, g, cam, gate, cull_column, flags, radius_out, dL_host, rgb_host, grads, imp,
                                stream));
   CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return BGS_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// NEXT-4 supervision: Eq.7 photometric loss + gradient on the owned tiles, Eq.8 regulariser
+// ---------------------------------------------------------------------------------------
+bgs_status bgs_loss_photo(bgs_ctx* ctx, const float* rgb, const float* target, float lambda, float batch_inv,
+                          float* dL_drgb, double* out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_loss_photo before bgs_raster_fwd");
+  if (!rgb || !target || !dL_drgb || !out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "loss pointer is NULL");
+  if (!(lambda >= 0.f && lambda <= 1.f)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "lambda outside [0, 1]");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int W = ctx->cam.W, H = ctx->cam.H;
+  const size_t plane = size_t(W) * H;
+  const float* x = rgb;
+  if (ctx->world > 1) {
+    // the owned pixels of every rank summed into one full image (x + 0 = x: every rank holds
+    // the same bits), so windows across ownership boundaries match the single-GPU loss
+    CKS(ensure(ctx, ctx->loss_img, 3 * plane * 4));
+    CK(cudaMemsetAsync(ctx->loss_img.p, 0, 3 * plane * 4, s));
+    launch_owned_copy(rgb, W, H, ctx->cam.TX, ctx->t_begin, ctx->t_end, P_<float>(ctx->loss_img), s);
+    CKS(launched(ctx));
+    CKS(ctx->tr->allreduce_f32(ctx, P_<float>(ctx->loss_img), int64_t(3 * plane), s));
+    x = P_<float>(ctx->loss_img);
+  }
+  const int64_t nb = loss_n_blocks(W, H);
+  CKS(ensure(ctx, ctx->loss_part, size_t(nb) * sizeof(double2)));
+  CKS(ensure(ctx, ctx->loss_sums, 8 * sizeof(double)));
+  LossArgs a{};
+  a.x = x;
+  a.y = target;
+  a.dL = dL_drgb;
+  a.partials = P_<double2>(ctx->loss_part);
+  a.W = W;
+  a.H = H;
+  a.TX = ctx->cam.TX;
+  a.t_begin = ctx->t_begin;
+  a.t_end = ctx->t_end;
+  const double n_elem = 3.0 * double(plane);
+  a.k_l1 = float(double(batch_inv) * (1.0 - double(lambda)) / n_elem);
+  a.k_ssim = float(double(batch_inv) * double(lambda) / n_elem);
+  // normalised 1-D window, sigma 1.5 (computed in double, rounded once)
+  double gw[11], gs = 0.0;
+  for (int k = 0; k < 11; ++k) gs += (gw[k] = std::exp(-double((k - 5) * (k - 5)) / (2.0 * 1.5 * 1.5)));
+  for (int k = 0; k < 11; ++k) a.g[k] = float(gw[k] / gs);
+  launch_loss_photo(a, s);
+  CKS(launched(ctx));
+  double* sums = P_<double>(ctx->loss_sums);
+  launch_loss_sums(a.partials, int(nb), sums, s);
+  CKS(launched(ctx));
+  if (ctx->world > 1) CKS(ctx->tr->allreduce_f64(ctx, sums, 2, s));
+  launch_loss_finish(sums, n_elem, double(lambda), out, s);
+  CKS(launched(ctx));
+  return BGS_OK;
+}
+
+bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, const int32_t* radius, float beta,
+                          const bgs_gaussian_grads* grads, double* out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  CKS(check_gaussians(ctx, g));
+  if (!out || (g->n_local > 0 && (!radius || !grads || !grads->scale)))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "loss_scale pointer is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = g->n_local;
+  const int nb = scale_n_blocks(n);
+  CKS(ensure(ctx, ctx->loss_part, size_t(nb) * sizeof(double2)));
+  CKS(ensure(ctx, ctx->loss_sums, 8 * sizeof(double)));
+  double* sums = P_<double>(ctx->loss_sums) + 4;
+  launch_scale_sum(reinterpret_cast<const float4*>(g->scale), radius, n, P_<double2>(ctx->loss_part), s);
+  CKS(launched(ctx));
+  launch_loss_sums(P_<double2>(ctx->loss_part), nb, sums, s);
+  CKS(launched(ctx));
+  if (ctx->world > 1) CKS(ctx->tr->allreduce_f64(ctx, sums, 2, s));
+  launch_scale_finish(sums, out, s);
+  CKS(launched(ctx));
+  if (n > 0) {
+    launch_scale_grad(reinterpret_cast<const float4*>(g->scale), radius, n, sums, beta, grads->scale, s);
+    CKS(launched(ctx));
+  }
   return BGS_OK;
 }
 

@@ -143,6 +143,22 @@ def grad_image(H: int, W: int, seed: int = 7, sigma: float = 1e-3) -> np.ndarray
     return (rng.standard_normal((3, H, W), dtype=np.float32) * np.float32(sigma)).astype(np.float32)
 
 
+def target_image(H: int, W: int, seed: int = 9) -> np.ndarray:
+    """Ground-truth image I_b of Eq.7 for the supervision tests and bench: seeded smooth colour
+    field (a few random plane waves per channel) plus pixel noise, clipped to [0, 1], float32
+    [3,H,W].  No method arithmetic."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    yy, xx = np.mgrid[0:H, 0:W].astype(np.float64)
+    img = np.empty((3, H, W), np.float64)
+    for c in range(3):
+        f = 0.45 + np.zeros((H, W))
+        for _ in range(4):
+            kx, ky = rng.uniform(-0.08, 0.08, 2)
+            f += rng.uniform(0.05, 0.15) * np.sin(kx * xx + ky * yy + rng.uniform(0, 2 * np.pi))
+        img[c] = f + 0.05 * rng.standard_normal((H, W))
+    return np.clip(img, 0.0, 1.0).astype(np.float32)
+
+
 # ----------------------------------------------------------------------------------------
 # tiny scene (configs[0])
 # ----------------------------------------------------------------------------------------

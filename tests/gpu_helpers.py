@@ -54,7 +54,7 @@ class GpuStep:
     """One view through a1..a12 on one ctx (world 1) or an in-process group (world > 1)."""
 
     def __init__(self, scene, cam, M=1, gate=None, cull_global=None, flags=0, dLdC=None, importance=True,
-                 ctxs=None, device=0):
+                 ctxs=None, device=0, target=None, lam=0.2, batch_inv=1.0, beta=None):
         import paper_2605_13794_b200.bgs as B
         self.B = B
         self.M = M
@@ -106,6 +106,14 @@ class GpuStep:
                     out["recv"] = rec_view(recv)
                     out["recv_raw"] = recv
                     B.bgs_raster_fwd(ctx, flags | (B.BGS_IMPORTANCE if importance else 0), rgb, T, nc, stream)
+                    if target is not None:  # NEXT-4 Eq.7 on the owned tiles
+                        tgt = torch.from_numpy(np.ascontiguousarray(target, np.float32)).to(dev)
+                        dlo = torch.full((3, H, W), 7.0, device=dev)  # sentinel: non-owned pixels untouched
+                        lo = torch.full((3,), -1.0, dtype=torch.float64, device=dev)
+                        B.bgs_loss_photo(ctx, rgb, tgt, lam, batch_inv, dlo, lo, stream)
+                        stream.synchronize()
+                        out["loss"] = lo.cpu().numpy()
+                        out["dl_loss"] = dlo.cpu().numpy()
                     if dLdC is not None:
                         dl = torch.from_numpy(np.ascontiguousarray(dLdC, np.float32)).to(dev)
                         B.bgs_raster_bwd(ctx, dl, T, nc, stream)
@@ -114,6 +122,13 @@ class GpuStep:
                     grads = g.zeros_grads()
                     if dLdC is not None:
                         B.bgs_project_bwd(ctx, g, bcam, grads, stream)
+                    if beta is not None:  # NEXT-4 Eq.8
+                        sg = g.zeros_grads()
+                        so = torch.full((2,), -1.0, dtype=torch.float64, device=dev)
+                        B.bgs_loss_scale(ctx, g, radius, beta, sg, so, stream)
+                        stream.synchronize()
+                        out["loss_scale"] = so.cpu().numpy()
+                        out["g_scale_reg"] = sg.scale.cpu().numpy()
                     if importance:
                         s = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
                         crad = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
@@ -165,6 +180,10 @@ class GpuStep:
         gs = np.zeros((n, 4), np.float32)
         gsh = np.zeros((n, 48), np.float32)
         TX = (self.W + 15) // 16
+        self.dl_loss = np.full((3, self.H, self.W), np.nan, np.float32) if "dl_loss" in self.rank[0] else None
+        self.loss = [self.rank[r].get("loss") for r in range(M)]
+        self.loss_scale = [self.rank[r].get("loss_scale") for r in range(M)]
+        self.g_scale_reg = np.zeros((n, 4), np.float32) if "g_scale_reg" in self.rank[0] else None
         for r in range(M):
             o = self.rank[r]
             gids = np.arange(r, n, M)
@@ -176,6 +195,8 @@ class GpuStep:
                 self.img[:, ys, xs] = o["rgb"][:, ys, xs]
                 self.T[ys, xs] = o["T"][ys, xs]
                 self.nc[ys, xs] = o["nc"][ys, xs]
+                if self.dl_loss is not None:
+                    self.dl_loss[:, ys, xs] = o["dl_loss"][:, ys, xs]
             lid = o["rec_lidx"]
             g = lid.astype(np.int64) * M + r
             acc = o["acc_local"]
@@ -187,6 +208,8 @@ class GpuStep:
                 self.c_rad[gids] = o["c_rad"]
                 self.c_vis[gids] = o["c_vis"]
                 self.cull_bits[gids] = S.unpack_bits(o["cull"], len(gids))
+            if self.g_scale_reg is not None:
+                self.g_scale_reg[gids] = o["g_scale_reg"][:len(gids)]
             gm[gids] = o["grads"]["mean_opac"]
             gq[gids] = o["grads"]["quat"]
             gs[gids] = o["grads"]["scale"]
