@@ -361,6 +361,12 @@ def run_native(args):
     e2e_s = time.perf_counter() - t1
     e2e_views = args.steps / D.max_over_ranks(e2e_s, torch.device(dev))
 
+    # ---- NEXT-4 supervised training step: bgs_train_view_step = a1..a12 with Eq.7 (L1 + SSIM on
+    # the owned tiles, its gradient as this view's dL/dC) and Eq.8 (scale regulariser); lambda 0.2
+    # (3DGS), B = 4 views per step (batch_inv 1/4), beta 0.01 / B; one seeded target image
+    train = train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_rad, c_vis, stream, l2_flush,
+                       inflight, barrier, dev, H, W, n_local, world)
+
     # ---- scoring views/s: the a12 sweep step = NO_COLOR projection, routing,
     # sort, instrumented forward, reverse exchange of (w, a), importance; no backward
     sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -424,12 +430,16 @@ def run_native(args):
     from paper_2605_13794_b200.roofline import load_traffic, stage_rooflines
     peaks = load_peaks()
     stage_avg = stage_ms / args.steps
+    traffic = (load_traffic(os.path.join(ROOT, "profiles", "ncu_traffic.json"))
+               if args.config == "rubble" and world == 1 else None)
     roof = stage_rooflines(stage_avg, qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
                            sm_mhz=clk.get("sm_mhz"), E=E_sum / args.steps, A=A_sum / args.steps,
-                           cull=cull_cols is not None,
-                           traffic=load_traffic(os.path.join(ROOT, "profiles", "ncu_traffic.json"))
-                           if args.config == "rubble" and world == 1 else None)
+                           cull=cull_cols is not None, traffic=traffic, names=stage_names)
     dominant = max(roof, key=lambda r: r["ms"])
+    train_roof = stage_rooflines(train.pop("stages_avg"), qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
+                                 E=E_sum / args.steps, A=A_sum / args.steps, cull=cull_cols is not None,
+                                 traffic=traffic, names=stage_names)
+    train["loss_roofline"] = next((r for r in train_roof if r["stage"] == "loss"), None)
 
     result = {
         "metric": METRIC, "value": round(views_per_s, 3), "unit": "views/s", "n_gpus": world, "steps": args.steps,
@@ -456,6 +466,7 @@ def run_native(args):
                     "value": round(1000.0 / score_ms_max, 3) if score_ms_max > 0 else None, "unit": "views/s",
                     "ms_per_view": round(score_ms_max, 4)},
         "simplify": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in simplify.items()},
+        "train": train,
         "stages_ms": {n: round(float(v), 4) for n, v in zip(stage_names, stage_avg)},
         "roofline": {k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
         "roofline_kernel": dominant["stage"],
@@ -473,6 +484,90 @@ def run_native(args):
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_rad, c_vis, stream, l2_flush,
+               inflight, barrier, dev, H, W, n_local, world):
+    """NEXT-4: the supervised step (bgs_train_view_step) timed like the headline (views in flight,
+    device events, max over ranks), its stage breakdown (one view at a time, L2 flushed), and its
+    end-to-end rate through bgs_train_view_step_host_async (target image H2D, loss D2H)."""
+    import torch
+    from paper_2605_13794_b200 import dist as D
+    lam, binv, beta = 0.2, 0.25, 0.01 / 4
+    tgt = torch.from_numpy(S.target_image(H, W)).to(dev)
+    for p in per:
+        p["dl"] = torch.zeros(3, H, W, device=dev)
+        p["loss"] = torch.zeros(5, dtype=torch.float64, device=dev)
+
+    def train_on(k, v):
+        p = per[k]
+        B.bgs_train_view_step(ctxs[k], g, cams[v % len(cams)], gate,
+                              cull_cols[v % len(cams)] if cull_cols is not None else None, 0, p["radius"],
+                              B.supervision(tgt, lam, binv, beta, p["loss"]), p["rgb"], p["Tf"], p["nc"], p["dl"],
+                              grads, B.importance_out(s_imp, c_rad, c_vis, p["cull"], 99, 100), p["stream"])
+
+    for k in range(inflight):
+        with torch.cuda.stream(per[k]["stream"]):
+            for w in range(args.warmup):
+                train_on(k, w)
+    torch.cuda.synchronize()
+    barrier()
+    # stage breakdown: one view at a time, L2 flushed before each
+    stages = np.zeros(len(B.STAGES))
+    with torch.cuda.stream(stream):
+        B.bgs_set_stage_timing(ctxs[0], True)
+        for k in range(args.steps):
+            l2_flush.zero_()
+            stream.synchronize()
+            train_on(0, args.warmup + k)
+            stream.synchronize()
+            st = B.bgs_stage_times(ctxs[0])
+            stages += np.array([st[n] for n in B.STAGES])
+        B.bgs_set_stage_timing(ctxs[0], False)
+    torch.cuda.synchronize()
+    barrier()
+    # headline-style: views in flight
+    ev_start = torch.cuda.Event(enable_timing=True)
+    ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(inflight)]
+    ev_start.record(per[0]["stream"])
+    for k in range(1, inflight):
+        per[k]["stream"].wait_event(ev_start)
+    for k in range(args.steps):
+        train_on(k % inflight, args.warmup + k)
+    for k in range(inflight):
+        ev_end[k].record(per[k]["stream"])
+    torch.cuda.synchronize()
+    ms = D.max_over_ranks(max(ev_start.elapsed_time(e) for e in ev_end), torch.device(dev)) / args.steps
+    loss = per[0]["loss"].cpu().tolist()
+    barrier()
+    # end to end: every view's target uploaded from pinned memory, its loss read back
+    tgt_h = [torch.from_numpy(S.target_image(H, W, seed=9 + k)).pin_memory() for k in range(inflight)]
+    loss_h = [torch.zeros(5, dtype=torch.float64).pin_memory() for _ in range(inflight)]
+
+    def host_on(k, v):
+        p = per[k]
+        B.bgs_train_view_step_host_async(ctxs[k], g, cams[v % len(cams)], gate,
+                                         cull_cols[v % len(cams)] if cull_cols is not None else None, 0,
+                                         p["radius"], tgt_h[k], lam, binv, beta, loss_h[k], grads,
+                                         B.importance_out(s_imp, c_rad, c_vis, p["cull"], 99, 100), p["stream"])
+
+    for k in range(inflight):
+        host_on(k, k)
+    torch.cuda.synchronize()
+    barrier()
+    t1 = time.perf_counter()
+    for k in range(args.steps):
+        host_on(k % inflight, args.warmup + k)
+    torch.cuda.synchronize()
+    e2e = args.steps / D.max_over_ranks(time.perf_counter() - t1, torch.device(dev))
+    return {"metric": "supervised training views/s (a1-a12 + Eq.7 L1+SSIM on owned tiles + Eq.8, NEXT-4)",
+            "value": round(1000.0 / ms, 3), "unit": "views/s", "ms_per_view": round(ms, 4),
+            "lambda": lam, "batch_inv": binv, "beta": beta,
+            "stages_ms": {n: round(float(v) / args.steps, 4) for n, v in zip(B.STAGES, stages)},
+            "stages_avg": stages / args.steps,
+            "loss_last_view": {"l": loss[0], "L1": loss[1], "SSIM": loss[2], "L_scale": loss[3], "V": loss[4]},
+            "e2e": {"value": round(e2e, 3), "unit": "views/s", "h2d_bytes_per_step": int(3 * H * W * 4),
+                    "d2h_bytes_per_step": 40}}
 
 
 def load_peaks():

@@ -241,10 +241,11 @@ bgs_status bgs_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const 
                                     const bgs_gaussian_grads* grads, const bgs_importance_out* importance,
                                     void* stream);
 
-/* Per-stage device timing of bgs_view_step: when enabled, CUDA events are recorded on the
- * working stream between its stages; bgs_stage_times waits for the last one and writes the
- * elapsed ms of the most recent step: [project, route, sort, raster_fwd, raster_bwd,
- * route_reverse, project_bwd, importance] (ms_out host f32 [8]). */
+/* Per-stage device timing of bgs_view_step / bgs_train_view_step: when enabled, CUDA events are
+ * recorded on the working stream between its stages; bgs_stage_times waits for the last one and
+ * writes the elapsed ms of the most recent step: [project, route, sort, raster_fwd, loss,
+ * raster_bwd, route_reverse, project_bwd, importance] (ms_out host f32 [9]; loss is ~0 without
+ * supervision). */
 bgs_status bgs_set_stage_timing(bgs_ctx* ctx, int32_t enable);
 bgs_status bgs_stage_times(bgs_ctx* ctx, float* ms_out);
 
@@ -324,12 +325,42 @@ bgs_status bgs_loss_photo(bgs_ctx* ctx, const float* rgb, const float* target, f
                           float* dL_drgb, double* out, void* stream);
 
 /* Eq.8 scale regulariser of one view: L_scale = (1/|V|) sum_{i in V} min_j s_ij,
- * V = Gaussians with radius > 0 in this view over ALL ranks (radius from bgs_project);
- * grads->scale[i][argmin_j s_ij] += beta / |V| for the visible local Gaussians (first axis
- * among equal minima, R35; beta includes the caller's 1/B).  out: device f64 [2], overwritten
- * with {L_scale, |V|}; |V| = 0 gives L_scale = 0 and no gradient. */
-bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, const int32_t* radius, float beta,
-                          const bgs_gaussian_grads* grads, double* out, void* stream);
+ * V = the Gaussians with radius > 0 in the view last projected on this ctx (bgs_project's
+ * records), over ALL ranks; grads->scale[i][argmin_j s_ij] += beta / |V| for the visible local
+ * Gaussians (first axis among equal minima, R35; beta includes the caller's 1/B).  g: the shard
+ * that view was projected from.  out: device f64 [2], overwritten with {L_scale, |V|}; |V| = 0
+ * gives L_scale = 0 and no gradient. */
+bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, float beta, const bgs_gaussian_grads* grads,
+                          double* out, void* stream);
+
+/* a1..a12 with supervision (NEXT-4): after the forward, Eq.7 on the owned tiles writes
+ * this view's dL/dC into dL_scratch (device f32 [3][H][W]) and Eq.8 adds to grads->scale
+ * (beta != 0; needs grads); the backward then runs on that dL/dC. */
+typedef struct {
+  const float* target;  /* device f32 [3][H][W], the view's ground-truth image I_b */
+  float lambda;         /* Eq.7 blend, [0, 1] */
+  float batch_inv;      /* 1/B of Eq.7 */
+  float beta;           /* Eq.8 weight including the caller's 1/B; 0 skips Eq.8 */
+  double* loss_out;     /* device f64 [5], overwritten: {l_v, L1_v, SSIM_v, L_scale, |V|} */
+} bgs_supervision;
+
+bgs_status bgs_train_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                               const uint32_t* cull_column, uint32_t flags, int32_t* radius_out,
+                               const bgs_supervision* sup, float* rgb, float* t_final, int32_t* n_contrib,
+                               float* dL_scratch, const bgs_gaussian_grads* grads, const bgs_importance_out* importance,
+                               void* stream);
+
+/* The same step from host buffers, asynchronous like bgs_view_step_host_async: target_host
+ * (f32 [3][H][W], pinned for overlap) is uploaded on a ctx-owned copy stream that the loss waits
+ * for; the five loss values (as loss_out above) are downloaded to loss_host (f64 [5], pinned)
+ * as soon as the loss is final, overlapping the backward.  A later sync of `stream` covers
+ * loss_host. */
+bgs_status bgs_train_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                                          const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                                          int32_t* radius_out, const float* target_host, float lambda,
+                                          float batch_inv, float beta, double* loss_host,
+                                          const bgs_gaussian_grads* grads, const bgs_importance_out* importance,
+                                          void* stream);
 
 #ifdef __cplusplus
 }

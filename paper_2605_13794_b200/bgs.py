@@ -97,7 +97,10 @@ _SIGS = {
     "bgs_prune_mass_cut": [_vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp],
     "bgs_redistribute": [_vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_loss_photo": [_vp, _vp, _vp, C.c_float, C.c_float, _vp, _vp, _vp],
-    "bgs_loss_scale": [_vp, _vp, _vp, C.c_float, _vp, _vp, _vp],
+    "bgs_loss_scale": [_vp, _vp, C.c_float, _vp, _vp, _vp],
+    "bgs_train_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_train_view_step_host_async": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, C.c_float, C.c_float, C.c_float,
+                                       _vp, _vp, _vp, _vp],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -337,12 +340,49 @@ def bgs_loss_photo(ctx: Context, rgb, target, lam: float, batch_inv: float, dL_d
                                   _ptr(out), _stream(stream)), "bgs_loss_photo")
 
 
-def bgs_loss_scale(ctx: Context, g: GaussianPlanes, radius, beta: float, grads: GradPlanes, out, stream=None):
+def bgs_loss_scale(ctx: Context, g: GaussianPlanes, beta: float, grads: GradPlanes, out, stream=None):
     """NEXT-4, Eq.8: out (device f64[2]) = {L_scale, |V|}; grads.scale += beta/|V| on argmin axes."""
     gs = g.struct()
     gr = grads.struct()
-    ctx.check(_lib.bgs_loss_scale(ctx.handle, C.byref(gs), _ptr(radius), float(beta), C.byref(gr), _ptr(out),
+    ctx.check(_lib.bgs_loss_scale(ctx.handle, C.byref(gs), float(beta), C.byref(gr), _ptr(out),
                                   _stream(stream)), "bgs_loss_scale")
+
+
+class bgs_supervision(C.Structure):
+    _fields_ = [("target", C.c_void_p), ("lam", C.c_float), ("batch_inv", C.c_float), ("beta", C.c_float),
+                ("loss_out", C.c_void_p)]
+
+
+def supervision(target, lam: float, batch_inv: float, beta: float, loss_out) -> bgs_supervision:
+    return bgs_supervision(_ptr(target), float(lam), float(batch_inv), float(beta), _ptr(loss_out))
+
+
+def bgs_train_view_step(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags, radius_out,
+                        sup: bgs_supervision, rgb, t_final, n_contrib, dL_scratch, grads: GradPlanes | None,
+                        importance: bgs_importance_out | None, stream=None):
+    gs = g.struct()
+    gr = grads.struct() if grads is not None else None
+    ctx.check(_lib.bgs_train_view_step(ctx.handle, C.byref(gs), C.byref(cam),
+                                       C.byref(gate) if gate is not None else None, _ptr(cull_column), flags,
+                                       _ptr(radius_out), C.byref(sup), _ptr(rgb), _ptr(t_final), _ptr(n_contrib),
+                                       _ptr(dL_scratch), C.byref(gr) if gr is not None else None,
+                                       C.byref(importance) if importance is not None else None, _stream(stream)),
+              "bgs_train_view_step")
+
+
+def bgs_train_view_step_host_async(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags,
+                                   radius_out, target_host, lam: float, batch_inv: float, beta: float, loss_host,
+                                   grads: GradPlanes | None, importance: bgs_importance_out | None, stream=None):
+    gs = g.struct()
+    gr = grads.struct() if grads is not None else None
+    ctx.check(_lib.bgs_train_view_step_host_async(ctx.handle, C.byref(gs), C.byref(cam),
+                                                  C.byref(gate) if gate is not None else None, _ptr(cull_column),
+                                                  flags, _ptr(radius_out), _ptr(target_host), float(lam),
+                                                  float(batch_inv), float(beta), _ptr(loss_host),
+                                                  C.byref(gr) if gr is not None else None,
+                                                  C.byref(importance) if importance is not None else None,
+                                                  _stream(stream)),
+              "bgs_train_view_step_host_async")
 
 
 def bgs_view_step(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags, radius_out, rgb, t_final,
@@ -422,12 +462,13 @@ def bgs_set_stage_timing(ctx: Context, enable: bool):
     ctx.check(_lib.bgs_set_stage_timing(ctx.handle, int(bool(enable))), "bgs_set_stage_timing")
 
 
-STAGES = ("project", "route", "sort", "raster_fwd", "raster_bwd", "route_reverse", "project_bwd", "importance")
+STAGES = ("project", "route", "sort", "raster_fwd", "loss", "raster_bwd", "route_reverse", "project_bwd",
+          "importance")
 
 
 def bgs_stage_times(ctx: Context) -> dict:
     """Device ms per stage of the most recent bgs_view_step (stage timing enabled)."""
-    out = (C.c_float * 8)()
+    out = (C.c_float * len(STAGES))()
     ctx.check(_lib.bgs_stage_times(ctx.handle, out), "bgs_stage_times")
     return dict(zip(STAGES, [float(x) for x in out]))
 

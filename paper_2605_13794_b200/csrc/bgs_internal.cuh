@@ -291,9 +291,9 @@ void launch_loss_sums(const double2* partials, int n, double* sums, cudaStream_t
 void launch_loss_finish(const double* sums, double n_elem, double lambda, double* out, cudaStream_t s);
 void launch_owned_copy(const float* rgb, int W, int H, int TX, int t_begin, int t_end, float* full, cudaStream_t s);
 int scale_n_blocks(int64_t n);
-void launch_scale_sum(const float4* scale, const int32_t* radius, int64_t n, double2* partials, cudaStream_t s);
+void launch_scale_sum(const float4* scale, const uint32_t* lidx, int64_t n, double2* partials, cudaStream_t s);
 void launch_scale_finish(const double* sums, double* out, cudaStream_t s);
-void launch_scale_grad(const float4* scale, const int32_t* radius, int64_t n, const double* sums, float beta,
+void launch_scale_grad(const float4* scale, const uint32_t* lidx, int64_t n, const double* sums, float beta,
                        float* g_scale, cudaStream_t s);
 
 }  // namespace bgs

@@ -30,6 +30,10 @@ struct Transport;
 
 }  // namespace
 
+// bgs_stage_times: project, route, sort, raster_fwd, loss, raster_bwd, route_reverse, project_bwd,
+// importance
+constexpr int kStages = 9;
+
 struct bgs_ctx {
   int rank = 0, world = 1, device = 0;
   std::shared_ptr<Transport> tr;
@@ -49,7 +53,7 @@ struct bgs_ctx {
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
       imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask,
-      loss_img, loss_part, loss_sums;
+      loss_img, loss_part, loss_sums, scr_tgt, scr_loss;
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
@@ -60,7 +64,7 @@ struct bgs_ctx {
   bool stage_timing = false, stage_recorded = false;  // bgs_set_stage_timing / bgs_stage_times
   cudaStream_t h2d = nullptr, d2h = nullptr;          // host-buffer step: copy streams
   cudaEvent_t ev_in = nullptr, ev_dl = nullptr, ev_fwd = nullptr, ev_out = nullptr;
-  cudaEvent_t stage_ev[9] = {};
+  cudaEvent_t stage_ev[kStages + 1] = {};
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
 };
 
@@ -424,7 +428,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -1002,11 +1006,23 @@ bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, ui
 
 // dl_ready: event the compositing backward waits for (dL/dC still arriving); fwd_done: event
 // recorded once the image is final (the host path copies it out while the backward runs)
+// the host-buffer steps' copy streams and events (created on first use)
+static bgs_status copy_streams(bgs_ctx* ctx) {
+  if (!ctx->h2d) {
+    CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ctx->ev_in, &ctx->ev_dl, &ctx->ev_fwd, &ctx->ev_out})
+      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  return BGS_OK;
+}
+
 static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
                                  const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
                                  int32_t* radius_out, float* rgb, float* t_final, int32_t* n_contrib, const float* dL,
                                  const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream,
-                                 cudaEvent_t dl_ready, cudaEvent_t fwd_done) {
+                                 cudaEvent_t dl_ready, cudaEvent_t fwd_done, const bgs_supervision* sup = nullptr,
+                                 float* dL_sup = nullptr, cudaEvent_t loss_done = nullptr) {
   if (imp) flags |= BGS_IMPORTANCE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // stage boundaries (bgs_stage_times): events on the working stream, recorded only when enabled
@@ -1026,17 +1042,25 @@ static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs
   CKS(bgs_raster_fwd(ctx, flags, rgb, t_final, n_contrib, stream));
   if (fwd_done) CK(cudaEventRecord(fwd_done, s));
   CKS(mark(4));
-  if (dl_ready) CK(cudaStreamWaitEvent(s, dl_ready, 0));
-  if (dL) CKS(bgs_raster_bwd(ctx, dL, t_final, n_contrib, stream));
+  if (dl_ready) CK(cudaStreamWaitEvent(s, dl_ready, 0));  // dL/dC (or the target image) uploaded
+  if (sup) {
+    // NEXT-4: Eq.7 on the owned tiles gives this view's dL/dC; Eq.8 adds to the scale gradient
+    CKS(bgs_loss_photo(ctx, rgb, sup->target, sup->lambda, sup->batch_inv, dL_sup, sup->loss_out, stream));
+    if (sup->beta != 0.f) CKS(bgs_loss_scale(ctx, g, sup->beta, grads, sup->loss_out + 3, stream));
+    if (loss_done) CK(cudaEventRecord(loss_done, s));
+    dL = dL_sup;
+  }
   CKS(mark(5));
-  CKS(bgs_route_reverse(ctx, stream));
+  if (dL) CKS(bgs_raster_bwd(ctx, dL, t_final, n_contrib, stream));
   CKS(mark(6));
-  if (dL && grads) CKS(bgs_project_bwd(ctx, g, cam, grads, stream));
+  CKS(bgs_route_reverse(ctx, stream));
   CKS(mark(7));
+  if (dL && grads) CKS(bgs_project_bwd(ctx, g, cam, grads, stream));
+  CKS(mark(8));
   if (imp)
     CKS(bgs_importance(ctx, g->n_local, radius_out, nullptr, nullptr, imp->mass_num, imp->mass_den, imp->s,
                        imp->c_rad, imp->c_vis, imp->cull_out, stream));
-  CKS(mark(8));
+  CKS(mark(9));
   ctx->stage_recorded = ctx->stage_timing;
   return BGS_OK;
 }
@@ -1047,6 +1071,61 @@ bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera*
                          const bgs_importance_out* imp, void* stream) {
   return view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, rgb, t_final, n_contrib, dL, grads, imp,
                         stream, nullptr, nullptr);
+}
+
+static bgs_status check_sup(bgs_ctx* ctx, const bgs_supervision* sup, bool need_target) {
+  if (!sup) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "supervision is NULL");
+  if ((need_target && !sup->target) || !sup->loss_out)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "supervision target / loss_out is NULL");
+  return BGS_OK;
+}
+
+bgs_status bgs_train_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                               const uint32_t* cull_column, uint32_t flags, int32_t* radius_out,
+                               const bgs_supervision* sup, float* rgb, float* t_final, int32_t* n_contrib,
+                               float* dL_scratch, const bgs_gaussian_grads* grads, const bgs_importance_out* imp,
+                               void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_sup(ctx, sup, true));
+  if (!dL_scratch) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "dL_scratch is NULL");
+  return view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, rgb, t_final, n_contrib, nullptr, grads,
+                        imp, stream, nullptr, nullptr, sup, dL_scratch, nullptr);
+}
+
+bgs_status bgs_train_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                                          const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                                          int32_t* radius_out, const float* target_host, float lambda,
+                                          float batch_inv, float beta, double* loss_host,
+                                          const bgs_gaussian_grads* grads, const bgs_importance_out* imp,
+                                          void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  CKS(set_camera(ctx, cam));
+  if (!target_host || !loss_host) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "host target / loss pointer is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t npix = size_t(ctx->cam.W) * ctx->cam.H;
+  CKS(ensure(ctx, ctx->scr_rgb, npix * 12));
+  CKS(ensure(ctx, ctx->scr_dl, npix * 12));
+  CKS(ensure(ctx, ctx->scr_tgt, npix * 12));
+  CKS(ensure(ctx, ctx->scr_t, npix * 4));
+  CKS(ensure(ctx, ctx->scr_n, npix * 4));
+  CKS(ensure(ctx, ctx->scr_loss, 8 * sizeof(double)));
+  CKS(copy_streams(ctx));
+  // target upload on its own copy engine (needed only by the loss, after the forward); the loss
+  // download starts as soon as the loss is final, overlapping the backward
+  CK(cudaEventRecord(ctx->ev_in, s));
+  CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_in, 0));
+  CK(cudaMemcpyAsync(ctx->scr_tgt.p, target_host, npix * 12, cudaMemcpyHostToDevice, ctx->h2d));
+  CK(cudaEventRecord(ctx->ev_dl, ctx->h2d));
+  bgs_supervision sup{P_<float>(ctx->scr_tgt), lambda, batch_inv, beta, P_<double>(ctx->scr_loss)};
+  CKS(view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
+                     P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), nullptr, grads, imp, stream, ctx->ev_dl,
+                     nullptr, &sup, P_<float>(ctx->scr_dl), ctx->ev_fwd));
+  CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_fwd, 0));
+  CK(cudaMemcpyAsync(loss_host, ctx->scr_loss.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h));
+  CK(cudaEventRecord(ctx->ev_out, ctx->d2h));
+  CK(cudaStreamWaitEvent(s, ctx->ev_out, 0));
+  return BGS_OK;
 }
 
 bgs_status bgs_set_stage_timing(bgs_ctx* ctx, int32_t enable) {
@@ -1060,8 +1139,8 @@ bgs_status bgs_stage_times(bgs_ctx* ctx, float* ms_out) {
   CKS(check_ctx(ctx));
   if (!ms_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_stage_times: ms_out is NULL");
   if (!ctx->stage_recorded) return fail(ctx, BGS_ERR_CONTRACT, "no bgs_view_step with stage timing enabled");
-  CK(cudaEventSynchronize(ctx->stage_ev[8]));
-  for (int k = 0; k < 8; ++k) CK(cudaEventElapsedTime(ms_out + k, ctx->stage_ev[k], ctx->stage_ev[k + 1]));
+  CK(cudaEventSynchronize(ctx->stage_ev[kStages]));
+  for (int k = 0; k < kStages; ++k) CK(cudaEventElapsedTime(ms_out + k, ctx->stage_ev[k], ctx->stage_ev[k + 1]));
   return BGS_OK;
 }
 
@@ -1079,12 +1158,7 @@ bgs_status bgs_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const 
   CKS(ensure(ctx, ctx->scr_dl, npix * 12));
   CKS(ensure(ctx, ctx->scr_t, npix * 4));
   CKS(ensure(ctx, ctx->scr_n, npix * 4));
-  if (!ctx->h2d) {
-    CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ctx->ev_in, &ctx->ev_dl, &ctx->ev_fwd, &ctx->ev_out})
-      CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  }
+  CKS(copy_streams(ctx));
   // dL/dC upload on its own copy engine, needed only by the compositing backward; it starts once
   // this ctx's previous step no longer reads the scratch (everything queued on s so far)
   CK(cudaEventRecord(ctx->ev_in, s));
@@ -1168,28 +1242,29 @@ bgs_status bgs_loss_photo(bgs_ctx* ctx, const float* rgb, const float* target, f
   return BGS_OK;
 }
 
-bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, const int32_t* radius, float beta,
-                          const bgs_gaussian_grads* grads, double* out, void* stream) {
+bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, float beta, const bgs_gaussian_grads* grads,
+                          double* out, void* stream) {
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   CKS(check_gaussians(ctx, g));
-  if (!out || (g->n_local > 0 && (!radius || !grads || !grads->scale)))
-    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "loss_scale pointer is NULL");
+  if (ctx->stage < 1) return fail(ctx, BGS_ERR_CONTRACT, "bgs_loss_scale before bgs_project");
+  if (!out || !grads || !grads->scale) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "loss_scale pointer is NULL");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t n = g->n_local;
-  const int nb = scale_n_blocks(n);
+  const int64_t F = ctx->F;  // this view's records = the local visible set (radius > 0)
+  const uint32_t* lidx = P_<uint32_t>(ctx->rec_lidx);
+  const int nb = scale_n_blocks(F);
   CKS(ensure(ctx, ctx->loss_part, size_t(nb) * sizeof(double2)));
   CKS(ensure(ctx, ctx->loss_sums, 8 * sizeof(double)));
   double* sums = P_<double>(ctx->loss_sums) + 4;
-  launch_scale_sum(reinterpret_cast<const float4*>(g->scale), radius, n, P_<double2>(ctx->loss_part), s);
+  launch_scale_sum(reinterpret_cast<const float4*>(g->scale), lidx, F, P_<double2>(ctx->loss_part), s);
   CKS(launched(ctx));
   launch_loss_sums(P_<double2>(ctx->loss_part), nb, sums, s);
   CKS(launched(ctx));
   if (ctx->world > 1) CKS(ctx->tr->allreduce_f64(ctx, sums, 2, s));
   launch_scale_finish(sums, out, s);
   CKS(launched(ctx));
-  if (n > 0) {
-    launch_scale_grad(reinterpret_cast<const float4*>(g->scale), radius, n, sums, beta, grads->scale, s);
+  if (F > 0) {
+    launch_scale_grad(reinterpret_cast<const float4*>(g->scale), lidx, F, sums, beta, grads->scale, s);
     CKS(launched(ctx));
   }
   return BGS_OK;

@@ -23,6 +23,10 @@ These are what the METHOD must move or compute, not what a kernel happens to do:
   a10 reverse (M>1)  48 D (send back) + 48 D (gather)                                     [bytes]
   a11 project bwd    240 F (params) + 52 F (partials + index) + 2 x 236 F (grads RMW)     [bytes]
   a12 importance     52 F (w, a, index) + 2 x 16 F (s, c_rad, c_vis RMW) + N/8 (Cull)    [bytes]
+  NEXT-4 loss        213 FP32 ops per image element (3 H W): window statistics 3 products +
+                     5 maps x 2 separable 11-tap passes = 113, SSIM and its partials 25,
+                     3 partial maps x 2 passes = 66, dS, L1 sign, sums 9 (the 5 px halo a
+                     32x32 tile recomputes is not counted)                                [ALU]
 Peaks: HBM = MEASURED_PEAKS.json hbm_gbs (copy bandwidth); ALU = 148 SMs x 128 FP32 lanes x
 sm_max clock (one FP32 instruction per lane per clock; FFMA counted as one op).
 """
@@ -30,6 +34,7 @@ from __future__ import annotations
 
 FWD_OPS = 19.0
 BWD_OPS = 33.0
+LOSS_OPS = 213.0
 
 
 def _avg(qs, k):
@@ -37,15 +42,17 @@ def _avg(qs, k):
 
 
 def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=None, cull=False, traffic=None,
-                    A=None):
+                    A=None, names=None):
     """traffic: optional {stage: DRAM bytes per view} from a committed ncu capture (profiles/)."""
     traffic = traffic or {}
     N = float(n_local)
+    A_contrib = A  # contributing (pixel, splat) pairs
     A, F, R, D, P = (_avg(qs, k) for k in ("n_active", "F", "R", "D", "P"))
     passes = _avg(qs, "sort_passes")
     hbm = float(peaks["hbm_gbs"])
     alu = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12  # T ops/s
-    names = ("project", "route", "sort", "raster_fwd", "raster_bwd", "route_reverse", "project_bwd", "importance")
+    names = names or ("project", "route", "sort", "raster_fwd", "loss", "raster_bwd", "route_reverse", "project_bwd",
+                      "importance")
     bytes_ = {
         "project": 16 * N + N + (N / 8 if cull else 0) + 32 * A + 192 * F + 52 * F + 4 * N,
         "route": (48 * D + 48 * R) if world > 1 else 0.0,
@@ -55,13 +62,21 @@ def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=No
         "importance": 52 * F + 32 * F + N / 8,
     }
     E = float(E) if E is not None else 0.0
-    A = float(A) if A is not None else E
+    Ac = float(A_contrib) if A_contrib is not None else E
     ops = {"raster_fwd": FWD_OPS * E, "raster_bwd": BWD_OPS * E}
-    ops_a = {"raster_fwd": FWD_OPS * A, "raster_bwd": BWD_OPS * A}
+    ops_a = {"raster_fwd": FWD_OPS * Ac, "raster_bwd": BWD_OPS * Ac}
     out = []
     for name, ms in zip(names, stage_ms):
         ms = float(ms)
-        if name in ops:
+        if name == "loss":
+            if ms <= 0:
+                continue  # no supervision in this step
+            o = LOSS_OPS * 3.0 * W * H
+            ach = o / (ms * 1e-3) / 1e12
+            out.append(dict(stage=name, ms=round(ms, 4), bound="alu", achieved=round(ach, 3), peak=round(alu, 2),
+                            unit="TFLOP/s", frac=round(ach / alu, 4), traffic=traffic.get(name),
+                            work=f"{o:.3e} ops ({LOSS_OPS:.0f} x 3 H W)"))
+        elif name in ops:
             ach = ops[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
             ach_a = ops_a[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
             k = FWD_OPS if name == "raster_fwd" else BWD_OPS

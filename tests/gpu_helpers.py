@@ -125,7 +125,7 @@ class GpuStep:
                     if beta is not None:  # NEXT-4 Eq.8
                         sg = g.zeros_grads()
                         so = torch.full((2,), -1.0, dtype=torch.float64, device=dev)
-                        B.bgs_loss_scale(ctx, g, radius, beta, sg, so, stream)
+                        B.bgs_loss_scale(ctx, g, beta, sg, so, stream)
                         stream.synchronize()
                         out["loss_scale"] = so.cpu().numpy()
                         out["g_scale_reg"] = sg.scale.cpu().numpy()
