@@ -16,6 +16,7 @@
  *   bgs_importance     a12 Eq.3 score, c^rad, c^vis top-99% mass, Cull column
  *   bgs_loss_photo     NEXT-4 Eq.7 L1 + SSIM on the owned tiles with its gradient
  *   bgs_loss_scale     NEXT-4 Eq.8 scale regulariser over the visible set
+ *   bgs_adam_step      NEXT-3 fused activation-chain-rule + Adam step on the owned shard
  * bgs_view_step / bgs_view_step_host run a1..a11 (+a12 when requested) in one call.
  *
  * Conventions (all entry points):
@@ -361,6 +362,44 @@ bgs_status bgs_train_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, 
                                           float batch_inv, float beta, double* loss_host,
                                           const bgs_gaussian_grads* grads, const bgs_importance_out* importance,
                                           void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3: optimizer step on the owned shard ("each GPU stores only its
+ * local shard and its optimizer state")
+ * --------------------------------------------------------------------------------------- */
+/* RAW (pre-activation) parameters of the local shard and their Adam moments, device, n_local
+ * rows each, layouts as bgs_gaussians: mean_logit float4 (mu_x, mu_y, mu_z, opacity logit),
+ * quat_raw float4 (w, x, y, z, any non-zero norm), log_scale float4 (log s_x, log s_y, log s_z, 0),
+ * sh [n][48].  m[k] / v[k]: first / second moments of plane k (0 mean_logit, 1 quat_raw,
+ * 2 log_scale, 3 sh), same layouts. */
+typedef struct {
+  int64_t n_local;
+  float* mean_logit;
+  float* quat_raw;
+  float* log_scale;
+  float* sh;
+  float* m[4];
+  float* v[4];
+} bgs_train_params;
+
+/* Adam hyper-parameters (reading R38: the 3DGS parameter groups; values are the caller's).
+ * step = t >= 1 (bias corrections 1 - beta^t). */
+typedef struct {
+  float lr_mean, lr_opacity, lr_quat, lr_scale, lr_sh_dc, lr_sh_rest;
+  double beta1, beta2, eps;  /* double: 1 - beta and the bias corrections are formed on the host */
+  int32_t step;
+} bgs_adam_hparams;
+
+/* One fused optimizer step over the shard: grads (w.r.t. the ACTIVATED parameters, as the view
+ * steps accumulate them) -> chain rule through opacity = sigmoid(logit), s = exp(log s),
+ * q = q_raw/|q_raw| (mean and SH identity) -> Adam m, v, bias-corrected update of the raw
+ * parameters -> activated planes written to act (mean_opac, quat, scale; act->sh may equal
+ * p->sh, else the SH rows are copied; act->lod untouched) -> grads ZEROED for the next step.
+ * visible: nullable device u32[ceil(n/32)] bit mask; rows with bit 0 are not read or written
+ * (selective Adam); NULL updates every row (standard Adam). */
+bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaussian_grads* grads,
+                         const bgs_gaussians_out* act, const uint32_t* visible, const bgs_adam_hparams* h,
+                         void* stream);
 
 #ifdef __cplusplus
 }

@@ -99,6 +99,7 @@ _SIGS = {
     "bgs_loss_photo": [_vp, _vp, _vp, C.c_float, C.c_float, _vp, _vp, _vp],
     "bgs_loss_scale": [_vp, _vp, C.c_float, _vp, _vp, _vp],
     "bgs_train_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_adam_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_train_view_step_host_async": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, C.c_float, C.c_float, C.c_float,
                                        _vp, _vp, _vp, _vp],
 }
@@ -346,6 +347,57 @@ def bgs_loss_scale(ctx: Context, g: GaussianPlanes, beta: float, grads: GradPlan
     gr = grads.struct()
     ctx.check(_lib.bgs_loss_scale(ctx.handle, C.byref(gs), float(beta), C.byref(gr), _ptr(out),
                                   _stream(stream)), "bgs_loss_scale")
+
+
+class bgs_train_params(C.Structure):
+    _fields_ = [("n_local", C.c_int64), ("mean_logit", C.c_void_p), ("quat_raw", C.c_void_p),
+                ("log_scale", C.c_void_p), ("sh", C.c_void_p), ("m", C.c_void_p * 4), ("v", C.c_void_p * 4)]
+
+
+class bgs_adam_hparams(C.Structure):
+    _fields_ = [("lr_mean", C.c_float), ("lr_opacity", C.c_float), ("lr_quat", C.c_float), ("lr_scale", C.c_float),
+                ("lr_sh_dc", C.c_float), ("lr_sh_rest", C.c_float), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("step", C.c_int32)]
+
+
+class TrainParams:
+    """Raw parameters of a shard + Adam moments (bgs_train_params), torch device tensors."""
+
+    def __init__(self, mean_logit, quat_raw, log_scale, sh):
+        self.mean_logit, self.quat_raw, self.log_scale, self.sh = mean_logit, quat_raw, log_scale, sh
+        self.m = [torch.zeros_like(t) for t in (mean_logit, quat_raw, log_scale, sh)]
+        self.v = [torch.zeros_like(t) for t in (mean_logit, quat_raw, log_scale, sh)]
+
+    @property
+    def n(self) -> int:
+        return int(self.mean_logit.shape[0])
+
+    def struct(self) -> bgs_train_params:
+        s = bgs_train_params()
+        s.n_local = self.n
+        s.mean_logit, s.quat_raw = self.mean_logit.data_ptr(), self.quat_raw.data_ptr()
+        s.log_scale, s.sh = self.log_scale.data_ptr(), self.sh.data_ptr()
+        for k in range(4):
+            s.m[k] = self.m[k].data_ptr()
+            s.v[k] = self.v[k].data_ptr()
+        return s
+
+
+def adam_hparams(lr_mean=1.6e-4, lr_opacity=0.05, lr_quat=1e-3, lr_scale=5e-3, lr_sh_dc=2.5e-3,
+                 lr_sh_rest=2.5e-3 / 20, beta1=0.9, beta2=0.999, eps=1e-15, step=1) -> bgs_adam_hparams:
+    """Defaults: the 3DGS parameter groups (reading R38)."""
+    return bgs_adam_hparams(lr_mean, lr_opacity, lr_quat, lr_scale, lr_sh_dc, lr_sh_rest, beta1, beta2, eps, step)
+
+
+def bgs_adam_step(ctx: Context, p: TrainParams, grads: GradPlanes, act: GaussianPlanes, visible,
+                  h: bgs_adam_hparams, stream=None):
+    """NEXT-3: fused activation chain rule + Adam; writes act (activated planes), zeroes grads."""
+    ps = p.struct()
+    gr = grads.struct()
+    ao = bgs_gaussians_out(act.mean_opac.shape[0], act.mean_opac.data_ptr(), act.quat.data_ptr(),
+                           act.scale.data_ptr(), act.sh.data_ptr(), act.lod.data_ptr())
+    ctx.check(_lib.bgs_adam_step(ctx.handle, C.byref(ps), C.byref(gr), C.byref(ao), _ptr(visible), C.byref(h),
+                                 _stream(stream)), "bgs_adam_step")
 
 
 class bgs_supervision(C.Structure):

@@ -296,4 +296,19 @@ void launch_scale_finish(const double* sums, double* out, cudaStream_t s);
 void launch_scale_grad(const float4* scale, const uint32_t* lidx, int64_t n, const double* sums, float beta,
                        float* g_scale, cudaStream_t s);
 
+// NEXT-3 fused Adam on the owned shard (adam.cu)
+struct AdamArgs {
+  int64_t n;
+  float4* p[3];        // raw: (mu, opacity logit), q_raw, (log s, 0)
+  float4* m[3];
+  float4* v[3];
+  float4* g[3];        // gradients w.r.t. the ACTIVATED parameters; zeroed after the step
+  float4* act[3];      // activated planes written: (mu, sigmoid), q / |q|, (exp(log s), 0)
+  float *sh_p, *sh_m, *sh_v, *sh_g, *sh_act;  // [n][48]; sh_act may equal sh_p (then not written)
+  const uint32_t* visible;  // nullable bit mask: rows with bit 0 are not touched
+  float lr_mean, lr_opacity, lr_quat, lr_scale, lr_sh_dc, lr_sh_rest;
+  float b1, b2, om1, om2, eps, c1, c2;  // om = 1 - b (double on the host), c1 = 1/(1 - b1^t), c2 = 1/(1 - b2^t)
+};
+void launch_adam(const AdamArgs& a, cudaStream_t s);
+
 }  // namespace bgs

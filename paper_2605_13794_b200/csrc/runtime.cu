@@ -1270,6 +1270,62 @@ bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, float beta, cons
   return BGS_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// NEXT-3: fused Adam on the owned shard (adam.cu)
+// ---------------------------------------------------------------------------------------
+bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaussian_grads* grads,
+                         const bgs_gaussians_out* act, const uint32_t* visible, const bgs_adam_hparams* h,
+                         void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (!p || !grads || !act || !h) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "adam: NULL argument");
+  if (p->n_local < 0) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "adam: n_local < 0");
+  if (h->step < 1) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "adam: step must be >= 1");
+  if (!(h->beta1 >= 0.0 && h->beta1 < 1.0 && h->beta2 >= 0.0 && h->beta2 < 1.0))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "adam: betas outside [0, 1)");
+  if (p->n_local == 0) return BGS_OK;
+  if (act->capacity < p->n_local) return fail(ctx, BGS_ERR_CAPACITY, "adam: act capacity < n_local");
+  const float* planes[] = {p->mean_logit, p->quat_raw, p->log_scale, p->sh, p->m[0], p->m[1], p->m[2], p->m[3],
+                           p->v[0], p->v[1], p->v[2], p->v[3], grads->mean_opac, grads->quat, grads->scale,
+                           grads->sh, act->mean_opac, act->quat, act->scale, act->sh};
+  for (const float* q : planes)
+    if (!q) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "adam: plane pointer is NULL");
+  AdamArgs a{};
+  a.n = p->n_local;
+  float* raw[3] = {p->mean_logit, p->quat_raw, p->log_scale};
+  float* gr[3] = {grads->mean_opac, grads->quat, grads->scale};
+  float* ac[3] = {act->mean_opac, act->quat, act->scale};
+  for (int k = 0; k < 3; ++k) {
+    a.p[k] = reinterpret_cast<float4*>(raw[k]);
+    a.m[k] = reinterpret_cast<float4*>(p->m[k]);
+    a.v[k] = reinterpret_cast<float4*>(p->v[k]);
+    a.g[k] = reinterpret_cast<float4*>(gr[k]);
+    a.act[k] = reinterpret_cast<float4*>(ac[k]);
+  }
+  a.sh_p = p->sh;
+  a.sh_m = p->m[3];
+  a.sh_v = p->v[3];
+  a.sh_g = grads->sh;
+  a.sh_act = act->sh;
+  a.visible = visible;
+  a.lr_mean = h->lr_mean;
+  a.lr_opacity = h->lr_opacity;
+  a.lr_quat = h->lr_quat;
+  a.lr_scale = h->lr_scale;
+  a.lr_sh_dc = h->lr_sh_dc;
+  a.lr_sh_rest = h->lr_sh_rest;
+  a.b1 = float(h->beta1);
+  a.b2 = float(h->beta2);
+  a.om1 = float(1.0 - h->beta1);
+  a.om2 = float(1.0 - h->beta2);
+  a.eps = float(h->eps);
+  a.c1 = float(1.0 / (1.0 - std::pow(h->beta1, double(h->step))));
+  a.c2 = float(1.0 / (1.0 - std::pow(h->beta2, double(h->step))));
+  launch_adam(a, static_cast<cudaStream_t>(stream));
+  CKS(launched(ctx, 2));
+  return BGS_OK;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------------------
