@@ -560,6 +560,10 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
         host_on(k % inflight, args.warmup + k)
     torch.cuda.synchronize()
     e2e = args.steps / D.max_over_ranks(time.perf_counter() - t1, torch.device(dev))
+    # NEXT-3: the optimizer step of the batch (bgs_adam_step) on this rank's shard, dense (every row)
+    # and selective (rows some view of the batch projected: the union of the records' c_rad bits)
+    adam = adam_step_timing(B, S, g, grads, ctxs[0], stream, dev, n_local, l2_flush, cams, gate, cull_cols, per,
+                            s_imp, c_rad, c_vis, args)
     return {"metric": "supervised training views/s (a1-a12 + Eq.7 L1+SSIM on owned tiles + Eq.8, NEXT-4)",
             "value": round(1000.0 / ms, 3), "unit": "views/s", "ms_per_view": round(ms, 4),
             "lambda": lam, "batch_inv": binv, "beta": beta,
@@ -567,7 +571,63 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
             "stages_avg": stages / args.steps,
             "loss_last_view": {"l": loss[0], "L1": loss[1], "SSIM": loss[2], "L_scale": loss[3], "V": loss[4]},
             "e2e": {"value": round(e2e, 3), "unit": "views/s", "h2d_bytes_per_step": int(3 * H * W * 4),
-                    "d2h_bytes_per_step": 40}}
+                    "d2h_bytes_per_step": 40},
+            "adam": adam,
+            "batch_of_4_views_per_s": {
+                "dense_adam": round(4000.0 / (4 * ms + adam["dense_ms"]), 3),
+                "selective_adam": round(4000.0 / (4 * ms + adam["selective_ms"]), 3)}}
+
+
+def adam_step_timing(B, S, g, grads, ctx, stream, dev, n_local, l2_flush, cams, gate, cull_cols, per, s_imp, c_rad,
+                     c_vis, args):
+    """bgs_adam_step on the shard: raw planes derived from the activated ones, device-timed (L2
+    flushed before each), dense and with the visibility mask of a 4-view batch."""
+    import torch
+    from paper_2605_13794_b200 import dist as D
+    mo = g.mean_opac
+    o = mo[:, 3].clamp(1e-6, 1 - 1e-6)
+    ml = torch.cat([mo[:, :3], torch.log(o / (1 - o))[:, None]], 1).contiguous()
+    tp = B.TrainParams(ml, g.quat.clone(), torch.log(g.scale.clamp_min(1e-30)).contiguous(), g.sh.clone())
+    tp.log_scale[:, 3] = 0
+    act = B.GaussianPlanes(torch.empty_like(mo), torch.empty_like(g.quat), torch.empty_like(g.scale), tp.sh, g.lod)
+    # the batch's visible rows: radius > 0 in any of 4 views (from the in-flight contexts' last views)
+    vis = torch.zeros(max(n_local, 1), dtype=torch.bool, device=dev)
+    for p in per[:4]:
+        vis |= p["radius"][:max(n_local, 1)] > 0
+    bits = vis.view(-1)
+    pad = (-bits.numel()) % 32
+    words = torch.nn.functional.pad(bits.to(torch.int64), (0, pad)).view(-1, 32)
+    mask = (words << torch.arange(32, device=dev, dtype=torch.int64)).sum(1).to(torch.int64)
+    mask = torch.where(mask >= 2 ** 31, mask - 2 ** 32, mask).to(torch.int32).contiguous()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    out = {}
+    with torch.cuda.stream(stream):
+        for name, m in (("dense", None), ("selective", mask)):
+            tot = 0.0
+            for k in range(args.warmup + args.steps):
+                l2_flush.zero_()
+                stream.synchronize()
+                ev[0].record(stream)
+                B.bgs_adam_step(ctx, tp, grads, act, m, B.adam_hparams(step=k + 1), stream)
+                ev[1].record(stream)
+                stream.synchronize()
+                if k >= args.warmup:
+                    tot += ev[0].elapsed_time(ev[1])
+            out[f"{name}_ms"] = round(D.max_over_ranks(tot / args.steps, torch.device(dev)), 4)
+    rows = float(vis[:n_local].sum().item())
+    # algorithmic bytes per updated row: read raw 240 + grads 240 + m 240 + v 240; write raw 240 +
+    # m 240 + v 240 + activated 48 (SH aliases the raw plane) + zeroed grads 240
+    per_row = 4 * 240 + 4 * 240 + 48
+    peaks_gbs = load_peaks()["hbm_gbs"]
+    for name, nrows in (("dense", float(n_local)), ("selective", rows)):
+        ach = per_row * nrows / (out[f"{name}_ms"] * 1e-3) / 1e9 if out[f"{name}_ms"] > 0 else 0.0
+        out[f"{name}_roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks_gbs, "unit": "GB/s",
+                                   "frac": round(ach / peaks_gbs, 4), "rows": int(nrows),
+                                   "work": f"{per_row} B x rows"}
+    out["note"] = ("one optimizer step per batch of B = 4 views (P:342); selective = rows projected by any view "
+                   "of the batch (visibility mask), dense = every row of the shard")
+    del tp, act
+    return out
 
 
 def load_peaks():
