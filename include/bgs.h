@@ -17,6 +17,7 @@
  *   bgs_loss_photo     NEXT-4 Eq.7 L1 + SSIM on the owned tiles with its gradient
  *   bgs_loss_scale     NEXT-4 Eq.8 scale regulariser over the visible set
  *   bgs_adam_step      NEXT-3 fused activation-chain-rule + Adam step on the owned shard
+ *   bgs_densify_*      NEXT-3 phi-reweighted density statistic, clone / split / prune with heritage
  * bgs_view_step / bgs_view_step_host run a1..a11 (+a12 when requested) in one call.
  *
  * Conventions (all entry points):
@@ -400,6 +401,40 @@ typedef struct {
 bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaussian_grads* grads,
                          const bgs_gaussians_out* act, const uint32_t* visible, const bgs_adam_hparams* h,
                          void* stream);
+
+/* Density-control statistic of one view (R37): after bgs_route_reverse of the view on
+ * this ctx, for every local Gaussian the view projected (radius > 0):
+ *   stat[i] += phi_i * |(dL/dmx * W/2, dL/dmy * H/2)|,  count[i] += 1
+ * (dL/dmean2d from the owner-summed compositing partials, in NDC units as the 3DGS view-space
+ * statistic).  phi: nullable device f64 [n_local] (bgs_score_phi; NULL = 1).  stat: device f32,
+ * count: device u32 [n_local], accumulated with reductions (views in flight may share them). */
+bgs_status bgs_densify_accumulate(bgs_ctx* ctx, int64_t n_local, const double* phi, float* stat, uint32_t* count,
+                                  void* stream);
+
+/* Density-control thresholds (R39, R40; values are the caller's).  The decisions
+ * are taken in fp32 as l < logit(min_opacity), max_j log s_ij > log(dense_extent) (thresholds
+ * rounded once from double) and stat / max(1, count) >= grad_threshold. */
+typedef struct {
+  float grad_threshold;  /* tau on stat / max(1, count) (3DGS: 2e-4) */
+  float dense_extent;    /* percent_dense * scene extent: clone if max_j s_ij <= this, else split */
+  float min_opacity;     /* prune rows with opacity below this (3DGS: 0.005) */
+  float split_div;       /* split children scale = s / split_div (3DGS: 1.6) */
+  uint64_t seed;         /* split samples: z = N(0, I) of (seed, parent global id, child, axis) */
+} bgs_densify_params;
+
+/* Clone / split / prune the local shard ("clones, splits, and prunes"; heritage rule P:194:
+ * clone keeps the level, split increments it).  in: the shard's raw parameters and Adam moments
+ * (bgs_train_params), lod_in u8 [n]; stat / count from bgs_densify_accumulate.  out: raw planes
+ * and moments of the new shard, out->n_local = CAPACITY in rows; lod_out u8 [capacity]; act_out
+ * (nullable): activated planes of the new shard (act_out->sh may equal out->sh).  Order: kept
+ * originals (input order), clones (parent order), first then second children of split parents;
+ * moments copied for originals, zero for new rows.  *n_out (host) = new row count;
+ * BGS_ERR_CAPACITY (nothing written) when it exceeds the capacity.  out must not alias in.  The
+ * caller re-zeros stat / count for the new shard.  Global ids are j*M + rank as before; a
+ * skew-triggered bgs_redistribute can follow.  HOST-SYNC. */
+bgs_status bgs_densify_apply(bgs_ctx* ctx, const bgs_train_params* in, const uint8_t* lod_in, const float* stat,
+                             const uint32_t* count, const bgs_densify_params* dp, const bgs_train_params* out,
+                             uint8_t* lod_out, const bgs_gaussians_out* act_out, int64_t* n_out, void* stream);
 
 #ifdef __cplusplus
 }

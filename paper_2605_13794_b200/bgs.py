@@ -100,6 +100,8 @@ _SIGS = {
     "bgs_loss_scale": [_vp, _vp, C.c_float, _vp, _vp, _vp],
     "bgs_train_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_adam_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_densify_accumulate": [_vp, C.c_int64, _vp, _vp, _vp, _vp],
+    "bgs_densify_apply": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_train_view_step_host_async": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, C.c_float, C.c_float, C.c_float,
                                        _vp, _vp, _vp, _vp],
 }
@@ -398,6 +400,37 @@ def bgs_adam_step(ctx: Context, p: TrainParams, grads: GradPlanes, act: Gaussian
                            act.scale.data_ptr(), act.sh.data_ptr(), act.lod.data_ptr())
     ctx.check(_lib.bgs_adam_step(ctx.handle, C.byref(ps), C.byref(gr), C.byref(ao), _ptr(visible), C.byref(h),
                                  _stream(stream)), "bgs_adam_step")
+
+
+class bgs_densify_params(C.Structure):
+    _fields_ = [("grad_threshold", C.c_float), ("dense_extent", C.c_float), ("min_opacity", C.c_float),
+                ("split_div", C.c_float), ("seed", C.c_uint64)]
+
+
+def densify_params(grad_threshold=2e-4, dense_extent=0.01, min_opacity=0.005, split_div=1.6,
+                   seed=0) -> bgs_densify_params:
+    """3DGS defaults (tau 2e-4, opacity 0.005, split / 1.6); dense_extent = percent_dense * extent."""
+    return bgs_densify_params(grad_threshold, dense_extent, min_opacity, split_div, seed)
+
+
+def bgs_densify_accumulate(ctx: Context, n_local: int, phi, stat, count, stream=None):
+    ctx.check(_lib.bgs_densify_accumulate(ctx.handle, int(n_local), _ptr(phi), _ptr(stat), _ptr(count),
+                                          _stream(stream)), "bgs_densify_accumulate")
+
+
+def bgs_densify_apply(ctx: Context, p_in: TrainParams, lod_in, stat, count, dp: bgs_densify_params,
+                      p_out: TrainParams, lod_out, act_out: GaussianPlanes | None, stream=None) -> int:
+    """NEXT-3 clone / split / prune; p_out rows = capacity; returns the new row count."""
+    si, so = p_in.struct(), p_out.struct()
+    ao = None
+    if act_out is not None:
+        ao = bgs_gaussians_out(act_out.mean_opac.shape[0], act_out.mean_opac.data_ptr(), act_out.quat.data_ptr(),
+                               act_out.scale.data_ptr(), act_out.sh.data_ptr(), act_out.lod.data_ptr())
+    n = C.c_int64(0)
+    ctx.check(_lib.bgs_densify_apply(ctx.handle, C.byref(si), _ptr(lod_in), _ptr(stat), _ptr(count), C.byref(dp),
+                                     C.byref(so), _ptr(lod_out), C.byref(ao) if ao is not None else None,
+                                     C.byref(n), _stream(stream)), "bgs_densify_apply")
+    return int(n.value)
 
 
 class bgs_supervision(C.Structure):

@@ -311,4 +311,43 @@ struct AdamArgs {
 };
 void launch_adam(const AdamArgs& a, cudaStream_t s);
 
+// NEXT-3 density control (densify.cu)
+struct DensifyAccArgs {
+  int64_t F;
+  const uint32_t* lidx;  // local index of each record
+  const Rec* recs;       // the view's local records (mx, my, A, B | C, o, ...)
+  const Acc* acc;        // owner-summed moments per local record
+  const double* phi;     // nullable: phi = 1
+  float half_w, half_h;  // NDC scaling of dL/dmean2d (R37)
+  float* stat;
+  uint32_t* count;
+};
+void launch_densify_accumulate(const DensifyAccArgs& a, cudaStream_t s);
+
+struct DensifyArgs {
+  int64_t n;
+  int rank, world;
+  const float4* p_in[3];
+  const float4* m_in[3];
+  const float4* v_in[3];
+  const float *sh_in, *sh_m_in, *sh_v_in;
+  const uint8_t* lod_in;
+  const float* stat;
+  const uint32_t* count;
+  float tau, log_extent, logit_min, log_div;
+  unsigned long long seed;
+  uint32_t* block_counts;        // 3 per block, scanned in place
+  unsigned long long* totals;    // kept, clones, split parents
+  float4* p_out[3];
+  float4* m_out[3];
+  float4* v_out[3];
+  float *sh_out, *sh_m_out, *sh_v_out;
+  uint8_t* lod_out;
+  float4* act[3];                // nullable: activated planes of the output
+  float* sh_act;
+};
+int64_t densify_n_blocks(int64_t n);
+void launch_densify_count(const DensifyArgs& a, cudaStream_t s);
+void launch_densify_emit(const DensifyArgs& a, cudaStream_t s);
+
 }  // namespace bgs

@@ -1326,6 +1326,110 @@ bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaus
   return BGS_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// NEXT-3: density control (densify.cu)
+// ---------------------------------------------------------------------------------------
+bgs_status bgs_densify_accumulate(bgs_ctx* ctx, int64_t n_local, const double* phi, float* stat, uint32_t* count,
+                                  void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (ctx->stage < 6) return fail(ctx, BGS_ERR_CONTRACT, "bgs_densify_accumulate before bgs_route_reverse");
+  if (n_local != ctx->n_local) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: n_local differs from the view's");
+  if (ctx->F > 0 && (!stat || !count)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: stat / count NULL");
+  DensifyAccArgs a{};
+  a.F = ctx->F;
+  a.lidx = P_<uint32_t>(ctx->rec_lidx);
+  a.recs = P_<Rec>(ctx->recs);
+  a.acc = ctx->acc_local;
+  a.phi = phi;
+  a.half_w = 0.5f * float(ctx->cam.W);
+  a.half_h = 0.5f * float(ctx->cam.H);
+  a.stat = stat;
+  a.count = count;
+  if (a.F > 0) {
+    launch_densify_accumulate(a, static_cast<cudaStream_t>(stream));
+    CKS(launched(ctx));
+  }
+  return BGS_OK;
+}
+
+static bool planes_ok(const bgs_train_params* p) {
+  if (!p->mean_logit || !p->quat_raw || !p->log_scale || !p->sh) return false;
+  for (int k = 0; k < 4; ++k)
+    if (!p->m[k] || !p->v[k]) return false;
+  return true;
+}
+
+bgs_status bgs_densify_apply(bgs_ctx* ctx, const bgs_train_params* in, const uint8_t* lod_in, const float* stat,
+                             const uint32_t* count, const bgs_densify_params* dp, const bgs_train_params* out,
+                             uint8_t* lod_out, const bgs_gaussians_out* act_out, int64_t* n_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  if (!in || !out || !dp || !n_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: NULL argument");
+  if (in->n_local < 0) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: n_local < 0");
+  if (!(dp->split_div > 0.f)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: split_div must be > 0");
+  *n_out = 0;
+  if (in->n_local == 0) return BGS_OK;
+  if (!planes_ok(in) || !planes_ok(out) || !lod_in || !lod_out || !stat || !count)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: plane pointer is NULL");
+  if (act_out && (!act_out->mean_opac || !act_out->quat || !act_out->scale || !act_out->sh))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: act_out plane pointer is NULL");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DensifyArgs a{};
+  a.n = in->n_local;
+  a.rank = ctx->rank;
+  a.world = ctx->world;
+  const float* ip[3] = {in->mean_logit, in->quat_raw, in->log_scale};
+  float* op[3] = {out->mean_logit, out->quat_raw, out->log_scale};
+  for (int k = 0; k < 3; ++k) {
+    a.p_in[k] = reinterpret_cast<const float4*>(ip[k]);
+    a.m_in[k] = reinterpret_cast<const float4*>(in->m[k]);
+    a.v_in[k] = reinterpret_cast<const float4*>(in->v[k]);
+    a.p_out[k] = reinterpret_cast<float4*>(op[k]);
+    a.m_out[k] = reinterpret_cast<float4*>(out->m[k]);
+    a.v_out[k] = reinterpret_cast<float4*>(out->v[k]);
+  }
+  a.sh_in = in->sh;
+  a.sh_m_in = in->m[3];
+  a.sh_v_in = in->v[3];
+  a.sh_out = out->sh;
+  a.sh_m_out = out->m[3];
+  a.sh_v_out = out->v[3];
+  a.lod_in = lod_in;
+  a.lod_out = lod_out;
+  a.stat = stat;
+  a.count = count;
+  a.tau = dp->grad_threshold;
+  if (!(dp->dense_extent > 0.f) || !(dp->min_opacity > 0.f && dp->min_opacity < 1.f))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: dense_extent > 0 and 0 < min_opacity < 1 required");
+  a.log_extent = float(std::log(double(dp->dense_extent)));
+  a.logit_min = float(std::log(double(dp->min_opacity) / (1.0 - double(dp->min_opacity))));
+  a.log_div = float(std::log(double(dp->split_div)));
+  a.seed = dp->seed;
+  if (act_out) {
+    a.act[0] = reinterpret_cast<float4*>(act_out->mean_opac);
+    a.act[1] = reinterpret_cast<float4*>(act_out->quat);
+    a.act[2] = reinterpret_cast<float4*>(act_out->scale);
+    a.sh_act = act_out->sh;
+  }
+  const int64_t nb = densify_n_blocks(a.n);
+  CKS(ensure(ctx, ctx->dcnt, size_t(3 * nb + 8) * 4 + 64));
+  a.block_counts = P_<uint32_t>(ctx->dcnt) + 16;
+  a.totals = P_<unsigned long long>(ctx->dcnt);
+  launch_densify_count(a, s);
+  CKS(launched(ctx, 2));
+  unsigned long long tot[3];
+  CK(cudaMemcpyAsync(tot, a.totals, sizeof tot, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t n_new = int64_t(tot[0] + tot[1] + 2 * tot[2]);
+  *n_out = n_new;
+  if (n_new > out->n_local || (act_out && n_new > act_out->capacity))
+    return fail(ctx, BGS_ERR_CAPACITY, "densify: new shard exceeds the output capacity");
+  launch_densify_emit(a, s);
+  CKS(launched(ctx));
+  return BGS_OK;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------------------

@@ -54,7 +54,7 @@ class GpuStep:
     """One view through a1..a12 on one ctx (world 1) or an in-process group (world > 1)."""
 
     def __init__(self, scene, cam, M=1, gate=None, cull_global=None, flags=0, dLdC=None, importance=True,
-                 ctxs=None, device=0, target=None, lam=0.2, batch_inv=1.0, beta=None):
+                 ctxs=None, device=0, target=None, lam=0.2, batch_inv=1.0, beta=None, densify=False, phi=None):
         import paper_2605_13794_b200.bgs as B
         self.B = B
         self.M = M
@@ -119,6 +119,14 @@ class GpuStep:
                         B.bgs_raster_bwd(ctx, dl, T, nc, stream)
                     B.bgs_route_reverse(ctx, stream)
                     out["acc_local"] = acc_view(ctx.debug_buffer("acc_local"))
+                    if densify:  # NEXT-3 statistic of this view
+                        stat = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
+                        cnt = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+                        ph = None if phi is None else torch.from_numpy(np.ascontiguousarray(phi[r::M])).to(dev)
+                        B.bgs_densify_accumulate(ctx, n, ph, stat, cnt, stream)
+                        stream.synchronize()
+                        out["dc_stat"] = stat.cpu().numpy()[:n]
+                        out["dc_count"] = cnt.cpu().numpy()[:n]
                     grads = g.zeros_grads()
                     if dLdC is not None:
                         B.bgs_project_bwd(ctx, g, bcam, grads, stream)
@@ -184,6 +192,8 @@ class GpuStep:
         self.loss = [self.rank[r].get("loss") for r in range(M)]
         self.loss_scale = [self.rank[r].get("loss_scale") for r in range(M)]
         self.g_scale_reg = np.zeros((n, 4), np.float32) if "g_scale_reg" in self.rank[0] else None
+        self.dc_stat = np.zeros(n, np.float32) if "dc_stat" in self.rank[0] else None
+        self.dc_count = np.zeros(n, np.int64) if "dc_stat" in self.rank[0] else None
         for r in range(M):
             o = self.rank[r]
             gids = np.arange(r, n, M)
@@ -208,6 +218,9 @@ class GpuStep:
                 self.c_rad[gids] = o["c_rad"]
                 self.c_vis[gids] = o["c_vis"]
                 self.cull_bits[gids] = S.unpack_bits(o["cull"], len(gids))
+            if self.dc_stat is not None:
+                self.dc_stat[gids] = o["dc_stat"]
+                self.dc_count[gids] = o["dc_count"]
             if self.g_scale_reg is not None:
                 self.g_scale_reg[gids] = o["g_scale_reg"][:len(gids)]
             gm[gids] = o["grads"]["mean_opac"]
