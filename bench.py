@@ -498,6 +498,10 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
     for p in per:
         p["dl"] = torch.zeros(3, H, W, device=dev)
         p["loss"] = torch.zeros(5, dtype=torch.float64, device=dev)
+    # NEXT-3 density statistic, accumulated by every training view (3DGS: every iteration of the
+    # densification window), phi from the importance counts the views accumulate
+    dc_stat = torch.zeros(max(n_local, 1), dtype=torch.float32, device=dev)
+    dc_count = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
 
     def train_on(k, v):
         p = per[k]
@@ -505,6 +509,7 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
                               cull_cols[v % len(cams)] if cull_cols is not None else None, 0, p["radius"],
                               B.supervision(tgt, lam, binv, beta, p["loss"]), p["rgb"], p["Tf"], p["nc"], p["dl"],
                               grads, B.importance_out(s_imp, c_rad, c_vis, p["cull"], 99, 100), p["stream"])
+        B.bgs_densify_accumulate(ctxs[k], n_local, None, dc_stat, dc_count, p["stream"])
 
     for k in range(inflight):
         with torch.cuda.stream(per[k]["stream"]):
@@ -563,7 +568,7 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
     # NEXT-3: the optimizer step of the batch (bgs_adam_step) on this rank's shard, dense (every row)
     # and selective (rows some view of the batch projected: the union of the records' c_rad bits)
     adam = adam_step_timing(B, S, g, grads, ctxs[0], stream, dev, n_local, l2_flush, cams, gate, cull_cols, per,
-                            s_imp, c_rad, c_vis, args)
+                            s_imp, c_rad, c_vis, args, dc_stat, dc_count)
     return {"metric": "supervised training views/s (a1-a12 + Eq.7 L1+SSIM on owned tiles + Eq.8, NEXT-4)",
             "value": round(1000.0 / ms, 3), "unit": "views/s", "ms_per_view": round(ms, 4),
             "lambda": lam, "batch_inv": binv, "beta": beta,
@@ -579,7 +584,7 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
 
 
 def adam_step_timing(B, S, g, grads, ctx, stream, dev, n_local, l2_flush, cams, gate, cull_cols, per, s_imp, c_rad,
-                     c_vis, args):
+                     c_vis, args, dc_stat, dc_count):
     """bgs_adam_step on the shard: raw planes derived from the activated ones, device-timed (L2
     flushed before each), dense and with the visibility mask of a 4-view batch."""
     import torch
@@ -626,6 +631,35 @@ def adam_step_timing(B, S, g, grads, ctx, stream, dev, n_local, l2_flush, cams, 
                                    "work": f"{per_row} B x rows"}
     out["note"] = ("one optimizer step per batch of B = 4 views (P:342); selective = rows projected by any view "
                    "of the batch (visibility mask), dense = every row of the shard")
+    # NEXT-3 density control on the shard with the statistic of the timed training views (tau chosen
+    # as the 99th percentile of the per-Gaussian average so that ~1% densify; 3DGS's 2e-4 is scale-
+    # dependent), extent 1% of the scene (1000 units): wall time of the HOST-SYNC call
+    with torch.cuda.stream(stream):
+        avg = (dc_stat[:n_local] / dc_count[:n_local].clamp_min(1).float())
+        tau = float(torch.quantile(avg[avg > 0][:1 << 24].float(), 0.99).item()) if bool((avg > 0).any()) else 1.0
+        cap = 2 * n_local + 1
+        tout = B.TrainParams(*(torch.empty(cap, c, device=dev) for c in (4, 4, 4, 48)))
+        lod_out = torch.empty(cap, dtype=torch.uint8, device=dev)
+        act2 = B.GaussianPlanes(torch.empty(cap, 4, device=dev), torch.empty(cap, 4, device=dev),
+                                torch.empty(cap, 4, device=dev), tout.sh, lod_out)
+        dp = B.densify_params(tau, 10.0, 0.005, 1.6, 1234)
+        B.bgs_densify_apply(ctx, tp, g.lod, dc_stat, dc_count, dp, tout, lod_out, act2, stream)  # warm-up
+        stream.synchronize()
+        t1 = time.perf_counter()
+        n_new = B.bgs_densify_apply(ctx, tp, g.lod, dc_stat, dc_count, dp, tout, lod_out, act2, stream)
+        stream.synchronize()
+        ms = (time.perf_counter() - t1) * 1e3
+        # algorithmic bytes: read every input row (raw 240 + m, v 480 + lod 1 + stat, count 8), write
+        # every output row (raw + m + v 720 + activated 48 + lod 1)
+        byt = n_local * (240 + 480 + 1 + 8) + n_new * (720 + 48 + 1)
+        out["densify"] = {"apply_ms": round(D.max_over_ranks(ms, torch.device(dev)), 4), "rows_in": int(n_local),
+                          "rows_out": int(n_new), "tau": tau, "dense_extent": 10.0,
+                          "roofline": {"bound": "hbm", "achieved": round(byt / (ms * 1e-3) / 1e9, 1),
+                                       "peak": peaks_gbs, "unit": "GB/s",
+                                       "frac": round(byt / (ms * 1e-3) / 1e9 / peaks_gbs, 4)},
+                          "note": "statistic accumulated by every timed training view (bgs_densify_accumulate); "
+                                  "apply is HOST-SYNC, wall time incl. the count round trip"}
+        del tout, act2
     del tp, act
     return out
 
