@@ -24,6 +24,8 @@ STAGE_OF = {
     "k_fill_bits": "importance", "k_imp_coop": "importance", "k_imp_stats": "importance", "k_imp_hist": "importance",
     "k_imp_decide": "importance", "k_imp_gid_hist": "importance", "k_imp_gid_decide": "importance",
     "k_imp_mark": "importance",
+    "k_loss_photo": "loss", "k_loss_sums": "loss", "k_loss_finish": "loss", "k_owned_copy": "loss",
+    "k_scale_sum": "loss", "k_scale_finish": "loss", "k_scale_grad": "loss",
 }
 
 
