@@ -144,26 +144,17 @@ __global__ void k_dc_scan(uint32_t* counts, int64_t nb, unsigned long long* tota
   if (threadIdx.x < 3) totals[threadIdx.x] = carry[threadIdx.x];
 }
 
+// 16-byte planes, level and activated 16-byte planes of one output row (one thread per row: the
+// rows of a warp land in one or two contiguous runs)
 __device__ __forceinline__ void put_row(const DensifyArgs& a, int64_t src, int64_t dst, bool fresh, float4 ml,
                                         float4 q, float4 ls, int lod) {
   a.p_out[0][dst] = ml;
   a.p_out[1][dst] = q;
   a.p_out[2][dst] = ls;
-  const float4* shs = reinterpret_cast<const float4*>(a.sh_in) + src * 12;
-  float4* shd = reinterpret_cast<float4*>(a.sh_out) + dst * 12;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int k = 0; k < 3; ++k) {
     a.m_out[k][dst] = fresh ? z4 : a.m_in[k][src];
     a.v_out[k][dst] = fresh ? z4 : a.v_in[k][src];
-  }
-  float4* mshd = reinterpret_cast<float4*>(a.sh_m_out) + dst * 12;
-  float4* vshd = reinterpret_cast<float4*>(a.sh_v_out) + dst * 12;
-  const float4* mshs = reinterpret_cast<const float4*>(a.sh_m_in) + src * 12;
-  const float4* vshs = reinterpret_cast<const float4*>(a.sh_v_in) + src * 12;
-  for (int k = 0; k < 12; ++k) {
-    shd[k] = shs[k];
-    mshd[k] = fresh ? z4 : mshs[k];
-    vshd[k] = fresh ? z4 : vshs[k];
   }
   a.lod_out[dst] = uint8_t(lod > 255 ? 255 : lod);
   if (a.act[0]) {  // activated planes for the next render
@@ -171,9 +162,43 @@ __device__ __forceinline__ void put_row(const DensifyArgs& a, int64_t src, int64
     const float in = 1.f / sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
     a.act[1][dst] = make_float4(q.x * in, q.y * in, q.z * in, q.w * in);
     a.act[2][dst] = make_float4(expf(ls.x), expf(ls.y), expf(ls.z), 0.f);
-    if (a.sh_act && a.sh_act != a.sh_out) {
-      float4* sha = reinterpret_cast<float4*>(a.sh_act) + dst * 12;
-      for (int k = 0; k < 12; ++k) sha[k] = shs[k];
+  }
+}
+
+// The 192-B SH rows (parameter, m, v and the activated copy) of the warp's output rows, copied by
+// the whole warp one row at a time: lane e moves float4 e of the row set (12 per plane), so every
+// load and store is a contiguous 192-B run instead of 16 B per lane at a 192-B stride.
+__device__ __forceinline__ void copy_sh_rows(const DensifyArgs& a, int64_t src, int64_t d0, int64_t d1, bool f0,
+                                             bool f1) {
+  const int l = threadIdx.x & 31;
+  const bool act = a.act[0] && a.sh_act && a.sh_act != a.sh_out;
+  const int ne = act ? 48 : 36;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = 0; j < 32; ++j) {
+    const int64_t sj = __shfl_sync(0xffffffffu, src, j);
+    for (int t = 0; t < 2; ++t) {
+      const int64_t dj = __shfl_sync(0xffffffffu, t ? d1 : d0, j);
+      const bool fj = __shfl_sync(0xffffffffu, t ? f1 : f0, j);
+      if (dj < 0) continue;  // warp-uniform
+      for (int e = l; e < ne; e += 32) {
+        const int plane = e / 12, k = e % 12;
+        float4 v;
+        float* dstp;
+        if (plane == 0) {
+          v = reinterpret_cast<const float4*>(a.sh_in)[sj * 12 + k];
+          dstp = a.sh_out;
+        } else if (plane == 1) {
+          v = fj ? z4 : reinterpret_cast<const float4*>(a.sh_m_in)[sj * 12 + k];
+          dstp = a.sh_m_out;
+        } else if (plane == 2) {
+          v = fj ? z4 : reinterpret_cast<const float4*>(a.sh_v_in)[sj * 12 + k];
+          dstp = a.sh_v_out;
+        } else {
+          v = reinterpret_cast<const float4*>(a.sh_in)[sj * 12 + k];
+          dstp = a.sh_act;
+        }
+        reinterpret_cast<float4*>(dstp)[dj * 12 + k] = v;
+      }
     }
   }
 }
@@ -197,15 +222,27 @@ __global__ void __launch_bounds__(kDcThreads) k_dc_emit(DensifyArgs a) {
   uint32_t off[3] = {0, 0, 0};
   for (int j = 0; j < w; ++j)
     for (int c = 0; c < 3; ++c) off[c] += wpre[c][j];
-  if (i >= a.n) return;
+  // every lane of a live warp stays for the cooperative SH copy (rows past n have no destination)
   const uint32_t* base = a.block_counts + 3 * int64_t(blockIdx.x);
   const int64_t K = int64_t(a.totals[0]), Cn = int64_t(a.totals[1]), Sn = int64_t(a.totals[2]);
-  const float4 ml = a.p_in[0][i], q = a.p_in[1][i], ls = a.p_in[2][i];
-  const int lod = int(a.lod_in[i]);
-  if (d.keep) put_row(a, i, int64_t(base[0]) + off[0] + __popc(bk & lt), false, ml, q, ls, lod);
-  if (d.clone) put_row(a, i, K + int64_t(base[1]) + off[1] + __popc(bc & lt), true, ml, q, ls, lod);
+  const int64_t ii = i < a.n ? i : 0;
+  const float4 ml = a.p_in[0][ii], q = a.p_in[1][ii], ls = a.p_in[2][ii];
+  const int lod = int(a.lod_in[ii]);
+  int64_t d0 = -1, d1 = -1;
+  bool f0 = false, f1 = true;
+  if (d.keep) {
+    d0 = int64_t(base[0]) + off[0] + __popc(bk & lt);
+    put_row(a, i, d0, false, ml, q, ls, lod);
+  }
+  if (d.clone) {
+    d1 = K + int64_t(base[1]) + off[1] + __popc(bc & lt);
+    put_row(a, i, d1, true, ml, q, ls, lod);
+  }
   if (d.split) {
     const int64_t r = int64_t(base[2]) + off[2] + __popc(bs & lt);
+    d0 = K + Cn + r;
+    d1 = K + Cn + Sn + r;
+    f0 = true;
     const unsigned long long gid = (unsigned long long)i * unsigned(a.world) + unsigned(a.rank);
     // R(q) of the normalised quaternion (w, x, y, z), rows
     const float in = 1.f / sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
@@ -224,6 +261,7 @@ __global__ void __launch_bounds__(kDcThreads) k_dc_emit(DensifyArgs a) {
       put_row(a, i, K + Cn + int64_t(c) * Sn + r, true, mc, q, lsc, lod + 1);
     }
   }
+  copy_sh_rows(a, ii, d0, d1, f0, f1);
 }
 
 }  // namespace
