@@ -49,11 +49,43 @@ def parse():
     p.add_argument("--stages", action="store_true", help="also print per-stage timings to stderr")
     p.add_argument("--layout", default="morton", choices=["morton", "input"],
                    help="shard storage order: Z-order (bgs_spatial_order) or the generator's random ids")
+    p.add_argument("--host-threads", type=int, default=0,
+                   help="1: one host thread per in-flight context (the ABI's one-ctx-per-host-thread model), so "
+                        "a context's HOST-SYNC calls block only its own thread; 0: one thread submits all views")
     p.add_argument("--inflight", type=int, default=4,
                    help="views in flight per rank (one ctx + stream each); 4 = the paper's batch of B = 4 "
                         "views per step (P:342). Measured on Rubble: 1 -> 1061, 2 -> 1183, 3 -> 1220, "
                         "4 -> 1224 views/s")
     return p.parse_args()
+
+
+def submit_views(fn, inflight: int, ids, threaded: bool, device: int):
+    """Enqueue view ids[j] on in-flight context j % inflight via fn(k, v).  threaded: one host thread
+    per context (ctypes releases the GIL inside the ABI calls), so the host round trip of one view's
+    HOST-SYNC projection does not hold back the submission of the other contexts' views."""
+    if not threaded or inflight == 1:
+        for j, v in enumerate(ids):
+            fn(j % inflight, v)
+        return
+    import torch
+    errs = []
+
+    def worker(k):
+        try:
+            torch.cuda.set_device(device)
+            for j, v in enumerate(ids):
+                if j % inflight == k:
+                    fn(k, v)
+        except Exception as e:  # surfaced after the join
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(inflight)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
 
 
 # ------------------------------------------------------------------------------------------
@@ -315,8 +347,7 @@ def run_native(args):
     ev_start.record(per[0]["stream"])
     for k in range(1, inflight):
         per[k]["stream"].wait_event(ev_start)
-    for k in range(args.steps):
-        view_on(k % inflight, args.warmup + k)
+    submit_views(view_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads), local)
     for k in range(inflight):
         ev_end[k].record(per[k]["stream"])
     torch.cuda.synchronize()
@@ -355,8 +386,7 @@ def run_native(args):
     torch.cuda.synchronize()
     barrier()
     t1 = time.perf_counter()
-    for k in range(args.steps):
-        host_view(k % inflight, args.warmup + k)
+    submit_views(host_view, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads), local)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t1
     e2e_views = args.steps / D.max_over_ranks(e2e_s, torch.device(dev))
@@ -450,6 +480,7 @@ def run_native(args):
                    "parallelism": f"index-parity shards x {world}, tile-owner all-to-all",
                    "shard_layout": args.layout,
                    "views_in_flight": inflight,
+                   "host_threads": bool(args.host_threads),
                    "l2": ("inputs exceed L2 (shard 1.8 GB per view read); views in flight are not flushed "
                           "between; single_view_ms / stages_ms: one view at a time, L2 flushed (256 MB write) "
                           "before each"),
@@ -537,8 +568,8 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
     ev_start.record(per[0]["stream"])
     for k in range(1, inflight):
         per[k]["stream"].wait_event(ev_start)
-    for k in range(args.steps):
-        train_on(k % inflight, args.warmup + k)
+    submit_views(train_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads),
+                 int(str(dev).split(":")[-1]))
     for k in range(inflight):
         ev_end[k].record(per[k]["stream"])
     torch.cuda.synchronize()
@@ -561,8 +592,8 @@ def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_
     torch.cuda.synchronize()
     barrier()
     t1 = time.perf_counter()
-    for k in range(args.steps):
-        host_on(k % inflight, args.warmup + k)
+    submit_views(host_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads),
+                 int(str(dev).split(":")[-1]))
     torch.cuda.synchronize()
     e2e = args.steps / D.max_over_ranks(time.perf_counter() - t1, torch.device(dev))
     # NEXT-3: the optimizer step of the batch (bgs_adam_step) on this rank's shard, dense (every row)
