@@ -21,6 +21,7 @@
 // so a round costs one grid barrier.  Histograms are warp-aggregated (__match_any_sync +
 // __reduce_add_sync on three 24-bit limbs of w) before the shared-memory atomics.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "bgs_internal.cuh"
 
@@ -525,7 +526,12 @@ static int coop_blocks() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_imp_coop, 256, 0);
-    blocks = sms * (per_sm < 4 ? per_sm : 4);
+    // 2 CTAs per SM: a cooperative grid holds its SM slots while it waits at grid syncs, which
+    // starves the other views in flight; measured on Rubble (4 in flight / one view's importance
+    // stage): 4/SM 1273-1294 views/s / 0.091 ms, 2/SM 1336-1343 / 0.105 ms, 1/SM 1342 / 0.155 ms
+    const char* e = getenv("BGS_IMP_COOP_PER_SM");  // tuning only
+    const int cap = e && atoi(e) > 0 ? atoi(e) : 2;
+    blocks = sms * (per_sm < cap ? per_sm : cap);
     if (blocks < 1) blocks = 1;
   }
   return blocks;

@@ -20,6 +20,8 @@
 // same-address atomics serialise at the L2): every counter here is touched once per CTA.
 #include "bgs_internal.cuh"
 
+#include <cstdlib>
+
 namespace bgs {
 namespace {
 
@@ -400,6 +402,8 @@ int persistent_blocks(K kernel) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0);
   if (sms <= 0) sms = 148;
   if (occ <= 0) occ = 1;
+  const char* e = getenv("BGS_PERSIST_PER_SM");  // tuning only
+  if (e && atoi(e) > 0 && atoi(e) < occ) occ = atoi(e);
   return sms * occ;
 }
 
