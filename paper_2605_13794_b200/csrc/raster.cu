@@ -35,8 +35,16 @@
 namespace bgs {
 namespace {
 
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
+constexpr int kWarps = 4;  // warp blocks per tile unit (four 8x8 quadrants, or four 8x4 in a half tile)
+#ifndef BGS_RASTER_CTA_WARPS
+#define BGS_RASTER_CTA_WARPS 1
+#endif
+// warps per CTA: 1 = every warp block is its own CTA, so a warp that finishes its walk releases its
+// slot at once instead of waiting for the slowest quadrant of its tile (with views in flight the
+// slot goes to another view's kernels)
+constexpr int kCtaWarps = BGS_RASTER_CTA_WARPS;
+constexpr int kCtasPerUnit = kWarps / kCtaWarps;
+constexpr int kThreads = 32 * kCtaWarps;
 // Warp strip width: a warp's 32 lanes cover kStripW columns x 32/kStripW rows per pixel slot.
 constexpr int kStripW = 8;  // 8x8 blocks cull ~8% more records per warp than 16x4 strips (measured)
 constexpr int kLaneRows = 32 / kStripW;
@@ -223,18 +231,19 @@ template <bool kImportance>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __restrict__ rgb,
                                                          float* __restrict__ t_final,
                                                          int32_t* __restrict__ n_contrib) {
-  __shared__ WRec s_rec[kWarps][32];
+  __shared__ WRec s_rec[kCtaWarps][32];
   const uint32_t* __restrict__ vals = a.pass_ctrl[kValsSel] ? a.vals[1] : a.vals[0];
-  const int warp = threadIdx.x >> 5;
-  const int b = blockIdx.x;
+  const int lw = threadIdx.x >> 5;
+  const int warp = lw + int(blockIdx.x % kCtasPerUnit) * kCtaWarps;
+  const int b = int(blockIdx.x / kCtasPerUnit);
   if (b < 2 * a.n_split) {
     const int lt = int(__ldg(a.tile_perm + (b >> 1)));
     fwd_strip<kImportance, 1>(a, vals, lt, kStripW * (warp % kStripsX), (b & 1) * 8 + kLaneRows * (warp / kStripsX),
-                              (b & 1) * kWarps + warp, s_rec[warp], rgb, t_final, n_contrib);
+                              (b & 1) * kWarps + warp, s_rec[lw], rgb, t_final, n_contrib);
   } else {
     const int lt = int(__ldg(a.tile_perm + (b - a.n_split)));
     fwd_strip<kImportance, 2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), warp,
-                              s_rec[warp], rgb, t_final, n_contrib);
+                              s_rec[lw], rgb, t_final, n_contrib);
   }
 }
 
@@ -421,17 +430,18 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
 __global__ void __launch_bounds__(kThreads) k_raster_bwd(RasterArgs a, const float* __restrict__ dL,
                                                          const float* __restrict__ t_final,
                                                          const int32_t* __restrict__ n_contrib) {
-  __shared__ WRec s_rec[kWarps][32];
+  __shared__ WRec s_rec[kCtaWarps][32];
   const uint32_t* __restrict__ vals = a.pass_ctrl[kValsSel] ? a.vals[1] : a.vals[0];
-  const int warp = threadIdx.x >> 5;
-  const int b = blockIdx.x;
+  const int lw = threadIdx.x >> 5;
+  const int warp = lw + int(blockIdx.x % kCtasPerUnit) * kCtaWarps;
+  const int b = int(blockIdx.x / kCtasPerUnit);
   if (b < 2 * a.n_split) {
     const int lt = int(__ldg(a.tile_perm + (b >> 1)));
     bwd_strip<1>(a, vals, lt, kStripW * (warp % kStripsX), (b & 1) * 8 + kLaneRows * (warp / kStripsX),
-                 (b & 1) * kWarps + warp, s_rec[warp], dL, t_final, n_contrib);
+                 (b & 1) * kWarps + warp, s_rec[lw], dL, t_final, n_contrib);
   } else {
     const int lt = int(__ldg(a.tile_perm + (b - a.n_split)));
-    bwd_strip<2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), warp, s_rec[warp], dL,
+    bwd_strip<2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), warp, s_rec[lw], dL,
                  t_final, n_contrib);
   }
 }
@@ -464,9 +474,9 @@ int launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_
   b.n_split = split_count(a.n_tiles);
   const unsigned grid = unsigned(a.n_tiles + b.n_split);
   if (flags & BGS_IMPORTANCE)
-    k_raster_fwd<true><<<grid, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+    k_raster_fwd<true><<<grid * kCtasPerUnit, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
   else
-    k_raster_fwd<false><<<grid, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+    k_raster_fwd<false><<<grid * kCtasPerUnit, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
   return b.n_split;
 }
 
@@ -477,7 +487,7 @@ void launch_raster_bwd(const RasterArgs& a, const float* dL, const float* t_fina
   // culls worse and a warp walks to the deepest of 128 pixels)
   // a.n_split: the forward's split (the contributor masks are per warp block of that layout)
   const RasterArgs& b = a;
-  k_raster_bwd<<<unsigned(a.n_tiles + b.n_split), kThreads, 0, s>>>(b, dL, t_final, n_contrib);
+  k_raster_bwd<<<unsigned(a.n_tiles + b.n_split) * kCtasPerUnit, kThreads, 0, s>>>(b, dL, t_final, n_contrib);
 }
 
 }  // namespace bgs
