@@ -468,7 +468,7 @@ def run_native(args):
     dominant = max(roof, key=lambda r: r["ms"])
     train_roof = stage_rooflines(train.pop("stages_avg"), qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
                                  E=E_sum / args.steps, A=A_sum / args.steps, cull=cull_cols is not None,
-                                 traffic=traffic, names=stage_names)
+                                 traffic=traffic, names=stage_names, with_loss=True)
     train["loss_roofline"] = next((r for r in train_roof if r["stage"] == "loss"), None)
 
     result = {
@@ -499,7 +499,11 @@ def run_native(args):
         "simplify": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in simplify.items()},
         "train": train,
         "stages_ms": {n: round(float(v), 4) for n, v in zip(stage_names, stage_avg)},
-        "roofline": {k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+        "roofline": dict({k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
+                         basis=(f"{dominant['work']} per view (SURVEY 8(d) per-unit ops x E_min); exceeds 1 when "
+                                "exact box culling skips list entries that cannot contribute; the strict "
+                                "contributing-pair basis is frac_contributing in roofline_stages"
+                                if dominant["bound"] == "alu" else f"{dominant['work']} per view (SURVEY 8(d))")),
         "roofline_kernel": dominant["stage"],
         "roofline_stages": roof,
         "e2e": {"value": round(e2e_views, 3), "unit": "views/s", "h2d_bytes_per_step": int(3 * H * W * 4),

@@ -42,7 +42,7 @@ def _avg(qs, k):
 
 
 def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=None, cull=False, traffic=None,
-                    A=None, names=None):
+                    A=None, names=None, with_loss=False):
     """traffic: optional {stage: DRAM bytes per view} from a committed ncu capture (profiles/)."""
     traffic = traffic or {}
     N = float(n_local)
@@ -69,8 +69,8 @@ def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=No
     for name, ms in zip(names, stage_ms):
         ms = float(ms)
         if name == "loss":
-            if ms <= 0:
-                continue  # no supervision in this step
+            if not with_loss:
+                continue  # no supervision in this step (the stage events bracket nothing)
             o = LOSS_OPS * 3.0 * W * H
             ach = o / (ms * 1e-3) / 1e12
             out.append(dict(stage=name, ms=round(ms, 4), bound="alu", achieved=round(ach, 3), peak=round(alu, 2),
