@@ -81,3 +81,31 @@ def test_adam_parity(masked):
             assert np.allclose(got, a[k][rows], rtol=2e-6, atol=1e-7), k
     finally:
         ctx.close()
+
+
+def test_adam_edge_cases():
+    """Empty shard is a no-op; step 0 and betas outside [0, 1) are refused; a too-small act is refused."""
+    import paper_2605_13794_b200.bgs as B
+    dev = "cuda"
+    ctx = B.Context(0, 1, 0)
+    try:
+        e = B.TrainParams(*(torch.zeros(0, c, device=dev) for c in (4, 4, 4, 48)))
+        act0 = B.GaussianPlanes(*(torch.zeros(0, c, device=dev) for c in (4, 4, 4, 48)),
+                                torch.zeros(0, dtype=torch.uint8, device=dev))
+        g0 = B.GradPlanes(*(torch.zeros(0, c, device=dev) for c in (4, 4, 4, 48)))
+        B.bgs_adam_step(ctx, e, g0, act0, None, B.adam_hparams(step=1))
+        n = 5
+        p = B.TrainParams(*(torch.ones(n, c, device=dev) for c in (4, 4, 4, 48)))
+        g = B.GradPlanes(*(torch.ones(n, c, device=dev) for c in (4, 4, 4, 48)))
+        small = B.GaussianPlanes(*(torch.zeros(n - 1, c, device=dev) for c in (4, 4, 4, 48)),
+                                 torch.zeros(n - 1, dtype=torch.uint8, device=dev))
+        for h, what in ((B.adam_hparams(step=0), "step"), (B.adam_hparams(beta1=1.0), "betas")):
+            with pytest.raises(B.BgsError) as err:
+                B.bgs_adam_step(ctx, p, g, small, None, h)
+            assert "INVALID" in str(err.value), what
+        with pytest.raises(B.BgsError) as err:
+            B.bgs_adam_step(ctx, p, g, small, None, B.adam_hparams(step=1))
+        assert "CAPACITY" in str(err.value)
+        assert float(p.mean_logit.sum().item()) == 4.0 * n  # nothing written on refusal
+    finally:
+        ctx.close()
