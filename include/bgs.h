@@ -301,9 +301,17 @@ bgs_status bgs_prune_stochastic(bgs_ctx* ctx, int64_t n_local, const double* s, 
 bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s, int32_t num, int32_t den,
                               uint8_t* keep_out, int32_t* all_zero_out, void* stream);
 
+/* Every rank's shard size (sizes_out: host int64 [world]) for a skew policy ("an
+ * index-parity redistribution rebalances shard sizes across GPUs once the per-GPU skew exceeds a
+ * fixed threshold"; the threshold is the caller's).  HOST-SYNC. */
+bgs_status bgs_shard_sizes(bgs_ctx* ctx, int64_t n_local, int64_t* sizes_out);
+
 /* Index-parity redistribution of the survivors (R33): rows with keep[i] != 0 are
  * renumbered densely in global-id order (new gid), sent to rank new_gid mod M and stored at
- * local index new_gid div M of `out` (exact copies).  *n_out (host) = this rank's new shard
+ * local index new_gid div M of `out` (exact copies).  Shards may be unequal (after density
+ * control): the global order is gid = j M + m over slices padded to the largest shard.  To
+ * carry Adam moments, call again with the moment planes in place of the parameter planes and
+ * the same keep mask (the renumbering is deterministic).  *n_out (host) = this rank's new shard
  * size; BGS_ERR_CAPACITY when it exceeds out->capacity.  out must not alias in.  HOST-SYNC. */
 bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t* keep, const bgs_gaussians_out* out,
                             int64_t* n_out, void* stream);

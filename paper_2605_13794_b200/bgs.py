@@ -96,6 +96,7 @@ _SIGS = {
     "bgs_prune_stochastic": [_vp, C.c_int64, _vp, C.c_int64, C.c_uint64, _vp, _vp],
     "bgs_prune_mass_cut": [_vp, C.c_int64, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp],
     "bgs_redistribute": [_vp, _vp, _vp, _vp, _vp, _vp],
+    "bgs_shard_sizes": [_vp, C.c_int64, _vp],
     "bgs_loss_photo": [_vp, _vp, _vp, C.c_float, C.c_float, _vp, _vp, _vp],
     "bgs_loss_scale": [_vp, _vp, C.c_float, _vp, _vp, _vp],
     "bgs_train_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -335,6 +336,13 @@ def bgs_importance(ctx: Context, n_local: int, radius, w_fixed, a, s, c_rad, c_v
     ctx.check(_lib.bgs_importance(ctx.handle, int(n_local), _ptr(radius), _ptr(w_fixed), _ptr(a), mass_num, mass_den,
                                   _ptr(s), _ptr(c_rad), _ptr(c_vis), _ptr(cull_out), _stream(stream)),
               "bgs_importance")
+
+
+def bgs_shard_sizes(ctx: Context, n_local: int) -> list:
+    """Every rank's shard size (host list), for a skew-triggered redistribution policy."""
+    out = (C.c_int64 * ctx.world)()
+    ctx.check(_lib.bgs_shard_sizes(ctx.handle, int(n_local), out), "bgs_shard_sizes")
+    return [int(v) for v in out]
 
 
 def bgs_loss_photo(ctx: Context, rgb, target, lam: float, batch_inv: float, dL_drgb, out, stream=None):

@@ -1560,6 +1560,18 @@ bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s_sco
   return BGS_OK;
 }
 
+bgs_status bgs_shard_sizes(bgs_ctx* ctx, int64_t n_local, int64_t* sizes_out) {
+  CKS(check_ctx(ctx));
+  if (!sizes_out || n_local < 0) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_shard_sizes: arguments");
+  const int M = ctx->world;
+  if (M > 64) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_shard_sizes: world > 64");
+  std::vector<unsigned long long> sz(size_t(M), 0ull);
+  sz[size_t(ctx->rank)] = (unsigned long long)n_local;
+  CKS(sum_over_ranks(ctx, sz.data(), M, ctx->side ? ctx->side : nullptr));
+  for (int d = 0; d < M; ++d) sizes_out[d] = int64_t(sz[size_t(d)]);
+  return BGS_OK;
+}
+
 bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t* keep, const bgs_gaussians_out* out,
                             int64_t* n_out, void* stream) {
   CKS(check_ctx(ctx));
@@ -1570,12 +1582,17 @@ bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int M = ctx->world, rank = ctx->rank;
   const int64_t n = in->n_local;
-  unsigned long long Nv = (unsigned long long)n;
-  CKS(sum_over_ranks(ctx, &Nv, 1, s));
-  const int64_t N = int64_t(Nv);
-  if (n != (N - rank + M - 1) / M)
-    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_redistribute: shard is not the index-parity slice (S:166)");
-  const int64_t wpr = ((N + M - 1) / M + 31) / 32;  // mask words per rank
+  // every rank's shard size (one-hot sums).  The global order is gid = j M + m over slices padded
+  // to the largest shard (rows j >= n_m are absent, i.e. not kept), so shards left unequal by
+  // density control redistribute as well (P:170 skew-triggered rebalancing)
+  if (M > 64) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_redistribute: world > 64");
+  std::vector<unsigned long long> sz(size_t(M), 0ull);
+  sz[size_t(rank)] = (unsigned long long)n;
+  CKS(sum_over_ranks(ctx, sz.data(), M, s));
+  int64_t n_max = 0;
+  for (unsigned long long v : sz) n_max = std::max<int64_t>(n_max, int64_t(v));
+  const int64_t N = n_max * M;
+  const int64_t wpr = (n_max + 31) / 32;  // mask words per rank
   CKS(ensure(ctx, ctx->masks, size_t(std::max<int64_t>((M + 1) * wpr, 1)) * 4));
   uint32_t* masks = P_<uint32_t>(ctx->masks);
   CK(cudaMemsetAsync(masks, 0, size_t((M + 1) * wpr) * 4, s));

@@ -155,3 +155,51 @@ def test_redistribute_exact_copies(M):
             assert m == len(mine)
             for got, src in zip(arrs, (mo, q, sc, sh, lod)):
                 assert np.array_equal(got.view(np.uint8), src[mine].view(np.uint8)), (n, p, r)
+
+
+@pytest.mark.parametrize("M", [1, 2, 3])
+def test_redistribute_unequal_shards(M):
+    """After density control the shards differ in size; bgs_shard_sizes reports them and
+    bgs_redistribute rebalances in the index-parity order gid = j M + m over slices padded to the
+    largest shard (absent rows not kept), exact copies ((100, 200) -> (150, 150))."""
+    import paper_2605_13794_b200.bgs as B
+    rng = np.random.default_rng(77 + M)
+    sizes = [int(x) for x in rng.integers(300, 1400, M)]
+    if M == 2:
+        sizes = [100, 200]
+    n_max = max(sizes)
+    rows = {}
+    for r in range(M):
+        n = sizes[r]
+        rows[r] = (rng.standard_normal((n, 4)).astype(np.float32), rng.standard_normal((n, 4)).astype(np.float32),
+                   rng.random((n, 4)).astype(np.float32), rng.standard_normal((n, 48)).astype(np.float32),
+                   rng.integers(0, 6, n).astype(np.uint8))
+    keep_by_gid = np.zeros(n_max * M, bool)
+    for r in range(M):
+        keep_by_gid[np.arange(sizes[r]) * M + r] = True  # rebalance: every present row survives
+    new_gid = SO.redistribute(keep_by_gid, M)
+    nk = int(keep_by_gid.sum())
+
+    def fn(r, ctx, st):
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        g = B.GaussianPlanes(*(t(a) for a in rows[r]))
+        sz = B.bgs_shard_sizes(ctx, sizes[r])
+        cap = max(1, (nk + M - 1) // M)
+        out = B.GaussianPlanes(torch.full((cap, 4), np.nan, device="cuda"), torch.zeros(cap, 4, device="cuda"),
+                               torch.zeros(cap, 4, device="cuda"), torch.zeros(cap, 48, device="cuda"),
+                               torch.zeros(cap, dtype=torch.uint8, device="cuda"))
+        kk = torch.ones(max(sizes[r], 1), dtype=torch.uint8, device="cuda")
+        m = B.bgs_redistribute(ctx, g, kk, out, st)
+        return sz, m, [x[:m].cpu().numpy() for x in (out.mean_opac, out.quat, out.scale, out.sh, out.lod)]
+
+    res = _per_rank(M, fn)
+    kept = np.nonzero(keep_by_gid)[0]
+    for r, (sz, m, arrs) in enumerate(res):
+        assert sz == sizes
+        mine = kept[new_gid[kept] % M == r]  # old gids landing on rank r, in new-local order
+        assert m == len(mine) == (nk - r + M - 1) // M
+        for k, got in enumerate(arrs):
+            src = np.stack([rows[g % M][k][g // M] for g in mine]) if len(mine) else got
+            assert np.array_equal(got.view(np.uint8), np.asarray(src).view(np.uint8)), (M, r, k)
+    if M == 2:
+        assert [m for _, m, _ in res] == [150, 150]
