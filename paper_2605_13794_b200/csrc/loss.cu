@@ -161,10 +161,12 @@ __global__ void __launch_bounds__(kLThreads) k_loss_photo(LossArgs a) {
         const float sx2 = m[2][o] - mux * mux, sy2 = m[3][o] - muy * muy, sxy = m[4][o] - mux * muy;
         const float ln = 2.f * mux * muy + kC1, cn = 2.f * sxy + kC2;
         const float ld = mux * mux + muy * muy + kC1, cd = sx2 + sy2 + kC2;
+        // one IEEE reciprocal: 1/ld = cd inv and 1/cd = ld inv (the products round once more than
+        // the quotients would; fp32 tolerance of the parity tests)
         const float inv = 1.f / (ld * cd);
         const float ssim = ln * cn * inv;
-        const float f_mu = 2.f * muy * cn * inv - ssim * 2.f * mux / ld;
-        const float f_s = -ssim / cd;
+        const float f_mu = 2.f * muy * cn * inv - ssim * 2.f * mux * (cd * inv);
+        const float f_s = -ssim * (ld * inv);
         const float f_c = 2.f * ln * inv;
         fa = f_mu - 2.f * mux * f_s - muy * f_c;
         fb = f_s;
