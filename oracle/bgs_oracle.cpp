@@ -132,6 +132,17 @@ template <> double exp_t<double>(double p) { return std::exp(p); }
 
 template <class T>
 T thr_of(T o);
+// -power of Eq.1 on the projected ellipse, power = -1/2 (A dx^2 + C dy^2) - B dx dy (DESIGN.md
+// §4.3, reading R9), evaluated in the pinned order both sides use: with hA = A/2, hC = C/2 (exact),
+// -power = fma(hC dy, dy, fma(B dx, dy, (hA dx) dx)), every product and fma rounded once (std::fma
+// is the correctly rounded IEEE fused multiply-add, the GPU's FFMA)
+template <class T>
+T neg_power(T A, T B, T C, T dx, T dy) {
+  const T hA = k<T>(0.5) * A, hC = k<T>(0.5) * C;
+  const T t1 = (hA * dx) * dx;
+  return std::fma(hC * dy, dy, std::fma(B * dx, dy, t1));
+}
+
 // thr = -log(255 o): alpha = o*G >= 1/255  <=>  power >= thr  (D3; computed in fp64, rounded)
 template <> float thr_of<float>(float o) { return static_cast<float>(-std::log(255.0 * static_cast<double>(o))); }
 template <> double thr_of<double>(double o) { return -std::log(255.0 * o); }
@@ -306,7 +317,7 @@ void composite_tile_pixels(Step<T>& st, const std::vector<int64_t>& list, int ti
         const Proj<T>& p = st.proj[list[kk]];
         // Eq.1 evaluated on the projected ellipse: power = -1/2 d^T Sigma'^-1 d
         T dx = p.mx - T(px), dy = p.my - T(py);
-        T power = (k<T>(-0.5) * ((p.A * dx) * dx + (p.C * dy) * dy)) - (p.B * dx) * dy;
+        T power = -neg_power<T>(p.A, p.B, p.C, dx, dy);
         if (power > T(0)) continue;
         st.margin_thr = std::min(st.margin_thr, std::fabs(double(power) - double(p.thr)));
         if (power < p.thr) continue;  // alpha < 1/255 (R9, D3)
@@ -863,7 +874,7 @@ void or_bruteforce(void* hv, float* img, float* t_final, int32_t* n_contrib_all)
         const Proj<float>& p = st.proj[g];
         if (tx < p.rect[0] || tx >= p.rect[2] || ty < p.rect[1] || ty >= p.rect[3]) continue;
         float dx = p.mx - float(px), dy = p.my - float(py);
-        float power = (-0.5f * ((p.A * dx) * dx + (p.C * dy) * dy)) - (p.B * dx) * dy;
+        float power = -neg_power<float>(p.A, p.B, p.C, dx, dy);
         if (power > 0.f || power < p.thr) continue;
         float G = static_cast<float>(std::exp(double(power)));
         float alpha = std::min(0.99f, p.opac * G);

@@ -28,8 +28,8 @@
 // each lane ending with one value; the 9th with 5 shuffles) and issued as 9 parallel
 // red.global.add.f32 from 9 lanes.
 //
-// The power expression is pinned with __fmul_rn/__fadd_rn (no FMA) so that the alpha-cut
-// decision, n_contrib and a are bit-identical to the oracle's.
+// The power expression is pinned (explicit __fmul_rn / __fmaf_rn, the oracle's neg_power order) so
+// that the alpha-cut decision, n_contrib and a are bit-identical to the oracle's.
 #include "bgs_internal.cuh"
 
 namespace bgs {
@@ -56,16 +56,14 @@ struct WRec {
   float4 rgb;  // r, g, b, -
 };
 
-// nq = -power.  The oracle's pinned fp32 expression is power = (-0.5*((A dx)dx + (C dy)dy)) -
-// (B dx)dy with every op rounded.  Halving A and C is exact and commutes with round-to-nearest
-// (normal range), so with hA = A/2, hC = C/2: RN(RN(hA dx)dx + RN(hC dy)dy) = RN(t1 + t2)/2 and
-// RN(that + (B dx)dy) = -power bit for bit (up to the sign of an exact zero, which no test
-// below distinguishes): one multiply fewer per pixel, same decisions.
+// nq = -power, in the pinned order the oracle uses (bgs_oracle.cpp neg_power):
+// with hA = A/2, hC = C/2 (exact halvings), nq = fma(hC dy, dy, fma(B dx, dy, (hA dx) dx)), every
+// product and fma rounded once, so the alpha-cut decision, n_contrib and a are bit-identical to
+// the oracle's.  (hA dx) dx and B dx depend on the record and the lane's column only, so a slot
+// costs one multiply and two FFMAs.
 __device__ __forceinline__ float pinned_negpower(float hA, float B, float hC, float dx, float dy) {
   const float t1 = __fmul_rn(__fmul_rn(hA, dx), dx);
-  const float t2 = __fmul_rn(__fmul_rn(hC, dy), dy);
-  const float t3 = __fmul_rn(__fmul_rn(B, dx), dy);
-  return __fadd_rn(__fadd_rn(t1, t2), t3);
+  return __fmaf_rn(__fmul_rn(hC, dy), dy, __fmaf_rn(__fmul_rn(B, dx), dy, t1));
 }
 
 // power <= 0 && power >= thr  <=>  nq >= 0 && nq <= -thr (also for +-0)
