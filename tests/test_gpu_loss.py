@@ -113,3 +113,17 @@ def test_scale_regulariser_parity(tiny_loss):
     nz = g != 0
     want[:, :3][nz] = np.float32(0.5 / nv)
     assert np.array_equal(gs.g_scale_reg, want)
+
+
+def test_photo_loss_full_size():
+    """BASELINE image size (1152x864, the bench's Rubble views) with many 32x32 loss tiles and a ragged
+    last tile row (864 = 27 x 32; 1152 = 36 x 32): loss terms and the gradient on every pixel."""
+    sc = S.gen_small(23, 3000, 1152, 864, spread=2.0)
+    cam = sc.cameras[0]
+    tgt = S.target_image(cam["H"], cam["W"], seed=8)
+    gs = GpuStep(sc, cam, M=1, target=tgt, lam=LAM, batch_inv=BINV, importance=False)
+    try:
+        assert gs.img.max() > 0.05  # something rendered
+        _check_photo(gs, tgt)
+    finally:
+        gs.close()
