@@ -421,6 +421,36 @@ def run_native(args):
                 stream.synchronize()
                 score_ms += sev[0].elapsed_time(sev[1])
     score_ms_max = D.max_over_ranks(score_ms, torch.device(dev)) / args.steps
+
+    # the same sweep step with the views in flight (a scoring pass sweeps all V training views, so
+    # its views overlap like the training batch's): one ctx + stream per view in flight
+    def score_on(k, v):
+        p = per[k]
+        cam = cams[v % len(cams)]
+        cull = cull_cols[v % len(cams)] if cull_cols is not None else None
+        st_k = p["stream"]
+        B.bgs_project(ctxs[k], g, cam, gate, cull, B.BGS_NO_COLOR, p["radius"], st_k)
+        B.bgs_route(ctxs[k], None, st_k)
+        B.bgs_sort_tiles(ctxs[k], st_k)
+        B.bgs_raster_fwd(ctxs[k], B.BGS_IMPORTANCE, p["rgb"], p["Tf"], p["nc"], st_k)
+        B.bgs_route_reverse(ctxs[k], st_k)
+        B.bgs_importance(ctxs[k], n_local, p["radius"], None, None, s_imp, c_rad, c_vis, p["cull"], 99, 100, st_k)
+
+    for k in range(inflight):
+        score_on(k, args.warmup + k)
+    torch.cuda.synchronize()
+    barrier()
+    sev_start = torch.cuda.Event(enable_timing=True)
+    sev_end = [torch.cuda.Event(enable_timing=True) for _ in range(inflight)]
+    sev_start.record(per[0]["stream"])
+    for k in range(1, inflight):
+        per[k]["stream"].wait_event(sev_start)
+    submit_views(score_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads), local)
+    for k in range(inflight):
+        sev_end[k].record(per[k]["stream"])
+    torch.cuda.synchronize()
+    score_inflight_ms = D.max_over_ranks(max(sev_start.elapsed_time(e) for e in sev_end),
+                                         torch.device(dev)) / args.steps
     P_max = D.max_over_ranks(P_rank, torch.device(dev))
 
     # ---- NEXT-1 scheduled simplification on the same shard, with the s / c_rad / c_vis the
@@ -495,7 +525,11 @@ def run_native(args):
                      "owned_pairs_max_over_mean": (P_max * world / P_all) if P_all else None},
         "scoring": {"metric": "scoring views/s (a1-a8 NO_COLOR + a10 + a12, no backward)",
                     "value": round(1000.0 / score_ms_max, 3) if score_ms_max > 0 else None, "unit": "views/s",
-                    "ms_per_view": round(score_ms_max, 4)},
+                    "ms_per_view": round(score_ms_max, 4),
+                    "note": "value: one view at a time, L2 flushed before each; in_flight: the sweep's views "
+                            "overlapped like the training batch (one ctx + stream each)",
+                    "in_flight": {"value": round(1000.0 / score_inflight_ms, 3), "unit": "views/s",
+                                  "ms_per_view": round(score_inflight_ms, 4), "views_in_flight": inflight}},
         "simplify": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in simplify.items()},
         "train": train,
         "stages_ms": {n: round(float(v), 4) for n, v in zip(stage_names, stage_avg)},
