@@ -134,3 +134,54 @@ def test_apply_capacity_and_empty():
         assert math.isfinite(float(tout.mean_logit.sum().item()))
     finally:
         ctx.close()
+
+
+def test_apply_full_size_sampled():
+    """A 2M-row shard: category totals exact (oracle decisions over every row), and 3000 sampled
+    kept originals / clones / children at their oracle positions (kept: rank among kept; clones:
+    K + rank among clones; children: K + C + c S + rank among split parents)."""
+    import paper_2605_13794_b200.bgs as B
+    n = 2_000_003
+    params, state, lod, stat, count = _shard(n, 99)
+    dev = "cuda"
+    keys = ("mean_logit", "quat_raw", "log_scale", "sh")
+    tin = B.TrainParams(*(torch.from_numpy(params[k]).to(dev) for k in keys))
+    for j, k in enumerate(keys):
+        tin.m[j].copy_(torch.from_numpy(state["m"][k]))
+        tin.v[j].copy_(torch.from_numpy(state["v"][k]))
+    cap = 2 * n + 1
+    tout = B.TrainParams(*(torch.empty(cap, c, device=dev) for c in (4, 4, 4, 48)))
+    lod_out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    ctx = B.Context(0, 1, 0)
+    try:
+        nn = B.bgs_densify_apply(ctx, tin, torch.from_numpy(lod).to(dev), torch.from_numpy(stat).to(dev),
+                                 torch.from_numpy(count).to(dev), B.densify_params(TAU, EXT, MINO, DIV, SEED), tout,
+                                 lod_out, None)
+        torch.cuda.synchronize()
+        keep, clone, split = DC.decide(params, stat, count, TAU, EXT, MINO)
+        K, Cn, Sn = int(keep.sum()), int(clone.sum()), int(split.sum())
+        assert nn == K + Cn + 2 * Sn and Cn > 0 and Sn > 0
+        rng = np.random.default_rng(4)
+        ck = np.cumsum(keep) - 1
+        cc = np.cumsum(clone) - 1
+        cs = np.cumsum(split) - 1
+        ml_out = tout.mean_logit
+        for cat, mask, pos in (("keep", keep, lambda i: ck[i]), ("clone", clone, lambda i: K + cc[i])):
+            for i in rng.choice(np.flatnonzero(mask), 1000, replace=False):
+                got = ml_out[int(pos(i))].cpu().numpy()
+                assert np.array_equal(got, params["mean_logit"][i]), (cat, i)
+                assert int(lod_out[int(pos(i))].item()) == int(lod[i]), (cat, i)
+        for i in rng.choice(np.flatnonzero(split), 500, replace=False):
+            for c in range(2):
+                q = K + Cn + c * Sn + int(cs[i])
+                got = ml_out[q].double().cpu().numpy()
+                # child c of parent gid i: mu + R(q) (s z) with the oracle's sampler
+                qr = params["quat_raw"][i].astype(np.float64)
+                R = DC.rotation(qr / np.linalg.norm(qr))
+                s = np.exp(params["log_scale"][i, :3].astype(np.float64))
+                z = np.array([DC.normal01(SEED, int(i), c, a) for a in range(3)])
+                want = params["mean_logit"][i, :3].astype(np.float64) + R @ (s * z)
+                assert np.all(np.abs(got[:3] - want) <= 1e-6 * np.abs(want) + 1e-5 * s.max()), (i, c)
+                assert int(lod_out[q].item()) == min(255, int(lod[i]) + 1)
+    finally:
+        ctx.close()

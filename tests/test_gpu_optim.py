@@ -109,3 +109,43 @@ def test_adam_edge_cases():
         assert float(p.mean_logit.sum().item()) == 4.0 * n  # nothing written on refusal
     finally:
         ctx.close()
+
+
+def test_adam_full_size_sampled():
+    """The Rubble shard size (6M rows), three steps; 20000 sampled rows against the oracle."""
+    import paper_2605_13794_b200.bgs as B
+    n = 6_000_000
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    dev = "cuda"
+
+    def rnd(*shape):
+        return torch.randn(*shape, device=dev, generator=gen)
+
+    tp = B.TrainParams(rnd(n, 4), rnd(n, 4), torch.cat([rnd(n, 3) * 0.5 - 3.0, torch.zeros(n, 1, device=dev)], 1),
+                       rnd(n, 48))
+    idx = torch.randperm(n, generator=torch.Generator().manual_seed(5))[:20000].sort().values
+    p = {k: getattr(tp, k)[idx.to(dev)].double().cpu().numpy() for k in ("mean_logit", "quat_raw", "log_scale", "sh")}
+    st = {"m": {k: np.zeros_like(v) for k, v in p.items()}, "v": {k: np.zeros_like(v) for k, v in p.items()}}
+    act = B.GaussianPlanes(torch.zeros(n, 4, device=dev), torch.zeros(n, 4, device=dev), torch.zeros(n, 4, device=dev),
+                           tp.sh, torch.zeros(n, dtype=torch.uint8, device=dev))
+    gp = B.GradPlanes(*(torch.zeros(n, c, device=dev) for c in (4, 4, 4, 48)))
+    ctx = B.Context(0, 1, 0)
+    try:
+        for t in range(1, 4):
+            g = {"mean_opac": rnd(n, 4), "quat": rnd(n, 4), "scale": torch.cat([rnd(n, 3), torch.zeros(n, 1, device=dev)], 1),
+                 "sh": rnd(n, 48)}
+            gs = {k: v[idx.to(dev)].double().cpu().numpy() for k, v in g.items()}
+            for k in ("mean_opac", "quat", "scale", "sh"):
+                getattr(gp, k).copy_(g[k])
+            B.bgs_adam_step(ctx, tp, gp, act, None, B.adam_hparams(**H, step=t))
+            torch.cuda.synchronize()
+            p, st, a = OP.adam_step(p, st, gs, dict(H, step=t))
+        lr_of = {"mean_logit": np.r_[[H["lr_mean"]] * 3, H["lr_opacity"]], "quat_raw": H["lr_quat"],
+                 "log_scale": H["lr_scale"], "sh": OP.sh_lr(len(idx), H["lr_sh_dc"], H["lr_sh_rest"])}
+        for k in ("mean_logit", "quat_raw", "log_scale", "sh"):
+            got = getattr(tp, k)[idx.to(dev)].double().cpu().numpy()
+            assert np.all(np.abs(got - p[k]) <= 1e-6 * np.abs(p[k]) + 1e-3 * lr_of[k]), k
+        got = act.mean_opac[idx.to(dev)].double().cpu().numpy()
+        assert np.allclose(got, a["mean_opac"], rtol=2e-6, atol=1e-7)
+    finally:
+        ctx.close()
