@@ -190,6 +190,9 @@ class Context:
             st = _cudart().cudaMemcpy(C.c_void_p(out.data_ptr()), p, C.c_size_t(n), 3)  # device to device
             if int(st) != 0:
                 raise RuntimeError(f"cudaMemcpy failed: {st}")
+            # a device-to-device cudaMemcpy does not block the host, and it runs on the legacy
+            # stream, which torch's non-blocking streams do not wait for: finish it before `out` is used
+            torch.cuda.synchronize(self.device)
         return out.view(dtype) if n else out
 
     def close(self):
