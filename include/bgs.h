@@ -158,6 +158,7 @@ bgs_status bgs_query(bgs_ctx* ctx, int64_t* out /*[BGS_Q_COUNT] host*/);
  *   8 tile owner map [T] i32    9 dest mask [F] u8    10 per-tile pair counts (all ranks) [T] i32
  *   11 device counters [8] u64 (0 F, 1 P_all, 2 n_lod, 3 n_active, 4 P, 5 candidates, 6 and 7 the
  *      depth range of buffer 3) */
+/* (synchronizes the ctx's device before answering: a test-only accessor) */
 bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** dev_ptr, int64_t* bytes);
 
 /* ---------------------------------------------------------------------------------------

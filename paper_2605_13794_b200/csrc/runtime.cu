@@ -463,7 +463,11 @@ bgs_status bgs_query(bgs_ctx* ctx, int64_t* out) {
 }
 
 bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** ptr, int64_t* bytes) {
+  // test-only accessor: settle all queued work first (the selectors below are read with a
+  // synchronous copy on the legacy stream, which does not wait for non-blocking streams)
   if (!ctx || !ptr || !bytes) return BGS_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
   void* p = nullptr;
   int64_t b = 0;
   uint32_t sel = 0;
