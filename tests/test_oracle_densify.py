@@ -3,7 +3,6 @@
 import math
 
 import numpy as np
-import pytest
 from scipy import stats
 
 from oracle import densify as DC
