@@ -8,7 +8,6 @@ chosen away from every discontinuity (alpha cut, 0.99 clamp, early stop, integer
 rect): the test asserts the margins before differencing.
 """
 import numpy as np
-import pytest
 
 import oracle as O
 import synthetic as S
