@@ -53,7 +53,7 @@ struct bgs_ctx {
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
       imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask,
-      loss_img, loss_part, loss_sums, scr_tgt, scr_loss;
+      loss_img, loss_part, loss_sums, scr_tgt, scr_loss, scr_in2;
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
@@ -64,6 +64,10 @@ struct bgs_ctx {
   bool stage_timing = false, stage_recorded = false;  // bgs_set_stage_timing / bgs_stage_times
   cudaStream_t h2d = nullptr, d2h = nullptr;          // host-buffer step: copy streams
   cudaEvent_t ev_in = nullptr, ev_dl = nullptr, ev_fwd = nullptr, ev_out = nullptr;
+  // host-buffer steps: the uploaded input (dL/dC or the target) alternates between two buffers, so
+  // a view's upload waits only for the view two steps back that read the same buffer
+  cudaEvent_t ev_in_free[2] = {nullptr, nullptr};
+  int in_parity = 0;
   cudaEvent_t stage_ev[kStages + 1] = {};
   std::vector<int64_t> send_cnt, recv_cnt, send_off, recv_off;
 };
@@ -428,7 +432,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -440,7 +444,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   for (cudaEvent_t e : c->stage_ev)
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_in, c->ev_dl, c->ev_fwd, c->ev_out})
+  for (cudaEvent_t e : {c->ev_in, c->ev_dl, c->ev_fwd, c->ev_out, c->ev_in_free[0], c->ev_in_free[1]})
     if (e) cudaEventDestroy(e);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
@@ -1015,7 +1019,7 @@ static bgs_status copy_streams(bgs_ctx* ctx) {
   if (!ctx->h2d) {
     CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ctx->ev_in, &ctx->ev_dl, &ctx->ev_fwd, &ctx->ev_out})
+    for (cudaEvent_t* e : {&ctx->ev_in, &ctx->ev_dl, &ctx->ev_fwd, &ctx->ev_out, &ctx->ev_in_free[0], &ctx->ev_in_free[1]})
       CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   return BGS_OK;
@@ -1114,17 +1118,22 @@ bgs_status bgs_train_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, 
   CKS(ensure(ctx, ctx->scr_t, npix * 4));
   CKS(ensure(ctx, ctx->scr_n, npix * 4));
   CKS(ensure(ctx, ctx->scr_loss, 8 * sizeof(double)));
+  CKS(ensure(ctx, ctx->scr_in2, npix * 12));
   CKS(copy_streams(ctx));
-  // target upload on its own copy engine (needed only by the loss, after the forward); the loss
-  // download starts as soon as the loss is final, overlapping the backward
-  CK(cudaEventRecord(ctx->ev_in, s));
-  CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_in, 0));
-  CK(cudaMemcpyAsync(ctx->scr_tgt.p, target_host, npix * 12, cudaMemcpyHostToDevice, ctx->h2d));
+  // target upload on its own copy engine into the buffer this ctx's view before last used (needed
+  // only by the loss, after the forward); the loss download starts as soon as the loss is final,
+  // overlapping the backward
+  const int b = ctx->in_parity;
+  ctx->in_parity ^= 1;
+  float* tgt = P_<float>(b ? ctx->scr_in2 : ctx->scr_tgt);
+  CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_in_free[b], 0));
+  CK(cudaMemcpyAsync(tgt, target_host, npix * 12, cudaMemcpyHostToDevice, ctx->h2d));
   CK(cudaEventRecord(ctx->ev_dl, ctx->h2d));
-  bgs_supervision sup{P_<float>(ctx->scr_tgt), lambda, batch_inv, beta, P_<double>(ctx->scr_loss)};
+  bgs_supervision sup{tgt, lambda, batch_inv, beta, P_<double>(ctx->scr_loss)};
   CKS(view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
                      P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), nullptr, grads, imp, stream, ctx->ev_dl,
                      nullptr, &sup, P_<float>(ctx->scr_dl), ctx->ev_fwd));
+  CK(cudaEventRecord(ctx->ev_in_free[b], s));
   CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_fwd, 0));
   CK(cudaMemcpyAsync(loss_host, ctx->scr_loss.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h));
   CK(cudaEventRecord(ctx->ev_out, ctx->d2h));
@@ -1162,16 +1171,20 @@ bgs_status bgs_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const 
   CKS(ensure(ctx, ctx->scr_dl, npix * 12));
   CKS(ensure(ctx, ctx->scr_t, npix * 4));
   CKS(ensure(ctx, ctx->scr_n, npix * 4));
+  CKS(ensure(ctx, ctx->scr_in2, npix * 12));
   CKS(copy_streams(ctx));
-  // dL/dC upload on its own copy engine, needed only by the compositing backward; it starts once
-  // this ctx's previous step no longer reads the scratch (everything queued on s so far)
-  CK(cudaEventRecord(ctx->ev_in, s));
-  CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_in, 0));
-  CK(cudaMemcpyAsync(ctx->scr_dl.p, dL_host, npix * 12, cudaMemcpyHostToDevice, ctx->h2d));
+  // dL/dC upload on its own copy engine, needed only by the compositing backward, into the buffer
+  // this ctx's view before last read (two alternating buffers): it overlaps the previous view
+  const int b = ctx->in_parity;
+  ctx->in_parity ^= 1;
+  float* dl = P_<float>(b ? ctx->scr_in2 : ctx->scr_dl);
+  CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_in_free[b], 0));
+  CK(cudaMemcpyAsync(dl, dL_host, npix * 12, cudaMemcpyHostToDevice, ctx->h2d));
   CK(cudaEventRecord(ctx->ev_dl, ctx->h2d));
   CKS(view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
-                     P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), P_<float>(ctx->scr_dl), grads, imp, stream,
+                     P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), dl, grads, imp, stream,
                      ctx->ev_dl, ctx->ev_fwd));
+  CK(cudaEventRecord(ctx->ev_in_free[b], s));
   // the image is final after the forward: download it while the backward runs; the working
   // stream then waits for the download, so a sync of `stream` covers rgb_host
   CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_fwd, 0));
