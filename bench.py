@@ -54,8 +54,8 @@ def parse():
                         "a context's HOST-SYNC calls block only its own thread; 0: one thread submits all views")
     p.add_argument("--inflight", type=int, default=4,
                    help="views in flight per rank (one ctx + stream each); 4 = the paper's batch of B = 4 "
-                        "views per step (P:342). Measured on Rubble: 1 -> 1061, 2 -> 1183, 3 -> 1220, "
-                        "4 -> 1224 views/s")
+                        "views per step (P:342). Measured on Rubble (second session): 1 -> 1219, 4 -> 1383, "
+                        "6 -> 1388, 8 -> 1386 views/s")
     return p.parse_args()
 
 
