@@ -59,6 +59,10 @@ def lib():
         _lib.or_get.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_void_p]
         _lib.or_d2_threshold.restype = C.c_float
         _lib.or_d2_threshold.argtypes = [C.c_double, C.c_int32]
+        _lib.or_thr.restype = C.c_float
+        _lib.or_thr.argtypes = [C.c_float]
+        _lib.or_ln.restype = C.c_double
+        _lib.or_ln.argtypes = [C.c_double]
         _lib.or_sh_basis.argtypes = [C.c_double, C.c_double, C.c_double, C.c_void_p]
         _lib.or_bruteforce.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.or_importance.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
@@ -156,6 +160,15 @@ class OracleStep:
 
 def d2_threshold(d0: float, l: int) -> float:
     return float(lib().or_d2_threshold(d0, l))
+
+
+def thr(o: float) -> float:
+    """O3 alpha-cut threshold thr = (float)(-ln(255 o)) with the oracle's fixed-sequence ln."""
+    return float(lib().or_thr(float(o)))
+
+
+def ln_fixed(u: float) -> float:
+    return float(lib().or_ln(float(u)))
 
 
 def sh_basis(d) -> np.ndarray:

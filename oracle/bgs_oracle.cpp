@@ -143,8 +143,31 @@ T neg_power(T A, T B, T C, T dx, T dy) {
   return std::fma(hC * dy, dy, std::fma(B * dx, dy, t1));
 }
 
-// thr = -log(255 o): alpha = o*G >= 1/255  <=>  power >= thr  (D3; computed in fp64, rounded)
-template <> float thr_of<float>(float o) { return static_cast<float>(-std::log(255.0 * static_cast<double>(o))); }
+// Natural logarithm in a fixed sequence of IEEE fp64 operations (reading R30, used for
+// thr below so that the alpha-cut threshold is the same bits on both sides by construction rather
+// than by two libm's agreeing): u = m 2^e, m in [sqrt(2)/2, sqrt(2)) (exact split),
+// ln m = 2 atanh(f) with f = (m - 1)/(m + 1) and the odd series sum_{k<12} f^(2k+1)/(2k+1) in
+// Horner form; -ffp-contract=off keeps every step one rounded operation.  Pinned against libm's
+// log and oracle/simplify.py in tests/test_oracle_pins.py (P17).
+double ln_fixed(double u) {
+  int e = 0;
+  double m = std::frexp(u, &e);  // u = m 2^e, m in [0.5, 1): exact
+  m = m * 2.0;
+  e -= 1;
+  if (m > 1.4142135623730951) {
+    m = m * 0.5;
+    e += 1;
+  }
+  const double f = (m - 1.0) / (m + 1.0);
+  const double f2 = f * f;
+  double p = 1.0 / 23.0;
+  for (int k = 10; k >= 0; --k) p = p * f2 + 1.0 / double(2 * k + 1);
+  const double lm = (f + f) * p;
+  return double(e) * 0.6931471805599453 + lm;
+}
+
+// thr = -ln(255 o): alpha = o*G >= 1/255  <=>  power >= thr  (D3; computed in fp64, rounded)
+template <> float thr_of<float>(float o) { return static_cast<float>(-ln_fixed(255.0 * static_cast<double>(o))); }
 template <> double thr_of<double>(double o) { return -std::log(255.0 * o); }
 
 template <class T>
@@ -850,6 +873,9 @@ int64_t or_get(void* hv, const char* name, int32_t rank, void* out) {
 }
 
 float or_d2_threshold(double d0, int32_t l) { return d2_threshold(d0, l); }
+
+float or_thr(float o) { return thr_of<float>(o); }
+double or_ln(double u) { return ln_fixed(u); }
 
 void or_sh_basis(double x, double y, double z, double* Y) { sh_basis<double>(x, y, z, Y); }
 

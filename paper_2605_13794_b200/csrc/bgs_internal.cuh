@@ -350,4 +350,32 @@ int64_t densify_n_blocks(int64_t n);
 void launch_densify_count(const DensifyArgs& a, cudaStream_t s);
 void launch_densify_emit(const DensifyArgs& a, cudaStream_t s);
 
+// Pinned fp64 natural logarithm (reading R30; also the alpha-cut threshold thr = -ln(255 o), D3):
+// u = m 2^e with m in [sqrt(2)/2, sqrt(2)) (exact split), ln(m) = 2 atanh(f), f = (m - 1)/(m + 1),
+// the 12-term odd series in Horner form, every step one correctly rounded IEEE op (explicit _rn
+// intrinsics: no contraction in any TU), so the oracle's plain-C++ / numpy versions of the same
+// steps give the same bits.  u > 0, normal, finite.
+__device__ __forceinline__ double ln_pinned(double u) {
+  // 1/(2k+1) as correctly rounded doubles (compile-time IEEE division)
+  constexpr double kInvOdd[12] = {1.0 / 1,  1.0 / 3,  1.0 / 5,  1.0 / 7,  1.0 / 9,  1.0 / 11,
+                                  1.0 / 13, 1.0 / 15, 1.0 / 17, 1.0 / 19, 1.0 / 21, 1.0 / 23};
+  const unsigned long long b = __double_as_longlong(u);
+  int e = int((b >> 52) & 0x7ff) - 1023;
+  double m = __longlong_as_double((long long)((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull));  // [1, 2)
+  if (m > 1.4142135623730951) {
+    m = __dmul_rn(m, 0.5);
+    e += 1;
+  }
+  const double f = __ddiv_rn(__dadd_rn(m, -1.0), __dadd_rn(m, 1.0));
+  const double f2 = __dmul_rn(f, f);
+  double p = kInvOdd[11];
+#pragma unroll
+  for (int k = 10; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, f2), kInvOdd[k]);
+  const double lm = __dmul_rn(__dadd_rn(f, f), p);
+  return __dadd_rn(__dmul_rn(double(e), 0.6931471805599453), lm);
+}
+
+// thr = -ln(255 o) rounded to float: alpha = o G >= 1/255 <=> power >= thr (D3), pinned (above)
+__device__ __forceinline__ float alpha_cut_thr(float o) { return float(-ln_pinned(__dmul_rn(255.0, double(o)))); }
+
 }  // namespace bgs

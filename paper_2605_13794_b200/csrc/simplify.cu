@@ -19,14 +19,6 @@ namespace bgs {
 
 namespace {
 
-constexpr double kLn2 = 0.6931471805599453;
-constexpr double kSqrt2 = 1.4142135623730951;
-constexpr int kSeries = 12;
-// 1/(2k+1) as correctly rounded doubles: compile-time IEEE division gives the same bits as the
-// oracle's runtime np.float64(1.0) / np.float64(2k+1)
-__constant__ double kInvOdd[kSeries] = {1.0 / 1,  1.0 / 3,  1.0 / 5,  1.0 / 7,  1.0 / 9,  1.0 / 11,
-                                        1.0 / 13, 1.0 / 15, 1.0 / 17, 1.0 / 19, 1.0 / 21, 1.0 / 23};
-
 __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
   unsigned long long z = x + 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -37,24 +29,6 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 __device__ __forceinline__ double uniform_open(unsigned long long seed, unsigned long long gid) {
   const unsigned long long x = mix64(seed ^ mix64(gid));
   return __dmul_rn(__dadd_rn(double(x >> 11), 0.5), 1.1102230246251565e-16);  // 2^-53
-}
-
-// ln(u), u > 0 finite, bit-identical to oracle/simplify.py ln_pinned (R30)
-__device__ double ln_pinned(double u) {
-  const unsigned long long b = __double_as_longlong(u);
-  int e = int((b >> 52) & 0x7ff) - 1023;
-  double m = __longlong_as_double((long long)((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull));  // [1, 2)
-  if (m > kSqrt2) {
-    m = __dmul_rn(m, 0.5);
-    e += 1;
-  }
-  const double f = __ddiv_rn(__dadd_rn(m, -1.0), __dadd_rn(m, 1.0));
-  const double f2 = __dmul_rn(f, f);
-  double p = kInvOdd[kSeries - 1];
-#pragma unroll
-  for (int k = kSeries - 2; k >= 0; --k) p = __dadd_rn(__dmul_rn(p, f2), kInvOdd[k]);
-  const double lm = __dmul_rn(__dadd_rn(f, f), p);
-  return __dadd_rn(__dmul_rn(double(e), kLn2), lm);
 }
 
 // order-preserving map of a double onto u64 (larger double -> larger u64)

@@ -99,12 +99,12 @@ __global__ void __launch_bounds__(256) k_emit(SortArgs a) {
     dbits = q2.y;
     if (a.aux) {
       // per-record raster constants, computed once here instead of once per (tile, warp):
-      // thr = -log(255 o) (alpha >= 1/255 <=> power >= thr, D3) and the half extents of the
+      // thr = -ln(255 o) (alpha >= 1/255 <=> power >= thr, D3; pinned fp64 ln, bgs_internal.cuh) and the half extents of the
       // ellipse {d : d^T Q d <= -2 thr} (sqrt(-2 thr (Q^-1)_xx), sqrt(-2 thr (Q^-1)_yy)) widened
       // by 1e-3 relative + 0.01 px so that box culling is conservative under fp32 rounding
       const float4 q0 = __ldg(reinterpret_cast<const float4*>(a.recv + r));
       const float4 q1 = __ldg(reinterpret_cast<const float4*>(a.recv + r) + 1);
-      const float thr = float(-log(255.0 * double(q1.y)));
+      const float thr = alpha_cut_thr(q1.y);
       const float k = -2.0f * thr;
       const float det = q0.z * q1.x - q0.w * q0.w;
       float hx = -1e30f, hy = -1e30f;  // empty box: never contributes

@@ -25,26 +25,60 @@ def _f32(x):
     return np.asarray(x, np.float64).astype(np.float32)
 
 
-def _flip_info(st, gs, cam):
-    """Pixels whose early-stop decision may legitimately differ (exp rounding), and the gids
-    whose a / w / gradients they can affect (every splat of that pixel's list up to max nc)."""
+def _flip_info(st, gs, cam, sample=None):
+    """Pixels whose early-stop decision actually differs between the oracle and the GPU (exp
+    rounding), and the gids whose a / w / gradients those flips can affect (every
+    splat of that pixel's list up to the deeper of the two stops).  Candidates (oracle test value
+    T(1-alpha) within ET_MARGIN relative of 1e-4) are reported, but only actual flips excuse
+    anything.  `sample`: restrict to a boolean pixel mask (tile-sampled oracle runs)."""
     H, W = cam["H"], cam["W"]
     margin = st.get("et_margin").reshape(H, W)
     nc_o = st.get("n_contrib").reshape(H, W)
     cand = margin < ET_MARGIN
-    diff = (nc_o != gs.nc)
-    flips = diff & cand
+    flips = (nc_o != gs.nc) & cand
+    if sample is not None:
+        cand, flips = cand & sample, flips & sample
     affected = set()
     TX = (W + 15) // 16
-    ys, xs = np.nonzero(cand)
-    tiles = st.get("pair_tile", 0)
-    gids = st.get("pair_gid", 0)
-    lo, hi = st.get("range_lo", 0), st.get("range_hi", 0)
-    for y, x in zip(ys, xs):
+    for y, x in zip(*np.nonzero(flips)):
         t = (y // 16) * TX + x // 16
+        for r in range(st.M):
+            b, e = st.get("tile_range", r)
+            if b <= t < e:
+                break
+        gids = st.get("pair_gid", r)
+        lo, hi = st.get("range_lo", r), st.get("range_hi", r)
         upto = max(nc_o[y, x], gs.nc[y, x]) + 1
-        affected.update(gids[lo[t]:min(hi[t], lo[t] + upto)].tolist())
+        lt = t - b
+        affected.update(gids[lo[lt]:min(hi[lt], lo[lt] + upto)].tolist())
     return cand, flips, affected
+
+
+def _excused_ok(st, gs, affected):
+    """The excusal stays small: under 1% of the splats that contribute to the view."""
+    contributing = int((st.get("a") > 0).sum())
+    assert len(affected) <= 0.01 * max(contributing, 1), (len(affected), contributing)
+
+
+def _check_grads(sc_n, st, gs, keep, group_tol=1e-3, what=""):
+    """Parameter gradients vs the oracle: |d| <= 1e-3 |g| + 1e-5 max|g| per group."""
+    for name, width in (("d_mean", 3), ("d_quat", 4), ("d_scale", 3), ("d_opac", 1), ("d_sh", 48)):
+        ref = st.get(name).reshape(sc_n, width)[keep]
+        got = gs.grads[name].reshape(sc_n, width)[keep]
+        tol = group_tol * np.abs(ref) + 1e-5 * np.abs(ref).max(initial=0)
+        bad = np.abs(got - ref) > tol
+        assert not bad.any(), (what, name, int(bad.sum()),
+                               float(np.max(np.abs(got - ref) / (np.abs(ref) + 1e-30), initial=0)))
+
+
+def _check_g2d(st, gs, keep, what=""):
+    """The 9 owner-summed compositing partials dL/d(mx, my, A, B, C, o, r, g, b) per splat."""
+    g_ref = st.get("g2d").reshape(-1, 9)
+    for k in range(9):
+        ref, got = g_ref[keep, k], gs.g2d[keep, k]
+        tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max(initial=0)
+        bad = np.abs(got - ref) > tol
+        assert not bad.any(), (what, k, int(bad.sum()))
 
 
 @pytest.fixture(scope="module")
@@ -107,25 +141,22 @@ def test_raster_fwd_parity(tiny_run):
     keep[list(affected)] = False
     dw = np.abs(gs.w.astype(np.float64) - w_o.astype(np.float64))
     assert np.all(dw[keep] <= a_o[keep] + 1e-5 * w_o[keep].astype(np.float64))
+    _excused_ok(st, gs, affected)
     print(f"flip candidates {cand.sum()}, flips {flips.sum()}, affected splats {len(affected)}")
 
 
 def test_backward_parity(tiny_run):
+    """All 9 compositing partials and every parameter gradient of every splat except those whose
+    list holds an actual early-stop flip (<= 1% of the contributing splats; 0 on this scene)."""
     sc, cam, dl, st, gs = tiny_run
-    _, _, affected = _flip_info(st, gs, cam)
+    _, flips, affected = _flip_info(st, gs, cam)
+    _excused_ok(st, gs, affected)
     keep = np.ones(sc.n, bool)
     keep[list(affected)] = False
-    g_ref = st.get("g2d").reshape(-1, 9)
-    for k in range(9):
-        ref, got = g_ref[keep, k], gs.g2d[keep, k]
-        tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
-        assert np.all(np.abs(got - ref) <= tol), k
-    for name, width in (("d_mean", 3), ("d_quat", 4), ("d_scale", 3), ("d_opac", 1), ("d_sh", 48)):
-        ref = st.get(name).reshape(sc.n, width)[keep]
-        got = gs.grads[name].reshape(sc.n, width)[keep]
-        tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
-        bad = np.abs(got - ref) > tol
-        assert not bad.any(), (name, int(bad.sum()), float(np.max(np.abs(got - ref) / (np.abs(ref) + 1e-30))))
+    contributing = st.get("a") > 0
+    assert (keep & contributing).sum() >= 0.99 * contributing.sum()
+    _check_g2d(st, gs, keep, "tiny")
+    _check_grads(sc.n, st, gs, keep, what="tiny")
 
 
 def test_importance_parity(tiny_run):
@@ -220,10 +251,21 @@ def test_multirank_local_group_parity(tiny_scene, tiny_run, M):
         assert np.array_equal(gs.img, gs1.img) and np.array_equal(gs.T, gs1.T) and np.array_equal(gs.nc, gs1.nc)
         assert np.array_equal(gs.a, gs1.a) and np.array_equal(gs.w, gs1.w)
         assert np.array_equal(gs.c_vis, gs1.c_vis) and np.array_equal(gs.cull_bits, gs1.cull_bits)
-        for name in ("d_mean", "d_quat", "d_scale", "d_opac", "d_sh"):
-            ref = gs1.grads[name]
-            tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
-            assert np.all(np.abs(gs.grads[name] - ref) <= tol), name
+        # against the oracle at the same M (owner partials summed in dest-rank order, O10): pixels,
+        # counts, a, w and every gradient, excusing only actual early-stop flips
+        H, W = cam["H"], cam["W"]
+        cand, flips, affected = _flip_info(st, gs, cam)
+        _excused_ok(st, gs, affected)
+        ok = ~flips
+        assert np.abs(gs.img - st.get("img").reshape(3, H, W))[:, ok].max() <= 1e-4
+        assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
+        keep = np.ones(sc.n, bool)
+        keep[list(affected)] = False
+        assert np.array_equal(gs.a[keep], st.get("a")[keep])
+        w_o = st.get("w_fixed").astype(np.float64)
+        assert np.all(np.abs(gs.w.astype(np.float64) - w_o)[keep] <= st.get("a")[keep] + 1e-5 * w_o[keep])
+        _check_g2d(st, gs, keep, f"M={M}")
+        _check_grads(sc.n, st, gs, keep, what=f"M={M}")
     finally:
         gs.close()
 
@@ -285,44 +327,102 @@ def test_spatial_order_layout():
         gs.close()
 
 
-@pytest.mark.parametrize("config,view", [("rubble", 7)])
-def test_full_size_sampled(config, view):
-    """BASELINE configs[1] at full size (6M Gaussians, 1152x864) in the bench's launch
-    configuration: projection, records, the complete sorted pair sequence and ranges bit-exact;
-    pixels compared on a 1/16 sample of the tiles (the ones the oracle composites)."""
-    sc = S.gen_city(config)
-    cam = sc.cameras[view]
-    st = O.OracleStep(sc, cam, M=1, tile_frac=1.0 / 16)
-    gs = GpuStep(sc, cam, M=1, importance=False)
-    try:
-        assert np.array_equal(gs.radius, st.get("radius"))
-        rec = gs.rank[0]["records"]
-        order = np.argsort(rec["gid"])
-        valid = np.nonzero(st.get("radius") > 0)[0]
-        assert np.array_equal(rec["gid"][order], valid)
-        m2 = st.get("mean2d").reshape(-1, 2)[valid]
-        assert np.array_equal(rec["mx"][order].view(np.uint32), _f32(m2[:, 0]).view(np.uint32))
-        assert np.array_equal(rec["rgb"][order].view(np.uint32),
-                              _f32(st.get("rgb").reshape(-1, 3)[valid]).view(np.uint32))
-        o = gs.rank[0]
-        tiles = o["key_tile"]
-        assert np.array_equal(tiles, st.get("pair_tile", 0))
-        assert np.array_equal(o["recv"]["gid"][o["vals"]], st.get("pair_gid", 0))
-        assert np.array_equal(o["ranges"][:, 0], st.get("range_lo", 0))
-        H, W = cam["H"], cam["W"]
-        TX = (W + 15) // 16
-        sample = np.zeros((H, W), bool)
-        for t in range(0, TX * ((H + 15) // 16), 16):
-            ty, tx = divmod(t, TX)
-            sample[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
-        cand = st.get("et_margin").reshape(H, W) < ET_MARGIN
-        ok = sample & ~cand
-        assert ok.sum() > 0.05 * H * W
-        img = st.get("img").reshape(3, H, W)
-        assert np.abs(gs.img - img)[:, ok].max() <= 1e-4
-        assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
-    finally:
-        gs.close()
+def _tile_sample(H, W, stride=16):
+    """Pixels of the tiles t = 0, stride, 2 stride, ... (the oracle's tile_frac sample)."""
+    TX = (W + 15) // 16
+    sample = np.zeros((H, W), bool)
+    for t in range(0, TX * ((H + 15) // 16), stride):
+        ty, tx = divmod(t, TX)
+        sample[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
+    return sample
+
+
+@pytest.fixture(scope="module")
+def rubble_full():
+    """BASELINE configs[1] at full size (6M Gaussians, 1152x864), view 7, in the bench's launch
+    configuration.  dL/dC is the seeded noise image zeroed outside a 1/16 tile sample, so the
+    oracle's tile-sampled compositing backward (tile_frac = 1/16) sees the same upstream gradient
+    as the GPU's full-image backward: every parameter gradient is then comparable."""
+    sc = S.gen_city("rubble")
+    cam = sc.cameras[7]
+    H, W = cam["H"], cam["W"]
+    sample = _tile_sample(H, W)
+    dl = S.grad_image(H, W) * sample[None]
+    st = O.OracleStep(sc, cam, M=1, tile_frac=1.0 / 16, dLdC=dl)
+    gs = GpuStep(sc, cam, M=1, dLdC=dl)
+    yield sc, cam, sample, st, gs
+    gs.close()
+
+
+def test_full_size_sampled(rubble_full):
+    """Projection, records, the complete sorted pair sequence and ranges bit-exact at full size;
+    pixels and n_contrib on the 1/16 tile sample (the ones the oracle composites)."""
+    sc, cam, sample, st, gs = rubble_full
+    assert np.array_equal(gs.radius, st.get("radius"))
+    rec = gs.rank[0]["records"]
+    order = np.argsort(rec["gid"])
+    valid = np.nonzero(st.get("radius") > 0)[0]
+    assert np.array_equal(rec["gid"][order], valid)
+    m2 = st.get("mean2d").reshape(-1, 2)[valid]
+    assert np.array_equal(rec["mx"][order].view(np.uint32), _f32(m2[:, 0]).view(np.uint32))
+    assert np.array_equal(rec["rgb"][order].view(np.uint32),
+                          _f32(st.get("rgb").reshape(-1, 3)[valid]).view(np.uint32))
+    o = gs.rank[0]
+    assert np.array_equal(o["key_tile"], st.get("pair_tile", 0))
+    assert np.array_equal(o["recv"]["gid"][o["vals"]], st.get("pair_gid", 0))
+    assert np.array_equal(o["ranges"][:, 0], st.get("range_lo", 0))
+    assert np.array_equal(o["ranges"][:, 1], st.get("range_hi", 0))
+    H, W = cam["H"], cam["W"]
+    cand, flips, affected = _flip_info(st, gs, cam, sample)
+    ok = sample & ~flips
+    assert ok.sum() > 0.05 * H * W
+    img = st.get("img").reshape(3, H, W)
+    assert np.abs(gs.img - img)[:, ok].max() <= 1e-4
+    assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
+    print(f"full size: flip candidates {cand.sum()}, flips {flips.sum()}, affected {len(affected)}")
+
+
+def test_full_size_sampled_gradients(rubble_full):
+    """All 9 compositing partials and all parameter gradients of the 6M-Gaussian view (upstream
+    gradient on the 1/16 tile sample) against the fp64 oracle, excusing only actual flips."""
+    sc, cam, sample, st, gs = rubble_full
+    _, flips, affected = _flip_info(st, gs, cam, sample)
+    _excused_ok(st, gs, affected)
+    keep = np.ones(sc.n, bool)
+    keep[list(affected)] = False
+    touched = np.abs(st.get("g2d").reshape(-1, 9)).sum(1) > 0
+    assert touched.sum() > 10_000
+    _check_g2d(st, gs, keep, "rubble")
+    _check_grads(sc.n, st, gs, keep, what="rubble")
+
+
+def test_full_size_importance(rubble_full):
+    """a12 on the full 6M shard: c_rad, c_vis and the Cull column bit-exact against the oracle's
+    selection (std::sort and scan, O12) on the GPU's own w_fixed and a; s the same fp64 sum."""
+    sc, cam, sample, st, gs = rubble_full
+    assert (gs.w > 0).sum() > 100_000
+    ref = O.importance(gs.radius, gs.w, gs.a)
+    assert np.array_equal(gs.c_rad, ref["c_rad"])
+    assert np.array_equal(gs.c_vis, ref["c_vis"])
+    assert np.array_equal(gs.cull_bits, S.unpack_bits(ref["cull"], sc.n))
+    np.testing.assert_allclose(gs.s, ref["s"], rtol=1e-12, atol=0)
+    # w and a on the sampled tiles: the oracle composites only those, so a splat lying wholly
+    # inside them has comparable totals
+    H, W = cam["H"], cam["W"]
+    TX = (W + 15) // 16
+    rect = st.get("rect").reshape(-1, 4)
+    in_sample = np.zeros(sc.n, bool)
+    vis = np.nonzero(st.get("radius") > 0)[0]
+    r = rect[vis]
+    single = (r[:, 2] - r[:, 0] == 1) & (r[:, 3] - r[:, 1] == 1)
+    t = r[:, 1] * TX + r[:, 0]
+    in_sample[vis[single & (t % 16 == 0)]] = True
+    _, _, affected = _flip_info(st, gs, cam, sample)
+    in_sample[list(affected)] = False
+    assert in_sample.sum() > 1000
+    assert np.array_equal(gs.a[in_sample], st.get("a")[in_sample])
+    w_o = st.get("w_fixed").astype(np.float64)[in_sample]
+    assert np.all(np.abs(gs.w[in_sample].astype(np.float64) - w_o) <= st.get("a")[in_sample] + 1e-5 * w_o)
 
 
 @pytest.mark.parametrize("split", ["default", "0"])
@@ -350,16 +450,23 @@ def test_edge_cases(case, split, monkeypatch):
     try:
         assert np.array_equal(gs.radius, st.get("radius"))
         H, W = cam["H"], cam["W"]
-        cand = st.get("et_margin").reshape(H, W) < ET_MARGIN
-        assert np.abs(gs.img - st.get("img").reshape(3, H, W))[:, ~cand].max(initial=0) <= 1e-4
-        assert np.array_equal(gs.nc[~cand], st.get("n_contrib").reshape(H, W)[~cand])
+        _, flips, _ = _flip_info(st, gs, cam)
+        assert np.abs(gs.img - st.get("img").reshape(3, H, W))[:, ~flips].max(initial=0) <= 1e-4
+        assert np.array_equal(gs.nc[~flips], st.get("n_contrib").reshape(H, W)[~flips])
         o = gs.rank[0]
         tiles = o["key_tile"]
         assert np.array_equal(tiles, st.get("pair_tile", 0))
         assert np.array_equal(o["recv"]["gid"][o["vals"]], st.get("pair_gid", 0))
+        _, flips, affected = _flip_info(st, gs, cam)
+        keep = np.ones(sc.n, bool)
+        keep[list(affected)] = False
+        assert np.array_equal(gs.a[keep], st.get("a")[keep])
+        _check_g2d(st, gs, keep, case)
+        _check_grads(sc.n, st, gs, keep, what=case)
         if case == "empty":
             assert np.all(gs.img == 0) and np.all(gs.T == 1) and np.all(gs.nc == 0)
             assert gs.rank[0]["q"]["F"] == 0 and gs.rank[0]["q"]["P"] == 0
+            assert all(np.all(v == 0) for v in gs.grads.values())
     finally:
         gs.close()
 
@@ -430,13 +537,11 @@ def test_raster_work_units_parity(tiny_scene, monkeypatch, split):
         ok = ~flips
         assert np.abs(gs.img - st.get("img").reshape(3, H, W))[:, ok].max() <= 1e-4
         assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
+        _excused_ok(st, gs, affected)
         keep = np.ones(sc.n, bool)
         keep[list(affected)] = False
         assert np.array_equal(gs.a[keep], st.get("a")[keep])
-        for name, width in (("d_mean", 3), ("d_quat", 4), ("d_scale", 3), ("d_opac", 1), ("d_sh", 48)):
-            ref = st.get(name).reshape(sc.n, width)[keep]
-            got = gs.grads[name].reshape(sc.n, width)[keep]
-            tol = 1e-3 * np.abs(ref) + 1e-5 * np.abs(ref).max()
-            assert not (np.abs(got - ref) > tol).any(), name
+        _check_g2d(st, gs, keep, f"split {split}")
+        _check_grads(sc.n, st, gs, keep, what=f"split {split}")
     finally:
         gs.close()

@@ -487,3 +487,75 @@ def test_P12_selection_vs_sort_and_scan():
             assert 100 * int(w[~r["in_set"]].sum()) <= total  # culled mass <= 1%
         s_expect = np.where(a > 0, (w.astype(np.float64) / 2 ** 24) / (a + 1e-8), 0.0)
         np.testing.assert_allclose(r["s"], s_expect, rtol=1e-12)
+
+
+# ------------------------------------------------------------------------------------------
+# P17: the alpha-cut threshold thr = -ln(255 o) (SPEC S:137 alpha_min = 1/255; D3) is computed
+# with a fixed-sequence fp64 ln (reading R30) so that both sides round the same value; pinned
+# here against libm's correctly rounded log, not against itself.
+# ------------------------------------------------------------------------------------------
+def test_P17_fixed_ln_matches_libm():
+    rng = np.random.default_rng(17)
+    u = np.concatenate([np.exp(rng.uniform(np.log(1e-6), np.log(1e6), 20000)),
+                        255.0 * rng.uniform(0.0, 1.0, 20000).astype(np.float32).astype(np.float64),
+                        [1.0, 2.0, 0.5, 255.0, math.sqrt(2.0), math.nextafter(math.sqrt(2.0), 2.0)]])
+    u = u[u > 0]
+    for x in u:
+        got, ref = O.ln_fixed(float(x)), math.log(float(x))
+        # within 2 ulp of the correctly rounded value (the series truncation is < 1e-19 relative)
+        assert abs(got - ref) <= 2 * math.ulp(ref) + 1e-300, (x, got, ref)
+    assert O.ln_fixed(1.0) == 0.0
+    for k in range(-20, 21):
+        assert abs(O.ln_fixed(2.0 ** k) - k * math.log(2.0)) <= math.ulp(k * math.log(2.0)) + 1e-300
+
+
+def test_P17_threshold_bits():
+    """thr(o) is float32(-ln(255 o)): equal to the rounding of libm's value except where that
+    double lies within an ulp of a float rounding boundary (then one float ulp apart at most);
+    and alpha >= 1/255 <=> power >= thr on a dense grid of powers."""
+    rng = np.random.default_rng(3)
+    o = np.concatenate([rng.uniform(0.004, 1.0, 20000), [1.0 / 255 + 1e-7, 0.5, 0.99, 1.0 - 1e-7]]).astype(np.float32)
+    same = 0
+    for v in o:
+        t = O.thr(float(v))
+        ref = np.float32(-math.log(255.0 * float(v)))
+        assert abs(np.float64(t) - np.float64(ref)) <= np.spacing(np.float32(abs(ref)) + np.float32(1e-30)), v
+        same += t == ref
+    assert same >= len(o) - 2
+    for v in (0.05, 0.3, 0.8):
+        t = O.thr(v)
+        p = np.float64(np.float32(t))
+        # a power just above thr keeps alpha above 1/255 (up to the float rounding of thr)
+        assert np.float32(v) * math.exp(p + 1e-6) >= 1.0 / 255 * (1 - 1e-6)
+        assert np.float32(v) * math.exp(p - 1e-3) < 1.0 / 255
+
+
+# ------------------------------------------------------------------------------------------
+# P6b: the SH colour is evaluated along the viewing ray, camera -> Gaussian (3DGS convention,
+# d = (mu - c_v)/|mu - c_v|; P:143).  A splat whose only view-dependent term is the band-1 x
+# function is brighter seen from the side where the ray runs along +x; a reversed direction
+# (c_v - mu) swaps the two colours.
+# ------------------------------------------------------------------------------------------
+def test_P6b_view_direction_sign():
+    mu = np.array([[0.3, -0.2, 0.1]], np.float32)
+    k_x = None
+    Yx = O.sh_basis([1.0, 0.0, 0.0])
+    for k in (1, 2, 3):  # the band-1 function that varies along x (P6: real SH up to sign)
+        if abs(Yx[k]) > 0.4:
+            k_x = k
+    assert k_x is not None and abs(O.sh_basis([0, 1.0, 0])[k_x]) < 1e-12
+    sh = np.zeros((1, 16, 3), np.float32)
+    sh[0, k_x, 0] = 0.2 / Yx[k_x]  # red = 0.5 + 0.2 x_dir
+    out = {}
+    for side, f in (("minus_x", 1.0), ("plus_x", -1.0)):
+        pos = mu[0].astype(np.float64) - 5.0 * f * np.array([1.0, 0, 0])
+        R = np.array([[0, 1, 0], [0, 0, f], [f, 0, 0]], np.float64)  # rows right, down, forward = f e_x
+        assert np.isclose(np.linalg.det(R), 1.0)
+        sc, _ = _one_scene(mu, sh=sh, W=33, H=33)
+        cam = S.make_camera(33, 33, R, -R @ pos)
+        sc.cameras = [cam]
+        st = O.OracleStep(sc, cam)
+        assert st.get("radius")[0] > 0
+        out[side] = st.get("rgb").reshape(-1, 3)[0, 0]
+    # camera on the -x side: the ray camera -> Gaussian runs along +x
+    assert abs(out["minus_x"] - 0.7) < 1e-6 and abs(out["plus_x"] - 0.3) < 1e-6, out

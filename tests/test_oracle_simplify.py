@@ -105,7 +105,7 @@ def test_mass_cut_spec_examples():
     # scores (0.5, 0.3, 0.15, 0.05), target 0.99: first three hold 0.95 < 0.99 -> all four  [S:312]
     keep, _ = SO.prune_mass_cut(np.array([0.5, 0.3, 0.15, 0.05]), gid, 99, 100)
     assert keep.all()
-    # a first element whose mass alone reaches the target is the whole prefix  [S:313]
+    # a first element whose mass alone reaches the target is the whole prefix  [S:317]
     keep, _ = SO.prune_mass_cut(np.array([0.995, 0.002, 0.002, 0.001]), gid, 99, 100)
     assert keep.tolist() == [True, False, False, False]
     # all-zero scores: only the forced first element, with the warning  [S:310]
