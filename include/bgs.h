@@ -28,9 +28,10 @@
  *  - All inputs and fixed-size outputs are CALLER-owned.  Variable-size intermediates
  *    (records, exchange buffers, pairs, per-splat gradients) live in the ctx arena and stay
  *    valid until the next call of the same stage on that ctx.
- *  - Every call enqueues on `stream` (a cudaStream_t passed as void*; NULL selects the legacy
- *    default stream).  Calls marked HOST-SYNC block the host on that stream once (to size
- *    variable buffers).
+ *  - Every call enqueues on `stream` (a cudaStream_t passed as void*; NULL selects the calling
+ *    thread's per-thread default stream cudaStreamPerThread, never the legacy default stream).
+ *    Successive calls on one ctx must use one stream (or be ordered by the caller).  Calls marked
+ *    HOST-SYNC block the host on that stream once (to size variable buffers).
  *  - One ctx per rank and per host thread.  world > 1 uses NCCL (ncclCommInitRank from a
  *    unique id) or, for single-GPU testing, an in-process group sharing one device.
  *  - Layouts: Gaussian parameters are structure-of-arrays of 16-byte rows so kernels issue
@@ -173,8 +174,14 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
 /* a3+a4.  Per-tile pair counts are all-reduced, tiles split into contiguous cost-balanced
  * runs (owner(t) = min(M-1, floor((2 P_t + c_t) M / (2 C))), c_t = pairs_t + 1, D6), and
  * every record is sent to each rank owning a tile of its rect in ONE all-to-all.
- * tile_owner_out: nullable device int32[T].  HOST-SYNC (exchange sizes). */
-bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream);
+ * tile_owner_in: nullable device int32[T]; when given it replaces that split (it must be
+ * contiguous non-decreasing runs in [0, world), identical on every rank, else
+ * BGS_ERR_INVALID_ARGUMENT; the pair counts are still all-reduced for the owners' P).
+ * tile_owner_out: nullable device int32[T], the map used.  n_recv_out: nullable host int64, R (the
+ * records this rank receives).  World 1: the identity (owner 0 everywhere, R = F).
+ * HOST-SYNC (exchange sizes). */
+bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_owner_out, int64_t* n_recv_out,
+                     void* stream);
 
 /* a5+a6+a7.  Pairs (owned tile, received record) keyed (tile, depth); onesweep LSD radix sort;
  * runs of equal keys ordered by global id (R12); per-tile [start,end) ranges. */
@@ -429,6 +436,8 @@ typedef struct {
   float min_opacity;     /* prune rows with opacity below this (3DGS: 0.005) */
   float split_div;       /* split children scale = s / split_div (3DGS: 1.6) */
   uint64_t seed;         /* split samples: z = N(0, I) of (seed, parent global id, child, axis) */
+  int32_t k_levels;      /* K, the number of LOD levels (1..256): a split child's level is
+                            min(parent level + 1, K - 1) (heritage rule; S:374, S:379 keep l in [0, K-1]) */
 } bgs_densify_params;
 
 /* Clone / split / prune the local shard ("clones, splits, and prunes"; heritage rule P:194:
@@ -437,7 +446,8 @@ typedef struct {
  * and moments of the new shard, out->n_local = CAPACITY in rows; lod_out u8 [capacity]; act_out
  * (nullable): activated planes of the new shard (act_out->sh may equal out->sh).  Order: kept
  * originals (input order), clones (parent order), first then second children of split parents;
- * moments copied for originals, zero for new rows.  *n_out (host) = new row count;
+ * moments copied for originals, zero for new rows; clones keep the parent's level, split children get
+ * min(level + 1, K - 1).  *n_out (host) = new row count;
  * BGS_ERR_CAPACITY (nothing written) when it exceeds the capacity.  out must not alias in.  The
  * caller re-zeros stat / count for the new shard.  Global ids are j*M + rank as before; a
  * skew-triggered bgs_redistribute can follow.  HOST-SYNC. */

@@ -68,8 +68,10 @@ def decide(params: dict, stat, count, tau: float, dense_extent: float, min_opaci
 
 
 def apply(params: dict, state: dict, lod, stat, count, tau, dense_extent, min_opacity, split_div, seed,
-          rank: int = 0, world: int = 1):
-    """New (params, state, lod) of the shard; params / state keyed like oracle/optim.py."""
+          rank: int = 0, world: int = 1, k_levels: int = 256):
+    """New (params, state, lod) of the shard; params / state keyed like oracle/optim.py.
+    Heritage rule (SPEC apply_heritage): a clone keeps the parent's level, a split
+    child gets min(l + 1, K - 1) so every level stays in [0, K - 1]."""
     keep, clone, split = decide(params, stat, count, tau, dense_extent, min_opacity)
     keys = ("mean_logit", "quat_raw", "log_scale", "sh")
     P = {k: np.asarray(params[k], np.float64) for k in keys}
@@ -86,7 +88,7 @@ def apply(params: dict, state: dict, lod, stat, count, tau, dense_extent, min_op
             out[k].append(over.get(k, P[k][i]))
             om[k].append(np.zeros_like(P[k][i]) if fresh else Sm[k][i])
             ov[k].append(np.zeros_like(P[k][i]) if fresh else Sv[k][i])
-        olod.append(min(255, lod[i] + over.get("dlod", 0)))
+        olod.append(min(k_levels - 1, lod[i] + over.get("dlod", 0)))
 
     for i in np.flatnonzero(keep):
         emit(i, False)

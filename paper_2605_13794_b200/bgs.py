@@ -79,7 +79,7 @@ _SIGS = {
     "bgs_query": [_vp, _vp],
     "bgs_debug_buffer": [_vp, C.c_int32, _vp, _vp],
     "bgs_project": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp],
-    "bgs_route": [_vp, _vp, _vp],
+    "bgs_route": [_vp, _vp, _vp, _vp, _vp],
     "bgs_sort_tiles": [_vp, _vp],
     "bgs_raster_fwd": [_vp, C.c_uint32, _vp, _vp, _vp, _vp],
     "bgs_raster_bwd": [_vp, _vp, _vp, _vp, _vp],
@@ -306,8 +306,12 @@ def bgs_project(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate: bgs_lod_
                                _ptr(cull_column), flags, _ptr(radius_out), _stream(stream)), "bgs_project")
 
 
-def bgs_route(ctx: Context, tile_owner_out=None, stream=None):
-    ctx.check(_lib.bgs_route(ctx.handle, _ptr(tile_owner_out), _stream(stream)), "bgs_route")
+def bgs_route(ctx: Context, tile_owner_out=None, stream=None, tile_owner_in=None) -> int:
+    """a3 + a4; returns R (records received by this rank)."""
+    r = C.c_int64(0)
+    ctx.check(_lib.bgs_route(ctx.handle, _ptr(tile_owner_in), _ptr(tile_owner_out), C.byref(r), _stream(stream)),
+              "bgs_route")
+    return int(r.value)
 
 
 def bgs_sort_tiles(ctx: Context, stream=None):
@@ -415,13 +419,14 @@ def bgs_adam_step(ctx: Context, p: TrainParams, grads: GradPlanes, act: Gaussian
 
 class bgs_densify_params(C.Structure):
     _fields_ = [("grad_threshold", C.c_float), ("dense_extent", C.c_float), ("min_opacity", C.c_float),
-                ("split_div", C.c_float), ("seed", C.c_uint64)]
+                ("split_div", C.c_float), ("seed", C.c_uint64), ("k_levels", C.c_int32)]
 
 
 def densify_params(grad_threshold=2e-4, dense_extent=0.01, min_opacity=0.005, split_div=1.6,
-                   seed=0) -> bgs_densify_params:
-    """3DGS defaults (tau 2e-4, opacity 0.005, split / 1.6); dense_extent = percent_dense * extent."""
-    return bgs_densify_params(grad_threshold, dense_extent, min_opacity, split_div, seed)
+                   seed=0, k_levels=256) -> bgs_densify_params:
+    """3DGS defaults (tau 2e-4, opacity 0.005, split / 1.6); dense_extent = percent_dense * extent;
+    k_levels = K (split children's level is min(l + 1, K - 1))."""
+    return bgs_densify_params(grad_threshold, dense_extent, min_opacity, split_div, seed, k_levels)
 
 
 def bgs_densify_accumulate(ctx: Context, n_local: int, phi, stat, count, stream=None):

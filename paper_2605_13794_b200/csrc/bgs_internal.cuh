@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/bgs.h"
 
 namespace bgs {
@@ -184,8 +186,8 @@ void launch_project_bwd(const ProjectBwdArgs& a, cudaStream_t s);
 
 // routing (a3, a4, a10) for world > 1
 void launch_tile_costs(const int32_t* diff, int TX, int TY, int32_t* pairs_t, cudaStream_t s);
-void launch_owner_map(const int32_t* pairs_t, int T, int world, int32_t* owner, int32_t* run /*[2*world]*/,
-                      long long* pown /*[world]*/, cudaStream_t s);
+void launch_owner_map(const int32_t* pairs_t, int T, int world, int32_t* owner, int32_t* run, long long* pown,
+                      const int32_t* given, cudaStream_t s);
 void launch_dest_count(const Rec* recs, int64_t F, const int32_t* owner, int TX, int world, uint8_t* dest_mask,
                        uint32_t* block_counts, cudaStream_t s);
 void launch_block_scan(uint32_t* block_counts, int64_t n_blocks, int world, unsigned long long* totals,
@@ -336,6 +338,7 @@ struct DensifyArgs {
   const uint32_t* count;
   float tau, log_extent, logit_min, log_div;
   unsigned long long seed;
+  int max_level;  // K - 1: split children's level is min(l + 1, K - 1) (heritage rule)
   uint32_t* block_counts;        // 3 per block, scanned in place
   unsigned long long* totals;    // kept, clones, split parents
   float4* p_out[3];
@@ -377,5 +380,34 @@ __device__ __forceinline__ double ln_pinned(double u) {
 
 // thr = -ln(255 o) rounded to float: alpha = o G >= 1/255 <=> power >= thr (D3), pinned (above)
 __device__ __forceinline__ float alpha_cut_thr(float o) { return float(-ln_pinned(__dmul_rn(255.0, double(o)))); }
+
+// Per-device cache of a host-side launch parameter (SM count, occupancy-derived grid size, a
+// dynamic shared-memory opt-in done once per device).  `slots` is a function-local static array;
+// the value is computed on first use on each device ordinal of the calling thread's current device
+// (compute() must return > 0 and be idempotent: two threads racing on a first use both store the
+// same value).
+constexpr int kMaxDevices = 64;
+template <class F>
+inline int per_device(std::atomic<int> (&slots)[kMaxDevices], F compute) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return compute();
+  int v = slots[dev].load(std::memory_order_acquire);
+  if (v <= 0) {
+    v = compute();
+    slots[dev].store(v, std::memory_order_release);
+  }
+  return v;
+}
+
+inline int device_sm_count() {
+  static std::atomic<int> slots[kMaxDevices];
+  return per_device(slots, [] {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+  });
+}
 
 }  // namespace bgs

@@ -156,7 +156,7 @@ __device__ __forceinline__ void put_row(const DensifyArgs& a, int64_t src, int64
     a.m_out[k][dst] = fresh ? z4 : a.m_in[k][src];
     a.v_out[k][dst] = fresh ? z4 : a.v_in[k][src];
   }
-  a.lod_out[dst] = uint8_t(lod > 255 ? 255 : lod);
+  a.lod_out[dst] = uint8_t(lod);
   if (a.act[0]) {  // activated planes for the next render
     a.act[0][dst] = make_float4(ml.x, ml.y, ml.z, 1.f / (1.f + expf(-ml.w)));
     const float in = 1.f / sqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kDcThreads) k_dc_emit(DensifyArgs a) {
       const float4 mc = make_float4(ml.x + (R[0] * v[0] + R[1] * v[1] + R[2] * v[2]),
                                     ml.y + (R[3] * v[0] + R[4] * v[1] + R[5] * v[2]),
                                     ml.z + (R[6] * v[0] + R[7] * v[1] + R[8] * v[2]), ml.w);
-      put_row(a, i, K + Cn + int64_t(c) * Sn + r, true, mc, q, lsc, lod + 1);
+      put_row(a, i, K + Cn + int64_t(c) * Sn + r, true, mc, q, lsc, lod + 1 < a.max_level ? lod + 1 : a.max_level);
     }
   }
   copy_sh_rows(a, ii, d0, d1, f0, f1);

@@ -520,11 +520,10 @@ void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s
 int64_t imp_set_words() { return kImpSetWords; }
 
 static int coop_blocks() {
-  static int blocks = 0;
-  if (blocks == 0) {
-    int per_sm = 0, dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<int> slots[kMaxDevices];
+  return per_device(slots, [] {
+    int per_sm = 0, blocks = 0;
+    const int sms = device_sm_count();
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_imp_coop, 256, 0);
     // 2 CTAs per SM: a cooperative grid holds its SM slots while it waits at grid syncs, which
     // starves the other views in flight; measured on Rubble (4 in flight / one view's importance
@@ -532,9 +531,8 @@ static int coop_blocks() {
     const char* e = getenv("BGS_IMP_COOP_PER_SM");  // tuning only
     const int cap = e && atoi(e) > 0 ? atoi(e) : 2;
     blocks = sms * (per_sm < cap ? per_sm : cap);
-    if (blocks < 1) blocks = 1;
-  }
-  return blocks;
+    return blocks < 1 ? 1 : blocks;
+  });
 }
 
 int64_t imp_cand_words(int64_t n_items) {

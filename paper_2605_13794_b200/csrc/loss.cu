@@ -370,11 +370,11 @@ int64_t loss_n_blocks(int W, int H) {
 }
 
 void launch_loss_photo(const LossArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<int> attr[kMaxDevices];
+  per_device(attr, [] {
     cudaFuncSetAttribute(k_loss_photo, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(LossSmem)));
-    attr = true;
-  }
+    return 1;
+  });
   const dim3 grid(unsigned((a.W + kLT - 1) / kLT), unsigned((a.H + kLT - 1) / kLT), 3u);
   k_loss_photo<<<grid, kLThreads, sizeof(LossSmem), s>>>(a);
 }

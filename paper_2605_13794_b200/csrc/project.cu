@@ -419,13 +419,15 @@ void launch_project(const ProjectArgs& a, cudaStream_t s) {
   if (a.n <= 0) return;
   const int64_t blocks = (a.n + kCullChunk - 1) / kCullChunk;
   k_cull<<<unsigned(blocks), 256, 0, s>>>(a);
-  static const int proj_blocks = persistent_blocks(k_project);
+  static std::atomic<int> slots[kMaxDevices];
+  const int proj_blocks = per_device(slots, [] { return persistent_blocks(k_project); });
   k_project<<<proj_blocks, 256, 0, s>>>(a);
 }
 
 void launch_color(const ProjectArgs& a, cudaStream_t s) {
   if (a.n <= 0 || a.no_color) return;
-  static const int color_blocks = persistent_blocks(k_color);
+  static std::atomic<int> slots[kMaxDevices];
+  const int color_blocks = per_device(slots, [] { return persistent_blocks(k_color); });
   k_color<<<color_blocks, 256, 0, s>>>(a);
 }
 

@@ -451,14 +451,7 @@ static int split_count(int n_tiles) {
   // read at every launch (a getenv), so tests can force either work unit on small images
   const char* e = getenv("BGS_SPLIT_TILES");
   const int env = e ? atoi(e) : -1;
-  int sms = 148;
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
-  }
-  sms = cached > 0 ? cached : sms;
+  const int sms = device_sm_count();
   // 2 x SMs: measured on Rubble (fwd+bwd ms per view) 0.58 unsplit, 0.530 at 148, 0.526 at 296,
   // 0.535 at 592
   const int want = env >= 0 ? env : 2 * sms;

@@ -43,9 +43,11 @@ __global__ void __launch_bounds__(1024) k_tile_costs(const int32_t* diff, int TX
   for (int t = threadIdx.x; t < TX * TY; t += blockDim.x) pairs[t] = s_d[(t / TX) * W1 + (t % TX)];
 }
 
+// given != nullptr: the caller's owner map (bgs_route's tile_owner_in) replaces the a3 split; it
+// must be contiguous non-decreasing runs in [0, world) (checked: pown[world] = 1 when it is not)
 __global__ void __launch_bounds__(1024) k_owner_map(const int32_t* pairs, int T, int world, int32_t* owner,
                                                     int32_t* run /*[2*world]: begin, end*/,
-                                                    long long* pown /*[world]*/) {
+                                                    long long* pown /*[world + 1]*/, const int32_t* given) {
   extern __shared__ long long s_c[];  // T inclusive prefix of c_t
   // serial-per-chunk scan: T <= 65025, chunks per thread
   const int nt = blockDim.x;
@@ -74,12 +76,23 @@ __global__ void __launch_bounds__(1024) k_owner_map(const int32_t* pairs, int T,
   }
   __syncthreads();
   const long long C = s_c[T];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
   for (int t = threadIdx.x; t < T; t += nt) {
-    const long long ct = (long long)pairs[t] + 1;
-    long long o = ((2 * s_c[t] + ct) * world) / (2 * C);
-    owner[t] = int32_t(o < world - 1 ? o : world - 1);
+    if (given) {
+      const int32_t o = given[t];
+      const bool bad = o < 0 || o >= world || (t > 0 && given[t - 1] > o);
+      if (bad) s_bad = 1;
+      owner[t] = o < 0 ? 0 : (o >= world ? world - 1 : o);
+    } else {
+      const long long ct = (long long)pairs[t] + 1;
+      long long o = ((2 * s_c[t] + ct) * world) / (2 * C);
+      owner[t] = int32_t(o < world - 1 ? o : world - 1);
+    }
   }
   __syncthreads();
+  if (threadIdx.x == 0) pown[world] = s_bad;
   if (threadIdx.x < world) {
     const int r = threadIdx.x;
     int lo = 0, hi = T;  // first t with owner >= r
@@ -246,23 +259,23 @@ __global__ void k_reduce_sum(PtrList src, T* dst, int64_t n) {
 
 void launch_tile_costs(const int32_t* diff, int TX, int TY, int32_t* pairs_t, cudaStream_t s) {
   const size_t smem = size_t(TX + 1) * (TY + 1) * sizeof(int32_t);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<int> attr[kMaxDevices];
+  per_device(attr, [] {
     cudaFuncSetAttribute(k_tile_costs, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+    return 1;
+  });
   k_tile_costs<<<1, 1024, smem, s>>>(diff, TX, TY, pairs_t);
 }
 
 void launch_owner_map(const int32_t* pairs_t, int T, int world, int32_t* owner, int32_t* run, long long* pown,
-                      cudaStream_t s) {
+                      const int32_t* given, cudaStream_t s) {
   const size_t smem = size_t(T + 1) * sizeof(long long);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<int> attr[kMaxDevices];
+  per_device(attr, [] {
     cudaFuncSetAttribute(k_owner_map, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  k_owner_map<<<1, 1024, smem, s>>>(pairs_t, T, world, owner, run, pown);
+    return 1;
+  });
+  k_owner_map<<<1, 1024, smem, s>>>(pairs_t, T, world, owner, run, pown, given);
 }
 
 void launch_dest_count(const Rec* recs, int64_t F, const int32_t* owner, int TX, int world, uint8_t* dest_mask,

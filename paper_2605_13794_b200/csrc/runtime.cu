@@ -53,7 +53,8 @@ struct bgs_ctx {
   DevBuf counters, recs, rec_lidx, tile_diff, tile_pairs, owner, runinfo, dest_mask, block_counts, totals,
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
       imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask,
-      loss_img, loss_part, loss_sums, scr_tgt, scr_loss, scr_in2;
+      loss_img, loss_part, loss_sums, scr_tgt, scr_loss, scr_in2,
+      scr_dlsup;  // supervised steps' dL/dC (never one of the host-upload double buffers)
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
@@ -73,6 +74,13 @@ struct bgs_ctx {
 };
 
 namespace {
+
+// The ABI's stream argument: NULL selects the calling thread's per-thread default stream
+// (cudaStreamPerThread), never the legacy default stream; it is still ordered with
+// legacy-stream work of the same process (the per-thread stream is a blocking stream).
+inline cudaStream_t as_stream(void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : cudaStreamPerThread;
+}
 
 #define CK(call)                                                                     \
   do {                                                                               \
@@ -319,9 +327,7 @@ bgs_status check_ctx(bgs_ctx* ctx) {
   return BGS_OK;
 }
 
-bgs_status check_stream(bgs_ctx*, void*) {
-  return BGS_OK;  // NULL is the legacy default stream (allowed; callers should prefer their own)
-}
+bgs_status check_stream(bgs_ctx*, void*) { return BGS_OK; }
 
 bgs_status set_camera(bgs_ctx* ctx, const bgs_camera* c) {
   if (!c) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "camera is NULL");
@@ -389,7 +395,7 @@ bgs_status bgs_ctx_create(int32_t rank, int32_t world, const void* uid, int32_t 
   c->device = device;
   bgs_status st = ctx_alloc_common(c);
   if (st != BGS_OK) {
-    delete c;
+    bgs_ctx_destroy(c);
     return st;
   }
   if (world > 1) {
@@ -397,7 +403,8 @@ bgs_status bgs_ctx_create(int32_t rank, int32_t world, const void* uid, int32_t 
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof id);
     if (ncclCommInitRank(&t->comm, world, id, rank) != ncclSuccess) {
-      delete c;
+      t->comm = nullptr;
+      bgs_ctx_destroy(c);  // frees the pinned buffers and the arena allocated above
       return BGS_ERR_NCCL;
     }
     c->tr = t;
@@ -417,9 +424,15 @@ bgs_status bgs_ctx_create_local_group(int32_t world, int32_t device, bgs_ctx** o
     c->rank = r;
     c->world = world;
     c->device = device;
-    if (ctx_alloc_common(c) != BGS_OK) return BGS_ERR_CUDA;
-    if (world > 1) c->tr = std::make_shared<LocalTransport>(grp);
     out[r] = c;
+    if (ctx_alloc_common(c) != BGS_OK) {
+      for (int k = 0; k <= r; ++k) {  // no partially created group is left behind
+        bgs_ctx_destroy(out[k]);
+        out[k] = nullptr;
+      }
+      return BGS_ERR_CUDA;
+    }
+    if (world > 1) c->tr = std::make_shared<LocalTransport>(grp);
   }
   return BGS_OK;
 }
@@ -432,7 +445,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2, &c->scr_dlsup,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -513,7 +526,7 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
   CKS(check_gaussians(ctx, g));
   CKS(set_camera(ctx, cam));
   if (g->n_local > 0 && !radius_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "radius_out is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   ctx->stage = 0;
   ctx->n_local = g->n_local;
   ProjectArgs a{};
@@ -613,11 +626,12 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
 // ---------------------------------------------------------------------------------------
 // a3 + a4
 // ---------------------------------------------------------------------------------------
-bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream) {
+bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_owner_out, int64_t* n_recv_out,
+                     void* stream) {
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 1) return fail(ctx, BGS_ERR_CONTRACT, "bgs_route before bgs_project");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const int M = ctx->world;
   if (M == 1) {
     ctx->recv = P_<Rec>(ctx->recs);
@@ -627,6 +641,7 @@ bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream) {
     ctx->t_end = ctx->T;
     ctx->P = ctx->P_all;
     if (tile_owner_out) CK(cudaMemsetAsync(tile_owner_out, 0, size_t(ctx->T) * 4, s));
+    if (n_recv_out) *n_recv_out = ctx->R;
     ctx->stage = 2;
     return BGS_OK;
   }
@@ -635,13 +650,13 @@ bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream) {
   // a3: per-tile pair counts -> all ranks -> owner map
   CKS(ensure(ctx, ctx->tile_pairs, size_t(T) * 4));
   CKS(ensure(ctx, ctx->owner, size_t(T) * 4));
-  CKS(ensure(ctx, ctx->runinfo, size_t(2 * M) * 4 + size_t(M) * 8 + 64));
+  CKS(ensure(ctx, ctx->runinfo, 64 + size_t(M + 1) * 8));
   launch_tile_costs(P_<int32_t>(ctx->tile_diff), ctx->cam.TX, ctx->cam.TY, P_<int32_t>(ctx->tile_pairs), s);
   CKS(launched(ctx));
   CKS(ctx->tr->allreduce_i32(ctx, P_<int32_t>(ctx->tile_pairs), T, s));
   int32_t* run = P_<int32_t>(ctx->runinfo);
   long long* pown = reinterpret_cast<long long*>(P_<char>(ctx->runinfo) + 64);
-  launch_owner_map(P_<int32_t>(ctx->tile_pairs), T, M, P_<int32_t>(ctx->owner), run, pown, s);
+  launch_owner_map(P_<int32_t>(ctx->tile_pairs), T, M, P_<int32_t>(ctx->owner), run, pown, tile_owner_in, s);
   CKS(launched(ctx));
   if (tile_owner_out) CK(cudaMemcpyAsync(tile_owner_out, ctx->owner.p, size_t(T) * 4, cudaMemcpyDeviceToDevice, s));
   // a4: destination masks, per-destination counts, count exchange
@@ -661,12 +676,13 @@ bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream) {
     CKS(launched(ctx));
   }
   CKS(ctx->tr->alltoall1(ctx, P_<int64_t>(ctx->totals), P_<int64_t>(ctx->xchg_counts), s));
-  int64_t* h = ctx->h_misc;  // [0,M) send, [M,2M) recv, [2M,4M) run, [4M,5M) pown
+  int64_t* h = ctx->h_misc;  // [0,M) send, [M,2M) recv, [2M,4M) run, [4M,5M] pown + bad-map flag
   CK(cudaMemcpyAsync(h, ctx->totals.p, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(h + M, ctx->xchg_counts.p, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(h + 2 * M, run, size_t(2 * M) * 4, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(h + 4 * M, pown, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + 4 * M, pown, size_t(M + 1) * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  if (h[5 * M]) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "tile_owner_in: not contiguous non-decreasing runs in [0, world)");
   ctx->send_cnt.assign(h, h + M);
   ctx->recv_cnt.assign(h + M, h + 2 * M);
   const int32_t* hrun = reinterpret_cast<const int32_t*>(h + 2 * M);
@@ -695,6 +711,7 @@ bgs_status bgs_route(bgs_ctx* ctx, int32_t* tile_owner_out, void* stream) {
   CKS(ctx->tr->alltoallv(ctx, ctx->send.p, ctx->send_cnt.data(), ctx->send_off.data(), ctx->recvbuf.p,
                          ctx->recv_cnt.data(), ctx->recv_off.data(), sizeof(Rec), s));
   ctx->recv = P_<Rec>(ctx->recvbuf);
+  if (n_recv_out) *n_recv_out = R;
   ctx->stage = 2;
   return BGS_OK;
 }
@@ -706,7 +723,7 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 2) return fail(ctx, BGS_ERR_CONTRACT, "bgs_sort_tiles before bgs_route");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const int64_t P = ctx->P;
   if (P >= (int64_t(1) << 30)) return fail(ctx, BGS_ERR_CAPACITY, "more than 2^30 pairs in one view");
   const int nt = ctx->t_end - ctx->t_begin;
@@ -804,7 +821,7 @@ bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_fin
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 3) return fail(ctx, BGS_ERR_CONTRACT, "bgs_raster_fwd before bgs_sort_tiles");
   if (!rgb || !t_final || !n_contrib) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "output image pointer is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   CKS(ensure(ctx, ctx->acc, size_t(std::max<int64_t>(ctx->R, 1)) * sizeof(Acc)));
   CK(cudaMemsetAsync(ctx->acc.p, 0, size_t(std::max<int64_t>(ctx->R, 1)) * sizeof(Acc), s));
   // contributor masks: one word per (warp block, 32-entry chunk of its tile's list), chunk index
@@ -825,7 +842,7 @@ bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL, const float* t_final, c
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_raster_bwd before bgs_raster_fwd");
   if (!dL || !t_final || !n_contrib) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "image pointer is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   RasterArgs a = raster_args(ctx);
   a.n_split = ctx->raster_split;
   if (a.n_tiles > 0) {
@@ -840,7 +857,7 @@ bgs_status bgs_route_reverse(bgs_ctx* ctx, void* stream) {
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_route_reverse before bgs_raster_fwd");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const int M = ctx->world;
   if (M == 1) {
     ctx->acc_local = P_<Acc>(ctx->acc);
@@ -872,7 +889,7 @@ bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camer
   if (!grads || !grads->mean_opac || !grads->quat || !grads->scale || !grads->sh)
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "gradient pointer is NULL");
   if (!cam) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "camera is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   ProjectBwdArgs a{};
   a.mean_opac = reinterpret_cast<const float4*>(g->mean_opac);
   a.quat = reinterpret_cast<const float4*>(g->quat);
@@ -906,7 +923,7 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   if (dense && (!a_in || !radius)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "dense w_fixed needs a and radius");
   if (!dense && ctx->stage < 6) return fail(ctx, BGS_ERR_CONTRACT, "bgs_importance before bgs_route_reverse");
   if (!dense && n_local != ctx->n_local) return fail(ctx, BGS_ERR_CONTRACT, "stale n_local (S:384)");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   ImportanceArgs a{};
   a.n_items = dense ? n_local : ctx->F;
   a.item_lidx = dense ? nullptr : P_<uint32_t>(ctx->rec_lidx);
@@ -977,7 +994,7 @@ bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, ui
   if (n < 0 || (n > 0 && (!mean_opac || !perm_out))) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "spatial_order args");
   if (n >= (int64_t(1) << 30)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "spatial_order: n >= 2^30");
   if (n == 0) return BGS_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   ctx->stage = 0;  // reuses the sort scratch: the current view's intermediates are gone
   SortArgs a{};
   for (int b = 0; b < 2; ++b) {
@@ -1032,7 +1049,7 @@ static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs
                                  cudaEvent_t dl_ready, cudaEvent_t fwd_done, const bgs_supervision* sup = nullptr,
                                  float* dL_sup = nullptr, cudaEvent_t loss_done = nullptr) {
   if (imp) flags |= BGS_IMPORTANCE;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   // stage boundaries (bgs_stage_times): events on the working stream, recorded only when enabled
   auto mark = [&](int k) -> bgs_status {
     if (ctx->stage_timing) CK(cudaEventRecord(ctx->stage_ev[k], s));
@@ -1043,7 +1060,7 @@ static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs
   CKS(mark(0));
   CKS(bgs_project(ctx, g, cam, gate, cull_column, flags, radius_out, stream));
   CKS(mark(1));
-  CKS(bgs_route(ctx, nullptr, stream));
+  CKS(bgs_route(ctx, nullptr, nullptr, nullptr, stream));
   CKS(mark(2));
   CKS(bgs_sort_tiles(ctx, stream));
   CKS(mark(3));
@@ -1054,7 +1071,10 @@ static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs
   if (sup) {
     // NEXT-4: Eq.7 on the owned tiles gives this view's dL/dC; Eq.8 adds to the scale gradient
     CKS(bgs_loss_photo(ctx, rgb, sup->target, sup->lambda, sup->batch_inv, dL_sup, sup->loss_out, stream));
-    if (sup->beta != 0.f) CKS(bgs_loss_scale(ctx, g, sup->beta, grads, sup->loss_out + 3, stream));
+    if (sup->beta != 0.f)
+      CKS(bgs_loss_scale(ctx, g, sup->beta, grads, sup->loss_out + 3, stream));
+    else
+      CK(cudaMemsetAsync(sup->loss_out + 3, 0, 2 * sizeof(double), s));  // {L_scale, |V|} = 0: not computed
     if (loss_done) CK(cudaEventRecord(loss_done, s));
     dL = dL_sup;
   }
@@ -1110,10 +1130,10 @@ bgs_status bgs_train_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, 
   CKS(check_stream(ctx, stream));
   CKS(set_camera(ctx, cam));
   if (!target_host || !loss_host) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "host target / loss pointer is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const size_t npix = size_t(ctx->cam.W) * ctx->cam.H;
   CKS(ensure(ctx, ctx->scr_rgb, npix * 12));
-  CKS(ensure(ctx, ctx->scr_dl, npix * 12));
+  CKS(ensure(ctx, ctx->scr_dlsup, npix * 12));
   CKS(ensure(ctx, ctx->scr_tgt, npix * 12));
   CKS(ensure(ctx, ctx->scr_t, npix * 4));
   CKS(ensure(ctx, ctx->scr_n, npix * 4));
@@ -1132,7 +1152,7 @@ bgs_status bgs_train_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, 
   bgs_supervision sup{tgt, lambda, batch_inv, beta, P_<double>(ctx->scr_loss)};
   CKS(view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, P_<float>(ctx->scr_rgb),
                      P_<float>(ctx->scr_t), P_<int32_t>(ctx->scr_n), nullptr, grads, imp, stream, ctx->ev_dl,
-                     nullptr, &sup, P_<float>(ctx->scr_dl), ctx->ev_fwd));
+                     nullptr, &sup, P_<float>(ctx->scr_dlsup), ctx->ev_fwd));
   CK(cudaEventRecord(ctx->ev_in_free[b], s));
   CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_fwd, 0));
   CK(cudaMemcpyAsync(loss_host, ctx->scr_loss.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->d2h));
@@ -1165,7 +1185,7 @@ bgs_status bgs_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const 
   CKS(check_stream(ctx, stream));
   CKS(set_camera(ctx, cam));
   if (!dL_host || !rgb_host) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "host image pointer is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const size_t npix = size_t(ctx->cam.W) * ctx->cam.H;
   CKS(ensure(ctx, ctx->scr_rgb, npix * 12));
   CKS(ensure(ctx, ctx->scr_dl, npix * 12));
@@ -1200,7 +1220,7 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
                               const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream) {
   CKS(bgs_view_step_host_async(ctx, g, cam, gate, cull_column, flags, radius_out, dL_host, rgb_host, grads, imp,
                                stream));
-  CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  CK(cudaStreamSynchronize(as_stream(stream)));
   return BGS_OK;
 }
 
@@ -1214,7 +1234,7 @@ bgs_status bgs_loss_photo(bgs_ctx* ctx, const float* rgb, const float* target, f
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_loss_photo before bgs_raster_fwd");
   if (!rgb || !target || !dL_drgb || !out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "loss pointer is NULL");
   if (!(lambda >= 0.f && lambda <= 1.f)) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "lambda outside [0, 1]");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const int W = ctx->cam.W, H = ctx->cam.H;
   const size_t plane = size_t(W) * H;
   const float* x = rgb;
@@ -1266,7 +1286,7 @@ bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, float beta, cons
   CKS(check_gaussians(ctx, g));
   if (ctx->stage < 1) return fail(ctx, BGS_ERR_CONTRACT, "bgs_loss_scale before bgs_project");
   if (!out || !grads || !grads->scale) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "loss_scale pointer is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const int64_t F = ctx->F;  // this view's records = the local visible set (radius > 0)
   const uint32_t* lidx = P_<uint32_t>(ctx->rec_lidx);
   const int nb = scale_n_blocks(F);
@@ -1338,7 +1358,7 @@ bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaus
   a.eps = float(h->eps);
   a.c1 = float(1.0 / (1.0 - std::pow(h->beta1, double(h->step))));
   a.c2 = float(1.0 / (1.0 - std::pow(h->beta2, double(h->step))));
-  launch_adam(a, static_cast<cudaStream_t>(stream));
+  launch_adam(a, as_stream(stream));
   CKS(launched(ctx, 2));
   return BGS_OK;
 }
@@ -1364,7 +1384,7 @@ bgs_status bgs_densify_accumulate(bgs_ctx* ctx, int64_t n_local, const double* p
   a.stat = stat;
   a.count = count;
   if (a.F > 0) {
-    launch_densify_accumulate(a, static_cast<cudaStream_t>(stream));
+    launch_densify_accumulate(a, as_stream(stream));
     CKS(launched(ctx));
   }
   return BGS_OK;
@@ -1391,7 +1411,7 @@ bgs_status bgs_densify_apply(bgs_ctx* ctx, const bgs_train_params* in, const uin
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: plane pointer is NULL");
   if (act_out && (!act_out->mean_opac || !act_out->quat || !act_out->scale || !act_out->sh))
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: act_out plane pointer is NULL");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   DensifyArgs a{};
   a.n = in->n_local;
   a.rank = ctx->rank;
@@ -1423,6 +1443,9 @@ bgs_status bgs_densify_apply(bgs_ctx* ctx, const bgs_train_params* in, const uin
   a.logit_min = float(std::log(double(dp->min_opacity) / (1.0 - double(dp->min_opacity))));
   a.log_div = float(std::log(double(dp->split_div)));
   a.seed = dp->seed;
+  if (dp->k_levels < 1 || dp->k_levels > 256)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: k_levels must be in [1, 256]");
+  a.max_level = dp->k_levels - 1;
   if (act_out) {
     a.act[0] = reinterpret_cast<float4*>(act_out->mean_opac);
     a.act[1] = reinterpret_cast<float4*>(act_out->quat);
@@ -1510,7 +1533,7 @@ bgs_status bgs_score_phi(bgs_ctx* ctx, int64_t n_local, const uint32_t* c_rad, c
   CKS(check_stream(ctx, stream));
   if (n_local < 0 || (n_local > 0 && (!c_rad || !c_vis || !phi)))
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_score_phi: arguments");
-  launch_phi(n_local, c_rad, c_vis, phi, static_cast<cudaStream_t>(stream));
+  launch_phi(n_local, c_rad, c_vis, phi, as_stream(stream));
   return n_local > 0 ? launched(ctx) : BGS_OK;
 }
 
@@ -1521,7 +1544,7 @@ bgs_status bgs_prune_stochastic(bgs_ctx* ctx, int64_t n_local, const double* s_s
   if (n_local < 0 || (n_local > 0 && (!s_score || !keep_out)))
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_prune_stochastic: arguments");
   if (n_local >= (int64_t(1) << 32) / ctx->world) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "global ids exceed 32 bits");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   unsigned long long N = (unsigned long long)n_local;
   CKS(sum_over_ranks(ctx, &N, 1, s));
   if (keep_count <= 0 || (unsigned long long)keep_count >= N) {
@@ -1547,7 +1570,7 @@ bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s_sco
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_prune_mass_cut: arguments");
   if (den <= 0 || num <= 0 || num > den) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "mass cut needs 0 < num <= den");
   if (n_local >= (int64_t(1) << 32) / ctx->world) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "global ids exceed 32 bits");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   if (all_zero_out) *all_zero_out = 0;
   CKS(ensure(ctx, ctx->sel_keys, size_t(std::max<int64_t>(n_local, 1)) * 8));
   CKS(ensure(ctx, ctx->dcnt, 64 * 8));
@@ -1596,7 +1619,7 @@ bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t
   if (!in || !out || !n_out || in->n_local < 0 || (in->n_local > 0 && (!keep || !in->mean_opac || !in->quat ||
                                                                      !in->scale || !in->sh)))
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_redistribute: arguments");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t s = as_stream(stream);
   const int M = ctx->world, rank = ctx->rank;
   const int64_t n = in->n_local;
   // every rank's shard size (one-hot sums).  The global order is gid = j M + m over slices padded

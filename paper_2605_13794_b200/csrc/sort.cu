@@ -395,14 +395,12 @@ __global__ void __launch_bounds__(256) k_ranges_fixup(SortArgs a, int64_t P) {
 void launch_emit(const SortArgs& a, cudaStream_t s) {
   if (a.n_recv <= 0) return;
   const int64_t chunks = (a.n_recv + 255) / 256;
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<int> slots[kMaxDevices];
+  const int max_blocks = per_device(slots, [] {
+    int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, 256, 0);
-    max_blocks = sms * (occ < 4 ? (occ > 0 ? occ : 1) : 4);
-  }
+    return device_sm_count() * (occ < 4 ? (occ > 0 ? occ : 1) : 4);
+  });
   const int64_t blocks = chunks < max_blocks ? chunks : max_blocks;
   k_emit<<<unsigned(blocks), 256, 0, s>>>(a);
 }
@@ -419,11 +417,11 @@ static void sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* l
   constexpr int PART = kSortBlock * ITEMS;
   const int n_parts = int((P + PART - 1) / PART);
   const size_t smem = size_t(PART) * (sizeof(K) + sizeof(uint32_t));
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<int> attr[kMaxDevices];
+  per_device(attr, [smem] {
     cudaFuncSetAttribute(k_onesweep<8, K, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr_set = true;
-  }
+    return 1;
+  });
   for (int p = 0; p < a.n_passes; ++p) {
     k_onesweep<8, K, ITEMS><<<n_parts, 256, smem, s>>>(a, P, p, n_parts);
     ++*launches;

@@ -54,7 +54,8 @@ class GpuStep:
     """One view through a1..a12 on one ctx (world 1) or an in-process group (world > 1)."""
 
     def __init__(self, scene, cam, M=1, gate=None, cull_global=None, flags=0, dLdC=None, importance=True,
-                 ctxs=None, device=0, target=None, lam=0.2, batch_inv=1.0, beta=None, densify=False, phi=None):
+                 ctxs=None, device=0, target=None, lam=0.2, batch_inv=1.0, beta=None, densify=False, phi=None,
+                 owner_in=None):
         import paper_2605_13794_b200.bgs as B
         self.B = B
         self.M = M
@@ -92,7 +93,8 @@ class GpuStep:
                     out["q_project"] = ctx.query()
                     out["records"] = rec_view(ctx.debug_buffer("records"))
                     out["rec_lidx"] = ctx.debug_buffer("rec_lidx").view(torch.int32).cpu().numpy()
-                    B.bgs_route(ctx, owner, stream)
+                    oin = None if owner_in is None else torch.from_numpy(np.ascontiguousarray(owner_in, np.int32)).to(dev)
+                    out["R_route"] = B.bgs_route(ctx, owner, stream, tile_owner_in=oin)
                     out["owner"] = owner.cpu().numpy()
                     B.bgs_sort_tiles(ctx, stream)
                     out["q"] = ctx.query()

@@ -81,11 +81,14 @@ def test_apply_parity(world, rank):
     ctxs = B.Context.local_group(world, 0) if world > 1 else [B.Context(0, 1, 0)]
     try:
         nn = B.bgs_densify_apply(ctxs[rank], tin, torch.from_numpy(lod).to(dev), torch.from_numpy(stat).to(dev),
-                                 torch.from_numpy(count).to(dev), B.densify_params(TAU, EXT, MINO, DIV, SEED), tout,
-                                 lod_out, act)
+                                 torch.from_numpy(count).to(dev), B.densify_params(TAU, EXT, MINO, DIV, SEED, k_levels=6),
+                                 tout, lod_out, act)
         torch.cuda.synchronize()
-        ref, rst, rlod, cnt = DC.apply(params, state, lod, stat, count, TAU, EXT, MINO, DIV, SEED, rank, world)
+        ref, rst, rlod, cnt = DC.apply(params, state, lod, stat, count, TAU, EXT, MINO, DIV, SEED, rank, world,
+                                       k_levels=6)
         assert cnt["kept"] > 0 and cnt["clones"] > 0 and cnt["splits"] > 0
+        # heritage rule at the ceiling: a split of a level-(K-1) parent stays at K-1
+        assert rlod.max() == 5 and (rlod[cnt["kept"] + cnt["clones"]:] == 5).any()
         assert nn == len(rlod)
         assert np.array_equal(lod_out.cpu().numpy()[:nn], rlod)
         K, Cn = cnt["kept"], cnt["clones"]

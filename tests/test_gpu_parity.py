@@ -270,6 +270,27 @@ def test_multirank_local_group_parity(tiny_scene, tiny_run, M):
         gs.close()
 
 
+def test_route_given_owner_map(tiny_scene, tiny_run):
+    """bgs_route's tile_owner_in: the oracle's owner map passed in reproduces the
+    a3 split's routing; a map that is not contiguous runs is refused on every rank."""
+    import paper_2605_13794_b200.bgs as B
+    sc, cam, dl, st1, gs1 = tiny_run
+    M = 3
+    st = O.OracleStep(sc, cam, M=M, dLdC=dl)
+    gs = GpuStep(sc, cam, M=M, dLdC=dl, owner_in=st.get("owner"))
+    try:
+        for r in range(M):
+            assert np.array_equal(gs.rank[r]["owner"], st.get("owner"))
+            assert gs.rank[r]["R_route"] == len(st.get("recv", r))
+        assert np.array_equal(gs.img, gs1.img) and np.array_equal(gs.nc, gs1.nc)
+    finally:
+        gs.close()
+    bad = st.get("owner").copy()
+    bad[0], bad[-1] = bad[-1], bad[0]
+    with pytest.raises(B.BgsError, match="tile_owner_in"):
+        GpuStep(sc, cam, M=M, dLdC=dl, owner_in=bad)
+
+
 def test_gate_and_cull_bit_exact():
     sc = S.gen_city("rubble", n=200_000, W=576, H=432, V=4)
     cam = sc.cameras[2]

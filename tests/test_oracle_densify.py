@@ -67,6 +67,22 @@ def test_split_one_large_gaussian():
     assert np.array_equal(out["sh"][:9], p["sh"][keep])
 
 
+def test_split_heritage_clamped_at_finest_level():
+    """SPEC apply_heritage examples: clone keeps l, split gives min(l + 1, K - 1), so
+    (K - 1, split) -> K - 1 and every level stays in [0, K - 1]."""
+    K = 6
+    p, s, lod = _shard(4)
+    lod[:] = [0, K - 1, K - 2, K - 1]
+    p["log_scale"][[1, 2], :3] = np.log(0.5)                          # 1, 2 split; 3 clones
+    stat = np.zeros(4)
+    stat[1:] = 1.0
+    out, _, ol, cnt = DC.apply(p, s, lod, stat, np.ones(4), TAU, EXT, MINO, DIV, 3, k_levels=K)
+    assert cnt == dict(kept=2, clones=1, splits=2)
+    # kept originals (0, 3), the clone of 3, first children (1, 2), second children (1, 2)
+    assert list(ol) == [0, K - 1, K - 1, K - 1, K - 1, K - 1, K - 1]
+    assert ol.max() <= K - 1
+
+
 def test_prune_low_opacity_including_children():
     p, s, lod = _shard(6)
     p["mean_logit"][[1, 3], 3] = math.log(0.004 / 0.996)              # opacity 0.004 < 0.005
