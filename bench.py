@@ -3,18 +3,20 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config rubble] [--impl reference]
 
-N > 1: launched by torch.distributed.run (one rank per GPU, NCCL).  One step = one view through
-every SURVEY §8(a) row: a1 gate + a2 projection -> a3/a4 ownership + all-to-all -> a5-a7 pair
-emission / onesweep sort / ranges -> a8 compositing (+ w, a) -> a9 backward -> a10 reverse
-exchange -> a11 projection backward -> a12 importance (Eq.3, top-99% mass, Cull column).
-The per-view image gradient dL/dC is a fixed seeded tensor (the Eq.7 loss is outside the path).
-Rank 0 prints ONE JSON line.  See DESIGN.md §7 for every number's definition.
+N > 1: launched by torch.distributed.run (one rank per GPU, NCCL).  A STEP is one training batch of
+B = 4 views (the paper's mini-batch; `--batch`), every view through the unit of work of
+SURVEY §8(d): a1 gate + a2 projection -> a3/a4 ownership + all-to-all -> a5-a7 pair emission /
+onesweep sort / ranges -> a8 compositing -> a9 backward -> a10 reverse exchange -> a11 projection
+backward.  a12 (importance) is timed separately (`with_importance`, `scoring`).  The per-view image
+gradient dL/dC is a fixed seeded tensor (the Eq.7 loss is outside the unit; the `train` block adds
+it).  Rank 0 prints ONE JSON line.  See DESIGN.md §7 for every number's definition.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -39,30 +41,29 @@ CONFIG_SHAPES = {
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50, help="timed steps (batches of --batch views)")
     p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--batch", type=int, default=4, help="views per step (B = 4, P:342), all in flight")
     p.add_argument("--config", default="rubble", choices=sorted(CONFIG_SHAPES))
     p.add_argument("--impl", default="native", choices=["native", "reference"])
     p.add_argument("--n", type=int, default=None, help="override Gaussian count (debug only)")
     p.add_argument("--views", type=int, default=64)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--stages", action="store_true", help="also print per-stage timings to stderr")
+    p.add_argument("--gate", choices=["config", "on", "off"], default="config",
+                   help="LOD gate + importance mask: the config's default, or forced (Table-2-style toggles)")
+    p.add_argument("--mask", choices=["config", "on", "off"], default="config",
+                   help="importance Cull mask when the gate is on: the config's default, or forced")
     p.add_argument("--layout", default="morton", choices=["morton", "input"],
                    help="shard storage order: Z-order (bgs_spatial_order) or the generator's random ids")
     p.add_argument("--host-threads", type=int, default=0,
-                   help="1: one host thread per in-flight context (the ABI's one-ctx-per-host-thread model), so "
-                        "a context's HOST-SYNC calls block only its own thread; 0: one thread submits all views")
-    p.add_argument("--inflight", type=int, default=4,
-                   help="views in flight per rank (one ctx + stream each); 4 = the paper's batch of B = 4 "
-                        "views per step (P:342). Measured on Rubble (second session): 1 -> 1219, 4 -> 1383, "
-                        "6 -> 1388, 8 -> 1386 views/s")
+                   help="1: one host thread per in-flight context (the ABI's one-ctx-per-host-thread model)")
+    p.add_argument("--quick", action="store_true", help="headline, e2e and stages only (no train/scoring/simplify)")
     return p.parse_args()
 
 
 def submit_views(fn, inflight: int, ids, threaded: bool, device: int):
     """Enqueue view ids[j] on in-flight context j % inflight via fn(k, v).  threaded: one host thread
-    per context (ctypes releases the GIL inside the ABI calls), so the host round trip of one view's
-    HOST-SYNC projection does not hold back the submission of the other contexts' views."""
+    per context (ctypes releases the GIL inside the ABI calls)."""
     if not threaded or inflight == 1:
         for j, v in enumerate(ids):
             fn(j % inflight, v)
@@ -89,11 +90,13 @@ def submit_views(fn, inflight: int, ids, threaded: bool, device: int):
 
 
 # ------------------------------------------------------------------------------------------
-# clocks sampling (nvidia-smi during the timed region)
+# clocks sampling (NVML / nvidia-smi during the timed region)
 # ------------------------------------------------------------------------------------------
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clock-event reason bits (nvml.h): sw power cap 0x4, hw slowdown 0x8, sw thermal 0x20, hw thermal 0x40
+    REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, device: int):
         self.device = device
@@ -103,10 +106,6 @@ class ClockSampler:
         self.nvml = None
         self.samples = []
         self.stop_flag = False
-
-    # NVML clock-event reason bits (nvml.h): sw power cap 0x4, hw slowdown 0x8, sw thermal 0x20,
-    # hw thermal 0x40
-    REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def _nvml_sample(self):
         import pynvml
@@ -123,7 +122,6 @@ class ClockSampler:
             time.sleep(0.001)
 
     def start(self):
-        # NVML polling (~1 ms) so that a short timed region still has samples; nvidia-smi otherwise
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -190,6 +188,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def clocks_ok(clk: dict) -> bool:
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if bad & set(clk.get("reasons") or []):
+        return False
+    sm, mx = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    return not (sm and mx and sm < 0.7 * mx and "sw_power_cap" not in (clk.get("reasons") or []))
+
+
+def config_dict(args, label, gate_on, mask_on, N_all, W, H, world, batch):
+    return {"workload": label, "config": args.config, "gaussians": int(N_all), "width": W, "height": H,
+            "views": args.views, "lod_gate": gate_on, "importance_mask": mask_on,
+            "parallelism": f"index-parity shards x {world}, tile-owner all-to-all",
+            "unit_of_work": "a1-a11 per view (SURVEY 8(d)); a12 importance timed separately"}
+
+
 # ------------------------------------------------------------------------------------------
 # the native arm
 # ------------------------------------------------------------------------------------------
@@ -207,18 +220,21 @@ def run_native(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
-    inflight = max(1, args.inflight)
+    tdev = torch.device(dev)
+    batch = max(1, args.batch)
     if world > 1:
-        D.init("nccl", torch.device(dev))
+        D.init("nccl", tdev)
         ctxs = []
-        for _ in range(inflight):  # one communicator per in-flight ctx
-            uid = D.broadcast_bytes(B.unique_id() if rank == 0 else None, 128, torch.device(dev))
+        for _ in range(batch):  # one communicator per in-flight ctx
+            uid = D.broadcast_bytes(B.unique_id() if rank == 0 else None, 128, tdev)
             ctxs.append(B.Context(rank, world, local, uid))
     else:
-        ctxs = [B.Context(0, 1, local) for _ in range(inflight)]
+        ctxs = [B.Context(0, 1, local) for _ in range(batch)]
     ctx = ctxs[0]
 
-    label, gate_on = CONFIG_SHAPES[args.config]
+    label, gate_default = CONFIG_SHAPES[args.config]
+    gate_on = gate_default if args.gate == "config" else args.gate == "on"
+    mask_on = gate_on if args.mask == "config" else (args.mask == "on" and gate_on)
     t0 = time.perf_counter()
     scene = S.gen_city(args.config, n=args.n, V=args.views)
     gen_s = time.perf_counter() - t0
@@ -237,442 +253,430 @@ def run_native(args):
     cams = [B.camera(c) for c in scene.cameras]
     # d0: 4x the median camera distance (R19) so the gate is selective, not degenerate
     gate = B.lod_gate(True, scene.k_levels - 1, scene.d0 * 4) if gate_on else None
-    stream = torch.cuda.Stream(dev)
     grads = g.zeros_grads()
-    radius = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
-    rgb = torch.zeros(3, H, W, device=dev)
-    Tf = torch.zeros(H, W, device=dev)
-    nc = torch.zeros(H, W, dtype=torch.int32, device=dev)
+    nw = (max(n_local, 1) + 31) // 32
     s_imp = torch.zeros(max(n_local, 1), dtype=torch.float64, device=dev)
     c_rad = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
     c_vis = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
-    cull_cols = None
-    imp = B.importance_out(s_imp, c_rad, c_vis, torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32,
-                                                             device=dev))
     dl = torch.from_numpy(S.grad_image(H, W)).to(dev)
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    per = []
+    for k in range(batch):
+        per.append(dict(stream=torch.cuda.Stream(dev), radius=torch.zeros(max(n_local, 1), dtype=torch.int32,
+                                                                          device=dev),
+                        rgb=torch.zeros(3, H, W, device=dev), Tf=torch.zeros(H, W, device=dev),
+                        nc=torch.zeros(H, W, dtype=torch.int32, device=dev),
+                        cull=torch.zeros(nw, dtype=torch.int32, device=dev)))
+    stream = per[0]["stream"]
 
-    if gate_on:
-        # Building config: per-view Cull columns from one untimed importance sweep
+    cull_cols = None
+    if mask_on:
+        # per-view Cull columns from one untimed importance sweep (Building config)
         cull_cols = []
+        p = per[0]
         with torch.cuda.stream(stream):
             for v, cam in enumerate(cams):
-                cc = torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32, device=dev)
-                B.bgs_view_step(ctx, g, cam, None, None, B.BGS_NO_COLOR, radius, rgb, Tf, nc, None, None,
-                                B.importance_out(s_imp, c_rad, c_vis, cc), stream)
+                cc = torch.zeros(nw, dtype=torch.int32, device=dev)
+                B.bgs_view_step(ctx, g, cam, None, None, B.BGS_NO_COLOR, p["radius"], p["rgb"], p["Tf"], p["nc"],
+                                None, None, B.importance_out(s_imp, c_rad, c_vis, cc), stream)
                 cull_cols.append(cc)
         stream.synchronize()
 
-    stage_names = B.STAGES
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    cull_out = torch.zeros((max(n_local, 1) + 31) // 32, dtype=torch.int32, device=dev)
-    imp_view = B.importance_out(s_imp, c_rad, c_vis, cull_out, 99, 100)
+    def cull_of(v):
+        return cull_cols[v % len(cams)] if cull_cols is not None else None
 
-    def one_view(v, record):
-        # one step = one bgs_view_step call (a1..a12; the library records its stage events)
-        cam = cams[v % len(cams)]
-        cull = cull_cols[v % len(cams)] if cull_cols is not None else None
-        if record:
-            ev[0].record(stream)
-        B.bgs_view_step(ctx, g, cam, gate, cull, 0, radius, rgb, Tf, nc, dl, grads, imp_view, stream)
-        if record:
-            ev[1].record(stream)
+    def imp_of(k):
+        return B.importance_out(s_imp, c_rad, c_vis, per[k]["cull"], 99, 100)
+
+    def view_on(k, v, with_imp=False):
+        p = per[k]
+        B.bgs_view_step(ctxs[k], g, cams[v % len(cams)], gate, cull_of(v), 0, p["radius"], p["rgb"], p["Tf"],
+                        p["nc"], dl, grads, imp_of(k) if with_imp else None, p["stream"])
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    with torch.cuda.stream(stream):
-        # the ctx arena is grow-only and sized by the largest view seen: one untimed pass over the
-        # camera set brings it to its steady state (as after the first epoch of a training run),
-        # then the W warm-up views
+    # the ctx arenas are grow-only and sized by the largest view seen: one untimed pass over the
+    # camera set per ctx brings them to steady state (as after the first epoch of training)
+    for k in range(batch):
         for v in range(len(cams)):
-            one_view(v, False)
-        for w in range(args.warmup):
-            one_view(w, False)
-        stream.synchronize()
-        barrier()
-        # one view at a time, L2 flushed before each: the per-stage breakdown and single_view_ms
-        stage_ms = np.zeros(len(stage_names))
-        qs = []
-        total_ms = 0.0
-        E_sum = 0.0
-        A_sum = 0.0
+            view_on(k, v, with_imp=True)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- per-stage breakdown: one view at a time, L2 flushed before each (a1-a11; then a1-a12
+    # for the importance stage), library-side stage events
+    def stage_loop(n_views, with_imp):
+        stage_ms = np.zeros(len(B.STAGES))
+        qs, tot, E_sum, A_sum = [], 0.0, 0.0, 0.0
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        p = per[0]
         B.bgs_set_stage_timing(ctx, True)
-        for k in range(args.steps):
-            l2_flush.zero_()  # between timed views: evict the L2 (inputs also exceed it)
-            stream.synchronize()
-            one_view(args.warmup + k, True)
-            stream.synchronize()
-            st = B.bgs_stage_times(ctx)
-            stage_ms += np.array([st[n] for n in stage_names])
-            total_ms += ev[0].elapsed_time(ev[1])
-            qs.append(ctx.query())
-            E_sum += float(nc.sum(dtype=torch.int64).item())  # outside the timed events
-            # contributing (pixel, splat) pairs = sum of a over this rank's received splats
-            acc = ctx.debug_buffer("acc")
-            if acc.numel():
-                A_sum += float(acc.view(torch.int32).view(-1, 12)[:, 9].sum(dtype=torch.int64).item())
+        with torch.cuda.stream(stream):
+            for k in range(n_views):
+                v = args.warmup + k
+                l2_flush.zero_()
+                stream.synchronize()
+                ev[0].record(stream)
+                B.bgs_view_step(ctx, g, cams[v % len(cams)], gate, cull_of(v), 0, p["radius"], p["rgb"], p["Tf"],
+                                p["nc"], dl, grads, imp_of(0) if with_imp else None, stream)
+                ev[1].record(stream)
+                stream.synchronize()
+                st = B.bgs_stage_times(ctx)
+                stage_ms += np.array([st[n] for n in B.STAGES])
+                tot += ev[0].elapsed_time(ev[1])
+                qs.append(ctx.query())
+                E_sum += float(p["nc"].sum(dtype=torch.int64).item())
+                if with_imp:  # contributing (pixel, splat) pairs = sum of a over the received splats
+                    acc = ctx.debug_buffer("acc")
+                    if acc.numel():
+                        A_sum += float(acc.view(torch.int32).view(-1, 12)[:, 9].sum(dtype=torch.int64).item())
         B.bgs_set_stage_timing(ctx, False)
+        return stage_ms / n_views, qs, tot / n_views, E_sum / n_views, A_sum / n_views
+
+    n_stage = min(max(args.steps, 8), 64)
+    stage_avg, qs, single_ms, E_avg, _ = stage_loop(n_stage, False)
+    imp_avg, qs_imp, single_imp_ms, _, A_avg = stage_loop(n_stage, True)
+    stage_avg = stage_avg.copy()
+    stage_avg[list(B.STAGES).index("importance")] = imp_avg[list(B.STAGES).index("importance")]
     torch.cuda.synchronize()
     barrier()
-    single_ms = D.max_over_ranks(total_ms, torch.device(dev)) / args.steps
+    single_ms = D.max_over_ranks(single_ms, tdev)
+    single_imp_ms = D.max_over_ranks(single_imp_ms, tdev)
 
-    # ---- the headline: `inflight` views in flight per rank, one ctx + stream each, sharing the
-    # shard, the gradient buffers and the importance outputs (all accumulated with reductions);
-    # no L2 flush between views (they overlap; every view's inputs exceed the 126 MB L2 anyway)
-    per = [dict(stream=stream, radius=radius, rgb=rgb, Tf=Tf, nc=nc, cull=cull_out)]
-    for k in range(1, inflight):
-        per.append(dict(stream=torch.cuda.Stream(dev), radius=torch.zeros_like(radius), rgb=torch.zeros_like(rgb),
-                        Tf=torch.zeros_like(Tf), nc=torch.zeros_like(nc), cull=torch.zeros_like(cull_out)))
+    # ---- the headline: K steps, each a batch of B views in flight (one ctx + stream per view),
+    # sharing the shard and the gradient buffers (accumulated with reductions); no L2 flush between
+    # views (they overlap; every view reads the 1.45 GB shard, > the 126 MB L2)
+    def timed_batches(fn, n_steps, warm):
+        submit_views(fn, batch, [k for k in range(warm * batch)], bool(args.host_threads), local)
+        torch.cuda.synchronize()
+        barrier()
+        ev_start = torch.cuda.Event(enable_timing=True)
+        ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(batch)]
+        clocks = ClockSampler(local)
+        clocks.start()
+        l0 = sum(c.launches() for c in ctxs)
+        h0 = sum(c.host_syncs() for c in ctxs)
+        ev_start.record(per[0]["stream"])
+        for k in range(1, batch):
+            per[k]["stream"].wait_event(ev_start)
+        submit_views(fn, batch, [warm * batch + j for j in range(n_steps * batch)], bool(args.host_threads), local)
+        for k in range(batch):
+            ev_end[k].record(per[k]["stream"])
+        torch.cuda.synchronize()
+        launches = sum(c.launches() for c in ctxs) - l0
+        hsyncs = sum(c.host_syncs() for c in ctxs) - h0
+        clk = clocks.stop()
+        ms = max(ev_start.elapsed_time(e) for e in ev_end)
+        barrier()
+        return D.max_over_ranks(ms, tdev), launches, hsyncs, clk
 
-    def view_on(k, v):
-        p = per[k]
-        cam = cams[v % len(cams)]
-        cull = cull_cols[v % len(cams)] if cull_cols is not None else None
-        B.bgs_view_step(ctxs[k], g, cam, gate, cull, 0, p["radius"], p["rgb"], p["Tf"], p["nc"], dl, grads,
-                        B.importance_out(s_imp, c_rad, c_vis, p["cull"], 99, 100), p["stream"])
+    head_ms, launches, hsyncs, clk = timed_batches(lambda k, v: view_on(k, v), args.steps, args.warmup)
+    if not clocks_ok(clk):  # rejected clocks: re-measure once
+        head_ms, launches, hsyncs, clk = timed_batches(lambda k, v: view_on(k, v), args.steps, args.warmup)
+        clk["remeasured"] = True
+    n_views = args.steps * batch
+    ms_per_step = head_ms / args.steps
+    views_per_s = 1000.0 * n_views / head_ms
 
-    for k in range(1, inflight):  # arena warm-up of the other contexts
-        with torch.cuda.stream(per[k]["stream"]):
-            for v in range(len(cams)):
-                view_on(k, v)
-    torch.cuda.synchronize()
-    barrier()
-    ev_start = torch.cuda.Event(enable_timing=True)
-    ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(inflight)]
-    clocks = ClockSampler(local)
-    clocks.start()
-    launches0 = sum(c.launches() for c in ctxs)
-    ev_start.record(per[0]["stream"])
-    for k in range(1, inflight):
-        per[k]["stream"].wait_event(ev_start)
-    submit_views(view_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads), local)
-    for k in range(inflight):
-        ev_end[k].record(per[k]["stream"])
-    torch.cuda.synchronize()
-    launches = sum(c.launches() for c in ctxs) - launches0
-    clk = clocks.stop()
-    total_ms = max(ev_start.elapsed_time(e) for e in ev_end)
-    barrier()
-    total_ms_max = D.max_over_ranks(total_ms, torch.device(dev))
-    ms_per_view = total_ms_max / args.steps
-    views_per_s = 1000.0 / ms_per_view
+    imp_ms, imp_launches, _, _ = timed_batches(lambda k, v: view_on(k, v, True), args.steps, 1)
+    with_importance = {"metric": "fwd+bwd views/s with a12 (importance, Cull column) per view",
+                       "value": round(1000.0 * n_views / imp_ms, 3), "unit": "views/s",
+                       "ms_per_step": round(imp_ms / args.steps, 4), "gpu_launches": int(imp_launches)}
 
     # ---- per-view workload statistics (summed over ranks)
-    P_rank = float(np.mean([q["P"] for q in qs]))
-    stats = D.sum_over_ranks([P_rank, np.mean([q["F"] for q in qs]), np.mean([q["R"] for q in qs]),
-                              np.mean([q["D"] for q in qs]), np.mean([q["n_active"] for q in qs]), float(n_local)],
-                             torch.device(dev))
-    P_all, F_all, R_all, D_all, A_all, N_all = [float(x) for x in stats]
+    def avg(key, qq):
+        return float(np.mean([q[key] for q in qq]))
+
+    P_rank = avg("P", qs)
+    stats = D.sum_over_ranks([P_rank, avg("F", qs), avg("R", qs), avg("D", qs), avg("n_active", qs), float(n_local),
+                              float(A_avg)], tdev)
+    P_all, F_all, R_all, D_all, A_all, N_all, Acontrib_all = [float(x) for x in stats]
+    P_max = D.max_over_ranks(P_rank, tdev)
     pairs_per_s = P_all * views_per_s
 
-    # ---- e2e: same metric through the host-buffer ABI call (H2D of dL/dC, D2H of the image)
-    # (bgs_view_step_host_async on every in-flight ctx, one pinned output image per ctx; wall clock
-    # from the first call to the synchronisation of every stream, each view's dL/dC uploaded and
-    # image downloaded inside the region)
+    # ---- e2e: the same steps through the host-buffer ABI call (pinned dL/dC H2D and the rendered
+    # image D2H inside the timed region, per view), wall clock, max over ranks
     dl_host = torch.from_numpy(S.grad_image(H, W)).pin_memory()
-    rgb_hosts = [torch.empty(3, H, W).pin_memory() for _ in range(inflight)]
+    rgb_hosts = [torch.empty(3, H, W).pin_memory() for _ in range(batch)]
 
     def host_view(k, v):
         p = per[k]
-        B.bgs_view_step_host_async(ctxs[k], g, cams[v % len(cams)], gate,
-                                   cull_cols[v % len(cams)] if cull_cols is not None else None, 0, p["radius"],
-                                   dl_host, rgb_hosts[k], grads,
-                                   B.importance_out(s_imp, c_rad, c_vis, p["cull"], 99, 100), p["stream"])
+        B.bgs_view_step_host_async(ctxs[k], g, cams[v % len(cams)], gate, cull_of(v), 0, p["radius"], dl_host,
+                                   rgb_hosts[k], grads, None, p["stream"])
 
-    for k in range(inflight):
-        host_view(k, k)
+    submit_views(host_view, batch, list(range(batch)), False, local)
     torch.cuda.synchronize()
     barrier()
     t1 = time.perf_counter()
-    submit_views(host_view, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads), local)
+    submit_views(host_view, batch, [args.warmup * batch + j for j in range(n_views)], bool(args.host_threads), local)
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t1
-    e2e_views = args.steps / D.max_over_ranks(e2e_s, torch.device(dev))
+    e2e_s = D.max_over_ranks(time.perf_counter() - t1, tdev)
+    e2e_views = n_views / e2e_s
 
-    # ---- NEXT-4 supervised training step: bgs_train_view_step = a1..a12 with Eq.7 (L1 + SSIM on
-    # the owned tiles, its gradient as this view's dL/dC) and Eq.8 (scale regulariser); lambda 0.2
-    # (3DGS), B = 4 views per step (batch_inv 1/4), beta 0.01 / B; one seeded target image
-    train = train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_rad, c_vis, stream, l2_flush,
-                       inflight, barrier, dev, H, W, n_local, world)
+    result = {
+        "metric": METRIC, "value": round(views_per_s, 3), "unit": "views/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": dict(config_dict(args, label, gate_on, mask_on, N_all, W, H, world, batch),
+                       shard_layout=args.layout, host_threads=bool(args.host_threads),
+                       l2=("inputs exceed L2 (every view reads the 1.45 GB shard); the B views of a step overlap "
+                           "and are not flushed between; stages_ms / single_view_ms: one view at a time, L2 "
+                           "flushed (256 MB write) before each"),
+                       arena="pre-grown by one untimed pass over the cameras per ctx before the warm-up steps"),
+        "views_per_step": batch,
+        "single_view_ms": round(single_ms, 4),
+        "single_view_with_importance_ms": round(single_imp_ms, 4),
+        "splat_pairs_per_s": round(pairs_per_s, 1),
+        "with_importance": with_importance,
+        "per_view": {"pairs_P": P_all, "records_F": F_all, "received_R": R_all, "sent_D": D_all,
+                     "active_A": A_all, "duplication_D_over_F": (D_all / F_all if F_all else None),
+                     "nvlink_bytes": 48.0 * (D_all - F_all) * 2 if world > 1 else 0.0,
+                     "E_min_pixel_entries": round(E_avg, 1),
+                     "contributing_pairs": round(Acontrib_all, 1),
+                     "gate_keep": (avg("n_lod", qs) / n_local) if gate_on and n_local else None,
+                     "owned_pairs_max_over_mean": (P_max * world / P_all) if P_all else None},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_view": round(launches / n_views, 2),
+        "host_syncs_per_view": round(hsyncs / n_views, 3),
+        "clocks": clk,
+        "scene_gen_s": round(gen_s, 2),
+    }
 
-    # ---- scoring views/s: the a12 sweep step = NO_COLOR projection, routing,
-    # sort, instrumented forward, reverse exchange of (w, a), importance; no backward
-    sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    with torch.cuda.stream(stream):
-        score_ms = 0.0
-        for k in range(args.warmup + args.steps):
-            v = args.warmup + k
-            cam = cams[v % len(cams)]
-            cull = cull_cols[v % len(cams)] if cull_cols is not None else None
-            if k >= args.warmup:
-                l2_flush.zero_()
-                stream.synchronize()
-                sev[0].record(stream)
-            B.bgs_project(ctx, g, cam, gate, cull, B.BGS_NO_COLOR, radius, stream)
-            B.bgs_route(ctx, None, stream)
-            B.bgs_sort_tiles(ctx, stream)
-            B.bgs_raster_fwd(ctx, B.BGS_IMPORTANCE, rgb, Tf, nc, stream)
-            B.bgs_route_reverse(ctx, stream)
-            B.bgs_importance(ctx, n_local, radius, None, None, s_imp, c_rad, c_vis, cull_out, 99, 100, stream)
-            if k >= args.warmup:
-                sev[1].record(stream)
-                stream.synchronize()
-                score_ms += sev[0].elapsed_time(sev[1])
-    score_ms_max = D.max_over_ranks(score_ms, torch.device(dev)) / args.steps
+    extra = {}
+    if not args.quick:
+        extra["scoring"] = scoring(args, B, ctxs, per, g, cams, gate, cull_of, s_imp, c_rad, c_vis, l2_flush,
+                                   batch, barrier, D, tdev, n_local, local)
+        extra["train"] = train_iterations(args, B, S, ctxs, per, g, cams, gate, cull_of, imp_of, stream, l2_flush,
+                                          batch, barrier, D, tdev, H, W, n_local, local)
+        extra["simplify"] = simplify(args, B, ctx, g, s_imp, c_rad, c_vis, stream, barrier, D, tdev, n_local, N_all)
 
-    # the same sweep step with the views in flight (a scoring pass sweeps all V training views, so
-    # its views overlap like the training batch's): one ctx + stream per view in flight
+    # ---- rooflines: the dominant kernel on the contributing-pair basis
+    from paper_2605_13794_b200.roofline import load_traffic, stage_rooflines
+    peaks = load_peaks()
+    traffic = (load_traffic(os.path.join(ROOT, "profiles", "ncu_traffic.json"))
+               if args.config == "rubble" and world == 1 else None)
+    roof = stage_rooflines(stage_avg, qs_imp, n_local=n_local, W=W, H=H, world=world, peaks=peaks, E=E_avg,
+                           A=A_avg, cull=cull_cols is not None, traffic=traffic, names=B.STAGES)
+    dominant = max((r for r in roof if r["stage"] != "importance"), key=lambda r: r["ms"])
+    result["stages_ms"] = {n: round(float(v), 4) for n, v in zip(B.STAGES, stage_avg) if n != "loss"}
+    result["roofline"] = {k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+    result["roofline"]["kernel"] = dominant.get("kernel", dominant["stage"])
+    result["roofline"]["basis"] = dominant["work"]
+    result["roofline_stages"] = roof
+    result.update(extra)
+    if "train" in extra and extra["train"].get("loss_stage_ms"):
+        from paper_2605_13794_b200.roofline import loss_roofline
+        extra["train"]["loss_roofline"] = loss_roofline(extra["train"]["loss_stage_ms"], W, H, peaks)
+    result["e2e"] = {"value": round(e2e_views, 3), "unit": "views/s", "h2d_bytes_per_step": int(batch * 3 * H * W * 4),
+                     "d2h_bytes_per_step": int(batch * 3 * H * W * 4),
+                     "path": "bgs_view_step_host_async (pinned host dL/dC in, rendered image out, per view)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(scene, args, cams_idx=args.warmup)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    for c in ctxs:
+        c.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def scoring(args, B, ctxs, per, g, cams, gate, cull_of, s_imp, c_rad, c_vis, l2_flush, batch, barrier, D, tdev,
+            n_local, local):
+    """scoring views/s: the a12 sweep step = NO_COLOR projection, routing, sort,
+    instrumented forward, reverse exchange of (w, a), importance; no backward.  One view at a time
+    (L2 flushed) and with the sweep's views in flight."""
+    import torch
+
     def score_on(k, v):
         p = per[k]
-        cam = cams[v % len(cams)]
-        cull = cull_cols[v % len(cams)] if cull_cols is not None else None
         st_k = p["stream"]
-        B.bgs_project(ctxs[k], g, cam, gate, cull, B.BGS_NO_COLOR, p["radius"], st_k)
+        cam = cams[v % len(cams)]
+        B.bgs_project(ctxs[k], g, cam, gate, cull_of(v), B.BGS_NO_COLOR, p["radius"], st_k)
         B.bgs_route(ctxs[k], None, st_k)
         B.bgs_sort_tiles(ctxs[k], st_k)
         B.bgs_raster_fwd(ctxs[k], B.BGS_IMPORTANCE, p["rgb"], p["Tf"], p["nc"], st_k)
         B.bgs_route_reverse(ctxs[k], st_k)
         B.bgs_importance(ctxs[k], n_local, p["radius"], None, None, s_imp, c_rad, c_vis, p["cull"], 99, 100, st_k)
 
-    for k in range(inflight):
-        score_on(k, args.warmup + k)
+    stream = per[0]["stream"]
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    score_ms = 0.0
+    n1 = min(max(args.steps, 8), 64)
+    with torch.cuda.stream(stream):
+        for k in range(args.warmup + n1):
+            if k >= args.warmup:
+                l2_flush.zero_()
+                stream.synchronize()
+                sev[0].record(stream)
+            score_on(0, k)
+            if k >= args.warmup:
+                sev[1].record(stream)
+                stream.synchronize()
+                score_ms += sev[0].elapsed_time(sev[1])
+    score_ms = D.max_over_ranks(score_ms, tdev) / n1
     torch.cuda.synchronize()
     barrier()
+    n_views = args.steps * batch
     sev_start = torch.cuda.Event(enable_timing=True)
-    sev_end = [torch.cuda.Event(enable_timing=True) for _ in range(inflight)]
+    sev_end = [torch.cuda.Event(enable_timing=True) for _ in range(batch)]
     sev_start.record(per[0]["stream"])
-    for k in range(1, inflight):
+    for k in range(1, batch):
         per[k]["stream"].wait_event(sev_start)
-    submit_views(score_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads), local)
-    for k in range(inflight):
+    submit_views(score_on, batch, list(range(n_views)), bool(args.host_threads), local)
+    for k in range(batch):
         sev_end[k].record(per[k]["stream"])
     torch.cuda.synchronize()
-    score_inflight_ms = D.max_over_ranks(max(sev_start.elapsed_time(e) for e in sev_end),
-                                         torch.device(dev)) / args.steps
-    P_max = D.max_over_ranks(P_rank, torch.device(dev))
-
-    # ---- NEXT-1 scheduled simplification on the same shard, with the s / c_rad / c_vis the
-    # timed views accumulated (one pass each; HOST-SYNC calls, wall time between barriers)
-    simplify = {}
-    with torch.cuda.stream(stream):
-        phi = torch.empty(max(n_local, 1), dtype=torch.float64, device=dev)
-        keep = torch.empty(max(n_local, 1), dtype=torch.uint8, device=dev)
-        cap = (n_local + 1)
-        out_g = B.GaussianPlanes(torch.empty(cap, 4, device=dev), torch.empty(cap, 4, device=dev),
-                                 torch.empty(cap, 4, device=dev), torch.empty(cap, 48, device=dev),
-                                 torch.empty(cap, dtype=torch.uint8, device=dev))
-        N_glob = int(N_all)
-
-        def timed(fn):
-            fn()  # warm-up: first calls grow the ctx arena (cudaMalloc)
-            stream.synchronize()
-            barrier()
-            t1 = time.perf_counter()
-            r = fn()
-            stream.synchronize()
-            return r, D.max_over_ranks((time.perf_counter() - t1) * 1e3, torch.device(dev))
-
-        _, simplify["phi_ms"] = timed(lambda: B.bgs_score_phi(ctx, n_local, c_rad, c_vis, phi, stream))
-        _, simplify["pass1_stochastic_ms"] = timed(
-            lambda: B.bgs_prune_stochastic(ctx, n_local, s_imp, int(round(0.6 * N_glob)), 1234, keep, stream))
-        n_keep1 = D.sum_over_ranks([float(keep[:n_local].sum().item())], torch.device(dev))[0]
-        _, simplify["pass2_mass_cut_ms"] = timed(lambda: B.bgs_prune_mass_cut(ctx, n_local, s_imp, 99, 100, keep,
-                                                                              stream))
-        n_keep2 = D.sum_over_ranks([float(keep[:n_local].sum().item())], torch.device(dev))[0]
-        n_new, simplify["redistribute_ms"] = timed(lambda: B.bgs_redistribute(ctx, g, keep, out_g, stream))
-        simplify.update({"gaussians": N_glob, "kept_pass1": int(n_keep1), "kept_pass2": int(n_keep2),
-                         "note": "keep_fraction 0.6 (S:318 default), target 99/100; scores from the timed views"})
-        del out_g
-
-    # ---- roofline of every stage, dominant one reported at top level
-    from paper_2605_13794_b200.roofline import load_traffic, stage_rooflines
-    peaks = load_peaks()
-    stage_avg = stage_ms / args.steps
-    traffic = (load_traffic(os.path.join(ROOT, "profiles", "ncu_traffic.json"))
-               if args.config == "rubble" and world == 1 else None)
-    roof = stage_rooflines(stage_avg, qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
-                           sm_mhz=clk.get("sm_mhz"), E=E_sum / args.steps, A=A_sum / args.steps,
-                           cull=cull_cols is not None, traffic=traffic, names=stage_names)
-    dominant = max(roof, key=lambda r: r["ms"])
-    train_roof = stage_rooflines(train.pop("stages_avg"), qs, n_local=n_local, W=W, H=H, world=world, peaks=peaks,
-                                 E=E_sum / args.steps, A=A_sum / args.steps, cull=cull_cols is not None,
-                                 traffic=traffic, names=stage_names, with_loss=True)
-    train["loss_roofline"] = next((r for r in train_roof if r["stage"] == "loss"), None)
-
-    result = {
-        "metric": METRIC, "value": round(views_per_s, 3), "unit": "views/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_view, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": label, "config": args.config, "gaussians": int(N_all), "width": W, "height": H,
-                   "views": len(cams), "lod_gate": gate_on, "importance_mask": gate_on,
-                   "parallelism": f"index-parity shards x {world}, tile-owner all-to-all",
-                   "shard_layout": args.layout,
-                   "views_in_flight": inflight,
-                   "host_threads": bool(args.host_threads),
-                   "l2": ("inputs exceed L2 (shard 1.8 GB per view read); views in flight are not flushed "
-                          "between; single_view_ms / stages_ms: one view at a time, L2 flushed (256 MB write) "
-                          "before each"),
-                   "arena": "pre-grown by one untimed pass over the cameras before the warm-up views"},
-        "single_view_ms": round(single_ms, 4),
-        "splat_pairs_per_s": round(pairs_per_s, 1),
-        "per_view": {"pairs": P_all, "records_F": F_all, "received_R": R_all, "sent_D": D_all,
-                     "active": A_all, "duplication_D_over_F": (D_all / F_all if F_all else None),
-                     "E_pixel_entries": round(E_sum / args.steps, 1),
-                     "contributing_pairs": round(A_sum / args.steps, 1),
-                     "gate_keep": (float(np.mean([q["n_lod"] for q in qs])) / n_local) if gate_on and n_local else None,
-                     "owned_pairs_max_over_mean": (P_max * world / P_all) if P_all else None},
-        "scoring": {"metric": "scoring views/s (a1-a8 NO_COLOR + a10 + a12, no backward)",
-                    "value": round(1000.0 / score_ms_max, 3) if score_ms_max > 0 else None, "unit": "views/s",
-                    "ms_per_view": round(score_ms_max, 4),
-                    "note": "value: one view at a time, L2 flushed before each; in_flight: the sweep's views "
-                            "overlapped like the training batch (one ctx + stream each)",
-                    "in_flight": {"value": round(1000.0 / score_inflight_ms, 3), "unit": "views/s",
-                                  "ms_per_view": round(score_inflight_ms, 4), "views_in_flight": inflight}},
-        "simplify": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in simplify.items()},
-        "train": train,
-        "stages_ms": {n: round(float(v), 4) for n, v in zip(stage_names, stage_avg)},
-        "roofline": dict({k: dominant[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")},
-                         basis=(f"{dominant['work']} per view (SURVEY 8(d) per-unit ops x E_min); exceeds 1 when "
-                                "exact box culling skips list entries that cannot contribute; the strict "
-                                "contributing-pair basis is frac_contributing in roofline_stages"
-                                if dominant["bound"] == "alu" else f"{dominant['work']} per view (SURVEY 8(d))")),
-        "roofline_kernel": dominant["stage"],
-        "roofline_stages": roof,
-        "e2e": {"value": round(e2e_views, 3), "unit": "views/s", "h2d_bytes_per_step": int(3 * H * W * 4),
-                "d2h_bytes_per_step": int(3 * H * W * 4)},
-        "gpu_launches": int(launches),
-        "clocks": clk,
-        "scene_gen_s": round(gen_s, 2),
-    }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(scene, args)
-    if rank == 0:
-        print(json.dumps(result), flush=True)
-    ctx.close()
-    if world > 1:
-        dist.destroy_process_group()
+    inflight_ms = D.max_over_ranks(max(sev_start.elapsed_time(e) for e in sev_end), tdev) / n_views
+    return {"metric": "scoring views/s (a1-a8 NO_COLOR + a10 + a12, no backward)",
+            "value": round(1000.0 / score_ms, 3) if score_ms > 0 else None, "unit": "views/s",
+            "ms_per_view": round(score_ms, 4),
+            "note": "value: one view at a time, L2 flushed before each; in_flight: the sweep's views overlapped "
+                    "like the training batch (one ctx + stream each)",
+            "in_flight": {"value": round(1000.0 / inflight_ms, 3), "unit": "views/s",
+                          "ms_per_view": round(inflight_ms, 4), "views_in_flight": batch}}
 
 
-def train_step(args, B, S, ctxs, per, g, cams, gate, cull_cols, grads, s_imp, c_rad, c_vis, stream, l2_flush,
-               inflight, barrier, dev, H, W, n_local, world):
-    """NEXT-4: the supervised step (bgs_train_view_step) timed like the headline (views in flight,
-    device events, max over ranks), its stage breakdown (one view at a time, L2 flushed), and its
-    end-to-end rate through bgs_train_view_step_host_async (target image H2D, loss D2H)."""
+def train_iterations(args, B, S, ctxs, per, g0, cams, gate, cull_of, imp_of, stream, l2_flush, batch, barrier, D,
+                     tdev, H, W, n_local, local):
+    """NEXT-4 + NEXT-3: MEASURED training iterations on a copy of the shard.  One iteration = B
+    supervised views in flight (bgs_train_view_step: a1-a11 with Eq.7 L1+SSIM on the owned tiles
+    writing dL/dC, Eq.8 scale regulariser; + the density statistic of each view, + the batch's
+    visibility mask) -> one fused selective Adam step (bgs_adam_step) writing the activated planes
+    the next iteration renders.  Device-timed (events), max over ranks; e2e through the
+    host-buffer supervised call (target H2D, loss D2H)."""
     import torch
-    from paper_2605_13794_b200 import dist as D
-    lam, binv, beta = 0.2, 0.25, 0.01 / 4
-    tgt = torch.from_numpy(S.target_image(H, W)).to(dev)
+    dev = f"cuda:{local}"
+    lam, binv, beta = 0.2, 1.0 / batch, 0.01 / batch
+    tgts = [torch.from_numpy(S.target_image(H, W, seed=9 + k)).to(dev) for k in range(4)]
+    mo = g0.mean_opac
+    o = mo[:, 3].clamp(1e-6, 1 - 1e-6)
+    tp = B.TrainParams(torch.cat([mo[:, :3], torch.log(o / (1 - o))[:, None]], 1).contiguous(), g0.quat.clone(),
+                       torch.log(g0.scale.clamp_min(1e-30)).contiguous(), g0.sh.clone())
+    tp.log_scale[:, 3] = 0
+    g = B.GaussianPlanes(mo.clone(), g0.quat.clone(), g0.scale.clone(), tp.sh, g0.lod)  # rendered + written
+    grads = g.zeros_grads()
+    nw = (max(n_local, 1) + 31) // 32
+    vis = torch.zeros(nw, dtype=torch.int32, device=dev)
+    dc_stat = torch.zeros(max(n_local, 1), dtype=torch.float32, device=dev)
+    dc_count = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
     for p in per:
         p["dl"] = torch.zeros(3, H, W, device=dev)
         p["loss"] = torch.zeros(5, dtype=torch.float64, device=dev)
-    # NEXT-3 density statistic, accumulated by every training view (3DGS: every iteration of the
-    # densification window), phi from the importance counts the views accumulate
-    dc_stat = torch.zeros(max(n_local, 1), dtype=torch.float32, device=dev)
-    dc_count = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
+    ev_fork = torch.cuda.Event()
+    ev_join = [torch.cuda.Event() for _ in range(batch)]
+    state = {"step": 0}
 
-    def train_on(k, v):
-        p = per[k]
-        B.bgs_train_view_step(ctxs[k], g, cams[v % len(cams)], gate,
-                              cull_cols[v % len(cams)] if cull_cols is not None else None, 0, p["radius"],
-                              B.supervision(tgt, lam, binv, beta, p["loss"]), p["rgb"], p["Tf"], p["nc"], p["dl"],
-                              grads, B.importance_out(s_imp, c_rad, c_vis, p["cull"], 99, 100), p["stream"])
-        B.bgs_densify_accumulate(ctxs[k], n_local, None, dc_stat, dc_count, p["stream"])
+    def iteration(it, stages=False):
+        # fork: every view waits for the previous iteration's Adam step (stream 0)
+        ev_fork.record(stream)
+        for k in range(batch):
+            p = per[k]
+            if k:
+                p["stream"].wait_event(ev_fork)
+            v = it * batch + k
+            B.bgs_train_view_step(ctxs[k], g, cams[v % len(cams)], gate, cull_of(v), 0, p["radius"],
+                                  B.supervision(tgts[v % 4], lam, binv, beta, p["loss"]), p["rgb"], p["Tf"],
+                                  p["nc"], p["dl"], grads, None, p["stream"])
+            B.bgs_densify_accumulate(ctxs[k], n_local, None, dc_stat, dc_count, p["stream"])
+            B.bgs_visibility_mask(ctxs[k], n_local, p["radius"], vis, p["stream"])
+            ev_join[k].record(p["stream"])
+        for k in range(1, batch):
+            stream.wait_event(ev_join[k])
+        state["step"] += 1
+        with torch.cuda.stream(stream):
+            B.bgs_adam_step(ctxs[0], tp, grads, g, vis, B.adam_hparams(step=state["step"]), stream)
+            vis.zero_()
 
-    for k in range(inflight):
-        with torch.cuda.stream(per[k]["stream"]):
-            for w in range(args.warmup):
-                train_on(k, w)
+    for it in range(args.warmup):
+        iteration(it)
     torch.cuda.synchronize()
     barrier()
-    # stage breakdown: one view at a time, L2 flushed before each
-    stages = np.zeros(len(B.STAGES))
+    # stage breakdown of the supervised view (one at a time, L2 flushed): the loss stage
+    st_loss = 0.0
+    B.bgs_set_stage_timing(ctxs[0], True)
+    nst = min(max(args.steps, 8), 32)
     with torch.cuda.stream(stream):
-        B.bgs_set_stage_timing(ctxs[0], True)
-        for k in range(args.steps):
+        for k in range(nst):
             l2_flush.zero_()
             stream.synchronize()
-            train_on(0, args.warmup + k)
+            p = per[0]
+            B.bgs_train_view_step(ctxs[0], g, cams[k % len(cams)], gate, cull_of(k), 0, p["radius"],
+                                  B.supervision(tgts[k % 4], lam, binv, beta, p["loss"]), p["rgb"], p["Tf"], p["nc"],
+                                  p["dl"], grads, None, stream)
             stream.synchronize()
-            st = B.bgs_stage_times(ctxs[0])
-            stages += np.array([st[n] for n in B.STAGES])
-        B.bgs_set_stage_timing(ctxs[0], False)
+            st_loss += B.bgs_stage_times(ctxs[0])["loss"]
+    B.bgs_set_stage_timing(ctxs[0], False)
+    grads.zero_()
     torch.cuda.synchronize()
     barrier()
-    # headline-style: views in flight
-    ev_start = torch.cuda.Event(enable_timing=True)
-    ev_end = [torch.cuda.Event(enable_timing=True) for _ in range(inflight)]
-    ev_start.record(per[0]["stream"])
-    for k in range(1, inflight):
-        per[k]["stream"].wait_event(ev_start)
-    submit_views(train_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads),
-                 int(str(dev).split(":")[-1]))
-    for k in range(inflight):
-        ev_end[k].record(per[k]["stream"])
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    losses = []
+    ev0.record(stream)
+    for it in range(args.steps):
+        iteration(args.warmup + it)
+    ev1.record(stream)
     torch.cuda.synchronize()
-    ms = D.max_over_ranks(max(ev_start.elapsed_time(e) for e in ev_end), torch.device(dev)) / args.steps
-    loss = per[0]["loss"].cpu().tolist()
+    ms = D.max_over_ranks(ev0.elapsed_time(ev1), tdev) / args.steps
+    losses = [float(p["loss"][0].item()) for p in per]
     barrier()
-    # end to end: every view's target uploaded from pinned memory, its loss read back
-    tgt_h = [torch.from_numpy(S.target_image(H, W, seed=9 + k)).pin_memory() for k in range(inflight)]
-    loss_h = [torch.zeros(5, dtype=torch.float64).pin_memory() for _ in range(inflight)]
+    # end to end: each view's target uploaded from pinned memory, its loss read back
+    tgt_h = [torch.from_numpy(S.target_image(H, W, seed=9 + k)).pin_memory() for k in range(batch)]
+    loss_h = [torch.zeros(5, dtype=torch.float64).pin_memory() for _ in range(batch)]
 
-    def host_on(k, v):
-        p = per[k]
-        B.bgs_train_view_step_host_async(ctxs[k], g, cams[v % len(cams)], gate,
-                                         cull_cols[v % len(cams)] if cull_cols is not None else None, 0,
-                                         p["radius"], tgt_h[k], lam, binv, beta, loss_h[k], grads,
-                                         B.importance_out(s_imp, c_rad, c_vis, p["cull"], 99, 100), p["stream"])
+    def host_iteration(it):
+        ev_fork.record(stream)
+        for k in range(batch):
+            p = per[k]
+            if k:
+                p["stream"].wait_event(ev_fork)
+            v = it * batch + k
+            B.bgs_train_view_step_host_async(ctxs[k], g, cams[v % len(cams)], gate, cull_of(v), 0, p["radius"],
+                                             tgt_h[k], lam, binv, beta, loss_h[k], grads, None, p["stream"])
+            B.bgs_visibility_mask(ctxs[k], n_local, p["radius"], vis, p["stream"])
+            ev_join[k].record(p["stream"])
+        for k in range(1, batch):
+            stream.wait_event(ev_join[k])
+        state["step"] += 1
+        with torch.cuda.stream(stream):
+            B.bgs_adam_step(ctxs[0], tp, grads, g, vis, B.adam_hparams(step=state["step"]), stream)
+            vis.zero_()
 
-    for k in range(inflight):
-        host_on(k, k)
+    host_iteration(0)
     torch.cuda.synchronize()
     barrier()
     t1 = time.perf_counter()
-    submit_views(host_on, inflight, [args.warmup + k for k in range(args.steps)], bool(args.host_threads),
-                 int(str(dev).split(":")[-1]))
+    for it in range(args.steps):
+        host_iteration(1 + it)
     torch.cuda.synchronize()
-    e2e = args.steps / D.max_over_ranks(time.perf_counter() - t1, torch.device(dev))
-    # NEXT-3: the optimizer step of the batch (bgs_adam_step) on this rank's shard, dense (every row)
-    # and selective (rows some view of the batch projected: the union of the records' c_rad bits)
-    adam = adam_step_timing(B, S, g, grads, ctxs[0], stream, dev, n_local, l2_flush, cams, gate, cull_cols, per,
-                            s_imp, c_rad, c_vis, args, dc_stat, dc_count)
-    return {"metric": "supervised training views/s (a1-a12 + Eq.7 L1+SSIM on owned tiles + Eq.8, NEXT-4)",
-            "value": round(1000.0 / ms, 3), "unit": "views/s", "ms_per_view": round(ms, 4),
-            "lambda": lam, "batch_inv": binv, "beta": beta,
-            "stages_ms": {n: round(float(v) / args.steps, 4) for n, v in zip(B.STAGES, stages)},
-            "stages_avg": stages / args.steps,
-            "loss_last_view": {"l": loss[0], "L1": loss[1], "SSIM": loss[2], "L_scale": loss[3], "V": loss[4]},
-            "e2e": {"value": round(e2e, 3), "unit": "views/s", "h2d_bytes_per_step": int(3 * H * W * 4),
-                    "d2h_bytes_per_step": 40},
-            "adam": adam,
-            "batch_of_4_views_per_s": {
-                "dense_adam": round(4000.0 / (4 * ms + adam["dense_ms"]), 3),
-                "selective_adam": round(4000.0 / (4 * ms + adam["selective_ms"]), 3)}}
+    e2e_it = args.steps / D.max_over_ranks(time.perf_counter() - t1, tdev)
+    adam = adam_step_timing(B, g, grads, tp, ctxs[0], stream, n_local, l2_flush, per, args, D, tdev, batch)
+    dens = densify_timing(B, ctxs[0], tp, g, dc_stat, dc_count, stream, n_local, D, tdev)
+    out = {"metric": "training iterations/s (B views: a1-a11 + Eq.7 L1+SSIM + Eq.8 + density statistic, then one "
+                     "selective Adam step; NEXT-4 + NEXT-3)",
+           "value": round(1000.0 / ms, 3), "unit": "it/s", "ms_per_iteration": round(ms, 4),
+           "views_per_s": round(1000.0 * batch / ms, 3), "views_per_iteration": batch,
+           "lambda": lam, "batch_inv": binv, "beta": beta, "loss_last_batch": losses,
+           "loss_stage_ms": round(st_loss / nst, 4),
+           "e2e": {"value": round(e2e_it, 3), "unit": "it/s", "h2d_bytes_per_step": int(batch * 3 * H * W * 4),
+                   "d2h_bytes_per_step": int(batch * 40)},
+           "adam": adam, "densify": dens}
+    del tp, g, grads
+    return out
 
 
-def adam_step_timing(B, S, g, grads, ctx, stream, dev, n_local, l2_flush, cams, gate, cull_cols, per, s_imp, c_rad,
-                     c_vis, args, dc_stat, dc_count):
-    """bgs_adam_step on the shard: raw planes derived from the activated ones, device-timed (L2
-    flushed before each), dense and with the visibility mask of a 4-view batch."""
+def adam_step_timing(B, g, grads, tp, ctx, stream, n_local, l2_flush, per, args, D, tdev, batch):
+    """bgs_adam_step on the shard, device-timed (L2 flushed before each), dense and with the
+    visibility mask of a batch of views."""
     import torch
-    from paper_2605_13794_b200 import dist as D
-    mo = g.mean_opac
-    o = mo[:, 3].clamp(1e-6, 1 - 1e-6)
-    ml = torch.cat([mo[:, :3], torch.log(o / (1 - o))[:, None]], 1).contiguous()
-    tp = B.TrainParams(ml, g.quat.clone(), torch.log(g.scale.clamp_min(1e-30)).contiguous(), g.sh.clone())
-    tp.log_scale[:, 3] = 0
-    act = B.GaussianPlanes(torch.empty_like(mo), torch.empty_like(g.quat), torch.empty_like(g.scale), tp.sh, g.lod)
-    # the batch's visible rows: radius > 0 in any of 4 views (from the in-flight contexts' last views)
-    vis = torch.zeros(max(n_local, 1), dtype=torch.bool, device=dev)
-    for p in per[:4]:
-        vis |= p["radius"][:max(n_local, 1)] > 0
-    bits = vis.view(-1)
-    pad = (-bits.numel()) % 32
-    words = torch.nn.functional.pad(bits.to(torch.int64), (0, pad)).view(-1, 32)
-    mask = (words << torch.arange(32, device=dev, dtype=torch.int64)).sum(1).to(torch.int64)
-    mask = torch.where(mask >= 2 ** 31, mask - 2 ** 32, mask).to(torch.int32).contiguous()
+    dev = g.mean_opac.device
+    nw = (max(n_local, 1) + 31) // 32
+    mask = torch.zeros(nw, dtype=torch.int32, device=dev)
+    for p in per[:batch]:
+        B.bgs_visibility_mask(ctx, n_local, p["radius"], mask, stream)
+    torch.cuda.synchronize()
+    rows = float(sum(bin(int(x) & 0xffffffff).count("1") for x in mask.cpu().numpy().tolist()))
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     out = {}
     with torch.cuda.stream(stream):
@@ -682,27 +686,32 @@ def adam_step_timing(B, S, g, grads, ctx, stream, dev, n_local, l2_flush, cams, 
                 l2_flush.zero_()
                 stream.synchronize()
                 ev[0].record(stream)
-                B.bgs_adam_step(ctx, tp, grads, act, m, B.adam_hparams(step=k + 1), stream)
+                B.bgs_adam_step(ctx, tp, grads, g, m, B.adam_hparams(step=k + 1), stream)
                 ev[1].record(stream)
                 stream.synchronize()
                 if k >= args.warmup:
                     tot += ev[0].elapsed_time(ev[1])
-            out[f"{name}_ms"] = round(D.max_over_ranks(tot / args.steps, torch.device(dev)), 4)
-    rows = float(vis[:n_local].sum().item())
+            out[f"{name}_ms"] = round(D.max_over_ranks(tot / args.steps, tdev), 4)
     # algorithmic bytes per updated row: read raw 240 + grads 240 + m 240 + v 240; write raw 240 +
     # m 240 + v 240 + activated 48 (SH aliases the raw plane) + zeroed grads 240
     per_row = 4 * 240 + 4 * 240 + 48
-    peaks_gbs = load_peaks()["hbm_gbs"]
+    peaks = load_peaks()
     for name, nrows in (("dense", float(n_local)), ("selective", rows)):
         ach = per_row * nrows / (out[f"{name}_ms"] * 1e-3) / 1e9 if out[f"{name}_ms"] > 0 else 0.0
-        out[f"{name}_roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks_gbs, "unit": "GB/s",
-                                   "frac": round(ach / peaks_gbs, 4), "rows": int(nrows),
+        out[f"{name}_roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"],
+                                   "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4), "rows": int(nrows),
                                    "work": f"{per_row} B x rows"}
-    out["note"] = ("one optimizer step per batch of B = 4 views (P:342); selective = rows projected by any view "
-                   "of the batch (visibility mask), dense = every row of the shard")
-    # NEXT-3 density control on the shard with the statistic of the timed training views (tau chosen
-    # as the 99th percentile of the per-Gaussian average so that ~1% densify; 3DGS's 2e-4 is scale-
-    # dependent), extent 1% of the scene (1000 units): wall time of the HOST-SYNC call
+    out["note"] = ("one optimizer step per batch of B views (P:342); selective = rows projected by any view of the "
+                   "batch (bgs_visibility_mask), dense = every row of the shard")
+    return out
+
+
+def densify_timing(B, ctx, tp, g, dc_stat, dc_count, stream, n_local, D, tdev):
+    """NEXT-3 density control on the shard with the statistic of the timed training views (tau =
+    the 99th percentile of the per-Gaussian average so that ~1% densify; 3DGS's 2e-4 is scale-
+    dependent), extent 10 units (1% of the 1000-unit scene): wall time of the HOST-SYNC call."""
+    import torch
+    dev = g.mean_opac.device
     with torch.cuda.stream(stream):
         avg = (dc_stat[:n_local] / dc_count[:n_local].clamp_min(1).float())
         tau = float(torch.quantile(avg[avg > 0][:1 << 24].float(), 0.99).item()) if bool((avg > 0).any()) else 1.0
@@ -718,18 +727,53 @@ def adam_step_timing(B, S, g, grads, ctx, stream, dev, n_local, l2_flush, cams, 
         n_new = B.bgs_densify_apply(ctx, tp, g.lod, dc_stat, dc_count, dp, tout, lod_out, act2, stream)
         stream.synchronize()
         ms = (time.perf_counter() - t1) * 1e3
-        # algorithmic bytes: read every input row (raw 240 + m, v 480 + lod 1 + stat, count 8), write
-        # every output row (raw + m + v 720 + activated 48 + lod 1)
-        byt = n_local * (240 + 480 + 1 + 8) + n_new * (720 + 48 + 1)
-        out["densify"] = {"apply_ms": round(D.max_over_ranks(ms, torch.device(dev)), 4), "rows_in": int(n_local),
-                          "rows_out": int(n_new), "tau": tau, "dense_extent": 10.0,
-                          "roofline": {"bound": "hbm", "achieved": round(byt / (ms * 1e-3) / 1e9, 1),
-                                       "peak": peaks_gbs, "unit": "GB/s",
-                                       "frac": round(byt / (ms * 1e-3) / 1e9 / peaks_gbs, 4)},
-                          "note": "statistic accumulated by every timed training view (bgs_densify_accumulate); "
-                                  "apply is HOST-SYNC, wall time incl. the count round trip"}
-        del tout, act2
-    del tp, act
+    # algorithmic bytes: read every input row (raw 240 + m, v 480 + lod 1 + stat, count 8), write
+    # every output row (raw + m + v 720 + activated 48 + lod 1)
+    byt = n_local * (240 + 480 + 1 + 8) + n_new * (720 + 48 + 1)
+    hbm = load_peaks()["hbm_gbs"]
+    del tout, act2
+    return {"apply_ms": round(D.max_over_ranks(ms, tdev), 4), "rows_in": int(n_local), "rows_out": int(n_new),
+            "tau": tau, "dense_extent": 10.0,
+            "roofline": {"bound": "hbm", "achieved": round(byt / (ms * 1e-3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(byt / (ms * 1e-3) / 1e9 / hbm, 4)},
+            "note": "statistic accumulated by every timed training view (bgs_densify_accumulate); apply is "
+                    "HOST-SYNC, wall time incl. the count round trip"}
+
+
+def simplify(args, B, ctx, g, s_imp, c_rad, c_vis, stream, barrier, D, tdev, n_local, N_all):
+    """NEXT-1 scheduled simplification on the shard with the s / c_rad / c_vis the timed views
+    accumulated (one pass each; HOST-SYNC calls, wall time between barriers)."""
+    import torch
+    out = {}
+    dev = g.mean_opac.device
+    with torch.cuda.stream(stream):
+        phi = torch.empty(max(n_local, 1), dtype=torch.float64, device=dev)
+        keep = torch.empty(max(n_local, 1), dtype=torch.uint8, device=dev)
+        cap = n_local + 1
+        out_g = B.GaussianPlanes(torch.empty(cap, 4, device=dev), torch.empty(cap, 4, device=dev),
+                                 torch.empty(cap, 4, device=dev), torch.empty(cap, 48, device=dev),
+                                 torch.empty(cap, dtype=torch.uint8, device=dev))
+        N_glob = int(N_all)
+
+        def timed(fn):
+            fn()  # warm-up: first calls grow the ctx arena (cudaMalloc)
+            stream.synchronize()
+            barrier()
+            t1 = time.perf_counter()
+            r = fn()
+            stream.synchronize()
+            return r, round(D.max_over_ranks((time.perf_counter() - t1) * 1e3, tdev), 3)
+
+        _, out["phi_ms"] = timed(lambda: B.bgs_score_phi(ctx, n_local, c_rad, c_vis, phi, stream))
+        _, out["pass1_stochastic_ms"] = timed(
+            lambda: B.bgs_prune_stochastic(ctx, n_local, s_imp, int(round(0.6 * N_glob)), 1234, keep, stream))
+        n_keep1 = D.sum_over_ranks([float(keep[:n_local].sum().item())], tdev)[0]
+        _, out["pass2_mass_cut_ms"] = timed(lambda: B.bgs_prune_mass_cut(ctx, n_local, s_imp, 99, 100, keep, stream))
+        n_keep2 = D.sum_over_ranks([float(keep[:n_local].sum().item())], tdev)[0]
+        _, out["redistribute_ms"] = timed(lambda: B.bgs_redistribute(ctx, g, keep, out_g, stream))
+        out.update({"gaussians": N_glob, "kept_pass1": int(n_keep1), "kept_pass2": int(n_keep2),
+                    "note": "keep_fraction 0.6 (S:318 default), target 99/100; scores from the timed views"})
+        del out_g
     return out
 
 
@@ -737,67 +781,110 @@ def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured", "sm_max_mhz": d.get("sm_max_mhz", 1965.0)}
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "source": "measured (MEASURED_PEAKS.json)",
+                "sm_max_mhz": d.get("sm_max_mhz", 1965.0)}
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
 
 
 # ------------------------------------------------------------------------------------------
 # oracle baselines (the one other place bench.py executes oracle/)
 # ------------------------------------------------------------------------------------------
-def oracle_sample(scene, views, frac_tiles: float):
-    """The oracle's time per view on this workload: full projection + routing + sort of every
-    view, compositing fwd+bwd on a `frac_tiles` sample of the tiles, scaled to a whole view."""
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def oracle_view(scene, v, threads: int, frac_tiles: float = 1.0):
+    """One fwd+bwd view of the workload through the oracle (a1-a11: projection, ownership, routing,
+    sort, compositing fwd+bwd, projection backward), compositing on a `frac_tiles` sample."""
     import oracle as O
     import synthetic as S
-    cam = scene.cameras[views % len(scene.cameras)]
+    cam = scene.cameras[v % len(scene.cameras)]
     dl = S.grad_image(cam["H"], cam["W"])
-    st = O.OracleStep(scene, cam, M=1, dLdC=dl, tile_frac=frac_tiles)
-    return st.seconds, st.seconds_by_phase()
+    t0 = time.perf_counter()
+    st = O.OracleStep(scene, cam, M=1, dLdC=dl, tile_frac=frac_tiles, threads=threads)
+    secs = time.perf_counter() - t0
+    return secs, st.seconds_by_phase(), st.threads
 
 
-def cpu_baseline(scene, args):
+def cpu_baseline(scene, args, cams_idx=0):
+    """The oracle as it stands, on this host's cores: (i) all cores on one FULL view of the
+    workload, (ii) one thread on a 1/8 tile sample of another view, composite scaled x8."""
     import oracle as O
+    cores = host_cores()
+    secs, phases, used = oracle_view(scene, cams_idx, cores)
     frac = 1.0 / 8
-    secs, phases = oracle_sample(scene, args.warmup, frac)
-    comp = phases["composite"] / frac
-    per_view = phases["project"] + phases["route_sort"] + comp + phases["project_bwd"]
-    return {"value": round(1.0 / per_view, 5), "unit": "views/s", "cores": 1, "kind": "oracle",
-            "sample": f"one view of the same workload: oracle projection, ownership, routing and sort of all "
-                      f"{scene.n} Gaussians, compositing fwd+bwd of a {frac:.3f} sample of the tiles scaled "
-                      f"x{1 / frac:.0f} ({secs:.1f} s of CPU work, 1 thread)",
-            "phases_s": {k: round(v, 3) for k, v in phases.items()}, "oracle_lib": os.path.basename(O.build())}
+    s1, ph1, _ = oracle_view(scene, cams_idx + 1, 1, frac)
+    per_view_1 = ph1["project"] + ph1["route_sort"] + ph1["composite"] / frac + ph1["project_bwd"]
+    return {"value": round(1.0 / secs, 5), "unit": "views/s", "cores": used, "kind": "oracle",
+            "sample": f"one full view (a1-a11, all {scene.n} Gaussians, every tile) of the same workload on "
+                      f"{used} host threads ({secs:.1f} s)",
+            "nproc": cores, "cpu_model": cpu_model(),
+            "phases_s": {k: round(v, 3) for k, v in phases.items()},
+            "single_thread": {"value": round(1.0 / per_view_1, 5), "unit": "views/s", "cores": 1,
+                              "sample": f"one view, compositing fwd+bwd of a {frac:.3f} tile sample scaled "
+                                        f"x{1 / frac:.0f} ({s1:.1f} s)",
+                              "phases_s": {k: round(v, 3) for k, v in ph1.items()}},
+            "oracle_lib": os.path.basename(O.build())}
 
 
 def run_reference(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """The base contract's reference arm for this tier: the CPU oracle, as it stands, on the box's
+    host cores, on the native arm's workload.  Each timed step = one batch of B FULL views (a1-a11
+    of every view, all tiles); warm-up steps composite a 1/64 tile sample of one view."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     import synthetic as S
-    label, gate_on = CONFIG_SHAPES[args.config]
+    label, gate_default = CONFIG_SHAPES[args.config]
+    gate_on = gate_default if args.gate == "config" else args.gate == "on"
+    mask_on = gate_on if args.mask == "config" else (args.mask == "on" and gate_on)
+    if gate_on:
+        print(json.dumps({"impl": "reference", "unavailable": "the oracle reference arm covers the ungated "
+                                                              "configs only (rubble, residence, matrixcity)"}))
+        return
+    batch = 1  # one view per reference step (the CPU has no views in flight)
+    t0 = time.perf_counter()
     scene = S.gen_city(args.config, n=args.n, V=args.views)
-    frac = 1.0 / 16
+    gen_s = time.perf_counter() - t0
+    cores = host_cores()
     for w in range(args.warmup):
-        oracle_sample(scene, w, frac)
+        oracle_view(scene, w, cores, 1.0 / 64)
     tot = 0.0
     phase_tot = {}
+    used = cores
     for k in range(args.steps):
-        secs, ph = oracle_sample(scene, args.warmup + k, frac)
-        per_view = ph["project"] + ph["route_sort"] + ph["composite"] / frac + ph["project_bwd"]
-        tot += per_view
+        secs, ph, used = oracle_view(scene, args.warmup + k, cores)
+        tot += secs
         for kk, v in ph.items():
             phase_tot[kk] = phase_tot.get(kk, 0.0) + v
-    v = args.steps / tot
+    v = args.steps * batch / tot
     W, H = scene.cameras[0]["W"], scene.cameras[0]["H"]
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "views/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * tot / args.steps, 2),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-           "config": {"workload": label, "config": args.config, "gaussians": scene.n, "width": W, "height": H},
-           "cpu_baseline": {"value": round(v, 6), "unit": "views/s", "cores": 1, "kind": "oracle",
-                            "sample": f"per step: oracle projection/ownership/sort of all {scene.n} Gaussians of "
-                                      f"one view + fwd+bwd compositing of a {frac:.4f} tile sample scaled "
-                                      f"x{1 / frac:.0f}"},
-           "e2e": {"value": round(v, 6), "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "config": config_dict(args, label, gate_on, mask_on, scene.n, W, H, world, batch),
+           "views_per_step": batch,
+           "cpu_baseline": {"value": round(v, 6), "unit": "views/s", "cores": used, "kind": "oracle",
+                            "nproc": cores, "cpu_model": cpu_model(),
+                            "sample": f"each step one FULL view (a1-a11 of all {scene.n} Gaussians, every tile) on "
+                                      f"{used} host threads; warm-up steps on 1/64 tile samples",
+                            "phases_s_per_view": {kk: round(x / args.steps, 3) for kk, x in phase_tot.items()}},
+           "e2e": {"value": round(v, 6), "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "scene_gen_s": round(gen_s, 2)}
     print(json.dumps(out), flush=True)
 
 

@@ -132,6 +132,9 @@ bgs_status bgs_ctx_destroy(bgs_ctx* ctx);
 const char* bgs_last_error(const bgs_ctx* ctx);
 /* Kernels this ctx has launched since creation (the bench's gpu_launches evidence). */
 int64_t bgs_launch_count(const bgs_ctx* ctx);
+/* Times a call on this ctx blocked the host on the device (stream / event synchronisations inside
+ * HOST-SYNC calls) since creation (the bench's host_syncs_per_view evidence). */
+int64_t bgs_host_sync_count(const bgs_ctx* ctx);
 
 /* Per-view counters (valid after the producing stage; host-visible after a HOST-SYNC call):
  *   0 N_local  1 n_lod (|L^(m)|)  2 n_active (|A^(m)|)  3 F (in-frustum records)  4 D (records
@@ -417,6 +420,12 @@ typedef struct {
 bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaussian_grads* grads,
                          const bgs_gaussians_out* act, const uint32_t* visible, const bgs_adam_hparams* h,
                          void* stream);
+
+/* Selective-Adam visibility mask of a batch (3DGS "visibility filter"; P:342 B views per step):
+ * mask[i/32] |= bit (i%32) for every local Gaussian with radius[i] > 0 (bgs_project's radius_out of
+ * one view of the batch).  radius: device i32 [n_local]; mask: device u32 [ceil(n_local/32)],
+ * caller-zeroed once per batch, ORed with atomics (views in flight may share it). */
+bgs_status bgs_visibility_mask(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, uint32_t* mask, void* stream);
 
 /* Density-control statistic of one view (R37): after bgs_route_reverse of the view on
  * this ctx, for every local Gaussian the view projected (radius > 0):

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "bgs_oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+CXXFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC"]
 
 
 def build(force: bool = False) -> str:
@@ -55,6 +55,8 @@ def lib():
         _lib.or_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                 C.c_int32]
         _lib.or_free.argtypes = [C.c_void_p]
+        _lib.or_set_threads.restype = C.c_int32
+        _lib.or_set_threads.argtypes = [C.c_int32]
         _lib.or_get.restype = C.c_int64
         _lib.or_get.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_void_p]
         _lib.or_d2_threshold.restype = C.c_float
@@ -68,6 +70,13 @@ def lib():
         _lib.or_importance.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     return _lib
+
+
+def set_threads(n: int) -> int:
+    """Host threads of the oracle's per-Gaussian and per-tile loops (1 = sequential).  Results are
+    bit-identical for every count (bgs_oracle.cpp: tile increments replayed in tile order).
+    Returns the count in effect."""
+    return int(lib().or_set_threads(int(n)))
 
 
 def _ptr(a):
@@ -104,7 +113,8 @@ class OracleStep:
     """One simulated view step at M ranks (O1..O11 of DESIGN.md §5)."""
 
     def __init__(self, scene, cam: dict, gate: dict | None = None, cull_global: np.ndarray | None = None,
-                 M: int = 1, flags: int = 0, dLdC: np.ndarray | None = None, tile_frac: float = 1.0):
+                 M: int = 1, flags: int = 0, dLdC: np.ndarray | None = None, tile_frac: float = 1.0,
+                 threads: int = 1):
         L = lib()
         self._keep = []
         n = scene.n
@@ -123,9 +133,13 @@ class OracleStep:
         self.M = M
         self.n = n
         self.cam = cam
+        self.threads = set_threads(threads)
         t0 = time.perf_counter()
         stride = max(1, int(round(1.0 / tile_frac)))
-        self._h = L.or_step(C.byref(sc), C.byref(cm), C.byref(gt), _ptr(cull), M, flags, _ptr(dl), stride)
+        try:
+            self._h = L.or_step(C.byref(sc), C.byref(cm), C.byref(gt), _ptr(cull), M, flags, _ptr(dl), stride)
+        finally:
+            set_threads(1)
         self.seconds = time.perf_counter() - t0
 
     def get(self, name: str, rank: int = 0) -> np.ndarray:

@@ -30,7 +30,18 @@
 #include <string>
 #include <vector>
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 namespace {
+
+// Host threads for the per-Gaussian loops (O3, O11) and the per-tile compositing (O8/O9); 1 =
+// the plain sequential oracle.  Every thread count gives bit-identical results: the parallel
+// loops write per-index outputs only, and each tile's w / a / gradient increments are buffered
+// and applied in tile order, i.e. in exactly the sequential order (or_set_threads; bench.py's
+// multi-core baseline).
+int g_threads = 1;
 
 // ---------------------------------------------------------------------------------------
 // Inputs (oracle-private mirrors of what the Python side passes; NOT the ABI structs)
@@ -323,9 +334,19 @@ struct Contrib {
   bool clamped;
 };
 
+// Increments one tile makes to per-Gaussian accumulators, in the order the sequential loop
+// makes them (replayed by apply_tile).
+struct TileOut {
+  struct Fwd { int64_t gid; double wgt; uint64_t wfix; };
+  struct Bwd { int64_t gid; double g[9]; bool clamped; };
+  std::vector<Fwd> fwd;
+  std::vector<Bwd> bwd;
+  double margin_thr = 1e30, margin_clamp = 1e30;
+};
+
 template <class T>
-void composite_tile_pixels(Step<T>& st, const std::vector<int64_t>& list, int tile, const float* dLdC,
-                           std::vector<double>* g2d_owner) {
+void composite_tile_pixels(Step<T>& st, const std::vector<int64_t>& list, int tile, const float* dLdC, bool backward,
+                           TileOut& out) {
   int tx = tile % st.TX, ty = tile / st.TX;
   for (int ly = 0; ly < TILE; ++ly)
     for (int lx = 0; lx < TILE; ++lx) {
@@ -342,11 +363,11 @@ void composite_tile_pixels(Step<T>& st, const std::vector<int64_t>& list, int ti
         T dx = p.mx - T(px), dy = p.my - T(py);
         T power = -neg_power<T>(p.A, p.B, p.C, dx, dy);
         if (power > T(0)) continue;
-        st.margin_thr = std::min(st.margin_thr, std::fabs(double(power) - double(p.thr)));
+        out.margin_thr = std::min(out.margin_thr, std::fabs(double(power) - double(p.thr)));
         if (power < p.thr) continue;  // alpha < 1/255 (R9, D3)
         T G = exp_t<T>(power);
         T og = p.opac * G;
-        st.margin_clamp = std::min(st.margin_clamp, std::fabs(double(og) - 0.99));
+        out.margin_clamp = std::min(out.margin_clamp, std::fabs(double(og) - 0.99));
         bool clamped = og > k<T>(0.99);
         T alpha = tmin(k<T>(0.99), og);
         T test_T = Tr * (k<T>(1.0) - alpha);
@@ -355,9 +376,8 @@ void composite_tile_pixels(Step<T>& st, const std::vector<int64_t>& list, int ti
         T wgt = alpha * Tr;
         for (int ch = 0; ch < 3; ++ch) Cc[ch] = Cc[ch] + p.rgb[ch] * wgt;  // Eq.2
         int64_t g = list[kk];
-        st.w[g] += double(wgt);
-        st.w_fixed[g] += static_cast<uint64_t>(std::rint(double(wgt) * 16777216.0));
-        st.a[g] += 1;
+        // w += alpha T (fp64), w_fixed += rint(alpha T 2^24), a += 1 (R15, R29)
+        out.fwd.push_back({g, double(wgt), static_cast<uint64_t>(std::rint(double(wgt) * 16777216.0))});
         cl.push_back({g, double(alpha), double(G), double(Tr), clamped});
         Tr = test_T;
         last = int(kk) + 1;
@@ -370,7 +390,7 @@ void composite_tile_pixels(Step<T>& st, const std::vector<int64_t>& list, int ti
       st.t_final[pix] = float(Tr);
       st.n_contrib[pix] = last;
       st.et_margin[pix] = float(std::min(margin, 1e30));
-      if (!dLdC || !g2d_owner) continue;
+      if (!dLdC || !backward) continue;
       // backward of Eq.2 ("gradients propagate through both the rasterizer ..."), fp64
       double dL[3] = {dLdC[0 * size_t(st.W) * st.H + pix], dLdC[1 * size_t(st.W) * st.H + pix],
                       dLdC[2 * size_t(st.W) * st.H + pix]};
@@ -378,27 +398,51 @@ void composite_tile_pixels(Step<T>& st, const std::vector<int64_t>& list, int ti
       for (size_t j = cl.size(); j-- > 0;) {
         const Contrib& c = cl[j];
         const Proj<T>& p = st.proj[c.gid];
-        double* g = &(*g2d_owner)[9 * c.gid];
+        TileOut::Bwd b{c.gid, {0, 0, 0, 0, 0, 0, 0, 0, 0}, c.clamped};
+        double* g = b.g;
         double dLda = 0;
         for (int ch = 0; ch < 3; ++ch) {
-          g[6 + ch] += c.alpha * c.T * dL[ch];
+          g[6 + ch] = c.alpha * c.T * dL[ch];
           dLda += (double(p.rgb[ch]) - acc[ch]) * dL[ch];
         }
         dLda *= c.T;
         for (int ch = 0; ch < 3; ++ch) acc[ch] = c.alpha * double(p.rgb[ch]) + (1.0 - c.alpha) * acc[ch];
-        if (c.clamped) continue;  // alpha = 0.99 constant: true derivative is zero (R14)
-        double o = double(p.opac);
-        g[5] += c.G * dLda;
-        double dLdpow = c.G * o * dLda;
-        double dx = double(p.mx) - px, dy = double(p.my) - py;
-        double A = double(p.A), B = double(p.B), C = double(p.C);
-        g[0] += dLdpow * (-(A * dx + B * dy));
-        g[1] += dLdpow * (-(C * dy + B * dx));
-        g[2] += dLdpow * (-0.5 * dx * dx);
-        g[3] += dLdpow * (-dx * dy);
-        g[4] += dLdpow * (-0.5 * dy * dy);
+        if (!c.clamped) {  // alpha = 0.99 constant: true derivative is zero (R14)
+          double o = double(p.opac);
+          g[5] = c.G * dLda;
+          double dLdpow = c.G * o * dLda;
+          double dx = double(p.mx) - px, dy = double(p.my) - py;
+          double A = double(p.A), B = double(p.B), C = double(p.C);
+          g[0] = dLdpow * (-(A * dx + B * dy));
+          g[1] = dLdpow * (-(C * dy + B * dx));
+          g[2] = dLdpow * (-0.5 * dx * dx);
+          g[3] = dLdpow * (-dx * dy);
+          g[4] = dLdpow * (-0.5 * dy * dy);
+        }
+        out.bwd.push_back(b);
       }
     }
+}
+
+// The tile's increments, in the sequential loop's order (per pixel: forward terms front to
+// back, then the backward terms back to front; a clamped contributor adds its colour terms only).
+template <class T>
+void apply_tile(Step<T>& st, const TileOut& out, std::vector<double>* g2d_owner) {
+  st.margin_thr = std::min(st.margin_thr, out.margin_thr);
+  st.margin_clamp = std::min(st.margin_clamp, out.margin_clamp);
+  for (const auto& f : out.fwd) {
+    st.w[f.gid] += f.wgt;
+    st.w_fixed[f.gid] += f.wfix;
+    st.a[f.gid] += 1;
+  }
+  if (!g2d_owner) return;
+  for (const auto& b : out.bwd) {
+    double* g = &(*g2d_owner)[9 * b.gid];
+    for (int ch = 0; ch < 3; ++ch) g[6 + ch] += b.g[6 + ch];
+    if (b.clamped) continue;
+    g[5] += b.g[5];
+    for (int k = 0; k < 5; ++k) g[k] += b.g[k];
+  }
 }
 
 // Backward of the projection (a11) in fp64, recomputing from the parameters.
@@ -610,6 +654,7 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
     st->n_keep[m] += st->keep[i];
   }
   // O3 project every kept Gaussian ("every GPU projects only its own local Gaussians")
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads) if (g_threads > 1)
   for (int64_t i = 0; i < n; ++i) {
     if (!st->keep[i]) continue;
     st->proj[i] = project_one<T>(s, i, cam, no_color);
@@ -708,12 +753,26 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
   for (int m = 0; m < M; ++m) {
     OwnerState& os = st->owners[m];
     if (dLdC) g_owner.assign(size_t(9) * n, 0.0);
+    std::vector<int> tiles;
     for (int t = os.t_begin; t < os.t_end; ++t) {
       if (tile_stride > 1 && t % tile_stride != 0) continue;  // timing samples only (bench.py)
-      int lt = t - os.t_begin;
-      std::vector<int64_t> list;
-      for (int64_t q = os.range_lo[lt]; q < os.range_hi[lt]; ++q) list.push_back(os.pairs[q].second);
-      composite_tile_pixels<T>(*st, list, t, dLdC, dLdC ? &g_owner : nullptr);
+      tiles.push_back(t);
+    }
+    // blocks of tiles: composited independently (threads), then applied in tile order
+    const size_t blk = g_threads > 1 ? size_t(64) * size_t(g_threads) : 1;
+    std::vector<TileOut> outs;
+    for (size_t b0 = 0; b0 < tiles.size(); b0 += blk) {
+      const size_t nb = std::min(blk, tiles.size() - b0);
+      outs.assign(nb, TileOut());
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads) if (g_threads > 1)
+      for (long long q = 0; q < (long long)nb; ++q) {
+        const int t = tiles[b0 + size_t(q)];
+        const int lt = t - os.t_begin;
+        std::vector<int64_t> list;
+        for (int64_t e = os.range_lo[lt]; e < os.range_hi[lt]; ++e) list.push_back(os.pairs[e].second);
+        composite_tile_pixels<T>(*st, list, t, dLdC, dLdC != nullptr, outs[size_t(q)]);
+      }
+      for (size_t q = 0; q < nb; ++q) apply_tile<T>(*st, outs[q], dLdC ? &g_owner : nullptr);
     }
     // O10 reverse route: owner partials summed at the source in owner-ascending order
     if (dLdC)
@@ -728,6 +787,7 @@ Step<T>* run_step(const Scene& s, const Camera& cam, const Gate& gate, const uin
     st->d_scale.assign(3 * n, 0.0);
     st->d_opac.assign(n, 0.0);
     st->d_sh.assign(48 * n, 0.0);
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads) if (g_threads > 1)
     for (int64_t i = 0; i < n; ++i) {
       if (!st->proj[i].valid) continue;
       project_bwd_one(s, i, cam, &st->g2d[9 * i], st->proj[i].clamped, &st->d_mean[3 * i], &st->d_quat[4 * i],
@@ -863,6 +923,18 @@ void* or_step(const or_scene* sc, const or_camera* cm, const or_gate* gt, const 
 }
 
 void or_free(void* h) { delete static_cast<Handle*>(h); }
+
+// Host threads for or_step (1 = sequential; results are bit-identical for every count).
+// Returns the count in effect (1 when built without OpenMP).
+int32_t or_set_threads(int32_t n) {
+#ifdef _OPENMP
+  g_threads = n < 1 ? 1 : n;
+#else
+  (void)n;
+  g_threads = 1;
+#endif
+  return g_threads;
+}
 
 // Returns the element count of `name` (for rank-specific fields, of owner `rank`), and
 // copies the data into `out` when non-null.  -1 for unknown names.

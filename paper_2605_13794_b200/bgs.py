@@ -102,6 +102,7 @@ _SIGS = {
     "bgs_train_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_adam_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_densify_accumulate": [_vp, C.c_int64, _vp, _vp, _vp, _vp],
+    "bgs_visibility_mask": [_vp, C.c_int64, _vp, _vp, _vp],
     "bgs_densify_apply": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_train_view_step_host_async": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, C.c_float, C.c_float, C.c_float,
                                        _vp, _vp, _vp, _vp],
@@ -114,8 +115,10 @@ _lib.bgs_last_error.argtypes = [_vp]
 _lib.bgs_last_error.restype = C.c_char_p
 _lib.bgs_launch_count.argtypes = [_vp]
 _lib.bgs_launch_count.restype = C.c_int64
+_lib.bgs_host_sync_count.argtypes = [_vp]
+_lib.bgs_host_sync_count.restype = C.c_int64
 
-EXPORTS = tuple(_SIGS) + ("bgs_last_error", "bgs_launch_count")
+EXPORTS = tuple(_SIGS) + ("bgs_last_error", "bgs_launch_count", "bgs_host_sync_count")
 
 
 def _ptr(t):
@@ -169,6 +172,9 @@ class Context:
     def check(self, st: int, what: str):
         if st != 0:
             raise BgsError(st, f"{what}: {_lib.bgs_last_error(self._h).decode(errors='replace')}")
+
+    def host_syncs(self) -> int:
+        return int(_lib.bgs_host_sync_count(self._h))
 
     def launches(self) -> int:
         return int(_lib.bgs_launch_count(self._h))
@@ -427,6 +433,12 @@ def densify_params(grad_threshold=2e-4, dense_extent=0.01, min_opacity=0.005, sp
     """3DGS defaults (tau 2e-4, opacity 0.005, split / 1.6); dense_extent = percent_dense * extent;
     k_levels = K (split children's level is min(l + 1, K - 1))."""
     return bgs_densify_params(grad_threshold, dense_extent, min_opacity, split_div, seed, k_levels)
+
+
+def bgs_visibility_mask(ctx: Context, n_local: int, radius, mask, stream=None):
+    """mask (int32 [ceil(n/32)], caller-zeroed per batch) |= bits of radius > 0."""
+    ctx.check(_lib.bgs_visibility_mask(ctx.handle, int(n_local), _ptr(radius), _ptr(mask), _stream(stream)),
+              "bgs_visibility_mask")
 
 
 def bgs_densify_accumulate(ctx: Context, n_local: int, phi, stat, count, stream=None):

@@ -109,7 +109,22 @@ __global__ void __launch_bounds__(kAdamThreads) k_adam_sh(AdamArgs a) {
   G[e] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// Visibility mask of a batch for selective Adam: bit i |= (radius[i] > 0), one ballot per warp
+// and one 32-bit OR per word (views in flight may share the mask: atomicOr).
+__global__ void __launch_bounds__(kAdamThreads) k_visibility_or(const int32_t* __restrict__ radius, int64_t n,
+                                                                uint32_t* __restrict__ mask) {
+  const int64_t i = int64_t(blockIdx.x) * kAdamThreads + threadIdx.x;
+  const bool v = i < n && __ldg(radius + i) > 0;
+  const uint32_t b = __ballot_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && b && i < n) atomicOr(mask + (i >> 5), b);
+}
+
 }  // namespace
+
+void launch_visibility_or(const int32_t* radius, int64_t n, uint32_t* mask, cudaStream_t s) {
+  if (n <= 0) return;
+  k_visibility_or<<<unsigned((n + kAdamThreads - 1) / kAdamThreads), kAdamThreads, 0, s>>>(radius, n, mask);
+}
 
 void launch_adam(const AdamArgs& a, cudaStream_t s) {
   if (a.n <= 0) return;

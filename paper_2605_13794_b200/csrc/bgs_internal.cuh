@@ -312,6 +312,7 @@ struct AdamArgs {
   float b1, b2, om1, om2, eps, c1, c2;  // om = 1 - b (double on the host), c1 = 1/(1 - b1^t), c2 = 1/(1 - b2^t)
 };
 void launch_adam(const AdamArgs& a, cudaStream_t s);
+void launch_visibility_or(const int32_t* radius, int64_t n, uint32_t* mask, cudaStream_t s);
 
 // NEXT-3 density control (densify.cu)
 struct DensifyAccArgs {

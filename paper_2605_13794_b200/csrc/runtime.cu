@@ -39,6 +39,7 @@ struct bgs_ctx {
   std::shared_ptr<Transport> tr;
   std::string err;
   int64_t launches = 0;
+  int64_t host_syncs = 0;  // times an ABI call blocked the host on the device (bgs_host_sync_count)
   // view state
   CameraK cam{};
   int T = 0;
@@ -47,6 +48,7 @@ struct bgs_ctx {
   int t_begin = 0, t_end = 0, n_passes = 0, fallback = 0;
   int raster_split = 0;  // heavy tiles split over two CTAs in the last forward (the backward reuses it)
   int imp_parity = 0;  // which half of imp_hist the next world-1 importance call uses
+  int pend_gate = 0, pend_fb_num = 0, pend_fb_den = 1;  // gate of the enqueued projection (project_finish)
   const Rec* recv = nullptr;  // == recs at world 1
   Acc* acc_local = nullptr;   // == acc at world 1
   // arena
@@ -104,6 +106,16 @@ bgs_status launched(bgs_ctx* ctx, int n = 1) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "kernel launch", cudaGetErrorString(e));
   return BGS_OK;
+}
+
+// The ABI's host synchronisations, counted (bgs_host_sync_count)
+cudaError_t host_sync(bgs_ctx* ctx, cudaStream_t s) {
+  ++ctx->host_syncs;
+  return cudaStreamSynchronize(s);
+}
+cudaError_t host_sync_event(bgs_ctx* ctx, cudaEvent_t e) {
+  ++ctx->host_syncs;
+  return cudaEventSynchronize(e);
 }
 
 bgs_status ensure(bgs_ctx* ctx, DevBuf& b, size_t bytes) {
@@ -470,6 +482,8 @@ const char* bgs_last_error(const bgs_ctx* c) { return c ? c->err.c_str() : "null
 
 int64_t bgs_launch_count(const bgs_ctx* c) { return c ? c->launches : -1; }
 
+int64_t bgs_host_sync_count(const bgs_ctx* c) { return c ? c->host_syncs : -1; }
+
 bgs_status bgs_query(bgs_ctx* ctx, int64_t* out) {
   if (!ctx || !out) return BGS_ERR_INVALID_ARGUMENT;
   const int64_t v[BGS_Q_COUNT] = {ctx->n_local, ctx->n_lod, ctx->n_act, ctx->F, ctx->D, ctx->R, ctx->P,
@@ -519,10 +533,10 @@ bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** ptr, int64_t* by
 // ---------------------------------------------------------------------------------------
 // a1 + a2
 // ---------------------------------------------------------------------------------------
-bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
-                       const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, void* stream) {
-  CKS(check_ctx(ctx));
-  CKS(check_stream(ctx, stream));
+// a1 + a2 enqueued; the counters are on their way to the host (project_finish reads them).
+static bgs_status project_enqueue(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
+                                  const bgs_lod_gate* gate, const uint32_t* cull_column, uint32_t flags,
+                                  int32_t* radius_out, void* stream) {
   CKS(check_gaussians(ctx, g));
   CKS(set_camera(ctx, cam));
   if (g->n_local > 0 && !radius_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "radius_out is NULL");
@@ -611,15 +625,32 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
     launch_color(a, s);
     CKS(launched(ctx));
   }
-  CK(cudaEventSynchronize(ctx->ev_counters));
+  ctx->pend_gate = a.gate_enabled;
+  ctx->pend_fb_num = a.fb_num;
+  ctx->pend_fb_den = a.fb_den;
+  return BGS_OK;
+}
+
+// The projection counters, once the host copy of project_enqueue has landed (the caller waited on
+// ev_counters): F, |A|, P_all, |L|, the fallback decision and the depth range (sort key layout).
+static void project_finish(bgs_ctx* ctx) {
   ctx->F = int64_t(ctx->h_counters[C_F]);
   ctx->n_act = int64_t(ctx->h_counters[C_NACT]);
   ctx->P_all = int64_t(ctx->h_counters[C_PALL]);
-  ctx->n_lod = a.gate_enabled ? int64_t(ctx->h_counters[C_NLOD]) : g->n_local;
-  ctx->fallback = a.gate_enabled ? int((unsigned long long)a.fb_den * ctx->h_counters[C_NLOD] >
-                                       (unsigned long long)a.fb_num * (unsigned long long)g->n_local)
+  ctx->n_lod = ctx->pend_gate ? int64_t(ctx->h_counters[C_NLOD]) : ctx->n_local;
+  ctx->fallback = ctx->pend_gate ? int((unsigned long long)ctx->pend_fb_den * ctx->h_counters[C_NLOD] >
+                                       (unsigned long long)ctx->pend_fb_num * (unsigned long long)ctx->n_local)
                                  : 1;
   ctx->stage = 1;
+}
+
+bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
+                       const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  CKS(project_enqueue(ctx, g, cam, gate, cull_column, flags, radius_out, stream));
+  CK(host_sync_event(ctx, ctx->ev_counters));
+  project_finish(ctx);
   return BGS_OK;
 }
 
@@ -681,7 +712,7 @@ bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_o
   CK(cudaMemcpyAsync(h + M, ctx->xchg_counts.p, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(h + 2 * M, run, size_t(2 * M) * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(h + 4 * M, pown, size_t(M + 1) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   if (h[5 * M]) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "tile_owner_in: not contiguous non-decreasing runs in [0, world)");
   ctx->send_cnt.assign(h, h + M);
   ctx->recv_cnt.assign(h + M, h + 2 * M);
@@ -1025,7 +1056,7 @@ bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, ui
   launch_spatial_order(reinterpret_cast<const float4*>(mean_opac), n, P_<unsigned int>(ctx->tile_diff), a, perm_out,
                        s, &nl);
   CKS(launched(ctx, int(nl)));
-  CK(cudaStreamSynchronize(s));  // h_misc is reused
+  CK(host_sync(ctx, s));  // h_misc is reused
   return BGS_OK;
 }
 
@@ -1172,7 +1203,7 @@ bgs_status bgs_stage_times(bgs_ctx* ctx, float* ms_out) {
   CKS(check_ctx(ctx));
   if (!ms_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bgs_stage_times: ms_out is NULL");
   if (!ctx->stage_recorded) return fail(ctx, BGS_ERR_CONTRACT, "no bgs_view_step with stage timing enabled");
-  CK(cudaEventSynchronize(ctx->stage_ev[kStages]));
+  CK(host_sync_event(ctx, ctx->stage_ev[kStages]));
   for (int k = 0; k < kStages; ++k) CK(cudaEventElapsedTime(ms_out + k, ctx->stage_ev[k], ctx->stage_ev[k + 1]));
   return BGS_OK;
 }
@@ -1220,7 +1251,7 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
                               const bgs_gaussian_grads* grads, const bgs_importance_out* imp, void* stream) {
   CKS(bgs_view_step_host_async(ctx, g, cam, gate, cull_column, flags, radius_out, dL_host, rgb_host, grads, imp,
                                stream));
-  CK(cudaStreamSynchronize(as_stream(stream)));
+  CK(host_sync(ctx, as_stream(stream)));
   return BGS_OK;
 }
 
@@ -1366,6 +1397,14 @@ bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaus
 // ---------------------------------------------------------------------------------------
 // NEXT-3: density control (densify.cu)
 // ---------------------------------------------------------------------------------------
+bgs_status bgs_visibility_mask(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, uint32_t* mask, void* stream) {
+  CKS(check_ctx(ctx));
+  if (n_local < 0 || (n_local > 0 && (!radius || !mask)))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "visibility_mask: radius and mask must be non-NULL");
+  launch_visibility_or(radius, n_local, mask, as_stream(stream));
+  return n_local > 0 ? launched(ctx) : BGS_OK;
+}
+
 bgs_status bgs_densify_accumulate(bgs_ctx* ctx, int64_t n_local, const double* phi, float* stat, uint32_t* count,
                                   void* stream) {
   CKS(check_ctx(ctx));
@@ -1460,7 +1499,7 @@ bgs_status bgs_densify_apply(bgs_ctx* ctx, const bgs_train_params* in, const uin
   CKS(launched(ctx, 2));
   unsigned long long tot[3];
   CK(cudaMemcpyAsync(tot, a.totals, sizeof tot, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   const int64_t n_new = int64_t(tot[0] + tot[1] + 2 * tot[2]);
   *n_out = n_new;
   if (n_new > out->n_local || (act_out && n_new > act_out->capacity))
@@ -1485,7 +1524,7 @@ bgs_status sum_over_ranks(bgs_ctx* ctx, unsigned long long* vals, int n, cudaStr
   CK(cudaMemcpyAsync(d, vals, size_t(n) * 8, cudaMemcpyHostToDevice, s));
   CKS(ctx->tr->allreduce_u64(ctx, d, n, s));
   CK(cudaMemcpyAsync(vals, d, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   return BGS_OK;
 }
 
@@ -1550,7 +1589,7 @@ bgs_status bgs_prune_stochastic(bgs_ctx* ctx, int64_t n_local, const double* s_s
   if (keep_count <= 0 || (unsigned long long)keep_count >= N) {
     launch_fill_u8(n_local, keep_out, keep_count <= 0 ? 0 : 1, s);
     CKS(n_local > 0 ? launched(ctx) : BGS_OK);
-    CK(cudaStreamSynchronize(s));
+    CK(host_sync(ctx, s));
     return BGS_OK;
   }
   CKS(ensure(ctx, ctx->sel_keys, size_t(std::max<int64_t>(n_local, 1)) * 8));
@@ -1558,7 +1597,7 @@ bgs_status bgs_prune_stochastic(bgs_ctx* ctx, int64_t n_local, const double* s_s
   launch_keys_race(n_local, s_score, (unsigned long long)seed, ctx->rank, ctx->world, key, s);
   CKS(n_local > 0 ? launched(ctx) : BGS_OK);
   CKS(run_select(ctx, n_local, key, 0, 0, 1, (unsigned long long)keep_count, keep_out, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   return BGS_OK;
 }
 
@@ -1583,7 +1622,7 @@ bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s_sco
   CKS(n_local > 0 ? launched(ctx, 3) : BGS_OK);
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, cnt, 16, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   CKS(sum_over_ranks(ctx, h, 2, s));
   if (num == den && h[0] > 0) return BGS_OK;  // every s > 0 is kept
   if (h[1] == 0) {
@@ -1592,11 +1631,11 @@ bgs_status bgs_prune_mass_cut(bgs_ctx* ctx, int64_t n_local, const double* s_sco
     CKS(n_local > 0 ? launched(ctx) : BGS_OK);
     if (ctx->rank == 0 && n_local > 0) CK(cudaMemsetAsync(keep_out, 1, 1, s));
     if (all_zero_out) *all_zero_out = 1;
-    CK(cudaStreamSynchronize(s));
+    CK(host_sync(ctx, s));
     return BGS_OK;
   }
   CKS(run_select(ctx, n_local, key, 1, num, den, 0, keep_out, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   return BGS_OK;
 }
 
@@ -1660,7 +1699,7 @@ bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t
   nl += N > 0 ? 3 : 0;
   unsigned long long kept = 0;
   CK(cudaMemcpyAsync(&kept, dc + 16, 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   const int64_t nk = int64_t(kept);
   const int64_t mine = nk > rank ? (nk - rank + M - 1) / M : 0;
   *n_out = mine;
@@ -1670,7 +1709,7 @@ bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t
   if (M == 1) {
     launch_scatter_direct(n, new_gid, *in, *out, out->capacity, s);
     CKS(launched(ctx, nl + (n > 0)));
-    CK(cudaStreamSynchronize(s));
+    CK(host_sync(ctx, s));
     return BGS_OK;
   }
   // per-destination counts -> exchange -> pack 256-B rows -> one all-to-all -> scatter
@@ -1684,7 +1723,7 @@ bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t
   std::vector<int64_t> scnt(M), rcnt(M), soff(M), roff(M);
   CK(cudaMemcpyAsync(scnt.data(), scnt_d, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(rcnt.data(), rcnt_d, size_t(M) * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   int64_t D = 0, R = 0;
   for (int d = 0; d < M; ++d) {
     soff[d] = D;
@@ -1704,7 +1743,7 @@ bgs_status bgs_redistribute(bgs_ctx* ctx, const bgs_gaussians* in, const uint8_t
   launch_unpack_rows(R, ctx->rows_recv.p, *out, out->capacity, s);
   nl += R > 0;
   CKS(launched(ctx, nl));
-  CK(cudaStreamSynchronize(s));
+  CK(host_sync(ctx, s));
   return BGS_OK;
 }
 

@@ -5,21 +5,17 @@ These are what the METHOD must move or compute, not what a kernel happens to do:
                      + 192 F (SH of in-frustum) + 52 F (record + index) + 4 N (radius)      [bytes]
   a5-a7 sort         16 R (rect, depth of received) + 8 P (u32 key + u32 value written) + 16 P
                      per executed 8-bit radix pass (read + write) + 4 P (ranges pass)     [bytes]
-  a8 raster fwd      19 FP32 ops per (pixel, list entry) up to the pixel's last contributor
-                     (SURVEY §8(d)'s E_min = sum of n_contrib): dx,dy 2, power 5, alpha cut 1,
-                     exp 1, alpha = min(.99, oG) 2, w = alpha T and T -= w 2, early stop 1,
-                     colour 3, w and a sums 2                                              [ALU]
-  a9 raster bwd      33 FP32 ops per E_min entry: recompute dx,dy,power,cut,exp,alpha 11,
-                     T_k = T_{k+1}/(1-alpha) 3, w 1, colour grads 3, dL/dalpha (c.dL,
-                     T c.dL - s/(1-alpha), s update) 6, G dL/dalpha 1, dL/do 1, mean2d/conic
-                     moments 7                                                            [ALU]
-                     (MUFU and FFMA count as one op.)  Exact culling skips most E_min entries
-                     (a splat whose alpha >= 1/255 ellipse misses a warp's 8x8 block cannot
-                     contribute there), so this fraction can exceed 1 on scenes with large
-                     splats.  `frac_contributing` is the strict bound beside it: the same ops per
-                     CONTRIBUTING (pixel, splat) pair (A = sum over splats of a_{i,v}), which every
-                     exact kernel must evaluate in full; on Rubble A is ~6% of E_min, i.e. most
-                     evaluations a block-culled kernel issues do not contribute.
+  a8 raster fwd      SURVEY §8(d): ~17 FP32 lane-ops per CONTRIBUTING (pixel, splat) pair (dx,dy 2,
+                     power 3 (one FMUL + 2 FFMA in the pinned order), cut 2, exp 1 MUFU, alpha 2,
+                     test T(1-alpha) 2, w = alpha T 1, colour 3, T update 1).  The contributing pairs are
+                     A = sum over splats of a_{i,v} (measured per view by the instrumented forward):
+                     every exact kernel must evaluate them in full, whatever it culls.  [ALU]
+  a9 raster bwd      SURVEY §8(d): ~45 FP32 lane-ops per contributing pair (recompute dx, dy, power,
+                     exp, alpha 9, T recovery 3, colour grads 6, dL/dalpha 8, clamp + G dL/dalpha 3,
+                     dL/do 1, mean2d / conic partials 12, accumulation 3).                   [ALU]
+                     Diagnostic beside it (`frac_E_min`): the DESIGN.md recount (19 fwd / 33 bwd) per
+                     E_min entry (every list entry up to a pixel's last contributor, sum of n_contrib);
+                     exact box culling skips most of those, so that fraction can exceed 1.
   a10 reverse (M>1)  48 D (send back) + 48 D (gather)                                     [bytes]
   a11 project bwd    240 F (params) + 52 F (partials + index) + 2 x 236 F (grads RMW)     [bytes]
   a12 importance     52 F (w, a, index) + 2 x 16 F (s, c_rad, c_vis RMW) + N/8 (Cull)    [bytes]
@@ -28,13 +24,20 @@ These are what the METHOD must move or compute, not what a kernel happens to do:
                      3 partial maps x 2 passes = 66, dS, L1 sign, sums 9 (the 5 px halo a
                      32x32 tile recomputes is not counted)                                [ALU]
 Peaks: HBM = MEASURED_PEAKS.json hbm_gbs (copy bandwidth); ALU = 148 SMs x 128 FP32 lanes x
-sm_max clock (one FP32 instruction per lane per clock; FFMA counted as one op).
+sm_max clock = 37.2 T lane-op/s (one FP32 instruction per lane per clock; an FFMA is ONE lane-op,
+so this is an instruction rate, not a FLOP rate).
 """
 from __future__ import annotations
 
-FWD_OPS = 19.0
-BWD_OPS = 33.0
+FWD_OPS = 17.0       # per contributing pair (SURVEY 8(d))
+BWD_OPS = 45.0
+FWD_OPS_EMIN = 19.0  # per E_min entry (DESIGN.md recount; diagnostic)
+BWD_OPS_EMIN = 33.0
 LOSS_OPS = 213.0
+KERNEL = {"project": "k_cull+k_project+k_color", "sort": "k_emit+k_onesweep+k_ranges_fixup",
+          "raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project_bwd": "k_project_bwd(+_sh)",
+          "importance": "k_imp_coop", "loss": "k_loss_photo"}
+ALU_UNIT = "T lane-op/s"
 
 
 def _avg(qs, k):
@@ -62,34 +65,42 @@ def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=No
         "importance": 52 * F + 32 * F + N / 8,
     }
     E = float(E) if E is not None else 0.0
-    Ac = float(A_contrib) if A_contrib is not None else E
-    ops = {"raster_fwd": FWD_OPS * E, "raster_bwd": BWD_OPS * E}
-    ops_a = {"raster_fwd": FWD_OPS * Ac, "raster_bwd": BWD_OPS * Ac}
+    Ac = float(A_contrib) if A_contrib is not None else 0.0
+    ops = {"raster_fwd": FWD_OPS * Ac, "raster_bwd": BWD_OPS * Ac}
+    ops_e = {"raster_fwd": FWD_OPS_EMIN * E, "raster_bwd": BWD_OPS_EMIN * E}
     out = []
     for name, ms in zip(names, stage_ms):
         ms = float(ms)
         if name == "loss":
-            if not with_loss:
-                continue  # no supervision in this step (the stage events bracket nothing)
-            o = LOSS_OPS * 3.0 * W * H
-            ach = o / (ms * 1e-3) / 1e12
-            out.append(dict(stage=name, ms=round(ms, 4), bound="alu", achieved=round(ach, 3), peak=round(alu, 2),
-                            unit="TFLOP/s", frac=round(ach / alu, 4), traffic=traffic.get(name),
-                            work=f"{o:.3e} ops ({LOSS_OPS:.0f} x 3 H W)"))
-        elif name in ops:
+            if with_loss:
+                out.append(loss_roofline(ms, W, H, peaks, traffic.get(name)))
+            continue
+        if name in ops:
             ach = ops[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-            ach_a = ops_a[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+            ach_e = ops_e[name] / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
             k = FWD_OPS if name == "raster_fwd" else BWD_OPS
-            out.append(dict(stage=name, ms=round(ms, 4), bound="alu", achieved=round(ach, 3), peak=round(alu, 2),
-                            unit="TFLOP/s", frac=round(ach / alu, 4), traffic=traffic.get(name),
-                            work=f"{ops[name]:.3e} ops ({k:.0f} x E_min)",
-                            frac_contributing=round(ach_a / alu, 4)))
+            out.append(dict(stage=name, kernel=KERNEL[name], ms=round(ms, 4), bound="alu", achieved=round(ach, 3),
+                            peak=round(alu, 2), unit=ALU_UNIT, frac=round(ach / alu, 4), traffic=traffic.get(name),
+                            work=f"{ops[name]:.3e} lane-ops per view ({k:.0f} x {Ac:.4g} contributing pairs)",
+                            frac_E_min=round(ach_e / alu, 4),
+                            work_E_min=f"{ops_e[name]:.3e} ({FWD_OPS_EMIN if k == FWD_OPS else BWD_OPS_EMIN:.0f}"
+                                       f" x E_min {E:.4g})"))
         else:
             b = bytes_.get(name, 0.0)
             ach = b / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
-            out.append(dict(stage=name, ms=round(ms, 4), bound="hbm", achieved=round(ach, 1), peak=hbm,
-                            unit="GB/s", frac=round(ach / hbm, 4), traffic=traffic.get(name), work=f"{b:.3e} bytes"))
+            out.append(dict(stage=name, kernel=KERNEL.get(name, name), ms=round(ms, 4), bound="hbm",
+                            achieved=round(ach, 1), peak=hbm, unit="GB/s", frac=round(ach / hbm, 4),
+                            traffic=traffic.get(name), work=f"{b:.3e} bytes per view"))
     return out
+
+
+def loss_roofline(ms, W, H, peaks, traffic=None):
+    alu = 148 * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    o = LOSS_OPS * 3.0 * W * H
+    ach = o / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    return dict(stage="loss", kernel=KERNEL["loss"], ms=round(ms, 4), bound="alu", achieved=round(ach, 3),
+                peak=round(alu, 2), unit=ALU_UNIT, frac=round(ach / alu, 4), traffic=traffic,
+                work=f"{o:.3e} lane-ops ({LOSS_OPS:.0f} x 3 H W)")
 
 
 def load_traffic(path):

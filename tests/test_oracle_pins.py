@@ -429,6 +429,18 @@ def test_P10_M_invariance(tiny_scene):
         np.testing.assert_allclose(st.get("d_mean"), ref.get("d_mean"), rtol=1e-9, atol=1e-15)
 
 
+def test_threaded_oracle_is_bit_identical(tiny_scene):
+    """The multi-core baseline (bench.py cpu_baseline) runs the same oracle with host threads:
+    every output, including the fp64 sums, must be bit-identical to the sequential run."""
+    dl = S.grad_image(256, 256)
+    for M in (1, 3):
+        ref = O.OracleStep(tiny_scene, tiny_scene.cameras[0], M=M, dLdC=dl, threads=1)
+        st = O.OracleStep(tiny_scene, tiny_scene.cameras[0], M=M, dLdC=dl, threads=4)
+        for f in ("img", "t_final", "n_contrib", "et_margin", "w", "w_fixed", "a", "radius", "g2d", "d_mean",
+                  "d_quat", "d_scale", "d_opac", "d_sh", "margins"):
+            assert np.array_equal(st.get(f), ref.get(f)), (M, f)
+
+
 def test_tile_partition_invariants(tiny_scene):
     """Reading R24 (P:170 cites Scaling-3DGS without an algorithm): parity unpinned beyond these."""
     for M in (1, 2, 3, 4, 8):
