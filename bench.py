@@ -381,6 +381,11 @@ def run_native(args):
     views_per_s = 1000.0 * n_views / head_ms
 
     imp_ms, imp_launches, _, _ = timed_batches(lambda k, v: view_on(k, v, True), args.steps, 1)
+
+    # ---- NEXT-2: the same steps through bgs_batch_step (one call per batch of B views: one host
+    # read and, at world > 1, one exchange per batch), eagerly and as a CUDA graph (BGS_GRAPH)
+    batch_api = batch_step_timing(args, B, g, cams, gate, cull_of, per, dl, grads, batch, barrier, D, tdev, world,
+                                  rank, local)
     with_importance = {"metric": "fwd+bwd views/s with a12 (importance, Cull column) per view",
                        "value": round(1000.0 * n_views / imp_ms, 3), "unit": "views/s",
                        "ms_per_step": round(imp_ms / args.steps, 4), "gpu_launches": int(imp_launches)}
@@ -430,6 +435,7 @@ def run_native(args):
         "single_view_with_importance_ms": round(single_imp_ms, 4),
         "splat_pairs_per_s": round(pairs_per_s, 1),
         "with_importance": with_importance,
+        "batch_step": batch_api,
         "per_view": {"pairs_P": P_all, "records_F": F_all, "received_R": R_all, "sent_D": D_all,
                      "active_A": A_all, "duplication_D_over_F": (D_all / F_all if F_all else None),
                      "nvlink_bytes": 48.0 * (D_all - F_all) * 2 if world > 1 else 0.0,
@@ -480,6 +486,62 @@ def run_native(args):
         c.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def batch_step_timing(args, B, g, cams, gate, cull_of, per, dl, grads, batch, barrier, D, tdev, world, rank, local):
+    """K steps through bgs_batch_step (NEXT-2), device-timed like the headline; per batch: launches,
+    host syncs and collectives (the library's counters)."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        uid = D.broadcast_bytes(B.unique_id() if rank == 0 else None, 128, tdev)
+        bctx = B.Context(rank, world, local, uid)
+    else:
+        bctx = B.Context(0, 1, local)
+    stream = per[0]["stream"]
+    V = len(cams)
+    n_arr = V // batch if V % batch == 0 else V
+    arrs = []
+    for i in range(n_arr):
+        vs = []
+        for k in range(batch):
+            v = (i * batch + k) % V
+            p = per[k]
+            vs.append(B.batch_view(cams[v], p["radius"], p["rgb"], p["Tf"], p["nc"], dl, cull_column=cull_of(v)))
+        arrs.append((B.bgs_batch_view * batch)(*vs))
+    out = {}
+    for name, flags in (("eager", 0), ("graph", B.BGS_GRAPH)):
+        with torch.cuda.stream(stream):
+            for i in range(args.warmup + 1):
+                B.bgs_batch_step(bctx, g, arrs[i % n_arr], gate, flags, grads, None, stream)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            s0 = bctx.batch_stats()
+            l0, h0 = bctx.launches(), bctx.host_syncs()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(args.steps):
+                B.bgs_batch_step(bctx, g, arrs[(args.warmup + 1 + i) % n_arr], gate, flags, grads, None, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = D.max_over_ranks(e0.elapsed_time(e1), tdev)
+        s1 = bctx.batch_stats()
+        nv = args.steps * batch
+        out[name] = {"value": round(1000.0 * nv / ms, 3), "unit": "views/s", "ms_per_step": round(ms / args.steps, 4),
+                     "gpu_launches_per_view": round((bctx.launches() - l0) / nv, 2),
+                     "host_syncs_per_view": round((bctx.host_syncs() - h0) / nv, 3),
+                     "collectives_per_step": round((s1["collectives"] - s0["collectives"]) / args.steps, 2),
+                     "graph_launches": s1["graph_launches"] - s0["graph_launches"],
+                     "graph_instantiations": s1["graph_instantiations"] - s0["graph_instantiations"],
+                     "graph_fallbacks": s1["graph_fallbacks"] - s0["graph_fallbacks"]}
+        if world > 1:
+            dist.barrier()
+    bctx.close()
+    out["note"] = ("bgs_batch_step: B views per call on internal view slots, one host read per batch, at world > 1 "
+                   "one tile-cost all-reduce + one count exchange + one record all-to-all + one reverse per batch; "
+                   "graph = everything after the host read recorded as one CUDA graph (updated in place)")
+    return out
 
 
 def scoring(args, B, ctxs, per, g, cams, gate, cull_of, s_imp, c_rad, c_vis, l2_flush, batch, barrier, D, tdev,

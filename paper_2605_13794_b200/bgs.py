@@ -25,6 +25,7 @@ _lib = C.CDLL(LIB_PATH)
 
 BGS_NO_COLOR = 1
 BGS_IMPORTANCE = 2
+BGS_GRAPH = 4
 BGS_Q_COUNT = 14
 Q_NAMES = ("n_local", "n_lod", "n_active", "F", "D", "R", "P", "tile_begin", "tile_end", "fallback",
            "sort_passes", "P_all", "width", "height")
@@ -44,6 +45,12 @@ class bgs_camera(C.Structure):
     _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
                 ("width", C.c_int32), ("height", C.c_int32), ("R", C.c_float * 9), ("t", C.c_float * 3),
                 ("campos", C.c_float * 3), ("near_clip", C.c_float)]
+
+
+class bgs_batch_view(C.Structure):
+    _fields_ = [("cam", bgs_camera), ("cull_column", C.c_void_p), ("radius_out", C.c_void_p), ("rgb", C.c_void_p),
+                ("t_final", C.c_void_p), ("n_contrib", C.c_void_p), ("dL_drgb", C.c_void_p),
+                ("cull_out", C.c_void_p)]
 
 
 class bgs_gaussians(C.Structure):
@@ -103,6 +110,9 @@ _SIGS = {
     "bgs_adam_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_densify_accumulate": [_vp, C.c_int64, _vp, _vp, _vp, _vp],
     "bgs_visibility_mask": [_vp, C.c_int64, _vp, _vp, _vp],
+    "bgs_batch_step": [_vp, C.c_int32, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp],
+    "bgs_batch_view_ctx": [_vp, C.c_int32, _vp],
+    "bgs_batch_stats": [_vp, _vp],
     "bgs_densify_apply": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_train_view_step_host_async": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, C.c_float, C.c_float, C.c_float,
                                        _vp, _vp, _vp, _vp],
@@ -202,9 +212,23 @@ class Context:
         return out.view(dtype) if n else out
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and not getattr(self, "_borrowed", False):
             _lib.bgs_ctx_destroy(self._h)
-            self._h = None
+        self._h = None
+
+    def batch_view(self, b: int) -> "Context":
+        """Borrowed Context of view slot b of the last bgs_batch_step (query / debug_buffer only)."""
+        h = C.c_void_p()
+        self.check(_lib.bgs_batch_view_ctx(self._h, int(b), C.byref(h)), "bgs_batch_view_ctx")
+        c = Context(self.rank, self.world, self.device, _handle=h)
+        c._borrowed = True
+        return c
+
+    def batch_stats(self) -> dict:
+        out = (C.c_int64 * 6)()
+        self.check(_lib.bgs_batch_stats(self._h, out), "bgs_batch_stats")
+        return dict(zip(("host_syncs", "collectives", "batches", "graph_launches", "graph_instantiations",
+                         "graph_fallbacks"), list(out)))
 
 
 _CUDART = None
@@ -496,6 +520,25 @@ def bgs_train_view_step_host_async(ctx: Context, g: GaussianPlanes, cam: bgs_cam
                                                   C.byref(importance) if importance is not None else None,
                                                   _stream(stream)),
               "bgs_train_view_step_host_async")
+
+
+def batch_view(cam: bgs_camera, radius_out, rgb, t_final, n_contrib, dL_drgb=None, cull_column=None,
+               cull_out=None) -> bgs_batch_view:
+    return bgs_batch_view(cam, _ptr(cull_column), _ptr(radius_out), _ptr(rgb), _ptr(t_final), _ptr(n_contrib),
+                          _ptr(dL_drgb), _ptr(cull_out))
+
+
+def bgs_batch_step(ctx: Context, g: GaussianPlanes, views, gate=None, flags: int = 0, grads: GradPlanes | None = None,
+                   importance: bgs_importance_out | None = None, stream=None):
+    """NEXT-2: a1..a11 (+a12) of len(views) views in one call (one host read, one exchange per batch).
+    views: a list of bgs_batch_view or a prebuilt ctypes array of them."""
+    arr = views if isinstance(views, C.Array) else (bgs_batch_view * len(views))(*views)
+    gs = g.struct()
+    gr = grads.struct() if grads is not None else None
+    ctx.check(_lib.bgs_batch_step(ctx.handle, len(views), C.byref(gs), C.byref(gate) if gate is not None else None,
+                                  int(flags), arr, C.byref(gr) if gr is not None else None,
+                                  C.byref(importance) if importance is not None else None, _stream(stream)),
+              "bgs_batch_step")
 
 
 def bgs_view_step(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, cull_column, flags, radius_out, rgb, t_final,

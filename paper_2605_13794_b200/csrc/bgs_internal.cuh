@@ -188,14 +188,15 @@ void launch_project_bwd(const ProjectBwdArgs& a, cudaStream_t s);
 void launch_tile_costs(const int32_t* diff, int TX, int TY, int32_t* pairs_t, cudaStream_t s);
 void launch_owner_map(const int32_t* pairs_t, int T, int world, int32_t* owner, int32_t* run, long long* pown,
                       const int32_t* given, cudaStream_t s);
-void launch_dest_count(const Rec* recs, int64_t F, const int32_t* owner, int TX, int world, uint8_t* dest_mask,
-                       uint32_t* block_counts, cudaStream_t s);
-void launch_block_scan(uint32_t* block_counts, int64_t n_blocks, int world, unsigned long long* totals,
-                       cudaStream_t s);
-void launch_pack(const Rec* recs, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs, int world,
-                 const int64_t* send_base, Rec* send, cudaStream_t s);
-void launch_gather_sum(const Acc* rev, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs,
-                       int world, const int64_t* send_base, Acc* out, cudaStream_t s);
+// F_dev (nullable): the record count on the device (batched steps); F is then the grid's capacity
+void launch_dest_count(const Rec* recs, int64_t F, const unsigned long long* F_dev, const int32_t* owner, int TX,
+                       int world, uint8_t* dest_mask, uint32_t* block_counts, cudaStream_t s);
+void launch_block_scan(uint32_t* block_counts, int64_t F, const unsigned long long* F_dev, int world,
+                       unsigned long long* totals, cudaStream_t s);
+void launch_pack(const Rec* recs, int64_t F, const unsigned long long* F_dev, const uint8_t* dest_mask,
+                 const uint32_t* block_offs, int world, const int64_t* send_base, Rec* send, cudaStream_t s);
+void launch_gather_sum(const Acc* rev, int64_t F, const unsigned long long* F_dev, const uint8_t* dest_mask,
+                       const uint32_t* block_offs, int world, const int64_t* send_base, Acc* out, cudaStream_t s);
 struct PtrList {
   const void* p[kMaxWorld];
   int n;

@@ -115,6 +115,14 @@ __global__ void __launch_bounds__(1024) k_owner_map(const int32_t* pairs, int T,
   }
 }
 
+// Record count: the host's F, or (batched steps, F_dev != nullptr) the projection counter on the
+// device, bounded by the launch capacity F (the grid covers the capacity; CTAs past the count exit).
+__device__ __forceinline__ int64_t rec_count(int64_t F, const unsigned long long* F_dev) {
+  if (!F_dev) return F;
+  const int64_t d = int64_t(*F_dev);
+  return d < F ? d : F;
+}
+
 __device__ __forceinline__ uint32_t dest_mask_of(uint32_t rect, const int32_t* owner, int TX) {
   const int x0 = rect & 255, y0 = (rect >> 8) & 255, x1 = (rect >> 16) & 255, y1 = rect >> 24;
   uint32_t m = 0;
@@ -144,10 +152,13 @@ __device__ __forceinline__ void block_positions(uint32_t mask, int world, uint32
   }
 }
 
-__global__ void __launch_bounds__(kRouteBlock) k_dest_count(const Rec* recs, int64_t F, const int32_t* owner,
+__global__ void __launch_bounds__(kRouteBlock) k_dest_count(const Rec* recs, int64_t F_cap,
+                                                            const unsigned long long* F_dev, const int32_t* owner,
                                                             int TX, int world, uint8_t* dest_mask,
                                                             uint32_t* block_counts) {
   __shared__ uint32_t s_w[kRouteBlock / 32][kMaxWorld];
+  const int64_t F = rec_count(F_cap, F_dev);
+  if (int64_t(blockIdx.x) * blockDim.x >= F && blockIdx.x > 0) return;  // past the count (block 0 always writes)
   const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t mask = 0;
   if (f < F) {
@@ -163,9 +174,12 @@ __global__ void __launch_bounds__(kRouteBlock) k_dest_count(const Rec* recs, int
   }
 }
 
-__global__ void __launch_bounds__(kMaxWorld * 32) k_block_scan(uint32_t* counts, int64_t n_blocks, int world,
+__global__ void __launch_bounds__(kMaxWorld * 32) k_block_scan(uint32_t* counts, int64_t F_cap,
+                                                               const unsigned long long* F_dev, int world,
                                                                unsigned long long* totals) {
   // one warp per destination: exclusive scan over blocks
+  const int64_t F = rec_count(F_cap, F_dev);
+  const int64_t n_blocks = F > 0 ? (F + kRouteBlock - 1) / kRouteBlock : 1;
   const int d = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (d >= world) return;
   unsigned long long run = 0;
@@ -184,10 +198,13 @@ __global__ void __launch_bounds__(kMaxWorld * 32) k_block_scan(uint32_t* counts,
   if (lane == 0) totals[d] = run;
 }
 
-__global__ void __launch_bounds__(kRouteBlock) k_pack(const Rec* recs, int64_t F, const uint8_t* dest_mask,
+__global__ void __launch_bounds__(kRouteBlock) k_pack(const Rec* recs, int64_t F_cap,
+                                                      const unsigned long long* F_dev, const uint8_t* dest_mask,
                                                       const uint32_t* block_offs, int world,
                                                       const int64_t* send_base, Rec* send) {
   __shared__ uint32_t s_w[kRouteBlock / 32][kMaxWorld];
+  const int64_t F = rec_count(F_cap, F_dev);
+  if (int64_t(blockIdx.x) * blockDim.x >= F) return;
   const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint32_t mask = f < F ? dest_mask[f] : 0u;
   uint32_t pos[kMaxWorld];
@@ -205,10 +222,13 @@ __global__ void __launch_bounds__(kRouteBlock) k_pack(const Rec* recs, int64_t F
   }
 }
 
-__global__ void __launch_bounds__(kRouteBlock) k_gather_sum(const Acc* rev, int64_t F, const uint8_t* dest_mask,
+__global__ void __launch_bounds__(kRouteBlock) k_gather_sum(const Acc* rev, int64_t F_cap,
+                                                            const unsigned long long* F_dev, const uint8_t* dest_mask,
                                                             const uint32_t* block_offs, int world,
                                                             const int64_t* send_base, Acc* out) {
   __shared__ uint32_t s_w[kRouteBlock / 32][kMaxWorld];
+  const int64_t F = rec_count(F_cap, F_dev);
+  if (int64_t(blockIdx.x) * blockDim.x >= F) return;
   const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint32_t mask = f < F ? dest_mask[f] : 0u;
   uint32_t pos[kMaxWorld];
@@ -278,28 +298,31 @@ void launch_owner_map(const int32_t* pairs_t, int T, int world, int32_t* owner, 
   k_owner_map<<<1, 1024, smem, s>>>(pairs_t, T, world, owner, run, pown, given);
 }
 
-void launch_dest_count(const Rec* recs, int64_t F, const int32_t* owner, int TX, int world, uint8_t* dest_mask,
-                       uint32_t* block_counts, cudaStream_t s) {
-  const int64_t nb = (F + kRouteBlock - 1) / kRouteBlock;
-  if (nb > 0) k_dest_count<<<unsigned(nb), kRouteBlock, 0, s>>>(recs, F, owner, TX, world, dest_mask, block_counts);
-}
-
-void launch_block_scan(uint32_t* block_counts, int64_t n_blocks, int world, unsigned long long* totals,
-                       cudaStream_t s) {
-  k_block_scan<<<1, kMaxWorld * 32, 0, s>>>(block_counts, n_blocks, world, totals);
-}
-
-void launch_pack(const Rec* recs, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs, int world,
-                 const int64_t* send_base, Rec* send, cudaStream_t s) {
-  const int64_t nb = (F + kRouteBlock - 1) / kRouteBlock;
-  if (nb > 0) k_pack<<<unsigned(nb), kRouteBlock, 0, s>>>(recs, F, dest_mask, block_offs, world, send_base, send);
-}
-
-void launch_gather_sum(const Acc* rev, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs, int world,
-                       const int64_t* send_base, Acc* out, cudaStream_t s) {
+// F: the record count, or with F_dev the capacity the grid covers (the count is read on the device)
+void launch_dest_count(const Rec* recs, int64_t F, const unsigned long long* F_dev, const int32_t* owner, int TX,
+                       int world, uint8_t* dest_mask, uint32_t* block_counts, cudaStream_t s) {
   const int64_t nb = (F + kRouteBlock - 1) / kRouteBlock;
   if (nb > 0)
-    k_gather_sum<<<unsigned(nb), kRouteBlock, 0, s>>>(rev, F, dest_mask, block_offs, world, send_base, out);
+    k_dest_count<<<unsigned(nb), kRouteBlock, 0, s>>>(recs, F, F_dev, owner, TX, world, dest_mask, block_counts);
+}
+
+void launch_block_scan(uint32_t* block_counts, int64_t F, const unsigned long long* F_dev, int world,
+                       unsigned long long* totals, cudaStream_t s) {
+  k_block_scan<<<1, kMaxWorld * 32, 0, s>>>(block_counts, F, F_dev, world, totals);
+}
+
+void launch_pack(const Rec* recs, int64_t F, const unsigned long long* F_dev, const uint8_t* dest_mask,
+                 const uint32_t* block_offs, int world, const int64_t* send_base, Rec* send, cudaStream_t s) {
+  const int64_t nb = (F + kRouteBlock - 1) / kRouteBlock;
+  if (nb > 0)
+    k_pack<<<unsigned(nb), kRouteBlock, 0, s>>>(recs, F, F_dev, dest_mask, block_offs, world, send_base, send);
+}
+
+void launch_gather_sum(const Acc* rev, int64_t F, const unsigned long long* F_dev, const uint8_t* dest_mask,
+                       const uint32_t* block_offs, int world, const int64_t* send_base, Acc* out, cudaStream_t s) {
+  const int64_t nb = (F + kRouteBlock - 1) / kRouteBlock;
+  if (nb > 0)
+    k_gather_sum<<<unsigned(nb), kRouteBlock, 0, s>>>(rev, F, F_dev, dest_mask, block_offs, world, send_base, out);
 }
 
 void launch_reduce_sum_i32(PtrList src, int32_t* dst, int64_t n, cudaStream_t s) {

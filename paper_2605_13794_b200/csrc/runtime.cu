@@ -27,7 +27,13 @@ struct DevBuf {
 };
 
 struct Transport;
+struct BatchState;
 
+}  // namespace
+
+struct bgs_ctx;
+namespace {
+void destroy_batch(bgs_ctx* c);  // NEXT-2 batch state (defined with bgs_batch_step)
 }  // namespace
 
 // bgs_stage_times: project, route, sort, raster_fwd, loss, raster_bwd, route_reverse, project_bwd,
@@ -40,6 +46,10 @@ struct bgs_ctx {
   std::string err;
   int64_t launches = 0;
   int64_t host_syncs = 0;  // times an ABI call blocked the host on the device (bgs_host_sync_count)
+  int64_t collectives = 0;  // transport collectives issued (bgs_batch_stats)
+  bool capturing = false;         // a CUDA graph capture is open on this ctx's work: ensure() must not grow
+  bool grew_in_capture = false;   // ... and it had to (the batch then runs eagerly)
+  BatchState* batch = nullptr;    // NEXT-2 batched step (bgs_batch_step), created on first use
   // view state
   CameraK cam{};
   int T = 0;
@@ -121,6 +131,10 @@ cudaError_t host_sync_event(bgs_ctx* ctx, cudaEvent_t e) {
 bgs_status ensure(bgs_ctx* ctx, DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (bytes <= b.cap) return BGS_OK;
+  if (ctx->capturing) {  // a graph is being captured: growing (cudaFree / cudaMalloc) is not allowed
+    ctx->grew_in_capture = true;
+    return fail(ctx, BGS_ERR_CAPACITY, "arena growth needed during graph capture");
+  }
   if (b.p) {
     cudaError_t e = cudaFree(b.p);
     if (e != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, "cudaFree", cudaGetErrorString(e));
@@ -158,6 +172,15 @@ struct Transport {
   virtual bgs_status alltoall1(bgs_ctx* ctx, const int64_t* send, int64_t* recv, cudaStream_t s) = 0;
   virtual bgs_status alltoallv(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
                                const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) = 0;
+  // device int64 [world][n] -> [world][n]: send[p n .. p n + n) goes to rank p (batched counts)
+  virtual bgs_status alltoall_n(bgs_ctx* ctx, const int64_t* send, int64_t* recv, int n, cudaStream_t s) = 0;
+  // ONE grouped exchange of nb segment sets (the views of a batch): for every view b and peer p,
+  // send[b] + soff[b M + p] (scnt[b M + p] elements) goes to p, and recv[b] + roff[b M + k] gets
+  // rcnt[b M + k] elements from k
+  virtual bgs_status alltoallv_batch(bgs_ctx* ctx, int nb, const void* const* send, const int64_t* scnt,
+                                     const int64_t* soff, void* const* recv, const int64_t* rcnt, const int64_t* roff,
+                                     size_t elem, cudaStream_t s) = 0;
+  virtual bool capturable() const = 0;  // collectives may be recorded into a CUDA graph
 };
 
 bgs_status nccl_fail(bgs_ctx* ctx, ncclResult_t r, const char* what) {
@@ -170,22 +193,27 @@ struct NcclTransport : Transport {
     if (comm) ncclCommDestroy(comm);
   }
   bgs_status allreduce_i32(bgs_ctx* ctx, int32_t* buf, int64_t n, cudaStream_t s) override {
+    ++ctx->collectives;
     ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclInt32, ncclSum, comm, s);
     return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
   }
   bgs_status allreduce_u64(bgs_ctx* ctx, unsigned long long* buf, int64_t n, cudaStream_t s) override {
+    ++ctx->collectives;
     ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclUint64, ncclSum, comm, s);
     return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
   }
   bgs_status allreduce_f32(bgs_ctx* ctx, float* buf, int64_t n, cudaStream_t s) override {
+    ++ctx->collectives;
     ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclFloat32, ncclSum, comm, s);
     return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
   }
   bgs_status allreduce_f64(bgs_ctx* ctx, double* buf, int64_t n, cudaStream_t s) override {
+    ++ctx->collectives;
     ncclResult_t r = ncclAllReduce(buf, buf, size_t(n), ncclFloat64, ncclSum, comm, s);
     return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllReduce");
   }
   bgs_status alltoall1(bgs_ctx* ctx, const int64_t* send, int64_t* recv, cudaStream_t s) override {
+    ++ctx->collectives;
     ncclResult_t r = ncclGroupStart();
     for (int p = 0; p < ctx->world && r == ncclSuccess; ++p) {
       r = ncclSend(send + p, 1, ncclInt64, p, comm, s);
@@ -197,6 +225,7 @@ struct NcclTransport : Transport {
   }
   bgs_status alltoallv(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
                        const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) override {
+    ++ctx->collectives;
     ncclResult_t r = ncclGroupStart();
     for (int p = 0; p < ctx->world && r == ncclSuccess; ++p) {
       if (scnt[p] > 0)
@@ -208,6 +237,37 @@ struct NcclTransport : Transport {
     if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclSend/Recv records");
     return r2 == ncclSuccess ? BGS_OK : nccl_fail(ctx, r2, "ncclGroupEnd");
   }
+  bgs_status alltoall_n(bgs_ctx* ctx, const int64_t* send, int64_t* recv, int n, cudaStream_t s) override {
+    ++ctx->collectives;
+    ncclResult_t r = ncclGroupStart();
+    for (int p = 0; p < ctx->world && r == ncclSuccess; ++p) {
+      r = ncclSend(send + size_t(p) * n, size_t(n), ncclInt64, p, comm, s);
+      if (r == ncclSuccess) r = ncclRecv(recv + size_t(p) * n, size_t(n), ncclInt64, p, comm, s);
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclSend/Recv batched counts");
+    return r2 == ncclSuccess ? BGS_OK : nccl_fail(ctx, r2, "ncclGroupEnd");
+  }
+  bgs_status alltoallv_batch(bgs_ctx* ctx, int nb, const void* const* send, const int64_t* scnt, const int64_t* soff,
+                             void* const* recv, const int64_t* rcnt, const int64_t* roff, size_t elem,
+                             cudaStream_t s) override {
+    ++ctx->collectives;
+    const int M = ctx->world;
+    ncclResult_t r = ncclGroupStart();
+    for (int b = 0; b < nb && r == ncclSuccess; ++b)
+      for (int p = 0; p < M && r == ncclSuccess; ++p) {
+        const size_t i = size_t(b) * M + p;
+        if (scnt[i] > 0)
+          r = ncclSend(static_cast<const char*>(send[b]) + soff[i] * elem, size_t(scnt[i]) * elem, ncclChar, p, comm,
+                       s);
+        if (r == ncclSuccess && rcnt[i] > 0)
+          r = ncclRecv(static_cast<char*>(recv[b]) + roff[i] * elem, size_t(rcnt[i]) * elem, ncclChar, p, comm, s);
+      }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclSend/Recv batched records");
+    return r2 == ncclSuccess ? BGS_OK : nccl_fail(ctx, r2, "ncclGroupEnd");
+  }
+  bool capturable() const override { return true; }
 };
 
 // In-process group of `world` contexts on one device (test transport).  Collectives are
@@ -221,8 +281,9 @@ struct LocalGroup {
   uint64_t gen = 0;
   std::vector<const void*> ptr;
   std::vector<const int64_t*> cnt, off;
+  std::vector<const void* const*> bptr;  // batched exchange: per rank, its nb send pointers
   std::vector<cudaEvent_t> ready, done;
-  explicit LocalGroup(int w) : world(w), ptr(w), cnt(w), off(w), ready(w), done(w) {
+  explicit LocalGroup(int w) : world(w), ptr(w), cnt(w), off(w), bptr(w), ready(w), done(w) {
     for (int i = 0; i < w; ++i) {
       cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
@@ -256,6 +317,7 @@ struct LocalTransport : Transport {
   }
   template <class T, class L>
   bgs_status allreduce(bgs_ctx* ctx, T* buf, int64_t n, cudaStream_t s, L launch) {
+    ++ctx->collectives;
     const int r = ctx->rank;
     CKS(ensure(ctx, tmp, size_t(n) * sizeof(T)));
     g->ptr[r] = buf;
@@ -298,6 +360,7 @@ struct LocalTransport : Transport {
   }
   bgs_status exchange(bgs_ctx* ctx, const void* send, const int64_t* scnt, const int64_t* soff, void* recv,
                       const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) {
+    ++ctx->collectives;
     const int r = ctx->rank;
     g->ptr[r] = send;
     g->cnt[r] = scnt;
@@ -328,6 +391,39 @@ struct LocalTransport : Transport {
                        const int64_t* rcnt, const int64_t* roff, size_t elem, cudaStream_t s) override {
     return exchange(ctx, send, scnt, soff, recv, rcnt, roff, elem, s);
   }
+  bgs_status alltoall_n(bgs_ctx* ctx, const int64_t* send, int64_t* recv, int n, cudaStream_t s) override {
+    std::vector<int64_t> cnt(ctx->world, n), idx(ctx->world);
+    for (int k = 0; k < ctx->world; ++k) idx[k] = int64_t(k) * n;
+    return exchange(ctx, send, cnt.data(), idx.data(), recv, cnt.data(), idx.data(), sizeof(int64_t), s);
+  }
+  bgs_status alltoallv_batch(bgs_ctx* ctx, int nb, const void* const* send, const int64_t* scnt, const int64_t* soff,
+                             void* const* recv, const int64_t* rcnt, const int64_t* roff, size_t elem,
+                             cudaStream_t s) override {
+    ++ctx->collectives;
+    const int r = ctx->rank, M = ctx->world;
+    g->bptr[r] = send;
+    g->cnt[r] = scnt;
+    g->off[r] = soff;
+    CK(cudaEventRecord(g->ready[r], s));
+    g->barrier();
+    for (int k = 0; k < M; ++k) CK(cudaStreamWaitEvent(s, g->ready[k], 0));
+    for (int b = 0; b < nb; ++b)
+      for (int k = 0; k < M; ++k) {
+        const size_t mine = size_t(b) * M + k, theirs = size_t(b) * M + r;
+        const int64_t c = g->cnt[k][theirs];
+        if (c != rcnt[mine]) return fail(ctx, BGS_ERR_INTERNAL, "local batched exchange: count mismatch");
+        if (c > 0)
+          CK(cudaMemcpyAsync(static_cast<char*>(recv[b]) + roff[mine] * elem,
+                             static_cast<const char*>(g->bptr[k][b]) + g->off[k][theirs] * elem, size_t(c) * elem,
+                             cudaMemcpyDeviceToDevice, s));
+      }
+    CK(cudaEventRecord(g->done[r], s));
+    g->barrier();
+    for (int k = 0; k < M; ++k) CK(cudaStreamWaitEvent(s, g->done[k], 0));
+    g->barrier();
+    return BGS_OK;
+  }
+  bool capturable() const override { return false; }  // host barriers order the copies
 };
 
 // ---------------------------------------------------------------------------------------
@@ -473,6 +569,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
+  destroy_batch(c);
   c->tr.reset();
   delete c;
   return BGS_OK;
@@ -700,10 +797,10 @@ bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_o
   CKS(ensure(ctx, ctx->send_base, size_t(M) * 8));
   CK(cudaMemsetAsync(ctx->totals.p, 0, size_t(M) * 8, s));
   if (F > 0) {
-    launch_dest_count(ctx->recs.p ? P_<Rec>(ctx->recs) : nullptr, F, P_<int32_t>(ctx->owner), ctx->cam.TX, M,
-                      P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), s);
+    launch_dest_count(ctx->recs.p ? P_<Rec>(ctx->recs) : nullptr, F, nullptr, P_<int32_t>(ctx->owner), ctx->cam.TX,
+                      M, P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), s);
     CKS(launched(ctx));
-    launch_block_scan(P_<uint32_t>(ctx->block_counts), nb, M, P_<unsigned long long>(ctx->totals), s);
+    launch_block_scan(P_<uint32_t>(ctx->block_counts), F, nullptr, M, P_<unsigned long long>(ctx->totals), s);
     CKS(launched(ctx));
   }
   CKS(ctx->tr->alltoall1(ctx, P_<int64_t>(ctx->totals), P_<int64_t>(ctx->xchg_counts), s));
@@ -735,7 +832,7 @@ bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_o
   CKS(ensure(ctx, ctx->recvbuf, size_t(std::max<int64_t>(R, 1)) * sizeof(Rec)));
   CK(cudaMemcpyAsync(ctx->send_base.p, ctx->send_off.data(), size_t(M) * 8, cudaMemcpyHostToDevice, s));
   if (F > 0) {
-    launch_pack(P_<Rec>(ctx->recs), F, P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), M,
+    launch_pack(P_<Rec>(ctx->recs), F, nullptr, P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), M,
                 P_<int64_t>(ctx->send_base), P_<Rec>(ctx->send), s);
     CKS(launched(ctx));
   }
@@ -901,8 +998,8 @@ bgs_status bgs_route_reverse(bgs_ctx* ctx, void* stream) {
   CKS(ctx->tr->alltoallv(ctx, ctx->acc.p, ctx->recv_cnt.data(), ctx->recv_off.data(), ctx->rev.p,
                          ctx->send_cnt.data(), ctx->send_off.data(), sizeof(Acc), s));
   if (ctx->F > 0) {
-    launch_gather_sum(P_<Acc>(ctx->rev), ctx->F, P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), M,
-                      P_<int64_t>(ctx->send_base), P_<Acc>(ctx->accl), s);
+    launch_gather_sum(P_<Acc>(ctx->rev), ctx->F, nullptr, P_<uint8_t>(ctx->dest_mask),
+                      P_<uint32_t>(ctx->block_counts), M, P_<int64_t>(ctx->send_base), P_<Acc>(ctx->accl), s);
     CKS(launched(ctx));
   }
   ctx->acc_local = P_<Acc>(ctx->accl);
@@ -1254,6 +1351,474 @@ bgs_status bgs_view_step_host(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_ca
   CK(host_sync(ctx, as_stream(stream)));
   return BGS_OK;
 }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// NEXT-2: the batched step.  B views of one training batch ("a
+// mini-batch of B cameras") in ONE call: each view runs on an internal view slot (its own arena
+// and stream, like a ctx per view in flight), the host reads sizes ONCE per batch (the projection
+// counters and, at world > 1, the exchanged counts), and at world > 1 the batch makes one tile-cost
+// all-reduce, one count exchange, ONE record all-to-all and ONE reverse all-to-all ("the
+// batch's records concatenated into one exchange") instead of four collectives per view.
+// BGS_GRAPH: everything after the host read is recorded as one CUDA graph (re-captured per batch,
+// the executable updated in place) and launched with one call.
+// ---------------------------------------------------------------------------------------
+namespace {
+
+constexpr int kMaxBatch = 16;
+
+struct BatchState {
+  std::vector<bgs_ctx*> slots;
+  std::vector<cudaStream_t> streams, gstreams;  // per slot: eager work / graph-capture work
+  std::vector<cudaEvent_t> done, gdone;
+  cudaEvent_t fork = nullptr, gfork = nullptr;
+  cudaStream_t cap = nullptr;                    // capture origin
+  cudaGraphExec_t exec = nullptr;
+  DevBuf pairs, tot_send, tot_recv;              // [B][T] int32, [M][B] int64 x 2
+  int64_t* h = nullptr;                          // pinned host staging
+  size_t h_words = 0;
+  int64_t graph_launches = 0, graph_instantiations = 0, graph_fallbacks = 0, batches = 0;
+  bool graph_unsupported = false;  // a capture failed for another reason than arena growth: stay eager
+};
+
+void destroy_batch(bgs_ctx* c) {
+  BatchState* bs = c->batch;
+  if (!bs) return;
+  for (bgs_ctx* sl : bs->slots) {
+    sl->tr.reset();
+    bgs_ctx_destroy(sl);
+  }
+  for (auto v : {&bs->streams, &bs->gstreams})
+    for (cudaStream_t st : *v) cudaStreamDestroy(st);
+  for (auto v : {&bs->done, &bs->gdone})
+    for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  if (bs->fork) cudaEventDestroy(bs->fork);
+  if (bs->gfork) cudaEventDestroy(bs->gfork);
+  if (bs->cap) cudaStreamDestroy(bs->cap);
+  if (bs->exec) cudaGraphExecDestroy(bs->exec);
+  for (DevBuf* b : {&bs->pairs, &bs->tot_send, &bs->tot_recv})
+    if (b->p) cudaFree(b->p);
+  if (bs->h) cudaFreeHost(bs->h);
+  delete bs;
+  c->batch = nullptr;
+}
+
+bgs_status batch_prepare(bgs_ctx* ctx, int B) {
+  if (!ctx->batch) {
+    ctx->batch = new BatchState();
+    CK(cudaEventCreateWithFlags(&ctx->batch->fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->batch->gfork, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&ctx->batch->cap, cudaStreamNonBlocking));
+  }
+  BatchState& bs = *ctx->batch;
+  while (int(bs.slots.size()) < B) {
+    auto* c = new bgs_ctx();
+    c->rank = ctx->rank;
+    c->world = ctx->world;
+    c->device = ctx->device;
+    bs.slots.push_back(c);  // owned by the batch from here on (destroy_batch frees it)
+    if (ctx_alloc_common(c) != BGS_OK) return fail(ctx, BGS_ERR_CUDA, "batch view slot", c->err.c_str());
+    c->tr = ctx->tr;  // per-view collectives of a slot (a12 at world > 1) go through the parent's transport
+    cudaStream_t st, gst;
+    cudaEvent_t e, ge;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    bs.streams.push_back(st);
+    CK(cudaStreamCreateWithFlags(&gst, cudaStreamNonBlocking));
+    bs.gstreams.push_back(gst);
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    bs.done.push_back(e);
+    CK(cudaEventCreateWithFlags(&ge, cudaEventDisableTiming));
+    bs.gdone.push_back(ge);
+  }
+  const size_t words = size_t(kMaxWorld) * kMaxBatch * 8 + 64;
+  if (bs.h_words < words) {
+    if (bs.h) CK(cudaFreeHost(bs.h));
+    bs.h = nullptr;
+    CK(cudaMallocHost(&bs.h, words * sizeof(int64_t)));
+    bs.h_words = words;
+  }
+  return BGS_OK;
+}
+
+// fork: streams[0..B) wait for `from`; join: `to` waits for every stream's last work
+bgs_status fork_streams(bgs_ctx* ctx, cudaEvent_t ev, cudaStream_t from, const std::vector<cudaStream_t>& st, int B) {
+  CK(cudaEventRecord(ev, from));
+  for (int b = 0; b < B; ++b) CK(cudaStreamWaitEvent(st[b], ev, 0));
+  return BGS_OK;
+}
+bgs_status join_streams(bgs_ctx* ctx, const std::vector<cudaEvent_t>& ev, const std::vector<cudaStream_t>& st,
+                        cudaStream_t to, int B) {
+  for (int b = 0; b < B; ++b) {
+    CK(cudaEventRecord(ev[b], st[b]));
+    CK(cudaStreamWaitEvent(to, ev[b], 0));
+  }
+  return BGS_OK;
+}
+
+// a3 + a4 for the whole batch at world > 1 (the counterpart of bgs_route): one all-reduce of the
+// B x T tile pair counts, one exchange of the B x M per-destination totals, the ONE host read of the
+// batch (projection counters, totals, owner runs), then one grouped all-to-all of every view's
+// records.  All on stream s, after the slots' projections were joined into it.
+bgs_status batch_route(bgs_ctx* ctx, int B, cudaStream_t s) {
+  BatchState& bs = *ctx->batch;
+  const int M = ctx->world;
+  const int T = bs.slots[0]->T;
+  for (int b = 1; b < B; ++b)
+    if (bs.slots[b]->T != T || bs.slots[b]->cam.TX != bs.slots[0]->cam.TX)
+      return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "batch views must share the image size (one tile grid)");
+  if (T > 16384) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "world > 1 supports at most 16384 tiles");
+  CKS(ensure(ctx, bs.pairs, size_t(B) * T * 4));
+  CKS(ensure(ctx, bs.tot_send, size_t(M) * B * 8));
+  CKS(ensure(ctx, bs.tot_recv, size_t(M) * B * 8));
+  int32_t* pairs = P_<int32_t>(bs.pairs);
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    launch_tile_costs(P_<int32_t>(sl->tile_diff), sl->cam.TX, sl->cam.TY, pairs + size_t(b) * T, s);
+    CKS(launched(ctx));
+  }
+  CKS(ctx->tr->allreduce_i32(ctx, pairs, int64_t(B) * T, s));  // collective 1 of the batch
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    const int64_t cap = std::max<int64_t>(sl->n_local, 1);  // F is on the device until the host read
+    const int64_t nb = (cap + kRouteBlock - 1) / kRouteBlock;
+    CKS(ensure(sl, sl->owner, size_t(T) * 4));
+    CKS(ensure(sl, sl->runinfo, 64 + size_t(M + 1) * 8));
+    CKS(ensure(sl, sl->dest_mask, size_t(cap)));
+    CKS(ensure(sl, sl->block_counts, size_t(nb) * M * 4));
+    CKS(ensure(sl, sl->totals, size_t(M) * 8));
+    CKS(ensure(sl, sl->send_base, size_t(M) * 8));
+    int32_t* run = P_<int32_t>(sl->runinfo);
+    long long* pown = reinterpret_cast<long long*>(P_<char>(sl->runinfo) + 64);
+    launch_owner_map(pairs + size_t(b) * T, T, M, P_<int32_t>(sl->owner), run, pown, nullptr, s);
+    const unsigned long long* F_dev = P_<unsigned long long>(sl->counters) + C_F;
+    launch_dest_count(P_<Rec>(sl->recs), cap, F_dev, P_<int32_t>(sl->owner), sl->cam.TX, M, P_<uint8_t>(sl->dest_mask),
+                      P_<uint32_t>(sl->block_counts), s);
+    launch_block_scan(P_<uint32_t>(sl->block_counts), cap, F_dev, M, P_<unsigned long long>(sl->totals), s);
+    CKS(launched(ctx, 3));
+    // totals of view b for destination d -> tot_send[d B + b]
+    CK(cudaMemcpy2DAsync(P_<int64_t>(bs.tot_send) + b, size_t(B) * 8, sl->totals.p, 8, 8, size_t(M),
+                         cudaMemcpyDeviceToDevice, s));
+  }
+  CKS(ctx->tr->alltoall_n(ctx, P_<int64_t>(bs.tot_send), P_<int64_t>(bs.tot_recv), B, s));  // collective 2
+  // the one host read of the batch
+  int64_t* h = bs.h;  // [0, MB) send, [MB, 2MB) recv, then per view: run (M int64 = 2M int32), pown (M + 1)
+  const size_t MB = size_t(M) * B;
+  CK(cudaMemcpyAsync(h, bs.tot_send.p, MB * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + MB, bs.tot_recv.p, MB * 8, cudaMemcpyDeviceToHost, s));
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    int64_t* hb = h + 2 * MB + size_t(b) * (2 * M + 1);
+    CK(cudaMemcpyAsync(hb, sl->runinfo.p, size_t(2 * M) * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hb + M, P_<char>(sl->runinfo) + 64, size_t(M + 1) * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamWaitEvent(s, sl->ev_counters, 0));  // the slot's projection counters reached the host
+  }
+  CK(host_sync(ctx, s));
+  int64_t* hbase = h + 2 * MB + size_t(B) * (2 * M + 1);  // send_base staging, B x M
+  std::vector<const void*> sends(B);
+  std::vector<void*> recvs(B);
+  std::vector<int64_t> scnt(MB), soff(MB), rcnt(MB), roff(MB);
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    project_finish(sl);
+    const int64_t* hb = h + 2 * MB + size_t(b) * (2 * M + 1);
+    const int32_t* hrun = reinterpret_cast<const int32_t*>(hb);
+    sl->t_begin = hrun[2 * ctx->rank];
+    sl->t_end = hrun[2 * ctx->rank + 1];
+    sl->P = hb[M + ctx->rank];
+    sl->send_cnt.assign(M, 0);
+    sl->recv_cnt.assign(M, 0);
+    sl->send_off.assign(M, 0);
+    sl->recv_off.assign(M, 0);
+    int64_t D = 0, R = 0;
+    for (int d = 0; d < M; ++d) {
+      sl->send_cnt[d] = h[size_t(d) * B + b];
+      sl->recv_cnt[d] = h[MB + size_t(d) * B + b];
+      sl->send_off[d] = D;
+      sl->recv_off[d] = R;
+      D += sl->send_cnt[d];
+      R += sl->recv_cnt[d];
+      scnt[size_t(b) * M + d] = sl->send_cnt[d];
+      soff[size_t(b) * M + d] = sl->send_off[d];
+      rcnt[size_t(b) * M + d] = sl->recv_cnt[d];
+      roff[size_t(b) * M + d] = sl->recv_off[d];
+      hbase[size_t(b) * M + d] = sl->send_off[d];
+    }
+    if (D != [&] { int64_t c = 0; for (int d = 0; d < M; ++d) c += sl->send_cnt[d]; return c; }() || sl->F < 0)
+      return fail(ctx, BGS_ERR_INTERNAL, "batch route: inconsistent counts");
+    sl->D = D;
+    sl->R = R;
+    CKS(ensure(sl, sl->send, size_t(std::max<int64_t>(D, 1)) * sizeof(Rec)));
+    CKS(ensure(sl, sl->recvbuf, size_t(std::max<int64_t>(R, 1)) * sizeof(Rec)));
+    CK(cudaMemcpyAsync(sl->send_base.p, hbase + size_t(b) * M, size_t(M) * 8, cudaMemcpyHostToDevice, s));
+    if (sl->F > 0) {
+      launch_pack(P_<Rec>(sl->recs), sl->F, nullptr, P_<uint8_t>(sl->dest_mask), P_<uint32_t>(sl->block_counts), M,
+                  P_<int64_t>(sl->send_base), P_<Rec>(sl->send), s);
+      CKS(launched(ctx));
+    }
+    sends[b] = sl->send.p;
+    recvs[b] = sl->recvbuf.p;
+  }
+  CKS(ctx->tr->alltoallv_batch(ctx, B, sends.data(), scnt.data(), soff.data(), recvs.data(), rcnt.data(),
+                               roff.data(), sizeof(Rec), s));  // collective 3: ONE exchange of the batch
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    sl->recv = P_<Rec>(sl->recvbuf);
+    sl->stage = 2;
+  }
+  return BGS_OK;
+}
+
+// a10 for the whole batch at world > 1: ONE grouped all-to-all of every view's accumulators back
+// along the transposed counts, then each view's owner-ordered gather-sum.
+bgs_status batch_reverse(bgs_ctx* ctx, int B, cudaStream_t s) {
+  BatchState& bs = *ctx->batch;
+  const int M = ctx->world;
+  const size_t MB = size_t(M) * B;
+  std::vector<const void*> sends(B);
+  std::vector<void*> recvs(B);
+  std::vector<int64_t> scnt(MB), soff(MB), rcnt(MB), roff(MB);
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    CKS(ensure(sl, sl->rev, size_t(std::max<int64_t>(sl->D, 1)) * sizeof(Acc)));
+    CKS(ensure(sl, sl->accl, size_t(std::max<int64_t>(sl->F, 1)) * sizeof(Acc)));
+    for (int d = 0; d < M; ++d) {
+      scnt[size_t(b) * M + d] = sl->recv_cnt[d];
+      soff[size_t(b) * M + d] = sl->recv_off[d];
+      rcnt[size_t(b) * M + d] = sl->send_cnt[d];
+      roff[size_t(b) * M + d] = sl->send_off[d];
+    }
+    sends[b] = sl->acc.p;
+    recvs[b] = sl->rev.p;
+  }
+  CKS(ctx->tr->alltoallv_batch(ctx, B, sends.data(), scnt.data(), soff.data(), recvs.data(), rcnt.data(),
+                               roff.data(), sizeof(Acc), s));  // collective 4
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    if (sl->F > 0) {
+      launch_gather_sum(P_<Acc>(sl->rev), sl->F, nullptr, P_<uint8_t>(sl->dest_mask), P_<uint32_t>(sl->block_counts),
+                        M, P_<int64_t>(sl->send_base), P_<Acc>(sl->accl), s);
+      CKS(launched(ctx));
+    }
+    sl->acc_local = P_<Acc>(sl->accl);
+    sl->stage = 6;
+  }
+  return BGS_OK;
+}
+
+// the view's Cull column: the caller's, else the slot's scratch (sized before the batch runs)
+uint32_t* slot_cull(bgs_ctx* sl, const bgs_batch_view& v) {
+  return v.cull_out ? v.cull_out : P_<uint32_t>(sl->scr_n);
+}
+
+// a5..a9 (+ a10 at world 1, a11, a12) of view slot b on stream st, everything after the sizes are
+// known.  part 0: all of it at world 1; at world > 1 part 1 = a5..a9, part 2 = a11 (a10 and a12 run
+// batched / serialised on the parent stream).
+bgs_status slot_post(bgs_ctx* sl, const bgs_gaussians* g, const bgs_batch_view& v, uint32_t flags,
+                     const bgs_gaussian_grads* grads, const bgs_importance_out* imp, cudaStream_t st, int part) {
+  if (part != 2) {
+    CKS(bgs_sort_tiles(sl, st));
+    CKS(bgs_raster_fwd(sl, flags, v.rgb, v.t_final, v.n_contrib, st));
+    if (v.dL_drgb) CKS(bgs_raster_bwd(sl, v.dL_drgb, v.t_final, v.n_contrib, st));
+    if (part == 1) return BGS_OK;
+    CKS(bgs_route_reverse(sl, st));
+  }
+  if (v.dL_drgb && grads) CKS(bgs_project_bwd(sl, g, &v.cam, grads, st));
+  if (part == 0 && imp)
+    CKS(bgs_importance(sl, g->n_local, v.radius_out, nullptr, nullptr, imp->mass_num, imp->mass_den, imp->s,
+                       imp->c_rad, imp->c_vis, slot_cull(sl, v), st));
+  return BGS_OK;
+}
+
+void clear_capture(bgs_ctx* ctx, int B) {
+  for (int b = 0; b < B; ++b) ctx->batch->slots[b]->capturing = false;
+  ctx->capturing = false;
+}
+
+// world 1, BGS_GRAPH: record the post-read part of all B views as one graph (slots forked from the
+// capture stream), update the executable in place (or instantiate it), launch it on s.  Returns
+// BGS_OK with *ran = false when the capture had to be abandoned (an arena must grow first, or a
+// launch is not capturable): the caller then runs the same work eagerly.
+bgs_status batch_graph(bgs_ctx* ctx, int B, const bgs_gaussians* g, const bgs_batch_view* views, uint32_t flags,
+                       const bgs_gaussian_grads* grads, const bgs_importance_out* imp, cudaStream_t s, bool* ran) {
+  BatchState& bs = *ctx->batch;
+  *ran = false;
+  if (bs.graph_unsupported) return BGS_OK;
+  std::vector<int> parity(B);
+  for (int b = 0; b < B; ++b) parity[b] = bs.slots[b]->imp_parity;
+  CK(cudaStreamBeginCapture(bs.cap, cudaStreamCaptureModeThreadLocal));
+  bgs_status st = BGS_OK;
+  for (int b = 0; b < B; ++b) {
+    bs.slots[b]->capturing = true;
+    bs.slots[b]->grew_in_capture = false;
+  }
+  st = fork_streams(ctx, bs.gfork, bs.cap, bs.gstreams, B);
+  for (int b = 0; b < B && st == BGS_OK; ++b) {
+    st = slot_post(bs.slots[b], g, views[b], flags, grads, imp, bs.gstreams[b], 0);
+    if (st != BGS_OK) ctx->err = bs.slots[b]->err;
+  }
+  if (st == BGS_OK) st = join_streams(ctx, bs.gdone, bs.gstreams, bs.cap, B);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(bs.cap, &graph);
+  clear_capture(ctx, B);
+  if (st != BGS_OK || ec != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    // streams that joined the failed capture are back to normal after EndCapture; any error the
+    // failed capture left is cleared so the eager run starts clean
+    (void)cudaGetLastError();
+    bool grew = false;
+    for (int b = 0; b < B; ++b) {
+      grew |= bs.slots[b]->grew_in_capture;
+      bs.slots[b]->imp_parity = parity[b];  // the captured importance calls never ran
+      bs.slots[b]->err.clear();
+    }
+    ctx->err.clear();
+    if (!grew) bs.graph_unsupported = true;
+    ++bs.graph_fallbacks;
+    return BGS_OK;
+  }
+  bool updated = false;
+  if (bs.exec) {
+    cudaGraphExecUpdateResultInfo info{};
+    updated = cudaGraphExecUpdate(bs.exec, graph, &info) == cudaSuccess;
+    if (!updated) {
+      (void)cudaGetLastError();
+      cudaGraphExecDestroy(bs.exec);
+      bs.exec = nullptr;
+    }
+  }
+  if (!bs.exec) {
+    const cudaError_t ei = cudaGraphInstantiate(&bs.exec, graph, 0);
+    if (ei != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      bs.exec = nullptr;
+      return fail(ctx, BGS_ERR_CUDA, "cudaGraphInstantiate", cudaGetErrorString(ei));
+    }
+    ++bs.graph_instantiations;
+  }
+  cudaGraphDestroy(graph);
+  CK(cudaGraphLaunch(bs.exec, s));
+  ++bs.graph_launches;
+  for (int b = 0; b < B; ++b) ctx->launches += bs.slots[b]->launches, bs.slots[b]->launches = 0;
+  *ran = true;
+  return BGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+bgs_status bgs_batch_step(bgs_ctx* ctx, int32_t n_views, const bgs_gaussians* g, const bgs_lod_gate* gate,
+                          uint32_t flags, const bgs_batch_view* views, const bgs_gaussian_grads* grads,
+                          const bgs_importance_out* imp, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_stream(ctx, stream));
+  CKS(check_gaussians(ctx, g));
+  const int B = n_views;
+  if (B < 1 || B > kMaxBatch || !views) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "n_views must be in [1, 16]");
+  for (int b = 0; b < B; ++b) {
+    const bgs_batch_view& v = views[b];
+    if ((g->n_local > 0 && !v.radius_out) || !v.rgb || !v.t_final || !v.n_contrib)
+      return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "batch view: radius / rgb / t_final / n_contrib pointer is NULL");
+  }
+  if (imp && (!imp->s || !imp->c_rad || !imp->c_vis))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "importance s / c_rad / c_vis must be non-NULL");
+  const bool graph = (flags & BGS_GRAPH) != 0;
+  if (graph && ctx->world > 1 && !ctx->tr->capturable())
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "BGS_GRAPH at world > 1 needs the NCCL transport");
+  CKS(batch_prepare(ctx, B));
+  BatchState& bs = *ctx->batch;
+  cudaStream_t s = as_stream(stream);
+  if (imp)
+    for (int b = 0; b < B; ++b)
+      if (!views[b].cull_out)
+        CKS(ensure(bs.slots[b], bs.slots[b]->scr_n, size_t((g->n_local + 31) / 32 + 1) * 4));
+  const uint32_t vflags = (flags & BGS_NO_COLOR) | (imp ? BGS_IMPORTANCE : 0u);
+  ++bs.batches;
+  // a1 + a2 of every view on its slot stream
+  CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
+  for (int b = 0; b < B; ++b) {
+    bgs_ctx* sl = bs.slots[b];
+    sl->err.clear();
+    const bgs_status st = project_enqueue(sl, g, &views[b].cam, gate, views[b].cull_column, vflags,
+                                          views[b].radius_out, bs.streams[b]);
+    if (st != BGS_OK) return fail(ctx, st, "batch view projection", sl->err.c_str());
+  }
+  CKS(join_streams(ctx, bs.done, bs.streams, s, B));
+  if (ctx->world == 1) {
+    // the one host read of the batch: every view's projection counters
+    for (int b = 0; b < B; ++b) CK(cudaEventSynchronize(bs.slots[b]->ev_counters));
+    ++ctx->host_syncs;
+    for (int b = 0; b < B; ++b) {
+      project_finish(bs.slots[b]);
+      CKS(bgs_route(bs.slots[b], nullptr, nullptr, nullptr, s));  // identity at world 1 (no work)
+    }
+    bool ran = false;
+    if (graph) CKS(batch_graph(ctx, B, g, views, vflags, grads, imp, s, &ran));
+    if (!ran) {
+      CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
+      for (int b = 0; b < B; ++b) {
+        const bgs_status st = slot_post(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], 0);
+        if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
+      }
+      CKS(join_streams(ctx, bs.done, bs.streams, s, B));
+    }
+  } else {
+    CKS(batch_route(ctx, B, s));
+    CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
+    for (int b = 0; b < B; ++b) {
+      const bgs_status st = slot_post(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], 1);
+      if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
+    }
+    CKS(join_streams(ctx, bs.done, bs.streams, s, B));
+    CKS(batch_reverse(ctx, B, s));
+    CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
+    for (int b = 0; b < B; ++b) {
+      const bgs_status st = slot_post(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], 2);
+      if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
+    }
+    CKS(join_streams(ctx, bs.done, bs.streams, s, B));
+    if (imp)  // a12's selection rounds are collectives: serialised on the parent stream, view order
+      for (int b = 0; b < B; ++b) {
+        bgs_ctx* sl = bs.slots[b];
+        const bgs_status st = bgs_importance(sl, g->n_local, views[b].radius_out, nullptr, nullptr, imp->mass_num,
+                                             imp->mass_den, imp->s, imp->c_rad, imp->c_vis, slot_cull(sl, views[b]), s);
+        if (st != BGS_OK) return fail(ctx, st, "batch view importance", sl->err.c_str());
+      }
+  }
+  // the slots' launches and collectives are the batch's
+  for (int b = 0; b < B; ++b) {
+    ctx->launches += bs.slots[b]->launches;
+    bs.slots[b]->launches = 0;
+    ctx->collectives += bs.slots[b]->collectives;
+    bs.slots[b]->collectives = 0;
+    ctx->host_syncs += bs.slots[b]->host_syncs;
+    bs.slots[b]->host_syncs = 0;
+  }
+  return BGS_OK;
+}
+
+bgs_status bgs_batch_view_ctx(bgs_ctx* ctx, int32_t b, bgs_ctx** out) {
+  if (!ctx || !out) return BGS_ERR_INVALID_ARGUMENT;
+  if (!ctx->batch || b < 0 || b >= int32_t(ctx->batch->slots.size()))
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "no such batch view slot (run bgs_batch_step first)");
+  *out = ctx->batch->slots[b];
+  return BGS_OK;
+}
+
+bgs_status bgs_batch_stats(bgs_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return BGS_ERR_INVALID_ARGUMENT;
+  const BatchState* bs = ctx->batch;
+  const int64_t v[6] = {ctx->host_syncs, ctx->collectives, bs ? bs->batches : 0, bs ? bs->graph_launches : 0,
+                        bs ? bs->graph_instantiations : 0, bs ? bs->graph_fallbacks : 0};
+  std::memcpy(out, v, sizeof v);
+  return BGS_OK;
+}
+
+}  // extern "C"
+
+
+extern "C" {
 
 // ---------------------------------------------------------------------------------------
 // NEXT-4 supervision: Eq.7 photometric loss + gradient on the owned tiles, Eq.8 regulariser
