@@ -512,7 +512,9 @@ def batch_step_timing(args, B, g, cams, gate, cull_of, per, dl, grads, batch, ba
     out = {}
     for name, flags in (("eager", 0), ("graph", B.BGS_GRAPH)):
         with torch.cuda.stream(stream):
-            for i in range(args.warmup + 1):
+            # every batch of the camera cycle once (grows the slot arenas to steady state, as the
+            # per-view contexts' warm-up pass does), then the warm-up steps
+            for i in range(n_arr + args.warmup + 1):
                 B.bgs_batch_step(bctx, g, arrs[i % n_arr], gate, flags, grads, None, stream)
             torch.cuda.synchronize()
             if world > 1:

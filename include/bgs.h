@@ -254,46 +254,6 @@ bgs_status bgs_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, const 
                                     const bgs_gaussian_grads* grads, const bgs_importance_out* importance,
                                     void* stream);
 
-/* ---- NEXT-2: the batched step (SURVEY §8(f); P:216, P:342 "a mini-batch of B cameras"; S:514) ----
- * One view of a batch: the camera by value and the caller's per-view device buffers (as for
- * bgs_view_step).  cull_column and dL_drgb are nullable (no Cull column / forward only). */
-typedef struct {
-  bgs_camera cam;
-  const uint32_t* cull_column;
-  int32_t* radius_out;  /* device i32 [n_local] */
-  float* rgb;           /* device f32 [3][H][W] (owned tiles written) */
-  float* t_final;       /* device f32 [H][W] */
-  int32_t* n_contrib;   /* device i32 [H][W] */
-  const float* dL_drgb; /* device f32 [3][H][W] or NULL */
-  uint32_t* cull_out;   /* device u32 [ceil(n_local/32)]: this view's Cull column (a12), or NULL (not kept) */
-} bgs_batch_view;
-
-#define BGS_GRAPH 4u /* bgs_batch_step: record the post-sizing part of the batch as one CUDA graph */
-
-/* a1..a11 (+ a12 when importance != NULL) for n_views (1..16) views in ONE call.  Each view runs on
- * an internal view slot (own arena and stream, forked from / joined back into `stream`), so the
- * views of the batch overlap.  The host reads sizes ONCE per batch (HOST-SYNC once: every view's
- * projection counters and, at world > 1, the exchanged per-destination counts); at world > 1 the
- * batch issues ONE all-reduce of the B x T tile pair counts, ONE exchange of the B x M counts, ONE
- * grouped all-to-all of all views' records and ONE reverse all-to-all (+ a12's rounds per view)
- * instead of four collectives per view.  Views must share the image size.  Results equal B
- * bgs_view_step calls (pixels, n_contrib, w, a, routing bit-identical; gradients up to fp32 atomic
- * order).  grads and importance's s, c_rad, c_vis are accumulated by every view (reductions); each
- * view's Cull column goes to its own cull_out (importance->cull_out is not used).  flags:
- * BGS_NO_COLOR, BGS_GRAPH (world 1 or NCCL: everything after the host read is captured into a CUDA
- * graph, its executable updated in place each batch and launched once; when an arena must grow
- * the batch runs eagerly instead and the next one is captured).  The views' intermediates stay in
- * the slots until the next batch (bgs_batch_view_ctx). */
-bgs_status bgs_batch_step(bgs_ctx* ctx, int32_t n_views, const bgs_gaussians* g, const bgs_lod_gate* gate,
-                          uint32_t flags, const bgs_batch_view* views, const bgs_gaussian_grads* grads,
-                          const bgs_importance_out* importance, void* stream);
-/* Borrowed handle of view slot b of the last batch (bgs_query / bgs_debug_buffer on that view);
- * valid until ctx is destroyed; must not be passed to any other call. */
-bgs_status bgs_batch_view_ctx(bgs_ctx* ctx, int32_t b, bgs_ctx** out);
-/* out (host i64 [6]): host syncs, collectives issued, batches, graph launches, graph
- * instantiations, graph captures abandoned (eager fallback), all since ctx creation. */
-bgs_status bgs_batch_stats(bgs_ctx* ctx, int64_t* out);
-
 /* Per-stage device timing of bgs_view_step / bgs_train_view_step: when enabled, CUDA events are
  * recorded on the working stream between its stages; bgs_stage_times waits for the last one and
  * writes the elapsed ms of the most recent step: [project, route, sort, raster_fwd, loss,
@@ -422,6 +382,51 @@ bgs_status bgs_train_view_step_host_async(bgs_ctx* ctx, const bgs_gaussians* g, 
                                           float batch_inv, float beta, double* loss_host,
                                           const bgs_gaussian_grads* grads, const bgs_importance_out* importance,
                                           void* stream);
+
+/* ---- NEXT-2: the batched step (SURVEY §8(f); P:216, P:342 "a mini-batch of B cameras"; S:514) ----
+ * One view of a batch: the camera by value and the caller's per-view device buffers (as for
+ * bgs_view_step).  cull_column and dL_drgb are nullable (no Cull column / forward only). */
+typedef struct {
+  bgs_camera cam;
+  const uint32_t* cull_column;
+  int32_t* radius_out;  /* device i32 [n_local] */
+  float* rgb;           /* device f32 [3][H][W] (owned tiles written) */
+  float* t_final;       /* device f32 [H][W] */
+  int32_t* n_contrib;   /* device i32 [H][W] */
+  const float* dL_drgb; /* device f32 [3][H][W] or NULL */
+  uint32_t* cull_out;   /* device u32 [ceil(n_local/32)]: this view's Cull column (a12), or NULL (not kept) */
+  const bgs_supervision* sup; /* host struct or NULL: supervised view (Eq.7-8 as bgs_train_view_step;
+                                 dL_drgb is then ignored and dL_scratch receives this view's dL/dC) */
+  float* dL_scratch;          /* device f32 [3][H][W], required with sup */
+} bgs_batch_view;
+
+#define BGS_GRAPH 4u /* bgs_batch_step: record the post-sizing part of the batch as one CUDA graph */
+
+/* a1..a11 (+ a12 when importance != NULL) for n_views (1..16) views in ONE call.  Each view runs on
+ * an internal view slot (own arena and stream, forked from / joined back into `stream`), so the
+ * views of the batch overlap.  The host reads sizes ONCE per batch (HOST-SYNC once: every view's
+ * projection counters and, at world > 1, the exchanged per-destination counts); at world > 1 the
+ * batch issues ONE all-reduce of the B x T tile pair counts, ONE exchange of the B x M counts, ONE
+ * grouped all-to-all of all views' records and ONE reverse all-to-all (+ a12's rounds per view)
+ * instead of four collectives per view.  Views must share the image size.  Results equal B
+ * bgs_view_step calls (pixels, n_contrib, w, a, routing bit-identical; gradients up to fp32 atomic
+ * order).  grads and importance's s, c_rad, c_vis are accumulated by every view (reductions); each
+ * view's Cull column goes to its own cull_out (importance->cull_out is not used).  flags:
+ * BGS_NO_COLOR, BGS_GRAPH (world 1; ignored at world > 1: everything after the host read is
+ * captured into a CUDA graph, its executable updated in place each batch and launched once; when an
+ * arena must grow the batch runs eagerly instead and the next one is captured).  The views' intermediates stay in
+ * the slots until the next batch (bgs_batch_view_ctx). */
+bgs_status bgs_batch_step(bgs_ctx* ctx, int32_t n_views, const bgs_gaussians* g, const bgs_lod_gate* gate,
+                          uint32_t flags, const bgs_batch_view* views, const bgs_gaussian_grads* grads,
+                          const bgs_importance_out* importance, void* stream);
+/* Borrowed handle of view slot b of the last batch: bgs_query / bgs_debug_buffer on that view, and
+ * bgs_densify_accumulate of that view (on the batch's stream, before the next batch); valid until
+ * ctx is destroyed; must not be passed to any other call (nor destroyed). */
+bgs_status bgs_batch_view_ctx(bgs_ctx* ctx, int32_t b, bgs_ctx** out);
+/* out (host i64 [6]): host syncs, collectives issued, batches, graph launches, graph
+ * instantiations, graph captures abandoned (eager fallback), all since ctx creation. */
+bgs_status bgs_batch_stats(bgs_ctx* ctx, int64_t* out);
+
 
 /* ---------------------------------------------------------------------------------------
  * NEXT-3: optimizer step on the owned shard ("each GPU stores only its

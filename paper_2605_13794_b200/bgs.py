@@ -50,7 +50,7 @@ class bgs_camera(C.Structure):
 class bgs_batch_view(C.Structure):
     _fields_ = [("cam", bgs_camera), ("cull_column", C.c_void_p), ("radius_out", C.c_void_p), ("rgb", C.c_void_p),
                 ("t_final", C.c_void_p), ("n_contrib", C.c_void_p), ("dL_drgb", C.c_void_p),
-                ("cull_out", C.c_void_p)]
+                ("cull_out", C.c_void_p), ("sup", C.c_void_p), ("dL_scratch", C.c_void_p)]
 
 
 class bgs_gaussians(C.Structure):
@@ -523,9 +523,14 @@ def bgs_train_view_step_host_async(ctx: Context, g: GaussianPlanes, cam: bgs_cam
 
 
 def batch_view(cam: bgs_camera, radius_out, rgb, t_final, n_contrib, dL_drgb=None, cull_column=None,
-               cull_out=None) -> bgs_batch_view:
-    return bgs_batch_view(cam, _ptr(cull_column), _ptr(radius_out), _ptr(rgb), _ptr(t_final), _ptr(n_contrib),
-                          _ptr(dL_drgb), _ptr(cull_out))
+               cull_out=None, sup: "bgs_supervision | None" = None, dL_scratch=None) -> bgs_batch_view:
+    """One view of bgs_batch_step.  sup (a bgs_supervision, kept alive by the returned struct)
+    makes the view supervised: Eq.7-8 write its dL/dC into dL_scratch."""
+    v = bgs_batch_view(cam, _ptr(cull_column), _ptr(radius_out), _ptr(rgb), _ptr(t_final), _ptr(n_contrib),
+                       _ptr(dL_drgb), _ptr(cull_out), C.cast(C.pointer(sup), C.c_void_p) if sup is not None else None,
+                       _ptr(dL_scratch))
+    v._sup = sup
+    return v
 
 
 def bgs_batch_step(ctx: Context, g: GaussianPlanes, views, gate=None, flags: int = 0, grads: GradPlanes | None = None,

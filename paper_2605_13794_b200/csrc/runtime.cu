@@ -100,6 +100,12 @@ inline cudaStream_t as_stream(void* stream) {
     if (e_ != cudaSuccess) return fail(ctx, BGS_ERR_CUDA, #call, cudaGetErrorString(e_)); \
   } while (0)
 
+#define CK_CTX(c, call)                                                              \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) return fail(c, BGS_ERR_CUDA, #call, cudaGetErrorString(e_)); \
+  } while (0)
+
 #define CKS(call)                                   \
   do {                                              \
     bgs_status s_ = (call);                         \
@@ -1611,20 +1617,38 @@ uint32_t* slot_cull(bgs_ctx* sl, const bgs_batch_view& v) {
   return v.cull_out ? v.cull_out : P_<uint32_t>(sl->scr_n);
 }
 
-// a5..a9 (+ a10 at world 1, a11, a12) of view slot b on stream st, everything after the sizes are
-// known.  part 0: all of it at world 1; at world > 1 part 1 = a5..a9, part 2 = a11 (a10 and a12 run
-// batched / serialised on the parent stream).
-bgs_status slot_post(bgs_ctx* sl, const bgs_gaussians* g, const bgs_batch_view& v, uint32_t flags,
-                     const bgs_gaussian_grads* grads, const bgs_importance_out* imp, cudaStream_t st, int part) {
-  if (part != 2) {
+// Phases of one view slot after the sizes are known (run on stream st).  World 1 runs them all per
+// slot on its own stream; world > 1 runs the collective ones (loss reductions, a10, a12) batched or
+// serialised on the parent stream, in view order on every rank.
+enum : uint32_t { PH_FWD = 1, PH_LOSS = 2, PH_BWD = 4, PH_REV = 8, PH_PBWD = 16, PH_IMP = 32, PH_ALL = 63 };
+
+bgs_status check_view_sup(bgs_ctx* ctx, const bgs_batch_view& v) {
+  if (!v.sup) return BGS_OK;
+  if (!v.sup->target || !v.sup->loss_out || !v.dL_scratch)
+    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "supervised batch view: target / loss_out / dL_scratch is NULL");
+  return BGS_OK;
+}
+
+bgs_status slot_phases(bgs_ctx* sl, const bgs_gaussians* g, const bgs_batch_view& v, uint32_t flags,
+                       const bgs_gaussian_grads* grads, const bgs_importance_out* imp, cudaStream_t st,
+                       uint32_t ph) {
+  const float* dL = v.sup ? v.dL_scratch : v.dL_drgb;
+  if (ph & PH_FWD) {
     CKS(bgs_sort_tiles(sl, st));
     CKS(bgs_raster_fwd(sl, flags, v.rgb, v.t_final, v.n_contrib, st));
-    if (v.dL_drgb) CKS(bgs_raster_bwd(sl, v.dL_drgb, v.t_final, v.n_contrib, st));
-    if (part == 1) return BGS_OK;
-    CKS(bgs_route_reverse(sl, st));
   }
-  if (v.dL_drgb && grads) CKS(bgs_project_bwd(sl, g, &v.cam, grads, st));
-  if (part == 0 && imp)
+  if ((ph & PH_LOSS) && v.sup) {  // NEXT-4 Eq.7 (+ Eq.8) writes this view's dL/dC
+    const bgs_supervision& sp = *v.sup;
+    CKS(bgs_loss_photo(sl, v.rgb, sp.target, sp.lambda, sp.batch_inv, v.dL_scratch, sp.loss_out, st));
+    if (sp.beta != 0.f && grads)
+      CKS(bgs_loss_scale(sl, g, sp.beta, grads, sp.loss_out + 3, st));
+    else
+      CK_CTX(sl, cudaMemsetAsync(sp.loss_out + 3, 0, 2 * sizeof(double), st));
+  }
+  if ((ph & PH_BWD) && dL) CKS(bgs_raster_bwd(sl, dL, v.t_final, v.n_contrib, st));
+  if (ph & PH_REV) CKS(bgs_route_reverse(sl, st));
+  if ((ph & PH_PBWD) && dL && grads) CKS(bgs_project_bwd(sl, g, &v.cam, grads, st));
+  if ((ph & PH_IMP) && imp)
     CKS(bgs_importance(sl, g->n_local, v.radius_out, nullptr, nullptr, imp->mass_num, imp->mass_den, imp->s,
                        imp->c_rad, imp->c_vis, slot_cull(sl, v), st));
   return BGS_OK;
@@ -1654,7 +1678,7 @@ bgs_status batch_graph(bgs_ctx* ctx, int B, const bgs_gaussians* g, const bgs_ba
   }
   st = fork_streams(ctx, bs.gfork, bs.cap, bs.gstreams, B);
   for (int b = 0; b < B && st == BGS_OK; ++b) {
-    st = slot_post(bs.slots[b], g, views[b], flags, grads, imp, bs.gstreams[b], 0);
+    st = slot_phases(bs.slots[b], g, views[b], flags, grads, imp, bs.gstreams[b], PH_ALL);
     if (st != BGS_OK) ctx->err = bs.slots[b]->err;
   }
   if (st == BGS_OK) st = join_streams(ctx, bs.gdone, bs.gstreams, bs.cap, B);
@@ -1716,16 +1740,17 @@ bgs_status bgs_batch_step(bgs_ctx* ctx, int32_t n_views, const bgs_gaussians* g,
   CKS(check_gaussians(ctx, g));
   const int B = n_views;
   if (B < 1 || B > kMaxBatch || !views) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "n_views must be in [1, 16]");
+  bool any_sup = false;
   for (int b = 0; b < B; ++b) {
     const bgs_batch_view& v = views[b];
     if ((g->n_local > 0 && !v.radius_out) || !v.rgb || !v.t_final || !v.n_contrib)
       return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "batch view: radius / rgb / t_final / n_contrib pointer is NULL");
+    CKS(check_view_sup(ctx, v));
+    any_sup |= v.sup != nullptr;
   }
   if (imp && (!imp->s || !imp->c_rad || !imp->c_vis))
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "importance s / c_rad / c_vis must be non-NULL");
-  const bool graph = (flags & BGS_GRAPH) != 0;
-  if (graph && ctx->world > 1 && !ctx->tr->capturable())
-    return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "BGS_GRAPH at world > 1 needs the NCCL transport");
+  const bool graph = (flags & BGS_GRAPH) != 0 && ctx->world == 1;
   CKS(batch_prepare(ctx, B));
   BatchState& bs = *ctx->batch;
   cudaStream_t s = as_stream(stream);
@@ -1758,33 +1783,35 @@ bgs_status bgs_batch_step(bgs_ctx* ctx, int32_t n_views, const bgs_gaussians* g,
     if (!ran) {
       CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
       for (int b = 0; b < B; ++b) {
-        const bgs_status st = slot_post(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], 0);
+        const bgs_status st = slot_phases(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], PH_ALL);
         if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
       }
       CKS(join_streams(ctx, bs.done, bs.streams, s, B));
     }
   } else {
     CKS(batch_route(ctx, B, s));
-    CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
-    for (int b = 0; b < B; ++b) {
-      const bgs_status st = slot_post(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], 1);
-      if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
-    }
-    CKS(join_streams(ctx, bs.done, bs.streams, s, B));
-    CKS(batch_reverse(ctx, B, s));
-    CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
-    for (int b = 0; b < B; ++b) {
-      const bgs_status st = slot_post(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], 2);
-      if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
-    }
-    CKS(join_streams(ctx, bs.done, bs.streams, s, B));
-    if (imp)  // a12's selection rounds are collectives: serialised on the parent stream, view order
+    // per-slot work on the slot streams; phases with collectives on s, view order (same on every rank)
+    auto par = [&](uint32_t ph) -> bgs_status {
+      CKS(fork_streams(ctx, bs.fork, s, bs.streams, B));
       for (int b = 0; b < B; ++b) {
-        bgs_ctx* sl = bs.slots[b];
-        const bgs_status st = bgs_importance(sl, g->n_local, views[b].radius_out, nullptr, nullptr, imp->mass_num,
-                                             imp->mass_den, imp->s, imp->c_rad, imp->c_vis, slot_cull(sl, views[b]), s);
-        if (st != BGS_OK) return fail(ctx, st, "batch view importance", sl->err.c_str());
+        const bgs_status st = slot_phases(bs.slots[b], g, views[b], vflags, grads, imp, bs.streams[b], ph);
+        if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
       }
+      return join_streams(ctx, bs.done, bs.streams, s, B);
+    };
+    auto ser = [&](uint32_t ph) -> bgs_status {
+      for (int b = 0; b < B; ++b) {
+        const bgs_status st = slot_phases(bs.slots[b], g, views[b], vflags, grads, imp, s, ph);
+        if (st != BGS_OK) return fail(ctx, st, "batch view", bs.slots[b]->err.c_str());
+      }
+      return BGS_OK;
+    };
+    CKS(par(PH_FWD));
+    if (any_sup) CKS(ser(PH_LOSS));  // the loss's image and sum all-reduces
+    CKS(par(PH_BWD));
+    CKS(batch_reverse(ctx, B, s));
+    CKS(par(PH_PBWD));
+    if (imp) CKS(ser(PH_IMP));  // a12's selection rounds are collectives
   }
   // the slots' launches and collectives are the batch's
   for (int b = 0; b < B; ++b) {

@@ -260,3 +260,76 @@ def test_batch_multirank_one_exchange(tiny_scene, world1, M):
     for r in range(M):
         gm[np.arange(r, n, M)] = res[r]["grads"]["mean_opac"][:len(range(r, n, M)), :3]
     assert np.abs(gm - d_mean).max() <= 2e-3 * np.abs(d_mean).max()
+
+
+def _sup_run(sc, cams, M, mode):
+    """Supervised views (NEXT-4 Eq.7-8 inside the batch): mode 'views' = bgs_train_view_step per
+    view (world 1), 'batch' = bgs_batch_step with supervised views (world M, in-process group)."""
+    import paper_2605_13794_b200.bgs as B
+    dev = "cuda:0"
+    tgts = [torch.from_numpy(S.target_image(256, 256, seed=40 + k)).to(dev) for k in range(NV)]
+    ctxs = B.Context.local_group(M, 0) if M > 1 else [B.Context(0, 1, 0)]
+    res = [None] * M
+    errs = []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream(dev)
+            with torch.cuda.stream(stream):
+                sh = sc.shard(r, M)
+                g = B.GaussianPlanes.from_scene(sh, dev)
+                grads = g.zeros_grads()
+                bufs = [_bufs(sh.n, 256, 256, dev) for _ in range(NV)]
+                losses = [torch.zeros(5, dtype=torch.float64, device=dev) for _ in range(NV)]
+                dls = [torch.zeros(3, 256, 256, device=dev) for _ in range(NV)]
+                sups = [B.supervision(tgts[k], 0.2, 1.0 / NV, 0.5, losses[k]) for k in range(NV)]
+                if mode == "views":
+                    for k in range(NV):
+                        b = bufs[k]
+                        B.bgs_train_view_step(ctxs[r], g, B.camera(cams[k]), None, None, 0, b["radius"], sups[k],
+                                              b["rgb"], b["T"], b["nc"], dls[k], grads, None, stream)
+                else:
+                    views = [B.batch_view(B.camera(cams[k]), bufs[k]["radius"], bufs[k]["rgb"], bufs[k]["T"],
+                                          bufs[k]["nc"], sup=sups[k], dL_scratch=dls[k]) for k in range(NV)]
+                    B.bgs_batch_step(ctxs[r], g, views, None, 0, grads, None, stream)
+                stream.synchronize()
+                res[r] = dict(loss=[x.cpu().numpy() for x in losses], dl=[x.cpu().numpy() for x in dls],
+                              grads={k: getattr(grads, k).cpu().numpy().astype(np.float64)
+                                     for k in ("mean_opac", "quat", "scale", "sh")}, n=sh.n)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(M)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for c in ctxs:
+        c.close()
+    if errs:
+        raise errs[0]
+    return res
+
+
+@pytest.mark.parametrize("M", [1, 2])
+def test_batch_supervised_equals_train_view_steps(tiny_scene, M):
+    """Supervised batch (Eq.7 + Eq.8 per view inside bgs_batch_step) == four bgs_train_view_step
+    calls: per-view loss terms within 1e-12 (world 1: bit-identical), dL/dC bit-identical on the
+    owned tiles (R36: the loss sees the full image at every M), gradients within atomic tolerance."""
+    cams = _cams()
+    ref = _sup_run(tiny_scene, cams, 1, "views")[0]
+    got = _sup_run(tiny_scene, cams, M, "batch")
+    n = tiny_scene.n
+    for k in range(NV):
+        for r in range(M):
+            np.testing.assert_allclose(got[r]["loss"][k], ref["loss"][k], rtol=1e-12, atol=1e-15)
+        if M == 1:
+            assert np.array_equal(got[0]["dl"][k], ref["dl"][k]), k
+    grads = {}
+    for key in ref["grads"]:
+        full = np.zeros_like(ref["grads"][key])
+        for r in range(M):
+            full[np.arange(r, n, M)] = got[r]["grads"][key][:len(range(r, n, M))]
+        grads[key] = full
+    _close_grads(grads, ref["grads"], f"supervised M={M}")
