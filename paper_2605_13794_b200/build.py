@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libbgs.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 SOURCES = ["runtime.cu", "project.cu", "sort.cu", "raster.cu", "project_bwd.cu", "route.cu", "importance.cu",
-           "layout.cu", "simplify.cu", "loss.cu", "adam.cu", "densify.cu"]
+           "layout.cu", "simplify.cu", "loss.cu", "adam.cu", "densify.cu", "bucket.cu"]
 # per-TU extra flags: the projection TU is pinned (no FMA contraction; IEEE div/sqrt are the
 # nvcc defaults) so that integer decisions match the oracle bit for bit (D2); the
 # simplification TU too (pinned fp64 ln of the race keys, R30; it also uses __d*_rn explicitly)

@@ -138,6 +138,16 @@ void launch_depth_range(const Rec* recv, int64_t n, unsigned long long* counters
 void launch_sort_passes(const SortArgs& a, int64_t P, cudaStream_t s, int64_t* launches, int key_bytes);
 void launch_ranges_fixup(const SortArgs& a, int64_t P, cudaStream_t s);
 void launch_tile_order(const uint2* ranges, int n_tiles, uint32_t* perm, cudaStream_t s);
+// bucket.cu: a5-a7 as a per-tile bucket sort.  tile_counts: pairs per tile (indexed by global tile,
+// the owned run [t_begin, t_end) is used); cursor: [t_end - t_begin] scratch.  Writes ranges, the
+// sorted 64-bit keys (f32 bits(depth) << 32 | gid) to keys[0] and the record indices to vals[0].
+// order: [t_end - t_begin] longest-first tile order (also the raster's tile_perm)
+void launch_bucket_sort(const SortArgs& a, const int32_t* tile_counts, uint32_t* cursor, uint32_t* order,
+                        cudaStream_t s, int64_t* launches);
+// Pairs per tile of a record set (rect coverage) for the tiles [t_lo, t_hi) (t_hi - t_lo <= 16384),
+// accumulated into counts[t - t_lo] (zeroed by the caller); n_dev (nullable): count on the device.
+void launch_tile_count(const Rec* recs, int64_t n_cap, const unsigned long long* n_dev, int TX, int t_lo, int t_hi,
+                       int32_t* counts, cudaStream_t s);
 // layout.cu: Morton permutation of a shard (keys/vals/digit_hist/pass_ctrl/status of `a` used as scratch)
 void launch_spatial_order(const float4* mean_opac, int64_t n, unsigned int* box, const SortArgs& a, uint32_t* perm,
                           cudaStream_t s, int64_t* launches);

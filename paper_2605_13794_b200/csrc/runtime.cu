@@ -66,7 +66,8 @@ struct bgs_ctx {
       send_base, send, recvbuf, keys[2], vals[2], digit_hist, pass_ctrl, status, ranges, acc, rev, accl, imp_state,
       imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask,
       loss_img, loss_part, loss_sums, scr_tgt, scr_loss, scr_in2,
-      scr_dlsup;  // supervised steps' dL/dC (never one of the host-upload double buffers)
+      scr_dlsup,  // supervised steps' dL/dC (never one of the host-upload double buffers)
+      bucket_cur;  // per-tile write cursors of the bucket sort
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
@@ -443,6 +444,13 @@ bgs_status check_ctx(bgs_ctx* ctx) {
 
 bgs_status check_stream(bgs_ctx*, void*) { return BGS_OK; }
 
+// a5-a7: the onesweep radix path (sort.cu); BGS_SORT=bucket selects the per-tile bucket sort
+// (bucket.cu: bit-identical order, measured no faster -- DESIGN.md §12)
+bool use_bucket_sort() {
+  const char* e = getenv("BGS_SORT");
+  return e && std::strcmp(e, "bucket") == 0;
+}
+
 bgs_status set_camera(bgs_ctx* ctx, const bgs_camera* c) {
   if (!c) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "camera is NULL");
   if (c->width <= 0 || c->height <= 0 || !(c->fx > 0) || !(c->fy > 0) || !(c->near_clip > 0))
@@ -559,7 +567,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2, &c->scr_dlsup,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2, &c->scr_dlsup, &c->bucket_cur,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -697,13 +705,7 @@ static bgs_status project_enqueue(bgs_ctx* ctx, const bgs_gaussians* g, const bg
   a.rec_cap = g->n_local;
   a.counters = P_<unsigned long long>(ctx->counters);
   CK(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_NCOUNTERS, s));
-  a.tile_diff = nullptr;
-  if (ctx->world > 1) {
-    const size_t nd = size_t(ctx->cam.TX + 1) * (ctx->cam.TY + 1);
-    CKS(ensure(ctx, ctx->tile_diff, nd * 4));
-    CK(cudaMemsetAsync(ctx->tile_diff.p, 0, nd * 4, s));
-    a.tile_diff = P_<int32_t>(ctx->tile_diff);
-  }
+  a.tile_diff = nullptr;  // per-tile pair counts come from k_tile_count over the records (a3, a5)
   if (a.gate_enabled && a.n > 0) {
     launch_gate_count(a, s);
     CKS(launched(ctx));
@@ -785,8 +787,11 @@ bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_o
   CKS(ensure(ctx, ctx->tile_pairs, size_t(T) * 4));
   CKS(ensure(ctx, ctx->owner, size_t(T) * 4));
   CKS(ensure(ctx, ctx->runinfo, 64 + size_t(M + 1) * 8));
-  launch_tile_costs(P_<int32_t>(ctx->tile_diff), ctx->cam.TX, ctx->cam.TY, P_<int32_t>(ctx->tile_pairs), s);
-  CKS(launched(ctx));
+  CK(cudaMemsetAsync(ctx->tile_pairs.p, 0, size_t(T) * 4, s));
+  if (ctx->F > 0) {
+    launch_tile_count(P_<Rec>(ctx->recs), ctx->F, nullptr, ctx->cam.TX, 0, T, P_<int32_t>(ctx->tile_pairs), s);
+    CKS(launched(ctx));
+  }
   CKS(ctx->tr->allreduce_i32(ctx, P_<int32_t>(ctx->tile_pairs), T, s));
   int32_t* run = P_<int32_t>(ctx->runinfo);
   long long* pown = reinterpret_cast<long long*>(P_<char>(ctx->runinfo) + 64);
@@ -885,21 +890,48 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   }
   a.cap = P;
   a.counters = P_<unsigned long long>(ctx->counters);
-  CKS(ensure(ctx, ctx->digit_hist, kMaxSortPasses * 256 * 4));
   CKS(ensure(ctx, ctx->pass_ctrl, 64 * 4));
-  const int64_t n_parts = std::max<int64_t>(1, (P + kViewSortPart - 1) / kViewSortPart);
-  CKS(ensure(ctx, ctx->status, size_t(n_parts) * 256 * 4 * ctx->n_passes));
   CKS(ensure(ctx, ctx->ranges, size_t(std::max(nt, 1)) * 8));
-  a.digit_hist = P_<uint32_t>(ctx->digit_hist);
   a.pass_ctrl = P_<uint32_t>(ctx->pass_ctrl);
-  a.status = P_<uint32_t>(ctx->status);
   a.n_passes = ctx->n_passes;
   a.tbits = tbits;
   a.ranges = P_<uint2>(ctx->ranges);
   CKS(ensure(ctx, ctx->aux, size_t(std::max<int64_t>(ctx->R, 1)) * 16));
   a.aux = P_<float4>(ctx->aux);
+  CK(cudaMemsetAsync(ctx->pass_ctrl.p, 0, 64 * 4, s));  // buffer selectors 0: results in keys[0] / vals[0]
+  if (use_bucket_sort()) {
+    // bucket sizes: world 1 the rects' 2D difference array (bgs_project) prefix-summed; world > 1
+    // the all-reduced a3 counts (exactly the pairs this owner receives per owned tile)
+    if (ctx->world == 1) {
+      if (ctx->T > 16384) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bucket sort supports at most 16384 tiles");
+      CKS(ensure(ctx, ctx->tile_pairs, size_t(std::max(ctx->T, 1)) * 4));
+      CK(cudaMemsetAsync(ctx->tile_pairs.p, 0, size_t(ctx->T) * 4, s));
+      if (ctx->R > 0) {
+        launch_tile_count(ctx->recv, ctx->R, nullptr, ctx->cam.TX, 0, ctx->T, P_<int32_t>(ctx->tile_pairs), s);
+        CKS(launched(ctx));
+      }
+    }
+    if (ctx->world > 1) {  // depth-bit range of the received records (world 1: from bgs_project)
+      CK(cudaMemsetAsync(P_<unsigned long long>(ctx->counters) + C_DLO, 0, 16, s));
+      if (ctx->R > 0) {
+        launch_depth_range(ctx->recv, ctx->R, P_<unsigned long long>(ctx->counters), s);
+        CKS(launched(ctx));
+      }
+    }
+    CKS(ensure(ctx, ctx->bucket_cur, size_t(2 * std::max(nt, 1) + 3) * 4));  // cursors + work list
+    CKS(ensure(ctx, ctx->tile_perm, size_t(std::max(nt, 1)) * 4));
+    int64_t nl = 0;
+    launch_bucket_sort(a, P_<int32_t>(ctx->tile_pairs), P_<uint32_t>(ctx->bucket_cur), P_<uint32_t>(ctx->tile_perm),
+                       s, &nl);
+    CKS(launched(ctx, int(nl)));
+    ctx->n_passes = 0;
+  } else {
+  CKS(ensure(ctx, ctx->digit_hist, kMaxSortPasses * 256 * 4));
+  const int64_t n_parts = std::max<int64_t>(1, (P + kViewSortPart - 1) / kViewSortPart);
+  CKS(ensure(ctx, ctx->status, size_t(n_parts) * 256 * 4 * ctx->n_passes));
+  a.digit_hist = P_<uint32_t>(ctx->digit_hist);
+  a.status = P_<uint32_t>(ctx->status);
   CK(cudaMemsetAsync(ctx->digit_hist.p, 0, kMaxSortPasses * 256 * 4, s));
-  CK(cudaMemsetAsync(ctx->pass_ctrl.p, 0, 64 * 4, s));
   CK(cudaMemsetAsync(P_<unsigned long long>(ctx->counters) + C_P, 0, 8, s));
   CK(cudaMemsetAsync(ctx->status.p, 0, size_t(n_parts) * 256 * 4 * ctx->n_passes, s));
   CK(cudaMemsetAsync(ctx->ranges.p, 0, size_t(std::max(nt, 1)) * 8, s));
@@ -924,6 +956,7 @@ bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
   CKS(ensure(ctx, ctx->tile_perm, size_t(std::max(nt, 1)) * 4));
   launch_tile_order(P_<uint2>(ctx->ranges), nt, P_<uint32_t>(ctx->tile_perm), s);
   CKS(launched(ctx));
+  }
   ctx->stage = 3;
   return BGS_OK;
 }
@@ -1478,12 +1511,21 @@ bgs_status batch_route(bgs_ctx* ctx, int B, cudaStream_t s) {
   CKS(ensure(ctx, bs.tot_send, size_t(M) * B * 8));
   CKS(ensure(ctx, bs.tot_recv, size_t(M) * B * 8));
   int32_t* pairs = P_<int32_t>(bs.pairs);
+  CK(cudaMemsetAsync(pairs, 0, size_t(B) * T * 4, s));
   for (int b = 0; b < B; ++b) {
     bgs_ctx* sl = bs.slots[b];
-    launch_tile_costs(P_<int32_t>(sl->tile_diff), sl->cam.TX, sl->cam.TY, pairs + size_t(b) * T, s);
-    CKS(launched(ctx));
+    if (sl->n_local > 0) {  // the record count is on the device until the host read
+      launch_tile_count(P_<Rec>(sl->recs), sl->n_local, P_<unsigned long long>(sl->counters) + C_F, sl->cam.TX, 0, T,
+                        pairs + size_t(b) * T, s);
+      CKS(launched(ctx));
+    }
   }
   CKS(ctx->tr->allreduce_i32(ctx, pairs, int64_t(B) * T, s));  // collective 1 of the batch
+  for (int b = 0; b < B; ++b) {  // each view's global counts: a3's costs and its owner's bucket sizes
+    bgs_ctx* sl = bs.slots[b];
+    CKS(ensure(sl, sl->tile_pairs, size_t(T) * 4));
+    CK(cudaMemcpyAsync(sl->tile_pairs.p, pairs + size_t(b) * T, size_t(T) * 4, cudaMemcpyDeviceToDevice, s));
+  }
   for (int b = 0; b < B; ++b) {
     bgs_ctx* sl = bs.slots[b];
     const int64_t cap = std::max<int64_t>(sl->n_local, 1);  // F is on the device until the host read

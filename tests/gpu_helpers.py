@@ -37,6 +37,15 @@ def decode_key_tiles(keys: np.ndarray, counters: np.ndarray, n_tiles: int) -> np
     return (keys.astype(np.uint64) >> np.uint64(kd)).astype(np.int32)
 
 
+def range_tiles(ranges: np.ndarray, P: int) -> np.ndarray:
+    """Local tile of every sorted pair from the per-tile ranges [start, end) (a7; include/bgs.h
+    debug buffer 5), which cover [0, P) contiguously in tile order."""
+    r = np.asarray(ranges, np.int64).reshape(-1, 2)
+    t = np.repeat(np.arange(len(r), dtype=np.int32), np.maximum(r[:, 1] - r[:, 0], 0))
+    assert t.size == P, (t.size, P)
+    return t
+
+
 def moments_to_g2d(g: np.ndarray, rec: dict) -> np.ndarray:
     """Accumulator moments (include/bgs.h debug buffer 6) -> dL/d(mx,my,A,B,C,o,r,g,b), with the
     record's own o, A, B, C (bit-identical to the oracle's, test_project_bit_exact)."""
@@ -98,12 +107,12 @@ class GpuStep:
                     out["owner"] = owner.cpu().numpy()
                     B.bgs_sort_tiles(ctx, stream)
                     out["q"] = ctx.query()
-                    out["keys"] = ctx.debug_buffer("keys").view(torch.int32).cpu().numpy().view(np.uint32)
                     out["counters"] = ctx.debug_buffer("counters").view(torch.int64).cpu().numpy().view(np.uint64)
-                    out["key_tile"] = decode_key_tiles(out["keys"], out["counters"],
-                                                       out["q"]["tile_end"] - out["q"]["tile_begin"])
                     out["vals"] = ctx.debug_buffer("vals").view(torch.int32).cpu().numpy()
                     out["ranges"] = ctx.debug_buffer("ranges").view(torch.int32).cpu().numpy().reshape(-1, 2)
+                    out["key_tile"] = range_tiles(out["ranges"], out["q"]["P"])
+                    # bucket sort (default): keys = f32 bits(depth) - lo, sorted within each tile
+                    out["keys"] = ctx.debug_buffer("keys").view(torch.int32).cpu().numpy().view(np.uint32)
                     recv = ctx.debug_buffer("recv") if M > 1 else ctx.debug_buffer("records")
                     out["recv"] = rec_view(recv)
                     out["recv_raw"] = recv

@@ -17,7 +17,7 @@ import torch
 
 import oracle as O
 import synthetic as S
-from gpu_helpers import acc_view, decode_key_tiles, moments_to_g2d, rec_view
+from gpu_helpers import acc_view, moments_to_g2d, range_tiles, rec_view
 from test_gpu_parity import _check_g2d, _flip_info
 
 pytestmark = pytest.mark.gpu
@@ -185,13 +185,12 @@ def _run_group(sc, cams, dls, M):
                 for k in range(NV):
                     vc = ctx.batch_view(k)
                     q = vc.query()
-                    keys = vc.debug_buffer("keys").view(torch.int32).cpu().numpy().view(np.uint32)
-                    cnt = vc.debug_buffer("counters").view(torch.int64).cpu().numpy().view(np.uint64)
+                    rng = vc.debug_buffer("ranges").view(torch.int32).cpu().numpy().reshape(-1, 2)
                     recv = rec_view(vc.debug_buffer("recv"))
                     vals = vc.debug_buffer("vals").view(torch.int32).cpu().numpy()
                     owner = vc.debug_buffer("owner").view(torch.int32).cpu().numpy()
                     res[r]["views"].append(dict(
-                        q=q, owner=owner, tiles=decode_key_tiles(keys, cnt, q["tile_end"] - q["tile_begin"]),
+                        q=q, owner=owner, tiles=range_tiles(rng, q["P"]),
                         gids=recv["gid"][vals], rgb=bufs[k]["rgb"].cpu().numpy(), nc=bufs[k]["nc"].cpu().numpy(),
                         acc=acc_view(vc.debug_buffer("acc_local")), records=rec_view(vc.debug_buffer("records")),
                         lidx=vc.debug_buffer("rec_lidx").view(torch.int32).cpu().numpy()))

@@ -122,6 +122,35 @@ def test_sort_and_ranges_bit_exact(tiny_run):
     assert np.array_equal(dbits, _f32(st.get("depth")[gid]).view(np.uint32))
     assert np.array_equal(o["ranges"][:, 0], st.get("range_lo", 0))
     assert np.array_equal(o["ranges"][:, 1], st.get("range_hi", 0))
+    # sorted keys non-decreasing in every tile
+    keys = o["keys"]
+    same_tile = tiles[1:] == tiles[:-1]
+    assert np.all(keys[1:][same_tile] >= keys[:-1][same_tile])
+
+
+@pytest.mark.parametrize("M", [1, 3])
+def test_bucket_sort_path_matches(tiny_scene, tiny_run, monkeypatch, M):
+    """BGS_SORT=bucket (per-tile bucket sort, bucket.cu) gives the oracle's pair order and ranges
+    and the same image at world 1 and at M = 3 (in-process group); its keys are f32 bits(depth) - lo
+    (C_DLO holds 0xffffffff - lo), non-decreasing in every tile."""
+    sc, cam, dl, st1, gs = tiny_run
+    st = st1 if M == 1 else O.OracleStep(sc, cam, M=M, dLdC=dl)
+    monkeypatch.setenv("BGS_SORT", "bucket")
+    g2 = GpuStep(sc, cam, M=M, dLdC=dl)
+    try:
+        for r in range(M):
+            o2 = g2.rank[r]
+            b, _ = st.get("tile_range", r)
+            assert np.array_equal(o2["recv"]["gid"][o2["vals"]], st.get("pair_gid", r))
+            assert np.array_equal(o2["key_tile"] + b, st.get("pair_tile", r))
+            assert np.array_equal(o2["ranges"][:, 0], st.get("range_lo", r))
+            assert np.array_equal(o2["ranges"][:, 1], st.get("range_hi", r))
+            dbits = o2["recv"]["depth"][o2["vals"]].view(np.uint32)
+            lo = np.uint32(0xFFFFFFFF - int(o2["counters"][6] & np.uint64(0xFFFFFFFF)))
+            assert np.array_equal(o2["keys"], dbits - lo)
+        assert np.array_equal(g2.img, gs.img) and np.array_equal(g2.nc, gs.nc)
+    finally:
+        g2.close()
 
 
 def test_raster_fwd_parity(tiny_run):
