@@ -561,7 +561,7 @@ def scoring(args, B, ctxs, per, g, cams, gate, cull_of, s_imp, c_rad, c_vis, l2_
         B.bgs_route(ctxs[k], None, st_k)
         B.bgs_sort_tiles(ctxs[k], st_k)
         B.bgs_raster_fwd(ctxs[k], B.BGS_IMPORTANCE, p["rgb"], p["Tf"], p["nc"], st_k)
-        B.bgs_route_reverse(ctxs[k], st_k)
+        B.bgs_route_reverse(ctxs[k], st_k, B.BGS_IMPORTANCE_ONLY)
         B.bgs_importance(ctxs[k], n_local, p["radius"], None, None, s_imp, c_rad, c_vis, p["cull"], 99, 100, st_k)
 
     stream = per[0]["stream"]

@@ -62,6 +62,7 @@ typedef struct bgs_ctx bgs_ctx;
 /* flags */
 #define BGS_NO_COLOR 1u   /* a2 skips SH colour (instrumented scoring pass "bypasses color shading") */
 #define BGS_IMPORTANCE 2u /* a8 accumulates w_fixed (sum of alpha*T in 2^-24 units) and a per splat */
+#define BGS_IMPORTANCE_ONLY 8u /* a10 sends only (w_fixed, a), 12 B per record (scoring sweeps: no backward) */
 
 /* Pinhole camera.  R row-major world->camera, x right, y down, camera looks +z;
  * campos = -R^T t is the camera centre c_v of Eq.5 (caller-computed); pixels are centred at
@@ -203,9 +204,11 @@ bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_fin
 bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL_drgb, const float* t_final, const int32_t* n_contrib,
                           void* stream);
 
-/* a10.  Returns per-received-splat partials (9 grads + w_fixed + a) to the source ranks along
- * the transposed counts of a4 and sums them per local record in destination-rank order. */
-bgs_status bgs_route_reverse(bgs_ctx* ctx, void* stream);
+/* a10.  Returns per-received-splat partials (9 grads + w_fixed + a, 48 B) to the source ranks along
+ * the transposed counts of a4 and sums them per local record in destination-rank order.
+ * flags: BGS_IMPORTANCE_ONLY sends (w_fixed, a) only, 12 B per record (the instrumented scoring
+ * pass "bypasses color shading" and has no backward); the gradients are then zero. */
+bgs_status bgs_route_reverse(bgs_ctx* ctx, uint32_t flags, void* stream);
 
 /* a11.  grads += d(loss)/d(activated params) for every projected local Gaussian. */
 bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,

@@ -26,6 +26,7 @@ _lib = C.CDLL(LIB_PATH)
 BGS_NO_COLOR = 1
 BGS_IMPORTANCE = 2
 BGS_GRAPH = 4
+BGS_IMPORTANCE_ONLY = 8
 BGS_Q_COUNT = 14
 Q_NAMES = ("n_local", "n_lod", "n_active", "F", "D", "R", "P", "tile_begin", "tile_end", "fallback",
            "sort_passes", "P_all", "width", "height")
@@ -90,7 +91,7 @@ _SIGS = {
     "bgs_sort_tiles": [_vp, _vp],
     "bgs_raster_fwd": [_vp, C.c_uint32, _vp, _vp, _vp, _vp],
     "bgs_raster_bwd": [_vp, _vp, _vp, _vp, _vp],
-    "bgs_route_reverse": [_vp, _vp],
+    "bgs_route_reverse": [_vp, C.c_uint32, _vp],
     "bgs_project_bwd": [_vp, _vp, _vp, _vp, _vp],
     "bgs_importance": [_vp, C.c_int64, _vp, _vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp, _vp, _vp],
     "bgs_view_step": [_vp, _vp, _vp, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
@@ -358,8 +359,9 @@ def bgs_raster_bwd(ctx: Context, dL_drgb, t_final, n_contrib, stream=None):
               "bgs_raster_bwd")
 
 
-def bgs_route_reverse(ctx: Context, stream=None):
-    ctx.check(_lib.bgs_route_reverse(ctx.handle, _stream(stream)), "bgs_route_reverse")
+def bgs_route_reverse(ctx: Context, stream=None, flags: int = 0):
+    """a10; flags BGS_IMPORTANCE_ONLY: (w, a) only, 12 B per record (scoring sweeps)."""
+    ctx.check(_lib.bgs_route_reverse(ctx.handle, int(flags), _stream(stream)), "bgs_route_reverse")
 
 
 def bgs_project_bwd(ctx: Context, g: GaussianPlanes, cam: bgs_camera, grads: GradPlanes, stream=None):

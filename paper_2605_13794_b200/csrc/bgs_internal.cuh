@@ -207,6 +207,10 @@ void launch_pack(const Rec* recs, int64_t F, const unsigned long long* F_dev, co
                  const uint32_t* block_offs, int world, const int64_t* send_base, Rec* send, cudaStream_t s);
 void launch_gather_sum(const Acc* rev, int64_t F, const unsigned long long* F_dev, const uint8_t* dest_mask,
                        const uint32_t* block_offs, int world, const int64_t* send_base, Acc* out, cudaStream_t s);
+// BGS_IMPORTANCE_ONLY reverse: (w, a) of the received records as 12-B units, and their gather-sum
+void launch_pack_imp(const Acc* acc, int64_t R, void* out, cudaStream_t s);
+void launch_gather_imp(const void* rev, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs, int world,
+                       const int64_t* send_base, Acc* out, cudaStream_t s);
 struct PtrList {
   const void* p[kMaxWorld];
   int n;

@@ -250,6 +250,38 @@ __global__ void __launch_bounds__(kRouteBlock) k_gather_sum(const Acc* rev, int6
   out[f] = s;
 }
 
+// BGS_IMPORTANCE_ONLY reverse (scoring sweeps, no backward): per received record only (w, a),
+// 12 B = uint3 {w lo, w hi, a} instead of the 48-B accumulator
+__global__ void __launch_bounds__(256) k_pack_imp(const Acc* __restrict__ acc, int64_t R, uint3* __restrict__ out) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const unsigned long long w = acc[r].w;
+  out[r] = make_uint3(uint32_t(w), uint32_t(w >> 32), acc[r].a);
+}
+
+__global__ void __launch_bounds__(kRouteBlock) k_gather_imp(const uint3* rev, int64_t F, const uint8_t* dest_mask,
+                                                            const uint32_t* block_offs, int world,
+                                                            const int64_t* send_base, Acc* out) {
+  __shared__ uint32_t s_w[kRouteBlock / 32][kMaxWorld];
+  const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint32_t mask = f < F ? dest_mask[f] : 0u;
+  uint32_t pos[kMaxWorld];
+  block_positions(mask, world, pos, s_w);
+  if (f >= F) return;
+  Acc s;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) s.g[k] = 0.f;
+  s.a = 0;
+  s.w = 0;
+  for (int d = 0; d < world; ++d) {  // destination-rank ascending (integer sums: order-free anyway)
+    if (!((mask >> d) & 1u)) continue;
+    const uint3 p = rev[send_base[d] + block_offs[int64_t(blockIdx.x) * world + d] + pos[d]];
+    s.w += (unsigned long long)p.x | ((unsigned long long)p.y << 32);
+    s.a += p.z;
+  }
+  out[f] = s;
+}
+
 __global__ void k_reduce_i32(PtrList src, int32_t* dst, int64_t n) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -323,6 +355,18 @@ void launch_gather_sum(const Acc* rev, int64_t F, const unsigned long long* F_de
   const int64_t nb = (F + kRouteBlock - 1) / kRouteBlock;
   if (nb > 0)
     k_gather_sum<<<unsigned(nb), kRouteBlock, 0, s>>>(rev, F, F_dev, dest_mask, block_offs, world, send_base, out);
+}
+
+void launch_pack_imp(const Acc* acc, int64_t R, void* out, cudaStream_t s) {
+  if (R > 0) k_pack_imp<<<unsigned((R + 255) / 256), 256, 0, s>>>(acc, R, static_cast<uint3*>(out));
+}
+
+void launch_gather_imp(const void* rev, int64_t F, const uint8_t* dest_mask, const uint32_t* block_offs, int world,
+                       const int64_t* send_base, Acc* out, cudaStream_t s) {
+  const int64_t nb = (F + kRouteBlock - 1) / kRouteBlock;
+  if (nb > 0)
+    k_gather_imp<<<unsigned(nb), kRouteBlock, 0, s>>>(static_cast<const uint3*>(rev), F, dest_mask, block_offs, world,
+                                                      send_base, out);
 }
 
 void launch_reduce_sum_i32(PtrList src, int32_t* dst, int64_t n, cudaStream_t s) {

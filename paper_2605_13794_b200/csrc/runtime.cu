@@ -1020,7 +1020,7 @@ bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL, const float* t_final, c
   return BGS_OK;
 }
 
-bgs_status bgs_route_reverse(bgs_ctx* ctx, void* stream) {
+bgs_status bgs_route_reverse(bgs_ctx* ctx, uint32_t flags, void* stream) {
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_route_reverse before bgs_raster_fwd");
@@ -1028,6 +1028,25 @@ bgs_status bgs_route_reverse(bgs_ctx* ctx, void* stream) {
   const int M = ctx->world;
   if (M == 1) {
     ctx->acc_local = P_<Acc>(ctx->acc);
+    ctx->stage = 6;
+    return BGS_OK;
+  }
+  if (flags & BGS_IMPORTANCE_ONLY) {  // 12-B (w, a) units instead of the 48-B accumulators
+    CKS(ensure(ctx, ctx->rev, size_t(std::max<int64_t>(std::max(ctx->D, ctx->R), 1)) * sizeof(Acc)));
+    CKS(ensure(ctx, ctx->accl, size_t(std::max<int64_t>(ctx->F, 1)) * sizeof(Acc)));
+    // pack the received records' (w, a) into the tail of rev (R x 12 B fits behind D x 12 B: rev
+    // holds max(D, R) 48-B units)
+    char* packed = P_<char>(ctx->rev) + size_t(std::max<int64_t>(ctx->D, 1)) * 12;
+    launch_pack_imp(P_<Acc>(ctx->acc), ctx->R, packed, s);
+    CKS(launched(ctx));
+    CKS(ctx->tr->alltoallv(ctx, packed, ctx->recv_cnt.data(), ctx->recv_off.data(), ctx->rev.p,
+                           ctx->send_cnt.data(), ctx->send_off.data(), 12, s));
+    if (ctx->F > 0) {
+      launch_gather_imp(ctx->rev.p, ctx->F, P_<uint8_t>(ctx->dest_mask), P_<uint32_t>(ctx->block_counts), M,
+                        P_<int64_t>(ctx->send_base), P_<Acc>(ctx->accl), s);
+      CKS(launched(ctx));
+    }
+    ctx->acc_local = P_<Acc>(ctx->accl);
     ctx->stage = 6;
     return BGS_OK;
   }
@@ -1248,7 +1267,8 @@ static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs
   CKS(mark(5));
   if (dL) CKS(bgs_raster_bwd(ctx, dL, t_final, n_contrib, stream));
   CKS(mark(6));
-  CKS(bgs_route_reverse(ctx, stream));
+  // no backward in this step (scoring sweep): only (w, a) travel back, 12 B per record
+  CKS(bgs_route_reverse(ctx, dL ? 0u : uint32_t(BGS_IMPORTANCE_ONLY), stream));
   CKS(mark(7));
   if (dL && grads) CKS(bgs_project_bwd(ctx, g, cam, grads, stream));
   CKS(mark(8));
@@ -1688,7 +1708,7 @@ bgs_status slot_phases(bgs_ctx* sl, const bgs_gaussians* g, const bgs_batch_view
       CK_CTX(sl, cudaMemsetAsync(sp.loss_out + 3, 0, 2 * sizeof(double), st));
   }
   if ((ph & PH_BWD) && dL) CKS(bgs_raster_bwd(sl, dL, v.t_final, v.n_contrib, st));
-  if (ph & PH_REV) CKS(bgs_route_reverse(sl, st));
+  if (ph & PH_REV) CKS(bgs_route_reverse(sl, dL ? 0u : uint32_t(BGS_IMPORTANCE_ONLY), st));
   if ((ph & PH_PBWD) && dL && grads) CKS(bgs_project_bwd(sl, g, &v.cam, grads, st));
   if ((ph & PH_IMP) && imp)
     CKS(bgs_importance(sl, g->n_local, v.radius_out, nullptr, nullptr, imp->mass_num, imp->mass_den, imp->s,

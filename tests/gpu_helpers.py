@@ -64,7 +64,7 @@ class GpuStep:
 
     def __init__(self, scene, cam, M=1, gate=None, cull_global=None, flags=0, dLdC=None, importance=True,
                  ctxs=None, device=0, target=None, lam=0.2, batch_inv=1.0, beta=None, densify=False, phi=None,
-                 owner_in=None):
+                 owner_in=None, imp_only=False):
         import paper_2605_13794_b200.bgs as B
         self.B = B
         self.M = M
@@ -128,7 +128,7 @@ class GpuStep:
                     if dLdC is not None:
                         dl = torch.from_numpy(np.ascontiguousarray(dLdC, np.float32)).to(dev)
                         B.bgs_raster_bwd(ctx, dl, T, nc, stream)
-                    B.bgs_route_reverse(ctx, stream)
+                    B.bgs_route_reverse(ctx, stream, B.BGS_IMPORTANCE_ONLY if imp_only else 0)
                     out["acc_local"] = acc_view(ctx.debug_buffer("acc_local"))
                     if densify:  # NEXT-3 statistic of this view
                         stat = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)

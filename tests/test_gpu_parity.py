@@ -299,6 +299,25 @@ def test_multirank_local_group_parity(tiny_scene, tiny_run, M):
         gs.close()
 
 
+@pytest.mark.parametrize("M", [2, 3])
+def test_importance_only_reverse(tiny_scene, tiny_run, M):
+    """BGS_IMPORTANCE_ONLY: the scoring pass's reverse exchange carries only (w, a),
+    12 B per record; w, a, s, c_rad, c_vis and the Cull column are bit-identical to the full 48-B
+    reverse and to world 1."""
+    sc, cam, dl, st1, gs1 = tiny_run
+    full = GpuStep(sc, cam, M=M, flags=1)  # NO_COLOR, forward only: the scoring pass
+    imp = GpuStep(sc, cam, M=M, flags=1, imp_only=True)
+    try:
+        for f in ("a", "w", "c_rad", "c_vis", "cull_bits"):
+            assert np.array_equal(getattr(imp, f), getattr(full, f)), f
+            assert np.array_equal(getattr(imp, f), getattr(gs1, f)), f
+        np.testing.assert_allclose(imp.s, full.s, rtol=1e-15, atol=0)
+        assert not imp.g2d.any()  # no gradients travel in this mode
+    finally:
+        full.close()
+        imp.close()
+
+
 def test_route_given_owner_map(tiny_scene, tiny_run):
     """bgs_route's tile_owner_in: the oracle's owner map passed in reproduces the
     a3 split's routing; a map that is not contiguous runs is refused on every rank."""
