@@ -26,6 +26,8 @@ STAGE_OF = {
     "k_imp_mark": "importance",
     "k_loss_photo": "loss", "k_loss_sums": "loss", "k_loss_finish": "loss", "k_owned_copy": "loss",
     "k_scale_sum": "loss", "k_scale_finish": "loss", "k_scale_grad": "loss",
+    "k_tile_count": "route", "k_bucket_ranges": "sort", "k_bucket_emit": "sort", "k_bucket_radix": "sort",
+    "k_depth_range": "sort", "k_pack_imp": "route_reverse", "k_gather_imp": "route_reverse",
 }
 
 
