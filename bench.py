@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--gate", choices=["config", "on", "off"], default="config",
                    help="LOD gate + importance mask: the config's default, or forced (Table-2-style toggles)")
     p.add_argument("--mask", choices=["config", "on", "off"], default="config",
-                   help="importance Cull mask when the gate is on: the config's default, or forced")
+                   help="importance Cull mask: the config's default, or forced (independent of the gate)")
     p.add_argument("--layout", default="morton", choices=["morton", "input"],
                    help="shard storage order: Z-order (bgs_spatial_order) or the generator's random ids")
     p.add_argument("--host-threads", type=int, default=0,
@@ -234,7 +234,7 @@ def run_native(args):
 
     label, gate_default = CONFIG_SHAPES[args.config]
     gate_on = gate_default if args.gate == "config" else args.gate == "on"
-    mask_on = gate_on if args.mask == "config" else (args.mask == "on" and gate_on)
+    mask_on = gate_default if args.mask == "config" else args.mask == "on"  # independent toggles (Table 2)
     t0 = time.perf_counter()
     scene = S.gen_city(args.config, n=args.n, V=args.views)
     gen_s = time.perf_counter() - t0
@@ -915,8 +915,8 @@ def run_reference(args):
     import synthetic as S
     label, gate_default = CONFIG_SHAPES[args.config]
     gate_on = gate_default if args.gate == "config" else args.gate == "on"
-    mask_on = gate_on if args.mask == "config" else (args.mask == "on" and gate_on)
-    if gate_on:
+    mask_on = gate_default if args.mask == "config" else args.mask == "on"
+    if gate_on or mask_on:
         print(json.dumps({"impl": "reference", "unavailable": "the oracle reference arm covers the ungated "
                                                               "configs only (rubble, residence, matrixcity)"}))
         return
