@@ -256,6 +256,16 @@ void launch_fill_bits(uint32_t* words, int64_t n_bits, cudaStream_t s);
 // `next` (same size) for the following call.  cand: u32 scratch [n_items].
 int64_t imp_set_words();
 int64_t imp_cand_words(int64_t n_items);  // u32 scratch the cooperative kernel's candidate segments need
+// world > 1, two collectives: coarse (count, mass) histogram over 4096 log-linear bins of w (zeroed
+// by the caller, all-reduced between the calls), the crossing bin, its candidates packed as
+// [count, pad, (w, gid) x count] u64 words, and the exact selection among every rank's candidates
+void launch_imp_stats_coarse(const ImportanceArgs& a, unsigned long long* hist, cudaStream_t s);
+void launch_imp_coarse_decide(ImpState* st, const unsigned long long* hist, int num, int den, cudaStream_t s);
+void launch_imp_gather_cand(const ImportanceArgs& a, const ImpState* st, unsigned long long* buf, cudaStream_t s);
+void launch_imp_select_cand(ImpState* st, const unsigned long long* gathered, int world, int64_t stride_words,
+                            int num, int den, cudaStream_t s);
+int64_t imp_coarse_words();
+size_t imp_state_ncand_offset();
 cudaError_t launch_imp_coop(const ImportanceArgs& a, ImpState* st, unsigned long long* set,
                             unsigned long long* next, uint32_t* cand, int num, int den, cudaStream_t s);
 

@@ -45,7 +45,8 @@ struct alignas(16) ImpState {
   unsigned long long next_cnt;   // items in the crossing bin of the last round (next round's candidates)
   uint32_t tshift;               // selection: (w >> tshift) >= prefix (0 after all rounds)
   uint32_t final_;               // threshold resolved (crossing bin holds one item): no more rounds
-  uint32_t pad1;
+  uint32_t bstar;                // world > 1 coarse path: the crossing coarse bin
+  unsigned long long ncand;      // world > 1 coarse path: items (all ranks) in the crossing bin
 };
 static_assert(sizeof(ImpState) <= kImpStateBytes, "ImpState fits its arena slot");
 
@@ -473,6 +474,197 @@ __global__ void k_fill_bits(uint32_t* words, int64_t n_bits) {
   words[t] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
 }
 
+// ---- world > 1, two collectives per view ---------------------------------------------------
+// (1) every rank: s, c_rad and a coarse histogram of w over 4096 log-linear bins (count, mass):
+//     bin(w) = 64 e + (6 bits below the leading one), e = msb(w); monotone in w.  ONE all-reduce.
+// (2) every rank decides the same crossing bin b* (mass above b* short of num/den of the total, with
+//     b* reaching it) and reads the global count of b* (one host read), packs its items of b* as
+//     (w, gid) and ONE all-gather gives every rank all of them.
+// (3) one CTA per rank selects exactly among the gathered candidates (radix rounds on w from the
+//     leading bit, then on gid among ties), so tau and the gid cut are bit-identical on every rank
+//     and equal to the round path's (same integer definition).
+constexpr int kCoarseBins = 4096;
+
+__device__ __forceinline__ uint32_t coarse_bin(unsigned long long w) {
+  const int e = 63 - __clzll((long long)w);
+  const uint32_t m = e >= 6 ? uint32_t(w >> (e - 6)) & 63u : uint32_t(w << (6 - e)) & 63u;
+  return uint32_t(e) * 64u + m;
+}
+
+__global__ void __launch_bounds__(256) k_imp_stats_coarse(ImportanceArgs a, unsigned long long* hist /*[2][4096]*/) {
+  extern __shared__ unsigned long long s_h[];  // [2][4096]
+  for (int i = threadIdx.x; i < 2 * kCoarseBins; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); base < a.n_items; base += stride) {
+    const int64_t t = base + lane;
+    unsigned long long w = 0;
+    if (t < a.n_items) {
+      const Item it = load_item(a, t);
+      w = it.w;
+      if (a.wbuf) a.wbuf[t] = it.w;
+      if (it.a > 0) atomicAdd(a.s + it.lidx, (double(it.w) * (1.0 / 16777216.0)) / (double(it.a) + 1e-8));
+      if (it.rad) atomicAdd(a.c_rad + it.lidx, 1u);
+    }
+    const bool cand = w != 0;
+    hist_add(cand, cand ? coarse_bin(w) : (1u << 20) + lane, w, lane, s_h, s_h + kCoarseBins);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kCoarseBins; i += blockDim.x)
+    if (s_h[i]) {
+      atomicAdd(hist + i, s_h[i]);
+      atomicAdd(hist + kCoarseBins + i, s_h[kCoarseBins + i]);
+    }
+}
+
+// one CTA of 1024: the crossing coarse bin from the top
+__global__ void __launch_bounds__(1024) k_imp_coarse_decide(ImpState* st, const unsigned long long* hist, int num,
+                                                            int den) {
+  __shared__ unsigned long long s_part[1024];
+  __shared__ unsigned long long s_total;
+  // thread j owns bins [4 j, 4 j + 4); suffix sums of the mass from the top
+  const int j = threadIdx.x;
+  unsigned long long m[4], loc = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    m[k] = hist[kCoarseBins + 4 * j + k];
+    loc += m[k];
+  }
+  s_part[j] = loc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {  // inclusive suffix scan: s_part[j] = mass of bins >= 4 j
+    const unsigned long long v = j + o < 1024 ? s_part[j + o] : 0ull;
+    __syncthreads();
+    s_part[j] += v;
+    __syncthreads();
+  }
+  if (j == 0) s_total = s_part[0];
+  __syncthreads();
+  const unsigned long long total = s_total;
+  const unsigned long long target = (unsigned long long)num * total;
+  unsigned long long above = j + 1 < 1024 ? s_part[j + 1] : 0ull;  // bins >= 4 j + 4
+  if (j == 0) {
+    st->total = total;
+    st->empty = total == 0;
+    st->final_ = 0;
+    st->need_gid = 0;
+    st->gid_thr = 0xffffffffu;
+    st->tshift = 0;
+    st->ncand = 0;
+  }
+  __syncthreads();
+  if (total == 0) return;
+  for (int k = 3; k >= 0; --k) {
+    const int b = 4 * j + k;
+    const bool cross = (unsigned long long)den * (above + m[k]) >= target && (unsigned long long)den * above < target;
+    if (cross && hist[b] > 0) {
+      st->bstar = uint32_t(b);
+      st->above = above;
+      st->ncand = hist[b];
+    }
+    above += m[k];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_imp_gather_cand(ImportanceArgs a, const ImpState* st,
+                                                         unsigned long long* buf /*[0] count, then (w, gid, -)*/) {
+  if (st->empty) return;
+  const uint32_t b = st->bstar;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < a.n_items; t += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long w = load_w(a, t);
+    if (w == 0 || coarse_bin(w) != b) continue;
+    const unsigned long long pos = atomicAdd(buf, 1ull);
+    const uint32_t lidx = a.item_lidx ? a.item_lidx[t] : uint32_t(t);
+    buf[2 + 2 * pos] = w;
+    buf[3 + 2 * pos] = gid_of(a, lidx);
+  }
+}
+
+// One CTA (256 threads): exact selection among the gathered candidates of every rank.  Rank r's
+// block starts at gath + r * stride (u64 words): [count][pad][(w, gid) x count].
+__global__ void __launch_bounds__(256) k_imp_select_cand(ImpState* st, const unsigned long long* gath, int world,
+                                                         int64_t stride, int num, int den) {
+  __shared__ unsigned long long s_hist[512];  // [256] counts, [256] masses (decide_body's layout)
+  unsigned long long* s_cnt = s_hist;
+  unsigned long long* s_mass = s_hist + 256;
+  __shared__ ImpState S;
+  if (st->empty) return;
+  if (threadIdx.x == 0) {
+    S = *st;
+    S.prefix = 0;
+    S.k = 0;
+    S.below = 0;
+    S.gprefix = 0;
+    S.need_gid = 0;
+    S.final_ = 0;
+    const int e = int(S.bstar / 64);
+    const int r0 = (kWRounds - 1) - e / 8;
+    S.r0 = uint32_t(r0 < 0 ? 0 : r0);
+    // digits above the leading bit are 0 for every candidate: the prefix starts from them
+  }
+  __syncthreads();
+  auto for_each = [&](auto fn) {
+    for (int r = 0; r < world; ++r) {
+      const unsigned long long* blk = gath + r * stride;
+      const int64_t n = int64_t(blk[0]);
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) fn(blk[2 + 2 * i], uint32_t(blk[3 + 2 * i]));
+    }
+  };
+  for (int r = int(S.r0); r < kWRounds && !S.final_; ++r) {
+    s_cnt[threadIdx.x] = 0;
+    s_mass[threadIdx.x] = 0;
+    __syncthreads();
+    const int shift = 8 * (kWRounds - 1 - r);
+    const unsigned long long prefix = S.prefix;
+    for_each([&](unsigned long long w, uint32_t) {
+      if (shift + 8 < 64 && (w >> (shift + 8)) != prefix) return;
+      const uint32_t d = uint32_t((w >> shift) & 255u);
+      atomicAdd(&s_cnt[d], 1ull);
+      atomicAdd(&s_mass[d], w);
+    });
+    __syncthreads();
+    decide_body(&S, r, s_cnt, num, den);  // reads hist[d] counts, hist[256 + d] masses
+  }
+  __syncthreads();
+  if (S.final_) {
+    // the crossing bin of an earlier round held exactly one candidate: its w is tau
+    const unsigned long long pre = S.prefix;
+    const uint32_t tsh = S.tshift;
+    for_each([&](unsigned long long w, uint32_t) {
+      if ((w >> tsh) == pre) S.tau = w;
+    });
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      S.prefix = S.tau;
+      S.tshift = 0;
+    }
+    __syncthreads();
+  }
+  if (S.need_gid) {
+    for (int r = 0; r < kGRounds; ++r) {
+      s_cnt[threadIdx.x] = 0;
+      __syncthreads();
+      const int shift = 8 * (kGRounds - 1 - r);
+      const unsigned long long tau = S.tau;
+      const uint32_t gp = S.gprefix;
+      for_each([&](unsigned long long w, uint32_t g) {
+        if (w != tau) return;
+        if (shift + 8 < 32 && (g >> (shift + 8)) != gp) return;
+        atomicAdd(&s_cnt[(g >> shift) & 255u], 1ull);
+      });
+      __syncthreads();
+      gid_decide_body(&S, r, s_cnt);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.tshift = 0;
+    S.prefix = S.tau;
+    *st = S;
+  }
+}
+
 unsigned grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
@@ -518,6 +710,34 @@ void launch_imp_mark(const ImportanceArgs& a, const ImpState* st, cudaStream_t s
 }
 
 int64_t imp_set_words() { return kImpSetWords; }
+
+void launch_imp_stats_coarse(const ImportanceArgs& a, unsigned long long* hist, cudaStream_t s) {
+  static std::atomic<int> attr[kMaxDevices];
+  per_device(attr, [] {
+    cudaFuncSetAttribute(k_imp_stats_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(2 * kCoarseBins * sizeof(unsigned long long)));
+    return 1;
+  });
+  if (a.n_items > 0)
+    k_imp_stats_coarse<<<grid_for(a.n_items) < 296u ? grid_for(a.n_items) : 296u, 256,
+                         2 * kCoarseBins * sizeof(unsigned long long), s>>>(a, hist);
+}
+
+void launch_imp_coarse_decide(ImpState* st, const unsigned long long* hist, int num, int den, cudaStream_t s) {
+  k_imp_coarse_decide<<<1, 1024, 0, s>>>(st, hist, num, den);
+}
+
+void launch_imp_gather_cand(const ImportanceArgs& a, const ImpState* st, unsigned long long* buf, cudaStream_t s) {
+  if (a.n_items > 0) k_imp_gather_cand<<<grid_for(a.n_items), 256, 0, s>>>(a, st, buf);
+}
+
+void launch_imp_select_cand(ImpState* st, const unsigned long long* gathered, int world, int64_t stride_words,
+                            int num, int den, cudaStream_t s) {
+  k_imp_select_cand<<<1, 256, 0, s>>>(st, gathered, world, stride_words, num, den);
+}
+
+int64_t imp_coarse_words() { return 2 * kCoarseBins; }
+size_t imp_state_ncand_offset() { return offsetof(ImpState, ncand); }
 
 static int coop_blocks() {
   static std::atomic<int> slots[kMaxDevices];

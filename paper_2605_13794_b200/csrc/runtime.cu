@@ -3,6 +3,7 @@
 // runs in the kernels of project.cu, sort.cu, raster.cu, project_bwd.cu, route.cu and
 // importance.cu.  There is no CPU fallback: without a CUDA device every call fails.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -67,7 +68,8 @@ struct bgs_ctx {
       imp_hist, imp_total, scr_rgb, scr_t, scr_n, scr_dl, xchg_counts, aux, tile_perm, cand, wbuf, cmask,
       loss_img, loss_part, loss_sums, scr_tgt, scr_loss, scr_in2,
       scr_dlsup,  // supervised steps' dL/dC (never one of the host-upload double buffers)
-      bucket_cur;  // per-tile write cursors of the bucket sort
+      bucket_cur,  // per-tile write cursors of the bucket sort
+      imp_cand, imp_gath;  // world > 1 importance: this rank's crossing-bin candidates, all ranks' gathered
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
   unsigned long long* h_counters = nullptr;  // pinned
@@ -187,6 +189,8 @@ struct Transport {
   virtual bgs_status alltoallv_batch(bgs_ctx* ctx, int nb, const void* const* send, const int64_t* scnt,
                                      const int64_t* soff, void* const* recv, const int64_t* rcnt, const int64_t* roff,
                                      size_t elem, cudaStream_t s) = 0;
+  // every rank's `bytes` bytes of send, concatenated in rank order into recv (world x bytes)
+  virtual bgs_status allgather(bgs_ctx* ctx, const void* send, void* recv, size_t bytes, cudaStream_t s) = 0;
   virtual bool capturable() const = 0;  // collectives may be recorded into a CUDA graph
 };
 
@@ -273,6 +277,11 @@ struct NcclTransport : Transport {
     ncclResult_t r2 = ncclGroupEnd();
     if (r != ncclSuccess) return nccl_fail(ctx, r, "ncclSend/Recv batched records");
     return r2 == ncclSuccess ? BGS_OK : nccl_fail(ctx, r2, "ncclGroupEnd");
+  }
+  bgs_status allgather(bgs_ctx* ctx, const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    ++ctx->collectives;
+    ncclResult_t r = ncclAllGather(send, recv, bytes, ncclChar, comm, s);
+    return r == ncclSuccess ? BGS_OK : nccl_fail(ctx, r, "ncclAllGather");
   }
   bool capturable() const override { return true; }
 };
@@ -430,6 +439,11 @@ struct LocalTransport : Transport {
     g->barrier();
     return BGS_OK;
   }
+  bgs_status allgather(bgs_ctx* ctx, const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+    std::vector<int64_t> cnt(ctx->world, int64_t(bytes)), zero(ctx->world, 0), roff(ctx->world);
+    for (int k = 0; k < ctx->world; ++k) roff[k] = int64_t(k) * int64_t(bytes);
+    return exchange(ctx, send, cnt.data(), zero.data(), recv, cnt.data(), roff.data(), 1, s);
+  }
   bool capturable() const override { return false; }  // host barriers order the copies
 };
 
@@ -443,6 +457,20 @@ bgs_status check_ctx(bgs_ctx* ctx) {
 }
 
 bgs_status check_stream(bgs_ctx*, void*) { return BGS_OK; }
+
+// NVTX range around every ABI stage (header-only NVTX v3: a no-op unless a tool such as Nsight
+// Systems attaches; lets a timeline show the stages of each view / batch)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// a12 at world > 1: the coarse-histogram + all-gather path (two collectives per view) unless
+// BGS_IMP=rounds selects the radix-round path (one all-reduce per round)
+bool use_imp_rounds() {
+  const char* e = getenv("BGS_IMP");
+  return e && std::strcmp(e, "rounds") == 0;
+}
 
 // a5-a7: the onesweep radix path (sort.cu); BGS_SORT=bucket selects the per-tile bucket sort
 // (bucket.cu: bit-identical order, measured no faster -- DESIGN.md §12)
@@ -567,7 +595,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2, &c->scr_dlsup, &c->bucket_cur,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2, &c->scr_dlsup, &c->bucket_cur, &c->imp_cand, &c->imp_gath,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -751,6 +779,7 @@ static void project_finish(bgs_ctx* ctx) {
 
 bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
                        const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, void* stream) {
+  NvtxRange nvtx_("bgs_project");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   CKS(project_enqueue(ctx, g, cam, gate, cull_column, flags, radius_out, stream));
@@ -764,6 +793,7 @@ bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* c
 // ---------------------------------------------------------------------------------------
 bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_owner_out, int64_t* n_recv_out,
                      void* stream) {
+  NvtxRange nvtx_("bgs_route");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 1) return fail(ctx, BGS_ERR_CONTRACT, "bgs_route before bgs_project");
@@ -859,6 +889,7 @@ bgs_status bgs_route(bgs_ctx* ctx, const int32_t* tile_owner_in, int32_t* tile_o
 // a5 + a6 + a7
 // ---------------------------------------------------------------------------------------
 bgs_status bgs_sort_tiles(bgs_ctx* ctx, void* stream) {
+  NvtxRange nvtx_("bgs_sort_tiles");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 2) return fail(ctx, BGS_ERR_CONTRACT, "bgs_sort_tiles before bgs_route");
@@ -984,6 +1015,7 @@ static RasterArgs raster_args(bgs_ctx* ctx) {
 
 bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_final, int32_t* n_contrib,
                           void* stream) {
+  NvtxRange nvtx_("bgs_raster_fwd");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 3) return fail(ctx, BGS_ERR_CONTRACT, "bgs_raster_fwd before bgs_sort_tiles");
@@ -1005,6 +1037,7 @@ bgs_status bgs_raster_fwd(bgs_ctx* ctx, uint32_t flags, float* rgb, float* t_fin
 
 bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL, const float* t_final, const int32_t* n_contrib,
                           void* stream) {
+  NvtxRange nvtx_("bgs_raster_bwd");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_raster_bwd before bgs_raster_fwd");
@@ -1021,6 +1054,7 @@ bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL, const float* t_final, c
 }
 
 bgs_status bgs_route_reverse(bgs_ctx* ctx, uint32_t flags, void* stream) {
+  NvtxRange nvtx_("bgs_route_reverse");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_route_reverse before bgs_raster_fwd");
@@ -1067,6 +1101,7 @@ bgs_status bgs_route_reverse(bgs_ctx* ctx, uint32_t flags, void* stream) {
 
 bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
                            const bgs_gaussian_grads* grads, void* stream) {
+  NvtxRange nvtx_("bgs_project_bwd");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   CKS(check_gaussians(ctx, g));
@@ -1099,6 +1134,7 @@ bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camer
 bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, const uint64_t* w_fixed,
                           const uint32_t* a_in, int32_t mass_num, int32_t mass_den, double* s_out, uint32_t* c_rad,
                           uint32_t* c_vis, uint32_t* cull_out, void* stream) {
+  NvtxRange nvtx_("bgs_importance");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (n_local < 0 || !s_out || !c_rad || !c_vis || !cull_out)
@@ -1143,6 +1179,37 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
     ctx->imp_parity ^= 1;
     CK(launch_imp_coop(a, st, cur, nxt, P_<uint32_t>(ctx->cand), mass_num, mass_den, s));
     return launched(ctx, 1);
+  }
+  if (!use_imp_rounds()) {
+    // two collectives per view (importance.cu): coarse histogram all-reduce, one host read of the
+    // crossing bin's global count, candidate all-gather, exact select on every rank
+    const int64_t HW = imp_coarse_words();
+    CKS(ensure(ctx, ctx->imp_hist, size_t(HW) * 8));
+    CK(cudaMemsetAsync(ctx->imp_hist.p, 0, size_t(HW) * 8, s));
+    unsigned long long* hist = P_<unsigned long long>(ctx->imp_hist);
+    launch_fill_bits(cull_out, n_local, s);
+    launch_imp_stats_coarse(a, hist, s);
+    CKS(launched(ctx, 2));
+    CKS(ctx->tr->allreduce_u64(ctx, hist, HW, s));
+    launch_imp_coarse_decide(st, hist, mass_num, mass_den, s);
+    CKS(launched(ctx));
+    CK(cudaMemcpyAsync(ctx->h_misc + 62, P_<char>(ctx->imp_state) + imp_state_ncand_offset(), 8,
+                       cudaMemcpyDeviceToHost, s));
+    CK(host_sync(ctx, s));
+    const int64_t ncand = ctx->h_misc[62];
+    if (ncand > 0) {
+      const int64_t words = 2 + 2 * ncand;  // [count, pad, (w, gid) x cap]; cap = global count
+      CKS(ensure(ctx, ctx->imp_cand, size_t(words) * 8));
+      CKS(ensure(ctx, ctx->imp_gath, size_t(words) * 8 * ctx->world));
+      CK(cudaMemsetAsync(ctx->imp_cand.p, 0, 16, s));
+      launch_imp_gather_cand(a, st, P_<unsigned long long>(ctx->imp_cand), s);
+      CKS(launched(ctx));
+      CKS(ctx->tr->allgather(ctx, ctx->imp_cand.p, ctx->imp_gath.p, size_t(words) * 8, s));
+      launch_imp_select_cand(st, P_<unsigned long long>(ctx->imp_gath), ctx->world, words, mass_num, mass_den, s);
+      CKS(launched(ctx));
+    }
+    launch_imp_mark(a, st, s);
+    return launched(ctx);
   }
   CKS(ensure(ctx, ctx->imp_total, 65 * 8));  // total + 64-bin MSB histogram
   CKS(ensure(ctx, ctx->imp_hist, size_t(WR * 512 + GR * 256) * 8));
@@ -1284,6 +1351,7 @@ bgs_status bgs_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera*
                          const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, float* rgb,
                          float* t_final, int32_t* n_contrib, const float* dL, const bgs_gaussian_grads* grads,
                          const bgs_importance_out* imp, void* stream) {
+  NvtxRange nvtx_("bgs_view_step");
   return view_step_impl(ctx, g, cam, gate, cull_column, flags, radius_out, rgb, t_final, n_contrib, dL, grads, imp,
                         stream, nullptr, nullptr);
 }
@@ -1300,6 +1368,7 @@ bgs_status bgs_train_view_step(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_c
                                const bgs_supervision* sup, float* rgb, float* t_final, int32_t* n_contrib,
                                float* dL_scratch, const bgs_gaussian_grads* grads, const bgs_importance_out* imp,
                                void* stream) {
+  NvtxRange nvtx_("bgs_train_view_step");
   CKS(check_ctx(ctx));
   CKS(check_sup(ctx, sup, true));
   if (!dL_scratch) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "dL_scratch is NULL");
@@ -1797,6 +1866,7 @@ extern "C" {
 bgs_status bgs_batch_step(bgs_ctx* ctx, int32_t n_views, const bgs_gaussians* g, const bgs_lod_gate* gate,
                           uint32_t flags, const bgs_batch_view* views, const bgs_gaussian_grads* grads,
                           const bgs_importance_out* imp, void* stream) {
+  NvtxRange nvtx_("bgs_batch_step");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   CKS(check_gaussians(ctx, g));
@@ -1914,6 +1984,7 @@ extern "C" {
 // ---------------------------------------------------------------------------------------
 bgs_status bgs_loss_photo(bgs_ctx* ctx, const float* rgb, const float* target, float lambda, float batch_inv,
                           float* dL_drgb, double* out, void* stream) {
+  NvtxRange nvtx_("bgs_loss_photo");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (ctx->stage < 4) return fail(ctx, BGS_ERR_CONTRACT, "bgs_loss_photo before bgs_raster_fwd");
@@ -1966,6 +2037,7 @@ bgs_status bgs_loss_photo(bgs_ctx* ctx, const float* rgb, const float* target, f
 
 bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, float beta, const bgs_gaussian_grads* grads,
                           double* out, void* stream) {
+  NvtxRange nvtx_("bgs_loss_scale");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   CKS(check_gaussians(ctx, g));
@@ -1998,6 +2070,7 @@ bgs_status bgs_loss_scale(bgs_ctx* ctx, const bgs_gaussians* g, float beta, cons
 bgs_status bgs_adam_step(bgs_ctx* ctx, const bgs_train_params* p, const bgs_gaussian_grads* grads,
                          const bgs_gaussians_out* act, const uint32_t* visible, const bgs_adam_hparams* h,
                          void* stream) {
+  NvtxRange nvtx_("bgs_adam_step");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (!p || !grads || !act || !h) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "adam: NULL argument");
@@ -2093,6 +2166,7 @@ static bool planes_ok(const bgs_train_params* p) {
 bgs_status bgs_densify_apply(bgs_ctx* ctx, const bgs_train_params* in, const uint8_t* lod_in, const float* stat,
                              const uint32_t* count, const bgs_densify_params* dp, const bgs_train_params* out,
                              uint8_t* lod_out, const bgs_gaussians_out* act_out, int64_t* n_out, void* stream) {
+  NvtxRange nvtx_("bgs_densify_apply");
   CKS(check_ctx(ctx));
   CKS(check_stream(ctx, stream));
   if (!in || !out || !dp || !n_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "densify: NULL argument");

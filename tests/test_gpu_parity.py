@@ -251,6 +251,82 @@ def test_importance_dense_path_bit_exact():
     ctx.close()
 
 
+@pytest.mark.parametrize("mode", ["coarse", "rounds"])
+def test_importance_selection_world3(mode, monkeypatch):
+    """a12 at world > 1 on identical w_fixed (dense path, index-parity shards over an in-process group
+    of 3): the two-collective path (coarse histogram all-reduce + crossing-bin all-gather, default) and
+    the radix-round path (BGS_IMP=rounds) both select bit-exactly the oracle's global top-99% set,
+    including heavy ties (gid order), one dominant item, heavy tails and an empty view."""
+    import threading
+    import paper_2605_13794_b200.bgs as B
+    if mode == "rounds":
+        monkeypatch.setenv("BGS_IMP", "rounds")
+    M = 3
+    rng = np.random.default_rng(11)
+    for trial in range(7):
+        n = int(rng.integers(2, 120_000))
+        if trial == 0:
+            w = np.zeros(n, np.uint64)
+        elif trial == 1:
+            w = (rng.integers(0, 4, n) * (1 << 20)).astype(np.uint64)  # massive ties
+        elif trial == 2:
+            w = rng.integers(1, 1 << 20, n).astype(np.uint64)
+            w[rng.integers(0, n)] = np.uint64(1 << 45)  # one dominant item
+        elif trial == 3:
+            w = np.exp(rng.uniform(np.log(1e3), np.log(1e12), n)).astype(np.uint64)
+        elif trial == 4:
+            w = np.full(n, np.uint64(1 << 30)) + rng.integers(0, 1 << 8, n).astype(np.uint64)
+        elif trial == 5:
+            w = np.full(n, np.uint64(12345))  # every item in one coarse bin, all tied
+        else:
+            w = rng.integers(0, 1 << 40, n).astype(np.uint64) * rng.integers(0, 2, n).astype(np.uint64)
+        a = np.where(w > 0, rng.integers(1, 300, n), 0).astype(np.uint32)
+        rad = np.where(a > 0, 4, 0).astype(np.int32)
+        ref = O.importance(rad, w, a)
+        ctxs = B.Context.local_group(M, 0)
+        res = [None] * M
+        errs = []
+
+        def run(r):
+            try:
+                torch.cuda.set_device(0)
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    dev = "cuda"
+                    ids = np.arange(r, n, M)
+                    m = len(ids)
+                    s_ = torch.zeros(max(m, 1), dtype=torch.float64, device=dev)
+                    cr = torch.zeros(max(m, 1), dtype=torch.int32, device=dev)
+                    cv = torch.zeros(max(m, 1), dtype=torch.int32, device=dev)
+                    cu = torch.zeros(max(1, (m + 31) // 32), dtype=torch.int32, device=dev)
+                    B.bgs_importance(ctxs[r], m, torch.from_numpy(rad[ids]).to(dev),
+                                     torch.from_numpy(w[ids].view(np.int64)).to(dev),
+                                     torch.from_numpy(a[ids].view(np.int32)).to(dev), s_, cr, cv, cu, stream=st)
+                    st.synchronize()
+                    res[r] = (cv.cpu().numpy()[:m].view(np.uint32), S.unpack_bits(cu.cpu().numpy(), m),
+                              ctxs[r].batch_stats()["collectives"])
+            except Exception as e:  # pragma: no cover
+                errs.append(e)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(M)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for c in ctxs:
+            c.close()
+        if errs:
+            raise errs[0]
+        cvis = np.zeros(n, np.uint32)
+        cull = np.zeros(n, bool)
+        for r in range(M):
+            cvis[r::M], cull[r::M] = res[r][0], res[r][1]
+        assert np.array_equal(cvis, ref["c_vis"]), (mode, trial)
+        assert np.array_equal(cull, S.unpack_bits(ref["cull"], n)), (mode, trial)
+        if mode == "coarse":
+            assert all(res[r][2] <= 2 for r in range(M)), [res[r][2] for r in range(M)]
+
+
 @pytest.mark.parametrize("M", [2, 3, 4])
 def test_multirank_local_group_parity(tiny_scene, tiny_run, M):
     """The M > 1 kernels (tile costs, owner map, dest masks, pack, exchange, reverse gather-sum,
