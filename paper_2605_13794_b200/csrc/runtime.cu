@@ -472,6 +472,12 @@ bool use_imp_rounds() {
   return e && std::strcmp(e, "rounds") == 0;
 }
 
+// a12 at world 1: the cooperative single-launch path when BGS_IMP=coop, else the coarse path
+bool use_imp_coop() {
+  const char* e = getenv("BGS_IMP");
+  return e && std::strcmp(e, "coop") == 0;
+}
+
 // a5-a7: the onesweep radix path (sort.cu); BGS_SORT=bucket selects the per-tile bucket sort
 // (bucket.cu: bit-identical order, measured no faster -- DESIGN.md §12)
 bool use_bucket_sort() {
@@ -1165,6 +1171,26 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   const int WR = imp_w_rounds(), GR = imp_g_rounds();
   CKS(ensure(ctx, ctx->imp_state, kImpStateBytes));
   ImpState* st = static_cast<ImpState*>(ctx->imp_state.p);
+  if (ctx->world == 1 && !use_imp_coop()) {
+    // world 1: the coarse-histogram path without collectives or host reads -- every item with w > 0
+    // in the crossing bin is gathered into a buffer of capacity n_items (an upper bound), then the
+    // same exact single-CTA selection; five short kernels instead of a cooperative grid that holds
+    // its SMs at grid barriers while other views are in flight
+    const int64_t HW = imp_coarse_words();
+    CKS(ensure(ctx, ctx->imp_hist, size_t(HW) * 8));
+    CK(cudaMemsetAsync(ctx->imp_hist.p, 0, size_t(HW) * 8, s));
+    const int64_t words = 2 + 2 * std::max<int64_t>(a.n_items, 1);
+    CKS(ensure(ctx, ctx->imp_cand, size_t(words) * 8));
+    CK(cudaMemsetAsync(ctx->imp_cand.p, 0, 16, s));
+    unsigned long long* hist = P_<unsigned long long>(ctx->imp_hist);
+    launch_fill_bits(cull_out, n_local, s);
+    launch_imp_stats_coarse(a, hist, s);
+    launch_imp_coarse_decide(st, hist, mass_num, mass_den, s);
+    launch_imp_gather_cand(a, st, P_<unsigned long long>(ctx->imp_cand), s);
+    launch_imp_select_cand(st, P_<unsigned long long>(ctx->imp_cand), 1, words, mass_num, mass_den, s);
+    launch_imp_mark(a, st, s);
+    return launched(ctx, 6);
+  }
   if (ctx->world == 1) {
     // one cooperative launch; its histogram sets alternate between calls and each call zeroes
     // the other one, so only a freshly allocated pair is cleared here

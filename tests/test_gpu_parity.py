@@ -204,7 +204,15 @@ def test_importance_parity(tiny_run):
     np.testing.assert_allclose(gs.s[keep], ref2["s"][keep], rtol=2e-5, atol=1e-9)
 
 
-def test_importance_dense_path_bit_exact():
+@pytest.fixture(params=["coarse", "coop"])
+def imp_mode(request, monkeypatch):
+    """a12 at world 1: the coarse-histogram path (default) and the cooperative one (BGS_IMP=coop)."""
+    if request.param == "coop":
+        monkeypatch.setenv("BGS_IMP", "coop")
+    return request.param
+
+
+def test_importance_dense_path_bit_exact(imp_mode):
     """bgs_importance with caller-supplied dense w_fixed equals the oracle selection on the same
     values, including heavy ties (count-only gid select) and an empty view."""
     import paper_2605_13794_b200.bgs as B
