@@ -611,18 +611,25 @@ __global__ void __launch_bounds__(256) k_imp_select_cand(ImpState* st, const uns
       for (int64_t i = threadIdx.x; i < n; i += blockDim.x) fn(blk[2 + 2 * i], uint32_t(blk[3 + 2 * i]));
     }
   };
+  const int lane = threadIdx.x & 31;
   for (int r = int(S.r0); r < kWRounds && !S.final_; ++r) {
     s_cnt[threadIdx.x] = 0;
     s_mass[threadIdx.x] = 0;
     __syncthreads();
     const int shift = 8 * (kWRounds - 1 - r);
     const unsigned long long prefix = S.prefix;
-    for_each([&](unsigned long long w, uint32_t) {
-      if (shift + 8 < 64 && (w >> (shift + 8)) != prefix) return;
-      const uint32_t d = uint32_t((w >> shift) & 255u);
-      atomicAdd(&s_cnt[d], 1ull);
-      atomicAdd(&s_mass[d], w);
-    });
+    // warp-uniform trip counts so the warp-aggregated histogram (most candidates share a digit in
+    // the first rounds: per-lane 64-bit shared atomics would serialise) can use warp collectives
+    for (int rr = 0; rr < world; ++rr) {
+      const unsigned long long* blk = gath + rr * stride;
+      const int64_t n = int64_t(blk[0]);
+      for (int64_t base = threadIdx.x & ~31; base < n; base += blockDim.x) {
+        const int64_t i = base + lane;
+        const unsigned long long w = i < n ? blk[2 + 2 * i] : 0ull;
+        const bool cand = i < n && !(shift + 8 < 64 && (w >> (shift + 8)) != prefix);
+        hist_add(cand, cand ? uint32_t((w >> shift) & 255u) : 256u + lane, w, lane, s_cnt, s_mass);
+      }
+    }
     __syncthreads();
     decide_body(&S, r, s_cnt, num, den);  // reads hist[d] counts, hist[256 + d] masses
   }
