@@ -77,6 +77,8 @@ struct bgs_ctx {
   cudaEvent_t ev_counters = nullptr;         // counters copied to the host (bgs_project)
   cudaEvent_t ev_geom = nullptr;             // geometry kernels done (bgs_project)
   cudaStream_t side = nullptr;               // carries the counters copy off the working stream
+  cudaStream_t hi = nullptr;                 // high-priority stream for the latency-bound stages (view steps)
+  cudaEvent_t ev_hi_fork = nullptr, ev_hi_join = nullptr;
   bool stage_timing = false, stage_recorded = false;  // bgs_set_stage_timing / bgs_stage_times
   cudaStream_t h2d = nullptr, d2h = nullptr;          // host-buffer step: copy streams
   cudaEvent_t ev_in = nullptr, ev_dl = nullptr, ev_fwd = nullptr, ev_out = nullptr;
@@ -465,6 +467,14 @@ struct NvtxRange {
   ~NvtxRange() { nvtxRangePop(); }
 };
 
+// View steps run their latency-bound stages (a1-a7, and a11 with BGS_PRIO=2) on a high-priority
+// stream of the ctx, so that with views in flight their short kernels are scheduled ahead of the
+// large compositing grids of the other views (BGS_PRIO=0: everything on the caller's stream)
+int prio_mode() {
+  const char* e = getenv("BGS_PRIO");
+  return e ? atoi(e) : 1;
+}
+
 // a12 at world > 1: the coarse-histogram + all-gather path (two collectives per view) unless
 // BGS_IMP=rounds selects the radix-round path (one all-reduce per round)
 bool use_imp_rounds() {
@@ -611,6 +621,9 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
   if (c->ev_counters) cudaEventDestroy(c->ev_counters);
   if (c->ev_geom) cudaEventDestroy(c->ev_geom);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->hi) cudaStreamDestroy(c->hi);
+  if (c->ev_hi_fork) cudaEventDestroy(c->ev_hi_fork);
+  if (c->ev_hi_join) cudaEventDestroy(c->ev_hi_join);
   for (cudaEvent_t e : c->stage_ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {c->ev_in, c->ev_dl, c->ev_fwd, c->ev_out, c->ev_in_free[0], c->ev_in_free[1]})
@@ -1336,12 +1349,31 @@ static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs
   };
   if (ctx->stage_timing && !ctx->stage_ev[0])
     for (auto& e : ctx->stage_ev) CK(cudaEventCreate(&e));
+  // latency-bound stages on the high-priority stream (not while stage events time the step)
+  const int pm = ctx->stage_timing ? 0 : prio_mode();
+  void* hs = stream;
+  if (pm > 0) {
+    if (!ctx->hi) {
+      int least = 0, greatest = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      CK(cudaStreamCreateWithPriority(&ctx->hi, cudaStreamNonBlocking, greatest));
+      CK(cudaEventCreateWithFlags(&ctx->ev_hi_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_hi_join, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(ctx->ev_hi_fork, s));
+    CK(cudaStreamWaitEvent(ctx->hi, ctx->ev_hi_fork, 0));
+    hs = ctx->hi;
+  }
   CKS(mark(0));
-  CKS(bgs_project(ctx, g, cam, gate, cull_column, flags, radius_out, stream));
+  CKS(bgs_project(ctx, g, cam, gate, cull_column, flags, radius_out, hs));
   CKS(mark(1));
-  CKS(bgs_route(ctx, nullptr, nullptr, nullptr, stream));
+  CKS(bgs_route(ctx, nullptr, nullptr, nullptr, hs));
   CKS(mark(2));
-  CKS(bgs_sort_tiles(ctx, stream));
+  CKS(bgs_sort_tiles(ctx, hs));
+  if (pm > 0) {
+    CK(cudaEventRecord(ctx->ev_hi_join, ctx->hi));
+    CK(cudaStreamWaitEvent(s, ctx->ev_hi_join, 0));
+  }
   CKS(mark(3));
   CKS(bgs_raster_fwd(ctx, flags, rgb, t_final, n_contrib, stream));
   if (fwd_done) CK(cudaEventRecord(fwd_done, s));
@@ -1363,7 +1395,17 @@ static bgs_status view_step_impl(bgs_ctx* ctx, const bgs_gaussians* g, const bgs
   // no backward in this step (scoring sweep): only (w, a) travel back, 12 B per record
   CKS(bgs_route_reverse(ctx, dL ? 0u : uint32_t(BGS_IMPORTANCE_ONLY), stream));
   CKS(mark(7));
-  if (dL && grads) CKS(bgs_project_bwd(ctx, g, cam, grads, stream));
+  if (dL && grads) {
+    if (pm > 1) {
+      CK(cudaEventRecord(ctx->ev_hi_fork, s));
+      CK(cudaStreamWaitEvent(ctx->hi, ctx->ev_hi_fork, 0));
+      CKS(bgs_project_bwd(ctx, g, cam, grads, ctx->hi));
+      CK(cudaEventRecord(ctx->ev_hi_join, ctx->hi));
+      CK(cudaStreamWaitEvent(s, ctx->ev_hi_join, 0));
+    } else {
+      CKS(bgs_project_bwd(ctx, g, cam, grads, stream));
+    }
+  }
   CKS(mark(8));
   if (imp)
     CKS(bgs_importance(ctx, g->n_local, radius_out, nullptr, nullptr, imp->mass_num, imp->mass_den, imp->s,

@@ -12,6 +12,7 @@ import paper_2605_13794_b200.bgs as B  # noqa: E402
 
 nviews = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 cfg = sys.argv[2] if len(sys.argv) > 2 else "rubble"
+with_imp = len(sys.argv) > 3 and sys.argv[3] == "imp"
 scene = S.gen_city(cfg, V=64)
 g = B.GaussianPlanes.from_scene(scene, "cuda")
 ctx = B.Context(0, 1, 0)
@@ -26,10 +27,15 @@ rgb, T = torch.zeros(3, H, W, device="cuda"), torch.zeros(H, W, device="cuda")
 nc = torch.zeros(H, W, dtype=torch.int32, device="cuda")
 dl = torch.from_numpy(S.grad_image(H, W)).cuda()
 grads = g.zeros_grads()
+imp = None
+if with_imp:
+    imp = B.importance_out(torch.zeros(n, dtype=torch.float64, device="cuda"), torch.zeros(n, dtype=torch.int32, device="cuda"),
+                           torch.zeros(n, dtype=torch.int32, device="cuda"),
+                           torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda"))
 st = torch.cuda.Stream()
 with torch.cuda.stream(st):
     for v in range(nviews):
         B.bgs_view_step(ctx, g, B.camera(scene.cameras[(5 + v) % 64]), None, None, 0, radius, rgb, T, nc, dl, grads,
-                        None, st)
+                        imp, st)
     st.synchronize()
 print("ok", ctx.query())
