@@ -7,6 +7,8 @@
 //   SH colour -> dsh and, through the normalised view direction, -> dmu (R2 clamp mask).
 // One thread per projected local record; gradients are accumulated (+=) into the caller's
 // parameter-shaped buffers (each local Gaussian has at most one record per view).
+#include <cstdlib>
+
 #include "bgs_internal.cuh"
 
 namespace bgs {
@@ -236,12 +238,113 @@ __global__ void __launch_bounds__(256) k_project_bwd_sh(ProjectBwdArgs a) {
   }
 }
 
+// Two threads per record (adjacent lanes, h = lane & 1): thread h loads the SH coefficients
+// 8h..8h+7 (six of the row's twelve float4) and writes their gradients; the colour (clamp test),
+// and the direction gradient are completed with one shuffle each.  Half the registers per thread
+// of k_project_bwd_sh, so twice the warps (and 192-B row loads) in flight.
+__global__ void __launch_bounds__(256) k_project_bwd_sh2(ProjectBwdArgs a) {
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t f = t >> 1;
+  const int h = int(threadIdx.x & 1);
+  const bool live = f < a.F;
+  const int64_t fr = live ? f : 0;  // dead threads follow record 0 so the pair's shuffles stay aligned
+  const uint32_t i = a.rec_lidx[fr];
+  const CameraK& cm = a.cam;
+  const float4 mo = __ldg(a.mean_opac + i);
+  const float* g = a.acc[fr].g;
+  const float g6 = g[6], g7 = g[7], g8 = g[8];
+  const float ddx = mo.x - cm.campos[0], ddy = mo.y - cm.campos[1], ddz = mo.z - cm.campos[2];
+  const float len = sqrtf(ddx * ddx + ddy * ddy + ddz * ddz), il = 1.f / len;
+  const float X = ddx * il, Y = ddy * il, Z = ddz * il;
+  const float xx = X * X, yy = Y * Y, zz = Z * Z, xy = X * Y, yz = Y * Z, xz = X * Z;
+  float Yb[16];
+  Yb[0] = 0.28209479177387814f;
+  Yb[1] = -SHC1 * Y;
+  Yb[2] = SHC1 * Z;
+  Yb[3] = -SHC1 * X;
+  Yb[4] = SHC2[0] * xy;
+  Yb[5] = SHC2[1] * yz;
+  Yb[6] = SHC2[2] * (2.f * zz - xx - yy);
+  Yb[7] = SHC2[3] * xz;
+  Yb[8] = SHC2[4] * (xx - yy);
+  Yb[9] = SHC3[0] * Y * (3.f * xx - yy);
+  Yb[10] = SHC3[1] * xy * Z;
+  Yb[11] = SHC3[2] * Y * (4.f * zz - xx - yy);
+  Yb[12] = SHC3[3] * Z * (2.f * zz - 3.f * xx - 3.f * yy);
+  Yb[13] = SHC3[4] * X * (4.f * zz - xx - yy);
+  Yb[14] = SHC3[5] * Z * (xx - yy);
+  Yb[15] = SHC3[6] * X * (xx - 3.f * yy);
+  const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i) + 6 * h;
+  float v[24];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const float4 q = __ldg(shp + k);
+    v[4 * k] = q.x;
+    v[4 * k + 1] = q.y;
+    v[4 * k + 2] = q.z;
+    v[4 * k + 3] = q.w;
+  }
+  // colour: this half's coefficients, then the pair's sum
+  float cp[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    float c = h == 0 ? 0.5f : 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += Yb[8 * h + k] * v[3 * k + ch];
+    cp[ch] = c;
+  }
+  float dcol[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const float c = cp[ch] + __shfl_xor_sync(0xffffffffu, cp[ch], 1);
+    dcol[ch] = c < 0.f ? 0.f : (ch == 0 ? g6 : (ch == 1 ? g7 : g8));
+  }
+  float sk[8];  // sk[k] for coefficient 8h + k
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sk[k] = dcol[0] * v[3 * k] + dcol[1] * v[3 * k + 1] + dcol[2] * v[3 * k + 2];
+  // d(sum_k sk Y_k)/d(x, y, z): the terms of this half's coefficients (0..7 or 8..15)
+  float ddir[3];
+  if (h == 0) {
+    ddir[0] = -SHC1 * sk[3] + SHC2[0] * Y * sk[4] - 2.f * SHC2[2] * X * sk[6] + SHC2[3] * Z * sk[7];
+    ddir[1] = -SHC1 * sk[1] + SHC2[0] * X * sk[4] + SHC2[1] * Z * sk[5] - 2.f * SHC2[2] * Y * sk[6];
+    ddir[2] = SHC1 * sk[2] + SHC2[1] * Y * sk[5] + 4.f * SHC2[2] * Z * sk[6] + SHC2[3] * X * sk[7];
+  } else {
+    ddir[0] = 2.f * SHC2[4] * X * sk[0] + 6.f * SHC3[0] * xy * sk[1] + SHC3[1] * yz * sk[2] -
+              2.f * SHC3[2] * xy * sk[3] - 6.f * SHC3[3] * xz * sk[4] + SHC3[4] * (4.f * zz - 3.f * xx - yy) * sk[5] +
+              2.f * SHC3[5] * xz * sk[6] + 3.f * SHC3[6] * (xx - yy) * sk[7];
+    ddir[1] = -2.f * SHC2[4] * Y * sk[0] + 3.f * SHC3[0] * (xx - yy) * sk[1] + SHC3[1] * xz * sk[2] +
+              SHC3[2] * (4.f * zz - xx - 3.f * yy) * sk[3] - 6.f * SHC3[3] * yz * sk[4] - 2.f * SHC3[4] * xy * sk[5] -
+              2.f * SHC3[5] * yz * sk[6] - 6.f * SHC3[6] * xy * sk[7];
+    ddir[2] = SHC3[1] * xy * sk[2] + 8.f * SHC3[2] * yz * sk[3] + SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * sk[4] +
+              8.f * SHC3[4] * xz * sk[5] + SHC3[5] * (xx - yy) * sk[6];
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) ddir[d] += __shfl_xor_sync(0xffffffffu, ddir[d], 1);
+  if (!live) return;
+  if (h == 0) {
+    const float dot = ddir[0] * X + ddir[1] * Y + ddir[2] * Z;
+    atomicAdd(a.g_mean_opac + i, make_float4((ddir[0] - X * dot) * il, (ddir[1] - Y * dot) * il,
+                                             (ddir[2] - Z * dot) * il, 0.f));
+  }
+  float4* gsh = reinterpret_cast<float4*>(a.g_sh + size_t(48) * i) + 6 * h;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const int e = 4 * k;  // float index within this half (coefficient 8h + e / 3, channel e % 3)
+    atomicAdd(gsh + k, make_float4(Yb[8 * h + (e) / 3] * dcol[(e) % 3], Yb[8 * h + (e + 1) / 3] * dcol[(e + 1) % 3],
+                                   Yb[8 * h + (e + 2) / 3] * dcol[(e + 2) % 3], Yb[8 * h + (e + 3) / 3] * dcol[(e + 3) % 3]));
+  }
+}
+
 }  // namespace
 
 void launch_project_bwd(const ProjectBwdArgs& a, cudaStream_t s) {
   if (a.F <= 0) return;
   k_project_bwd<<<unsigned((a.F + 127) / 128), 128, 0, s>>>(a);
-  k_project_bwd_sh<<<unsigned((a.F + 255) / 256), 256, 0, s>>>(a);
+  const char* e = getenv("BGS_SH_BWD");  // A/B: 1 = one thread per record
+  if (e && atoi(e) == 1)
+    k_project_bwd_sh<<<unsigned((a.F + 255) / 256), 256, 0, s>>>(a);
+  else
+    k_project_bwd_sh2<<<unsigned((2 * a.F + 255) / 256), 256, 0, s>>>(a);
 }
 
 }  // namespace bgs
