@@ -238,16 +238,21 @@ __global__ void __launch_bounds__(256) k_project_bwd_sh(ProjectBwdArgs a) {
   }
 }
 
-// Two threads per record (adjacent lanes, h = lane & 1): thread h loads the SH coefficients
-// 8h..8h+7 (six of the row's twelve float4) and writes their gradients; the colour (clamp test),
-// and the direction gradient are completed with one shuffle each.  Half the registers per thread
-// of k_project_bwd_sh, so twice the warps (and 192-B row loads) in flight.
-__global__ void __launch_bounds__(256) k_project_bwd_sh2(ProjectBwdArgs a) {
+// kT threads per record (adjacent lanes; 16 / kT SH coefficients = 12 / kT float4 of the row each):
+// the colour (clamp test) and the direction gradient (per-coefficient basis derivatives) are
+// completed with shuffles over the group.  Fewer registers per thread than one thread per record,
+// so more warps and more of the scattered 192-B row loads in flight: project_bwd 0.142 (1 thread)
+// -> 0.127 (2) -> 0.119 ms (4) per Rubble view, 1462 -> 1494 -> 1507 views/s in flight.
+template <int kT>
+__global__ void __launch_bounds__(256) k_project_bwd_shn(ProjectBwdArgs a) {
+  constexpr int kC = 16 / kT;      // coefficients per thread
+  constexpr int kV = 3 * kC;       // floats per thread
+  constexpr int kQ = kV / 4;       // float4 per thread
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t f = t >> 1;
-  const int h = int(threadIdx.x & 1);
+  const int64_t f = t / kT;
+  const int h = int(threadIdx.x % kT);
   const bool live = f < a.F;
-  const int64_t fr = live ? f : 0;  // dead threads follow record 0 so the pair's shuffles stay aligned
+  const int64_t fr = live ? f : 0;
   const uint32_t i = a.rec_lidx[fr];
   const CameraK& cm = a.cam;
   const float4 mo = __ldg(a.mean_opac + i);
@@ -257,81 +262,86 @@ __global__ void __launch_bounds__(256) k_project_bwd_sh2(ProjectBwdArgs a) {
   const float len = sqrtf(ddx * ddx + ddy * ddy + ddz * ddz), il = 1.f / len;
   const float X = ddx * il, Y = ddy * il, Z = ddz * il;
   const float xx = X * X, yy = Y * Y, zz = Z * Z, xy = X * Y, yz = Y * Z, xz = X * Z;
-  float Yb[16];
-  Yb[0] = 0.28209479177387814f;
-  Yb[1] = -SHC1 * Y;
-  Yb[2] = SHC1 * Z;
-  Yb[3] = -SHC1 * X;
-  Yb[4] = SHC2[0] * xy;
-  Yb[5] = SHC2[1] * yz;
-  Yb[6] = SHC2[2] * (2.f * zz - xx - yy);
-  Yb[7] = SHC2[3] * xz;
-  Yb[8] = SHC2[4] * (xx - yy);
-  Yb[9] = SHC3[0] * Y * (3.f * xx - yy);
-  Yb[10] = SHC3[1] * xy * Z;
-  Yb[11] = SHC3[2] * Y * (4.f * zz - xx - yy);
-  Yb[12] = SHC3[3] * Z * (2.f * zz - 3.f * xx - 3.f * yy);
-  Yb[13] = SHC3[4] * X * (4.f * zz - xx - yy);
-  Yb[14] = SHC3[5] * Z * (xx - yy);
-  Yb[15] = SHC3[6] * X * (xx - 3.f * yy);
-  const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i) + 6 * h;
-  float v[24];
+  float Yb[kC], dY[kC][3];
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {
+  for (int c = 0; c < kC; ++c) {
+    const int k = kC * h + c;
+    float y0 = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
+    switch (k) {
+      case 0: y0 = 0.28209479177387814f; break;
+      case 1: y0 = -SHC1 * Y; dy = -SHC1; break;
+      case 2: y0 = SHC1 * Z; dz = SHC1; break;
+      case 3: y0 = -SHC1 * X; dx = -SHC1; break;
+      case 4: y0 = SHC2[0] * xy; dx = SHC2[0] * Y; dy = SHC2[0] * X; break;
+      case 5: y0 = SHC2[1] * yz; dy = SHC2[1] * Z; dz = SHC2[1] * Y; break;
+      case 6: y0 = SHC2[2] * (2.f * zz - xx - yy); dx = -2.f * SHC2[2] * X; dy = -2.f * SHC2[2] * Y;
+              dz = 4.f * SHC2[2] * Z; break;
+      case 7: y0 = SHC2[3] * xz; dx = SHC2[3] * Z; dz = SHC2[3] * X; break;
+      case 8: y0 = SHC2[4] * (xx - yy); dx = 2.f * SHC2[4] * X; dy = -2.f * SHC2[4] * Y; break;
+      case 9: y0 = SHC3[0] * Y * (3.f * xx - yy); dx = 6.f * SHC3[0] * xy; dy = 3.f * SHC3[0] * (xx - yy); break;
+      case 10: y0 = SHC3[1] * xy * Z; dx = SHC3[1] * yz; dy = SHC3[1] * xz; dz = SHC3[1] * xy; break;
+      case 11: y0 = SHC3[2] * Y * (4.f * zz - xx - yy); dx = -2.f * SHC3[2] * xy;
+               dy = SHC3[2] * (4.f * zz - xx - 3.f * yy); dz = 8.f * SHC3[2] * yz; break;
+      case 12: y0 = SHC3[3] * Z * (2.f * zz - 3.f * xx - 3.f * yy); dx = -6.f * SHC3[3] * xz;
+               dy = -6.f * SHC3[3] * yz; dz = SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy); break;
+      case 13: y0 = SHC3[4] * X * (4.f * zz - xx - yy); dx = SHC3[4] * (4.f * zz - 3.f * xx - yy);
+               dy = -2.f * SHC3[4] * xy; dz = 8.f * SHC3[4] * xz; break;
+      case 14: y0 = SHC3[5] * Z * (xx - yy); dx = 2.f * SHC3[5] * xz; dy = -2.f * SHC3[5] * yz;
+               dz = SHC3[5] * (xx - yy); break;
+      default: y0 = SHC3[6] * X * (xx - 3.f * yy); dx = 3.f * SHC3[6] * (xx - yy); dy = -6.f * SHC3[6] * xy; break;
+    }
+    Yb[c] = y0;
+    dY[c][0] = dx;
+    dY[c][1] = dy;
+    dY[c][2] = dz;
+  }
+  const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i) + kQ * h;
+  float v[kV];
+#pragma unroll
+  for (int k = 0; k < kQ; ++k) {
     const float4 q = __ldg(shp + k);
     v[4 * k] = q.x;
     v[4 * k + 1] = q.y;
     v[4 * k + 2] = q.z;
     v[4 * k + 3] = q.w;
   }
-  // colour: this half's coefficients, then the pair's sum
   float cp[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     float c = h == 0 ? 0.5f : 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) c += Yb[8 * h + k] * v[3 * k + ch];
+    for (int k = 0; k < kC; ++k) c += Yb[k] * v[3 * k + ch];
+#pragma unroll
+    for (int o = 1; o < kT; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     cp[ch] = c;
   }
   float dcol[3];
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    const float c = cp[ch] + __shfl_xor_sync(0xffffffffu, cp[ch], 1);
-    dcol[ch] = c < 0.f ? 0.f : (ch == 0 ? g6 : (ch == 1 ? g7 : g8));
-  }
-  float sk[8];  // sk[k] for coefficient 8h + k
+  for (int ch = 0; ch < 3; ++ch) dcol[ch] = cp[ch] < 0.f ? 0.f : (ch == 0 ? g6 : (ch == 1 ? g7 : g8));
+  float ddir[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-  for (int k = 0; k < 8; ++k) sk[k] = dcol[0] * v[3 * k] + dcol[1] * v[3 * k + 1] + dcol[2] * v[3 * k + 2];
-  // d(sum_k sk Y_k)/d(x, y, z): the terms of this half's coefficients (0..7 or 8..15)
-  float ddir[3];
-  if (h == 0) {
-    ddir[0] = -SHC1 * sk[3] + SHC2[0] * Y * sk[4] - 2.f * SHC2[2] * X * sk[6] + SHC2[3] * Z * sk[7];
-    ddir[1] = -SHC1 * sk[1] + SHC2[0] * X * sk[4] + SHC2[1] * Z * sk[5] - 2.f * SHC2[2] * Y * sk[6];
-    ddir[2] = SHC1 * sk[2] + SHC2[1] * Y * sk[5] + 4.f * SHC2[2] * Z * sk[6] + SHC2[3] * X * sk[7];
-  } else {
-    ddir[0] = 2.f * SHC2[4] * X * sk[0] + 6.f * SHC3[0] * xy * sk[1] + SHC3[1] * yz * sk[2] -
-              2.f * SHC3[2] * xy * sk[3] - 6.f * SHC3[3] * xz * sk[4] + SHC3[4] * (4.f * zz - 3.f * xx - yy) * sk[5] +
-              2.f * SHC3[5] * xz * sk[6] + 3.f * SHC3[6] * (xx - yy) * sk[7];
-    ddir[1] = -2.f * SHC2[4] * Y * sk[0] + 3.f * SHC3[0] * (xx - yy) * sk[1] + SHC3[1] * xz * sk[2] +
-              SHC3[2] * (4.f * zz - xx - 3.f * yy) * sk[3] - 6.f * SHC3[3] * yz * sk[4] - 2.f * SHC3[4] * xy * sk[5] -
-              2.f * SHC3[5] * yz * sk[6] - 6.f * SHC3[6] * xy * sk[7];
-    ddir[2] = SHC3[1] * xy * sk[2] + 8.f * SHC3[2] * yz * sk[3] + SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * sk[4] +
-              8.f * SHC3[4] * xz * sk[5] + SHC3[5] * (xx - yy) * sk[6];
+  for (int k = 0; k < kC; ++k) {
+    const float sk = dcol[0] * v[3 * k] + dcol[1] * v[3 * k + 1] + dcol[2] * v[3 * k + 2];
+    ddir[0] += sk * dY[k][0];
+    ddir[1] += sk * dY[k][1];
+    ddir[2] += sk * dY[k][2];
   }
 #pragma unroll
-  for (int d = 0; d < 3; ++d) ddir[d] += __shfl_xor_sync(0xffffffffu, ddir[d], 1);
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int o = 1; o < kT; o <<= 1) ddir[d] += __shfl_xor_sync(0xffffffffu, ddir[d], o);
   if (!live) return;
   if (h == 0) {
     const float dot = ddir[0] * X + ddir[1] * Y + ddir[2] * Z;
     atomicAdd(a.g_mean_opac + i, make_float4((ddir[0] - X * dot) * il, (ddir[1] - Y * dot) * il,
                                              (ddir[2] - Z * dot) * il, 0.f));
   }
-  float4* gsh = reinterpret_cast<float4*>(a.g_sh + size_t(48) * i) + 6 * h;
+  float4* gsh = reinterpret_cast<float4*>(a.g_sh + size_t(48) * i) + kQ * h;
 #pragma unroll
-  for (int k = 0; k < 6; ++k) {
-    const int e = 4 * k;  // float index within this half (coefficient 8h + e / 3, channel e % 3)
-    atomicAdd(gsh + k, make_float4(Yb[8 * h + (e) / 3] * dcol[(e) % 3], Yb[8 * h + (e + 1) / 3] * dcol[(e + 1) % 3],
-                                   Yb[8 * h + (e + 2) / 3] * dcol[(e + 2) % 3], Yb[8 * h + (e + 3) / 3] * dcol[(e + 3) % 3]));
+  for (int k = 0; k < kQ; ++k) {
+    const int e = 4 * k;
+    atomicAdd(gsh + k, make_float4(Yb[(e) / 3] * dcol[(e) % 3], Yb[(e + 1) / 3] * dcol[(e + 1) % 3],
+                                   Yb[(e + 2) / 3] * dcol[(e + 2) % 3], Yb[(e + 3) / 3] * dcol[(e + 3) % 3]));
   }
 }
 
@@ -340,11 +350,14 @@ __global__ void __launch_bounds__(256) k_project_bwd_sh2(ProjectBwdArgs a) {
 void launch_project_bwd(const ProjectBwdArgs& a, cudaStream_t s) {
   if (a.F <= 0) return;
   k_project_bwd<<<unsigned((a.F + 127) / 128), 128, 0, s>>>(a);
-  const char* e = getenv("BGS_SH_BWD");  // A/B: 1 = one thread per record
-  if (e && atoi(e) == 1)
+  const char* e = getenv("BGS_SH_BWD");  // A/B: threads per record (1, 2 or 4)
+  const int mode = e ? atoi(e) : 4;
+  if (mode == 1)
     k_project_bwd_sh<<<unsigned((a.F + 255) / 256), 256, 0, s>>>(a);
+  else if (mode == 2)
+    k_project_bwd_shn<2><<<unsigned((2 * a.F + 255) / 256), 256, 0, s>>>(a);
   else
-    k_project_bwd_sh2<<<unsigned((2 * a.F + 255) / 256), 256, 0, s>>>(a);
+    k_project_bwd_shn<4><<<unsigned((4 * a.F + 255) / 256), 256, 0, s>>>(a);
 }
 
 }  // namespace bgs
