@@ -411,7 +411,8 @@ typedef struct {
  * projection counters and, at world > 1, the exchanged per-destination counts); at world > 1 the
  * batch issues ONE all-reduce of the B x T tile pair counts, ONE exchange of the B x M counts, ONE
  * grouped all-to-all of all views' records and ONE reverse all-to-all (+ a12's rounds per view)
- * instead of four collectives per view.  Views must share the image size.  Results equal B
+ * instead of four collectives per view.  Views must share the image size, and each view needs its own
+ * radius / rgb / t_final / n_contrib (/ cull_out, dL_scratch) buffers: the views run concurrently.  Results equal B
  * bgs_view_step calls (pixels, n_contrib, w, a, routing bit-identical; gradients up to fp32 atomic
  * order).  grads and importance's s, c_rad, c_vis are accumulated by every view (reductions); each
  * view's Cull column goes to its own cull_out (importance->cull_out is not used).  flags:

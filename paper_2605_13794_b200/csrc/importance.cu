@@ -544,14 +544,12 @@ __global__ void __launch_bounds__(1024) k_imp_coarse_decide(ImpState* st, const 
   const unsigned long long total = s_total;
   const unsigned long long target = (unsigned long long)num * total;
   unsigned long long above = j + 1 < 1024 ? s_part[j + 1] : 0ull;  // bins >= 4 j + 4
-  if (j == 0) {
-    st->total = total;
-    st->empty = total == 0;
-    st->final_ = 0;
-    st->need_gid = 0;
-    st->gid_thr = 0xffffffffu;
-    st->tshift = 0;
-    st->ncand = 0;
+  if (j == 0) {  // every field written (the selection copies the whole state)
+    ImpState z{};
+    z.total = total;
+    z.empty = total == 0;
+    z.gid_thr = 0xffffffffu;
+    *st = z;
   }
   __syncthreads();
   if (total == 0) return;

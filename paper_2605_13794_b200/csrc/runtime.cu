@@ -1240,7 +1240,8 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
       const int64_t words = 2 + 2 * ncand;  // [count, pad, (w, gid) x cap]; cap = global count
       CKS(ensure(ctx, ctx->imp_cand, size_t(words) * 8));
       CKS(ensure(ctx, ctx->imp_gath, size_t(words) * 8 * ctx->world));
-      CK(cudaMemsetAsync(ctx->imp_cand.p, 0, 16, s));
+      // the whole block is all-gathered (fixed size); slots past this rank's count are zero
+      CK(cudaMemsetAsync(ctx->imp_cand.p, 0, size_t(words) * 8, s));
       launch_imp_gather_cand(a, st, P_<unsigned long long>(ctx->imp_cand), s);
       CKS(launched(ctx));
       CKS(ctx->tr->allgather(ctx, ctx->imp_cand.p, ctx->imp_gath.p, size_t(words) * 8, s));

@@ -69,7 +69,10 @@ def _worker(rank, port, out_dir):
         vals = ctx.debug_buffer("vals").view(torch.int32).cpu().numpy()
         recv = ctx.debug_buffer("recv").cpu().numpy().view(np.uint32).reshape(-1, 12)
         # the batched step (one exchange per batch) on the same view twice
-        views = [B.batch_view(B.camera(cam), radius, rgb, T, nc, dl) for _ in range(2)]
+        bb = [dict(radius=torch.zeros(n, dtype=torch.int32, device=dev), rgb=torch.zeros(3, H, W, device=dev),
+                   T=torch.zeros(H, W, device=dev), nc=torch.zeros(H, W, dtype=torch.int32, device=dev))
+              for _ in range(2)]  # each view of a batch has its own outputs (the views run concurrently)
+        views = [B.batch_view(B.camera(cam), b["radius"], b["rgb"], b["T"], b["nc"], dl) for b in bb]
         c0 = ctx.batch_stats()["collectives"]
         B.bgs_batch_step(ctx, g, views, None, 0, grads, None, stream)
         stream.synchronize()
@@ -77,7 +80,7 @@ def _worker(rank, port, out_dir):
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), owner=owner.cpu().numpy(), rgb=rgb.cpu().numpy(),
              nc=nc.cpu().numpy(), tile_begin=q["tile_begin"], tile_end=q["tile_end"],
              pair_gid=recv[vals, 10].astype(np.int64), c_vis=cv.cpu().numpy(), batch_coll=batch_coll,
-             rgb_batch=rgb.cpu().numpy())
+             rgb_batch=bb[1]["rgb"].cpu().numpy())
     ctx.close()
     dist.destroy_process_group()
 
@@ -102,6 +105,7 @@ def test_nccl_world2_matches_oracle(tmp_path):
         assert (int(d["tile_begin"]), int(d["tile_end"])) == (b, e)
         assert np.array_equal(d["pair_gid"], st.get("pair_gid", r))
         assert int(d["batch_coll"]) == 4
+        assert np.array_equal(d["rgb_batch"], d["rgb"])
         for t in range(b, e):
             ty, tx = divmod(t, 16)
             img[:, ty * 16:ty * 16 + 16, tx * 16:tx * 16 + 16] = d["rgb"][:, ty * 16:ty * 16 + 16, tx * 16:tx * 16 + 16]

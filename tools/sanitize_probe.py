@@ -114,7 +114,12 @@ def main():
                 cu = torch.zeros((m + 31) // 32, dtype=torch.int32, device=dev)
                 B.bgs_view_step(grp[r], gg, B.camera(cams[0]), None, None, 0, mb["radius"], mb["rgb"], mb["T"],
                                 mb["nc"], dl, gr, B.importance_out(ss, c1, c2, cu), stream)
-                vv = [B.batch_view(B.camera(cams[k]), mb["radius"], mb["rgb"], mb["T"], mb["nc"], dl) for k in range(2)]
+                # each view of a batch needs its own output buffers (the views run concurrently)
+                vb2 = [dict(radius=torch.zeros(m, dtype=torch.int32, device=dev), rgb=torch.zeros(3, H, W, device=dev),
+                            T=torch.zeros(H, W, device=dev), nc=torch.zeros(H, W, dtype=torch.int32, device=dev))
+                       for _ in range(2)]
+                vv = [B.batch_view(B.camera(cams[k]), vb2[k]["radius"], vb2[k]["rgb"], vb2[k]["T"], vb2[k]["nc"], dl)
+                      for k in range(2)]
                 B.bgs_batch_step(grp[r], gg, vv, None, 0, gr, None, stream)
                 stream.synchronize()
         except Exception as e:  # pragma: no cover
