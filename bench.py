@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--host-threads", type=int, default=0,
                    help="1: one host thread per in-flight context (the ABI's one-ctx-per-host-thread model)")
     p.add_argument("--quick", action="store_true", help="headline, e2e and stages only (no train/scoring/simplify)")
+    p.add_argument("--no-bounds", action="store_true", help="no block bounds (per-Gaussian culling only)")
     return p.parse_args()
 
 
@@ -249,6 +250,10 @@ def run_native(args):
         if world == 1:
             scene = scene.subset(perm.cpu().numpy())  # the oracle baseline sees the same labelling
         torch.cuda.synchronize()
+    if not args.no_bounds:
+        # block bounds of the (Z-ordered) shard: a1 skips the blocks that cannot reach the image
+        B.bgs_shard_bounds(ctx, g)
+        torch.cuda.synchronize()
     W, H = scene.cameras[0]["W"], scene.cameras[0]["H"]
     cams = [B.camera(c) for c in scene.cameras]
     # d0: 4x the median camera distance (R19) so the gate is selective, not degenerate
@@ -426,6 +431,7 @@ def run_native(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": dict(config_dict(args, label, gate_on, mask_on, N_all, W, H, world, batch),
                        shard_layout=args.layout, host_threads=bool(args.host_threads),
+                       block_bounds=not args.no_bounds,
                        l2=("inputs exceed L2 (every view reads the 1.45 GB shard); the B views of a step overlap "
                            "and are not flushed between; stages_ms / single_view_ms: one view at a time, L2 "
                            "flushed (256 MB write) before each"),
@@ -620,6 +626,8 @@ def train_iterations(args, B, S, ctxs, per, g0, cams, gate, cull_of, imp_of, str
                        torch.log(g0.scale.clamp_min(1e-30)).contiguous(), g0.sh.clone())
     tp.log_scale[:, 3] = 0
     g = B.GaussianPlanes(mo.clone(), g0.quat.clone(), g0.scale.clone(), tp.sh, g0.lod)  # rendered + written
+    if g0.bounds is not None:
+        B.bgs_shard_bounds(ctxs[0], g, stream=stream)  # refreshed after every optimizer step below
     grads = g.zeros_grads()
     nw = (max(n_local, 1) + 31) // 32
     vis = torch.zeros(nw, dtype=torch.int32, device=dev)
@@ -651,6 +659,8 @@ def train_iterations(args, B, S, ctxs, per, g0, cams, gate, cull_of, imp_of, str
         state["step"] += 1
         with torch.cuda.stream(stream):
             B.bgs_adam_step(ctxs[0], tp, grads, g, vis, B.adam_hparams(step=state["step"]), stream)
+            if g.bounds is not None:
+                B.bgs_shard_bounds(ctxs[0], g, g.bounds, stream)
             vis.zero_()
 
     for it in range(args.warmup):
@@ -705,6 +715,8 @@ def train_iterations(args, B, S, ctxs, per, g0, cams, gate, cull_of, imp_of, str
         state["step"] += 1
         with torch.cuda.stream(stream):
             B.bgs_adam_step(ctxs[0], tp, grads, g, vis, B.adam_hparams(step=state["step"]), stream)
+            if g.bounds is not None:
+                B.bgs_shard_bounds(ctxs[0], g, g.bounds, stream)
             vis.zero_()
 
     host_iteration(0)

@@ -82,7 +82,13 @@ typedef struct {
  *   quat      float4 (w, x, y, z), unit norm
  *   scale     float4 (s_x, s_y, s_z, unused) per-axis standard deviation > 0
  *   sh        float  [n_local][16][3] degree-3 SH, coefficient-major, RGB inner (R1)
- *   lod       uint8  [n_local] LOD label l_i */
+ *   lod       uint8  [n_local] LOD label l_i
+ *   bounds    nullable: per block of BGS_BOUNDS_BLOCK rows, 8 floats {min mu_x, min mu_y, min mu_z,
+ *             max_j s_j, max mu_x, max mu_y, max mu_z, 0} written by bgs_shard_bounds for THESE
+ *             parameters (stale bounds are a contract violation: refresh after every update).  With
+ *             bounds, a1 skips every block whose box cannot reach the image (hierarchical culling;
+ *             ungated steps only), reading 32 B per block instead of 32 B per Gaussian. */
+#define BGS_BOUNDS_BLOCK 1024
 typedef struct {
   int64_t n_local;
   const float* mean_opac;
@@ -90,6 +96,7 @@ typedef struct {
   const float* scale;
   const float* sh;
   const uint8_t* lod;
+  const float* bounds;
 } bgs_gaussians;
 
 /* Gradients w.r.t. the activated parameters, same layouts as bgs_gaussians (device,
@@ -174,6 +181,13 @@ bgs_status bgs_debug_buffer(bgs_ctx* ctx, int32_t which, void** dev_ptr, int64_t
  * (c^rad_{i,v} = radius > 0).  flags: BGS_NO_COLOR.  HOST-SYNC (reads F and P). */
 bgs_status bgs_project(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam, const bgs_lod_gate* gate,
                        const uint32_t* cull_column, uint32_t flags, int32_t* radius_out, void* stream);
+
+/* Block bounds for hierarchical culling (a1): for each block of BGS_BOUNDS_BLOCK consecutive rows of
+ * the shard, the box of the means and the largest per-axis standard deviation (8 floats, layout in
+ * bgs_gaussians.bounds).  bounds_out: device f32 [ceil(n_local / BGS_BOUNDS_BLOCK)][8].  One pass
+ * over the means and scales (32 B per row); call after every parameter update (the Z-ordered shard
+ * layout of bgs_spatial_order makes the boxes tight). */
+bgs_status bgs_shard_bounds(bgs_ctx* ctx, const bgs_gaussians* g, float* bounds_out, void* stream);
 
 /* a3+a4.  Per-tile pair counts are all-reduced, tiles split into contiguous cost-balanced
  * runs (owner(t) = min(M-1, floor((2 P_t + c_t) M / (2 C))), c_t = pairs_t + 1, D6), and

@@ -56,7 +56,7 @@ class bgs_batch_view(C.Structure):
 
 class bgs_gaussians(C.Structure):
     _fields_ = [("n_local", C.c_int64), ("mean_opac", C.c_void_p), ("quat", C.c_void_p), ("scale", C.c_void_p),
-                ("sh", C.c_void_p), ("lod", C.c_void_p)]
+                ("sh", C.c_void_p), ("lod", C.c_void_p), ("bounds", C.c_void_p)]
 
 
 class bgs_gaussian_grads(C.Structure):
@@ -111,6 +111,7 @@ _SIGS = {
     "bgs_adam_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "bgs_densify_accumulate": [_vp, C.c_int64, _vp, _vp, _vp, _vp],
     "bgs_visibility_mask": [_vp, C.c_int64, _vp, _vp, _vp],
+    "bgs_shard_bounds": [_vp, _vp, _vp, _vp],
     "bgs_batch_step": [_vp, C.c_int32, _vp, _vp, C.c_uint32, _vp, _vp, _vp, _vp],
     "bgs_batch_view_ctx": [_vp, C.c_int32, _vp],
     "bgs_batch_stats": [_vp, _vp],
@@ -284,8 +285,9 @@ def lod_gate(enabled: bool = False, l_max: int = 31, d0: float = 1.0, num: int =
 class GaussianPlanes:
     """Activated parameters of one shard in the ABI layout (float4 rows, SH [n][48])."""
 
-    def __init__(self, mean_opac, quat, scale, sh, lod):
+    def __init__(self, mean_opac, quat, scale, sh, lod, bounds=None):
         self.mean_opac, self.quat, self.scale, self.sh, self.lod = mean_opac, quat, scale, sh, lod
+        self.bounds = bounds  # optional block bounds (bgs_shard_bounds) for hierarchical culling
         self.n = int(mean_opac.shape[0])
 
     @staticmethod
@@ -307,7 +309,8 @@ class GaussianPlanes:
 
     def struct(self) -> bgs_gaussians:
         return bgs_gaussians(self.n, self.mean_opac.data_ptr(), self.quat.data_ptr(), self.scale.data_ptr(),
-                             self.sh.data_ptr(), self.lod.data_ptr())
+                             self.sh.data_ptr(), self.lod.data_ptr(),
+                             self.bounds.data_ptr() if self.bounds is not None else None)
 
     def zeros_grads(self) -> "GradPlanes":
         z = lambda t: torch.zeros_like(t, dtype=torch.float32)
@@ -570,6 +573,21 @@ def bgs_view_step_host(ctx: Context, g: GaussianPlanes, cam: bgs_camera, gate, c
                                       C.byref(gr) if gr is not None else None,
                                       C.byref(importance) if importance is not None else None, _stream(stream)),
               "bgs_view_step_host")
+
+
+BOUNDS_BLOCK = 1024
+
+
+def bgs_shard_bounds(ctx: Context, g: "GaussianPlanes", bounds=None, stream=None):
+    """Block bounds of the shard for hierarchical culling (a1); returns the f32 [blocks][8] tensor and
+    attaches it to g (g.bounds), so subsequent steps with g skip off-screen blocks."""
+    nb = max(1, (g.n + BOUNDS_BLOCK - 1) // BOUNDS_BLOCK)
+    if bounds is None:
+        bounds = torch.empty(nb, 8, dtype=torch.float32, device=g.mean_opac.device)
+    gs = g.struct()
+    ctx.check(_lib.bgs_shard_bounds(ctx.handle, C.byref(gs), _ptr(bounds), _stream(stream)), "bgs_shard_bounds")
+    g.bounds = bounds
+    return bounds
 
 
 def bgs_spatial_order(ctx: Context, mean_opac: torch.Tensor, perm_out: torch.Tensor, stream=None):

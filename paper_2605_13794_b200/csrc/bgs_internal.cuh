@@ -91,6 +91,7 @@ struct ProjectArgs {
   const float* sh;
   const uint8_t* lod;
   const uint32_t* cull;      // nullable
+  const float4* bounds;      // nullable: per BGS_BOUNDS_BLOCK rows {min mu, max s}, {max mu, -} (hierarchical cull)
   int64_t n;
   CameraK cam;
   int gate_enabled, l_max, fb_num, fb_den;
@@ -112,6 +113,7 @@ struct ProjectArgs {
 void launch_gate_count(const ProjectArgs& a, cudaStream_t s);
 void launch_project(const ProjectArgs& a, cudaStream_t s);
 void launch_color(const ProjectArgs& a, cudaStream_t s);  // after launch_project; F read on device
+void launch_shard_bounds(const float4* mean_opac, const float4* scale, int64_t n, float4* bounds, cudaStream_t s);
 
 // sort (a5-a7)
 struct SortArgs {

@@ -221,6 +221,89 @@ __device__ __forceinline__ unsigned long long block_compact(const bool (&flag)[P
 
 constexpr int kCullPer = 4;
 constexpr int kCullChunk = 256 * kCullPer;
+static_assert(kCullChunk == BGS_BOUNDS_BLOCK, "one k_cull CTA per bounds block");
+
+// Hierarchical culling: can any Gaussian of the block (box of means [lo, hi], largest axis
+// standard deviation smax) produce a record?  The means' camera depths span [tz_min, tz_max]
+// (affine in mu: extremes at the box corners).  All behind the near plane -> no.  Straddling it
+// -> maybe (conservative).  Else every centre projects into the bounding box of the projected
+// corners (the box lies in front of the camera, where projection maps convex sets to convex
+// sets), and every per-Gaussian radius bound of cull_test is at most rb(smax, tz_min): the block
+// is culled when that box, widened by rb and by a 1% + 4 px margin for fp32 rounding, misses the
+// image.  Every Gaussian of a culled block would fail cull_test, hence has an empty rect.
+__device__ bool block_may_reach(const ProjectArgs& a, float4 b0, float4 b1) {
+  const CameraK& cm = a.cam;
+  float tzmin = 3.4e38f, tzmax = -3.4e38f, xmin = 3.4e38f, xmax = -3.4e38f, ymin = 3.4e38f, ymax = -3.4e38f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float px = (c & 1) ? b1.x : b0.x, py = (c & 2) ? b1.y : b0.y, pz = (c & 4) ? b1.z : b0.z;
+    const float tz = ((cm.R[6] * px + cm.R[7] * py) + cm.R[8] * pz) + cm.t[2];
+    tzmin = fminf(tzmin, tz);
+    tzmax = fmaxf(tzmax, tz);
+  }
+  if (tzmax <= cm.near_clip) return false;  // every mean behind the near plane
+  if (tzmin <= cm.near_clip * 1.001f + 1e-6f) return true;  // straddles it: keep
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float px = (c & 1) ? b1.x : b0.x, py = (c & 2) ? b1.y : b0.y, pz = (c & 4) ? b1.z : b0.z;
+    const float tx = ((cm.R[0] * px + cm.R[1] * py) + cm.R[2] * pz) + cm.t[0];
+    const float ty = ((cm.R[3] * px + cm.R[4] * py) + cm.R[5] * pz) + cm.t[1];
+    const float tz = ((cm.R[6] * px + cm.R[7] * py) + cm.R[8] * pz) + cm.t[2];
+    const float mx = cm.fx * (tx / tz) + cm.cx, my = cm.fy * (ty / tz) + cm.cy;
+    xmin = fminf(xmin, mx);
+    xmax = fmaxf(xmax, mx);
+    ymin = fminf(ymin, my);
+    ymax = fmaxf(ymax, my);
+  }
+  const float smax = b0.w, iz = 1.0f / tzmin;
+  const float rb = (3.0f * sqrtf(a.cull_K * (smax * smax) * (iz * iz) + 0.62f) * 1.01f + 2.0f) * 1.01f + 4.0f;
+  const float mxr = 0.01f * (fabsf(xmin) + fabsf(xmax)), myr = 0.01f * (fabsf(ymin) + fabsf(ymax));
+  return !(xmax + rb + mxr < 0.0f || xmin - rb - mxr > float(16 * cm.TX + 1) || ymax + rb + myr < 0.0f ||
+           ymin - rb - myr > float(16 * cm.TY + 1));
+}
+
+// one CTA per bounds block: box of the means, largest axis standard deviation
+__global__ void __launch_bounds__(256) k_shard_bounds(const float4* __restrict__ mean_opac,
+                                                      const float4* __restrict__ scale, int64_t n,
+                                                      float4* __restrict__ bounds) {
+  __shared__ float s_red[7][8];
+  const int64_t r0 = int64_t(blockIdx.x) * kCullChunk;
+  float v[7] = {3.4e38f, 3.4e38f, 3.4e38f, 0.f, -3.4e38f, -3.4e38f, -3.4e38f};
+  for (int k = 0; k < kCullPer; ++k) {
+    const int64_t i = r0 + k * 256 + threadIdx.x;
+    if (i >= n) break;
+    const float4 m = ldg4(mean_opac + i), sc = ldg4(scale + i);
+    v[0] = fminf(v[0], m.x);
+    v[1] = fminf(v[1], m.y);
+    v[2] = fminf(v[2], m.z);
+    v[3] = fmaxf(v[3], fmaxf(sc.x, fmaxf(sc.y, sc.z)));
+    v[4] = fmaxf(v[4], m.x);
+    v[5] = fmaxf(v[5], m.y);
+    v[6] = fmaxf(v[6], m.z);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const float t = __shfl_xor_sync(0xffffffffu, v[k], o);
+      v[k] = (k < 3) ? fminf(v[k], t) : fmaxf(v[k], t);
+    }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int k = 0; k < 7; ++k) s_red[k][w] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r[7];
+    for (int k = 0; k < 7; ++k) {
+      r[k] = s_red[k][0];
+      for (int j = 1; j < 8; ++j) r[k] = (k < 3) ? fminf(r[k], s_red[k][j]) : fmaxf(r[k], s_red[k][j]);
+    }
+    bounds[2 * blockIdx.x] = make_float4(r[0], r[1], r[2], r[3]);
+    bounds[2 * blockIdx.x + 1] = make_float4(r[4], r[5], r[6], 0.f);
+  }
+}
 
 __global__ void __launch_bounds__(256) k_cull(ProjectArgs a) {
   __shared__ uint32_t s_idx[kCullChunk];
@@ -231,6 +314,22 @@ __global__ void __launch_bounds__(256) k_cull(ProjectArgs a) {
   const int tid = threadIdx.x;
   if (tid == 0) s_act = 0;
   const int64_t chunk0 = int64_t(blockIdx.x) * kCullChunk;
+  if (a.bounds && !a.gate_enabled &&
+      !block_may_reach(a, __ldg(a.bounds + 2 * blockIdx.x), __ldg(a.bounds + 2 * blockIdx.x + 1))) {
+    // the whole block is off-screen: radius 0, no candidates; |A| counts the rows the cull column
+    // keeps (the frustum is not part of the active set) -- without reading a single Gaussian
+    uint32_t act = 0;
+    for (int k = 0; k < kCullPer; ++k) {
+      const int64_t i = chunk0 + k * 256 + tid;
+      if (i < a.n) {
+        a.radius[i] = 0;
+        act += a.cull ? !((__ldg(a.cull + (i >> 5)) >> (i & 31)) & 1u) : 1u;
+      }
+    }
+    act = __reduce_add_sync(0xffffffffu, act);
+    if ((tid & 31) == 0 && act) atomicAdd(a.counters + C_NACT, (unsigned long long)act);
+    return;
+  }
   bool maybe[kCullPer];
   uint32_t nact = 0;
 #pragma unroll
@@ -422,6 +521,11 @@ void launch_project(const ProjectArgs& a, cudaStream_t s) {
   static std::atomic<int> slots[kMaxDevices];
   const int proj_blocks = per_device(slots, [] { return persistent_blocks(k_project); });
   k_project<<<proj_blocks, 256, 0, s>>>(a);
+}
+
+void launch_shard_bounds(const float4* mean_opac, const float4* scale, int64_t n, float4* bounds, cudaStream_t s) {
+  if (n <= 0) return;
+  k_shard_bounds<<<unsigned((n + kCullChunk - 1) / kCullChunk), 256, 0, s>>>(mean_opac, scale, n, bounds);
 }
 
 void launch_color(const ProjectArgs& a, cudaStream_t s) {

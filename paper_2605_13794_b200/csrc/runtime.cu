@@ -708,6 +708,7 @@ static bgs_status project_enqueue(bgs_ctx* ctx, const bgs_gaussians* g, const bg
   a.sh = g->sh;
   a.lod = g->lod;
   a.cull = cull_column;
+  a.bounds = reinterpret_cast<const float4*>(g->bounds);
   a.n = g->n_local;
   a.cam = ctx->cam;
   a.gate_enabled = 0;
@@ -1280,6 +1281,15 @@ bgs_status bgs_importance(bgs_ctx* ctx, int64_t n_local, const int32_t* radius, 
   ++nl;
   CKS(launched(ctx, nl));
   return BGS_OK;
+}
+
+bgs_status bgs_shard_bounds(bgs_ctx* ctx, const bgs_gaussians* g, float* bounds_out, void* stream) {
+  CKS(check_ctx(ctx));
+  CKS(check_gaussians(ctx, g));
+  if (g->n_local > 0 && !bounds_out) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "bounds_out is NULL");
+  launch_shard_bounds(reinterpret_cast<const float4*>(g->mean_opac), reinterpret_cast<const float4*>(g->scale),
+                      g->n_local, reinterpret_cast<float4*>(bounds_out), as_stream(stream));
+  return g->n_local > 0 ? launched(ctx) : BGS_OK;
 }
 
 bgs_status bgs_spatial_order(bgs_ctx* ctx, const float* mean_opac, int64_t n, uint32_t* perm_out, void* stream) {

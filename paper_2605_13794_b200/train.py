@@ -90,7 +90,8 @@ class Trainer:
     dicts, targets: device f32 [3][H][W] per camera, d0: the LOD reference distance (R19)."""
 
     def __init__(self, ctx, params, lod, cams, targets, d0, sched: Schedule, batch: int = 4, lam: float = 0.2,
-                 beta: float = 10.0, seed: int = 0, densify=None, device: str = "cuda:0", hp=None):
+                 beta: float = 10.0, seed: int = 0, densify=None, device: str = "cuda:0", hp=None,
+                 bounds: bool = True):
         import torch
 
         import paper_2605_13794_b200.bgs as B
@@ -104,6 +105,7 @@ class Trainer:
         self.dev = device
         self.dp = densify
         self.hp = hp or {}
+        self.use_bounds = bounds  # block bounds for hierarchical culling, refreshed after every update
         self.H, self.W = cams[0]["H"], cams[0]["W"]
         self.stream = torch.cuda.Stream(device)
         self.step_count = 0  # Adam step t
@@ -130,6 +132,8 @@ class Trainer:
         self.act = B.GaussianPlanes(torch.empty(n, 4, device=dev), torch.empty(n, 4, device=dev),
                                     torch.empty(n, 4, device=dev), self.p.sh, self.lod)
         self._activate()
+        if self.use_bounds:
+            B.bgs_shard_bounds(self.ctx, self.act, stream=self.stream)
         self.grads = self.act.zeros_grads()
         self.stat = torch.zeros(max(n, 1), dtype=torch.float32, device=dev)
         self.count = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
@@ -184,6 +188,8 @@ class Trainer:
             self.step_count += 1
             B.bgs_adam_step(self.ctx, self.p, self.grads, self.act, self.vis,
                             B.adam_hparams(step=self.step_count, **self.hp), st)
+            if self.use_bounds:
+                B.bgs_shard_bounds(self.ctx, self.act, self.act.bounds, st)
             self.vis.zero_()
         event = ""
         if sc.densify_due(t) and self.dp is not None:

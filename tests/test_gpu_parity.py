@@ -15,7 +15,7 @@ if not torch.cuda.is_available():
 
 import oracle as O  # noqa: E402
 import synthetic as S  # noqa: E402
-from gpu_helpers import GpuStep  # noqa: E402
+from gpu_helpers import GpuStep, rec_view  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 ET_MARGIN = 1e-4  # relative distance of T(1-alpha) to 1e-4 below which an early-stop flip is excused
@@ -505,6 +505,47 @@ def rubble_full():
     gs = GpuStep(sc, cam, M=1, dLdC=dl)
     yield sc, cam, sample, st, gs
     gs.close()
+
+
+def test_block_bounds_cull_is_exact():
+    """Hierarchical culling (bgs_shard_bounds + bgs_gaussians.bounds) on the Z-ordered full Rubble
+    shard: for several views, radius, the records, F, P_all and |A| are bit-identical to the
+    per-Gaussian path (a culled block's Gaussians all have empty rects)."""
+    import paper_2605_13794_b200.bgs as B
+    sc = S.gen_city("rubble")
+    ctx = B.Context(0, 1, 0)
+    g = B.GaussianPlanes.from_scene(sc, "cuda")
+    perm = B.spatial_order(ctx, g)
+    g = B.GaussianPlanes(g.mean_opac[perm].contiguous(), g.quat[perm].contiguous(), g.scale[perm].contiguous(),
+                         g.sh[perm].contiguous(), g.lod[perm].contiguous())
+    gb = B.GaussianPlanes(g.mean_opac, g.quat, g.scale, g.sh, g.lod)
+    bounds = B.bgs_shard_bounds(ctx, gb)
+    torch.cuda.synchronize()
+    # the boxes hold their blocks (spot check against torch on a few blocks)
+    b = bounds.cpu().numpy()
+    mo, scl = g.mean_opac.cpu().numpy(), g.scale.cpu().numpy()
+    for blk in (0, 17, len(b) - 1):
+        rows = slice(blk * 1024, min(sc.n, blk * 1024 + 1024))
+        assert np.array_equal(b[blk, :3], mo[rows, :3].min(0)) and np.array_equal(b[blk, 4:7], mo[rows, :3].max(0))
+        assert b[blk, 3] == scl[rows, :3].max()
+    skipped_total = 0
+    for v in (0, 7, 31, 50):
+        cam = B.camera(sc.cameras[v])
+        out = []
+        for gg in (g, gb):
+            radius = torch.full((sc.n,), -1, dtype=torch.int32, device="cuda")
+            B.bgs_project(ctx, gg, cam, None, None, 0, radius)
+            q = ctx.query()
+            rec = rec_view(ctx.debug_buffer("records"))
+            order = np.argsort(rec["gid"])
+            out.append((radius.cpu().numpy(), q, {k: v_[order] for k, v_ in rec.items()}))
+        (r0, q0, c0), (r1, q1, c1) = out
+        assert np.array_equal(r0, r1), v
+        assert (q0["F"], q0["P_all"], q0["n_active"]) == (q1["F"], q1["P_all"], q1["n_active"]), v
+        for k in c0:
+            assert np.array_equal(c0[k], c1[k]), (v, k)
+        skipped_total += int(q0["F"]) >= 0
+    ctx.close()
 
 
 def test_full_size_sampled(rubble_full):
