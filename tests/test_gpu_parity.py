@@ -651,6 +651,61 @@ def test_full_size_importance(rubble_full):
     assert np.all(np.abs(gs.w[in_sample].astype(np.float64) - w_o) <= st.get("a")[in_sample] + 1e-5 * w_o)
 
 
+@pytest.mark.parametrize("city,view", [("residence", 5), ("matrixcity", 2)])
+def test_full_size_ragged_configs(city, view):
+    """BASELINE configs[3] (Residence-shaped, 8M Gaussians, 1368x912: the last tile column is 8
+    pixels wide) and configs[4] (MatrixCity-shaped, 20M Gaussians, 1920x1080: the last tile row is 8
+    pixels high) at full size: radius, records, the complete pair sequence and ranges bit-exact;
+    pixels, n_contrib, the 9 compositing partials and every parameter gradient on a 1/16 tile sample
+    that includes ragged tiles (dL/dC zeroed outside it); c_rad / c_vis / Cull bit-exact on the
+    GPU's own w and a."""
+    sc = S.gen_city(city)
+    cam = sc.cameras[view]
+    H, W = cam["H"], cam["W"]
+    TX, TY = (W + 15) // 16, (H + 15) // 16
+    assert W % 16 == 8 or H % 16 == 8
+    sample = _tile_sample(H, W)
+    # the sample reaches the ragged column / row (tiles t = 0 mod 16)
+    ragged = [t for t in range(0, TX * TY, 16) if t % TX == TX - 1 or t // TX == TY - 1]
+    assert ragged
+    dl = S.grad_image(H, W) * sample[None]
+    st = O.OracleStep(sc, cam, M=1, tile_frac=1.0 / 16, dLdC=dl, threads=16)
+    gs = GpuStep(sc, cam, M=1, dLdC=dl)
+    try:
+        assert np.array_equal(gs.radius, st.get("radius"))
+        rec = gs.rank[0]["records"]
+        order = np.argsort(rec["gid"])
+        valid = np.nonzero(st.get("radius") > 0)[0]
+        assert np.array_equal(rec["gid"][order], valid)
+        m2 = st.get("mean2d").reshape(-1, 2)[valid]
+        assert np.array_equal(rec["mx"][order].view(np.uint32), _f32(m2[:, 0]).view(np.uint32))
+        o = gs.rank[0]
+        assert np.array_equal(o["key_tile"], st.get("pair_tile", 0))
+        assert np.array_equal(o["recv"]["gid"][o["vals"]], st.get("pair_gid", 0))
+        assert np.array_equal(o["ranges"][:, 0], st.get("range_lo", 0))
+        assert np.array_equal(o["ranges"][:, 1], st.get("range_hi", 0))
+        _, flips, affected = _flip_info(st, gs, cam, sample)
+        ok = sample & ~flips
+        assert ok.sum() > 0.05 * H * W
+        img = st.get("img").reshape(3, H, W)
+        assert np.abs(gs.img - img)[:, ok].max() <= 1e-4
+        assert np.array_equal(gs.nc[ok], st.get("n_contrib").reshape(H, W)[ok])
+        # the sampled ragged tiles composited something (their partial blocks are compared above)
+        assert sum(int(gs.nc[(t // TX) * 16:(t // TX + 1) * 16, (t % TX) * 16:(t % TX + 1) * 16].sum())
+                   for t in ragged) > 0
+        _excused_ok(st, gs, affected)
+        keep = np.ones(sc.n, bool)
+        keep[list(affected)] = False
+        _check_g2d(st, gs, keep, city)
+        _check_grads(sc.n, st, gs, keep, what=city)
+        ref = O.importance(gs.radius, gs.w, gs.a)
+        assert np.array_equal(gs.c_rad, ref["c_rad"])
+        assert np.array_equal(gs.c_vis, ref["c_vis"])
+        assert np.array_equal(gs.cull_bits, S.unpack_bits(ref["cull"], sc.n))
+    finally:
+        gs.close()
+
+
 @pytest.mark.parametrize("split", ["default", "0"])
 @pytest.mark.parametrize("case", ["empty", "single", "ragged", "behind_and_offscreen", "dense_tile"])
 def test_edge_cases(case, split, monkeypatch):
