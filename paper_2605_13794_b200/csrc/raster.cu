@@ -23,10 +23,11 @@
 // Backward: the accumulator holds, per splat, sum gd, sum gd dx, sum gd dy, sum gd dx^2,
 // sum gd dx dy, sum gd dy^2 (gd = G dL/dalpha, dx = mx - px, dy = my - py) and the colour
 // partials; k_project_bwd turns the moments into dL/d(mean2d, conic) with the record's o, A, B, C.
-// Per (warp, record) each lane first adds the partials of its two pixels, then the
-// 9 partial gradients are reduced with a transposed butterfly (8 values in 4+2+1+2 shuffles,
-// each lane ending with one value; the 9th with 5 shuffles) and issued as 9 parallel
-// red.global.add.f32 from 9 lanes.
+// Per (warp, record) each lane first adds the partials of its two pixels.  With at most
+// kBwdAtomicLanes contributing lanes each of them issues two red.global.add.v4.f32 and one scalar
+// red; otherwise the 9 partial gradients are reduced with a transposed butterfly (8 values in
+// 4+2+1+2 shuffles, each lane ending with one value; the 9th with 5 shuffles) and issued as 9
+// parallel red.global.add.f32 from 9 lanes.
 //
 // The power expression is pinned (explicit __fmul_rn / __fmaf_rn, the oracle's neg_power order) so
 // that the alpha-cut decision, n_contrib and a are bit-identical to the oracle's.
@@ -313,6 +314,20 @@ __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float
 
 __device__ __forceinline__ float xsel(bool hi, float a, float b) { return hi ? a : b; }
 
+// contributing lanes up to which a (warp, record) visit reduces with per-lane vector atomics
+// (3 red instructions) instead of the butterfly (~54 instructions).  Measured on Rubble, 4 views in
+// flight (same box): bwd 0.249 ms at 4, 0.238 at 6, 0.229 at 8, 0.220 at 12, 0.221 at 16; 9 scalar
+// atomics per lane (round 1) were best at 4 (0.254 ms)
+#ifndef BGS_BWD_ATOMIC_LANES
+#define BGS_BWD_ATOMIC_LANES 12
+#endif
+constexpr int kBwdAtomicLanes = BGS_BWD_ATOMIC_LANES;
+
+__device__ __forceinline__ void red_add_v4(float* p, float x, float y, float z, float w) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(x), "f"(y), "f"(z), "f"(w)
+               : "memory");
+}
+
 // Backward of one warp's 16 x 2kPix strip starting at tile row `row0` (layout as fwd_strip).
 // More pixels per lane amortise the per-(warp, record) gradient reduction; fewer shorten the
 // walk of the heaviest tiles (k_raster_bwd's work split).
@@ -384,13 +399,11 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
       const unsigned cm = __ballot_sync(0xffffffffu, any);
       if (cm == 0) continue;
       float* dst = a.acc[__float_as_uint(s.co.w)].g;
-      // few contributors: direct atomics beat a 14-shuffle reduction (threshold measured on
-      // Rubble: bwd 0.317 ms at 2, 0.308 at 3, 0.306 at 4, 0.309 at 5, 0.325 at 6, 0.378 at 8)
-      if (__popc(cm) <= 4) {
-        if (any) {
-#pragma unroll
-          for (int k = 0; k < 9; ++k) atomicAdd(dst + k, g[k]);
-        }
+      // few contributing lanes: direct vector reductions (two red.v4 + one scalar per lane; the
+      // 48-B accumulator rows are 16-B aligned) beat the 14-shuffle butterfly below
+      if (__popc(cm) <= kBwdAtomicLanes) {
+        if (any) red_add_v4(dst, g[0], g[1], g[2], g[3]), red_add_v4(dst + 4, g[4], g[5], g[6], g[7]),
+            atomicAdd(dst + 8, g[8]);
         continue;
       }
       // transposed butterfly over g[0..7]: lane ends with the warp sum of g[my_idx]
