@@ -107,6 +107,7 @@ struct ProjectArgs {
   unsigned long long* counters;
   int32_t* tile_diff;        // nullable: (TY+1)*(TX+1) 2D difference array of rect coverage
   uint32_t* cand;            // [n] candidate list written by k_cull
+  float4* jdir;              // [3 F] per local record: colour Jacobian wrt the view direction + clamp bits (k_color)
   int64_t rec_cap;
 };
 
@@ -187,6 +188,7 @@ struct ProjectBwdArgs {
   const float* sh;
   const uint32_t* rec_lidx;
   const Acc* acc;            // per local record, owner-summed
+  const float4* jdir;        // [3 F] k_color's colour Jacobian wrt the view direction + clamp bits
   int64_t F;
   CameraK cam;
   float4* g_mean_opac;

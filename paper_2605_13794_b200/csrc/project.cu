@@ -469,17 +469,48 @@ __device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f) {
   Y[14] = (1.445305721320277f * z) * (xx - yy);
   Y[15] = (-0.5900435899266435f * x) * (xx - 3.0f * yy);
   float col[3];
+  uint32_t clamped = 0;
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
     float c = Y[0] * v[ch];
 #pragma unroll
     for (int k = 1; k < 16; ++k) c = c + Y[k] * v[3 * k + ch];
     c = c + 0.5f;
+    clamped |= uint32_t(c < 0.0f) << ch;
     col[ch] = c < 0.0f ? 0.0f : c;
   }
   rp[6] = col[0];
   rp[7] = col[1];
   rp[8] = col[2];
+  // For a11 (k_project_bwd): J[ch][d] = sum_k sh[k][ch] dY_k/d(x, y, z), the derivative of the
+  // unclamped colour along the normalised view direction (x, y, z treated as independent; the
+  // normalisation's projection is applied in the backward), and the clamp bits (R2: a clamped
+  // channel passes no gradient).  The backward then needs these 48 B instead of the 192-B SH row.
+  // Not part of the pinned record: its rounding only enters gradients (tolerance parity).
+  const float C1 = 0.4886025119029199f;
+  const float C20 = 1.0925484305920792f, C21 = -1.0925484305920792f, C22 = 0.31539156525252005f,
+              C23 = -1.0925484305920792f, C24 = 0.5462742152960396f;
+  const float C30 = -0.5900435899266435f, C31 = 2.890611442640554f, C32 = -0.4570457994644658f,
+              C33 = 0.3731763325901154f, C34 = -0.4570457994644658f, C35 = 1.445305721320277f,
+              C36 = -0.5900435899266435f;
+  float J[3][3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    const float* s = v + ch;  // s[3 k] = sh[k][ch]
+    J[ch][0] = -C1 * s[9] + C20 * y * s[12] - 2.f * C22 * x * s[18] + C23 * z * s[21] + 2.f * C24 * x * s[24] +
+               6.f * C30 * xy * s[27] + C31 * yz * s[30] - 2.f * C32 * xy * s[33] - 6.f * C33 * xz * s[36] +
+               C34 * (4.f * zz - 3.f * xx - yy) * s[39] + 2.f * C35 * xz * s[42] + 3.f * C36 * (xx - yy) * s[45];
+    J[ch][1] = -C1 * s[3] + C20 * x * s[12] + C21 * z * s[15] - 2.f * C22 * y * s[18] - 2.f * C24 * y * s[24] +
+               3.f * C30 * (xx - yy) * s[27] + C31 * xz * s[30] + C32 * (4.f * zz - xx - 3.f * yy) * s[33] -
+               6.f * C33 * yz * s[36] - 2.f * C34 * xy * s[39] - 2.f * C35 * yz * s[42] - 6.f * C36 * xy * s[45];
+    J[ch][2] = C1 * s[6] + C21 * y * s[15] + 4.f * C22 * z * s[18] + C23 * x * s[21] + C31 * xy * s[30] +
+               8.f * C32 * yz * s[33] + C33 * (6.f * zz - 3.f * xx - 3.f * yy) * s[36] + 8.f * C34 * xz * s[39] +
+               C35 * (xx - yy) * s[42];
+  }
+  float4* jp = a.jdir + 3 * f;
+  jp[0] = make_float4(J[0][0], J[0][1], J[0][2], J[1][0]);
+  jp[1] = make_float4(J[1][1], J[1][2], J[2][0], J[2][1]);
+  jp[2] = make_float4(J[2][2], __uint_as_float(clamped), 0.f, 0.f);
 }
 
 // SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2.

@@ -6,7 +6,10 @@
 //   t_c -> mu (Rcam^T), Sigma = M M^T with M = R(q) diag(s) -> ds, dq (R(q) as written, R13),
 //   SH colour -> dsh and, through the normalised view direction, -> dmu (R2 clamp mask).
 // One thread per projected local record; gradients are accumulated (+=) into the caller's
-// parameter-shaped buffers (each local Gaussian has at most one record per view).
+// parameter-shaped buffers (each local Gaussian has at most one record per view).  The colour's
+// direction derivative comes from k_color (the 3x3 Jacobian sum_k sh[k][ch] dY_k/ddir and the clamp
+// bits, 48 B per record), so neither kernel here reads the 192-B SH row: k_project_bwd applies the
+// direction term with the geometry, k_project_bwd_shg only writes dsh = Y_k dcol.
 #include <cstdlib>
 
 #include "bgs_internal.cuh"
@@ -155,186 +158,75 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjectBwdArgs a) {
   gy += 2.f * qz * dRq[2][1]; gz += 2.f * qy * dRq[2][1]; gw += 2.f * qx * dRq[2][1]; gx += 2.f * w * dRq[2][1];
   gx -= 4.f * qx * dRq[2][2]; gy -= 4.f * qy * dRq[2][2];
 
+  // colour -> view direction (mu - c_v)/|mu - c_v| -> mu: dL/ddir = sum_ch dcol_ch J[ch], then the
+  // normalisation's projection (I - d d^T)/|mu - c_v|
+  {
+    const float4 j0 = __ldg(a.jdir + 3 * f), j1 = __ldg(a.jdir + 3 * f + 1), j2 = __ldg(a.jdir + 3 * f + 2);
+    const uint32_t clamped = __float_as_uint(j2.y);
+    const float d0 = (clamped & 1u) ? 0.f : g[6], d1 = (clamped & 2u) ? 0.f : g[7], d2 = (clamped & 4u) ? 0.f : g[8];
+    const float gx_ = d0 * j0.x + d1 * j0.w + d2 * j1.z;
+    const float gy_ = d0 * j0.y + d1 * j1.x + d2 * j1.w;
+    const float gz_ = d0 * j0.z + d1 * j1.y + d2 * j2.x;
+    const float ddx = mo.x - cm.campos[0], ddy = mo.y - cm.campos[1], ddz = mo.z - cm.campos[2];
+    const float il = 1.f / sqrtf(ddx * ddx + ddy * ddy + ddz * ddz);
+    const float X = ddx * il, Y = ddy * il, Z = ddz * il;
+    const float dot = gx_ * X + gy_ * Y + gz_ * Z;
+    dmu[0] += (gx_ - X * dot) * il;
+    dmu[1] += (gy_ - Y * dot) * il;
+    dmu[2] += (gz_ - Z * dot) * il;
+  }
+
   // accumulate with 128-bit reductions (no read round trip on the SM; the L2 adds)
   atomicAdd(a.g_mean_opac + i, make_float4(dmu[0], dmu[1], dmu[2], g[5]));
   atomicAdd(a.g_quat + i, make_float4(gw, gx, gy, gz));
   atomicAdd(a.g_scale + i, make_float4(ds[0], ds[1], ds[2], 0.f));
 }
 
-// SH colour backward (second kernel: keeps each kernel's register footprint small so enough
-// warps are resident to hide the scattered 192-B row loads)
-__global__ void __launch_bounds__(256) k_project_bwd_sh(ProjectBwdArgs a) {
-  const int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// dL/dsh[k][ch] = Y_k(dir) dcol_ch (dcol = 0 on clamped channels, R2).  kT threads per record
+// (adjacent lanes), each writing 16 / kT coefficients = 12 / kT float4 of the gradient row with
+// 128-bit reductions: no SH row read (k_color's clamp bits decide dcol).
+template <int kT>
+__global__ void __launch_bounds__(256) k_project_bwd_shg(ProjectBwdArgs a) {
+  constexpr int kC = 16 / kT;      // coefficients per thread
+  constexpr int kQ = 3 * kC / 4;   // float4 per thread
+  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t f = t / kT;
+  const int h = int(threadIdx.x % kT);
   if (f >= a.F) return;
   const uint32_t i = a.rec_lidx[f];
   const CameraK& cm = a.cam;
   const float4 mo = __ldg(a.mean_opac + i);
   const float* g = a.acc[f].g;
-  const float g6 = g[6], g7 = g[7], g8 = g[8];
+  const uint32_t clamped = __float_as_uint(__ldg(reinterpret_cast<const float*>(a.jdir + 3 * f + 2) + 1));
+  const float dcol[3] = {(clamped & 1u) ? 0.f : g[6], (clamped & 2u) ? 0.f : g[7], (clamped & 4u) ? 0.f : g[8]};
   const float ddx = mo.x - cm.campos[0], ddy = mo.y - cm.campos[1], ddz = mo.z - cm.campos[2];
-  const float len = sqrtf(ddx * ddx + ddy * ddy + ddz * ddz), il = 1.f / len;
+  const float il = 1.f / sqrtf(ddx * ddx + ddy * ddy + ddz * ddz);
   const float X = ddx * il, Y = ddy * il, Z = ddz * il;
   const float xx = X * X, yy = Y * Y, zz = Z * Z, xy = X * Y, yz = Y * Z, xz = X * Z;
-  float Yb[16];
-  Yb[0] = 0.28209479177387814f;
-  Yb[1] = -SHC1 * Y;
-  Yb[2] = SHC1 * Z;
-  Yb[3] = -SHC1 * X;
-  Yb[4] = SHC2[0] * xy;
-  Yb[5] = SHC2[1] * yz;
-  Yb[6] = SHC2[2] * (2.f * zz - xx - yy);
-  Yb[7] = SHC2[3] * xz;
-  Yb[8] = SHC2[4] * (xx - yy);
-  Yb[9] = SHC3[0] * Y * (3.f * xx - yy);
-  Yb[10] = SHC3[1] * xy * Z;
-  Yb[11] = SHC3[2] * Y * (4.f * zz - xx - yy);
-  Yb[12] = SHC3[3] * Z * (2.f * zz - 3.f * xx - 3.f * yy);
-  Yb[13] = SHC3[4] * X * (4.f * zz - xx - yy);
-  Yb[14] = SHC3[5] * Z * (xx - yy);
-  Yb[15] = SHC3[6] * X * (xx - 3.f * yy);
-  const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i);
-  float v[48];
-#pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    const float4 t = __ldg(shp + k);
-    v[4 * k] = t.x;
-    v[4 * k + 1] = t.y;
-    v[4 * k + 2] = t.z;
-    v[4 * k + 3] = t.w;
-  }
-  float dcol[3];
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    float c = 0.5f;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) c += Yb[k] * v[3 * k + ch];
-    dcol[ch] = c < 0.f ? 0.f : (ch == 0 ? g6 : (ch == 1 ? g7 : g8));
-  }
-  float sk[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) sk[k] = dcol[0] * v[3 * k] + dcol[1] * v[3 * k + 1] + dcol[2] * v[3 * k + 2];
-  // d(sum_k sk Y_k)/d(x,y,z): the partial derivatives of the 16 basis functions, written out
-  float ddir[3];
-  ddir[0] = -SHC1 * sk[3] + SHC2[0] * Y * sk[4] - 2.f * SHC2[2] * X * sk[6] + SHC2[3] * Z * sk[7] +
-            2.f * SHC2[4] * X * sk[8] + 6.f * SHC3[0] * xy * sk[9] + SHC3[1] * yz * sk[10] -
-            2.f * SHC3[2] * xy * sk[11] - 6.f * SHC3[3] * xz * sk[12] + SHC3[4] * (4.f * zz - 3.f * xx - yy) * sk[13] +
-            2.f * SHC3[5] * xz * sk[14] + 3.f * SHC3[6] * (xx - yy) * sk[15];
-  ddir[1] = -SHC1 * sk[1] + SHC2[0] * X * sk[4] + SHC2[1] * Z * sk[5] - 2.f * SHC2[2] * Y * sk[6] -
-            2.f * SHC2[4] * Y * sk[8] + 3.f * SHC3[0] * (xx - yy) * sk[9] + SHC3[1] * xz * sk[10] +
-            SHC3[2] * (4.f * zz - xx - 3.f * yy) * sk[11] - 6.f * SHC3[3] * yz * sk[12] - 2.f * SHC3[4] * xy * sk[13] -
-            2.f * SHC3[5] * yz * sk[14] - 6.f * SHC3[6] * xy * sk[15];
-  ddir[2] = SHC1 * sk[2] + SHC2[1] * Y * sk[5] + 4.f * SHC2[2] * Z * sk[6] + SHC2[3] * X * sk[7] +
-            SHC3[1] * xy * sk[10] + 8.f * SHC3[2] * yz * sk[11] + SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * sk[12] +
-            8.f * SHC3[4] * xz * sk[13] + SHC3[5] * (xx - yy) * sk[14];
-  const float dot = ddir[0] * X + ddir[1] * Y + ddir[2] * Z;
-  atomicAdd(a.g_mean_opac + i, make_float4((ddir[0] - X * dot) * il, (ddir[1] - Y * dot) * il,
-                                           (ddir[2] - Z * dot) * il, 0.f));
-  float4* gsh = reinterpret_cast<float4*>(a.g_sh + size_t(48) * i);
-#pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    const int e = 4 * k;
-    atomicAdd(gsh + k, make_float4(Yb[(e) / 3] * dcol[(e) % 3], Yb[(e + 1) / 3] * dcol[(e + 1) % 3],
-                                   Yb[(e + 2) / 3] * dcol[(e + 2) % 3], Yb[(e + 3) / 3] * dcol[(e + 3) % 3]));
-  }
-}
-
-// kT threads per record (adjacent lanes; 16 / kT SH coefficients = 12 / kT float4 of the row each):
-// the colour (clamp test) and the direction gradient (per-coefficient basis derivatives) are
-// completed with shuffles over the group.  Fewer registers per thread than one thread per record,
-// so more warps and more of the scattered 192-B row loads in flight: project_bwd 0.142 (1 thread)
-// -> 0.127 (2) -> 0.119 ms (4) per Rubble view, 1462 -> 1494 -> 1507 views/s in flight.
-template <int kT>
-__global__ void __launch_bounds__(256) k_project_bwd_shn(ProjectBwdArgs a) {
-  constexpr int kC = 16 / kT;      // coefficients per thread
-  constexpr int kV = 3 * kC;       // floats per thread
-  constexpr int kQ = kV / 4;       // float4 per thread
-  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t f = t / kT;
-  const int h = int(threadIdx.x % kT);
-  const bool live = f < a.F;
-  const int64_t fr = live ? f : 0;
-  const uint32_t i = a.rec_lidx[fr];
-  const CameraK& cm = a.cam;
-  const float4 mo = __ldg(a.mean_opac + i);
-  const float* g = a.acc[fr].g;
-  const float g6 = g[6], g7 = g[7], g8 = g[8];
-  const float ddx = mo.x - cm.campos[0], ddy = mo.y - cm.campos[1], ddz = mo.z - cm.campos[2];
-  const float len = sqrtf(ddx * ddx + ddy * ddy + ddz * ddz), il = 1.f / len;
-  const float X = ddx * il, Y = ddy * il, Z = ddz * il;
-  const float xx = X * X, yy = Y * Y, zz = Z * Z, xy = X * Y, yz = Y * Z, xz = X * Z;
-  float Yb[kC], dY[kC][3];
+  float Yb[kC];
 #pragma unroll
   for (int c = 0; c < kC; ++c) {
     const int k = kC * h + c;
-    float y0 = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
+    float y0;
     switch (k) {
       case 0: y0 = 0.28209479177387814f; break;
-      case 1: y0 = -SHC1 * Y; dy = -SHC1; break;
-      case 2: y0 = SHC1 * Z; dz = SHC1; break;
-      case 3: y0 = -SHC1 * X; dx = -SHC1; break;
-      case 4: y0 = SHC2[0] * xy; dx = SHC2[0] * Y; dy = SHC2[0] * X; break;
-      case 5: y0 = SHC2[1] * yz; dy = SHC2[1] * Z; dz = SHC2[1] * Y; break;
-      case 6: y0 = SHC2[2] * (2.f * zz - xx - yy); dx = -2.f * SHC2[2] * X; dy = -2.f * SHC2[2] * Y;
-              dz = 4.f * SHC2[2] * Z; break;
-      case 7: y0 = SHC2[3] * xz; dx = SHC2[3] * Z; dz = SHC2[3] * X; break;
-      case 8: y0 = SHC2[4] * (xx - yy); dx = 2.f * SHC2[4] * X; dy = -2.f * SHC2[4] * Y; break;
-      case 9: y0 = SHC3[0] * Y * (3.f * xx - yy); dx = 6.f * SHC3[0] * xy; dy = 3.f * SHC3[0] * (xx - yy); break;
-      case 10: y0 = SHC3[1] * xy * Z; dx = SHC3[1] * yz; dy = SHC3[1] * xz; dz = SHC3[1] * xy; break;
-      case 11: y0 = SHC3[2] * Y * (4.f * zz - xx - yy); dx = -2.f * SHC3[2] * xy;
-               dy = SHC3[2] * (4.f * zz - xx - 3.f * yy); dz = 8.f * SHC3[2] * yz; break;
-      case 12: y0 = SHC3[3] * Z * (2.f * zz - 3.f * xx - 3.f * yy); dx = -6.f * SHC3[3] * xz;
-               dy = -6.f * SHC3[3] * yz; dz = SHC3[3] * (6.f * zz - 3.f * xx - 3.f * yy); break;
-      case 13: y0 = SHC3[4] * X * (4.f * zz - xx - yy); dx = SHC3[4] * (4.f * zz - 3.f * xx - yy);
-               dy = -2.f * SHC3[4] * xy; dz = 8.f * SHC3[4] * xz; break;
-      case 14: y0 = SHC3[5] * Z * (xx - yy); dx = 2.f * SHC3[5] * xz; dy = -2.f * SHC3[5] * yz;
-               dz = SHC3[5] * (xx - yy); break;
-      default: y0 = SHC3[6] * X * (xx - 3.f * yy); dx = 3.f * SHC3[6] * (xx - yy); dy = -6.f * SHC3[6] * xy; break;
+      case 1: y0 = -SHC1 * Y; break;
+      case 2: y0 = SHC1 * Z; break;
+      case 3: y0 = -SHC1 * X; break;
+      case 4: y0 = SHC2[0] * xy; break;
+      case 5: y0 = SHC2[1] * yz; break;
+      case 6: y0 = SHC2[2] * (2.f * zz - xx - yy); break;
+      case 7: y0 = SHC2[3] * xz; break;
+      case 8: y0 = SHC2[4] * (xx - yy); break;
+      case 9: y0 = SHC3[0] * Y * (3.f * xx - yy); break;
+      case 10: y0 = SHC3[1] * xy * Z; break;
+      case 11: y0 = SHC3[2] * Y * (4.f * zz - xx - yy); break;
+      case 12: y0 = SHC3[3] * Z * (2.f * zz - 3.f * xx - 3.f * yy); break;
+      case 13: y0 = SHC3[4] * X * (4.f * zz - xx - yy); break;
+      case 14: y0 = SHC3[5] * Z * (xx - yy); break;
+      default: y0 = SHC3[6] * X * (xx - 3.f * yy); break;
     }
     Yb[c] = y0;
-    dY[c][0] = dx;
-    dY[c][1] = dy;
-    dY[c][2] = dz;
-  }
-  const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i) + kQ * h;
-  float v[kV];
-#pragma unroll
-  for (int k = 0; k < kQ; ++k) {
-    const float4 q = __ldg(shp + k);
-    v[4 * k] = q.x;
-    v[4 * k + 1] = q.y;
-    v[4 * k + 2] = q.z;
-    v[4 * k + 3] = q.w;
-  }
-  float cp[3];
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    float c = h == 0 ? 0.5f : 0.f;
-#pragma unroll
-    for (int k = 0; k < kC; ++k) c += Yb[k] * v[3 * k + ch];
-#pragma unroll
-    for (int o = 1; o < kT; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    cp[ch] = c;
-  }
-  float dcol[3];
-#pragma unroll
-  for (int ch = 0; ch < 3; ++ch) dcol[ch] = cp[ch] < 0.f ? 0.f : (ch == 0 ? g6 : (ch == 1 ? g7 : g8));
-  float ddir[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-  for (int k = 0; k < kC; ++k) {
-    const float sk = dcol[0] * v[3 * k] + dcol[1] * v[3 * k + 1] + dcol[2] * v[3 * k + 2];
-    ddir[0] += sk * dY[k][0];
-    ddir[1] += sk * dY[k][1];
-    ddir[2] += sk * dY[k][2];
-  }
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int o = 1; o < kT; o <<= 1) ddir[d] += __shfl_xor_sync(0xffffffffu, ddir[d], o);
-  if (!live) return;
-  if (h == 0) {
-    const float dot = ddir[0] * X + ddir[1] * Y + ddir[2] * Z;
-    atomicAdd(a.g_mean_opac + i, make_float4((ddir[0] - X * dot) * il, (ddir[1] - Y * dot) * il,
-                                             (ddir[2] - Z * dot) * il, 0.f));
   }
   float4* gsh = reinterpret_cast<float4*>(a.g_sh + size_t(48) * i) + kQ * h;
 #pragma unroll
@@ -350,14 +242,7 @@ __global__ void __launch_bounds__(256) k_project_bwd_shn(ProjectBwdArgs a) {
 void launch_project_bwd(const ProjectBwdArgs& a, cudaStream_t s) {
   if (a.F <= 0) return;
   k_project_bwd<<<unsigned((a.F + 127) / 128), 128, 0, s>>>(a);
-  const char* e = getenv("BGS_SH_BWD");  // A/B: threads per record (1, 2 or 4)
-  const int mode = e ? atoi(e) : 4;
-  if (mode == 1)
-    k_project_bwd_sh<<<unsigned((a.F + 255) / 256), 256, 0, s>>>(a);
-  else if (mode == 2)
-    k_project_bwd_shn<2><<<unsigned((2 * a.F + 255) / 256), 256, 0, s>>>(a);
-  else
-    k_project_bwd_shn<4><<<unsigned((4 * a.F + 255) / 256), 256, 0, s>>>(a);
+  k_project_bwd_shg<4><<<unsigned((4 * a.F + 255) / 256), 256, 0, s>>>(a);
 }
 
 }  // namespace bgs

@@ -192,11 +192,12 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
           my_a = cnt;
         }
       } else {
-        contrib |= uint32_t(__any_sync(0xffffffffu, cs != 0)) << j;
+        contrib |= uint32_t(cs != 0) << j;  // this lane's pixels; OR-reduced over the warp below
       }
     }
     // contributor mask of this chunk for the backward: bit j = some pixel of the block took record j
     if (kImportance) contrib = __ballot_sync(0xffffffffu, my_a != 0);
+    else contrib = __reduce_or_sync(0xffffffffu, contrib);
     if (lane == 0) a.cmask[widx] = contrib;
     if (kImportance && my_a) {
       Acc* acc = a.acc + __float_as_uint(st.co.w);
@@ -406,8 +407,8 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
             atomicAdd(dst + 8, g[8]);
         continue;
       }
-      // transposed butterfly over g[0..7]: lane ends with the warp sum of g[my_idx]
       float v4[4], v2[2], v1;
+      // transposed butterfly over g[0..7]: lane ends with the warp sum of g[my_idx]
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float send = xsel(hi16, g[i], g[i + 4]);

@@ -59,6 +59,7 @@ struct bgs_ctx {
   int t_begin = 0, t_end = 0, n_passes = 0, fallback = 0;
   int raster_split = 0;  // heavy tiles split over two CTAs in the last forward (the backward reuses it)
   int imp_parity = 0;  // which half of imp_hist the next world-1 importance call uses
+  bool colored = false;  // the last projection ran k_color (its Jacobian feeds bgs_project_bwd)
   int pend_gate = 0, pend_fb_num = 0, pend_fb_den = 1;  // gate of the enqueued projection (project_finish)
   const Rec* recv = nullptr;  // == recs at world 1
   Acc* acc_local = nullptr;   // == acc at world 1
@@ -69,6 +70,7 @@ struct bgs_ctx {
       loss_img, loss_part, loss_sums, scr_tgt, scr_loss, scr_in2,
       scr_dlsup,  // supervised steps' dL/dC (never one of the host-upload double buffers)
       bucket_cur,  // per-tile write cursors of the bucket sort
+      jdir,  // per local record: k_color's colour Jacobian wrt the view direction + clamp bits (a11 input)
       imp_cand, imp_gath;  // world > 1 importance: this rank's crossing-bin candidates, all ranks' gathered
   // NEXT-1 simplification scratch (selection keys / state / histograms, keep masks, row exchange)
   DevBuf sel_keys, sel_state, sel_hist, masks, sblocks, new_gid, rows_send, rows_recv, dcnt;
@@ -611,7 +613,7 @@ bgs_status bgs_ctx_destroy(bgs_ctx* c) {
                     &c->dest_mask, &c->block_counts, &c->totals, &c->send_base, &c->send, &c->recvbuf,
                     &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1], &c->digit_hist, &c->pass_ctrl, &c->status,
                     &c->ranges, &c->acc, &c->rev, &c->accl, &c->imp_state, &c->imp_hist, &c->imp_total,
-                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2, &c->scr_dlsup, &c->bucket_cur, &c->imp_cand, &c->imp_gath,
+                    &c->scr_rgb, &c->scr_t, &c->scr_n, &c->scr_dl, &c->xchg_counts, &c->aux, &c->tile_perm, &c->cand, &c->wbuf, &c->cmask, &c->loss_img, &c->loss_part, &c->loss_sums, &c->scr_tgt, &c->scr_loss, &c->scr_in2, &c->scr_dlsup, &c->bucket_cur, &c->jdir, &c->imp_cand, &c->imp_gath,
                     &c->sel_keys, &c->sel_state, &c->sel_hist, &c->masks, &c->sblocks, &c->new_gid, &c->rows_send,
                     &c->rows_recv, &c->dcnt};
   for (DevBuf* b : bufs)
@@ -747,6 +749,9 @@ static bgs_status project_enqueue(bgs_ctx* ctx, const bgs_gaussians* g, const bg
   CKS(ensure(ctx, ctx->recs, size_t(std::max<int64_t>(g->n_local, 1)) * sizeof(Rec)));
   CKS(ensure(ctx, ctx->rec_lidx, size_t(std::max<int64_t>(g->n_local, 1)) * 4));
   CKS(ensure(ctx, ctx->cand, size_t(std::max<int64_t>(g->n_local, 1)) * 4));
+  if (!(flags & BGS_NO_COLOR)) CKS(ensure(ctx, ctx->jdir, size_t(std::max<int64_t>(g->n_local, 1)) * 48));
+  a.jdir = P_<float4>(ctx->jdir);
+  ctx->colored = !(flags & BGS_NO_COLOR);
   a.recs = P_<Rec>(ctx->recs);
   a.rec_lidx = P_<uint32_t>(ctx->rec_lidx);
   a.cand = P_<uint32_t>(ctx->cand);
@@ -1127,6 +1132,7 @@ bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camer
   CKS(check_gaussians(ctx, g));
   if (ctx->stage < 6) return fail(ctx, BGS_ERR_CONTRACT, "bgs_project_bwd before bgs_route_reverse");
   if (g->n_local != ctx->n_local) return fail(ctx, BGS_ERR_CONTRACT, "n_local differs from bgs_project's");
+  if (!ctx->colored) return fail(ctx, BGS_ERR_CONTRACT, "bgs_project_bwd after a BGS_NO_COLOR projection");
   if (!grads || !grads->mean_opac || !grads->quat || !grads->scale || !grads->sh)
     return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "gradient pointer is NULL");
   if (!cam) return fail(ctx, BGS_ERR_INVALID_ARGUMENT, "camera is NULL");
@@ -1138,6 +1144,7 @@ bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camer
   a.sh = g->sh;
   a.rec_lidx = P_<uint32_t>(ctx->rec_lidx);
   a.acc = ctx->acc_local;
+  a.jdir = P_<float4>(ctx->jdir);
   a.F = ctx->F;
   a.cam = ctx->cam;
   a.g_mean_opac = reinterpret_cast<float4*>(grads->mean_opac);

@@ -2,7 +2,8 @@
 
 These are what the METHOD must move or compute, not what a kernel happens to do:
   a1+a2 project      16 N (mu,o) + 1 N (lod) + N/8 (cull column, if any) + 32 A (q, s of active)
-                     + 192 F (SH of in-frustum) + 52 F (record + index) + 4 N (radius)      [bytes]
+                     + 192 F (SH of in-frustum) + 52 F (record + index) + 48 F (colour Jacobian
+                     along the view direction + clamp bits, for a11) + 4 N (radius)           [bytes]
   a5-a7 sort         16 R (rect, depth of received) + 8 P (u32 key + u32 value written) + 16 P
                      per executed 8-bit radix pass (read + write) + 4 P (ranges pass)     [bytes]
   a8 raster fwd      SURVEY §8(d): ~17 FP32 lane-ops per CONTRIBUTING (pixel, splat) pair (dx,dy 2,
@@ -17,7 +18,8 @@ These are what the METHOD must move or compute, not what a kernel happens to do:
                      E_min entry (every list entry up to a pixel's last contributor, sum of n_contrib);
                      exact box culling skips most of those, so that fraction can exceed 1.
   a10 reverse (M>1)  48 D (send back) + 48 D (gather)                                     [bytes]
-  a11 project bwd    240 F (params) + 52 F (partials + index) + 2 x 236 F (grads RMW)     [bytes]
+  a11 project bwd    48 F (mu, o, q, s) + 48 F (colour Jacobian + clamp bits) + 52 F (partials +
+                     index) + 2 x 236 F (grads RMW; the SH row itself is read once, by a2)  [bytes]
   a12 importance     52 F (w, a, index) + 2 x 16 F (s, c_rad, c_vis RMW) + N/8 (Cull)    [bytes]
   NEXT-4 loss        213 FP32 ops per image element (3 H W): window statistics 3 products +
                      5 maps x 2 separable 11-tap passes = 113, SSIM and its partials 25,
@@ -35,7 +37,7 @@ FWD_OPS_EMIN = 19.0  # per E_min entry (DESIGN.md recount; diagnostic)
 BWD_OPS_EMIN = 33.0
 LOSS_OPS = 213.0
 KERNEL = {"project": "k_cull+k_project+k_color", "sort": "k_emit+k_onesweep+k_ranges_fixup",
-          "raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project_bwd": "k_project_bwd(+_sh)",
+          "raster_fwd": "k_raster_fwd", "raster_bwd": "k_raster_bwd", "project_bwd": "k_project_bwd+k_project_bwd_shg",
           "importance": "k_imp_coop", "loss": "k_loss_photo"}
 ALU_UNIT = "T lane-op/s"
 
@@ -57,11 +59,11 @@ def stage_rooflines(stage_ms, qs, n_local, W, H, world, peaks, sm_mhz=None, E=No
     names = names or ("project", "route", "sort", "raster_fwd", "loss", "raster_bwd", "route_reverse", "project_bwd",
                       "importance")
     bytes_ = {
-        "project": 16 * N + N + (N / 8 if cull else 0) + 32 * A + 192 * F + 52 * F + 4 * N,
+        "project": 16 * N + N + (N / 8 if cull else 0) + 32 * A + 192 * F + 52 * F + 48 * F + 4 * N,
         "route": (48 * D + 48 * R) if world > 1 else 0.0,
         "sort": 16 * R + 8 * P + 16 * P * passes + 4 * P,
         "route_reverse": (96 * D) if world > 1 else 0.0,
-        "project_bwd": 240 * F + 52 * F + 2 * 236 * F,
+        "project_bwd": 48 * F + 48 * F + 52 * F + 2 * 236 * F,
         "importance": 52 * F + 32 * F + N / 8,
     }
     E = float(E) if E is not None else 0.0
