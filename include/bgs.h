@@ -224,7 +224,9 @@ bgs_status bgs_raster_bwd(bgs_ctx* ctx, const float* dL_drgb, const float* t_fin
  * pass "bypasses color shading" and has no backward); the gradients are then zero. */
 bgs_status bgs_route_reverse(bgs_ctx* ctx, uint32_t flags, void* stream);
 
-/* a11.  grads += d(loss)/d(activated params) for every projected local Gaussian. */
+/* a11.  grads += d(loss)/d(activated params) for every projected local Gaussian.  Reads the colour
+ * Jacobian along the view direction that a2 left in the arena, so the projection of this view must
+ * not have used BGS_NO_COLOR (BGS_ERR_CONTRACT otherwise). */
 bgs_status bgs_project_bwd(bgs_ctx* ctx, const bgs_gaussians* g, const bgs_camera* cam,
                            const bgs_gaussian_grads* grads, void* stream);
 
