@@ -101,7 +101,7 @@ _FIELD_DTYPES = {
     "w_fixed": np.uint64, "a": np.uint32, "g2d": np.float64, "d_mean": np.float64, "d_quat": np.float64,
     "d_scale": np.float64, "d_opac": np.float64, "d_sh": np.float64, "n_pairs_total": np.int64,
     "mean2d": np.float64, "conic": np.float64, "depth": np.float64, "rgb": np.float64, "thr": np.float64,
-    "rect": np.int32, "phase_seconds": np.float64, "img64": np.float64, "margins": np.float64, "tile_range": np.int32, "recv": np.int64, "pair_tile": np.int32, "pair_gid": np.int64,
+    "rect": np.int32, "rect3": np.int32, "phase_seconds": np.float64, "img64": np.float64, "margins": np.float64, "tile_range": np.int32, "recv": np.int64, "pair_tile": np.int32, "pair_gid": np.int64,
     "range_lo": np.int64, "range_hi": np.int64,
 }
 

@@ -105,7 +105,8 @@ struct Proj {
   T opac = 0;
   T thr = 0;               // alpha-test threshold in power space (D3 / R9)
   int radius = 0;
-  int rect[4] = {0, 0, 0, 0};  // xmin, ymin, xmax, ymax (tiles, exclusive max)
+  int rect[4] = {0, 0, 0, 0};   // tile footprint (R5): xmin, ymin, xmax, ymax (tiles, exclusive max)
+  int rect3[4] = {0, 0, 0, 0};  // the 3DGS rect it is cut from (validity, brute force)
   double int_margin = 1e30;    // distance of the pre-truncation floats to an integer (FD safety)
 };
 
@@ -268,6 +269,31 @@ Proj<T> project_one(const Scene& s, int64_t i, const Camera& cam, bool no_color)
   p.depth = tz;
   p.opac = T(s.opac[i]);
   p.thr = thr_of<T>(p.opac);
+  // Tile footprint (reading R5): the 3DGS rect cut to the tiles holding pixel centres of the box
+  // around the alpha >= 1/255 ellipse {d : d^T Q d <= -2 thr} (half extents sqrt(-2 thr (Q^-1)_xx),
+  // sqrt(-2 thr (Q^-1)_yy), widened by 1e-3 relative + 0.01 px so the box holds every pixel whose
+  // fp32 cut test passes).  A tile outside it has no pixel where the splat passes the alpha cut,
+  // so N(p) of Eq.2 is unchanged at every pixel (pin P1: tiled == brute force over the 3DGS rects).
+  for (int c = 0; c < 4; ++c) p.rect3[c] = p.rect[c];
+  {
+    T kk = k<T>(-2.0) * p.thr;
+    T cdet = p.A * p.C - p.B * p.B;
+    if (kk > T(0) && cdet > T(0)) {
+      T hx = std::sqrt((kk * p.C) / cdet) * k<T>(1.001) + k<T>(0.01);
+      T hy = std::sqrt((kk * p.A) / cdet) * k<T>(1.001) + k<T>(0.01);
+      int ex0 = static_cast<int>(tmin(T(TX), tmax(T(0), std::floor((p.mx - hx) / k<T>(16.0)))));
+      int ey0 = static_cast<int>(tmin(T(TY), tmax(T(0), std::floor((p.my - hy) / k<T>(16.0)))));
+      int ex1 = static_cast<int>(tmin(T(TX), tmax(T(0), std::floor((p.mx + hx) / k<T>(16.0)) + k<T>(1.0))));
+      int ey1 = static_cast<int>(tmin(T(TY), tmax(T(0), std::floor((p.my + hy) / k<T>(16.0)) + k<T>(1.0))));
+      p.rect[0] = std::max(p.rect[0], ex0);
+      p.rect[1] = std::max(p.rect[1], ey0);
+      p.rect[2] = std::max(p.rect[0], std::min(p.rect[2], ex1));
+      p.rect[3] = std::max(p.rect[1], std::min(p.rect[3], ey1));
+    } else {  // o <= 1/255: no pixel passes the cut
+      p.rect[2] = p.rect[0];
+      p.rect[3] = p.rect[1];
+    }
+  }
   if (!no_color) {
     // view-dependent colour c_i(d), d = (mu - c_v)/|mu - c_v|  (R1 degree 3, R2 clamp)
     T dx = mx - T(cam.campos[0]), dy = my - T(cam.campos[1]), dz = mz - T(cam.campos[2]);
@@ -872,6 +898,14 @@ int64_t get_field(Step<T>& st, const std::string& name, int rank, void* out) {
     }
     return 4 * n;
   }
+  if (name == "rect3") {
+    if (out) {
+      int32_t* o = static_cast<int32_t*>(out);
+      for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < 4; ++c) o[4 * i + c] = st.proj[i].valid ? st.proj[i].rect3[c] : 0;
+    }
+    return 4 * n;
+  }
   // per-owner structures
   if (rank < 0 || rank >= st.M) return -1;
   OwnerState& os = st.owners[rank];
@@ -970,7 +1004,7 @@ void or_bruteforce(void* hv, float* img, float* t_final, int32_t* n_contrib_all)
       int cnt = 0;
       for (int64_t g : order) {
         const Proj<float>& p = st.proj[g];
-        if (tx < p.rect[0] || tx >= p.rect[2] || ty < p.rect[1] || ty >= p.rect[3]) continue;
+        if (tx < p.rect3[0] || tx >= p.rect3[2] || ty < p.rect3[1] || ty >= p.rect3[3]) continue;
         float dx = p.mx - float(px), dy = p.my - float(py);
         float power = -neg_power<float>(p.A, p.B, p.C, dx, dy);
         if (power > 0.f || power < p.thr) continue;

@@ -172,6 +172,26 @@ __device__ __forceinline__ ProjOut project_exact(const ProjectArgs& a, int64_t i
         radius = rad;
         o.depth = tz;
         o.opac = mo.w;
+        // tile footprint (reading R5, the oracle's project_one): the 3DGS rect cut to the tiles
+        // holding pixel centres of the widened alpha >= 1/255 box; same float expressions
+        const float kk = -2.0f * alpha_cut_thr(mo.w);
+        const float cdet = o.A * o.C - o.B * o.B;
+        if (kk > 0.0f && cdet > 0.0f) {
+          const float hx = sqrtf((kk * o.C) / cdet) * 1.001f + 0.01f;
+          const float hy = sqrtf((kk * o.A) / cdet) * 1.001f + 0.01f;
+          const int ex0 = int(fminf(float(cm.TX), fmaxf(0.0f, floorf((o.mx - hx) / 16.0f))));
+          const int ey0 = int(fminf(float(cm.TY), fmaxf(0.0f, floorf((o.my - hy) / 16.0f))));
+          const int ex1 = int(fminf(float(cm.TX), fmaxf(0.0f, floorf((o.mx + hx) / 16.0f) + 1.0f)));
+          const int ey1 = int(fminf(float(cm.TY), fmaxf(0.0f, floorf((o.my + hy) / 16.0f) + 1.0f)));
+          o.x0 = max(o.x0, ex0);
+          o.y0 = max(o.y0, ey0);
+          o.x1 = max(o.x0, min(o.x1, ex1));
+          o.y1 = max(o.y0, min(o.y1, ey1));
+        } else {  // o <= 1/255: no pixel passes the cut
+          o.x1 = o.x0;
+          o.y1 = o.y0;
+        }
+        o.area = uint32_t((o.x1 - o.x0) * (o.y1 - o.y0));
         if (!a.no_color) {
           o.mux = mo.x;
           o.muy = mo.y;

@@ -571,3 +571,48 @@ def test_P6b_view_direction_sign():
         out[side] = st.get("rgb").reshape(-1, 3)[0, 0]
     # camera on the -x side: the ray camera -> Gaussian runs along +x
     assert abs(out["minus_x"] - 0.7) < 1e-6 and abs(out["plus_x"] - 0.3) < 1e-6, out
+
+
+# ------------------------------------------------------------------------------------------
+# P18: the tile footprint (reading R5) = the 3DGS rect cut to the box of the alpha >= 1/255
+# ellipse.  Pinned against the alpha test written out in fp64 numpy (Eq.2's N(p) membership,
+# R9: alpha = o exp(power) >= 1/255), not against the oracle's own box: every pixel centre of the
+# 3DGS rect where a splat passes the cut must lie in one of its footprint tiles.  P1 (tiled ==
+# brute force over the 3DGS rects, any M) pins the same property through the rendered image.
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("seed", [1, 2])
+def test_P18_footprint_holds_every_passing_pixel(seed):
+    sc = S.gen_tiny(seed=seed, n=3000)
+    cam = sc.cameras[0]
+    st = O.OracleStep(sc, cam)
+    TX = (cam["W"] + 15) // 16
+    rad = st.get("radius")
+    fp = st.get("rect").reshape(-1, 4)
+    r3 = st.get("rect3").reshape(-1, 4)
+    m2 = st.get("mean2d").reshape(-1, 2)
+    con = st.get("conic").reshape(-1, 3)
+    opac = sc.opac.astype(np.float64).ravel()
+    valid = np.nonzero(rad > 0)[0]
+    assert np.all(fp[valid, 0] >= r3[valid, 0]) and np.all(fp[valid, 1] >= r3[valid, 1])
+    assert np.all(fp[valid, 2] <= r3[valid, 2]) and np.all(fp[valid, 3] <= r3[valid, 3])
+    area = lambda r: np.maximum(r[:, 2] - r[:, 0], 0) * np.maximum(r[:, 3] - r[:, 1], 0)
+    a_fp, a_r3 = area(fp[valid]).sum(), area(r3[valid]).sum()
+    assert a_fp < 0.95 * a_r3  # the cut does remove tiles on this (anisotropic, low-opacity) scene
+    checked = 0
+    for i in valid:
+        x0, y0, x1, y1 = r3[i]
+        if (x1 - x0) * (y1 - y0) > 9:
+            continue
+        xs = np.arange(x0 * 16, min(x1 * 16, cam["W"]))
+        ys = np.arange(y0 * 16, min(y1 * 16, cam["H"]))
+        dx = m2[i, 0] - xs[None, :]
+        dy = m2[i, 1] - ys[:, None]
+        A, B, C = con[i]
+        power = -0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy
+        passing = (power <= 0) & (opac[i] * np.exp(power) >= 1.0 / 255.0 * (1 + 1e-6))
+        py, px = np.nonzero(passing)
+        tx, ty = xs[px] // 16, ys[py] // 16
+        inside = (tx >= fp[i, 0]) & (tx < fp[i, 2]) & (ty >= fp[i, 1]) & (ty < fp[i, 3])
+        assert inside.all(), (i, fp[i], r3[i])
+        checked += 1
+    assert checked > 1000
