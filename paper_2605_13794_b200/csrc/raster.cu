@@ -302,15 +302,20 @@ __device__ __forceinline__ bool eval_bwd(PixB& p, const WRec& s, float dx, float
   const float gd = (ok && og <= 0.99f) ? G * dLda : 0.f;
   // dL/do = sum gd; the geometry partials are linear in the per-pixel moments of gd
   // (dL/dpower = o gd, dpower/dmx = -(A dx + B dy), ...), so the record's o, A, B, C are
-  // applied once per record in k_project_bwd instead of once per pixel
+  // applied once per record in k_project_bwd instead of once per pixel.  A lane's pixels share
+  // their column, hence dx: the dx-moments sum gd dx = dx sum gd, sum gd dx^2 = dx^2 sum gd and
+  // sum gd dx dy = dx sum gd dy are formed once per (lane, record) by finish_moments.
   acc<kFirst>(g[5], gd);
-  const float gx = gd * dx, gy = gd * dy;
-  acc<kFirst>(g[0], gx);
+  const float gy = gd * dy;
   acc<kFirst>(g[1], gy);
-  acc<kFirst>(g[2], gx * dx);
-  acc<kFirst>(g[3], gx * dy);
   acc<kFirst>(g[4], gy * dy);
   return ok;
+}
+
+__device__ __forceinline__ void finish_moments(float* g, float dx) {
+  g[0] = dx * g[5];
+  g[2] = dx * g[0];
+  g[3] = dx * g[1];
 }
 
 __device__ __forceinline__ float xsel(bool hi, float a, float b) { return hi ? a : b; }
@@ -399,6 +404,7 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
       }
       const unsigned cm = __ballot_sync(0xffffffffu, any);
       if (cm == 0) continue;
+      finish_moments(g, dx);
       float* dst = a.acc[__float_as_uint(s.co.w)].g;
       // few contributing lanes: direct vector reductions (two red.v4 + one scalar per lane; the
       // 48-B accumulator rows are 16-B aligned) beat the 14-shuffle butterfly below

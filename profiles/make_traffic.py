@@ -28,7 +28,7 @@ STAGE_OF = {
     "k_scale_sum": "loss", "k_scale_finish": "loss", "k_scale_grad": "loss",
     "k_tile_count": "route", "k_bucket_ranges": "sort", "k_bucket_emit": "sort", "k_bucket_radix": "sort",
     "k_depth_range": "sort", "k_pack_imp": "route_reverse", "k_gather_imp": "route_reverse",
-    "k_project_bwd_shn": "project_bwd", "k_imp_stats_coarse": "importance", "k_imp_coarse_decide": "importance",
+    "k_project_bwd_shn": "project_bwd", "k_project_bwd_shg": "project_bwd", "k_imp_stats_coarse": "importance", "k_imp_coarse_decide": "importance",
     "k_imp_gather_cand": "importance", "k_imp_select_cand": "importance", "k_shard_bounds": "project",
 }
 
