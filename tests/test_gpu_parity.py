@@ -423,6 +423,44 @@ def test_route_given_owner_map(tiny_scene, tiny_run):
         GpuStep(sc, cam, M=M, dLdC=dl, owner_in=bad)
 
 
+@pytest.mark.gpu
+def test_project_bwd_needs_colour_projection(tiny_scene):
+    """a11 reads the colour Jacobian a2 leaves in the arena (include/bgs.h): after a BGS_NO_COLOR
+    projection of the view, bgs_project_bwd is refused with a contract error instead of reading a
+    stale Jacobian."""
+    import torch
+    import paper_2605_13794_b200.bgs as B
+    cam = tiny_scene.cameras[0]
+    H, W = cam["H"], cam["W"]
+    ctx = B.Context(0, 1, 0)
+    g = B.GaussianPlanes.from_scene(tiny_scene, "cuda")
+    grads = g.zeros_grads()
+    n = tiny_scene.n
+    radius = torch.zeros(n, dtype=torch.int32, device="cuda")
+    rgb, T = torch.zeros(3, H, W, device="cuda"), torch.zeros(H, W, device="cuda")
+    nc = torch.zeros(H, W, dtype=torch.int32, device="cuda")
+    dl = torch.from_numpy(S.grad_image(H, W)).cuda()
+    c = B.camera(cam)
+    B.bgs_project(ctx, g, c, None, None, B.BGS_NO_COLOR, radius)
+    B.bgs_route(ctx)
+    B.bgs_sort_tiles(ctx)
+    B.bgs_raster_fwd(ctx, 0, rgb, T, nc)
+    B.bgs_raster_bwd(ctx, dl, T, nc)
+    B.bgs_route_reverse(ctx)
+    with pytest.raises(B.BgsError, match="NO_COLOR"):
+        B.bgs_project_bwd(ctx, g, c, grads)
+    # the same view with colour goes through
+    B.bgs_project(ctx, g, c, None, None, 0, radius)
+    B.bgs_route(ctx)
+    B.bgs_sort_tiles(ctx)
+    B.bgs_raster_fwd(ctx, 0, rgb, T, nc)
+    B.bgs_raster_bwd(ctx, dl, T, nc)
+    B.bgs_route_reverse(ctx)
+    B.bgs_project_bwd(ctx, g, c, grads)
+    torch.cuda.synchronize()
+    assert torch.isfinite(grads.mean_opac).all() and grads.mean_opac.abs().sum() > 0
+
+
 def test_gate_and_cull_bit_exact():
     sc = S.gen_city("rubble", n=200_000, W=576, H=432, V=4)
     cam = sc.cameras[2]
