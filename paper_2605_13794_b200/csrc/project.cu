@@ -251,30 +251,28 @@ static_assert(kCullChunk == BGS_BOUNDS_BLOCK, "one k_cull CTA per bounds block")
 // sets), and every per-Gaussian radius bound of cull_test is at most rb(smax, tz_min): the block
 // is culled when that box, widened by rb and by a 1% + 4 px margin for fp32 rounding, misses the
 // image.  Every Gaussian of a culled block would fail cull_test, hence has an empty rect.
-__device__ bool block_may_reach(const ProjectArgs& a, float4 b0, float4 b1) {
+// Computed by one warp, a corner per lane (lanes 8-31 repeat corners 0-7); the min / max reductions
+// are exact in any order.
+__device__ bool block_may_reach_warp(const ProjectArgs& a, float4 b0, float4 b1) {
   const CameraK& cm = a.cam;
-  float tzmin = 3.4e38f, tzmax = -3.4e38f, xmin = 3.4e38f, xmax = -3.4e38f, ymin = 3.4e38f, ymax = -3.4e38f;
+  const int c = threadIdx.x & 7;
+  const float px = (c & 1) ? b1.x : b0.x, py = (c & 2) ? b1.y : b0.y, pz = (c & 4) ? b1.z : b0.z;
+  const float tx = ((cm.R[0] * px + cm.R[1] * py) + cm.R[2] * pz) + cm.t[0];
+  const float ty = ((cm.R[3] * px + cm.R[4] * py) + cm.R[5] * pz) + cm.t[1];
+  const float tz = ((cm.R[6] * px + cm.R[7] * py) + cm.R[8] * pz) + cm.t[2];
+  const float mx = cm.fx * (tx / tz) + cm.cx, my = cm.fy * (ty / tz) + cm.cy;
+  float tzmin = tz, tzmax = tz, xmin = mx, xmax = mx, ymin = my, ymax = my;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float px = (c & 1) ? b1.x : b0.x, py = (c & 2) ? b1.y : b0.y, pz = (c & 4) ? b1.z : b0.z;
-    const float tz = ((cm.R[6] * px + cm.R[7] * py) + cm.R[8] * pz) + cm.t[2];
-    tzmin = fminf(tzmin, tz);
-    tzmax = fmaxf(tzmax, tz);
+  for (int o = 1; o < 8; o <<= 1) {
+    tzmin = fminf(tzmin, __shfl_xor_sync(0xffffffffu, tzmin, o));
+    tzmax = fmaxf(tzmax, __shfl_xor_sync(0xffffffffu, tzmax, o));
+    xmin = fminf(xmin, __shfl_xor_sync(0xffffffffu, xmin, o));
+    xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+    ymin = fminf(ymin, __shfl_xor_sync(0xffffffffu, ymin, o));
+    ymax = fmaxf(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
   }
   if (tzmax <= cm.near_clip) return false;  // every mean behind the near plane
   if (tzmin <= cm.near_clip * 1.001f + 1e-6f) return true;  // straddles it: keep
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float px = (c & 1) ? b1.x : b0.x, py = (c & 2) ? b1.y : b0.y, pz = (c & 4) ? b1.z : b0.z;
-    const float tx = ((cm.R[0] * px + cm.R[1] * py) + cm.R[2] * pz) + cm.t[0];
-    const float ty = ((cm.R[3] * px + cm.R[4] * py) + cm.R[5] * pz) + cm.t[1];
-    const float tz = ((cm.R[6] * px + cm.R[7] * py) + cm.R[8] * pz) + cm.t[2];
-    const float mx = cm.fx * (tx / tz) + cm.cx, my = cm.fy * (ty / tz) + cm.cy;
-    xmin = fminf(xmin, mx);
-    xmax = fmaxf(xmax, mx);
-    ymin = fminf(ymin, my);
-    ymax = fmaxf(ymax, my);
-  }
   const float smax = b0.w, iz = 1.0f / tzmin;
   const float rb = (3.0f * sqrtf(a.cull_K * (smax * smax) * (iz * iz) + 0.62f) * 1.01f + 2.0f) * 1.01f + 4.0f;
   const float mxr = 0.01f * (fabsf(xmin) + fabsf(xmax)), myr = 0.01f * (fabsf(ymin) + fabsf(ymax));
@@ -334,8 +332,18 @@ __global__ void __launch_bounds__(256) k_cull(ProjectArgs a) {
   const int tid = threadIdx.x;
   if (tid == 0) s_act = 0;
   const int64_t chunk0 = int64_t(blockIdx.x) * kCullChunk;
-  if (a.bounds && !a.gate_enabled &&
-      !block_may_reach(a, __ldg(a.bounds + 2 * blockIdx.x), __ldg(a.bounds + 2 * blockIdx.x + 1))) {
+  // the block test once per CTA (warp 0), not once per thread
+  __shared__ int s_reach;
+  bool reach = true;
+  if (a.bounds && !a.gate_enabled) {
+    if (tid < 32) {
+      const bool r = block_may_reach_warp(a, __ldg(a.bounds + 2 * blockIdx.x), __ldg(a.bounds + 2 * blockIdx.x + 1));
+      if (tid == 0) s_reach = r;
+    }
+    __syncthreads();
+    reach = s_reach != 0;
+  }
+  if (!reach) {
     // the whole block is off-screen: radius 0, no candidates; |A| counts the rows the cull column
     // keeps (the frustum is not part of the active set) -- without reading a single Gaussian
     uint32_t act = 0;
