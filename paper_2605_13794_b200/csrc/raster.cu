@@ -84,11 +84,10 @@ __device__ __forceinline__ float fast_rcp(float x) {
   return r;
 }
 
-// Stage this lane's record (position idx of the sorted list) and test its ellipse box against
-// the warp's strip [x0, x0+15] x [y0, y0+h-1].
-__device__ __forceinline__ bool stage_test(const RasterArgs& a, const uint32_t* vals, uint32_t idx, float x0,
-                                           float y0, int w, int h, WRec& out) {
-  const uint32_t r = __ldg(vals + idx);
+// Stage this lane's record (received-record index r, read from the sorted list one chunk ahead) and
+// test its ellipse box against the warp's block [x0, x0+w-1] x [y0, y0+h-1].
+__device__ __forceinline__ bool stage_test(const RasterArgs& a, uint32_t r, float x0, float y0, int w, int h,
+                                           WRec& out) {
   const float4* p = reinterpret_cast<const float4*>(a.recv + r);
   const float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2);
   const float4 ax = __ldg(a.aux + r);
@@ -154,14 +153,19 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
   }
   // word of chunk k: ((range.x >> 5) + lt + k) kRasterSlots + slot (32-bit index: fewer live registers)
   uint32_t widx = ((range.x >> 5) + uint32_t(lt)) * kRasterSlots + uint32_t(slot);
+  // the sorted list is read one chunk ahead, so each chunk's record fetch waits on one L2 round
+  // trip (the record rows) instead of two (the list entry, then the rows)
+  uint32_t r_next = range.x + lane < range.y ? __ldg(vals + range.x + lane) : 0u;
   for (uint32_t base = range.x; base < range.y; base += 32, widx += kRasterSlots) {
     bool done = true;
 #pragma unroll
     for (int i = 0; i < kPix; ++i) done = done && p[i].T < 0.f;
     if (__all_sync(0xffffffffu, done)) break;
     const uint32_t idx = base + lane;
+    const uint32_t r = r_next;
+    r_next = idx + 32 < range.y ? __ldg(vals + idx + 32) : 0u;
     WRec st;
-    const bool hit = idx < range.y && stage_test(a, vals, idx, x0, y0, kStripW, kLaneRows * kPix, st);
+    const bool hit = idx < range.y && stage_test(a, r, x0, y0, kStripW, kLaneRows * kPix, st);
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (hit) mine[lane] = st;
     __syncwarp();
@@ -365,15 +369,25 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
   const bool hi16 = lane & 16, hi8 = lane & 8, hi4 = lane & 4;
   const int my_idx = (hi16 ? 4 : 0) + (hi8 ? 2 : 0) + (hi4 ? 1 : 0);
   // chunks of 32 list positions, from the warp's deepest contributor back to the front
-  for (int c = int((wlast + 31) / 32) - 1; c >= 0; --c) {
+  // the forward's contributor mask of a chunk: entries none of the block's pixels took are exactly
+  // the ones every pixel's `ok` rejects here (same power, cut and last decisions).  Mask words and
+  // list entries are read one chunk ahead (the walk goes back to front), so a chunk's record fetch
+  // waits on one L2 round trip instead of three (mask, list entry, rows).
+  const uint32_t* cmw = a.cmask + size_t((range.x >> 5) + uint32_t(lt)) * kRasterSlots + slot;
+  int c = int((wlast + 31) / 32) - 1;
+  uint32_t cw_next = c >= 0 ? __ldg(cmw + size_t(c) * kRasterSlots) : 0u;
+  uint32_t r_next = c >= 0 && uint32_t(c) * 32 + lane < wlast ? __ldg(vals + range.x + uint32_t(c) * 32 + lane) : 0u;
+  for (; c >= 0; --c) {
     const uint32_t pos0 = uint32_t(c) * 32;  // relative to range.x
     const uint32_t rel = pos0 + lane;
-    // the forward's contributor mask of this chunk: entries none of the block's pixels took are
-    // exactly the ones every pixel's `ok` rejects here (same power, cut and last decisions)
-    const uint32_t cw = __ldg(a.cmask + size_t((range.x >> 5) + uint32_t(lt) + uint32_t(c)) * kRasterSlots + slot);
+    const uint32_t cw = cw_next, r = r_next;
+    if (c > 0) {
+      cw_next = __ldg(cmw + size_t(c - 1) * kRasterSlots);
+      r_next = __ldg(vals + range.x + rel - 32);
+    }
     if (cw == 0u) continue;
     WRec st;
-    const bool hit = ((cw >> lane) & 1u) && rel < wlast && stage_test(a, vals, range.x + rel, x0, y0, kStripW, kStripH, st);
+    const bool hit = ((cw >> lane) & 1u) && rel < wlast && stage_test(a, r, x0, y0, kStripW, kStripH, st);
     unsigned m = __ballot_sync(0xffffffffu, hit);
     if (hit) mine[lane] = st;
     __syncwarp();

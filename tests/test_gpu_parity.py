@@ -745,7 +745,7 @@ def test_full_size_ragged_configs(city, view):
 
 
 @pytest.mark.parametrize("split", ["default", "0"])
-@pytest.mark.parametrize("case", ["empty", "single", "ragged", "behind_and_offscreen", "dense_tile"])
+@pytest.mark.parametrize("case", ["empty", "single", "ragged", "behind_and_offscreen", "dense_tile", "faint"])
 def test_edge_cases(case, split, monkeypatch):
     if split == "0":  # every tile on the two-pixels-per-lane work unit
         monkeypatch.setenv("BGS_SPLIT_TILES", "0")
@@ -759,6 +759,16 @@ def test_edge_cases(case, split, monkeypatch):
         sc.cameras = [S.make_camera(250, 181, np.eye(3), np.zeros(3))]
     elif case == "behind_and_offscreen":
         sc = S.gen_small(3, 400, 64, 48, spread=4.0)
+    elif case == "faint":
+        # the tile footprint (R5): a third of the splats below the alpha cut everywhere (o < 1/255:
+        # radius > 0, a record, but no tile), a third faint (footprint far inside the 3DGS rect), the
+        # rest strongly anisotropic (footprint a thin band of the rect)
+        sc = S.gen_tiny(n=3000, W=128, H=96, seed=6)
+        sc.cameras = [S.make_camera(128, 96, np.eye(3), np.zeros(3))]
+        k = np.arange(sc.n) % 3
+        sc.opac[k == 0] = 0.003
+        sc.opac[k == 1] = 0.01
+        sc.scales[k == 2] *= np.array([3.0, 0.15, 0.15], np.float32)
     else:
         # thousands of pairs in single tiles (long onesweep runs of one digit, many partitions)
         sc = S.gen_small(4, 9000, 64, 64, spread=0.08, sigma_range=(0.002, 0.01))
@@ -782,6 +792,14 @@ def test_edge_cases(case, split, monkeypatch):
         assert np.array_equal(gs.a[keep], st.get("a")[keep])
         _check_g2d(st, gs, keep, case)
         _check_grads(sc.n, st, gs, keep, what=case)
+        if case == "faint":
+            rect, rect3 = st.get("rect").reshape(-1, 4), st.get("rect3").reshape(-1, 4)
+            vis = gs.radius > 0
+            below = vis & (sc.opac.ravel() < 1 / 255)
+            assert below.sum() > 100 and np.all(rect[below, 2] == rect[below, 0])  # no tile
+            assert np.all(gs.a[below] == 0) and all(np.all(v.reshape(sc.n, -1)[below] == 0) for v in gs.grads.values())
+            area = lambda r: (r[:, 2] - r[:, 0]) * (r[:, 3] - r[:, 1])
+            assert area(rect[vis]).sum() < 0.7 * area(rect3[vis]).sum()
         if case == "empty":
             assert np.all(gs.img == 0) and np.all(gs.T == 1) and np.all(gs.nc == 0)
             assert gs.rank[0]["q"]["F"] == 0 and gs.rank[0]["q"]["P"] == 0
