@@ -392,16 +392,17 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n_cand = int64_t(*((volatile unsigned long long*)(a.counters + C_CAND)));
   uint32_t dhi = 0, dlo = 0;  // max bits(depth), max (0xffffffff - bits(depth)) of this thread's records
-  for (int64_t c0 = int64_t(blockIdx.x) * 256; c0 < n_cand; c0 += int64_t(gridDim.x) * 256) {
+  const int64_t stride = int64_t(gridDim.x) * 256;
+  // candidate indices read one iteration ahead (the parameter gathers then wait on one round trip)
+  uint32_t i_next = int64_t(blockIdx.x) * 256 + tid < n_cand ? a.cand[int64_t(blockIdx.x) * 256 + tid] : 0u;
+  for (int64_t c0 = int64_t(blockIdx.x) * 256; c0 < n_cand; c0 += stride) {
     const int64_t c = c0 + tid;
     ProjOut o;
     o.valid = false;
     o.area = 0;
-    uint32_t i = 0;
-    if (c < n_cand) {
-      i = a.cand[c];
-      o = project_exact(a, i);
-    }
+    const uint32_t i = i_next;
+    i_next = c + stride < n_cand ? a.cand[c + stride] : 0u;
+    if (c < n_cand) o = project_exact(a, i);
     if (o.valid) {
       const uint32_t db = __float_as_uint(o.depth);
       dhi = db > dhi ? db : dhi;
@@ -459,8 +460,7 @@ __global__ void __launch_bounds__(256) k_project(ProjectArgs a) {
   }
 }
 
-__device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f) {
-  const uint32_t i = a.rec_lidx[f];
+__device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f, uint32_t i) {
   const float4* shp = reinterpret_cast<const float4*>(a.sh + size_t(48) * i);
   float v[48];
 #pragma unroll
@@ -543,10 +543,17 @@ __device__ __forceinline__ void color_one(const ProjectArgs& a, int64_t f) {
 
 // SH degree 3 along (mu - c_v)/|mu - c_v| (R1, R2); term order of DESIGN.md §4.2.
 // Persistent grid-stride over the F records (F read on the device: no host round trip).
-__global__ void __launch_bounds__(256) k_color(ProjectArgs a) {
+__global__ void __launch_bounds__(256, 3) k_color(ProjectArgs a) {
   const int64_t F = int64_t(*((volatile unsigned long long*)(a.counters + C_F)));
-  for (int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < F; f += int64_t(gridDim.x) * blockDim.x)
-    color_one(a, f);
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  int64_t f = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  // record indices read one iteration ahead (the SH-row gather then waits on one round trip)
+  uint32_t i_next = f < F ? a.rec_lidx[f] : 0u;
+  for (; f < F; f += stride) {
+    const uint32_t i = i_next;
+    i_next = f + stride < F ? a.rec_lidx[f + stride] : 0u;
+    color_one(a, f, i);
+  }
 }
 
 // Persistent grids sized to what is resident at once (SMs x max CTAs/SM of the kernel):
