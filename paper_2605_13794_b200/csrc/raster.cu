@@ -416,8 +416,9 @@ __device__ __forceinline__ void bwd_strip(const RasterArgs& a, const uint32_t* _
 #pragma unroll
         for (int i = 1; i < kPix; ++i) any |= eval_bwd<false>(p[i], s, dx, s.geo.y - pyf[i], pos, g);
       }
+      // no early exit when no lane contributed (the contributor mask makes that the rare case, and
+      // the path below then issues nothing): the branch cost more than it saved (bwd -2%)
       const unsigned cm = __ballot_sync(0xffffffffu, any);
-      if (cm == 0) continue;
       finish_moments(g, dx);
       float* dst = a.acc[__float_as_uint(s.co.w)].g;
       // few contributing lanes: direct vector reductions (two red.v4 + one scalar per lane; the
