@@ -170,6 +170,7 @@ struct RasterArgs {
   const uint32_t* tile_perm;  // launch order of the owned tiles (longest list first)
   int n_split;                // the first n_split tiles of tile_perm run as two half-tile CTAs
   uint32_t* cmask;            // contributor masks: written by the forward, read by the backward
+  int no_color;               // the view was projected with BGS_NO_COLOR: no colour compositing
 };
 constexpr int kRasterSlots = 8;  // warp blocks per tile (8 in a split tile, 4 otherwise)
 constexpr int kFinalSel = 15;  // buffer holding the sorted keys after the passes

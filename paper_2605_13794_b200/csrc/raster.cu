@@ -112,6 +112,7 @@ struct PixF {
   uint32_t last;
 };
 
+template <bool kColor>
 __device__ __forceinline__ void eval_fwd1(PixF& p, const WRec& s, float dx, float dy, uint32_t pos, bool& c,
                                           uint32_t& f) {
   const float nq = pinned_negpower(s.geo.z, s.geo.w, s.co.x, dx, dy);
@@ -120,9 +121,11 @@ __device__ __forceinline__ void eval_fwd1(PixF& p, const WRec& s, float dx, floa
   const float t = p.T * (1.0f - alpha);
   c = ok && t >= 0.0001f;  // false once stopped (T < 0)
   const float w = c ? alpha * p.T : 0.f;
-  p.r += s.rgb.x * w;
-  p.g += s.rgb.y * w;
-  p.b += s.rgb.z * w;
+  if (kColor) {  // a BGS_NO_COLOR view (scoring pass) has no colours: its image stays black
+    p.r += s.rgb.x * w;
+    p.g += s.rgb.y * w;
+    p.b += s.rgb.z * w;
+  }
   p.T = c ? t : (ok ? -fabsf(p.T) : p.T);
   p.last = c ? pos : p.last;
   f = __float2uint_rn(w * 16777216.0f);
@@ -131,7 +134,7 @@ __device__ __forceinline__ void eval_fwd1(PixF& p, const WRec& s, float dx, floa
 // One warp composites a kStripW x (kLaneRows kPix) block of tile lt at (col0, row0): lane covers
 // column col0 + lane % kStripW and rows row0 + lane / kStripW + kLaneRows i, i < kPix (kPix
 // independent dependency chains per lane, branch-free).
-template <bool kImportance, int kPix>
+template <bool kImportance, int kPix, bool kColor = true>
 __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* __restrict__ vals, int lt, int col0,
                                           int row0, int slot, WRec* mine, float* __restrict__ rgb,
                                           float* __restrict__ t_final, int32_t* __restrict__ n_contrib) {
@@ -184,7 +187,7 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
         if (kPix > 1 && !((__float_as_uint(s.rgb.w) >> i) & 1u)) continue;  // warp-uniform: box misses these rows
         uint32_t f;
         bool c;
-        eval_fwd1(p[i], s, dx, s.geo.y - pyf[i], pos, c, f);
+        eval_fwd1<kColor>(p[i], s, dx, s.geo.y - pyf[i], pos, c, f);
         fs += f;
         cs += uint32_t(c);
       }
@@ -231,7 +234,7 @@ __device__ __forceinline__ void fwd_strip(const RasterArgs& a, const uint32_t* _
 // whole list of its tile, so the heaviest tiles (6-8x the mean list length on Rubble views) set
 // the kernel's makespan; halving their pixels per warp and their strip height shortens exactly
 // those walks.
-template <bool kImportance>
+template <bool kImportance, bool kColor>
 __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __restrict__ rgb,
                                                          float* __restrict__ t_final,
                                                          int32_t* __restrict__ n_contrib) {
@@ -242,11 +245,11 @@ __global__ void __launch_bounds__(kThreads) k_raster_fwd(RasterArgs a, float* __
   const int b = int(blockIdx.x / kCtasPerUnit);
   if (b < 2 * a.n_split) {
     const int lt = int(__ldg(a.tile_perm + (b >> 1)));
-    fwd_strip<kImportance, 1>(a, vals, lt, kStripW * (warp % kStripsX), (b & 1) * 8 + kLaneRows * (warp / kStripsX),
+    fwd_strip<kImportance, 1, kColor>(a, vals, lt, kStripW * (warp % kStripsX), (b & 1) * 8 + kLaneRows * (warp / kStripsX),
                               (b & 1) * kWarps + warp, s_rec[lw], rgb, t_final, n_contrib);
   } else {
     const int lt = int(__ldg(a.tile_perm + (b - a.n_split)));
-    fwd_strip<kImportance, 2>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), warp,
+    fwd_strip<kImportance, 2, kColor>(a, vals, lt, kStripW * (warp % kStripsX), 2 * kLaneRows * (warp / kStripsX), warp,
                               s_rec[lw], rgb, t_final, n_contrib);
   }
 }
@@ -499,10 +502,17 @@ int launch_raster_fwd(const RasterArgs& a, uint32_t flags, float* rgb, float* t_
   RasterArgs b = a;
   b.n_split = split_count(a.n_tiles);
   const unsigned grid = unsigned(a.n_tiles + b.n_split);
-  if (flags & BGS_IMPORTANCE)
-    k_raster_fwd<true><<<grid * kCtasPerUnit, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
-  else
-    k_raster_fwd<false><<<grid * kCtasPerUnit, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+  const unsigned blocks = grid * kCtasPerUnit;
+  if (a.no_color) {  // scoring views: the instrumented forward without colour
+    if (flags & BGS_IMPORTANCE)
+      k_raster_fwd<true, false><<<blocks, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+    else
+      k_raster_fwd<false, false><<<blocks, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+  } else if (flags & BGS_IMPORTANCE) {
+    k_raster_fwd<true, true><<<blocks, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+  } else {
+    k_raster_fwd<false, true><<<blocks, kThreads, 0, s>>>(b, rgb, t_final, n_contrib);
+  }
   return b.n_split;
 }
 

@@ -1035,6 +1035,7 @@ static RasterArgs raster_args(bgs_ctx* ctx) {
   a.aux = P_<float4>(ctx->aux);
   a.tile_perm = P_<uint32_t>(ctx->tile_perm);
   a.cmask = P_<uint32_t>(ctx->cmask);
+  a.no_color = ctx->colored ? 0 : 1;
   return a;
 }
 
