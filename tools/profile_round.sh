@@ -7,4 +7,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 1 --quick --no-cpu-baseline > /dev/null 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:"k_(cull|project|color|emit|onesweep|ranges_fixup|raster_fwd|raster_bwd|project_bwd|project_bwd_shg|imp_coop|loss_photo)" \
-  -s 40 -c 14 -o gpurun_out/full_r02c python tools/view_probe.py 6 > gpurun_out/ncu_full.log 2>&1
+  -s 40 -c 14 -o gpurun_out/full_r02d python tools/view_probe.py 6 > gpurun_out/ncu_full.log 2>&1
